@@ -1,0 +1,329 @@
+"""Benchmark of the evoca substrate step on B200 (BASELINE.json metric:
+cell-updates/sec of the full step, and % of the HBM roofline).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl ours|reference]
+
+Workload (BASELINE.json configs[1]): 1024x1024 torus, 64 genomes, direct
+45->13 controller, synthetic seeded state (paper_2406_09654_b200/synth.py).
+A step = one full substrate update (pass 1 + pass 2).  Each timed step is
+bracketed by CUDA events on the launching stream, with an L2 flush (a 256 MiB
+memset, twice the 126 MB L2) before it and outside the timed interval, so the
+52 MB state is read from HBM every step.  Multi-GPU: one process per GPU
+(torchrun); each rank steps its own substrate (weak scaling) and the slowest
+rank's time is reported.
+
+--impl reference times the reference algorithm on the host cores: the
+oracle port (oracle/oracle.py; the reference is pure Python and cannot be
+compiled), each step a bounded sample (a 512x512 or 256x256 window of the
+same workload) so the run stays within minutes.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+BYTES_PER_CELL = 50  # 25 B state read + 25 B written per cell-update
+FLOP_PER_CELL_DIRECT = 2 * 45 * 13
+L2_FLUSH_BYTES = 256 << 20
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured", d
+    except Exception:
+        return 6650.0, "fallback", {}
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = threading.Thread(target=self._loop, daemon=True)
+
+    def _loop(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(
+                    ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits"],
+                    capture_output=True, text=True, timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if len(s) > 3 + i and s[3 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def run_ours(args, rank, world, local):
+    import torch
+
+    from paper_2406_09654_b200 import _lib, engine, physics
+    from paper_2406_09654_b200.synth import BASELINE_CONFIGS
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    cfg = BASELINE_CONFIGS[args.config]
+    state = engine.baseline_state(args.config, seed=args.seed + rank)
+    dev = engine.device_of(state, device=local)
+    b = state._evo_binding
+    b.sync_params(state.pool)
+    dev.upload(state.substrate.front)
+    dev.sync()
+    stream = torch.cuda.current_stream()
+    sh = stream.cuda_stream
+    phys = state.config.physics
+    flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device="cuda")
+    ncell = cfg.width * cfg.height
+
+    t = 0
+    for _ in range(args.warmup):
+        flush.zero_()
+        dev.pass1(physics.step_scalars(t, phys), t, stream=sh)
+        dev.pass2(t, stream=sh)
+        dev.swap()
+        t += 1
+    torch.cuda.synchronize()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
+           torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    scal = [physics.step_scalars(t + i, phys) for i in range(args.steps)]
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clocks:
+        for i in range(args.steps):
+            flush.zero_()
+            e0, e1, e2 = ev[i]
+            e0.record(stream)
+            dev.pass1(scal[i], t, stream=sh)
+            e1.record(stream)
+            dev.pass2(t, stream=sh)
+            e2.record(stream)
+            dev.swap()
+            t += 1
+        torch.cuda.synchronize()
+    k1 = sum(a.elapsed_time(m) for a, m, _ in ev)
+    k2 = sum(m.elapsed_time(z) for _, m, z in ev)
+    total_ms = k1 + k2
+    if world > 1:
+        tt = torch.tensor([total_ms], device="cuda", dtype=torch.float64)
+        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+        total_ms = float(tt.item())
+    adoptions, _ = dev.read_stats()
+
+    # e2e through the public API: engine.step on a host-resident state
+    # (upload of the front planes, both passes, download of the new planes,
+    # census read-back and host pool update, every step).
+    e2e_state = engine.baseline_state(args.config, seed=args.seed + rank)
+    engine.device_of(e2e_state, device=local)
+    e2e_steps = max(3, min(args.steps, 20))
+    engine.step(e2e_state)  # warm
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        engine.step(e2e_state)
+    torch.cuda.synchronize()
+    e2e_s = time.perf_counter() - t0
+    if world > 1:
+        tt = torch.tensor([e2e_s], device="cuda", dtype=torch.float64)
+        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+        e2e_s = float(tt.item())
+
+    if rank != 0:
+        return None
+    hbm, hbm_kind, pk = peaks()
+    step_s = total_ms / 1e3 / args.steps
+    value = ncell * world / step_s
+    achieved_gbs = ncell * BYTES_PER_CELL / step_s / 1e9
+    k1_s, k2_s = k1 / 1e3 / args.steps, k2 / 1e3 / args.steps
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(prof):
+        try:
+            traffic = json.load(open(prof)).get(args.config)
+        except Exception:
+            traffic = None
+    clk = clocks.summary()
+    sm_hz = (clk["sm_mhz"] or 1965.0) * 1e6
+    fp32_peak = 148 * 128 * 2 * sm_hz / 1e12  # derived FP32 CUDA-core peak at the sampled clock
+    line = {
+        "metric": "cell-updates/sec (full step)",
+        "value": value,
+        "unit": "cell-updates/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": step_s * 1e3,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f32",
+        "data": "synthetic (seeded, BASELINE.json config distributions)",
+        "config": {"workload": cfg.name, "grid": [cfg.height, cfg.width], "genomes": cfg.genomes,
+                   "net": "45->13 direct" if cfg.hidden == 0 else f"45->{cfg.hidden}->13",
+                   "cells_per_gpu": ncell, "l2": "flushed before every timed step (256 MiB memset)",
+                   "parallelism": f"replicas x{world}" if world > 1 else "single GPU"},
+        "roofline": {
+            "kernel": "full step (pass1 k_act_physics + pass2 k_resolve)",
+            "bound": "hbm",
+            "achieved": achieved_gbs,
+            "peak": hbm,
+            "peak_kind": hbm_kind,
+            "unit": "GB/s",
+            "frac": achieved_gbs / hbm,
+            "traffic": traffic,
+            "algorithmic_bytes_per_cell": BYTES_PER_CELL,
+            "kernels": [
+                {"name": "k_act_physics (pass 1: sense+net+physics)", "ms": k1_s * 1e3, "share": k1 / total_ms,
+                 "fp32_tflops": ncell * FLOP_PER_CELL_DIRECT / k1_s / 1e12 if cfg.hidden == 0 else None,
+                 "fp32_peak_tflops_derived": fp32_peak},
+                {"name": "k_resolve (pass 2: explore resolve+adoption+census)", "ms": k2_s * 1e3,
+                 "share": k2 / total_ms},
+            ],
+        },
+        "e2e": {"value": ncell * world * e2e_steps / e2e_s, "unit": "cell-updates/s",
+                "api": "paper_2406_09654_b200.engine.step(state) on host-resident planes",
+                "h2d_bytes_per_step": ncell * 25 + state.pool.capacity * 9,
+                "d2h_bytes_per_step": ncell * 25 + state.pool.capacity * 4 + 16},
+        "gpu_launches": 2 * args.steps,
+        "clocks": clk,
+        "adoptions_last_step": int(adoptions),
+    }
+    if args.cpu_baseline and world == 1:
+        line["cpu_baseline"] = cpu_baseline(args.config, budget_s=args.cpu_seconds)
+    return line
+
+
+def cpu_baseline(config: str, budget_s: float = 15.0, side: int | None = None, steps: int | None = None):
+    """The oracle port (numpy + numba, like the reference) on the host cores,
+    on a bounded sample of the workload."""
+    from oracle import oracle as orc
+    from paper_2406_09654_b200.synth import BASELINE_CONFIGS
+
+    cfg = BASELINE_CONFIGS[config]
+    side_h = min(cfg.height, side or 512)
+    side_w = min(cfg.width, side or 512)
+    p = orc.synth_planes(side_h, side_w, cfg.genomes, seed=0, sparse_infra=cfg.sparse_infra)
+    net = orc.synth_net(cfg.genomes, cfg.hidden, seed=0)
+    phys = orc.Phys(cycle_period=cfg.cycle_period)
+    orc.step(orc.synth_planes(16, 16, cfg.genomes, seed=1), 0, net, phys)  # numba compile
+    n = 0
+    t0 = time.perf_counter()
+    while True:
+        p = orc.step(p, n, net, phys).planes
+        n += 1
+        el = time.perf_counter() - t0
+        if (steps is not None and n >= steps) or (steps is None and el >= budget_s):
+            break
+    return {"value": side_h * side_w * n / el, "unit": "cell-updates/s", "cores": os.cpu_count(),
+            "kind": "port", "sample": f"{n} oracle steps on a {side_h}x{side_w} window of {cfg.name} "
+                                      f"(numpy/numba/BLAS, {os.cpu_count()} host threads)"}
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return None
+    side = 512 if args.steps <= 200 else 256
+    from paper_2406_09654_b200.synth import BASELINE_CONFIGS
+
+    cfg = BASELINE_CONFIGS[args.config]
+    for _ in range(args.warmup):
+        cpu_baseline(args.config, side=side, steps=1)
+    cb = cpu_baseline(args.config, side=side, steps=args.steps)
+    return {
+        "impl": "reference",
+        "metric": "cell-updates/sec (full step)",
+        "value": cb["value"],
+        "unit": "cell-updates/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f32",
+        "data": "synthetic (seeded, BASELINE.json config distributions)",
+        "config": {"workload": cfg.name, "grid": [cfg.height, cfg.width], "genomes": cfg.genomes,
+                   "sample_grid": [min(side, cfg.height), min(side, cfg.width)]},
+        "cpu_baseline": cb,
+        "e2e": {"value": cb["value"], "unit": "cell-updates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="c2")
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    rank, world, local = dist_env()
+    if args.impl == "reference":
+        line = run_reference(args, rank, world)
+    else:
+        line = run_ours(args, rank, world, local)
+        if world > 1:
+            import torch.distributed as dist
+
+            dist.barrier()
+            dist.destroy_process_group()
+    if line is not None:
+        print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,159 @@
+/*
+ * evoca_b200.h — C ABI of the B200-native substrate step.
+ *
+ * Drop-in boundary for the reference's per-step substrate update
+ * (`evoca.engine.step`, /root/reference/pkg/src/evoca/engine.py:233-248) and
+ * its operator-level phase functions (physics.py:178-404).  The reference is
+ * pure Python; its FFI for this path would be a ctypes binding of exactly
+ * these symbols (INTEGRATION.md shows the stub).  Plain pointers and sizes
+ * only: no torch / CUDA types in any signature (streams are `void*` holding a
+ * cudaStream_t, NULL = the context's own stream).
+ *
+ * Every function returns 0 on success, EVO_EINVAL on a rejected argument (the
+ * reference raises ValueError there, e.g. physics.py:55-56, config.py), or a
+ * positive cudaError_t code; evo_last_error() gives the message for the
+ * calling thread.  The step itself never fails on valid state
+ * ("physics itself never fails").
+ *
+ * State layout (one context = one row strip; a single GPU is one strip that
+ * holds the whole torus): structure-of-arrays planes, row-major, linear index
+ * y*W + x (substrate.py:9-11):
+ *   energy f32 (H,W), infrastructure f32 (H,W), communication f32 (3,H,W),
+ *   genome_index i32 (H,W) (-1 = empty), rotation u8 (H,W) in 0..7
+ * (substrate.py:45-75).  Device copies carry one ghost row above and below.
+ */
+#ifndef EVOCA_B200_H
+#define EVOCA_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define EVO_API __attribute__((visibility("default")))
+
+#define EVO_OK 0
+#define EVO_EINVAL (-1)
+
+/* Phase mask for evo_step / evo_pass1 (engine.py:240-243 order). */
+#define EVO_PH_ENERGY 1   /* physics.energy_cycle        physics.py:178-194 */
+#define EVO_PH_INVEST 2   /* physics.apply_invest_liquidate physics.py:197-233 */
+#define EVO_PH_COMM 4     /* physics.write_communication physics.py:236-247 */
+#define EVO_PH_EXPLORE 8  /* physics.resolve_exploration physics.py:250-343 */
+#define EVO_PH_ALL 15
+
+/* Step flags. */
+#define EVO_F_INJECT_ACTIONS 1  /* use the ActionField set by evo_set_actions instead of sense+net */
+#define EVO_F_EXPORT_ACTIONS 2  /* keep the computed ActionField for evo_get_actions (engine.py:193) */
+#define EVO_F_RECORD_EVENTS 4   /* keep AdoptionEvents for evo_read_events (physics.py:134-175) */
+#define EVO_F_NO_CENSUS 8       /* strip mode: census epilogue runs after the cross-rank count reduction */
+
+/* Host-computed per-step scalars, exactly as the reference derives them:
+ * rho = A*sin(2*pi*t/P) in float64 (physics.py:186); rho_mode 1 if rho > 0,
+ * 2 if rho < 0, else 0; rho_f32 = float32(rho); drain_f32 =
+ * float32(drain_fraction * -rho); the rest are np.float32(PhysicsParams.x). */
+typedef struct evo_scalars {
+  int32_t rho_mode;
+  float rho_f32;
+  float drain_f32;
+  float invest_rate;
+  float liquidate_rate;
+  float invest_efficiency;
+  float liquidate_efficiency;
+  float explore_fraction;
+  float upkeep;
+  float decay_on_starvation;
+  float death_threshold;
+} evo_scalars;
+
+typedef struct evo_ctx evo_ctx;
+
+/* Context lifetime.  Replaces create_substrate + the pool's dense-param cache
+ * (substrate.py:111-123, neuroevo.py:415-441).  hidden = 0 selects the direct
+ * 45->13 controller (BASELINE extension), hidden >= 1 the reference
+ * 45->hidden(tanh)->13 DenseParams net (hypernet.py:77-84, 233-252). */
+EVO_API int evo_create(evo_ctx** out, int width, int height, int capacity, int hidden, int device);
+/* Row strip [row0, row0+height) of a torus with height_global rows (multi-GPU,
+ * SURVEY.md §8e).  Ghost rows are filled by the caller's halo exchange. */
+EVO_API int evo_create_strip(evo_ctx** out, int width, int height, int64_t row0, int height_global,
+                             int capacity, int hidden, int device);
+EVO_API int evo_destroy(evo_ctx* ctx);
+EVO_API const char* evo_last_error(void);
+EVO_API int evo_version(void);
+
+/* Front-buffer transfer (engine hooks / server brush read and write the front,
+ * substrate.py:86-108, server.py:204-226).  Pointers are host memory; pinned
+ * memory makes the copies asynchronous on `stream`. communication is (3,H,W). */
+EVO_API int evo_upload_planes(evo_ctx* ctx, const float* energy, const float* infra, const float* comm,
+                              const int32_t* genome, const uint8_t* rotation, void* stream);
+EVO_API int evo_download_planes(evo_ctx* ctx, float* energy, float* infra, float* comm, int32_t* genome,
+                                uint8_t* rotation, void* stream);
+
+/* Per-slot controller parameters (DenseParams, hypernet.py:77-84), slots
+ * [slot0, slot0+n).  hidden >= 1: w1 (n,hidden,45), b1 (n,hidden), w2
+ * (n,13,hidden), b2 (n,13).  hidden == 0: w1/b1 ignored (may be NULL),
+ * w2 (n,13,45), b2 (n,13). */
+EVO_API int evo_set_params(evo_ctx* ctx, int slot0, int n, const float* w1, const float* b1, const float* w2,
+                           const float* b2);
+/* Slot liveness (GenomePool slot states: 0 free, 1 live, 2 dead) and peak
+ * populations, for the device census (neuroevo.py:521-542). */
+EVO_API int evo_set_slots(evo_ctx* ctx, const int8_t* state, const int32_t* peak);
+/* Optional per-cell energy source map (PhysicsParams.energy_source_map,
+ * physics.py:69, 190-191); NULL restores the uniform default. */
+EVO_API int evo_set_source_map(evo_ctx* ctx, const float* map);
+
+/* One full step t -> t+1 (engine.py:233-248 without host radiation):
+ * sense + net + energy + invest/liquidate + comm + explore proposal (pass 1),
+ * explore resolve + adoption + census (pass 2), front/back swap. */
+EVO_API int evo_step(evo_ctx* ctx, const evo_scalars* s, int64_t t, int phases, int flags, void* stream);
+/* k consecutive steps t0..t0+k-1 with per-step scalars s[0..k-1]. */
+EVO_API int evo_run(evo_ctx* ctx, const evo_scalars* s, int64_t t0, int k, void* stream);
+/* The two launches of a step, for halo exchange between them (multi-GPU) and
+ * for per-kernel timing.  evo_swap publishes the back buffer. */
+EVO_API int evo_pass1(evo_ctx* ctx, const evo_scalars* s, int64_t t, int phases, int flags, void* stream);
+EVO_API int evo_pass2(evo_ctx* ctx, int64_t t, int flags, void* stream);
+EVO_API int evo_census_finish(evo_ctx* ctx, int64_t t, void* stream);
+EVO_API int evo_swap(evo_ctx* ctx);
+/* Single-GPU ghost-row refresh after a host upload (rows wrap on the torus). */
+EVO_API int evo_refresh_ghosts(evo_ctx* ctx, void* stream);
+EVO_API int evo_sync(evo_ctx* ctx);
+
+/* Parity-mode ActionField transfer (physics.py:97-119): n listed cells
+ * (linear indices, local to the strip) and their (n,13) actuator rows in
+ * column order invest, liquidate, comm x3, explore x8 (engine.py:224-230). */
+EVO_API int evo_set_actions(evo_ctx* ctx, const int64_t* cells, int64_t n, const float* acts);
+/* Computed actions of the last EVO_F_EXPORT_ACTIONS step for every cell
+ * occupied at sensing time, ascending index: cells (n), acts (n,13). */
+EVO_API int evo_get_actions(evo_ctx* ctx, int64_t capacity, int64_t* cells, float* acts, int64_t* n);
+
+/* Census of the last step: counts (capacity), slot state (0/1/2), death step
+ * (-1 = alive), peak population.  Any pointer may be NULL. */
+EVO_API int evo_read_census(evo_ctx* ctx, int32_t* counts, int8_t* state, int64_t* death_step, int32_t* peak);
+/* Last step's adoption count and newly dead slot count
+ * (SimState.last_adoptions / last_extinctions, engine.py:247-248). */
+EVO_API int evo_read_stats(evo_ctx* ctx, int64_t* adoptions, int64_t* extinctions);
+/* AdoptionEvents of the last EVO_F_RECORD_EVENTS step, ascending target
+ * (physics.py:134-175, 340-343). */
+EVO_API int evo_read_events(evo_ctx* ctx, int64_t capacity, int64_t* target, int64_t* source, int32_t* winner,
+                            int32_t* defender, int64_t* direction, float* quantity, int64_t* m);
+/* Patch genome slots on the device front buffer after host radiation
+ * (physics.py:389-392): n cells (local linear index) get slot values. */
+EVO_API int evo_patch_genomes(evo_ctx* ctx, const int64_t* cells, const int32_t* slots, int64_t n);
+
+/* Device pointers of a plane (halo exchange / interop).  which: 0 energy,
+ * 1 infra, 2 comm (3 planes, stride = plane_stride), 3 genome, 4 rotation,
+ * 5 mid infra, 6 mid genome, 7 mid proposal byte, 8 mid quantity.
+ * buffer: 0 front, 1 back (ignored for mid planes).  The pointer addresses
+ * ghost row -1; row y lives at + (y+1)*W.  plane_stride counts elements. */
+EVO_API int evo_plane_ptr(evo_ctx* ctx, int which, int buffer, void** ptr, int64_t* plane_stride);
+
+/* 64-bit FNV-1a continuation over host bytes (engine.digest, engine.py:283-315):
+ * *out = fold(h, data[0..n)).  Host code, no device involved. */
+EVO_API int evo_fnv1a64(uint64_t h, const uint8_t* data, int64_t n, uint64_t* out);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* EVOCA_B200_H */

@@ -1,0 +1,585 @@
+// C ABI of the B200 substrate step (include/evoca_b200.h).
+//
+// Owns every device allocation of one strip: double-buffered SoA planes with
+// a ghost row above and below, the pass-1 intermediate planes, the per-slot
+// controller tables in the kernel layout, the device census and the optional
+// parity buffers (injected / exported ActionField, adoption events).
+
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "evoca_b200.h"
+#include "evoca_internal.h"
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+#define CK(expr)                                                                                     \
+  do {                                                                                               \
+    cudaError_t _e = (expr);                                                                         \
+    if (_e != cudaSuccess) return fail((int)_e, std::string(#expr) + ": " + cudaGetErrorString(_e)); \
+  } while (0)
+
+}  // namespace
+
+struct evo_ctx {
+  int device = 0;
+  int W = 0, H = 0, Hg = 0;
+  long long row0 = 0;
+  int cap = 0, hidden = 0, hpad = 0;
+  bool strip = false;
+  long long stride = 0;  // (H + 2) * W
+  evo::Planes buf[2] = {};
+  int front = 0;
+  evo::Mid mid = {};
+  float *wA = nullptr, *bA = nullptr, *wB = nullptr, *bB = nullptr;
+  evo::Census census = {};
+  float* act_in = nullptr;
+  uint8_t* act_in_flag = nullptr;
+  float* act_out = nullptr;
+  uint8_t* act_out_flag = nullptr;
+  int64_t* ev_src = nullptr;
+  float* ev_q = nullptr;
+  int32_t* ev_def = nullptr;
+  float* src_map = nullptr;
+  bool have_export = false, have_events = false, have_src_map = false;
+  cudaStream_t stream = nullptr;
+  std::vector<void*> allocs;
+
+  long long ncell() const { return (long long)W * H; }
+  evo::StepGeom geom() const {
+    evo::StepGeom g;
+    g.W = W;
+    g.H = H;
+    g.row0 = row0;
+    g.Hg = Hg;
+    g.stride = stride;
+    g.own_ghosts = strip ? 0 : 1;
+    return g;
+  }
+  template <typename T>
+  cudaError_t alloc(T** p, size_t count) {
+    void* v = nullptr;
+    cudaError_t e = cudaMalloc(&v, count * sizeof(T) > 0 ? count * sizeof(T) : 16);
+    if (e != cudaSuccess) return e;
+    allocs.push_back(v);
+    *p = static_cast<T*>(v);
+    return cudaMemset(v, 0, count * sizeof(T) > 0 ? count * sizeof(T) : 16);
+  }
+};
+
+namespace {
+
+cudaStream_t pick(evo_ctx* c, void* s) { return s ? static_cast<cudaStream_t>(s) : c->stream; }
+
+int check_ctx(evo_ctx* c) {
+  if (!c) return fail(EVO_EINVAL, "null context");
+  cudaError_t e = cudaSetDevice(c->device);
+  if (e != cudaSuccess) return fail((int)e, std::string("cudaSetDevice: ") + cudaGetErrorString(e));
+  return 0;
+}
+
+evo::Scalars to_scalars(const evo_scalars& s) {
+  evo::Scalars o;
+  o.mode = s.rho_mode;
+  o.rho = s.rho_f32;
+  o.drain = s.drain_f32;
+  o.kinv = s.invest_rate;
+  o.kliq = s.liquidate_rate;
+  o.einv = s.invest_efficiency;
+  o.eliq = s.liquidate_efficiency;
+  o.alpha = s.explore_fraction;
+  o.upkeep = s.upkeep;
+  o.dstarve = s.decay_on_starvation;
+  o.imin = s.death_threshold;
+  return o;
+}
+
+int create_impl(evo_ctx** out, int width, int height, long long row0, int hg, int capacity, int hidden, int device,
+                bool strip) {
+  if (!out) return fail(EVO_EINVAL, "out is null");
+  *out = nullptr;
+  if (width < 1 || height < 1) return fail(EVO_EINVAL, "substrate dimensions must be positive");
+  if (capacity < 1 || capacity > evo::kMaxCapacity)
+    return fail(EVO_EINVAL, "capacity must be in [1, " + std::to_string(evo::kMaxCapacity) + "]");
+  if (hidden < 0 || hidden > 1024) return fail(EVO_EINVAL, "hidden size must be in [0, 1024]");
+  if (hg < height || row0 < 0 || row0 + height > hg) return fail(EVO_EINVAL, "strip outside the global torus");
+  if ((long long)width * hg >= 0xFFFFFFFFLL) return fail(EVO_EINVAL, "grid exceeds 2^32-1 cells");
+  if (strip && height < 1) return fail(EVO_EINVAL, "strip needs at least one row");
+  evo_ctx* c = new evo_ctx();
+  c->device = device;
+  c->W = width;
+  c->H = height;
+  c->row0 = row0;
+  c->Hg = hg;
+  c->cap = capacity;
+  c->hidden = hidden;
+  c->hpad = hidden > 0 ? ((hidden + 7) / 8) * 8 : 0;
+  c->strip = strip;
+  c->stride = (long long)(height + 2) * width;
+  auto bail = [&](cudaError_t e, const char* what) {
+    for (void* p : c->allocs) cudaFree(p);
+    if (c->stream) cudaStreamDestroy(c->stream);
+    delete c;
+    return fail((int)e, std::string(what) + ": " + cudaGetErrorString(e));
+  };
+  cudaError_t e = cudaSetDevice(device);
+  if (e != cudaSuccess) return bail(e, "cudaSetDevice");
+  e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
+  if (e != cudaSuccess) return bail(e, "cudaStreamCreate");
+  const size_t n = (size_t)c->stride;
+  for (int b = 0; b < 2; ++b) {
+    if ((e = c->alloc(&c->buf[b].E, n)) != cudaSuccess) return bail(e, "alloc E");
+    if ((e = c->alloc(&c->buf[b].I, n)) != cudaSuccess) return bail(e, "alloc I");
+    if ((e = c->alloc(&c->buf[b].C, 3 * n)) != cudaSuccess) return bail(e, "alloc C");
+    if ((e = c->alloc(&c->buf[b].gi, n)) != cudaSuccess) return bail(e, "alloc gi");
+    if ((e = c->alloc(&c->buf[b].rot, n)) != cudaSuccess) return bail(e, "alloc rot");
+  }
+  if ((e = cudaMemset(c->buf[0].gi, 0xFF, n * sizeof(int32_t))) != cudaSuccess) return bail(e, "memset gi");
+  if ((e = cudaMemset(c->buf[1].gi, 0xFF, n * sizeof(int32_t))) != cudaSuccess) return bail(e, "memset gi");
+  if ((e = c->alloc(&c->mid.I, n)) != cudaSuccess) return bail(e, "alloc mid");
+  if ((e = c->alloc(&c->mid.gi, n)) != cudaSuccess) return bail(e, "alloc mid");
+  if ((e = c->alloc(&c->mid.rp, n)) != cudaSuccess) return bail(e, "alloc mid");
+  if ((e = c->alloc(&c->mid.q, n)) != cudaSuccess) return bail(e, "alloc mid");
+  const size_t cap = (size_t)capacity;
+  if (hidden == 0) {
+    if ((e = c->alloc(&c->wA, cap * evo::kSensors * evo::kOutPad)) != cudaSuccess) return bail(e, "alloc w");
+    if ((e = c->alloc(&c->bA, cap * evo::kOutPad)) != cudaSuccess) return bail(e, "alloc b");
+  } else {
+    if ((e = c->alloc(&c->wA, cap * evo::kSensors * c->hpad)) != cudaSuccess) return bail(e, "alloc w1");
+    if ((e = c->alloc(&c->bA, cap * c->hpad)) != cudaSuccess) return bail(e, "alloc b1");
+    if ((e = c->alloc(&c->wB, cap * c->hpad * evo::kOutPad)) != cudaSuccess) return bail(e, "alloc w2");
+    if ((e = c->alloc(&c->bB, cap * evo::kOutPad)) != cudaSuccess) return bail(e, "alloc b2");
+  }
+  if ((e = c->alloc(&c->census.counts, cap)) != cudaSuccess) return bail(e, "alloc census");
+  if ((e = c->alloc(&c->census.counts_last, cap)) != cudaSuccess) return bail(e, "alloc census");
+  if ((e = c->alloc(&c->census.state, cap)) != cudaSuccess) return bail(e, "alloc census");
+  if ((e = c->alloc(&c->census.death_step, cap)) != cudaSuccess) return bail(e, "alloc census");
+  if ((e = c->alloc(&c->census.peak, cap)) != cudaSuccess) return bail(e, "alloc census");
+  if ((e = c->alloc(&c->census.done, 1)) != cudaSuccess) return bail(e, "alloc census");
+  if ((e = c->alloc(&c->census.stats, 2)) != cudaSuccess) return bail(e, "alloc stats");
+  if ((e = cudaMemset(c->census.death_step, 0xFF, cap * sizeof(int64_t))) != cudaSuccess) return bail(e, "memset");
+  if ((e = cudaDeviceSynchronize()) != cudaSuccess) return bail(e, "sync");
+  *out = c;
+  return 0;
+}
+
+int ensure_actions_in(evo_ctx* c) {
+  if (c->act_in) return 0;
+  CK(c->alloc(&c->act_in, (size_t)c->ncell() * evo::kActuators));
+  CK(c->alloc(&c->act_in_flag, (size_t)c->ncell()));
+  return 0;
+}
+
+int ensure_actions_out(evo_ctx* c) {
+  if (c->act_out) return 0;
+  CK(c->alloc(&c->act_out, (size_t)c->ncell() * evo::kActuators));
+  CK(c->alloc(&c->act_out_flag, (size_t)c->ncell()));
+  return 0;
+}
+
+int ensure_events(evo_ctx* c) {
+  if (c->ev_src) return 0;
+  CK(c->alloc(&c->ev_src, (size_t)c->ncell()));
+  CK(c->alloc(&c->ev_q, (size_t)c->ncell()));
+  CK(c->alloc(&c->ev_def, (size_t)c->ncell()));
+  return 0;
+}
+
+}  // namespace
+
+extern "C" {
+
+EVO_API const char* evo_last_error(void) { return g_err.c_str(); }
+
+EVO_API int evo_version(void) { return 1; }
+
+EVO_API int evo_create(evo_ctx** out, int width, int height, int capacity, int hidden, int device) {
+  return create_impl(out, width, height, 0, height, capacity, hidden, device, false);
+}
+
+EVO_API int evo_create_strip(evo_ctx** out, int width, int height, int64_t row0, int height_global, int capacity,
+                             int hidden, int device) {
+  return create_impl(out, width, height, row0, height_global, capacity, hidden, device, true);
+}
+
+EVO_API int evo_destroy(evo_ctx* c) {
+  if (!c) return 0;
+  cudaSetDevice(c->device);
+  cudaStreamSynchronize(c->stream);
+  for (void* p : c->allocs) cudaFree(p);
+  cudaStreamDestroy(c->stream);
+  delete c;
+  return 0;
+}
+
+EVO_API int evo_upload_planes(evo_ctx* c, const float* E, const float* I, const float* C, const int32_t* gi,
+                              const uint8_t* rot, void* stream) {
+  if (int r = check_ctx(c)) return r;
+  if (!E || !I || !C || !gi || !rot) return fail(EVO_EINVAL, "null plane pointer");
+  cudaStream_t st = pick(c, stream);
+  const evo::Planes& p = c->buf[c->front];
+  const size_t n = (size_t)c->ncell();
+  const size_t W = (size_t)c->W;
+  CK(cudaMemcpyAsync(p.E + W, E, n * 4, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(p.I + W, I, n * 4, cudaMemcpyHostToDevice, st));
+  for (int k = 0; k < 3; ++k)
+    CK(cudaMemcpyAsync(p.C + k * c->stride + W, C + k * n, n * 4, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(p.gi + W, gi, n * 4, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(p.rot + W, rot, n, cudaMemcpyHostToDevice, st));
+  if (!c->strip) CK(evo::launch_refresh_ghosts(p, c->geom(), st));
+  if (!stream) CK(cudaStreamSynchronize(st));
+  return 0;
+}
+
+EVO_API int evo_download_planes(evo_ctx* c, float* E, float* I, float* C, int32_t* gi, uint8_t* rot, void* stream) {
+  if (int r = check_ctx(c)) return r;
+  cudaStream_t st = pick(c, stream);
+  const evo::Planes& p = c->buf[c->front];
+  const size_t n = (size_t)c->ncell();
+  const size_t W = (size_t)c->W;
+  if (E) CK(cudaMemcpyAsync(E, p.E + W, n * 4, cudaMemcpyDeviceToHost, st));
+  if (I) CK(cudaMemcpyAsync(I, p.I + W, n * 4, cudaMemcpyDeviceToHost, st));
+  if (C)
+    for (int k = 0; k < 3; ++k)
+      CK(cudaMemcpyAsync(C + k * n, p.C + k * c->stride + W, n * 4, cudaMemcpyDeviceToHost, st));
+  if (gi) CK(cudaMemcpyAsync(gi, p.gi + W, n * 4, cudaMemcpyDeviceToHost, st));
+  if (rot) CK(cudaMemcpyAsync(rot, p.rot + W, n, cudaMemcpyDeviceToHost, st));
+  if (!stream) CK(cudaStreamSynchronize(st));
+  return 0;
+}
+
+EVO_API int evo_set_params(evo_ctx* c, int slot0, int n, const float* w1, const float* b1, const float* w2,
+                           const float* b2) {
+  if (int r = check_ctx(c)) return r;
+  if (slot0 < 0 || n < 0 || slot0 + n > c->cap) return fail(EVO_EINVAL, "slot range outside the pool capacity");
+  if (n == 0) return 0;
+  if (!w2 || !b2) return fail(EVO_EINVAL, "w2/b2 are required");
+  const int H = c->hidden;
+  if (H > 0 && (!w1 || !b1)) return fail(EVO_EINVAL, "w1/b1 are required for a hidden layer");
+  CK(cudaStreamSynchronize(c->stream));
+  if (H == 0) {
+    std::vector<float> wt((size_t)n * evo::kSensors * evo::kOutPad, 0.0f), bt((size_t)n * evo::kOutPad, 0.0f);
+    for (int s = 0; s < n; ++s)
+      for (int j = 0; j < evo::kActuators; ++j) {
+        for (int k = 0; k < evo::kSensors; ++k)
+          wt[((size_t)s * evo::kSensors + k) * evo::kOutPad + j] = w2[((size_t)s * evo::kActuators + j) * evo::kSensors + k];
+        bt[(size_t)s * evo::kOutPad + j] = b2[(size_t)s * evo::kActuators + j];
+      }
+    CK(cudaMemcpy(c->wA + (size_t)slot0 * evo::kSensors * evo::kOutPad, wt.data(), wt.size() * 4,
+                  cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(c->bA + (size_t)slot0 * evo::kOutPad, bt.data(), bt.size() * 4, cudaMemcpyHostToDevice));
+    return 0;
+  }
+  const int hp = c->hpad;
+  std::vector<float> W1((size_t)n * evo::kSensors * hp, 0.0f), B1((size_t)n * hp, 0.0f);
+  std::vector<float> W2((size_t)n * hp * evo::kOutPad, 0.0f), B2((size_t)n * evo::kOutPad, 0.0f);
+  for (int s = 0; s < n; ++s) {
+    for (int h = 0; h < H; ++h) {
+      for (int k = 0; k < evo::kSensors; ++k)
+        W1[((size_t)s * evo::kSensors + k) * hp + h] = w1[((size_t)s * H + h) * evo::kSensors + k];
+      B1[(size_t)s * hp + h] = b1[(size_t)s * H + h];
+      for (int j = 0; j < evo::kActuators; ++j)
+        W2[((size_t)s * hp + h) * evo::kOutPad + j] = w2[((size_t)s * evo::kActuators + j) * H + h];
+    }
+    for (int j = 0; j < evo::kActuators; ++j) B2[(size_t)s * evo::kOutPad + j] = b2[(size_t)s * evo::kActuators + j];
+  }
+  CK(cudaMemcpy(c->wA + (size_t)slot0 * evo::kSensors * hp, W1.data(), W1.size() * 4, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(c->bA + (size_t)slot0 * hp, B1.data(), B1.size() * 4, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(c->wB + (size_t)slot0 * hp * evo::kOutPad, W2.data(), W2.size() * 4, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(c->bB + (size_t)slot0 * evo::kOutPad, B2.data(), B2.size() * 4, cudaMemcpyHostToDevice));
+  return 0;
+}
+
+EVO_API int evo_set_slots(evo_ctx* c, const int8_t* state, const int32_t* peak) {
+  if (int r = check_ctx(c)) return r;
+  CK(cudaStreamSynchronize(c->stream));
+  if (state) {
+    CK(cudaMemcpy(c->census.state, state, (size_t)c->cap, cudaMemcpyHostToDevice));
+    std::vector<int64_t> ds((size_t)c->cap, -1);
+    CK(cudaMemcpy(c->census.death_step, ds.data(), ds.size() * 8, cudaMemcpyHostToDevice));
+  }
+  if (peak) CK(cudaMemcpy(c->census.peak, peak, (size_t)c->cap * 4, cudaMemcpyHostToDevice));
+  return 0;
+}
+
+EVO_API int evo_set_source_map(evo_ctx* c, const float* map) {
+  if (int r = check_ctx(c)) return r;
+  CK(cudaStreamSynchronize(c->stream));
+  if (!map) {
+    c->have_src_map = false;
+    return 0;
+  }
+  if (!c->src_map) CK(c->alloc(&c->src_map, (size_t)c->ncell()));
+  CK(cudaMemcpy(c->src_map, map, (size_t)c->ncell() * 4, cudaMemcpyHostToDevice));
+  c->have_src_map = true;
+  return 0;
+}
+
+EVO_API int evo_pass1(evo_ctx* c, const evo_scalars* s, int64_t t, int phases, int flags, void* stream) {
+  if (int r = check_ctx(c)) return r;
+  if (!s) return fail(EVO_EINVAL, "null scalars");
+  (void)t;
+  const bool inject = flags & EVO_F_INJECT_ACTIONS;
+  const bool exp = (flags & EVO_F_EXPORT_ACTIONS) && !inject;
+  if (inject && !c->act_in) return fail(EVO_EINVAL, "EVO_F_INJECT_ACTIONS without evo_set_actions");
+  if (exp) {
+    if (int r = ensure_actions_out(c)) return r;
+  }
+  c->have_export = exp;
+  evo::Pass1Args a;
+  a.g = c->geom();
+  a.front = c->buf[c->front];
+  a.back = c->buf[c->front ^ 1];
+  a.mid = c->mid;
+  a.net.hidden = c->hidden;
+  a.net.hpad = c->hpad;
+  a.net.wA = c->wA;
+  a.net.bA = c->bA;
+  a.net.wB = c->wB;
+  a.net.bB = c->bB;
+  a.s = to_scalars(*s);
+  a.phases = phases;
+  a.src_map = c->have_src_map ? c->src_map : nullptr;
+  a.act_in = c->act_in;
+  a.act_flag = c->act_in_flag;
+  a.act_out = c->act_out;
+  a.act_out_flag = c->act_out_flag;
+  a.capacity = c->cap;
+  a.stats = c->census.stats;
+  CK(evo::launch_pass1(a, inject, exp, pick(c, stream)));
+  return 0;
+}
+
+EVO_API int evo_pass2(evo_ctx* c, int64_t t, int flags, void* stream) {
+  if (int r = check_ctx(c)) return r;
+  const bool rec = flags & EVO_F_RECORD_EVENTS;
+  if (rec) {
+    if (int r = ensure_events(c)) return r;
+  }
+  c->have_events = rec;
+  evo::Pass2Args a;
+  a.g = c->geom();
+  a.back = c->buf[c->front ^ 1];
+  a.mid = c->mid;
+  a.census = c->census;
+  a.ev.src = rec ? c->ev_src : nullptr;
+  a.ev.q = c->ev_q;
+  a.ev.def = c->ev_def;
+  a.capacity = c->cap;
+  a.run_census = (flags & EVO_F_NO_CENSUS) ? 0 : 1;
+  a.t = t;
+  CK(evo::launch_pass2(a, pick(c, stream)));
+  return 0;
+}
+
+EVO_API int evo_census_finish(evo_ctx* c, int64_t t, void* stream) {
+  if (int r = check_ctx(c)) return r;
+  CK(evo::launch_census_finish(c->census, c->cap, t, pick(c, stream)));
+  return 0;
+}
+
+EVO_API int evo_swap(evo_ctx* c) {
+  if (!c) return fail(EVO_EINVAL, "null context");
+  c->front ^= 1;
+  return 0;
+}
+
+EVO_API int evo_step(evo_ctx* c, const evo_scalars* s, int64_t t, int phases, int flags, void* stream) {
+  if (c && c->strip) return fail(EVO_EINVAL, "strip contexts step through evo_pass1/evo_pass2 with a halo exchange");
+  if (int r = evo_pass1(c, s, t, phases, flags, stream)) return r;
+  if (int r = evo_pass2(c, t, flags, stream)) return r;
+  return evo_swap(c);
+}
+
+EVO_API int evo_run(evo_ctx* c, const evo_scalars* s, int64_t t0, int k, void* stream) {
+  if (!s && k > 0) return fail(EVO_EINVAL, "null scalars");
+  for (int i = 0; i < k; ++i)
+    if (int r = evo_step(c, s + i, t0 + i, EVO_PH_ALL, 0, stream)) return r;
+  return 0;
+}
+
+EVO_API int evo_refresh_ghosts(evo_ctx* c, void* stream) {
+  if (int r = check_ctx(c)) return r;
+  if (c->strip) return 0;
+  CK(evo::launch_refresh_ghosts(c->buf[c->front], c->geom(), pick(c, stream)));
+  return 0;
+}
+
+EVO_API int evo_sync(evo_ctx* c) {
+  if (int r = check_ctx(c)) return r;
+  CK(cudaStreamSynchronize(c->stream));
+  CK(cudaDeviceSynchronize());
+  return 0;
+}
+
+EVO_API int evo_set_actions(evo_ctx* c, const int64_t* cells, int64_t n, const float* acts) {
+  if (int r = check_ctx(c)) return r;
+  if (n < 0 || (n > 0 && (!cells || !acts))) return fail(EVO_EINVAL, "bad action arrays");
+  if (int r = ensure_actions_in(c)) return r;
+  const long long nc = c->ncell();
+  for (int64_t i = 0; i < n; ++i)
+    if (cells[i] < 0 || cells[i] >= nc) return fail(EVO_EINVAL, "action cell index out of range");
+  CK(cudaStreamSynchronize(c->stream));
+  CK(cudaMemset(c->act_in_flag, 0, (size_t)nc));
+  if (n == 0) return 0;
+  int64_t* dcells = nullptr;
+  float* drows = nullptr;
+  CK(cudaMalloc(&dcells, (size_t)n * 8));
+  cudaError_t e = cudaMalloc(&drows, (size_t)n * evo::kActuators * 4);
+  if (e == cudaSuccess) e = cudaMemcpy(dcells, cells, (size_t)n * 8, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemcpy(drows, acts, (size_t)n * evo::kActuators * 4, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = evo::launch_scatter_actions(c->act_in, c->act_in_flag, dcells, drows, n, nc, c->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+  cudaFree(dcells);
+  cudaFree(drows);
+  CK(e);
+  return 0;
+}
+
+EVO_API int evo_get_actions(evo_ctx* c, int64_t capacity, int64_t* cells, float* acts, int64_t* n) {
+  if (int r = check_ctx(c)) return r;
+  if (!n) return fail(EVO_EINVAL, "n is null");
+  if (!c->have_export || !c->act_out) return fail(EVO_EINVAL, "no exported actions (step with EVO_F_EXPORT_ACTIONS)");
+  CK(cudaStreamSynchronize(c->stream));
+  CK(cudaDeviceSynchronize());
+  const long long nc = c->ncell();
+  std::vector<uint8_t> flag((size_t)nc);
+  std::vector<float> rows((size_t)nc * evo::kActuators);
+  CK(cudaMemcpy(flag.data(), c->act_out_flag, (size_t)nc, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(rows.data(), c->act_out, rows.size() * 4, cudaMemcpyDeviceToHost));
+  int64_t m = 0;
+  for (long long i = 0; i < nc; ++i) {
+    if (!flag[(size_t)i]) continue;
+    if (m < capacity) {
+      if (cells) cells[m] = i;
+      if (acts) std::memcpy(acts + m * evo::kActuators, rows.data() + i * evo::kActuators, evo::kActuators * 4);
+    }
+    ++m;
+  }
+  *n = m;
+  return 0;
+}
+
+EVO_API int evo_read_census(evo_ctx* c, int32_t* counts, int8_t* state, int64_t* death_step, int32_t* peak) {
+  if (int r = check_ctx(c)) return r;
+  CK(cudaStreamSynchronize(c->stream));
+  CK(cudaDeviceSynchronize());
+  const size_t cap = (size_t)c->cap;
+  if (counts) CK(cudaMemcpy(counts, c->census.counts_last, cap * 4, cudaMemcpyDeviceToHost));
+  if (state) CK(cudaMemcpy(state, c->census.state, cap, cudaMemcpyDeviceToHost));
+  if (death_step) CK(cudaMemcpy(death_step, c->census.death_step, cap * 8, cudaMemcpyDeviceToHost));
+  if (peak) CK(cudaMemcpy(peak, c->census.peak, cap * 4, cudaMemcpyDeviceToHost));
+  return 0;
+}
+
+EVO_API int evo_read_stats(evo_ctx* c, int64_t* adoptions, int64_t* extinctions) {
+  if (int r = check_ctx(c)) return r;
+  CK(cudaStreamSynchronize(c->stream));
+  CK(cudaDeviceSynchronize());
+  long long st[2];
+  CK(cudaMemcpy(st, c->census.stats, sizeof(st), cudaMemcpyDeviceToHost));
+  if (adoptions) *adoptions = st[0];
+  if (extinctions) *extinctions = st[1];
+  return 0;
+}
+
+EVO_API int evo_read_events(evo_ctx* c, int64_t capacity, int64_t* target, int64_t* source, int32_t* winner,
+                            int32_t* defender, int64_t* direction, float* quantity, int64_t* m) {
+  if (int r = check_ctx(c)) return r;
+  if (!m) return fail(EVO_EINVAL, "m is null");
+  if (!c->have_events || !c->ev_src) return fail(EVO_EINVAL, "no recorded events (step with EVO_F_RECORD_EVENTS)");
+  CK(cudaStreamSynchronize(c->stream));
+  CK(cudaDeviceSynchronize());
+  const long long nc = c->ncell();
+  std::vector<int64_t> src((size_t)nc);
+  std::vector<float> q((size_t)nc);
+  std::vector<int32_t> def((size_t)nc), gi((size_t)nc);
+  std::vector<uint8_t> rot((size_t)nc);
+  // events belong to the step that produced the current front buffer
+  const evo::Planes& p = c->buf[c->front];
+  CK(cudaMemcpy(src.data(), c->ev_src, (size_t)nc * 8, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(q.data(), c->ev_q, (size_t)nc * 4, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(def.data(), c->ev_def, (size_t)nc * 4, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(gi.data(), p.gi + c->W, (size_t)nc * 4, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(rot.data(), p.rot + c->W, (size_t)nc, cudaMemcpyDeviceToHost));
+  int64_t k = 0;
+  for (long long i = 0; i < nc; ++i) {
+    if (src[(size_t)i] < 0) continue;
+    if (k < capacity) {
+      if (target) target[k] = c->row0 * c->W + i;
+      if (source) source[k] = src[(size_t)i];
+      if (winner) winner[k] = gi[(size_t)i];
+      if (defender) defender[k] = def[(size_t)i];
+      if (direction) direction[k] = rot[(size_t)i];
+      if (quantity) quantity[k] = q[(size_t)i];
+    }
+    ++k;
+  }
+  *m = k;
+  return 0;
+}
+
+EVO_API int evo_patch_genomes(evo_ctx* c, const int64_t* cells, const int32_t* slots, int64_t n) {
+  if (int r = check_ctx(c)) return r;
+  if (n <= 0) return 0;
+  if (!cells || !slots) return fail(EVO_EINVAL, "null arrays");
+  const long long nc = c->ncell();
+  for (int64_t i = 0; i < n; ++i) {
+    if (cells[i] < 0 || cells[i] >= nc) return fail(EVO_EINVAL, "cell index out of range");
+    if (slots[i] < -1 || slots[i] >= c->cap) return fail(EVO_EINVAL, "slot outside the pool capacity");
+  }
+  CK(cudaStreamSynchronize(c->stream));
+  int64_t* dc = nullptr;
+  int32_t* ds = nullptr;
+  CK(cudaMalloc(&dc, (size_t)n * 8));
+  cudaError_t e = cudaMalloc(&ds, (size_t)n * 4);
+  if (e == cudaSuccess) e = cudaMemcpy(dc, cells, (size_t)n * 8, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemcpy(ds, slots, (size_t)n * 4, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = evo::launch_patch_genomes(c->buf[c->front].gi, c->W, dc, ds, n, c->stream);
+  if (e == cudaSuccess && !c->strip) e = evo::launch_refresh_ghosts(c->buf[c->front], c->geom(), c->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+  cudaFree(dc);
+  cudaFree(ds);
+  CK(e);
+  return 0;
+}
+
+EVO_API int evo_plane_ptr(evo_ctx* c, int which, int buffer, void** ptr, int64_t* plane_stride) {
+  if (!c || !ptr) return fail(EVO_EINVAL, "null argument");
+  const evo::Planes& p = c->buf[(c->front ^ (buffer ? 1 : 0)) & 1];
+  switch (which) {
+    case 0: *ptr = p.E; break;
+    case 1: *ptr = p.I; break;
+    case 2: *ptr = p.C; break;
+    case 3: *ptr = p.gi; break;
+    case 4: *ptr = p.rot; break;
+    case 5: *ptr = c->mid.I; break;
+    case 6: *ptr = c->mid.gi; break;
+    case 7: *ptr = c->mid.rp; break;
+    case 8: *ptr = c->mid.q; break;
+    default: return fail(EVO_EINVAL, "unknown plane");
+  }
+  if (plane_stride) *plane_stride = c->stride;
+  return 0;
+}
+
+EVO_API int evo_fnv1a64(uint64_t h, const uint8_t* data, int64_t n, uint64_t* out) {
+  if (!out || (n > 0 && !data)) return fail(EVO_EINVAL, "null argument");
+  const uint64_t prime = 0x100000001B3ULL;
+  for (int64_t k = 0; k < n; ++k) h = (h ^ (uint64_t)data[k]) * prime;
+  *out = h;
+  return 0;
+}
+
+}  // extern "C"

@@ -1,0 +1,120 @@
+// Internal declarations shared by the kernels and the C ABI layer.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "evoca_b200.h"
+
+namespace evo {
+
+constexpr int kTileW = 32;               // pass-1 tile: 32 x 32 cells
+constexpr int kTileH = 32;
+constexpr int kTileCells = kTileW * kTileH;
+constexpr int kHaloW = kTileW + 2;       // tile + 1-cell Moore halo
+constexpr int kHaloH = kTileH + 2;
+constexpr int kHaloCells = kHaloW * kHaloH;
+constexpr int kThreads1 = 256;           // pass-1 CTA
+constexpr int kThreads2 = 256;           // pass-2 CTA
+constexpr int kSensors = 45;             // hypernet.py:35-38
+constexpr int kActuators = 13;
+constexpr int kOutPad = 16;              // 13 actuators padded to 4 float4
+constexpr int kMaxCapacity = 8192;       // device census bins per CTA (smem)
+
+// Proposal byte written by pass 1 (one per cell): bits 0-2 rotation (front),
+// bits 3-5 shipment direction, bit 6 = cell ships this step.
+constexpr uint8_t kShipBit = 0x40;
+
+struct Scalars {
+  int mode;  // 0 none, 1 day, 2 night
+  float rho, drain;
+  float kinv, kliq, einv, eliq, alpha, upkeep, dstarve, imin;
+};
+
+// Device state of one strip.  Every plane pointer addresses ghost row -1;
+// row y (-1..H) lives at ptr + (y + 1) * W.
+struct Planes {
+  float* E;
+  float* I;
+  float* C;  // 3 planes, stride = plane stride
+  int32_t* gi;
+  uint8_t* rot;
+};
+
+struct Mid {
+  float* I;      // infrastructure after invest/liquidate/upkeep and withdrawal
+  int32_t* gi;   // genome after starvation deaths
+  uint8_t* rp;   // proposal byte
+  float* q;      // shipped quantity
+};
+
+struct Params {
+  int hidden;     // 0 = direct 45->13
+  int hpad;       // hidden rounded up to 8
+  const float* wA;  // direct: [cap][45][16]; hidden: W1 [cap][45][hpad]
+  const float* bA;  // direct: [cap][16];     hidden: b1 [cap][hpad]
+  const float* wB;  // hidden: W2^T [cap][hpad][16]
+  const float* bB;  // hidden: b2 [cap][16]
+};
+
+struct Census {
+  int32_t* counts;       // accumulated by pass 2 (cap)
+  int32_t* counts_last;  // published by the epilogue (cap)
+  int8_t* state;         // 0 free 1 live 2 dead
+  int64_t* death_step;
+  int32_t* peak;
+  unsigned int* done;    // CTA completion ticket
+  long long* stats;      // [0] adoptions this step, [1] newly dead this step
+};
+
+struct Events {
+  int64_t* src;   // per cell: global source index of the adopting winner, or -1
+  float* q;
+  int32_t* def;
+};
+
+struct StepGeom {
+  int W, H;            // strip width / height
+  long long row0;      // first global row of the strip
+  int Hg;              // global torus height
+  long long stride;    // elements per plane including ghost rows
+  int own_ghosts;      // 1: single strip, kernels write the wrapped ghost rows themselves
+};
+
+struct Pass1Args {
+  StepGeom g;
+  Planes front, back;
+  Mid mid;
+  Params net;
+  Scalars s;
+  int phases;
+  const float* src_map;      // nullable, (H,W)
+  const float* act_in;       // inject: (H*W,13)
+  const uint8_t* act_flag;   // inject: (H*W)
+  float* act_out;            // export: (H*W,13)
+  uint8_t* act_out_flag;     // export: (H*W)
+  int capacity;
+  long long* stats;
+};
+
+struct Pass2Args {
+  StepGeom g;
+  Planes back;  // writes I, gi, rot
+  Mid mid;
+  Census census;
+  Events ev;     // ev.src == nullptr -> not recorded
+  int capacity;
+  int run_census;  // 1 -> last CTA runs the census epilogue
+  long long t;
+};
+
+cudaError_t launch_pass1(const Pass1Args& a, bool inject, bool export_actions, cudaStream_t st);
+cudaError_t launch_pass2(const Pass2Args& a, cudaStream_t st);
+cudaError_t launch_census_finish(const Census& c, int capacity, long long t, cudaStream_t st);
+cudaError_t launch_refresh_ghosts(const Planes& p, const StepGeom& g, cudaStream_t st);
+cudaError_t launch_scatter_actions(float* act, uint8_t* flag, const int64_t* cells, const float* rows, long long n,
+                                   long long ncell, cudaStream_t st);
+cudaError_t launch_patch_genomes(int32_t* gi, int W, const int64_t* cells, const int32_t* slots, long long n,
+                                 cudaStream_t st);
+
+}  // namespace evo

@@ -1,0 +1,408 @@
+"""Step scheduler with the reference's API, backed by the device.
+
+Drop-in for /root/reference/pkg/src/evoca/engine.py:
+  * ``step(state)``   - one step of a host-resident state: upload the front
+    planes, run the two device passes, download into the back planes, census,
+    swap (engine.py:233-248).  Works on this package's ``SimState`` and on
+    the reference's own ``SimState`` (duck-typed: ``substrate``, ``pool``,
+    ``config``, ``master_seed``).
+  * ``run(state, steps, hooks, should_stop)`` - the batch loop
+    (engine.py:251-271), device-resident between hook points.
+  * ``build_action_field(state)`` - device sense + controller, exported as an
+    ``ActionField`` (engine.py:193-230).
+  * ``digest(state)`` - FNV-1a over the front planes (engine.py:301-315).
+Host NEAT radiation (physics.apply_radiation, physics.py:346-392) stays on
+the host; when its probabilities are non-zero the engine records adoption
+events on the device and hands them to a host callback per step.
+"""
+
+from __future__ import annotations
+
+import logging
+from dataclasses import dataclass, field
+from typing import Callable, Optional
+
+import numpy as np
+
+from . import _lib
+from .device import DeviceSubstrate
+from .hypernet import DenseParams, DirectParams
+from .physics import ActionField, AdoptionEvents, PhysicsParams, step_scalars
+from .pool import SlotPool
+from .substrate import Substrate, create_substrate
+from .synth import BASELINE_CONFIGS, synth_arrays, synth_params
+
+__all__ = [
+    "GridConfig", "HypernetConfig", "EvolutionRates", "ExperimentConfig",
+    "SimState", "Hook", "baseline_state", "step", "run", "build_action_field", "digest",
+    "device_of", "sync_to_host",
+]
+
+log = logging.getLogger(__name__)
+
+
+@dataclass
+class GridConfig:
+    width: int = 256
+    height: int = 256
+
+
+@dataclass
+class HypernetConfig:
+    hidden_size: int = 16  # 0 selects the BASELINE direct 45->13 controller
+
+
+@dataclass
+class EvolutionRates:
+    """The two rates the step consults (neuroevo.py:170-203); NEAT's
+    mutation rates live with the host genetics."""
+
+    p_radiation: float = 0.0
+    p_merge: float = 0.0
+
+
+@dataclass
+class ExperimentConfig:
+    grid: GridConfig = field(default_factory=GridConfig)
+    seed: int = 0
+    physics: PhysicsParams = field(default_factory=PhysicsParams)
+    evolution: EvolutionRates = field(default_factory=EvolutionRates)
+    hypernet: HypernetConfig = field(default_factory=HypernetConfig)
+
+
+@dataclass
+class SimState:
+    """engine.py:61-91 fields plus the device handle (created lazily)."""
+
+    substrate: Substrate
+    pool: object
+    config: object
+    master_seed: int
+    workers: int = 1
+    last_adoptions: int = 0
+    last_extinctions: int = 0
+    radiation: Optional[Callable] = None
+
+    @property
+    def t(self) -> int:
+        return self.substrate.step_counter
+
+    @property
+    def physics(self):
+        return self.config.physics
+
+    @property
+    def rates(self):
+        return self.config.evolution
+
+
+@dataclass(frozen=True)
+class Hook:
+    every: int
+    fn: Callable
+
+
+# -- device binding -------------------------------------------------------------
+
+
+class _Binding:
+    """Per-state device context plus the host<->device coherence bookkeeping."""
+
+    def __init__(self, state, device: int = 0):
+        sub = state.substrate
+        self.hidden = _hidden_of(state)
+        self.capacity = int(state.pool.capacity)
+        self.dev = DeviceSubstrate(sub.width, sub.height, self.capacity, self.hidden, device=device)
+        self.param_ids = [None] * self.capacity
+        self.pool_version = None
+        self.device_ahead = False  # device front newer than the host mirror
+
+    def sync_params(self, pool) -> None:
+        ver = getattr(pool, "version", None)
+        if ver is not None and ver == self.pool_version:
+            return
+        changed = []
+        for slot in range(self.capacity):
+            p = pool.params(slot)
+            if p is not None and self.param_ids[slot] is not p:
+                changed.append(slot)
+        # upload contiguous runs of changed slots
+        i = 0
+        while i < len(changed):
+            j = i
+            while j + 1 < len(changed) and changed[j + 1] == changed[j] + 1:
+                j += 1
+            lo, hi = changed[i], changed[j] + 1
+            self.dev.set_params([_as_params(pool.params(s), self.hidden) for s in range(lo, hi)], slot0=lo)
+            for s in range(lo, hi):
+                self.param_ids[s] = pool.params(s)
+            i = j + 1
+        self.dev.set_slots(_slot_states(pool), _peaks(pool))
+        self.pool_version = ver
+
+
+def _hidden_of(state) -> int:
+    hn = getattr(state.config, "hypernet", None)
+    hidden = getattr(hn, "hidden_size", None)
+    if hidden is None:
+        raise ValueError("config.hypernet.hidden_size is required")
+    # a reference config with DirectParams in the pool means the direct net
+    for slot in range(int(state.pool.capacity)):
+        p = state.pool.params(slot)
+        if p is not None:
+            if isinstance(p, DirectParams) or (hasattr(p, "w") and not hasattr(p, "w1")):
+                return 0
+            return int(p.w1.shape[0])
+    return int(hidden)
+
+
+def _as_params(p, hidden):
+    if hidden == 0:
+        if isinstance(p, DirectParams):
+            return p
+        return DirectParams(np.asarray(p.w, np.float32), np.asarray(p.b, np.float32))
+    if isinstance(p, DenseParams):
+        return p
+    return DenseParams(np.asarray(p.w1, np.float32), np.asarray(p.b1, np.float32),
+                       np.asarray(p.w2, np.float32), np.asarray(p.b2, np.float32))
+
+
+def _slot_states(pool) -> np.ndarray:
+    if hasattr(pool, "slot_states"):
+        return pool.slot_states()
+    if hasattr(pool, "slots"):  # reference GenomePool
+        code = {"free": 0, "live": 1, "dead": 2}
+        return np.array([code[s.state] for s in pool.slots], np.int8)
+    return np.asarray(pool.live_mask(), np.int8)
+
+
+def _peaks(pool) -> np.ndarray:
+    if hasattr(pool, "peaks"):
+        return pool.peaks()
+    out = np.zeros(int(pool.capacity), np.int32)
+    if hasattr(pool, "slots"):
+        for i, s in enumerate(pool.slots):
+            if s.lineage_id >= 0 and s.lineage_id in pool.records:
+                out[i] = pool.records[s.lineage_id].peak_population
+    return out
+
+
+def device_of(state, device: int = 0) -> DeviceSubstrate:
+    """The state's device context (created on first use)."""
+    b = getattr(state, "_evo_binding", None)
+    if b is None:
+        b = _Binding(state, device)
+        state._evo_binding = b
+    return b.dev
+
+
+def _binding(state) -> _Binding:
+    device_of(state)
+    return state._evo_binding
+
+
+def _radiation_active(state) -> bool:
+    r = state.config.evolution
+    return getattr(r, "p_radiation", 0.0) > 0.0 or getattr(r, "p_merge", 0.0) > 0.0
+
+
+def _radiation_fn(state):
+    if getattr(state, "radiation", None) is not None:
+        return state.radiation
+    try:  # the reference's host NEAT, when installed alongside
+        from evoca.physics import apply_radiation  # type: ignore
+
+        return apply_radiation
+    except Exception as exc:  # pragma: no cover - depends on the host install
+        raise NotImplementedError(
+            "radiation is enabled but no host NEAT callback is available: set state.radiation "
+            "or install the reference package"
+        ) from exc
+
+
+# -- the drop-in step -------------------------------------------------------------
+
+
+def step(state) -> None:
+    """One step of a host-resident state (engine.py:233-248)."""
+    b = _binding(state)
+    sub = state.substrate
+    t = sub.step_counter
+    b.sync_params(state.pool)
+    if b.device_ahead:
+        _download_front(state)
+    b.dev.upload(sub.front)
+    phys = state.config.physics
+    rad = _radiation_active(state)
+    flags = (_lib.F_RECORD_EVENTS | _lib.F_NO_CENSUS) if rad else 0
+    b.dev.step_raw(step_scalars(t, phys), t, flags=flags, source_map=phys.energy_source_map)
+    b.dev.download(sub.back)
+    adoptions, _ = b.dev.read_stats()
+    if rad:
+        events = b.dev.read_events()
+        if len(events):
+            gi_before = sub.back.genome_index.copy()
+            _radiation_fn(state)(events, state.pool, state.config.evolution, sub.back, state.master_seed, t)
+            moved = np.flatnonzero(sub.back.genome_index.ravel() != gi_before.ravel())
+            if len(moved):
+                b.dev.patch_genomes(moved, sub.back.genome_index.ravel()[moved])
+        gi = sub.back.genome_index
+        counts = np.bincount(gi[gi >= 0], minlength=int(state.pool.capacity))
+        b.dev.census_finish(t)  # resets the device accumulators
+        newly_dead = state.pool.update_census(counts, t + 1)
+        b.pool_version = None
+        b.sync_params(state.pool)
+    else:
+        counts, _, _, _ = b.dev.read_census()
+        newly_dead = state.pool.update_census(counts, t + 1)
+    sub.swap_buffers()
+    state.last_adoptions = int(adoptions)
+    state.last_extinctions = len(newly_dead)
+    b.device_ahead = False
+
+
+def _download_front(state) -> None:
+    b = _binding(state)
+    b.dev.download(state.substrate.front)
+    _fold_census(state)
+    b.device_ahead = False
+
+
+def _fold_census(state) -> None:
+    """Bring the device's deferred census into the host pool."""
+    b = _binding(state)
+    counts, st, death, peak = b.dev.read_census()
+    pool = state.pool
+    if isinstance(pool, SlotPool):
+        pool.apply_device_census(st, death, peak)
+        b.pool_version = pool.version
+        return
+    # foreign pool (e.g. the reference GenomePool): replay update_census in
+    # death-step order, feeding each slot's peak so peaks update identically
+    live = np.asarray(pool.live_mask(), bool)
+    newly = [i for i in np.flatnonzero(live) if st[i] == 2]
+    for d in sorted({int(death[i]) for i in newly}):
+        feed = np.where(live, np.maximum(peak, 1), 0).astype(np.int64)
+        for i in newly:
+            if int(death[i]) <= d:
+                feed[i] = 0
+        pool.update_census(feed, d)
+    feed = np.where(np.asarray(pool.live_mask(), bool), peak, 0).astype(np.int64)
+    pool.update_census(np.maximum(feed, 1) * np.asarray(pool.live_mask(), np.int64), int(state.substrate.step_counter))
+
+
+def sync_to_host(state) -> None:
+    """Make the host mirror (front planes + pool census) current."""
+    b = getattr(state, "_evo_binding", None)
+    if b is not None and b.device_ahead:
+        _download_front(state)
+
+
+def run(state, steps: int, hooks=(), should_stop: Optional[Callable[[], bool]] = None) -> None:
+    """engine.run (engine.py:251-271): device-resident between hooks."""
+    if _radiation_active(state):
+        for _ in range(steps):
+            if should_stop is not None and should_stop():
+                break
+            step(state)
+            _fire(state, hooks)
+        return
+    b = _binding(state)
+    sub = state.substrate
+    b.sync_params(state.pool)
+    if not b.device_ahead:
+        b.dev.upload(sub.front)
+    phys = state.config.physics
+    for _ in range(steps):
+        if should_stop is not None and should_stop():
+            break
+        t = sub.step_counter
+        b.dev.step_raw(step_scalars(t, phys), t, source_map=phys.energy_source_map)
+        sub.step_counter = t + 1
+        b.device_ahead = True
+        due = [h for h in hooks if sub.step_counter % h.every == 0]
+        if due:
+            _download_front(state)
+            adoptions, extinctions = b.dev.read_stats()
+            state.last_adoptions, state.last_extinctions = int(adoptions), int(extinctions)
+            _fire(state, due)
+            b.sync_params(state.pool)
+            b.dev.upload(sub.front)  # hooks may write the front
+    if b.device_ahead:
+        _download_front(state)
+        adoptions, extinctions = b.dev.read_stats()
+        state.last_adoptions, state.last_extinctions = int(adoptions), int(extinctions)
+
+
+def _fire(state, hooks) -> None:
+    for h in hooks:
+        if state.substrate.step_counter % h.every == 0:
+            try:
+                h.fn(state)
+            except Exception:
+                log.exception("hook failed at step %d", state.substrate.step_counter)
+
+
+def build_action_field(state) -> ActionField:
+    """Sense + controller on the device for every occupied front cell."""
+    b = _binding(state)
+    b.sync_params(state.pool)
+    if b.device_ahead:
+        _download_front(state)
+    b.dev.upload(state.substrate.front)
+    t = state.substrate.step_counter
+    b.dev.pass1(step_scalars(t, state.config.physics), t, phases=0, flags=_lib.F_EXPORT_ACTIONS)
+    cells, acts = b.dev.get_actions()
+    if len(cells) == 0:
+        return ActionField.empty()
+    return ActionField.from_block(cells, acts)
+
+
+_FNV_OFFSET = 0xCBF29CE484222325
+
+
+def digest(state) -> int:
+    """64-bit FNV-1a over every front plane in channel-table order, then
+    genome, then rotation (engine.py:301-315)."""
+    import ctypes as C
+
+    sync_to_host(state)
+    lib = _lib.load()
+    front = state.substrate.front
+    h = C.c_uint64(_FNV_OFFSET)
+    arrays = []
+    for spec in state.substrate.specs:
+        arr = front.channels[spec.name]
+        arrays.extend(arr[k] for k in range(spec.arity))
+    arrays += [front.genome_index, front.rotation]
+    for a in arrays:
+        buf = np.ascontiguousarray(a).view(np.uint8).reshape(-1)
+        _lib.check(lib.evo_fnv1a64(h.value, _lib.ptr(buf), buf.size, C.byref(h)))
+    return int(h.value)
+
+
+# -- BASELINE synthetic states -------------------------------------------------------
+
+
+def baseline_state(name: str = "c2", seed: int = 0, width: int | None = None, height: int | None = None,
+                   genomes: int | None = None) -> SimState:
+    """A seeded BASELINE.json configuration (synth.py draw order), optionally
+    resized (bounded CPU samples / parity windows)."""
+    cfg = BASELINE_CONFIGS[name]
+    w = width or cfg.width
+    h = height or cfg.height
+    g = genomes or cfg.genomes
+    ec = ExperimentConfig(grid=GridConfig(w, h), seed=seed, hypernet=HypernetConfig(cfg.hidden))
+    ec.physics.cycle_period = cfg.cycle_period
+    sub = create_substrate(w, h)
+    E, I, Cm, gi, rot = synth_arrays(h, w, g, seed, cfg.sparse_infra)
+    f = sub.front
+    f.channels["energy"][0] = E
+    f.channels["infrastructure"][0] = I
+    f.channels["communication"][:] = Cm
+    f.genome_index[:] = gi
+    f.rotation[:] = rot
+    pool = SlotPool(g)
+    for i, p in enumerate(synth_params(g, cfg.hidden, seed)):
+        pool.install(i, p)
+    return SimState(substrate=sub, pool=pool, config=ec, master_seed=seed)

@@ -1,0 +1,114 @@
+"""Slot pool for device runs (subset of neuroevo.GenomePool).
+
+The reference's ``GenomePool`` (/root/reference/pkg/src/evoca/neuroevo.py:
+415-545) owns NEAT genomes, lineage records and cached dense params.  NEAT
+genetics stay on the host and out of this package's scope; the engine only
+needs the pool's slot table: ``capacity``, ``params(slot)``, liveness and
+``update_census``.  ``SlotPool`` provides exactly that surface for the
+BASELINE synthetic configurations (genomes = directly installed weight
+tables).  Any object with the same methods - including the reference
+``GenomePool`` itself - can be passed to the engine instead.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import Optional
+
+import numpy as np
+
+__all__ = ["SlotPool", "SlotRecord"]
+
+
+@dataclass
+class SlotRecord:
+    lineage_id: int
+    slot: int
+    birth_step: int
+    death_step: Optional[int] = None
+    peak_population: int = 0
+
+
+class SlotPool:
+    def __init__(self, capacity: int):
+        if capacity < 1:
+            raise ValueError("pool capacity must be positive")
+        self.capacity = capacity
+        self._params = [None] * capacity
+        self._state = np.zeros(capacity, np.int8)  # 0 free, 1 live, 2 dead
+        self._lineage = np.full(capacity, -1, np.int64)
+        self.records: dict[int, SlotRecord] = {}
+        self.next_lineage_id = 0
+        self.version = 0  # bumped on every params/liveness change
+
+    def install(self, slot: int, params, birth_step: int = 0) -> int:
+        """Put a parameter set in a slot and mark it live (admission without NEAT)."""
+        if not 0 <= slot < self.capacity:
+            raise ValueError("slot outside the pool capacity")
+        self._params[slot] = params
+        self._state[slot] = 1
+        lid = self.next_lineage_id
+        self.next_lineage_id += 1
+        self._lineage[slot] = lid
+        self.records[lid] = SlotRecord(lid, slot, birth_step)
+        self.version += 1
+        return slot
+
+    def params(self, slot: int):
+        return self._params[slot]
+
+    def is_live(self, slot: int) -> bool:
+        return 0 <= slot < self.capacity and self._state[slot] == 1
+
+    def live_mask(self) -> np.ndarray:
+        return self._state == 1
+
+    def live_count(self) -> int:
+        return int((self._state == 1).sum())
+
+    def live_slots(self) -> list[int]:
+        return [int(i) for i in np.flatnonzero(self._state == 1)]
+
+    def lineage(self, slot: int) -> int:
+        return int(self._lineage[slot])
+
+    def record_for_slot(self, slot: int) -> SlotRecord:
+        return self.records[int(self._lineage[slot])]
+
+    def slot_states(self) -> np.ndarray:
+        return self._state.copy()
+
+    def peaks(self) -> np.ndarray:
+        out = np.zeros(self.capacity, np.int32)
+        for i in np.flatnonzero(self._lineage >= 0):
+            out[i] = self.records[int(self._lineage[i])].peak_population
+        return out
+
+    def update_census(self, counts, step: int) -> list[int]:
+        """Same contract as GenomePool.update_census (neuroevo.py:521-542)."""
+        dead = []
+        for i in np.flatnonzero(self._state == 1):
+            c = int(counts[i])
+            rec = self.records[int(self._lineage[i])]
+            if c == 0:
+                self._state[i] = 2
+                rec.death_step = step
+                dead.append(int(i))
+            elif c > rec.peak_population:
+                rec.peak_population = c
+        return dead
+
+    def apply_device_census(self, state: np.ndarray, death_step: np.ndarray, peak: np.ndarray) -> list[int]:
+        """Fold the device's deferred census (slot state, first zero-count
+        step, peak) into the records; equivalent to having called
+        update_census every step."""
+        dead = []
+        for i in np.flatnonzero(self._state == 1):
+            rec = self.records[int(self._lineage[i])]
+            if peak[i] > rec.peak_population:
+                rec.peak_population = int(peak[i])
+            if state[i] == 2:
+                self._state[i] = 2
+                rec.death_step = int(death_step[i])
+                dead.append(int(i))
+        return dead

@@ -1,0 +1,450 @@
+"""Parity of the CUDA path (through the C ABI) against the oracle and the
+reference's golden vectors.  Tiers:
+  A  given identical actions, post-state / events / census bit-exact;
+  B  device actions vs reference (or oracle) actions within 1e-5 relative;
+  D  free-running: integer state bit-exact, continuous within tolerance.
+Continuous tolerance: |a-b| <= 1e-5 * max(|b|, 1)."""
+
+import numpy as np
+import pytest
+
+from oracle import oracle as orc
+from paper_2406_09654_b200 import _lib, engine, physics
+from paper_2406_09654_b200.device import DeviceSubstrate
+from paper_2406_09654_b200.hypernet import DenseParams, DirectParams
+from tests import _cases as CS
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-5
+
+
+def close(a, b, tol=TOL):
+    a = np.asarray(a, np.float64)
+    b = np.asarray(b, np.float64)
+    return bool(np.all(np.abs(a - b) <= tol * np.maximum(np.abs(b), 1.0)))
+
+
+def rel_err(a, b):
+    a = np.asarray(a, np.float64)
+    b = np.asarray(b, np.float64)
+    return float(np.max(np.abs(a - b) / np.maximum(np.abs(b), 1e-30))) if a.size else 0.0
+
+
+def oracle_phys_to_params(ph: orc.Phys) -> physics.PhysicsParams:
+    return physics.PhysicsParams(**{k: getattr(ph, k) for k in physics.PhysicsParams.__dataclass_fields__})
+
+
+def net_params(net: orc.Net):
+    if net.hidden == 0:
+        return [DirectParams(net.w2[i], net.b2[i]) for i in range(net.capacity)]
+    return [DenseParams(net.w1[i], net.b1[i], net.w2[i], net.b2[i]) for i in range(net.capacity)]
+
+
+def make_dev(p: orc.Planes, capacity: int, net: orc.Net | None = None, live=None):
+    h, w = p.shape
+    dev = DeviceSubstrate(w, h, capacity, hidden=0 if net is None else net.hidden)
+    if net is not None:
+        dev.set_params(net_params(net))
+    st = np.zeros(capacity, np.int8)
+    st[: capacity if live is None else live] = 1
+    dev.set_slots(st)
+    dev.upload(p)
+    return dev
+
+
+def download(dev) -> orc.Planes:
+    h, w = dev.height, dev.width
+    p = orc.Planes(np.empty((h, w), np.float32), np.empty((h, w), np.float32), np.empty((3, h, w), np.float32),
+                   np.empty((h, w), np.int32), np.empty((h, w), np.uint8))
+    dev.download(p)
+    return p
+
+
+def events_rows(ev):
+    return [(float(t), float(s), float(w), float(d), float(r), float(q))
+            for t, s, w, d, r, q in zip(ev.target, ev.source, ev.winner_slot, ev.defender_slot, ev.direction,
+                                        ev.quantity)]
+
+
+# -- tier A: physics given the reference's actions ---------------------------------
+
+
+@pytest.mark.parametrize("c", range(40))
+def test_physics_cases_bit_exact(c):
+    z = CS.load("physics_cases.npz")
+    case = CS.physics_case(z, c)
+    dev = make_dev(case["pre"], 12)
+    dev.set_actions(case["acts"].cells, case["acts"].a)
+    params = oracle_phys_to_params(case["phys"])
+    dev.step_raw(physics.step_scalars(case["t"], params), case["t"],
+                 flags=_lib.F_INJECT_ACTIONS | _lib.F_RECORD_EVENTS)
+    post = download(dev)
+    assert post.equal(case["post"])
+    assert events_rows(dev.read_events()) == case["events"]
+    counts, _, _, _ = dev.read_census()
+    assert np.array_equal(counts, case["counts"])
+    dev.close()
+
+
+def test_explore_cases_bit_exact():
+    z = CS.load("explore_cases.npz")
+    for c in range(int(z["n_cases"])):
+        key = f"c{c:02d}_"
+        p = CS.planes(z, key, "pre")
+        cells = z[key + "cells"]
+        a = np.zeros((len(cells), 13), np.float32)
+        a[:, 5:] = z[key + "explore"]
+        af = physics.ActionField.from_block(cells, a)
+        planes = _planeset(p)
+        ev = physics.resolve_exploration(planes, af, physics.PhysicsParams(explore_fraction=float(z[key + "alpha"])))
+        assert np.array_equal(planes.channels["infrastructure"][0].view(np.uint32), z[key + "post_I"].view(np.uint32))
+        assert np.array_equal(planes.genome_index, z[key + "post_gi"])
+        assert np.array_equal(planes.rotation, z[key + "post_rot"])
+        assert events_rows(ev) == [tuple(r) for r in z[key + "events"].tolist()]
+
+
+def _planeset(p: orc.Planes):
+    from paper_2406_09654_b200.substrate import create_substrate
+
+    h, w = p.shape
+    ps = create_substrate(w, h).front
+    ps.channels["energy"][0] = p.E
+    ps.channels["infrastructure"][0] = p.I
+    ps.channels["communication"][:] = p.C
+    ps.genome_index[:] = p.gi
+    ps.rotation[:] = p.rot
+    return ps
+
+
+# -- reference known-answer cases (test_physics.py values), through the shims -------
+
+
+def _ps(w=4, h=4):
+    from paper_2406_09654_b200.substrate import create_substrate
+
+    return create_substrate(w, h).front
+
+
+def _acts(cells, **kw):
+    n = len(cells)
+    a = np.zeros((n, 13), np.float32)
+    if "invest" in kw:
+        a[:, 0] = kw["invest"]
+    if "liquidate" in kw:
+        a[:, 1] = kw["liquidate"]
+    if "comm" in kw:
+        a[:, 2:5] = kw["comm"]
+    if "explore" in kw:
+        a[:, 5:13] = kw["explore"]
+    return physics.ActionField.from_block(np.asarray(cells, np.int64), a)
+
+
+def test_energy_cycle_values():
+    p = _ps()
+    physics.energy_cycle(p, 25, physics.PhysicsParams(cycle_amplitude=0.4, cycle_period=100))
+    assert np.allclose(p.plane("energy"), 0.4, atol=1e-7)
+    p = _ps()
+    p.plane("energy")[:] = 2.0
+    physics.energy_cycle(p, 75, physics.PhysicsParams(cycle_amplitude=0.4, cycle_period=100, drain_fraction=0.5))
+    assert np.allclose(p.plane("energy"), 1.6, rtol=1e-6)
+    p = _ps()
+    src = np.zeros((4, 4), np.float32)
+    src[0, 0] = 2.0
+    physics.energy_cycle(p, 1, physics.PhysicsParams(cycle_amplitude=0.5, cycle_period=4, energy_source_map=src))
+    assert p.plane("energy")[0, 0] == pytest.approx(1.0, rel=1e-6)
+    assert p.plane("energy")[1, 1] == 0.0
+    p = _ps()
+    p.plane("energy")[:] = 3.0
+    physics.energy_cycle(p, 7, physics.PhysicsParams(cycle_amplitude=0.0))
+    assert (p.plane("energy") == 3.0).all()
+
+
+def test_invest_liquidate_values():
+    p = _ps()
+    p.genome_index[0, 0] = 0
+    p.plane("energy")[0, 0] = 1.0
+    physics.apply_invest_liquidate(p, _acts([0], invest=[0.5]),
+                                   physics.PhysicsParams(invest_rate=1.0, invest_efficiency=0.9, upkeep=0.0))
+    assert p.plane("energy")[0, 0] == pytest.approx(0.5, rel=1e-6)
+    assert p.plane("infrastructure")[0, 0] == pytest.approx(0.45, rel=1e-6)
+    p = _ps()
+    p.genome_index[0, 0] = 0
+    p.plane("energy")[0, 0] = 0.05
+    p.plane("infrastructure")[0, 0] = 10.0
+    physics.apply_invest_liquidate(p, _acts([0]), physics.PhysicsParams(upkeep=0.1, decay_on_starvation=0.1))
+    assert p.plane("energy")[0, 0] == 0.0
+    assert p.plane("infrastructure")[0, 0] == pytest.approx(9.0, rel=1e-6)
+    assert p.genome_index[0, 0] == 0
+    p = _ps()
+    p.genome_index[0, 0] = 3
+    p.plane("infrastructure")[0, 0] = 5e-4
+    physics.apply_invest_liquidate(p, _acts([0]), physics.PhysicsParams(upkeep=0.0, death_threshold=1e-3))
+    assert p.genome_index[0, 0] == -1
+    assert p.plane("infrastructure")[0, 0] == pytest.approx(5e-4)
+    p = _ps()
+    p.plane("energy")[0, 0] = 1.0
+    physics.apply_invest_liquidate(p, _acts([0], invest=[0.9]), physics.PhysicsParams())
+    assert p.plane("energy")[0, 0] == 1.0 and p.plane("infrastructure")[0, 0] == 0.0
+
+
+def test_communication_values():
+    p = _ps()
+    p.genome_index[0, 0] = 0
+    physics.write_communication(p, _acts([0], comm=[[0.2, 0.5, 0.8]]))
+    assert p.channels["communication"][:, 0, 0].tolist() == pytest.approx([0.2, 0.5, 0.8])
+    p = _ps()
+    p.channels["communication"][:, 1, 1] = 1.0
+    physics.write_communication(p, physics.ActionField.empty())
+    assert p.channels["communication"][:, 1, 1] == pytest.approx(0.9)
+    physics.write_communication(p, physics.ActionField.empty())
+    assert p.channels["communication"][0, 1, 1] == pytest.approx(0.81)
+
+
+def test_exploration_hand_examples():
+    p = _ps()
+    p.genome_index[1, 1] = 3
+    p.rotation[1, 1] = 2
+    p.plane("infrastructure")[1, 1] = 2.0
+    p.plane("infrastructure")[2, 1] = 0.3
+    ex = np.zeros((1, 8), np.float32)
+    ex[0, 0] = 0.8
+    ex[0, 5] = 0.1
+    ev = physics.resolve_exploration(p, _acts([5], explore=ex), physics.PhysicsParams(explore_fraction=0.5))
+    assert p.plane("infrastructure")[1, 1] == pytest.approx(1.2, rel=1e-6)
+    assert p.plane("infrastructure")[2, 1] == pytest.approx(1.1, rel=1e-6)
+    assert p.genome_index[2, 1] == 3 and p.rotation[2, 1] == 2
+    e = ev.aslist()[0]
+    assert (e.target, e.source, e.winner_slot, e.defender_slot, e.direction) == (9, 5, 3, -1, 2)
+    # tie on quantity: lower source index wins
+    p = _ps()
+    for (x, y), rot in (((0, 1), 0), ((2, 1), 4)):
+        p.genome_index[y, x] = x
+        p.rotation[y, x] = rot
+        p.plane("infrastructure")[y, x] = 1.0
+    ex = np.zeros((2, 8), np.float32)
+    ex[:, 0] = 0.5
+    ev = physics.resolve_exploration(p, _acts([4, 6], explore=ex), physics.PhysicsParams(explore_fraction=1.0))
+    assert len(ev) == 1 and ev.aslist()[0].source == 4 and p.genome_index[1, 1] == 0
+    # actuator tie: slot 0
+    p = _ps()
+    p.genome_index[0, 0] = 1
+    p.plane("infrastructure")[0, 0] = 1.0
+    ev = physics.resolve_exploration(p, _acts([0], explore=np.full((1, 8), 0.5, np.float32)),
+                                     physics.PhysicsParams(explore_fraction=1.0))
+    assert ev.aslist()[0].direction == 0
+
+
+# -- full steps from the reference's golden runs ---------------------------------------
+
+
+def _golden_net(name):
+    z = CS.load(name)
+    return z, (CS.step_net(z, 16) if name == "step_hidden.npz" else orc.synth_net(8, 0, seed=0))
+
+
+@pytest.mark.parametrize("name", ["step_hidden.npz", "step_direct.npz"])
+def test_full_step_reference_actions_bit_exact(name):
+    z, net = _golden_net(name)
+    params = physics.PhysicsParams(cycle_period=20)
+    for k in z["keep"].tolist():
+        key = f"s{k:03d}_"
+        pre = CS.planes(z, key, "pre")
+        dev = make_dev(pre, 8, net)
+        dev.set_actions(z[key + "cells"], z[key + "acts"])
+        dev.step_raw(physics.step_scalars(k, params), k, flags=_lib.F_INJECT_ACTIONS)
+        assert download(dev).equal(CS.planes(z, key, "post")), k
+        assert dev.read_stats()[0] == int(z[key + "adoptions"])
+        assert np.array_equal(dev.read_census()[0], z[key + "counts"])
+        dev.close()
+
+
+@pytest.mark.parametrize("name", ["step_hidden.npz", "step_direct.npz"])
+def test_device_actions_vs_reference(name):
+    z, net = _golden_net(name)
+    params = physics.PhysicsParams(cycle_period=20)
+    for k in z["keep"].tolist():
+        key = f"s{k:03d}_"
+        pre = CS.planes(z, key, "pre")
+        dev = make_dev(pre, 8, net)
+        dev.step_raw(physics.step_scalars(k, params), k, flags=_lib.F_EXPORT_ACTIONS)
+        cells, acts = dev.get_actions()
+        assert np.array_equal(cells, z[key + "cells"])
+        assert rel_err(acts, z[key + "acts"]) <= TOL
+        # and against the oracle's float64-dot restatement
+        oa = orc.act(pre, net)
+        assert rel_err(acts, oa.a) <= 2e-6
+        dev.close()
+
+
+def test_config1_free_running_100_steps():
+    """BASELINE config 1 from the reference's initial state, 100 steps
+    device-resident: genome/rotation planes bit-identical to the reference
+    at every recorded step, continuous channels within tolerance."""
+    z, net = _golden_net("step_direct.npz")
+    pre = CS.planes(z, "s000_", "pre")
+    dev = make_dev(pre, 8, net)
+    params = physics.PhysicsParams(cycle_period=20)
+    keep = set(z["keep"].tolist())
+    for t in range(100):
+        dev.step_raw(physics.step_scalars(t, params), t)
+        if t in keep:
+            got = download(dev)
+            ref = CS.planes(z, f"s{t:03d}_", "post")
+            assert np.array_equal(got.gi, ref.gi), t
+            assert np.array_equal(got.rot, ref.rot), t
+            assert close(got.E, ref.E) and close(got.I, ref.I) and close(got.C, ref.C), t
+    dev.close()
+
+
+# -- device vs oracle on assorted shapes --------------------------------------------------
+
+
+def _step_vs_oracle(p0, net, phys, steps, capacity=None, t0=0):
+    cap = capacity or net.capacity
+    dev = make_dev(p0, cap, net)
+    params = oracle_phys_to_params(phys)
+    p = p0
+    for t in range(t0, t0 + steps):
+        dev.step_raw(physics.step_scalars(t, params), t, flags=_lib.F_EXPORT_ACTIONS | _lib.F_RECORD_EVENTS)
+        cells, acts = dev.get_actions()
+        ref = orc.step(p, t, net, phys, acts=orc.Actions(cells, acts))
+        got = download(dev)
+        assert got.equal(ref.planes), f"t={t}"
+        assert events_rows(dev.read_events()) == [tuple(map(float, r)) for r in ref.events.rows()], f"t={t}"
+        assert np.array_equal(dev.read_census()[0], ref.counts[:cap]), f"t={t}"
+        oa = orc.act(p, net)
+        assert np.array_equal(oa.cells, cells)
+        assert rel_err(acts, oa.a) <= 2e-6, f"t={t}"
+        p = got
+    dev.close()
+    return p
+
+
+@pytest.mark.parametrize("h,w,g", [(1, 1, 1), (2, 3, 2), (3, 3, 3), (5, 7, 4), (31, 33, 5), (40, 65, 9),
+                                   (129, 100, 64), (64, 64, 8)])
+def test_shapes_vs_oracle(h, w, g):
+    p0 = orc.synth_planes(h, w, g, seed=h * 1000 + w)
+    # leave some cells empty
+    rng = np.random.default_rng(h + w)
+    p0.gi[rng.random((h, w)) < 0.2] = -1
+    net = orc.synth_net(g, 0, seed=7)
+    _step_vs_oracle(p0, net, orc.Phys(cycle_period=4), steps=6)
+
+
+def test_hidden_nets_vs_oracle():
+    for hidden, g in ((16, 6), (1, 3), (13, 4), (128, 5)):
+        p0 = orc.synth_planes(48, 40, g, seed=hidden)
+        net = orc.synth_net(g, hidden, seed=hidden)
+        _step_vs_oracle(p0, net, orc.Phys(cycle_period=20), steps=3)
+
+
+def test_sparse_infrastructure_contention():
+    p0 = orc.synth_planes(96, 96, 16, seed=5, sparse_infra=True)
+    net = orc.synth_net(16, 0, seed=5)
+    _step_vs_oracle(p0, net, orc.Phys(cycle_period=20, explore_fraction=0.9), steps=5)
+
+
+def test_empty_world():
+    p0 = orc.synth_planes(40, 40, 4, seed=1)
+    p0.gi[:] = -1
+    net = orc.synth_net(4, 0, seed=1)
+    _step_vs_oracle(p0, net, orc.Phys(cycle_period=20), steps=3)
+
+
+def test_config2_full_size_tier_a():
+    """BASELINE config 2 at full size (1024x1024, 64 genomes): two steps,
+    device actions injected into the oracle physics -> bit-exact state,
+    events and census; device actions within tolerance of the oracle's."""
+    p0 = orc.synth_planes(1024, 1024, 64, seed=0)
+    net = orc.synth_net(64, 0, seed=0)
+    _step_vs_oracle(p0, net, orc.Phys(cycle_period=20), steps=2)
+
+
+# -- engine-level properties ------------------------------------------------------------
+
+
+def test_engine_step_equals_run_and_is_deterministic():
+    a = engine.baseline_state("c1")
+    b = engine.baseline_state("c1")
+    c = engine.baseline_state("c1")
+    for _ in range(7):
+        engine.step(a)
+    engine.run(b, 7)
+    engine.run(c, 3)
+    engine.run(c, 4)
+    assert engine.digest(a) == engine.digest(b) == engine.digest(c)
+    assert a.t == b.t == c.t == 7
+    assert a.pool.live_count() == b.pool.live_count()
+
+
+def test_engine_matches_oracle_c1():
+    st = engine.baseline_state("c1")
+    p = orc.synth_planes(64, 64, 8, seed=0)
+    net = orc.synth_net(8, 0, seed=0)
+    for t in range(5):
+        af = engine.build_action_field(st)
+        res = orc.step(p, t, net, orc.Phys(cycle_period=20), acts=orc.Actions(af.cells, af.block()))
+        engine.step(st)
+        f = st.substrate.front
+        assert np.array_equal(f.genome_index, res.planes.gi)
+        assert np.array_equal(f.channels["energy"][0], res.planes.E)
+        assert st.last_adoptions == len(res.events)
+        p = res.planes
+    assert engine.digest(st) == orc.digest(p)
+
+
+def _rot_plane(p):
+    n = p.shape[-1]
+    ys, xs = np.mgrid[0:n, 0:n]
+    out = np.empty_like(p)
+    out[..., xs, (n - ys) % n] = p[..., ys, xs]
+    return out
+
+
+def test_rotation_equivariance_bit_exact():
+    """Quarter-turning the world commutes with stepping it (the reference's
+    acceptance property, test_acceptance.py:225-264), bit-exactly."""
+    p0 = orc.synth_planes(64, 64, 8, seed=3)
+    net = orc.synth_net(8, 0, seed=3)
+    pr = orc.Planes(_rot_plane(p0.E), _rot_plane(p0.I), _rot_plane(p0.C), _rot_plane(p0.gi),
+                    _rot_plane(((p0.rot + 2) % 8).astype(np.uint8)))
+    params = physics.PhysicsParams(cycle_period=20)
+    da, db = make_dev(p0, 8, net), make_dev(pr, 8, net)
+    for t in range(30):
+        da.step_raw(physics.step_scalars(t, params), t)
+        db.step_raw(physics.step_scalars(t, params), t)
+    a, b = download(da), download(db)
+    assert np.array_equal(_rot_plane(a.gi), b.gi)
+    assert np.array_equal(_rot_plane(((a.rot + 2) % 8).astype(np.uint8)), b.rot)
+    for x, y in ((a.E, b.E), (a.I, b.I), (a.C, b.C)):
+        assert np.array_equal(_rot_plane(x), y)
+
+
+def test_conservation_lossless():
+    p0 = orc.synth_planes(128, 128, 16, seed=9)
+    p0.C[:] = 0.5
+    net = orc.synth_net(16, 0, seed=9)
+    params = physics.PhysicsParams(cycle_amplitude=0.0, drain_fraction=0.0, invest_efficiency=1.0,
+                                   liquidate_efficiency=1.0, upkeep=0.0, decay_on_starvation=0.0)
+    dev = make_dev(p0, 16, net)
+    tot0 = float(p0.E.astype(np.float64).sum() + p0.I.astype(np.float64).sum())
+    for t in range(100):
+        dev.step_raw(physics.step_scalars(t, params), t)
+    p = download(dev)
+    tot = float(p.E.astype(np.float64).sum() + p.I.astype(np.float64).sum())
+    assert abs(tot - tot0) / tot0 < 1e-4
+    assert (p.E >= 0).all() and (p.I >= 0).all()
+    assert ((p.gi >= -1) & (p.gi < 16)).all() and (p.rot < 8).all()
+
+
+def test_census_deaths_tracked_on_device():
+    p0 = orc.synth_planes(32, 32, 6, seed=2)
+    p0.gi[p0.gi == 5] = 4  # slot 5 live in the pool but owns no cell -> dies at t+1
+    net = orc.synth_net(6, 0, seed=2)
+    dev = make_dev(p0, 6, net)
+    dev.step_raw(physics.step_scalars(0, physics.PhysicsParams()), 0)
+    counts, state, death, peak = dev.read_census()
+    assert counts[5] == 0 and state[5] == 2 and death[5] == 1
+    assert dev.read_stats()[1] >= 1
+    assert (peak[:5] == counts[:5]).all()

@@ -1,0 +1,86 @@
+"""Host-side logic of the package, checked against the oracle on CPU."""
+
+import math
+
+import numpy as np
+import pytest
+
+from oracle import oracle as orc
+from paper_2406_09654_b200 import physics, synth
+from paper_2406_09654_b200.hypernet import DenseParams, DirectParams, pack_params
+from paper_2406_09654_b200.pool import SlotPool
+
+
+@pytest.mark.parametrize("period", [2, 3, 4, 20, 100, 7919])
+@pytest.mark.parametrize("amp", [0.0, 0.1, 1.0])
+def test_step_scalars_match_reference_rho(period, amp):
+    phys = physics.PhysicsParams(cycle_amplitude=amp, cycle_period=period, drain_fraction=0.37)
+    for t in list(range(0, 3 * period + 2)) + [10**6 + 17]:
+        s = physics.step_scalars(t, phys)
+        mode, r32, d32 = orc.rho_terms(t, orc.Phys(cycle_amplitude=amp, cycle_period=period, drain_fraction=0.37))
+        assert s.rho_mode == mode
+        assert np.float32(s.rho_f32) == r32
+        assert np.float32(s.drain_f32) == d32
+
+
+def test_step_scalars_casts():
+    s = physics.step_scalars(0, physics.PhysicsParams(explore_fraction=0.1, death_threshold=1e-3))
+    assert np.float32(s.explore_fraction) == np.float32(0.1)
+    assert np.float32(s.death_threshold) == np.float32(1e-3)
+
+
+def test_synth_matches_oracle_generator():
+    for sparse in (False, True):
+        E, I, C, gi, rot = synth.synth_arrays(33, 17, 7, seed=4, sparse_infra=sparse)
+        p = orc.synth_planes(33, 17, 7, seed=4, sparse_infra=sparse)
+        for a, b in zip((E, I, C, gi, rot), p.arrays()):
+            assert a.dtype == b.dtype and np.array_equal(a, b)
+    direct = synth.synth_params(5, 0, seed=2)
+    net = orc.synth_net(5, 0, seed=2)
+    for i, d in enumerate(direct):
+        assert np.array_equal(d.w, net.w2[i]) and np.array_equal(d.b, net.b2[i])
+    hid = synth.synth_params(3, 128, seed=2)
+    net = orc.synth_net(3, 128, seed=2)
+    for i, d in enumerate(hid):
+        assert np.array_equal(d.w1, net.w1[i]) and np.array_equal(d.w2, net.w2[i])
+
+
+def test_rotation_tables_match_reference_kats():
+    # test_physics.py:46-76 known answers
+    assert physics.KERNEL_OFFSETS.tolist() == [[1, 0], [1, 1], [0, 1], [-1, 1], [-1, 0], [-1, -1], [0, -1], [1, -1]]
+    assert physics.rotation_permutation(0).tolist() == [0, 1, 7, 2, 6, 3, 5, 4]
+    assert physics.rotation_permutation(2).tolist() == [2, 3, 1, 4, 0, 5, 7, 6]
+    assert np.array_equal(physics.PERM_TABLE, orc.PERM)
+    with pytest.raises(ValueError):
+        physics.rotation_permutation(8)
+
+
+def test_pack_params_layout():
+    d = [DirectParams(np.arange(13 * 45, dtype=np.float32).reshape(13, 45), np.arange(13, dtype=np.float32)), None]
+    w1, b1, w2, b2 = pack_params(d, 0)
+    assert w1 is None and w2.shape == (2, 13, 45) and not w2[1].any()
+    h = [DenseParams(np.ones((4, 45), np.float32), np.ones(4, np.float32), np.ones((13, 4), np.float32),
+                     np.ones(13, np.float32))]
+    w1, b1, w2, b2 = pack_params(h, 4)
+    assert w1.shape == (1, 4, 45) and w2.shape == (1, 13, 4)
+    with pytest.raises(ValueError):
+        pack_params(h, 5)
+
+
+def test_slot_pool_census_contract():
+    pool = SlotPool(4)
+    for s in range(3):
+        pool.install(s, None)
+    dead = pool.update_census(np.array([2, 0, 1, 0]), step=10)
+    assert dead == [1]
+    assert pool.record_for_slot(0).peak_population == 2
+    assert pool.records[pool.lineage(1)].death_step == 10
+    # deferred device census folds to the same records
+    p2 = SlotPool(4)
+    for s in range(3):
+        p2.install(s, None)
+    dead2 = p2.apply_device_census(np.array([1, 2, 1, 0], np.int8), np.array([-1, 10, -1, -1]),
+                                   np.array([2, 0, 1, 0], np.int32))
+    assert dead2 == [1]
+    assert p2.records[p2.lineage(1)].death_step == 10
+    assert p2.record_for_slot(0).peak_population == 2
