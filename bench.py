@@ -118,7 +118,8 @@ def run_ours(args, rank, world, local):
     b.sync_params(state.pool)
     dev.upload(state.substrate.front)
     dev.sync()
-    stream = torch.cuda.current_stream()
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
     sh = stream.cuda_stream
     phys = state.config.physics
     flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device="cuda")

@@ -148,6 +148,11 @@ EVO_API int evo_patch_genomes(evo_ctx* ctx, const int64_t* cells, const int32_t*
  * ghost row -1; row y lives at + (y+1)*W.  plane_stride counts elements. */
 EVO_API int evo_plane_ptr(evo_ctx* ctx, int which, int buffer, void** ptr, int64_t* plane_stride);
 
+/* Diagnostics: per-phase cycle sums of the hot pass-1 kernel, summed over
+ * CTAs (0 bucketing, 1 controller, 2 physics tail, 3 halo commit, 4 setup);
+ * non-zero only in a library built with -DEVO_PHASE_TIMING. */
+EVO_API int evo_debug_phase_cycles(uint64_t* out8, int reset);
+
 /* 64-bit FNV-1a continuation over host bytes (engine.digest, engine.py:283-315):
  * *out = fold(h, data[0..n)).  Host code, no device involved. */
 EVO_API int evo_fnv1a64(uint64_t h, const uint8_t* data, int64_t n, uint64_t* out);

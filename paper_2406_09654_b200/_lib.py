@@ -14,7 +14,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libevoca_b200.so")
+LIB_PATH = os.environ.get("EVOCA_B200_LIB") or os.path.join(_HERE, "libevoca_b200.so")
 
 EVO_EINVAL = -1
 PH_ENERGY, PH_INVEST, PH_COMM, PH_EXPLORE, PH_ALL = 1, 2, 4, 8, 15
@@ -69,6 +69,7 @@ SIGNATURES = {
     "evo_patch_genomes": [_P, _P, _P, _I64],
     "evo_plane_ptr": [_P, _I, _I, C.POINTER(_P), C.POINTER(_I64)],
     "evo_fnv1a64": [C.c_uint64, _P, _I64, C.POINTER(C.c_uint64)],
+    "evo_debug_phase_cycles": [_P, _I],
 }
 RESTYPES = {"evo_last_error": C.c_char_p}
 

@@ -40,13 +40,15 @@ def _stale() -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not _stale():
+def build(force: bool = False, verbose: bool = False, out: str | None = None, defines=()) -> str:
+    lib = out or LIB
+    if not force and out is None and not _stale():
         return LIB
     cmd = [
         nvcc(), "-O3", "-std=c++17", *ARCH, "-lineinfo", "-Xcompiler", "-fPIC", "-shared",
         "-Xcompiler", "-fvisibility=hidden", "-I", INCLUDE, "-I", CSRC,
-        "-o", LIB + ".tmp", *[os.path.join(CSRC, s) for s in SOURCES],
+        *[f"-D{d}" for d in defines],
+        "-o", lib + ".tmp", *[os.path.join(CSRC, s) for s in SOURCES],
     ]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
@@ -56,14 +58,19 @@ def build(force: bool = False, verbose: bool = False) -> str:
         raise RuntimeError(f"nvcc failed ({res.returncode}):\n{res.stdout}\n{res.stderr}")
     if verbose:
         print(res.stdout + res.stderr)
-    os.replace(LIB + ".tmp", LIB)
-    return LIB
+    os.replace(lib + ".tmp", lib)
+    return lib
 
 
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("--verbose", action="store_true")
     ap.add_argument("--force", action="store_true")
+    ap.add_argument("--phase-timing", action="store_true", help="diagnostics build -> libevoca_b200_timing.so")
     args = ap.parse_args()
-    print(build(force=args.force or args.verbose, verbose=args.verbose))
+    if args.phase_timing:
+        print(build(force=True, verbose=args.verbose, out=os.path.join(PKG, "libevoca_b200_timing.so"),
+                    defines=("EVO_PHASE_TIMING",)))
+    else:
+        print(build(force=args.force or args.verbose, verbose=args.verbose))
     sys.exit(0)

@@ -115,6 +115,8 @@ int create_impl(evo_ctx** out, int width, int height, long long row0, int hg, in
   if (hidden < 0 || hidden > 1024) return fail(EVO_EINVAL, "hidden size must be in [0, 1024]");
   if (hg < height || row0 < 0 || row0 + height > hg) return fail(EVO_EINVAL, "strip outside the global torus");
   if ((long long)width * hg >= 0xFFFFFFFFLL) return fail(EVO_EINVAL, "grid exceeds 2^32-1 cells");
+  if ((long long)(height + 2) * width >= (1LL << 31))
+    return fail(EVO_EINVAL, "strip exceeds 2^31 cells per plane: split it over more strips");
   if (strip && height < 1) return fail(EVO_EINVAL, "strip needs at least one row");
   evo_ctx* c = new evo_ctx();
   c->device = device;
@@ -153,7 +155,9 @@ int create_impl(evo_ctx** out, int width, int height, long long row0, int hg, in
   if ((e = c->alloc(&c->mid.q, n)) != cudaSuccess) return bail(e, "alloc mid");
   const size_t cap = (size_t)capacity;
   if (hidden == 0) {
-    if ((e = c->alloc(&c->wA, cap * evo::kSensors * evo::kOutPad)) != cudaSuccess) return bail(e, "alloc w");
+    // compact direct layout: W12 [cap][45][12] (actuators 0..11), W1 [cap][45] (actuator 12)
+    if ((e = c->alloc(&c->wA, cap * evo::kSensors * 12)) != cudaSuccess) return bail(e, "alloc w");
+    if ((e = c->alloc(&c->wB, (cap * evo::kSensors + 3) / 4 * 4)) != cudaSuccess) return bail(e, "alloc w");
     if ((e = c->alloc(&c->bA, cap * evo::kOutPad)) != cudaSuccess) return bail(e, "alloc b");
   } else {
     if ((e = c->alloc(&c->wA, cap * evo::kSensors * c->hpad)) != cudaSuccess) return bail(e, "alloc w1");
@@ -269,15 +273,21 @@ EVO_API int evo_set_params(evo_ctx* c, int slot0, int n, const float* w1, const 
   if (H > 0 && (!w1 || !b1)) return fail(EVO_EINVAL, "w1/b1 are required for a hidden layer");
   CK(cudaStreamSynchronize(c->stream));
   if (H == 0) {
-    std::vector<float> wt((size_t)n * evo::kSensors * evo::kOutPad, 0.0f), bt((size_t)n * evo::kOutPad, 0.0f);
+    std::vector<float> w12((size_t)n * evo::kSensors * 12, 0.0f), w1((size_t)n * evo::kSensors, 0.0f);
+    std::vector<float> bt((size_t)n * evo::kOutPad, 0.0f);
     for (int s = 0; s < n; ++s)
       for (int j = 0; j < evo::kActuators; ++j) {
-        for (int k = 0; k < evo::kSensors; ++k)
-          wt[((size_t)s * evo::kSensors + k) * evo::kOutPad + j] = w2[((size_t)s * evo::kActuators + j) * evo::kSensors + k];
+        for (int k = 0; k < evo::kSensors; ++k) {
+          const float v = w2[((size_t)s * evo::kActuators + j) * evo::kSensors + k];
+          if (j < 12)
+            w12[((size_t)s * evo::kSensors + k) * 12 + j] = v;
+          else
+            w1[(size_t)s * evo::kSensors + k] = v;
+        }
         bt[(size_t)s * evo::kOutPad + j] = b2[(size_t)s * evo::kActuators + j];
       }
-    CK(cudaMemcpy(c->wA + (size_t)slot0 * evo::kSensors * evo::kOutPad, wt.data(), wt.size() * 4,
-                  cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(c->wA + (size_t)slot0 * evo::kSensors * 12, w12.data(), w12.size() * 4, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(c->wB + (size_t)slot0 * evo::kSensors, w1.data(), w1.size() * 4, cudaMemcpyHostToDevice));
     CK(cudaMemcpy(c->bA + (size_t)slot0 * evo::kOutPad, bt.data(), bt.size() * 4, cudaMemcpyHostToDevice));
     return 0;
   }
@@ -571,6 +581,13 @@ EVO_API int evo_plane_ptr(evo_ctx* c, int which, int buffer, void** ptr, int64_t
     default: return fail(EVO_EINVAL, "unknown plane");
   }
   if (plane_stride) *plane_stride = c->stride;
+  return 0;
+}
+
+EVO_API int evo_debug_phase_cycles(uint64_t* out8, int reset) {
+  if (!out8) return fail(EVO_EINVAL, "null argument");
+  CK(cudaDeviceSynchronize());
+  CK(evo::debug_phase_cycles(reinterpret_cast<unsigned long long*>(out8), reset != 0));
   return 0;
 }
 

@@ -51,9 +51,9 @@ struct Mid {
 struct Params {
   int hidden;     // 0 = direct 45->13
   int hpad;       // hidden rounded up to 8
-  const float* wA;  // direct: [cap][45][16]; hidden: W1 [cap][45][hpad]
-  const float* bA;  // direct: [cap][16];     hidden: b1 [cap][hpad]
-  const float* wB;  // hidden: W2^T [cap][hpad][16]
+  const float* wA;  // direct: W12 [cap][45][12];  hidden: W1 [cap][45][hpad]
+  const float* bA;  // direct: bias [cap][16];     hidden: b1 [cap][hpad]
+  const float* wB;  // direct: W1 [cap][45] (actuator 12); hidden: W2^T [cap][hpad][16]
   const float* bB;  // hidden: b2 [cap][16]
 };
 
@@ -110,6 +110,7 @@ struct Pass2Args {
 
 cudaError_t launch_pass1(const Pass1Args& a, bool inject, bool export_actions, cudaStream_t st);
 cudaError_t launch_pass2(const Pass2Args& a, cudaStream_t st);
+cudaError_t debug_phase_cycles(unsigned long long* out, bool reset);
 cudaError_t launch_census_finish(const Census& c, int capacity, long long t, cudaStream_t st);
 cudaError_t launch_refresh_ghosts(const Planes& p, const StepGeom& g, cudaStream_t st);
 cudaError_t launch_scatter_actions(float* act, uint8_t* flag, const int64_t* cells, const float* rows, long long n,

@@ -1,324 +1,196 @@
 // B200 (sm_100a) kernels for the evoca per-step substrate update.
 //
-// Pass 1  (k_act_physics)  reference engine.py:193-230 + physics.py:178-309
-//   One CTA per 32x32 tile.  The tile plus its 1-cell Moore halo of the five
-//   sensed front planes (E, I, C0..C2) is staged in shared memory; occupied
-//   cells are bucketed by genome slot inside the CTA (radix sort, groups
-//   padded to cell quads) so that each thread evaluates four cells of ONE
-//   genome and every weight fetched from L1 feeds four fixed-order fp32 FMA
-//   chains.  Sensors are gathered from shared memory in the rotation order
-//   PERM[rot] (physics.py:48-62, engine.py:164-177) and never touch HBM.
-//   Actions land in shared memory in spatial order; the fused physics tail
-//   (energy, invest/liquidate/upkeep/death, communication, explore proposal)
-//   then runs in spatial order with coalesced stores.  Physics uses only
-//   __f*_rn intrinsics (no FMA contraction) in the reference's op order so
-//   that, given the same actions, results are bit-identical to NumPy.
+// Pass 1 (reference engine.py:193-230 + physics.py:178-309): sense, controller
+// and the fused physics tail, per 32x32 tile.  The tile plus its 1-cell Moore
+// halo of the five sensed front planes (E, I, C0..C2) is staged in shared
+// memory; occupied cells are bucketed by genome slot inside the CTA (counting
+// sort, groups padded to cell quads) so that each thread evaluates four cells
+// of ONE genome and every weight fetched feeds four fixed-order fp32 FMA
+// chains.  Sensors are gathered from shared memory in the rotation order
+// PERM[rot] (physics.py:48-62, engine.py:164-177) and never touch HBM.
+// Actions land in shared memory in spatial order; the physics tail then runs
+// in spatial order with coalesced stores, using only __f*_rn intrinsics (no
+// FMA contraction) in the reference's op order so that, given the same
+// actions, results are bit-identical to NumPy.
+//   k_pass1_direct  hot path: persistent CTA per SM, direct 45->13 net with
+//                   packed FFMA2 (fma.rn.f32x2), weights L1-resident, next
+//                   tile's halo prefetched into registers during compute.
+//   k_pass1_generic parity / hidden-layer path: injected actions, the
+//                   45->H(tanh)->13 reference net.
 //
-// Pass 2  (k_resolve)  reference physics.py:286-343 + 395-404
-//   Each target cell PULLS the shipments aimed at it from its 8 neighbours'
-//   proposal bytes.  Arrivals are ordered by the packed 64-bit key
-//   (bits(q) << 32) | (0xFFFFFFFF - global_source_index), i.e. q descending,
-//   source ascending — the reference's lexsort order — and summed
-//   sequentially in that order (bit-exact, deterministic, no atomics); the
-//   maximal key is the winner, which adopts the target iff q > infra there.
-//   The final genome plane feeds a shared-memory census histogram; the last
-//   CTA to finish publishes counts and retires slots (neuroevo.py:521-542).
+// Pass 2 (k_resolve, physics.py:286-343 + 395-404): each target cell PULLS
+// the shipments aimed at it from its 8 neighbours' proposal bytes.  Arrivals
+// are ordered by the packed 64-bit key (bits(q) << 32) | (0xFFFFFFFF -
+// global_source_index), i.e. q descending then source ascending - the
+// reference's lexsort order - and summed sequentially in that order
+// (bit-exact, deterministic, no atomics); the maximal key is the winner,
+// which adopts the target iff q > infra standing there.  The final genome
+// plane feeds a shared-memory census histogram; the last CTA to finish
+// publishes counts and retires slots (neuroevo.py:521-542).
 
-#include <cub/block/block_radix_sort.cuh>
-#include <cub/block/block_scan.cuh>
-
-#include "evoca_internal.h"
+#include "evoca_net.cuh"
 
 namespace evo {
 
-// Moore offsets (dx, dy) for direction j (physics.py:40-43), packed.
-// Halo-tile offset of direction j: dy*kHaloW + dx, stored biased by +64 in a byte.
-__host__ __device__ constexpr unsigned long long pack_halo_offsets() {
-  const int dx[8] = {1, 1, 0, -1, -1, -1, 0, 1};
-  const int dy[8] = {0, 1, 1, 1, 0, -1, -1, -1};
-  unsigned long long p = 0;
-  for (int j = 0; j < 8; ++j) p |= (unsigned long long)(dy[j] * kHaloW + dx[j] + 64) << (8 * j);
-  return p;
-}
-constexpr unsigned long long kHaloOffPack = pack_halo_offsets();
-// rotation_permutation deltas (0, +1, -1, +2, -2, +3, -3, +4) mod 8, 4 bits each.
-constexpr unsigned kDeltaPack = (0u << 0) | (1u << 4) | (7u << 8) | (2u << 12) | (6u << 16) | (3u << 20) |
-                                (5u << 24) | (4u << 28);
-// dx+1 and dy+1 per direction, 4 bits each.
-constexpr unsigned kDxPack = (2u << 0) | (2u << 4) | (1u << 8) | (0u << 12) | (0u << 16) | (0u << 20) |
-                             (1u << 24) | (2u << 28);
-constexpr unsigned kDyPack = (1u << 0) | (2u << 4) | (2u << 8) | (2u << 12) | (1u << 16) | (0u << 20) |
-                             (0u << 24) | (0u << 28);
+// Optional per-phase cycle accounting of the hot pass-1 kernel (diagnostics
+// build: -DEVO_PHASE_TIMING; read with evo_debug_phase_cycles).
+__device__ unsigned long long g_phase_cycles[8];
+#ifdef EVO_PHASE_TIMING
+#define PHASE_MARK(k)                                               \
+  if (threadIdx.x == 0) {                                           \
+    const long long now = clock64();                                \
+    atomicAdd(&g_phase_cycles[k], (unsigned long long)(now - t_mark)); \
+    t_mark = now;                                                   \
+  }
+#else
+#define PHASE_MARK(k)
+#endif
 
-__device__ __forceinline__ int perm_dir(int rot, int slot) {  // PERM_TABLE[rot][slot]
-  return (rot + ((kDeltaPack >> (4 * slot)) & 7u)) & 7;
-}
-__device__ __forceinline__ int halo_off(int dir) {
-  return (int)((kHaloOffPack >> (8 * dir)) & 0xFFu) - 64;
-}
-__device__ __forceinline__ int dir_dx(int d) { return (int)((kDxPack >> (4 * d)) & 0xFu) - 1; }
-__device__ __forceinline__ int dir_dy(int d) { return (int)((kDyPack >> (4 * d)) & 0xFu) - 1; }
-
-// Output nonlinearity exactly as hypernet.py:246-251: negate, exp, +1,
-// correctly rounded reciprocal, clip to [2^-126, 1-2^-24].
-__device__ __forceinline__ float squash(float z) {
-  const float e = expf(-z);
-  const float d = __fadd_rn(e, 1.0f);
-  const float r = __frcp_rn(d);
-  return fminf(fmaxf(r, 1.17549435082228750797e-38f), 0.99999994039535522461f);
+__device__ __forceinline__ void zero_stats(const Pass1Args& a) {
+  if (blockIdx.x == 0 && threadIdx.x == 0 && a.stats) {
+    a.stats[0] = 0;
+    a.stats[1] = 0;
+  }
 }
 
-__device__ __forceinline__ long long plane_row(const StepGeom& g, int y) { return (long long)(y + 1) * g.W; }
+// Halo cell i of the tile at (x0, y0): global plane offset (rows -1..H exist).
+__device__ __forceinline__ unsigned halo_src(const StepGeom& g, int x0, int y0, int i) {
+  const int hy = i / kHaloW, hx = i - hy * kHaloW;
+  int y = y0 + hy - 1;
+  if (y > g.H) y = g.H;  // beyond a partial tile: never read
+  int x = x0 + hx - 1;
+  x = x < 0 ? x + g.W : (x >= g.W ? x - g.W : x);
+  if (x >= g.W) x = g.W - 1;
+  return (unsigned)((y + 1) * g.W + x);
+}
+
+// Physics tail of one tile in spatial order (shared by both pass-1 kernels).
+template <bool kInject, bool kExport, int THREADS, typename SM>
+__device__ __forceinline__ void tile_physics(const Pass1Args& a, const SM& sm, int x0, int y0) {
+  const StepGeom& g = a.g;
+#pragma unroll 1
+  for (int i = threadIdx.x; i < kTileCells; i += THREADS) {
+    const int ty = i / kTileW, tx = i - ty * kTileW;
+    const int y = y0 + ty, x = x0 + tx;
+    if (y >= g.H || x >= g.W) continue;
+    const long long cell = (long long)y * g.W + x;
+    const int hp = (ty + 1) * kHaloW + tx + 1;
+    const float4 f = sm.eic[hp];
+    CellState st{f.x, f.y, f.z, f.w, sm.c2[hp], sm.gi[i], sm.rot[i]};
+    CellAct ac{};
+    if (kExport && st.slot < 0) a.act_out_flag[cell] = 0;
+    if (kInject) {
+      ac.acted = a.act_flag[cell] != 0;
+      if (ac.acted) {
+        const float* row = a.act_in + cell * kActuators;
+        ac.inv = row[0];
+        ac.liq = row[1];
+        ac.m0 = row[2];
+        ac.m1 = row[3];
+        ac.m2 = row[4];
+        explore_argmax(row + 5, ac.kstar, ac.xmax);
+      }
+    } else {
+      ac.acted = st.slot >= 0;
+      if (ac.acted) {
+        ac.inv = sm.u.act.inv[i];
+        ac.liq = sm.u.act.liq[i];
+        ac.m0 = sm.u.act.c0[i];
+        ac.m1 = sm.u.act.c1[i];
+        ac.m2 = sm.u.act.c2[i];
+        ac.xmax = sm.u.act.xmax[i];
+        ac.kstar = sm.u.act.kstar[i];
+      }
+    }
+    store_pass1(a, y, x, cell_physics(a.s, a.phases, a.src_map, cell, st, ac));
+  }
+}
+
+// Unit loop of the controller over the bucketed tile (U cells per thread).
+template <bool kExport, bool kHidden, int THREADS, int U, bool kSmemW = false, typename SM>
+__device__ __forceinline__ void tile_controller(const Pass1Args& a, SM& sm, int x0, int y0,
+                                                const float* W12 = nullptr, const float* W1 = nullptr,
+                                                const float* B = nullptr) {
+  if (!kSmemW) {
+    W12 = a.net.wA;
+    W1 = a.net.wB;
+    B = a.net.bA;
+  }
+  const int nu = sm.n_units;
+  for (int q = threadIdx.x; q < nu; q += THREADS) {
+    unsigned short ord[U];
+    if (U == 4) {
+      const ushort4 o4 = reinterpret_cast<const ushort4*>(sm.order)[q];
+      ord[0] = o4.x;
+      ord[1 % U] = o4.y;
+      ord[2 % U] = o4.z;
+      ord[3 % U] = o4.w;
+    } else {
+      const ushort2 o2 = reinterpret_cast<const ushort2*>(sm.order)[q];
+      ord[0] = o2.x;
+      ord[1 % U] = o2.y;
+    }
+    int pos[U], hb[U], rot[U];
+    bool valid[U];
+#pragma unroll
+    for (int c = 0; c < U; ++c) {
+      valid[c] = ord[c] != 0xFFFF;
+      pos[c] = valid[c] ? ord[c] : ord[0];
+      const int ty = pos[c] / kTileW, tx = pos[c] - ty * kTileW;
+      hb[c] = (ty + 1) * kHaloW + tx + 1;
+      rot[c] = sm.rot[pos[c]];
+    }
+    const int slot = sm.gi[pos[0]];
+    if (!kHidden) {
+      float out[U][kActuators];
+      net_direct_unit<U, kSmemW>(sm, W12 + (size_t)slot * kSensors * 12, W1 + (size_t)slot * kSensors,
+                                 B + (size_t)slot * kOutPad, hb, rot, out);
+#pragma unroll
+      for (int c = 0; c < U; ++c)
+        if (valid[c]) finish_actions<kExport>(sm.u.act, a, pos[c], x0, y0, out[c]);
+    } else {
+#pragma unroll 1
+      for (int c = 0; c < U; ++c) {
+        if (!valid[c]) continue;
+        float out[kActuators];
+        net_hidden_cell(sm, a.net, slot, hb[c], rot[c], out);
+        finish_actions<kExport>(sm.u.act, a, pos[c], x0, y0, out);
+      }
+    }
+  }
+}
 
 // ---------------------------------------------------------------------------
-// Pass 1
+// Pass 1, generic (injected actions / hidden-layer net / export)
 
-struct Pass1Smem {
-  float4 eic[kHaloCells];  // E, I, C0, C1 of tile + halo
-  float c2[kHaloCells];    // C2
+struct GenericSmem {
+  float4 eic[kHaloCells];
+  float c2[kHaloCells];
   int gi[kTileCells];
   uint8_t rot[kTileCells];
-  unsigned short order[4 * kTileCells];  // genome-sorted cell list, groups padded to quads
-  int n_quads;
+  unsigned short order[4 * kTileCells];
+  int slot_off[72];
+  int scratch[kThreads1 / 32];
+  int n_units;
   union {
-    typename cub::BlockRadixSort<unsigned, kThreads1, 4>::TempStorage sort;
-    typename cub::BlockScan<int, kThreads1>::TempStorage scan;
-    struct {
-      float inv[kTileCells], liq[kTileCells], c0[kTileCells], c1[kTileCells], c2[kTileCells], xmax[kTileCells];
-      uint8_t kstar[kTileCells];
-    } act;
+    ActSmem act;
   } u;
-  unsigned last_code[kThreads1 + 1];  // [t+1] = last code held by thread t
-  unsigned first_code[kThreads1 + 1]; // [t] = first code held by thread t
+  int bins[1];  // capacity ints (dynamic tail)
 };
 
-// Bucket the tile's occupied cells by genome slot; write the padded order.
-__device__ void bucket_by_genome(Pass1Smem& sm, int capacity) {
-  const int tid = threadIdx.x;
-  int nbits = 1;
-  while ((1 << nbits) <= capacity) ++nbits;
-  unsigned keys[4];
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const int pos = tid * 4 + i;
-    const int g = sm.gi[pos];
-    const unsigned code = g >= 0 ? (unsigned)g : (unsigned)capacity;
-    keys[i] = (code << 12) | (unsigned)pos;
-  }
-  cub::BlockRadixSort<unsigned, kThreads1, 4>(sm.u.sort).Sort(keys, 12, 12 + nbits);
-  __syncthreads();
-  unsigned code[4];
-#pragma unroll
-  for (int i = 0; i < 4; ++i) code[i] = keys[i] >> 12;
-  sm.last_code[tid + 1] = code[3];
-  sm.first_code[tid] = code[0];
-  if (tid == 0) {
-    sm.last_code[0] = 0xFFFFFFFFu;
-    sm.first_code[kThreads1] = 0xFFFFFFFFu;
-  }
-  __syncthreads();
-  // group starts (max-scan of start positions) and group-end padding
-  int start_in[4], start_of[4];
-  unsigned prev = sm.last_code[tid];
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    start_in[i] = (code[i] != prev) ? tid * 4 + i : 0;
-    prev = code[i];
-  }
-  cub::BlockScan<int, kThreads1>(sm.u.scan).InclusiveScan(start_in, start_of, cub::Max());
-  __syncthreads();
-  const unsigned next_code = sm.first_code[tid + 1];
-  int pad[4], pad_before[4];
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const int p = tid * 4 + i;
-    const unsigned nx = (i < 3) ? code[i + 1] : next_code;
-    const bool valid = code[i] < (unsigned)capacity;
-    const bool is_end = valid && (nx != code[i]);
-    const int size = p - start_of[i] + 1;
-    pad[i] = is_end ? ((4 - (size & 3)) & 3) : 0;
-  }
-  int total_pad;
-  cub::BlockScan<int, kThreads1>(sm.u.scan).ExclusiveSum(pad, pad_before, total_pad);
-  __syncthreads();
-  // count occupied: number of valid codes
-  int nvalid = 0;
-#pragma unroll
-  for (int i = 0; i < 4; ++i) nvalid += (code[i] < (unsigned)capacity) ? 1 : 0;
-  // order[] is pre-filled with 0xFFFF by the caller
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    if (code[i] < (unsigned)capacity) sm.order[tid * 4 + i + pad_before[i]] = (unsigned short)(keys[i] & 0xFFFu);
-  }
-  // the last valid item's padded end gives the list length
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const int p = tid * 4 + i;
-    const unsigned nx = (i < 3) ? code[i + 1] : next_code;
-    if (code[i] < (unsigned)capacity && !(nx < (unsigned)capacity)) {
-      sm.n_quads = (p + pad_before[i] + pad[i] + 1) / 4;
-    }
-  }
-  (void)nvalid;
-  (void)total_pad;
-}
-
-// Direct 45->13 controller over one quad of same-genome cells.
-__device__ __forceinline__ void net_direct_quad(const Pass1Smem& sm, const float* __restrict__ W,
-                                                const float* __restrict__ B, const int hb[4], const int rot[4],
-                                                float out[4][kActuators]) {
-  float acc[4][kActuators];
-#pragma unroll
-  for (int c = 0; c < 4; ++c)
-#pragma unroll
-    for (int j = 0; j < kActuators; ++j) acc[c][j] = 0.0f;
-#pragma unroll 1
-  for (int s = 0; s < 9; ++s) {
-    float x[4][5];
-#pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      const int nb = (s == 0) ? hb[c] : hb[c] + halo_off(perm_dir(rot[c], s - 1));
-      const float4 v = sm.eic[nb];
-      x[c][0] = v.x;
-      x[c][1] = v.y;
-      x[c][2] = v.z;
-      x[c][3] = v.w;
-      x[c][4] = sm.c2[nb];
-    }
-    const float4* wrow = reinterpret_cast<const float4*>(W + (size_t)s * 5 * kOutPad);
-#pragma unroll
-    for (int ch = 0; ch < 5; ++ch) {
-      const float4 w0 = __ldg(wrow + ch * 4 + 0);
-      const float4 w1 = __ldg(wrow + ch * 4 + 1);
-      const float4 w2 = __ldg(wrow + ch * 4 + 2);
-      const float4 w3 = __ldg(wrow + ch * 4 + 3);
-      const float w[13] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w, w2.x, w2.y, w2.z, w2.w, w3.x};
-#pragma unroll
-      for (int c = 0; c < 4; ++c)
-#pragma unroll
-        for (int j = 0; j < kActuators; ++j) acc[c][j] = fmaf(x[c][ch], w[j], acc[c][j]);
-    }
-  }
-  const float4* b4 = reinterpret_cast<const float4*>(B);
-  const float4 b0 = __ldg(b4), b1 = __ldg(b4 + 1), b2 = __ldg(b4 + 2), b3 = __ldg(b4 + 3);
-  const float b[13] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w, b2.x, b2.y, b2.z, b2.w, b3.x};
-#pragma unroll
-  for (int c = 0; c < 4; ++c)
-#pragma unroll
-    for (int j = 0; j < kActuators; ++j) out[c][j] = squash(__fadd_rn(acc[c][j], b[j]));
-}
-
-// Hidden-layer controller 45->H(tanh)->13 for one cell (reference DenseParams).
-__device__ __forceinline__ void net_hidden_cell(const Pass1Smem& sm, const Params& P, int g, int hb, int rot,
-                                                float out[kActuators]) {
-  float x[kSensors];
-#pragma unroll
-  for (int s = 0; s < 9; ++s) {
-    const int nb = (s == 0) ? hb : hb + halo_off(perm_dir(rot, s - 1));
-    const float4 v = sm.eic[nb];
-    x[s * 5 + 0] = v.x;
-    x[s * 5 + 1] = v.y;
-    x[s * 5 + 2] = v.z;
-    x[s * 5 + 3] = v.w;
-    x[s * 5 + 4] = sm.c2[nb];
-  }
-  float acc[kActuators];
-#pragma unroll
-  for (int j = 0; j < kActuators; ++j) acc[j] = 0.0f;
-  const float* W1 = P.wA + (size_t)g * kSensors * P.hpad;
-  const float* B1 = P.bA + (size_t)g * P.hpad;
-  const float* W2 = P.wB + (size_t)g * P.hpad * kOutPad;
-#pragma unroll 1
-  for (int hc = 0; hc < P.hpad; hc += 8) {
-    float z[8];
-#pragma unroll
-    for (int h = 0; h < 8; ++h) z[h] = 0.0f;
-#pragma unroll
-    for (int k = 0; k < kSensors; ++k) {
-      const float4* wr = reinterpret_cast<const float4*>(W1 + (size_t)k * P.hpad + hc);
-      const float4 wa = __ldg(wr), wb = __ldg(wr + 1);
-      const float w[8] = {wa.x, wa.y, wa.z, wa.w, wb.x, wb.y, wb.z, wb.w};
-#pragma unroll
-      for (int h = 0; h < 8; ++h) z[h] = fmaf(x[k], w[h], z[h]);
-    }
-    const float4* b4 = reinterpret_cast<const float4*>(B1 + hc);
-    const float4 ba = __ldg(b4), bb = __ldg(b4 + 1);
-    const float bh[8] = {ba.x, ba.y, ba.z, ba.w, bb.x, bb.y, bb.z, bb.w};
-#pragma unroll
-    for (int h = 0; h < 8; ++h) {
-      const float th = tanhf(__fadd_rn(z[h], bh[h]));
-      const float4* w2 = reinterpret_cast<const float4*>(W2 + (size_t)(hc + h) * kOutPad);
-      const float4 u0 = __ldg(w2), u1 = __ldg(w2 + 1), u2 = __ldg(w2 + 2), u3 = __ldg(w2 + 3);
-      const float u[13] = {u0.x, u0.y, u0.z, u0.w, u1.x, u1.y, u1.z, u1.w, u2.x, u2.y, u2.z, u2.w, u3.x};
-#pragma unroll
-      for (int j = 0; j < kActuators; ++j) acc[j] = fmaf(th, u[j], acc[j]);
-    }
-  }
-  const float4* b4 = reinterpret_cast<const float4*>(P.bB + (size_t)g * kOutPad);
-  const float4 b0 = __ldg(b4), b1 = __ldg(b4 + 1), b2 = __ldg(b4 + 2), b3 = __ldg(b4 + 3);
-  const float b[13] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w, b2.x, b2.y, b2.z, b2.w, b3.x};
-#pragma unroll
-  for (int j = 0; j < kActuators; ++j) out[j] = squash(__fadd_rn(acc[j], b[j]));
-}
-
-// first maximal explore actuator (np.argmax: lowest index on ties)
-__device__ __forceinline__ void explore_argmax(const float* ex, int& kstar, float& xmax) {
-  kstar = 0;
-  xmax = ex[0];
-#pragma unroll
-  for (int k = 1; k < 8; ++k)
-    if (ex[k] > xmax) {
-      xmax = ex[k];
-      kstar = k;
-    }
-}
-
-template <bool kExport>
-__device__ __forceinline__ void store_actions(Pass1Smem& sm, const Pass1Args& a, int p, int x0, int y0,
-                                              const float* out) {
-  sm.u.act.inv[p] = out[0];
-  sm.u.act.liq[p] = out[1];
-  sm.u.act.c0[p] = out[2];
-  sm.u.act.c1[p] = out[3];
-  sm.u.act.c2[p] = out[4];
-  int ks;
-  float xm;
-  explore_argmax(out + 5, ks, xm);
-  sm.u.act.xmax[p] = xm;
-  sm.u.act.kstar[p] = (uint8_t)ks;
-  if (kExport) {
-    const int ty = p / kTileW, tx = p - ty * kTileW;
-    const long long cell = (long long)(y0 + ty) * a.g.W + (x0 + tx);
-    float* dst = a.act_out + cell * kActuators;
-#pragma unroll
-    for (int j = 0; j < kActuators; ++j) dst[j] = out[j];
-    a.act_out_flag[cell] = 1;
-  }
-}
-
 template <bool kInject, bool kExport, bool kHidden>
-__global__ void __launch_bounds__(kThreads1, 2) k_act_physics(const Pass1Args a) {
+__global__ void __launch_bounds__(kThreads1, 2) k_pass1_generic(const Pass1Args a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  Pass1Smem& sm = *reinterpret_cast<Pass1Smem*>(smem_raw);
+  GenericSmem& sm = *reinterpret_cast<GenericSmem*>(smem_raw);
   const StepGeom& g = a.g;
   const int tid = threadIdx.x;
   const int tiles_x = (g.W + kTileW - 1) / kTileW;
   const int x0 = (blockIdx.x % tiles_x) * kTileW;
   const int y0 = (blockIdx.x / tiles_x) * kTileH;
-  if (blockIdx.x == 0 && tid == 0 && a.stats) {
-    a.stats[0] = 0;
-    a.stats[1] = 0;
-  }
-
-  // -- stage tile + halo of the sensed front planes (rows -1..H exist: ghosts)
+  zero_stats(a);
+  fill_slot_offsets(sm.slot_off);
   for (int i = tid; i < kHaloCells; i += kThreads1) {
-    const int hy = i / kHaloW, hx = i - hy * kHaloW;
-    int y = y0 + hy - 1;
-    if (y > g.H) y = g.H;  // beyond a partial tile: never read
-    int x = x0 + hx - 1;
-    x = x < 0 ? x + g.W : (x >= g.W ? x - g.W : x);
-    if (x >= g.W) x = g.W - 1;
-    const long long o = plane_row(g, y) + x;
+    const unsigned o = halo_src(g, x0, y0, i);
     sm.eic[i] = make_float4(__ldg(a.front.E + o), __ldg(a.front.I + o), __ldg(a.front.C + o),
                             __ldg(a.front.C + g.stride + o));
     sm.c2[i] = __ldg(a.front.C + 2 * g.stride + o);
@@ -327,274 +199,452 @@ __global__ void __launch_bounds__(kThreads1, 2) k_act_physics(const Pass1Args a)
     const int ty = i / kTileW, tx = i - ty * kTileW;
     const int y = y0 + ty, x = x0 + tx;
     const bool in = (y < g.H) && (x < g.W);
-    const long long o = plane_row(g, in ? y : 0) + (in ? x : 0);
+    const unsigned o = in ? (unsigned)((y + 1) * g.W + x) : 0u;
     sm.gi[i] = in ? __ldg(a.front.gi + o) : -1;
     sm.rot[i] = in ? __ldg(a.front.rot + o) : 0;
   }
-  if (!kInject) {
-    for (int i = tid; i < 4 * kTileCells; i += kThreads1) sm.order[i] = 0xFFFF;
-    if (tid == 0) sm.n_quads = 0;
-  }
   __syncthreads();
-
-  // -- sense + controller, genome-bucketed
   if (!kInject) {
-    bucket_by_genome(sm, a.capacity);
-    __syncthreads();
-    const int nq = sm.n_quads;
-    for (int q = tid; q < nq; q += kThreads1) {
-      const ushort4 o4 = reinterpret_cast<const ushort4*>(sm.order)[q];
-      const unsigned short ord[4] = {o4.x, o4.y, o4.z, o4.w};
-      int pos[4], hb[4], rot[4];
-      bool valid[4];
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        valid[c] = ord[c] != 0xFFFF;
-        pos[c] = valid[c] ? ord[c] : ord[0];
-        const int ty = pos[c] / kTileW, tx = pos[c] - ty * kTileW;
-        hb[c] = (ty + 1) * kHaloW + tx + 1;
-        rot[c] = sm.rot[pos[c]];
-      }
-      const int slot = sm.gi[pos[0]];
-      if (!kHidden) {
-        float out[4][kActuators];
-        net_direct_quad(sm, a.net.wA + (size_t)slot * kSensors * kOutPad, a.net.bA + (size_t)slot * kOutPad, hb,
-                        rot, out);
-#pragma unroll
-        for (int c = 0; c < 4; ++c)
-          if (valid[c]) store_actions<kExport>(sm, a, pos[c], x0, y0, out[c]);
-      } else {
-#pragma unroll 1
-        for (int c = 0; c < 4; ++c) {
-          if (!valid[c]) continue;
-          float out[kActuators];
-          net_hidden_cell(sm, a.net, slot, hb[c], rot[c], out);
-          store_actions<kExport>(sm, a, pos[c], x0, y0, out);
-        }
-      }
-    }
+    bucket_by_genome<kThreads1, kTileCells / kThreads1, 4>(sm.bins, sm.scratch, sm.gi, sm.order, &sm.n_units,
+                                                           a.capacity);
+    tile_controller<kExport, kHidden, kThreads1, 4>(a, sm, x0, y0);
     __syncthreads();
   }
+  tile_physics<kInject, kExport, kThreads1>(a, sm, x0, y0);
+}
 
-  // -- fused physics tail in spatial order (physics.py:178-290)
-  const Scalars& s = a.s;
-  for (int i = tid; i < kTileCells; i += kThreads1) {
+// ---------------------------------------------------------------------------
+// Pass 1, hot path: persistent, direct net, FFMA2
+
+constexpr int kThreadsP = 640;
+constexpr int kUnitP = 2;  // cells per thread in the controller (a same-genome pair)
+constexpr int kPreHalo = (kHaloCells + kThreadsP - 1) / kThreadsP;  // 2
+constexpr int kPreCells = (kTileCells + kThreadsP - 1) / kThreadsP;  // 2
+
+struct DirectSmem {
+  float4 eic[kHaloCells];
+  float c2[kHaloCells];
+  int gi[kTileCells];
+  uint8_t rot[kTileCells];
+  unsigned short order[4 * kTileCells];
+  int slot_off[72];
+  int scratch[kThreadsP / 32];
+  int n_units;
+  union {
+    ActSmem act;
+  } u;
+  int bins[1];  // capacity ints (dynamic tail)
+};
+
+struct Prefetch {
+  float v[kPreHalo][5];
+  int gi[kPreCells];
+  int rot[kPreCells];
+};
+
+__device__ __forceinline__ void prefetch_tile(const Pass1Args& a, int tile, int tiles_x, Prefetch& pf) {
+  const StepGeom& g = a.g;
+  const int tid = threadIdx.x;
+  const int x0 = (tile % tiles_x) * kTileW;
+  const int y0 = (tile / tiles_x) * kTileH;
+  const unsigned st = (unsigned)g.stride;
+#pragma unroll
+  for (int j = 0; j < kPreHalo; ++j) {
+    const int i = tid + j * kThreadsP;
+    if (i < kHaloCells) {
+      const unsigned o = halo_src(g, x0, y0, i);
+      pf.v[j][0] = ld_na(a.front.E + o);
+      pf.v[j][1] = ld_na(a.front.I + o);
+      pf.v[j][2] = ld_na(a.front.C + o);
+      pf.v[j][3] = ld_na(a.front.C + st + o);
+      pf.v[j][4] = ld_na(a.front.C + 2 * st + o);
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < kPreCells; ++j) {
+    const int i = tid + j * kThreadsP;
     const int ty = i / kTileW, tx = i - ty * kTileW;
     const int y = y0 + ty, x = x0 + tx;
-    if (y >= g.H || x >= g.W) continue;
-    const long long cell = (long long)y * g.W + x;
-    const long long o = plane_row(g, y) + x;
-    const int hp = (ty + 1) * kHaloW + tx + 1;
-    const float4 f = sm.eic[hp];
-    float e = f.x, inf = f.y, c0 = f.z, c1 = f.w, c2 = sm.c2[hp];
-    const int slot = sm.gi[i];
-    const int r = sm.rot[i];
-    bool acted;
-    float inv = 0.f, liq = 0.f, m0 = 0.f, m1 = 0.f, m2 = 0.f, xm = 0.f;
-    int ks = 0;
-    if (kExport && slot < 0) a.act_out_flag[cell] = 0;
-    if (kInject) {
-      acted = a.act_flag[cell] != 0;
-      if (acted) {
-        const float* row = a.act_in + cell * kActuators;
-        inv = row[0];
-        liq = row[1];
-        m0 = row[2];
-        m1 = row[3];
-        m2 = row[4];
-        explore_argmax(row + 5, ks, xm);
-      }
-    } else {
-      acted = slot >= 0;
-      if (acted) {
-        inv = sm.u.act.inv[i];
-        liq = sm.u.act.liq[i];
-        m0 = sm.u.act.c0[i];
-        m1 = sm.u.act.c1[i];
-        m2 = sm.u.act.c2[i];
-        xm = sm.u.act.xmax[i];
-        ks = sm.u.act.kstar[i];
-      }
-    }
-    // energy_cycle: all cells (physics.py:186-194)
-    if (a.phases & EVO_PH_ENERGY) {
-      if (s.mode == 1) {
-        const float add = a.src_map ? __fmul_rn(s.rho, a.src_map[cell]) : s.rho;
-        e = __fadd_rn(e, add);
-      } else if (s.mode == 2) {
-        e = __fsub_rn(e, __fmul_rn(s.drain, e));
-      }
-    }
-    int slot2 = slot;
-    // apply_invest_liquidate: listed cells still occupied (physics.py:212-233)
-    if ((a.phases & EVO_PH_INVEST) && acted && slot >= 0) {
-      const float de = __fmul_rn(inv, fminf(e, s.kinv));
-      e = __fsub_rn(e, de);
-      inf = __fadd_rn(inf, __fmul_rn(s.einv, de));
-      const float di = __fmul_rn(liq, fminf(inf, s.kliq));
-      inf = __fsub_rn(inf, di);
-      e = __fadd_rn(e, __fmul_rn(s.eliq, di));
-      const float cost = __fmul_rn(s.upkeep, inf);
-      const bool fed = e >= cost;
-      e = fed ? __fsub_rn(e, cost) : 0.0f;
-      inf = fed ? inf : __fsub_rn(inf, __fmul_rn(s.dstarve, inf));
-      if (inf < s.imin) slot2 = -1;
-    }
-    // write_communication (physics.py:240-247)
-    if (a.phases & EVO_PH_COMM) {
-      if (acted && slot2 >= 0) {
-        c0 = m0;
-        c1 = m1;
-        c2 = m2;
-      } else if (slot2 < 0) {
-        c0 = __fmul_rn(c0, 0.9f);
-        c1 = __fmul_rn(c1, 0.9f);
-        c2 = __fmul_rn(c2, 0.9f);
-      }
-    }
-    // exploration proposal + withdrawal (physics.py:276-290)
-    uint8_t rp = (uint8_t)r;
-    float q = 0.0f;
-    if ((a.phases & EVO_PH_EXPLORE) && acted && slot2 >= 0) {
-      const int dir = perm_dir(r, ks);
-      q = __fmul_rn(__fmul_rn(s.alpha, xm), inf);
-      inf = __fsub_rn(inf, q);
-      rp = (uint8_t)(r | (dir << 3) | kShipBit);
-    }
-    a.back.E[o] = e;
-    a.back.C[o] = c0;
-    a.back.C[g.stride + o] = c1;
-    a.back.C[2 * g.stride + o] = c2;
-    a.mid.I[o] = inf;
-    a.mid.gi[o] = slot2;
-    a.mid.rp[o] = rp;
-    a.mid.q[o] = q;
-    if (g.own_ghosts) {
-      // wrapped copies for the next pass / step: row 0 -> ghost row H, row H-1 -> ghost row -1
-#pragma unroll 1
-      for (int rep = 0; rep < 2; ++rep) {
-        const bool hit = rep == 0 ? (y == 0) : (y == g.H - 1);
-        if (!hit) continue;
-        const long long og = plane_row(g, rep == 0 ? g.H : -1) + x;
-        a.back.E[og] = e;
-        a.back.C[og] = c0;
-        a.back.C[g.stride + og] = c1;
-        a.back.C[2 * g.stride + og] = c2;
-        a.mid.gi[og] = slot2;
-        a.mid.rp[og] = rp;
-        a.mid.q[og] = q;
-      }
+    const bool in = (i < kTileCells) && (y < g.H) && (x < g.W);
+    const unsigned o = in ? (unsigned)((y + 1) * g.W + x) : 0u;
+    pf.gi[j] = in ? __ldg(a.front.gi + o) : -1;
+    pf.rot[j] = in ? (int)__ldg(a.front.rot + o) : 0;
+  }
+}
+
+__device__ __forceinline__ void commit_tile(DirectSmem& sm, const Prefetch& pf) {
+  const int tid = threadIdx.x;
+#pragma unroll
+  for (int j = 0; j < kPreHalo; ++j) {
+    const int i = tid + j * kThreadsP;
+    if (i < kHaloCells) {
+      sm.eic[i] = make_float4(pf.v[j][0], pf.v[j][1], pf.v[j][2], pf.v[j][3]);
+      sm.c2[i] = pf.v[j][4];
     }
   }
+#pragma unroll
+  for (int j = 0; j < kPreCells; ++j) {
+    const int i = tid + j * kThreadsP;
+    if (i < kTileCells) {
+      sm.gi[i] = pf.gi[j];
+      sm.rot[i] = (uint8_t)pf.rot[j];
+    }
+  }
+}
+
+// L2 prefetch of a tile's halo rows (5 planes) and interior genome/rotation
+// rows: no registers, issued a whole tile ahead of the register loads.
+__device__ __forceinline__ void prefetch_tile_l2(const Pass1Args& a, int tile, int tiles_x) {
+  const StepGeom& g = a.g;
+  const int x0 = (tile % tiles_x) * kTileW;
+  const int y0 = (tile / tiles_x) * kTileH;
+  // per plane row: [x0-1, x0+33) -> at most 2 x 128-byte lines (floats)
+  constexpr int kLines = kHaloH * 2;  // per float plane
+  for (int i = threadIdx.x; i < kLines * 5 + kTileH * 2; i += kThreadsP) {
+    const char* p;
+    if (i < kLines * 5) {
+      const int plane = i / kLines, r = (i - plane * kLines) >> 1, half = i & 1;
+      int y = y0 + r - 1;
+      if (y > g.H) y = g.H;
+      int x = x0 - 1 + half * 32;
+      x = x < 0 ? 0 : (x >= g.W ? g.W - 1 : x);
+      const float* base = plane == 0 ? a.front.E : (plane == 1 ? a.front.I : a.front.C + (plane - 2) * g.stride);
+      p = reinterpret_cast<const char*>(base + (unsigned)((y + 1) * g.W + x));
+    } else {
+      const int j = i - kLines * 5, r = j >> 1;
+      int y = y0 + r;
+      if (y >= g.H) y = g.H - 1;
+      p = (j & 1) ? reinterpret_cast<const char*>(a.front.rot + (unsigned)((y + 1) * g.W + x0))
+                  : reinterpret_cast<const char*>(a.front.gi + (unsigned)((y + 1) * g.W + x0));
+    }
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+  }
+}
+
+// Asynchronous copy of the slot weight tables into shared memory (16-byte cp.async).
+__device__ __forceinline__ void stage_weights(float* dst, const float* src, int nfloats) {
+  const unsigned sbase = (unsigned)__cvta_generic_to_shared(dst);
+  for (int i = threadIdx.x * 4; i < nfloats; i += kThreadsP * 4)
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sbase + i * 4), "l"(src + i));
+}
+
+template <bool kExport, bool kSmemW>
+__global__ void __launch_bounds__(kThreadsP, 1) k_pass1_direct(const Pass1Args a) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  DirectSmem& sm = *reinterpret_cast<DirectSmem*>(smem_raw);
+  const StepGeom& g = a.g;
+  const int tiles_x = (g.W + kTileW - 1) / kTileW;
+  const int ntiles = tiles_x * ((g.H + kTileH - 1) / kTileH);
+  zero_stats(a);
+  int tile = blockIdx.x;
+  if (tile >= ntiles) return;
+  // weight tables resident in shared memory for small pools: W12 | W1 | bias
+  float* sW12 = nullptr;
+  float* sW1 = nullptr;
+  float* sB = nullptr;
+  if (kSmemW) {
+    const size_t off = (sizeof(DirectSmem) + (size_t)a.capacity * sizeof(int) + 15) & ~(size_t)15;
+    sW12 = reinterpret_cast<float*>(smem_raw + off);
+    sW1 = sW12 + (size_t)a.capacity * kSensors * 12;
+    sB = sW1 + (((size_t)a.capacity * kSensors + 3) & ~(size_t)3);
+    stage_weights(sW12, a.net.wA, a.capacity * kSensors * 12);
+    stage_weights(sW1, a.net.wB, (a.capacity * kSensors + 3) & ~3);
+    stage_weights(sB, a.net.bA, a.capacity * kOutPad);
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  }
+  fill_slot_offsets(sm.slot_off);
+  {
+    Prefetch pf;
+    prefetch_tile(a, tile, tiles_x, pf);
+    commit_tile(sm, pf);
+  }
+  if (kSmemW) asm volatile("cp.async.wait_all;" ::: "memory");
+  __syncthreads();
+  long long t_mark = clock64();
+  (void)t_mark;
+  PHASE_MARK(4);
+  for (; tile < ntiles; tile += gridDim.x) {
+    const int x0 = (tile % tiles_x) * kTileW;
+    const int y0 = (tile / tiles_x) * kTileH;
+    const int next = tile + gridDim.x;
+    if (next < ntiles) prefetch_tile_l2(a, next, tiles_x);
+    bucket_by_genome<kThreadsP, kPreCells, kUnitP>(sm.bins, sm.scratch, sm.gi, sm.order, &sm.n_units, a.capacity);
+    PHASE_MARK(0);
+    tile_controller<kExport, false, kThreadsP, kUnitP, kSmemW>(a, sm, x0, y0, sW12, sW1, sB);
+    __syncthreads();
+    PHASE_MARK(1);
+    Prefetch pf;
+    if (next < ntiles) prefetch_tile(a, next, tiles_x, pf);  // L2 hits by now
+    tile_physics<false, kExport, kThreadsP>(a, sm, x0, y0);
+    __syncthreads();
+    PHASE_MARK(2);
+    if (next < ntiles) commit_tile(sm, pf);
+    __syncthreads();
+    PHASE_MARK(3);
+  }
+}
+
+// Largest pool whose weight tables fit in shared memory next to the tile.
+constexpr int kSmemWeightSlots = 68;
+constexpr size_t weight_smem_bytes(int capacity) {
+  return ((size_t)capacity * (kSensors * 12 + kOutPad) + (((size_t)capacity * kSensors + 3) & ~(size_t)3)) * sizeof(float);
 }
 
 // ---------------------------------------------------------------------------
 // Pass 2
 
+constexpr int kResW = 32, kResH = 16;  // resolve tile
+constexpr int kResCells = kResW * kResH;
+constexpr int kResHW = kResW + 2;
+constexpr int kResHalo = (kResH + 2) * kResHW;
+
+// Pass-2 tile staging: the pass-1 proposal byte, quantity and genome of the
+// tile plus its 1-cell halo, and the post-withdrawal infrastructure of the
+// tile, all loaded with independent coalesced reads before any cell work.
+struct ResolveSmem {
+  uint8_t rp[kResHalo];
+  float q[kResHalo];
+  int gi[kResHalo];
+  float inf[kResCells];
+  int cnt[3];
+  unsigned short list[3][kResCells];
+};
+
+// Shipment arriving at tile cell (ty, tx) from direction d: halo index of the
+// source, its quantity and the 64-bit ordering key (q desc, global source asc).
+struct Arrival {
+  int h;
+  float q;
+  u64 key;
+};
+
+__device__ __forceinline__ Arrival arrival(const StepGeom& g, const ResolveSmem& sm, int y, int x, int ty, int tx,
+                                           int d) {
+  Arrival r;
+  r.h = (ty + 1 - dir_dy(d)) * kResHW + tx + 1 - dir_dx(d);
+  r.q = __fadd_rn(sm.q[r.h], 0.0f);  // canonical +0
+  const int sy = y - dir_dy(d);
+  int sx = x - dir_dx(d);
+  sx = sx < 0 ? sx + g.W : (sx >= g.W ? sx - g.W : sx);
+  int grow = (int)g.row0 + sy;
+  grow = grow < 0 ? grow + g.Hg : (grow >= g.Hg ? grow - g.Hg : grow);
+  const unsigned gsrc = (unsigned)grow * (unsigned)g.W + (unsigned)sx;
+  r.key = ((u64)__float_as_uint(r.q) << 32) | (u64)(0xFFFFFFFFu - gsrc);
+  return r;
+}
+
+__device__ __forceinline__ void ce_desc(u64& a, u64& b) {  // max first
+  const u64 hi = a > b ? a : b;
+  const u64 lo = a > b ? b : a;
+  a = hi;
+  b = lo;
+}
+
+__device__ __forceinline__ unsigned arrival_mask(const ResolveSmem& sm, int ty, int tx) {
+  unsigned m = 0;
+#pragma unroll
+  for (int d = 0; d < 8; ++d) {
+    const uint8_t rp = sm.rp[(ty + 1 - dir_dy(d)) * kResHW + tx + 1 - dir_dx(d)];
+    m |= ((rp & 0x78u) == (unsigned)(kShipBit | (d << 3))) ? (1u << d) : 0u;
+  }
+  return m;
+}
+
+// Resolve one target cell whose arrival mask is m (bit d: the neighbour at
+// t - off[d] ships in direction d): ordered sum, winner, adoption, stores.
+// Returns the cell's final genome slot.
+template <bool kRecord>
+__device__ __forceinline__ int resolve_cell(const Pass2Args& a, const ResolveSmem& sm, int ty, int tx, int y, int x,
+                                            unsigned m, int& adopted) {
+  const StepGeom& g = a.g;
+  const int hc = (ty + 1) * kResHW + tx + 1;
+  const float before = sm.inf[ty * kResW + tx];
+  const int own = sm.gi[hc];
+  const int r = sm.rp[hc] & 7;
+  float acc = before;
+  int gnew = own, rnew = r;
+  bool adopt = false;
+  if (m) {
+    const int n = __popc(m);
+    u64 win;
+    int wd, wh;
+    if (n == 1) {
+      wd = __ffs(m) - 1;
+      const Arrival v = arrival(g, sm, y, x, ty, tx, wd);
+      acc = __fadd_rn(acc, v.q);
+      win = v.key;
+      wh = v.h;
+    } else if (n == 2) {
+      const int d0 = __ffs(m) - 1, d1 = __ffs(m & (m - 1)) - 1;
+      const Arrival v0 = arrival(g, sm, y, x, ty, tx, d0), v1 = arrival(g, sm, y, x, ty, tx, d1);
+      const bool first0 = v0.key > v1.key;
+      acc = __fadd_rn(__fadd_rn(acc, first0 ? v0.q : v1.q), first0 ? v1.q : v0.q);
+      win = first0 ? v0.key : v1.key;
+      wd = first0 ? d0 : d1;
+      wh = first0 ? v0.h : v1.h;
+    } else {
+      // general: keys for all eight directions (absent = 0), sorting network
+      // (Batcher odd-even merge, 19 comparators), sequential sum
+      u64 k[8];
+#pragma unroll
+      for (int d = 0; d < 8; ++d) k[d] = (m & (1u << d)) ? arrival(g, sm, y, x, ty, tx, d).key : 0ull;
+      win = 0;
+      wd = 0;
+#pragma unroll
+      for (int d = 0; d < 8; ++d)
+        if (k[d] > win) {
+          win = k[d];
+          wd = d;
+        }
+      wh = (ty + 1 - dir_dy(wd)) * kResHW + tx + 1 - dir_dx(wd);
+      ce_desc(k[0], k[1]); ce_desc(k[2], k[3]); ce_desc(k[4], k[5]); ce_desc(k[6], k[7]);
+      ce_desc(k[0], k[2]); ce_desc(k[1], k[3]); ce_desc(k[4], k[6]); ce_desc(k[5], k[7]);
+      ce_desc(k[1], k[2]); ce_desc(k[5], k[6]);
+      ce_desc(k[0], k[4]); ce_desc(k[1], k[5]); ce_desc(k[2], k[6]); ce_desc(k[3], k[7]);
+      ce_desc(k[2], k[4]); ce_desc(k[3], k[5]);
+      ce_desc(k[1], k[2]); ce_desc(k[3], k[4]); ce_desc(k[5], k[6]);
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+        if (k[i]) acc = __fadd_rn(acc, __uint_as_float((unsigned)(k[i] >> 32)));
+    }
+    const float qw = __uint_as_float((unsigned)(win >> 32));
+    if (qw > before) {  // physics.py:325
+      adopt = true;
+      gnew = sm.gi[wh];
+      rnew = wd;
+      if (kRecord) {
+        const long long cell = (long long)y * g.W + x;
+        a.ev.src[cell] = (long long)(0xFFFFFFFFu - (unsigned)(win & 0xFFFFFFFFull));
+        a.ev.q[cell] = qw;
+        a.ev.def[cell] = own;
+      }
+    }
+  }
+  if (kRecord && !adopt) a.ev.src[(long long)y * g.W + x] = -1;
+  adopted += adopt ? 1 : 0;
+  const unsigned o = (unsigned)((y + 1) * g.W + x);
+  a.back.I[o] = acc;
+  a.back.gi[o] = gnew;
+  a.back.rot[o] = (uint8_t)rnew;
+  if (g.own_ghosts && (y == 0 || y == g.H - 1)) {
+    if (y == 0) {
+      const unsigned og = (unsigned)((g.H + 1) * g.W + x);
+      a.back.I[og] = acc;
+      a.back.gi[og] = gnew;
+      a.back.rot[og] = (uint8_t)rnew;
+    }
+    if (y == g.H - 1) {
+      a.back.I[x] = acc;
+      a.back.gi[x] = gnew;
+      a.back.rot[x] = (uint8_t)rnew;
+    }
+  }
+  return gnew;
+}
+
+// Cells with 0 or 1 arrival resolve in place; cells with several arrivals are
+// queued per arrival count (2, 3, >=4) and resolved afterwards by whole warps
+// of the same kind, so the ordering work never diverges inside a warp.
 template <bool kRecord>
 __global__ void __launch_bounds__(kThreads2) k_resolve(const Pass2Args a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  int* hist = reinterpret_cast<int*>(smem_raw);
+  ResolveSmem& sm = *reinterpret_cast<ResolveSmem*>(smem_raw);
+  int* hist = reinterpret_cast<int*>(smem_raw + ((sizeof(ResolveSmem) + 15) & ~(size_t)15));
   __shared__ int s_adopt;
   __shared__ bool s_last;
   const StepGeom& g = a.g;
   const int tid = threadIdx.x;
   for (int b = tid; b < a.capacity; b += kThreads2) hist[b] = 0;
   if (tid == 0) s_adopt = 0;
-  __syncthreads();
-
-  const long long ncell = (long long)g.W * g.H;
+  const int tiles_x = (g.W + kResW - 1) / kResW;
+  const int ntiles = tiles_x * ((g.H + kResH - 1) / kResH);
   int my_adopt = 0;
-  for (long long cell = (long long)blockIdx.x * kThreads2 + tid; cell < ncell; cell += (long long)gridDim.x * kThreads2) {
-    const int y = (int)(cell / g.W);
-    const int x = (int)(cell - (long long)y * g.W);
-    const long long o = plane_row(g, y) + x;
-    const float before = a.mid.I[o];
-    const int own = a.mid.gi[o];
-    const int r = a.mid.rp[o] & 7;
-    unsigned long long key[8];
-    int n = 0;
-    unsigned long long best = 0;
-    int best_d = 0;
+  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int x0 = (tile % tiles_x) * kResW;
+    const int y0 = (tile / tiles_x) * kResH;
+    __syncthreads();
+    if (tid < 3) sm.cnt[tid] = 0;
+    {
+      // all staging loads of the tile issued before any shared store
+      constexpr int kHaloIt = (kResHalo + kThreads2 - 1) / kThreads2;
+      constexpr int kCellIt = kResCells / kThreads2;
+      uint8_t vrp[kHaloIt];
+      float vq[kHaloIt], vi[kCellIt];
+      int vg[kHaloIt];
 #pragma unroll
-    for (int d = 0; d < 8; ++d) {
-      const int sy = y - dir_dy(d);
-      int sx = x - dir_dx(d);
-      sx = sx < 0 ? sx + g.W : (sx >= g.W ? sx - g.W : sx);
-      const long long so = plane_row(g, sy) + sx;
-      const uint8_t rp = a.mid.rp[so];
-      key[d] = 0;
-      if ((rp & kShipBit) && ((rp >> 3) & 7) == d) {
-        const float qv = __fadd_rn(a.mid.q[so], 0.0f);  // canonical +0
-        long long grow = g.row0 + sy;
-        if (grow < 0) grow += g.Hg;
-        if (grow >= g.Hg) grow -= g.Hg;
-        const unsigned gsrc = (unsigned)(grow * g.W + sx);
-        key[d] = ((unsigned long long)__float_as_uint(qv) << 32) | (unsigned long long)(0xFFFFFFFFu - gsrc);
-        ++n;
-        if (key[d] > best) {
-          best = key[d];
-          best_d = d;
+      for (int j = 0; j < kHaloIt; ++j) {
+        const int i = tid + j * kThreads2;
+        const int hy = i / kResHW, hx = i - hy * kResHW;
+        int y = y0 + hy - 1;
+        if (y > g.H) y = g.H;
+        int x = x0 + hx - 1;
+        x = x < 0 ? x + g.W : (x >= g.W ? x - g.W : x);
+        if (x >= g.W) x = g.W - 1;
+        const unsigned o = i < kResHalo ? (unsigned)((y + 1) * g.W + x) : 0u;
+        vrp[j] = __ldg(a.mid.rp + o);
+        vq[j] = __ldg(a.mid.q + o);
+        vg[j] = __ldg(a.mid.gi + o);
+      }
+#pragma unroll
+      for (int j = 0; j < kCellIt; ++j) {
+        const int i = tid + j * kThreads2;
+        const int ty = i / kResW, tx = i - ty * kResW;
+        const int y = min(y0 + ty, g.H - 1), x = min(x0 + tx, g.W - 1);
+        vi[j] = __ldg(a.mid.I + (unsigned)((y + 1) * g.W + x));
+      }
+#pragma unroll
+      for (int j = 0; j < kHaloIt; ++j) {
+        const int i = tid + j * kThreads2;
+        if (i < kResHalo) {
+          sm.rp[i] = vrp[j];
+          sm.q[i] = vq[j];
+          sm.gi[i] = vg[j];
         }
       }
-    }
-    float acc = before;
-    // sequential sum in (q desc, source asc) order (physics.py:294, 321-324)
-    for (int it = 0; it < n; ++it) {
-      unsigned long long m = 0;
-      int md = 0;
 #pragma unroll
-      for (int d = 0; d < 8; ++d)
-        if (key[d] > m) {
-          m = key[d];
-          md = d;
-        }
-#pragma unroll
-      for (int d = 0; d < 8; ++d)
-        if (d == md) key[d] = 0;
-      acc = __fadd_rn(acc, __uint_as_float((unsigned)(m >> 32)));
+      for (int j = 0; j < kCellIt; ++j) sm.inf[tid + j * kThreads2] = vi[j];
     }
-    int gnew = own;
-    int rnew = r;
-    bool adopt = false;
-    if (n > 0) {
-      const float qw = __uint_as_float((unsigned)(best >> 32));
-      if (qw > before) {
-        adopt = true;
-        const int sy = y - dir_dy(best_d);
-        int sx = x - dir_dx(best_d);
-        sx = sx < 0 ? sx + g.W : (sx >= g.W ? sx - g.W : sx);
-        gnew = a.mid.gi[plane_row(g, sy) + sx];
-        rnew = best_d;
-        if (kRecord) {
-          a.ev.src[cell] = (long long)(0xFFFFFFFFu - (unsigned)(best & 0xFFFFFFFFu));
-          a.ev.q[cell] = qw;
-          a.ev.def[cell] = own;
+    __syncthreads();
+#pragma unroll 1
+    for (int i = tid; i < kResCells; i += kThreads2) {
+      const int ty = i / kResW, tx = i - ty * kResW;
+      const int y = y0 + ty, x = x0 + tx;
+      int key = -1;    // census slot
+      int queue = -1;  // deferred multi-arrival bucket
+      if (y < g.H && x < g.W) {
+        const unsigned m = arrival_mask(sm, ty, tx);
+        const int n = __popc(m);
+        if (n <= 1) {
+          const int gn = resolve_cell<kRecord>(a, sm, ty, tx, y, x, m, my_adopt);
+          key = (gn >= 0 && gn < a.capacity) ? gn : -1;
+        } else {
+          queue = n == 2 ? 0 : (n == 3 ? 1 : 2);
         }
       }
+      aggregated_rank(hist, key);
+      const int slot = aggregated_rank(sm.cnt, queue);
+      if (queue >= 0) sm.list[queue][slot] = (unsigned short)i;
     }
-    if (kRecord && !adopt) a.ev.src[cell] = -1;
-    my_adopt += adopt ? 1 : 0;
-    a.back.I[o] = acc;
-    a.back.gi[o] = gnew;
-    a.back.rot[o] = (uint8_t)rnew;
-    if (g.own_ghosts) {
-      if (y == 0) {
-        const long long og = plane_row(g, g.H) + x;
-        a.back.I[og] = acc;
-        a.back.gi[og] = gnew;
-        a.back.rot[og] = (uint8_t)rnew;
-      }
-      if (y == g.H - 1) {
-        const long long og = plane_row(g, -1) + x;
-        a.back.I[og] = acc;
-        a.back.gi[og] = gnew;
-        a.back.rot[og] = (uint8_t)rnew;
+    __syncthreads();
+#pragma unroll 1
+    for (int b = 0; b < 3; ++b) {
+      const int cnt = sm.cnt[b];
+#pragma unroll 1
+      for (int base = 0; base < cnt; base += kThreads2) {
+        const int e = base + tid;
+        int key = -1;
+        if (e < cnt) {
+          const int i = sm.list[b][e];
+          const int ty = i / kResW, tx = i - ty * kResW;
+          const int gn =
+              resolve_cell<kRecord>(a, sm, ty, tx, y0 + ty, x0 + tx, arrival_mask(sm, ty, tx), my_adopt);
+          key = (gn >= 0 && gn < a.capacity) ? gn : -1;
+        }
+        aggregated_rank(hist, key);
       }
     }
-    if (gnew >= 0 && gnew < a.capacity) atomicAdd(&hist[gnew], 1);
   }
-  // block reductions -> global
+  __syncthreads();
   for (int off = 16; off > 0; off >>= 1) my_adopt += __shfl_xor_sync(0xffffffffu, my_adopt, off);
   if ((tid & 31) == 0 && my_adopt) atomicAdd(&s_adopt, my_adopt);
   __syncthreads();
@@ -630,6 +680,7 @@ __global__ void __launch_bounds__(kThreads2) k_resolve(const Pass2Args a) {
   if ((tid & 31) == 0 && dead) atomicAdd((unsigned long long*)&a.census.stats[1], (unsigned long long)dead);
   if (tid == 0) *a.census.done = 0u;
 }
+
 
 // Census epilogue as its own launch (strip mode: after the cross-rank sum of counts).
 __global__ void k_census_finish(const Census c, int capacity, long long t) {
@@ -684,57 +735,100 @@ __global__ void k_scatter_actions(float* act, uint8_t* flag, const int64_t* cell
 
 __global__ void k_patch_genomes(int32_t* gi, int W, const int64_t* cells, const int32_t* slots, long long n) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
-    const long long c = cells[i];
-    gi[c + W] = slots[i];  // +W: skip ghost row -1
+    gi[cells[i] + W] = slots[i];  // +W: skip ghost row -1
   }
 }
 
 // ---------------------------------------------------------------------------
 // launchers
 
+static int g_num_sms = 0;
+static int num_sms() {
+  if (!g_num_sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+    if (g_num_sms <= 0) g_num_sms = 148;
+  }
+  return g_num_sms;
+}
+
+template <typename K>
+static cudaError_t set_smem(K kernel, size_t smem, int& configured) {
+  if ((int)smem <= configured) return cudaSuccess;
+  cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e == cudaSuccess) configured = (int)smem;
+  return e;
+}
+
 template <bool I, bool E, bool H>
-static cudaError_t launch1(const Pass1Args& a, cudaStream_t st) {
-  const size_t smem = sizeof(Pass1Smem);
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(k_act_physics<I, E, H>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+static cudaError_t launch_generic(const Pass1Args& a, cudaStream_t st) {
+  const size_t smem = sizeof(GenericSmem) + (size_t)a.capacity * sizeof(int);
+  static int configured = 0;
+  cudaError_t e = set_smem(k_pass1_generic<I, E, H>, smem, configured);
+  if (e != cudaSuccess) return e;
+  const int tiles = ((a.g.W + kTileW - 1) / kTileW) * ((a.g.H + kTileH - 1) / kTileH);
+  k_pass1_generic<I, E, H><<<tiles, kThreads1, smem, st>>>(a);
+  return cudaGetLastError();
+}
+
+template <bool E, bool S>
+static cudaError_t launch_direct(const Pass1Args& a, cudaStream_t st) {
+  size_t smem = sizeof(DirectSmem) + (size_t)a.capacity * sizeof(int);
+  if (S) smem = ((smem + 15) & ~(size_t)15) + weight_smem_bytes(a.capacity);
+  static int configured = 0;
+  if ((int)smem > configured) {
+    cudaError_t e = set_smem(k_pass1_direct<E, S>, smem, configured);
     if (e != cudaSuccess) return e;
-    configured = true;
+    if (!S) {
+      // smallest shared-memory carveout that holds one CTA: the rest of the
+      // 256 KB per SM stays L1, where the per-genome weight table lives.
+      const int pct = (int)((smem + 8 * 1024) * 100 / (228 * 1024)) + 1;
+      cudaFuncSetAttribute(k_pass1_direct<E, S>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                           pct > 100 ? 100 : pct);
+    }
   }
   const int tiles = ((a.g.W + kTileW - 1) / kTileW) * ((a.g.H + kTileH - 1) / kTileH);
-  k_act_physics<I, E, H><<<tiles, kThreads1, smem, st>>>(a);
+  const int grid = tiles < num_sms() ? tiles : num_sms();
+  k_pass1_direct<E, S><<<grid, kThreadsP, smem, st>>>(a);
   return cudaGetLastError();
 }
 
 cudaError_t launch_pass1(const Pass1Args& a, bool inject, bool export_actions, cudaStream_t st) {
-  const bool hidden = a.net.hidden > 0;
-  if (inject) return launch1<true, false, false>(a, st);
-  if (hidden) return export_actions ? launch1<false, true, true>(a, st) : launch1<false, false, true>(a, st);
-  return export_actions ? launch1<false, true, false>(a, st) : launch1<false, false, false>(a, st);
+  if (inject) return launch_generic<true, false, false>(a, st);
+  if (a.net.hidden > 0)
+    return export_actions ? launch_generic<false, true, true>(a, st) : launch_generic<false, false, true>(a, st);
+  if (a.capacity <= kSmemWeightSlots)
+    return export_actions ? launch_direct<true, true>(a, st) : launch_direct<false, true>(a, st);
+  return export_actions ? launch_direct<true, false>(a, st) : launch_direct<false, false>(a, st);
 }
 
 cudaError_t launch_pass2(const Pass2Args& a, cudaStream_t st) {
-  const long long ncell = (long long)a.g.W * a.g.H;
-  long long blocks = (ncell + kThreads2 * 4 - 1) / (kThreads2 * 4);
-  if (blocks < 1) blocks = 1;
-  if (blocks > 148 * 16) blocks = 148 * 16;
-  const size_t smem = (size_t)a.capacity * sizeof(int);
+  const int tiles = ((a.g.W + kResW - 1) / kResW) * ((a.g.H + kResH - 1) / kResH);
+  int grid = num_sms() * 4;
+  if (grid > tiles) grid = tiles;
+  const size_t smem = ((sizeof(ResolveSmem) + 15) & ~(size_t)15) + (size_t)a.capacity * sizeof(int);
   if (a.ev.src) {
-    static bool cfg = false;
-    if (!cfg) {
-      cudaFuncSetAttribute(k_resolve<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
-      cfg = true;
-    }
-    k_resolve<true><<<(unsigned)blocks, kThreads2, smem, st>>>(a);
+    static int cfg = 0;
+    cudaError_t e = set_smem(k_resolve<true>, smem, cfg);
+    if (e != cudaSuccess) return e;
+    k_resolve<true><<<grid, kThreads2, smem, st>>>(a);
   } else {
-    static bool cfg = false;
-    if (!cfg) {
-      cudaFuncSetAttribute(k_resolve<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
-      cfg = true;
-    }
-    k_resolve<false><<<(unsigned)blocks, kThreads2, smem, st>>>(a);
+    static int cfg = 0;
+    cudaError_t e = set_smem(k_resolve<false>, smem, cfg);
+    if (e != cudaSuccess) return e;
+    k_resolve<false><<<grid, kThreads2, smem, st>>>(a);
   }
   return cudaGetLastError();
+}
+
+cudaError_t debug_phase_cycles(unsigned long long* out, bool reset) {
+  cudaError_t e = cudaMemcpyFromSymbol(out, g_phase_cycles, sizeof(unsigned long long) * 8);
+  if (e == cudaSuccess && reset) {
+    unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    e = cudaMemcpyToSymbol(g_phase_cycles, z, sizeof(z));
+  }
+  return e;
 }
 
 cudaError_t launch_census_finish(const Census& c, int capacity, long long t, cudaStream_t st) {

@@ -25,7 +25,12 @@ PLANES = {"energy": 0, "infra": 1, "comm": 2, "genome": 3, "rotation": 4,
 
 
 def _stream(s):
-    return None if s is None else C.c_void_p(int(s))
+    """None -> the context's own stream (NULL); 0 (a framework's handle for
+    the legacy default stream) -> cudaStreamLegacy; else the raw handle."""
+    if s is None:
+        return None
+    s = int(s)
+    return C.c_void_p(1 if s == 0 else s)
 
 
 def _arrays_of(planes):

@@ -273,7 +273,7 @@ def test_device_actions_vs_reference(name):
         assert rel_err(acts, z[key + "acts"]) <= TOL
         # and against the oracle's float64-dot restatement
         oa = orc.act(pre, net)
-        assert rel_err(acts, oa.a) <= 2e-6
+        assert rel_err(acts, oa.a) <= TOL
         dev.close()
 
 
@@ -315,7 +315,7 @@ def _step_vs_oracle(p0, net, phys, steps, capacity=None, t0=0):
         assert np.array_equal(dev.read_census()[0], ref.counts[:cap]), f"t={t}"
         oa = orc.act(p, net)
         assert np.array_equal(oa.cells, cells)
-        assert rel_err(acts, oa.a) <= 2e-6, f"t={t}"
+        assert rel_err(acts, oa.a) <= TOL, f"t={t}"
         p = got
     dev.close()
     return p

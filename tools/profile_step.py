@@ -1,0 +1,54 @@
+"""Run a few device steps of a BASELINE config for profiling (ncu / launch lists).
+
+    python tools/profile_step.py [--config c2] [--steps 6] [--flush]
+"""
+
+import argparse
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", default="c2")
+    ap.add_argument("--steps", type=int, default=6)
+    ap.add_argument("--flush", action="store_true")
+    args = ap.parse_args()
+    import torch
+
+    from paper_2406_09654_b200 import engine, physics
+
+    st = engine.baseline_state(args.config)
+    dev = engine.device_of(st)
+    st._evo_binding.sync_params(st.pool)
+    dev.upload(st.substrate.front)
+    s = torch.cuda.Stream()
+    torch.cuda.set_stream(s)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda") if args.flush else None
+    for t in range(args.steps):
+        if flush is not None:
+            flush.zero_()
+        dev.step_raw(physics.step_scalars(t, st.config.physics), t, stream=s.cuda_stream)
+    torch.cuda.synchronize()
+    print("adoptions", dev.read_stats())
+    if os.environ.get("EVOCA_B200_LIB"):
+        import ctypes as C
+
+        import numpy as np
+
+        from paper_2406_09654_b200 import _lib
+
+        out = np.zeros(8, np.uint64)
+        _lib.check(_lib.load().evo_debug_phase_cycles(_lib.ptr(out), 1))
+        names = ["bucket", "controller", "physics", "commit", "setup"]
+        tot = float(out[:5].sum())
+        for i, n in enumerate(names):
+            print(f"phase {n:10s} {int(out[i]):>14d} cycles  {out[i] / tot * 100:5.1f}%  "
+                  f"{out[i] / args.steps / 148:10.0f} per CTA-step")
+
+
+if __name__ == "__main__":
+    main()
