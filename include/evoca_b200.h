@@ -143,7 +143,8 @@ EVO_API int evo_patch_genomes(evo_ctx* ctx, const int64_t* cells, const int32_t*
 
 /* Device pointers of a plane (halo exchange / interop).  which: 0 energy,
  * 1 infra, 2 comm (3 planes, stride = plane_stride), 3 genome, 4 rotation,
- * 5 mid infra, 6 mid genome, 7 mid proposal byte, 8 mid quantity.
+ * 5 mid infra, 6 mid genome, 7 mid proposal byte, 8 mid quantity, 9 census
+ * counts being accumulated (int32 [capacity]), 10 step stats (int64 [2]).
  * buffer: 0 front, 1 back (ignored for mid planes).  The pointer addresses
  * ghost row -1; row y lives at + (y+1)*W.  plane_stride counts elements. */
 EVO_API int evo_plane_ptr(evo_ctx* ctx, int which, int buffer, void** ptr, int64_t* plane_stride);

@@ -578,6 +578,8 @@ EVO_API int evo_plane_ptr(evo_ctx* c, int which, int buffer, void** ptr, int64_t
     case 6: *ptr = c->mid.gi; break;
     case 7: *ptr = c->mid.rp; break;
     case 8: *ptr = c->mid.q; break;
+    case 9: *ptr = c->census.counts; break;      /* int32 [capacity] accumulated counts */
+    case 10: *ptr = c->census.stats; break;      /* int64 [2] adoptions, extinctions */
     default: return fail(EVO_EINVAL, "unknown plane");
   }
   if (plane_stride) *plane_stride = c->stride;

@@ -21,7 +21,8 @@ from .physics import AdoptionEvents
 __all__ = ["DeviceSubstrate"]
 
 PLANES = {"energy": 0, "infra": 1, "comm": 2, "genome": 3, "rotation": 4,
-          "mid_infra": 5, "mid_genome": 6, "mid_proposal": 7, "mid_quantity": 8}
+          "mid_infra": 5, "mid_genome": 6, "mid_proposal": 7, "mid_quantity": 8,
+          "census_counts": 9, "stats": 10}
 
 
 def _stream(s):

@@ -1,0 +1,230 @@
+"""Row-strip sharding of the torus over GPUs.
+
+Each rank owns rows [row0, row0 + h) of the global H x W torus (x wraps
+locally, y wraps across rank world-1 <-> 0) as a strip context
+(evo_create_strip) whose planes carry one ghost row above and below.  The
+step's dependency radius is 2, split over the two passes:
+
+  1. before pass 1 the sensed front planes (E, I, C0..C2) exchange their
+     boundary rows with the neighbours (ghost rows -1 and h);
+  2. pass 1 (sense, controller, physics tail, shipment proposal);
+  3. the pass-1 outputs a neighbour's pass 2 needs - proposal byte,
+     shipped quantity, post-death genome - exchange boundary rows;
+  4. pass 2 (pull resolve, adoption) accumulates per-rank census counts;
+  5. the counts are summed over ranks (all_reduce) and every rank runs the
+     identical census epilogue, then swaps.
+
+Tie-breaks use global linear source indices ((row0 + y) * W + x), so the
+result is bit-identical for any number of strips (tests/test_strips*.py).
+Exchanges go through ``torch.distributed`` point-to-point operations
+(NCCL over NVLink on GPUs, gloo on CPU), batched per exchange.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+__all__ = ["StripPlan", "HaloComm", "DeviceStrip", "cuda_view"]
+
+
+@dataclass(frozen=True)
+class StripPlan:
+    height: int
+    width: int
+    world: int
+
+    def __post_init__(self):
+        if self.world < 1 or self.height < self.world:
+            raise ValueError("need at least one row per strip")
+
+    def rows(self, rank: int) -> tuple[int, int]:
+        """(row0, h): balanced split, the first H % world ranks one row longer."""
+        base, extra = divmod(self.height, self.world)
+        h = base + (1 if rank < extra else 0)
+        row0 = rank * base + min(rank, extra)
+        return row0, h
+
+    def up(self, rank: int) -> int:
+        """Rank owning global row row0 - 1."""
+        return (rank - 1) % self.world
+
+    def down(self, rank: int) -> int:
+        """Rank owning global row row0 + h."""
+        return (rank + 1) % self.world
+
+
+class HaloComm:
+    """Boundary-row exchange between vertically adjacent strips.
+
+    ``exchange(first, last, ghost_top, ghost_bottom)``: this rank's first
+    row goes to the upper neighbour (its ghost bottom), its last row to the
+    lower neighbour (its ghost top); the ghosts are filled likewise.  Works
+    on CUDA tensors (NCCL) and CPU tensors (gloo); with one rank it is a
+    local wrap copy.  The order of the four operations is the same on every
+    rank so that with two ranks (up == down) the per-peer matching is right.
+    """
+
+    def __init__(self, rank: int = 0, world: int = 1, group=None):
+        self.rank, self.world, self.group = rank, world, group
+
+    def exchange(self, first, last, ghost_top, ghost_bottom) -> None:
+        if self.world == 1:
+            ghost_bottom.copy_(first)
+            ghost_top.copy_(last)
+            return
+        import torch.distributed as dist
+
+        up = (self.rank - 1) % self.world
+        down = (self.rank + 1) % self.world
+        ops = [
+            dist.P2POp(dist.isend, first.contiguous(), up, self.group),
+            dist.P2POp(dist.isend, last.contiguous(), down, self.group),
+            dist.P2POp(dist.irecv, ghost_bottom, down, self.group),
+            dist.P2POp(dist.irecv, ghost_top, up, self.group),
+        ]
+        for r in dist.batch_isend_irecv(ops):
+            r.wait()
+
+    def sum_(self, t) -> None:
+        if self.world == 1:
+            return
+        import torch.distributed as dist
+
+        dist.all_reduce(t, op=dist.ReduceOp.SUM, group=self.group)
+
+
+class _CudaArray:
+    def __init__(self, ptr: int, shape, typestr: str):
+        self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": typestr, "data": (ptr, False),
+                                         "version": 3, "strides": None}
+
+
+_TYPESTR = {np.float32: "<f4", np.int32: "<i4", np.uint8: "|u1", np.int64: "<i8"}
+
+
+def cuda_view(ptr: int, shape, dtype):
+    """A torch CUDA tensor aliasing device memory owned by the C ABI."""
+    import torch
+
+    return torch.as_tensor(_CudaArray(ptr, shape, _TYPESTR[dtype]), device="cuda")
+
+
+class DeviceStrip:
+    """One rank's strip on its GPU, stepped with halo exchanges."""
+
+    FRONT = (("energy", 0), ("infra", 0), ("comm", 0), ("comm", 1), ("comm", 2))
+
+    def __init__(self, plan: StripPlan, rank: int, capacity: int, hidden: int = 0, device: int = 0,
+                 comm: HaloComm | None = None):
+        from .device import DeviceSubstrate
+
+        self.plan, self.rank = plan, rank
+        self.row0, self.h = plan.rows(rank)
+        self.W = plan.width
+        self.dev = DeviceSubstrate(plan.width, self.h, capacity, hidden, device, row0=self.row0,
+                                   height_global=plan.height)
+        self.comm = comm or HaloComm(rank, plan.world)
+
+    # -- views ----------------------------------------------------------------
+    def _plane(self, which: str, buffer: int, sub: int, dtype):
+        ptr, stride = self.dev.plane_ptr(which, buffer)
+        item = np.dtype(dtype).itemsize
+        return cuda_view(ptr + sub * stride * item, (self.h + 2, self.W), dtype)
+
+    def _rows(self, plane):
+        return plane[1], plane[self.h], plane[0], plane[self.h + 1]  # first, last, ghost top, ghost bottom
+
+    def exchange_front(self) -> None:
+        """Ghost rows of the sensed front planes (before pass 1)."""
+        import torch
+
+        views = [self._rows(self._plane(w, 0, k, np.float32)) for w, k in self.FRONT]
+        first = torch.stack([v[0] for v in views])
+        last = torch.stack([v[1] for v in views])
+        gt = torch.empty_like(first)
+        gb = torch.empty_like(first)
+        self.comm.exchange(first, last, gt, gb)
+        for i, v in enumerate(views):
+            v[2].copy_(gt[i])
+            v[3].copy_(gb[i])
+
+    def exchange_mid(self) -> None:
+        """Ghost rows of the pass-1 outputs pass 2 reads (proposal byte,
+        quantity, post-death genome)."""
+        import torch
+
+        gi = self._rows(self._plane("mid_genome", 0, 0, np.int32))
+        q = self._rows(self._plane("mid_quantity", 0, 0, np.float32))
+        rp = self._rows(self._plane("mid_proposal", 0, 0, np.uint8))
+        # pack as int32 words: genome, bits(q), proposal
+        first = torch.stack([gi[0], q[0].view(torch.int32), rp[0].to(torch.int32)])
+        last = torch.stack([gi[1], q[1].view(torch.int32), rp[1].to(torch.int32)])
+        gt = torch.empty_like(first)
+        gb = torch.empty_like(first)
+        self.comm.exchange(first, last, gt, gb)
+        gi[2].copy_(gt[0])
+        gi[3].copy_(gb[0])
+        q[2].copy_(gt[1].view(torch.float32))
+        q[3].copy_(gb[1].view(torch.float32))
+        rp[2].copy_(gt[2].to(torch.uint8))
+        rp[3].copy_(gb[2].to(torch.uint8))
+
+    def front_rows(self):
+        """(first, last, ghost_top, ghost_bottom) views of the sensed front planes, each (5, W)."""
+        return [self._rows(self._plane(w, 0, k, np.float32)) for w, k in self.FRONT]
+
+    def mid_rows(self):
+        return [self._rows(self._plane("mid_genome", 0, 0, np.int32)),
+                self._rows(self._plane("mid_quantity", 0, 0, np.float32)),
+                self._rows(self._plane("mid_proposal", 0, 0, np.uint8))]
+
+    def step(self, scalars, t: int, flags: int = 0) -> None:
+        import torch
+
+        from . import _lib
+
+        stream = torch.cuda.current_stream().cuda_stream
+        self.exchange_front()
+        self.dev.pass1(scalars, t, flags=flags, stream=stream)
+        self.exchange_mid()
+        self.dev.pass2(t, flags=flags | _lib.F_NO_CENSUS, stream=stream)
+        ptr, _ = self.dev.plane_ptr("census_counts")
+        self.comm.sum_(cuda_view(ptr, (self.dev.capacity,), np.int32))
+        self.dev.census_finish(t, stream=stream)
+        self.dev.swap()
+
+
+def step_local(strips, scalars, t: int, flags: int = 0) -> None:
+    """Step several strips driven by ONE process (e.g. a single-GPU
+    emulation of a multi-rank run, or peer devices in one process): the
+    same two exchanges and census sum as ``DeviceStrip.step``, done with
+    device-to-device copies between the strips' ghost rows."""
+    import torch
+
+    from . import _lib
+
+    n = len(strips)
+
+    def ring(views_of):
+        views = [views_of(s) for s in strips]
+        for r in range(n):
+            up, down = views[(r - 1) % n], views[(r + 1) % n]
+            for k in range(len(views[r])):
+                views[r][k][2].copy_(up[k][1])    # ghost top <- upper neighbour's last row
+                views[r][k][3].copy_(down[k][0])  # ghost bottom <- lower neighbour's first row
+
+    stream = torch.cuda.current_stream().cuda_stream
+    ring(lambda s: s.front_rows())
+    for s in strips:
+        s.dev.pass1(scalars, t, flags=flags, stream=stream)
+    ring(lambda s: s.mid_rows())
+    for s in strips:
+        s.dev.pass2(t, flags=flags | _lib.F_NO_CENSUS, stream=stream)
+    counts = [cuda_view(s.dev.plane_ptr("census_counts")[0], (s.dev.capacity,), np.int32) for s in strips]
+    total = torch.stack(counts).sum(0, dtype=torch.int32)
+    for c, s in zip(counts, strips):
+        c.copy_(total)
+        s.dev.census_finish(t, stream=stream)
+        s.dev.swap()
