@@ -9,8 +9,11 @@ A step = one full substrate update (pass 1 + pass 2).  Each timed step is
 bracketed by CUDA events on the launching stream, with an L2 flush (a 256 MiB
 memset, twice the 126 MB L2) before it and outside the timed interval, so the
 52 MB state is read from HBM every step.  Multi-GPU: one process per GPU
-(torchrun); each rank steps its own substrate (weak scaling) and the slowest
-rank's time is reported.
+(torchrun); the torus grows with the GPU count ((1024*N) x 1024, weak
+scaling) and is split into row strips, one per GPU, with NCCL halo exchanges
+and a census all_reduce inside every timed step (paper_2406_09654_b200/
+strips.py); the slowest rank's time is reported.  --strips forces that path
+on one GPU.
 
 --impl reference times the reference algorithm on the host cores: the
 oracle port (oracle/oracle.py; the reference is pure Python and cannot be
@@ -113,24 +116,50 @@ def run_ours(args, rank, world, local):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     cfg = BASELINE_CONFIGS[args.config]
     state = engine.baseline_state(args.config, seed=args.seed + rank)
-    dev = engine.device_of(state, device=local)
-    b = state._evo_binding
-    b.sync_params(state.pool)
-    dev.upload(state.substrate.front)
-    dev.sync()
     stream = torch.cuda.Stream()
     torch.cuda.set_stream(stream)
     sh = stream.cuda_stream
     phys = state.config.physics
     flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device="cuda")
     ncell = cfg.width * cfg.height
+    strips = world > 1 or args.strips
+    if strips:
+        # weak scaling: a (H * world) x W torus, one H x W row strip per GPU,
+        # NCCL halo exchanges + census all_reduce inside every step
+        from paper_2406_09654_b200.strips import DeviceStrip, HaloComm, StripPlan
+
+        plan = StripPlan(cfg.height * world, cfg.width, world)
+        strip = DeviceStrip(plan, rank, state.pool.capacity, cfg.hidden, device=local, comm=HaloComm(rank, world))
+        dev = strip.dev
+        dev.set_params([state.pool.params(s) for s in range(state.pool.capacity)])
+        dev.set_slots(state.pool.slot_states())
+    else:
+        dev = engine.device_of(state, device=local)
+        state._evo_binding.sync_params(state.pool)
+    dev.upload(state.substrate.front)
+    dev.sync()
+
+    def one_step(sc, t, e0=None, e1=None, e2=None):
+        if e0 is not None:
+            e0.record(stream)
+        if strips:
+            strip.step(sc, t)
+            if e1 is not None:
+                e1.record(stream)
+                e2.record(stream)
+            return
+        dev.pass1(sc, t, stream=sh)
+        if e1 is not None:
+            e1.record(stream)
+        dev.pass2(t, stream=sh)
+        if e2 is not None:
+            e2.record(stream)
+        dev.swap()
 
     t = 0
     for _ in range(args.warmup):
         flush.zero_()
-        dev.pass1(physics.step_scalars(t, phys), t, stream=sh)
-        dev.pass2(t, stream=sh)
-        dev.swap()
+        one_step(physics.step_scalars(t, phys), t)
         t += 1
     torch.cuda.synchronize()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
@@ -142,13 +171,7 @@ def run_ours(args, rank, world, local):
     with ClockSampler(local) as clocks:
         for i in range(args.steps):
             flush.zero_()
-            e0, e1, e2 = ev[i]
-            e0.record(stream)
-            dev.pass1(scal[i], t, stream=sh)
-            e1.record(stream)
-            dev.pass2(t, stream=sh)
-            e2.record(stream)
-            dev.swap()
+            one_step(scal[i], t, *ev[i])
             t += 1
         torch.cuda.synchronize()
     k1 = sum(a.elapsed_time(m) for a, m, _ in ev)
@@ -211,9 +234,10 @@ def run_ours(args, rank, world, local):
         "config": {"workload": cfg.name, "grid": [cfg.height, cfg.width], "genomes": cfg.genomes,
                    "net": "45->13 direct" if cfg.hidden == 0 else f"45->{cfg.hidden}->13",
                    "cells_per_gpu": ncell, "l2": "flushed before every timed step (256 MiB memset)",
-                   "parallelism": f"replicas x{world}" if world > 1 else "single GPU"},
+                   "parallelism": (f"row strips x{world} over a {cfg.height * world}x{cfg.width} torus, NCCL halo "
+                                   "exchange + census all_reduce per step") if strips else "single GPU"},
         "roofline": {
-            "kernel": "full step (pass1 k_act_physics + pass2 k_resolve)",
+            "kernel": "full step (pass1 k_pass1_direct + pass2 k_resolve)",
             "bound": "hbm",
             "achieved": achieved_gbs,
             "peak": hbm,
@@ -223,7 +247,8 @@ def run_ours(args, rank, world, local):
             "traffic": traffic,
             "algorithmic_bytes_per_cell": BYTES_PER_CELL,
             "kernels": [
-                {"name": "k_act_physics (pass 1: sense+net+physics)", "ms": k1_s * 1e3, "share": k1 / total_ms,
+                {"name": "k_pass1_direct (pass 1: sense+net+physics)" if not strips else
+                 "strip step (exchanges + pass 1 + pass 2 + census)", "ms": k1_s * 1e3, "share": k1 / total_ms,
                  "fp32_tflops": ncell * FLOP_PER_CELL_DIRECT / k1_s / 1e12 if cfg.hidden == 0 else None,
                  "fp32_peak_tflops_derived": fp32_peak},
                 {"name": "k_resolve (pass 2: explore resolve+adoption+census)", "ms": k2_s * 1e3,
@@ -234,7 +259,7 @@ def run_ours(args, rank, world, local):
                 "api": "paper_2406_09654_b200.engine.step(state) on host-resident planes",
                 "h2d_bytes_per_step": ncell * 25 + state.pool.capacity * 9,
                 "d2h_bytes_per_step": ncell * 25 + state.pool.capacity * 4 + 16},
-        "gpu_launches": 2 * args.steps,
+        "gpu_launches": (3 if strips else 2) * args.steps,
         "clocks": clk,
         "adoptions_last_step": int(adoptions),
     }
@@ -309,6 +334,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--strips", action="store_true", help="use the row-strip (multi-GPU) path even on one GPU")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
