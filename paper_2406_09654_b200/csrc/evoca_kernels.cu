@@ -119,16 +119,11 @@ __device__ __forceinline__ void tile_controller(const Pass1Args& a, SM& sm, int 
   const int nu = sm.n_units;
   for (int q = threadIdx.x; q < nu; q += THREADS) {
     unsigned short ord[U];
-    if (U == 4) {
-      const ushort4 o4 = reinterpret_cast<const ushort4*>(sm.order)[q];
-      ord[0] = o4.x;
-      ord[1 % U] = o4.y;
-      ord[2 % U] = o4.z;
-      ord[3 % U] = o4.w;
-    } else {
-      const ushort2 o2 = reinterpret_cast<const ushort2*>(sm.order)[q];
-      ord[0] = o2.x;
-      ord[1 % U] = o2.y;
+#pragma unroll
+    for (int c = 0; c < U; c += 2) {  // order entries are 16-bit, read in 32-bit pairs
+      const unsigned w = reinterpret_cast<const unsigned*>(sm.order)[(q * U + c) >> 1];
+      ord[c] = (unsigned short)(w & 0xFFFFu);
+      ord[(c + 1) % U] = (unsigned short)(w >> 16);
     }
     int pos[U], hb[U], rot[U];
     bool valid[U];
@@ -216,10 +211,10 @@ __global__ void __launch_bounds__(kThreads1, 2) k_pass1_generic(const Pass1Args 
 // ---------------------------------------------------------------------------
 // Pass 1, hot path: persistent, direct net, FFMA2
 
-constexpr int kThreadsP = 640;
-constexpr int kUnitP = 2;  // cells per thread in the controller (a same-genome pair)
-constexpr int kPreHalo = (kHaloCells + kThreadsP - 1) / kThreadsP;  // 2
-constexpr int kPreCells = (kTileCells + kThreadsP - 1) / kThreadsP;  // 2
+constexpr int kThreadsP = 576;  // >= units of a tile for pools <= 64 slots: one controller round
+constexpr int kUnitP = 2;       // cells per thread in the controller (a same-genome pair)
+constexpr int kPreHalo = (kHaloCells + kThreadsP - 1) / kThreadsP;
+constexpr int kPreCells = (kTileCells + kThreadsP - 1) / kThreadsP;
 
 struct DirectSmem {
   float4 eic[kHaloCells];
@@ -393,21 +388,22 @@ constexpr size_t weight_smem_bytes(int capacity) {
 // ---------------------------------------------------------------------------
 // Pass 2
 
-constexpr int kResW = 32, kResH = 16;  // resolve tile
-constexpr int kResCells = kResW * kResH;
-constexpr int kResHW = kResW + 2;
-constexpr int kResHalo = (kResH + 2) * kResHW;
+// Pass 2 works on warp tiles of 32 x 4 cells: each warp stages its own tile
+// plus 1-cell halo (proposal byte, quantity, post-death genome; infra of the
+// tile) in a private shared-memory slice and resolves it without any CTA
+// barrier, so the latency of one warp's loads overlaps the others' work.
+constexpr int kWtW = 32, kWtH = 4;  // warp tile
+constexpr int kWtCells = kWtW * kWtH;
+constexpr int kWtHW = kWtW + 2;
+constexpr int kWtHalo = (kWtH + 2) * kWtHW;
+constexpr int kWarps2 = kThreads2 / 32;
 
-// Pass-2 tile staging: the pass-1 proposal byte, quantity and genome of the
-// tile plus its 1-cell halo, and the post-withdrawal infrastructure of the
-// tile, all loaded with independent coalesced reads before any cell work.
-struct ResolveSmem {
-  uint8_t rp[kResHalo];
-  float q[kResHalo];
-  int gi[kResHalo];
-  float inf[kResCells];
-  int cnt[3];
-  unsigned short list[3][kResCells];
+struct WarpTile {
+  uint8_t rp[kWtHalo];
+  float q[kWtHalo];
+  int gi[kWtHalo];
+  float inf[kWtCells];
+  unsigned short queue[kWtCells];
 };
 
 // Shipment arriving at tile cell (ty, tx) from direction d: halo index of the
@@ -418,11 +414,11 @@ struct Arrival {
   u64 key;
 };
 
-__device__ __forceinline__ Arrival arrival(const StepGeom& g, const ResolveSmem& sm, int y, int x, int ty, int tx,
+__device__ __forceinline__ Arrival arrival(const StepGeom& g, const WarpTile& wt, int y, int x, int ty, int tx,
                                            int d) {
   Arrival r;
-  r.h = (ty + 1 - dir_dy(d)) * kResHW + tx + 1 - dir_dx(d);
-  r.q = __fadd_rn(sm.q[r.h], 0.0f);  // canonical +0
+  r.h = (ty + 1 - dir_dy(d)) * kWtHW + tx + 1 - dir_dx(d);
+  r.q = __fadd_rn(wt.q[r.h], 0.0f);  // canonical +0
   const int sy = y - dir_dy(d);
   int sx = x - dir_dx(d);
   sx = sx < 0 ? sx + g.W : (sx >= g.W ? sx - g.W : sx);
@@ -440,11 +436,11 @@ __device__ __forceinline__ void ce_desc(u64& a, u64& b) {  // max first
   b = lo;
 }
 
-__device__ __forceinline__ unsigned arrival_mask(const ResolveSmem& sm, int ty, int tx) {
+__device__ __forceinline__ unsigned arrival_mask(const WarpTile& wt, int ty, int tx) {
   unsigned m = 0;
 #pragma unroll
   for (int d = 0; d < 8; ++d) {
-    const uint8_t rp = sm.rp[(ty + 1 - dir_dy(d)) * kResHW + tx + 1 - dir_dx(d)];
+    const uint8_t rp = wt.rp[(ty + 1 - dir_dy(d)) * kWtHW + tx + 1 - dir_dx(d)];
     m |= ((rp & 0x78u) == (unsigned)(kShipBit | (d << 3))) ? (1u << d) : 0u;
   }
   return m;
@@ -452,42 +448,49 @@ __device__ __forceinline__ unsigned arrival_mask(const ResolveSmem& sm, int ty, 
 
 // Resolve one target cell whose arrival mask is m (bit d: the neighbour at
 // t - off[d] ships in direction d): ordered sum, winner, adoption, stores.
-// Returns the cell's final genome slot.
-template <bool kRecord>
-__device__ __forceinline__ int resolve_cell(const Pass2Args& a, const ResolveSmem& sm, int ty, int tx, int y, int x,
+// Returns the cell's final genome slot.  KIND restricts the compiled paths
+// (1: at most one arrival, 2: exactly two, 3: three or more) so that a warp
+// never executes predicated-off code of the other cases.
+template <bool kRecord, int KIND>
+__device__ __forceinline__ int resolve_cell(const Pass2Args& a, const WarpTile& wt, int ty, int tx, int y, int x,
                                             unsigned m, int& adopted) {
   const StepGeom& g = a.g;
-  const int hc = (ty + 1) * kResHW + tx + 1;
-  const float before = sm.inf[ty * kResW + tx];
-  const int own = sm.gi[hc];
-  const int r = sm.rp[hc] & 7;
+  const int hc = (ty + 1) * kWtHW + tx + 1;
+  const float before = wt.inf[ty * kWtW + tx];
+  const int own = wt.gi[hc];
+  const int r = wt.rp[hc] & 7;
   float acc = before;
   int gnew = own, rnew = r;
   bool adopt = false;
   if (m) {
-    const int n = __popc(m);
+    const int n = KIND == 1 ? 1 : (KIND == 2 ? 2 : 3);
     u64 win;
     int wd, wh;
-    if (n == 1) {
+    if (n == 1) {  // single arrival: no ordering, source index only for the event record
       wd = __ffs(m) - 1;
-      const Arrival v = arrival(g, sm, y, x, ty, tx, wd);
-      acc = __fadd_rn(acc, v.q);
-      win = v.key;
-      wh = v.h;
-    } else if (n == 2) {
+      wh = (ty + 1 - dir_dy(wd)) * kWtHW + tx + 1 - dir_dx(wd);
+      const float q = __fadd_rn(wt.q[wh], 0.0f);
+      acc = __fadd_rn(acc, q);
+      win = (u64)__float_as_uint(q) << 32;
+      if (kRecord) win = arrival(g, wt, y, x, ty, tx, wd).key;
+    } else if (n == 2) {  // order by q; the global source index only breaks exact ties
       const int d0 = __ffs(m) - 1, d1 = __ffs(m & (m - 1)) - 1;
-      const Arrival v0 = arrival(g, sm, y, x, ty, tx, d0), v1 = arrival(g, sm, y, x, ty, tx, d1);
-      const bool first0 = v0.key > v1.key;
-      acc = __fadd_rn(__fadd_rn(acc, first0 ? v0.q : v1.q), first0 ? v1.q : v0.q);
-      win = first0 ? v0.key : v1.key;
+      const int h0 = (ty + 1 - dir_dy(d0)) * kWtHW + tx + 1 - dir_dx(d0);
+      const int h1 = (ty + 1 - dir_dy(d1)) * kWtHW + tx + 1 - dir_dx(d1);
+      const float q0 = __fadd_rn(wt.q[h0], 0.0f), q1 = __fadd_rn(wt.q[h1], 0.0f);
+      bool first0 = q0 > q1;
+      if (q0 == q1) first0 = arrival(g, wt, y, x, ty, tx, d0).key > arrival(g, wt, y, x, ty, tx, d1).key;
+      acc = __fadd_rn(__fadd_rn(acc, first0 ? q0 : q1), first0 ? q1 : q0);
       wd = first0 ? d0 : d1;
-      wh = first0 ? v0.h : v1.h;
+      wh = first0 ? h0 : h1;
+      win = (u64)__float_as_uint(first0 ? q0 : q1) << 32;
+      if (kRecord) win = arrival(g, wt, y, x, ty, tx, wd).key;
     } else {
       // general: keys for all eight directions (absent = 0), sorting network
       // (Batcher odd-even merge, 19 comparators), sequential sum
       u64 k[8];
 #pragma unroll
-      for (int d = 0; d < 8; ++d) k[d] = (m & (1u << d)) ? arrival(g, sm, y, x, ty, tx, d).key : 0ull;
+      for (int d = 0; d < 8; ++d) k[d] = (m & (1u << d)) ? arrival(g, wt, y, x, ty, tx, d).key : 0ull;
       win = 0;
       wd = 0;
 #pragma unroll
@@ -496,7 +499,7 @@ __device__ __forceinline__ int resolve_cell(const Pass2Args& a, const ResolveSme
           win = k[d];
           wd = d;
         }
-      wh = (ty + 1 - dir_dy(wd)) * kResHW + tx + 1 - dir_dx(wd);
+      wh = (ty + 1 - dir_dy(wd)) * kWtHW + tx + 1 - dir_dx(wd);
       ce_desc(k[0], k[1]); ce_desc(k[2], k[3]); ce_desc(k[4], k[5]); ce_desc(k[6], k[7]);
       ce_desc(k[0], k[2]); ce_desc(k[1], k[3]); ce_desc(k[4], k[6]); ce_desc(k[5], k[7]);
       ce_desc(k[1], k[2]); ce_desc(k[5], k[6]);
@@ -510,7 +513,7 @@ __device__ __forceinline__ int resolve_cell(const Pass2Args& a, const ResolveSme
     const float qw = __uint_as_float((unsigned)(win >> 32));
     if (qw > before) {  // physics.py:325
       adopt = true;
-      gnew = sm.gi[wh];
+      gnew = wt.gi[wh];
       rnew = wd;
       if (kRecord) {
         const long long cell = (long long)y * g.W + x;
@@ -542,111 +545,119 @@ __device__ __forceinline__ int resolve_cell(const Pass2Args& a, const ResolveSme
   return gnew;
 }
 
-// Cells with 0 or 1 arrival resolve in place; cells with several arrivals are
-// queued per arrival count (2, 3, >=4) and resolved afterwards by whole warps
-// of the same kind, so the ordering work never diverges inside a warp.
 template <bool kRecord>
 __global__ void __launch_bounds__(kThreads2) k_resolve(const Pass2Args a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  ResolveSmem& sm = *reinterpret_cast<ResolveSmem*>(smem_raw);
-  int* hist = reinterpret_cast<int*>(smem_raw + ((sizeof(ResolveSmem) + 15) & ~(size_t)15));
+  WarpTile* wts = reinterpret_cast<WarpTile*>(smem_raw);
+  int* hist = reinterpret_cast<int*>(smem_raw + ((sizeof(WarpTile) * kWarps2 + 15) & ~(size_t)15));
   __shared__ int s_adopt;
   __shared__ bool s_last;
   const StepGeom& g = a.g;
-  const int tid = threadIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  WarpTile& wt = wts[warp];
   for (int b = tid; b < a.capacity; b += kThreads2) hist[b] = 0;
   if (tid == 0) s_adopt = 0;
-  const int tiles_x = (g.W + kResW - 1) / kResW;
-  const int ntiles = tiles_x * ((g.H + kResH - 1) / kResH);
+  __syncthreads();
+  const int tiles_x = (g.W + kWtW - 1) / kWtW;
+  const int ntiles = tiles_x * ((g.H + kWtH - 1) / kWtH);
   int my_adopt = 0;
-  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    const int x0 = (tile % tiles_x) * kResW;
-    const int y0 = (tile / tiles_x) * kResH;
-    __syncthreads();
-    if (tid < 3) sm.cnt[tid] = 0;
+  for (int tile = blockIdx.x * kWarps2 + warp; tile < ntiles; tile += gridDim.x * kWarps2) {
+    const int x0 = (tile % tiles_x) * kWtW;
+    const int y0 = (tile / tiles_x) * kWtH;
     {
-      // all staging loads of the tile issued before any shared store
-      constexpr int kHaloIt = (kResHalo + kThreads2 - 1) / kThreads2;
-      constexpr int kCellIt = kResCells / kThreads2;
-      uint8_t vrp[kHaloIt];
-      float vq[kHaloIt], vi[kCellIt];
-      int vg[kHaloIt];
+      // all staging loads of the warp tile issued before any shared store
+      // halo column lane (x0-1+lane) of every halo row, plus halo columns 32
+      // and 33 on lanes 0 and 1; ghost rows make the vertical wrap implicit
+      constexpr int kRows = kWtH + 2;
+      int xa = x0 - 1 + lane;
+      xa = xa < 0 ? xa + g.W : (xa >= g.W ? xa - g.W : xa);
+      if (xa >= g.W) xa = g.W - 1;
+      int xb = x0 + 31 + (lane & 1);
+      xb = xb >= g.W ? xb - g.W : xb;
+      if (xb >= g.W) xb = g.W - 1;
+      const bool extra = lane < 2;
+      uint8_t vrp[kRows], wrp[kRows];
+      float vq[kRows], wq[kRows], vi[kWtH];
+      int vg[kRows], wg[kRows];
 #pragma unroll
-      for (int j = 0; j < kHaloIt; ++j) {
-        const int i = tid + j * kThreads2;
-        const int hy = i / kResHW, hx = i - hy * kResHW;
-        int y = y0 + hy - 1;
-        if (y > g.H) y = g.H;
-        int x = x0 + hx - 1;
-        x = x < 0 ? x + g.W : (x >= g.W ? x - g.W : x);
-        if (x >= g.W) x = g.W - 1;
-        const unsigned o = i < kResHalo ? (unsigned)((y + 1) * g.W + x) : 0u;
-        vrp[j] = __ldg(a.mid.rp + o);
-        vq[j] = __ldg(a.mid.q + o);
-        vg[j] = __ldg(a.mid.gi + o);
+      for (int r = 0; r < kRows; ++r) {
+        const int y = min(y0 + r - 1, g.H);
+        const unsigned row = (unsigned)((y + 1) * g.W);
+        vrp[r] = __ldg(a.mid.rp + row + xa);
+        vq[r] = __ldg(a.mid.q + row + xa);
+        vg[r] = __ldg(a.mid.gi + row + xa);
+        if (extra) {
+          wrp[r] = __ldg(a.mid.rp + row + xb);
+          wq[r] = __ldg(a.mid.q + row + xb);
+          wg[r] = __ldg(a.mid.gi + row + xb);
+        }
       }
+      const int xi = min(x0 + lane, g.W - 1);
 #pragma unroll
-      for (int j = 0; j < kCellIt; ++j) {
-        const int i = tid + j * kThreads2;
-        const int ty = i / kResW, tx = i - ty * kResW;
-        const int y = min(y0 + ty, g.H - 1), x = min(x0 + tx, g.W - 1);
-        vi[j] = __ldg(a.mid.I + (unsigned)((y + 1) * g.W + x));
-      }
+      for (int j = 0; j < kWtH; ++j) vi[j] = __ldg(a.mid.I + (unsigned)((min(y0 + j, g.H - 1) + 1) * g.W + xi));
+      __syncwarp();
 #pragma unroll
-      for (int j = 0; j < kHaloIt; ++j) {
-        const int i = tid + j * kThreads2;
-        if (i < kResHalo) {
-          sm.rp[i] = vrp[j];
-          sm.q[i] = vq[j];
-          sm.gi[i] = vg[j];
+      for (int r = 0; r < kRows; ++r) {
+        wt.rp[r * kWtHW + lane] = vrp[r];
+        wt.q[r * kWtHW + lane] = vq[r];
+        wt.gi[r * kWtHW + lane] = vg[r];
+        if (extra) {
+          wt.rp[r * kWtHW + 32 + lane] = wrp[r];
+          wt.q[r * kWtHW + 32 + lane] = wq[r];
+          wt.gi[r * kWtHW + 32 + lane] = wg[r];
         }
       }
 #pragma unroll
-      for (int j = 0; j < kCellIt; ++j) sm.inf[tid + j * kThreads2] = vi[j];
+      for (int j = 0; j < kWtH; ++j) wt.inf[j * kWtW + lane] = vi[j];
+      __syncwarp();
     }
-    __syncthreads();
-#pragma unroll 1
-    for (int i = tid; i < kResCells; i += kThreads2) {
-      const int ty = i / kResW, tx = i - ty * kResW;
+    // cells with <= 1 arrival resolve in place; the rest are queued so that
+    // the ordering work runs on whole warps
+    // queue[0..n2): exactly two arrivals; queue[kWtCells-n3..): three or more
+    int n2 = 0, n3 = 0;
+#pragma unroll
+    for (int j = 0; j < kWtH; ++j) {
+      const int ty = j, tx = lane;
       const int y = y0 + ty, x = x0 + tx;
-      int key = -1;    // census slot
-      int queue = -1;  // deferred multi-arrival bucket
+      int key = -1;
+      int kind = 0;  // 0 resolved here, 2 / 3 deferred
       if (y < g.H && x < g.W) {
-        const unsigned m = arrival_mask(sm, ty, tx);
-        const int n = __popc(m);
-        if (n <= 1) {
-          const int gn = resolve_cell<kRecord>(a, sm, ty, tx, y, x, m, my_adopt);
+        const unsigned m = arrival_mask(wt, ty, tx);
+        if ((m & (m - 1)) == 0) {
+          const int gn = resolve_cell<kRecord, 1>(a, wt, ty, tx, y, x, m, my_adopt);
           key = (gn >= 0 && gn < a.capacity) ? gn : -1;
         } else {
-          queue = n == 2 ? 0 : (n == 3 ? 1 : 2);
+          kind = __popc(m) == 2 ? 2 : 3;
         }
       }
-      aggregated_rank(hist, key);
-      const int slot = aggregated_rank(sm.cnt, queue);
-      if (queue >= 0) sm.list[queue][slot] = (unsigned short)i;
+      const unsigned b2 = __ballot_sync(0xffffffffu, kind == 2);
+      const unsigned b3 = __ballot_sync(0xffffffffu, kind == 3);
+      const unsigned below = (1u << lane) - 1u;
+      if (kind == 2) wt.queue[n2 + __popc(b2 & below)] = (unsigned short)(ty * kWtW + tx);
+      if (kind == 3) wt.queue[kWtCells - 1 - (n3 + __popc(b3 & below))] = (unsigned short)(ty * kWtW + tx);
+      n2 += __popc(b2);
+      n3 += __popc(b3);
+      if (key >= 0) atomicAdd(&hist[key], 1);
     }
-    __syncthreads();
+    __syncwarp();
 #pragma unroll 1
-    for (int b = 0; b < 3; ++b) {
-      const int cnt = sm.cnt[b];
-#pragma unroll 1
-      for (int base = 0; base < cnt; base += kThreads2) {
-        const int e = base + tid;
-        int key = -1;
-        if (e < cnt) {
-          const int i = sm.list[b][e];
-          const int ty = i / kResW, tx = i - ty * kResW;
-          const int gn =
-              resolve_cell<kRecord>(a, sm, ty, tx, y0 + ty, x0 + tx, arrival_mask(sm, ty, tx), my_adopt);
-          key = (gn >= 0 && gn < a.capacity) ? gn : -1;
-        }
-        aggregated_rank(hist, key);
-      }
+    for (int e = lane; e < n2; e += 32) {
+      const int i = wt.queue[e];
+      const int ty = i / kWtW, tx = i - ty * kWtW;
+      const int gn = resolve_cell<kRecord, 2>(a, wt, ty, tx, y0 + ty, x0 + tx, arrival_mask(wt, ty, tx), my_adopt);
+      if (gn >= 0 && gn < a.capacity) atomicAdd(&hist[gn], 1);
     }
+#pragma unroll 1
+    for (int e = lane; e < n3; e += 32) {
+      const int i = wt.queue[kWtCells - 1 - e];
+      const int ty = i / kWtW, tx = i - ty * kWtW;
+      const int gn = resolve_cell<kRecord, 3>(a, wt, ty, tx, y0 + ty, x0 + tx, arrival_mask(wt, ty, tx), my_adopt);
+      if (gn >= 0 && gn < a.capacity) atomicAdd(&hist[gn], 1);
+    }
+    __syncwarp();
   }
-  __syncthreads();
   for (int off = 16; off > 0; off >>= 1) my_adopt += __shfl_xor_sync(0xffffffffu, my_adopt, off);
-  if ((tid & 31) == 0 && my_adopt) atomicAdd(&s_adopt, my_adopt);
+  if (lane == 0 && my_adopt) atomicAdd(&s_adopt, my_adopt);
   __syncthreads();
   if (tid == 0 && s_adopt) atomicAdd((unsigned long long*)&a.census.stats[0], (unsigned long long)s_adopt);
   for (int b = tid; b < a.capacity; b += kThreads2)
@@ -804,10 +815,14 @@ cudaError_t launch_pass1(const Pass1Args& a, bool inject, bool export_actions, c
 }
 
 cudaError_t launch_pass2(const Pass2Args& a, cudaStream_t st) {
-  const int tiles = ((a.g.W + kResW - 1) / kResW) * ((a.g.H + kResH - 1) / kResH);
-  int grid = num_sms() * 4;
-  if (grid > tiles) grid = tiles;
-  const size_t smem = ((sizeof(ResolveSmem) + 15) & ~(size_t)15) + (size_t)a.capacity * sizeof(int);
+  const int tiles = ((a.g.W + kWtW - 1) / kWtW) * ((a.g.H + kWtH - 1) / kWtH);
+  // few CTAs, many warp tiles each: the per-CTA census flush (capacity
+  // global atomics on shared addresses) and the completion ticket are
+  // serialised in L2, so they must not scale with the grid
+  int grid = num_sms() * 8;
+  const int need = (tiles + kWarps2 - 1) / kWarps2;
+  if (grid > need) grid = need;
+  const size_t smem = ((sizeof(WarpTile) * kWarps2 + 15) & ~(size_t)15) + (size_t)a.capacity * sizeof(int);
   if (a.ev.src) {
     static int cfg = 0;
     cudaError_t e = set_smem(k_resolve<true>, smem, cfg);

@@ -30,12 +30,22 @@ __device__ __forceinline__ float ld_na(const float* p) {
 // output exactly fmaf-chained (the FFMA2 lanes are independent fmaf).
 template <bool kSmemW>
 __device__ __forceinline__ float4 wload4(const float4* p) {
-  if (kSmemW) return *p;  // shared-memory weight table
+  if (kSmemW) {  // shared-memory weight table (explicit 32-bit shared address)
+    float4 r;
+    asm("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];"
+        : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
+        : "r"((unsigned)__cvta_generic_to_shared(p)));
+    return r;
+  }
   return __ldg(p);
 }
 template <bool kSmemW>
 __device__ __forceinline__ float wload1(const float* p) {
-  if (kSmemW) return *p;
+  if (kSmemW) {
+    float r;
+    asm("ld.shared.f32 %0, [%1];" : "=f"(r) : "r"((unsigned)__cvta_generic_to_shared(p)));
+    return r;
+  }
   return __ldg(p);
 }
 
@@ -51,35 +61,63 @@ __device__ __forceinline__ void net_direct_unit(const SM& sm, const float* __res
     for (int p = 0; p < 6; ++p) acc[c][p] = 0ull;
     acc12[c] = 0.0f;
   }
+  // software pipeline: the next slot's sensors are in flight while this
+  // slot's FMAs run (shared-memory latency dominates otherwise)
+  float xn[U][5];
+#pragma unroll
+  for (int c = 0; c < U; ++c) {
+    const float4 v = sm.eic[hb[c]];
+    xn[c][0] = v.x;
+    xn[c][1] = v.y;
+    xn[c][2] = v.z;
+    xn[c][3] = v.w;
+    xn[c][4] = sm.c2[hb[c]];
+  }
 #pragma unroll 1
   for (int s = 0; s < 9; ++s) {
     float x[U][5];
 #pragma unroll
-    for (int c = 0; c < U; ++c) {
-      const int nb = hb[c] + sm.slot_off[rot[c] * 9 + s];
-      const float4 v = sm.eic[nb];
-      x[c][0] = v.x;
-      x[c][1] = v.y;
-      x[c][2] = v.z;
-      x[c][3] = v.w;
-      x[c][4] = sm.c2[nb];
+    for (int c = 0; c < U; ++c)
+#pragma unroll
+      for (int ch = 0; ch < 5; ++ch) x[c][ch] = xn[c][ch];
+    if (s < 8) {
+#pragma unroll
+      for (int c = 0; c < U; ++c) {
+        const int nb = hb[c] + sm.slot_off[rot[c] * 9 + s + 1];
+        const float4 v = sm.eic[nb];
+        xn[c][0] = v.x;
+        xn[c][1] = v.y;
+        xn[c][2] = v.z;
+        xn[c][3] = v.w;
+        xn[c][4] = sm.c2[nb];
+      }
     }
     const float4* wrow = reinterpret_cast<const float4*>(W12 + (size_t)s * 5 * 12);
     const float* w1row = W1 + s * 5;
 #pragma unroll
     for (int ch = 0; ch < 5; ++ch) {
+#ifdef EVO_DIAG_NO_WEIGHTS  // diagnostics builds only: results are wrong
+      const float4 wa = make_float4(s * 1e-3f, ch * 1e-3f, 1e-3f, 2e-3f), wb = wa, wc = wa;
+      const float w12 = 1e-3f;
+#else
       const float4 wa = wload4<kSmemW>(wrow + ch * 3 + 0);
       const float4 wb = wload4<kSmemW>(wrow + ch * 3 + 1);
       const float4 wc = wload4<kSmemW>(wrow + ch * 3 + 2);
       const float w12 = wload1<kSmemW>(w1row + ch);
+#endif
       const u64 wp[6] = {pk2(wa.x, wa.y), pk2(wa.z, wa.w), pk2(wb.x, wb.y),
                          pk2(wb.z, wb.w), pk2(wc.x, wc.y), pk2(wc.z, wc.w)};
+#ifndef EVO_DIAG_NO_FMA
 #pragma unroll
       for (int c = 0; c < U; ++c) {
 #pragma unroll
         for (int p = 0; p < 6; ++p) ffma2(acc[c][p], x[c][ch], wp[p]);
         acc12[c] = fmaf(x[c][ch], w12, acc12[c]);
       }
+#else
+#pragma unroll
+      for (int c = 0; c < U; ++c) acc12[c] += x[c][ch] + __uint_as_float((unsigned)wp[ch % 6]) + w12;
+#endif
     }
   }
   const float4* b4 = reinterpret_cast<const float4*>(B);

@@ -16,12 +16,13 @@ def main():
     ap.add_argument("--config", default="c2")
     ap.add_argument("--steps", type=int, default=6)
     ap.add_argument("--flush", action="store_true")
+    ap.add_argument("--genomes", type=int, default=None)
     args = ap.parse_args()
     import torch
 
     from paper_2406_09654_b200 import engine, physics
 
-    st = engine.baseline_state(args.config)
+    st = engine.baseline_state(args.config, genomes=args.genomes)
     dev = engine.device_of(st)
     st._evo_binding.sync_params(st.pool)
     dev.upload(st.substrate.front)
