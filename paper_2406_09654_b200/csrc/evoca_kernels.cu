@@ -125,6 +125,7 @@ __device__ __forceinline__ void tile_controller(const Pass1Args& a, SM& sm, int 
       ord[c] = (unsigned short)(w & 0xFFFFu);
       ord[(c + 1) % U] = (unsigned short)(w >> 16);
     }
+    if (ord[0] == 0xFFFF) continue;  // a pure padding unit (groups padded past U cells)
     int pos[U], hb[U], rot[U];
     bool valid[U];
 #pragma unroll
@@ -136,6 +137,14 @@ __device__ __forceinline__ void tile_controller(const Pass1Args& a, SM& sm, int 
       rot[c] = sm.rot[pos[c]];
     }
     const int slot = sm.gi[pos[0]];
+#ifdef EVO_PHASE_TIMING
+    {  // diagnostics: distinct genome slots per warp-iteration of the unit loop
+      const unsigned act = __activemask();
+      const unsigned grp = __match_any_sync(act, slot);
+      if ((threadIdx.x & 31) == __ffs(grp) - 1) atomicAdd(&g_phase_cycles[6], 1ull);
+      if ((threadIdx.x & 31) == __ffs(act) - 1) atomicAdd(&g_phase_cycles[7], 1ull);
+    }
+#endif
     if (!kHidden) {
       float out[U][kActuators];
       net_direct_unit<U, kSmemW>(sm, W12 + (size_t)slot * kSensors * 12, W1 + (size_t)slot * kSensors,
@@ -211,7 +220,7 @@ __global__ void __launch_bounds__(kThreads1, 2) k_pass1_generic(const Pass1Args 
 // ---------------------------------------------------------------------------
 // Pass 1, hot path: persistent, direct net, FFMA2
 
-constexpr int kThreadsP = 576;  // >= units of a tile for pools <= 64 slots: one controller round
+constexpr int kThreadsP = 640;  // >= units of a tile for pools <= 64 slots: one controller round
 constexpr int kUnitP = 2;       // cells per thread in the controller (a same-genome pair)
 constexpr int kPreHalo = (kHaloCells + kThreadsP - 1) / kThreadsP;
 constexpr int kPreCells = (kTileCells + kThreadsP - 1) / kThreadsP;
@@ -363,7 +372,7 @@ __global__ void __launch_bounds__(kThreadsP, 1) k_pass1_direct(const Pass1Args a
     const int y0 = (tile / tiles_x) * kTileH;
     const int next = tile + gridDim.x;
     if (next < ntiles) prefetch_tile_l2(a, next, tiles_x);
-    bucket_by_genome<kThreadsP, kPreCells, kUnitP>(sm.bins, sm.scratch, sm.gi, sm.order, &sm.n_units, a.capacity);
+    bucket_by_genome<kThreadsP, kPreCells, 2 * kUnitP, kUnitP>(sm.bins, sm.scratch, sm.gi, sm.order, &sm.n_units, a.capacity);
     PHASE_MARK(0);
     tile_controller<kExport, false, kThreadsP, kUnitP, kSmemW>(a, sm, x0, y0, sW12, sW1, sB);
     __syncthreads();

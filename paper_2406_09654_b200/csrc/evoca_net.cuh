@@ -39,6 +39,22 @@ __device__ __forceinline__ float4 wload4(const float4* p) {
   }
   return __ldg(p);
 }
+// Two packed weights.  From shared memory one volatile 64-bit load (kept
+// apart so ptxas does not fuse neighbours into an LDS.128): measured on
+// B200, an LDS.64 whose lanes read a few genome rows is served in ONE
+// wavefront iff every even/odd lane pair reads the same row - hence the
+// bucketing pads genome groups to an even number of units - while an
+// LDS.128 never takes fewer than two (tools/microbench/lds_sizes.cu).
+template <bool kSmemW>
+__device__ __forceinline__ u64 wload2(const float* p) {
+  u64 r;
+  if (kSmemW) {
+    asm volatile("ld.volatile.shared.b64 %0, [%1];" : "=l"(r) : "r"((unsigned)__cvta_generic_to_shared(p)));
+  } else {
+    asm("ld.global.nc.b64 %0, [%1];" : "=l"(r) : "l"(p));
+  }
+  return r;
+}
 template <bool kSmemW>
 __device__ __forceinline__ float wload1(const float* p) {
   if (kSmemW) {
@@ -73,7 +89,7 @@ __device__ __forceinline__ void net_direct_unit(const SM& sm, const float* __res
     xn[c][3] = v.w;
     xn[c][4] = sm.c2[hb[c]];
   }
-#pragma unroll 1
+#pragma unroll
   for (int s = 0; s < 9; ++s) {
     float x[U][5];
 #pragma unroll
@@ -92,21 +108,20 @@ __device__ __forceinline__ void net_direct_unit(const SM& sm, const float* __res
         xn[c][4] = sm.c2[nb];
       }
     }
-    const float4* wrow = reinterpret_cast<const float4*>(W12 + (size_t)s * 5 * 12);
+    const float* wrow = W12 + (size_t)s * 5 * 12;
     const float* w1row = W1 + s * 5;
 #pragma unroll
     for (int ch = 0; ch < 5; ++ch) {
 #ifdef EVO_DIAG_NO_WEIGHTS  // diagnostics builds only: results are wrong
-      const float4 wa = make_float4(s * 1e-3f, ch * 1e-3f, 1e-3f, 2e-3f), wb = wa, wc = wa;
+      const u64 wq = pk2(s * 1e-3f, ch * 1e-3f);
+      const u64 wp[6] = {wq, wq, wq, wq, wq, wq};
       const float w12 = 1e-3f;
 #else
-      const float4 wa = wload4<kSmemW>(wrow + ch * 3 + 0);
-      const float4 wb = wload4<kSmemW>(wrow + ch * 3 + 1);
-      const float4 wc = wload4<kSmemW>(wrow + ch * 3 + 2);
+      u64 wp[6];
+#pragma unroll
+      for (int p = 0; p < 6; ++p) wp[p] = wload2<kSmemW>(wrow + ch * 12 + 2 * p);
       const float w12 = wload1<kSmemW>(w1row + ch);
 #endif
-      const u64 wp[6] = {pk2(wa.x, wa.y), pk2(wa.z, wa.w), pk2(wb.x, wb.y),
-                         pk2(wb.z, wb.w), pk2(wc.x, wc.y), pk2(wc.z, wc.w)};
 #ifndef EVO_DIAG_NO_FMA
 #pragma unroll
       for (int c = 0; c < U; ++c) {

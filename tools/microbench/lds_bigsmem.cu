@@ -11,7 +11,7 @@ __global__ void k(float* out, int iters, int off_floats) {
     const unsigned a = base + ((it * 16) & 1023);
     float x, y, z, w;
     asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(x), "=f"(y), "=f"(z), "=f"(w) : "r"(a));
-    acc += x + w;
+    acc += x + y + z + w;
   }
   if (acc == -1.f) out[0] = acc;
 }

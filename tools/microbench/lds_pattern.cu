@@ -32,7 +32,7 @@ __global__ void k(float* out, int iters) {
     if (VEC == 4) {
       float x, y, z, w;
       asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(x), "=f"(y), "=f"(z), "=f"(w) : "r"(a));
-      acc += x + w;
+      acc += x + y + z + w;
     } else {
       float x;
       asm volatile("ld.shared.f32 %0, [%1];" : "=f"(x) : "r"(a));

@@ -49,6 +49,8 @@ def main():
         for i, n in enumerate(names):
             print(f"phase {n:10s} {int(out[i]):>14d} cycles  {out[i] / tot * 100:5.1f}%  "
                   f"{out[i] / args.steps / 148:10.0f} per CTA-step")
+        if out[7]:
+            print(f"distinct genome slots per controller warp-iteration: {out[6] / out[7]:.2f}")
 
 
 if __name__ == "__main__":
