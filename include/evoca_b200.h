@@ -96,6 +96,10 @@ EVO_API int evo_download_planes(evo_ctx* ctx, float* energy, float* infra, float
  * w2 (n,13,45), b2 (n,13). */
 EVO_API int evo_set_params(evo_ctx* ctx, int slot0, int n, const float* w1, const float* b1, const float* w2,
                            const float* b2);
+/* Inverse of evo_set_params: read slots [slot0, slot0+n) back in the same
+ * reference layouts (used after evo_express_cppn to sync the host pool's
+ * cached DenseParams, neuroevo.py:476). */
+EVO_API int evo_get_params(evo_ctx* ctx, int slot0, int n, float* w1, float* b1, float* w2, float* b2);
 /* Slot liveness (GenomePool slot states: 0 free, 1 live, 2 dead) and peak
  * populations, for the device census (neuroevo.py:521-542). */
 EVO_API int evo_set_slots(evo_ctx* ctx, const int8_t* state, const int32_t* peak);
@@ -140,6 +144,26 @@ EVO_API int evo_read_events(evo_ctx* ctx, int64_t capacity, int64_t* target, int
 /* Patch genome slots on the device front buffer after host radiation
  * (physics.py:389-392): n cells (local linear index) get slot values. */
 EVO_API int evo_patch_genomes(evo_ctx* ctx, const int64_t* cells, const int32_t* slots, int64_t n);
+
+/* Batched CPPN expression: replaces the per-admission host call
+ * hypernet.generate_network(genome, layout, tau, w_max) (hypernet.py:183-220,
+ * invoked through GenomePool.admit's net_factory, neuroevo.py:476) for n
+ * genomes at once, writing the dense tables of their pool slots on the
+ * device (the layouts evo_set_params fills).  hidden == 0 substrates get the
+ * direct 45->13 block (input -> actuator queries, biases from the bias
+ * signal).  Programs come from paper_2406_09654_b200.neat.compile_programs:
+ *   node_off [n+1]; nodes [node_off[n]][4] = {act (0 sine, 1 gaussian,
+ *   2 sigmoid, 3 tanh, 4 identity, 5 abs; -1 input), input position | -1,
+ *   edge begin, edge end}; edge_src (node position within the genome) and
+ *   edge_w (float64) per enabled edge in connection-list order; outs [n][2]
+ *   (weight-signal, bias-signal node positions); coords = neuron layout
+ *   (45 inputs, hidden, 13 actuators) x (u, v) as make_layout builds it
+ *   (hypernet.py:64-74).  All host pointers.  tau in [0, 1) and w_max > 0
+ *   as hypernet.py:195-198 requires (else EVO_EINVAL). */
+EVO_API int evo_express_cppn(evo_ctx* ctx, int n, const int32_t* slots, const int32_t* node_off,
+                             const int32_t* nodes, const int32_t* edge_src, const double* edge_w,
+                             const int32_t* outs, const double* coords, double tau, double w_max,
+                             void* stream);
 
 /* Device pointers of a plane (halo exchange / interop).  which: 0 energy,
  * 1 infra, 2 comm (3 planes, stride = plane_stride), 3 genome, 4 rotation,

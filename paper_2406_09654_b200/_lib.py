@@ -51,6 +51,7 @@ SIGNATURES = {
     "evo_upload_planes": [_P, _P, _P, _P, _P, _P, _P],
     "evo_download_planes": [_P, _P, _P, _P, _P, _P, _P],
     "evo_set_params": [_P, _I, _I, _P, _P, _P, _P],
+    "evo_get_params": [_P, _I, _I, _P, _P, _P, _P],
     "evo_set_slots": [_P, _P, _P],
     "evo_set_source_map": [_P, _P],
     "evo_step": [_P, C.POINTER(EvoScalars), _I64, _I, _I, _P],
@@ -67,6 +68,7 @@ SIGNATURES = {
     "evo_read_stats": [_P, C.POINTER(_I64), C.POINTER(_I64)],
     "evo_read_events": [_P, _I64, _P, _P, _P, _P, _P, _P, C.POINTER(_I64)],
     "evo_patch_genomes": [_P, _P, _P, _I64],
+    "evo_express_cppn": [_P, _I, _P, _P, _P, _P, _P, _P, _P, C.c_double, C.c_double, _P],
     "evo_plane_ptr": [_P, _I, _I, C.POINTER(_P), C.POINTER(_I64)],
     "evo_fnv1a64": [C.c_uint64, _P, _I64, C.POINTER(C.c_uint64)],
     "evo_debug_phase_cycles": [_P, _I],

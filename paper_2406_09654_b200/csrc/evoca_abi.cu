@@ -8,6 +8,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdio>
+#include <algorithm>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -57,6 +58,16 @@ struct evo_ctx {
   std::vector<void*> allocs;
 
   long long ncell() const { return (long long)W * H; }
+  evo::Params params() const {
+    evo::Params p;
+    p.hidden = hidden;
+    p.hpad = hpad;
+    p.wA = wA;
+    p.bA = bA;
+    p.wB = wB;
+    p.bB = bB;
+    return p;
+  }
   evo::StepGeom geom() const {
     evo::StepGeom g;
     g.W = W;
@@ -311,6 +322,48 @@ EVO_API int evo_set_params(evo_ctx* c, int slot0, int n, const float* w1, const 
   return 0;
 }
 
+EVO_API int evo_get_params(evo_ctx* c, int slot0, int n, float* w1, float* b1, float* w2, float* b2) {
+  if (int r = check_ctx(c)) return r;
+  if (slot0 < 0 || n < 0 || slot0 + n > c->cap) return fail(EVO_EINVAL, "slot range outside the pool capacity");
+  if (n == 0) return 0;
+  if (!w2 || !b2) return fail(EVO_EINVAL, "w2/b2 are required");
+  const int H = c->hidden;
+  if (H > 0 && (!w1 || !b1)) return fail(EVO_EINVAL, "w1/b1 are required for a hidden layer");
+  CK(cudaStreamSynchronize(c->stream));
+  if (H == 0) {
+    std::vector<float> w12((size_t)n * evo::kSensors * 12), wl((size_t)n * evo::kSensors), bt((size_t)n * evo::kOutPad);
+    CK(cudaMemcpy(w12.data(), c->wA + (size_t)slot0 * evo::kSensors * 12, w12.size() * 4, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(wl.data(), c->wB + (size_t)slot0 * evo::kSensors, wl.size() * 4, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(bt.data(), c->bA + (size_t)slot0 * evo::kOutPad, bt.size() * 4, cudaMemcpyDeviceToHost));
+    for (int s = 0; s < n; ++s)
+      for (int j = 0; j < evo::kActuators; ++j) {
+        for (int k = 0; k < evo::kSensors; ++k)
+          w2[((size_t)s * evo::kActuators + j) * evo::kSensors + k] =
+              j < 12 ? w12[((size_t)s * evo::kSensors + k) * 12 + j] : wl[(size_t)s * evo::kSensors + k];
+        b2[(size_t)s * evo::kActuators + j] = bt[(size_t)s * evo::kOutPad + j];
+      }
+    return 0;
+  }
+  const int hp = c->hpad;
+  std::vector<float> W1((size_t)n * evo::kSensors * hp), B1((size_t)n * hp);
+  std::vector<float> W2((size_t)n * hp * evo::kOutPad), B2((size_t)n * evo::kOutPad);
+  CK(cudaMemcpy(W1.data(), c->wA + (size_t)slot0 * evo::kSensors * hp, W1.size() * 4, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(B1.data(), c->bA + (size_t)slot0 * hp, B1.size() * 4, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(W2.data(), c->wB + (size_t)slot0 * hp * evo::kOutPad, W2.size() * 4, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(B2.data(), c->bB + (size_t)slot0 * evo::kOutPad, B2.size() * 4, cudaMemcpyDeviceToHost));
+  for (int s = 0; s < n; ++s) {
+    for (int h = 0; h < H; ++h) {
+      for (int k = 0; k < evo::kSensors; ++k)
+        w1[((size_t)s * H + h) * evo::kSensors + k] = W1[((size_t)s * evo::kSensors + k) * hp + h];
+      b1[(size_t)s * H + h] = B1[(size_t)s * hp + h];
+      for (int j = 0; j < evo::kActuators; ++j)
+        w2[((size_t)s * evo::kActuators + j) * H + h] = W2[((size_t)s * hp + h) * evo::kOutPad + j];
+    }
+    for (int j = 0; j < evo::kActuators; ++j) b2[(size_t)s * evo::kActuators + j] = B2[(size_t)s * evo::kOutPad + j];
+  }
+  return 0;
+}
+
 EVO_API int evo_set_slots(evo_ctx* c, const int8_t* state, const int32_t* peak) {
   if (int r = check_ctx(c)) return r;
   CK(cudaStreamSynchronize(c->stream));
@@ -561,6 +614,81 @@ EVO_API int evo_patch_genomes(evo_ctx* c, const int64_t* cells, const int32_t* s
   if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
   cudaFree(dc);
   cudaFree(ds);
+  CK(e);
+  return 0;
+}
+
+EVO_API int evo_express_cppn(evo_ctx* c, int n, const int32_t* slots, const int32_t* node_off,
+                             const int32_t* nodes, const int32_t* edge_src, const double* edge_w,
+                             const int32_t* outs, const double* coords, double tau, double w_max, void* stream) {
+  if (int r = check_ctx(c)) return r;
+  if (!(tau >= 0.0 && tau < 1.0)) return fail(EVO_EINVAL, "tau must be in [0, 1)");
+  if (!(w_max > 0.0)) return fail(EVO_EINVAL, "w_max must be positive");
+  if (n < 0) return fail(EVO_EINVAL, "negative genome count");
+  if (n == 0) return 0;
+  if (!slots || !node_off || !nodes || !outs || !coords) return fail(EVO_EINVAL, "null arrays");
+  // validate the programs on the host: node ranges, topological edges, outputs
+  if (node_off[0] != 0) return fail(EVO_EINVAL, "node_off[0] must be 0");
+  int max_nodes = 0;
+  int64_t n_edges = 0;
+  for (int g = 0; g < n; ++g) {
+    if (slots[g] < 0 || slots[g] >= c->cap) return fail(EVO_EINVAL, "slot outside the pool capacity");
+    const int a = node_off[g], b = node_off[g + 1];
+    if (b <= a) return fail(EVO_EINVAL, "empty or unordered program");
+    max_nodes = std::max(max_nodes, b - a);
+    for (int i = a; i < b; ++i) {
+      const int32_t* nd = nodes + 4 * (size_t)i;
+      if (nd[0] < -1 || nd[0] > 5) return fail(EVO_EINVAL, "unknown activation code");
+      if (nd[0] < 0 && (nd[1] < 0 || nd[1] > 4)) return fail(EVO_EINVAL, "input position outside 0..4");
+      if (nd[2] < 0 || nd[3] < nd[2]) return fail(EVO_EINVAL, "bad edge range");
+      n_edges = std::max<int64_t>(n_edges, nd[3]);
+      for (int e = nd[2]; e < nd[3]; ++e)
+        if (!edge_src || !edge_w || edge_src[e] < 0 || edge_src[e] >= i - a)
+          return fail(EVO_EINVAL, "edge source is not an earlier node of the same program");
+    }
+    if (outs[2 * g] < 0 || outs[2 * g] >= b - a || outs[2 * g + 1] < 0 || outs[2 * g + 1] >= b - a)
+      return fail(EVO_EINVAL, "output node outside the program");
+  }
+  if (evo::cppn_threads(max_nodes) == 0) return fail(EVO_EINVAL, "pattern network too large (> 384 nodes)");
+  const int ncoord = 2 * (evo::kSensors + c->hidden + evo::kActuators);
+  const int total_nodes = node_off[n];
+  // one staging allocation: ints | doubles
+  const size_t bi = ((size_t)n + (n + 1) + 4 * (size_t)total_nodes + (size_t)n_edges + 2 * (size_t)n) * 4;
+  const size_t bd = ((size_t)n_edges + ncoord) * 8;
+  const size_t off_d = (bi + 15) & ~(size_t)15;
+  cudaStream_t st = pick(c, stream);
+  char* dbuf = nullptr;
+  CK(cudaMalloc(&dbuf, off_d + bd));
+  std::vector<char> h(off_d + bd);
+  size_t o = 0;
+  auto put = [&](const void* src, size_t bytes) {
+    if (bytes) std::memcpy(h.data() + o, src, bytes);
+    o += bytes;
+  };
+  evo::CppnBatch b{};
+  b.n = n;
+  b.max_nodes = max_nodes;
+  b.tau = tau;
+  b.w_max = w_max;
+  b.nodes = reinterpret_cast<const int4*>(dbuf + o);  // first: int4 needs 16-byte alignment
+  put(nodes, (size_t)total_nodes * 16);
+  b.slots = reinterpret_cast<const int32_t*>(dbuf + o);
+  put(slots, (size_t)n * 4);
+  b.node_off = reinterpret_cast<const int32_t*>(dbuf + o);
+  put(node_off, (size_t)(n + 1) * 4);
+  b.edge_src = reinterpret_cast<const int32_t*>(dbuf + o);
+  put(edge_src, (size_t)n_edges * 4);
+  b.outs = reinterpret_cast<const int32_t*>(dbuf + o);
+  put(outs, (size_t)n * 8);
+  o = off_d;
+  b.edge_w = reinterpret_cast<const double*>(dbuf + o);
+  put(edge_w, (size_t)n_edges * 8);
+  b.coords = reinterpret_cast<const double*>(dbuf + o);
+  put(coords, (size_t)ncoord * 8);
+  cudaError_t e = cudaMemcpyAsync(dbuf, h.data(), h.size(), cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess) e = evo::launch_express_cppn(b, c->params(), c->wA, c->bA, c->wB, c->bB, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  cudaFree(dbuf);
   CK(e);
   return 0;
 }

@@ -108,6 +108,24 @@ struct Pass2Args {
   long long t;
 };
 
+// Batched CPPN expression (evoca_cppn.cu): device copies of the linearised
+// programs (paper_2406_09654_b200/neat.py:compile_programs).
+struct CppnBatch {
+  int n;                  // genomes
+  int max_nodes;          // largest program
+  const int32_t* slots;   // [n] destination pool slots
+  const int32_t* node_off;  // [n + 1]
+  const int4* nodes;      // {act | -1, input position | -1, edge begin, edge end}
+  const int32_t* edge_src;  // node position within the genome
+  const double* edge_w;
+  const int32_t* outs;    // [n][2] weight / bias signal node positions
+  const double* coords;   // (45 + hidden + 13) x 2 neuron coordinates
+  double tau, w_max;
+};
+
+int cppn_threads(int max_nodes);  // 0 -> program too large
+cudaError_t launch_express_cppn(const CppnBatch& b, const Params& net, float* wA, float* bA, float* wB, float* bB,
+                                cudaStream_t st);
 cudaError_t launch_pass1(const Pass1Args& a, bool inject, bool export_actions, cudaStream_t st);
 cudaError_t launch_pass2(const Pass2Args& a, cudaStream_t st);
 cudaError_t debug_phase_cycles(unsigned long long* out, bool reset);

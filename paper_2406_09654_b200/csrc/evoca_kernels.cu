@@ -362,7 +362,6 @@ __global__ void __launch_bounds__(kThreadsP, 1) k_pass1_direct(const Pass1Args a
     prefetch_tile(a, tile, tiles_x, pf);
     commit_tile(sm, pf);
   }
-  if (kSmemW) asm volatile("cp.async.wait_all;" ::: "memory");
   __syncthreads();
   long long t_mark = clock64();
   (void)t_mark;
@@ -374,6 +373,10 @@ __global__ void __launch_bounds__(kThreadsP, 1) k_pass1_direct(const Pass1Args a
     if (next < ntiles) prefetch_tile_l2(a, next, tiles_x);
     bucket_by_genome<kThreadsP, kPreCells, 2 * kUnitP, kUnitP>(sm.bins, sm.scratch, sm.gi, sm.order, &sm.n_units, a.capacity);
     PHASE_MARK(0);
+    if (kSmemW && tile == (int)blockIdx.x) {  // weight staging overlapped the first halo load + bucketing
+      asm volatile("cp.async.wait_all;" ::: "memory");
+      __syncthreads();
+    }
     tile_controller<kExport, false, kThreadsP, kUnitP, kSmemW>(a, sm, x0, y0, sW12, sW1, sB);
     __syncthreads();
     PHASE_MARK(1);

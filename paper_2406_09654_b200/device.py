@@ -15,7 +15,7 @@ import numpy as np
 
 from . import _lib
 from ._lib import check, ptr
-from .hypernet import N_ACTUATORS, pack_params
+from .hypernet import N_ACTUATORS, N_SENSORS, pack_params
 from .physics import AdoptionEvents
 
 __all__ = ["DeviceSubstrate"]
@@ -211,6 +211,34 @@ class DeviceSubstrate:
         cells = np.ascontiguousarray(cells, np.int64)
         slots = np.ascontiguousarray(slots, np.int32)
         check(self.lib.evo_patch_genomes(self.ctx, ptr(cells), ptr(slots), len(cells)))
+
+    def get_params_arrays(self, slot0: int, n: int):
+        """Read slots [slot0, slot0+n) back (evo_get_params): (w1, b1, w2, b2)
+        in the reference layouts; w1/b1 are None for a direct substrate."""
+        H = self.hidden
+        w1 = np.zeros((n, H, N_SENSORS), np.float32) if H else None
+        b1 = np.zeros((n, H), np.float32) if H else None
+        w2 = np.zeros((n, N_ACTUATORS, H if H else N_SENSORS), np.float32)
+        b2 = np.zeros((n, N_ACTUATORS), np.float32)
+        check(self.lib.evo_get_params(self.ctx, slot0, n, ptr(w1), ptr(b1), ptr(w2), ptr(b2)))
+        return w1, b1, w2, b2
+
+    def express_cppn(self, slots, genomes, tau: float = 0.2, w_max: float = 3.0, stream=None) -> None:
+        """Generate the dense tables of ``slots`` from their pattern networks
+        on the device (evo_express_cppn; reference generate_network,
+        hypernet.py:183-220).  ``genomes`` are reference or neat.CppnGenome
+        objects; returns once the tables are written."""
+        from . import neat
+
+        slots = np.ascontiguousarray(slots, np.int32)
+        if len(slots) != len(genomes):
+            raise ValueError("one genome per slot")
+        if len(slots) == 0:
+            return
+        node_off, nodes, esrc, ew, outs = neat.compile_programs(genomes)
+        coords = neat.layout_coords(self.hidden)
+        check(self.lib.evo_express_cppn(self.ctx, len(slots), ptr(slots), ptr(node_off), ptr(nodes), ptr(esrc),
+                                        ptr(ew), ptr(outs), ptr(coords), float(tau), float(w_max), _stream(stream)))
 
     def plane_ptr(self, which: str, buffer: int = 0):
         p = C.c_void_p()

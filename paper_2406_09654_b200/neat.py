@@ -1,0 +1,292 @@
+"""Host-side NEAT genome types, mutation and CPPN program linearisation.
+
+NEAT genetics stay on the host (north_star (6)); this module is the part of
+the reference's ``neuroevo`` the device path needs to feed the batched CPPN
+kernel:
+
+* ``NodeGene`` / ``ConnGene`` / ``CppnGenome`` with the reference's field
+  names (/root/reference/pkg/src/evoca/neuroevo.py:54-85), so reference
+  genomes are accepted unchanged;
+* ``mutate`` - the reference's variation operator restated step for step
+  (neuroevo.py:233-299: weight reset/perturb, toggles, add-connection,
+  add-node, in that fixed order and draw order), so a given Philox stream
+  yields the same child (pinned by tests/golden/cppn_cases.npz);
+* ``init_genome`` (neuroevo.py:212-230) and ``init_c3_genome``, the
+  BASELINE config-3 pattern network (4 coordinate inputs -> 8 hidden
+  sin/gauss/tanh nodes -> weight output, weights N(0,1));
+* ``topo_order`` (hypernet.py:100-125: Kahn with an id-sorted frontier over
+  the full gene graph) and ``compile_programs``, which lays a batch of
+  genomes out as the flat program arrays of ``evo_express_cppn``.
+"""
+
+from __future__ import annotations
+
+import heapq
+from dataclasses import dataclass, replace
+
+import numpy as np
+
+__all__ = [
+    "ACTIVATIONS",
+    "NodeGene",
+    "ConnGene",
+    "CppnGenome",
+    "InnovationCounter",
+    "EvolutionRates",
+    "init_genome",
+    "init_c3_genome",
+    "mutate",
+    "topo_order",
+    "compile_programs",
+    "layout_coords",
+    "stream",
+]
+
+ACTIVATIONS = ("sine", "gaussian", "sigmoid", "tanh", "identity", "abs")  # neuroevo.py:43
+ACT_CODE = {a: i for i, a in enumerate(ACTIVATIONS)}  # device activation codes (evoca_b200.h)
+N_INPUTS = 5
+INPUT_IDS = (0, 1, 2, 3, 4)
+OUTPUT_IDS = (5, 6)
+FIRST_FREE_NODE_ID = 7
+
+
+@dataclass(frozen=True)
+class NodeGene:
+    id: int
+    role: str  # "input" | "hidden" | "output"
+    activation: str
+
+
+@dataclass(frozen=True)
+class ConnGene:
+    innovation: int
+    src: int
+    dst: int
+    weight: float
+    enabled: bool
+
+
+@dataclass(frozen=True)
+class CppnGenome:
+    nodes: tuple
+    connections: tuple
+
+
+class InnovationCounter:
+    """Shared innovation / node-id source (neuroevo.py:151-171)."""
+
+    def __init__(self, next_innovation: int = 0, next_node_id: int = FIRST_FREE_NODE_ID):
+        self.next_innovation = next_innovation
+        self.next_node_id = next_node_id
+
+    def new_innovation(self) -> int:
+        n = self.next_innovation
+        self.next_innovation += 1
+        return n
+
+    def new_node_id(self) -> int:
+        n = self.next_node_id
+        self.next_node_id += 1
+        return n
+
+
+@dataclass
+class EvolutionRates:
+    """Variation probabilities (neuroevo.py:174-208 defaults)."""
+
+    weight_perturb_prob: float = 0.8
+    weight_perturb_sigma: float = 0.5
+    weight_reset_prob: float = 0.05
+    add_connection_prob: float = 0.05
+    add_node_prob: float = 0.03
+    toggle_enable_prob: float = 0.01
+
+
+def stream(master_seed: int, step: int, purpose: str, index: int = 0) -> np.random.Generator:
+    """Counter-based Philox stream keyed by a blake2b digest of the
+    derivation tuple (the reference's rng.stream, rng.py:19-33)."""
+    import hashlib
+    import struct
+
+    m = 0xFFFFFFFFFFFFFFFF
+    tag = purpose.encode("utf-8")
+    packed = (struct.pack("<QQ", master_seed & m, step & m) + struct.pack("<H", len(tag)) + tag
+              + struct.pack("<Q", index & m))
+    key = int.from_bytes(hashlib.blake2b(packed, digest_size=16).digest(), "little")
+    return np.random.Generator(np.random.Philox(key=key))
+
+
+def _base_nodes():
+    return tuple([NodeGene(i, "input", "identity") for i in INPUT_IDS]
+                 + [NodeGene(i, "output", "tanh") for i in OUTPUT_IDS])
+
+
+def init_genome(rng: np.random.Generator, counter: InnovationCounter) -> CppnGenome:
+    """Every input wired to both outputs, weights U[-1, 1) (neuroevo.py:212-230)."""
+    conns = []
+    for src in INPUT_IDS:
+        for dst in OUTPUT_IDS:
+            conns.append(ConnGene(counter.new_innovation(), src, dst, float(rng.uniform(-1.0, 1.0)), True))
+    return CppnGenome(_base_nodes(), tuple(conns))
+
+
+def init_c3_genome(rng: np.random.Generator, counter: InnovationCounter, hidden: int = 8) -> CppnGenome:
+    """BASELINE config 3 pattern network: the four
+    coordinate inputs feed ``hidden`` nodes whose activations cycle through
+    sine/gaussian/tanh, which feed the weight output; weights N(0, 1).  The
+    constant input and the bias output stay unconnected (bias signal
+    tanh(0) = 0 => biases 0) until mutation wires them."""
+    acts = ("sine", "gaussian", "tanh")
+    nodes = list(_base_nodes())
+    hid = []
+    for h in range(hidden):
+        nid = counter.new_node_id()
+        nodes.append(NodeGene(nid, "hidden", acts[h % 3]))
+        hid.append(nid)
+    conns = []
+    for nid in hid:
+        for src in INPUT_IDS[:4]:
+            conns.append(ConnGene(counter.new_innovation(), src, nid, float(rng.standard_normal()), True))
+    for nid in hid:
+        conns.append(ConnGene(counter.new_innovation(), nid, OUTPUT_IDS[0], float(rng.standard_normal()), True))
+    return CppnGenome(tuple(nodes), tuple(conns))
+
+
+def _creates_cycle(conns, src: int, dst: int) -> bool:
+    """Is ``src`` reachable from ``dst`` in the full gene graph (neuroevo.py:121-143)."""
+    if src == dst:
+        return True
+    out: dict = {}
+    for c in conns:
+        out.setdefault(c.src, []).append(c.dst)
+    stack, seen = [dst], {dst}
+    while stack:
+        n = stack.pop()
+        if n == src:
+            return True
+        for m in out.get(n, ()):
+            if m not in seen:
+                seen.add(m)
+                stack.append(m)
+    return False
+
+
+def mutate(genome, rates: EvolutionRates, rng: np.random.Generator, counter: InnovationCounter) -> CppnGenome:
+    """Mutated copy of ``genome`` (neuroevo.py:233-299), same operation and
+    draw order as the reference."""
+    conns = list(genome.connections)
+    nodes = list(genome.nodes)
+    for i, c in enumerate(conns):
+        if rng.random() < rates.weight_reset_prob:
+            conns[i] = replace(c, weight=float(rng.uniform(-1.0, 1.0)))
+        elif rng.random() < rates.weight_perturb_prob:
+            conns[i] = replace(c, weight=c.weight + float(rng.normal(0.0, rates.weight_perturb_sigma)))
+    for i, c in enumerate(conns):
+        if rng.random() < rates.toggle_enable_prob:
+            conns[i] = replace(c, enabled=not c.enabled)
+    if rng.random() < rates.add_connection_prob:
+        roles = {n.id: n.role for n in nodes}
+        taken = {(c.src, c.dst) for c in conns}
+        ordered = sorted(roles)
+        cands = [(s, d) for s in ordered if roles[s] != "output" for d in ordered
+                 if roles[d] != "input" and (s, d) not in taken and not _creates_cycle(conns, s, d)]
+        if cands:
+            s, d = cands[int(rng.integers(len(cands)))]
+            conns.append(ConnGene(counter.new_innovation(), s, d, float(rng.uniform(-1.0, 1.0)), True))
+    if rng.random() < rates.add_node_prob:
+        enabled = [i for i, c in enumerate(conns) if c.enabled]
+        if enabled:
+            pick = enabled[int(rng.integers(len(enabled)))]
+            old = conns[pick]
+            nid = counter.new_node_id()
+            act = ACTIVATIONS[int(rng.integers(len(ACTIVATIONS)))]
+            conns[pick] = replace(old, enabled=False)
+            nodes.append(NodeGene(nid, "hidden", act))
+            conns.append(ConnGene(counter.new_innovation(), old.src, nid, 1.0, True))
+            conns.append(ConnGene(counter.new_innovation(), nid, old.dst, old.weight, True))
+    return CppnGenome(tuple(nodes), tuple(conns))
+
+
+def topo_order(genome) -> list:
+    """Kahn's algorithm over the full gene graph (disabled edges included),
+    id-sorted frontier (hypernet.py:100-125)."""
+    indeg = {n.id: 0 for n in genome.nodes}
+    out: dict = {n.id: [] for n in genome.nodes}
+    for c in genome.connections:
+        indeg[c.dst] += 1
+        out[c.src].append(c.dst)
+    frontier = [n for n, d in indeg.items() if d == 0]
+    heapq.heapify(frontier)
+    order = []
+    while frontier:
+        n = heapq.heappop(frontier)
+        order.append(n)
+        for m in out[n]:
+            indeg[m] -= 1
+            if indeg[m] == 0:
+                heapq.heappush(frontier, m)
+    if len(order) != len(indeg):
+        raise ValueError("gene graph contains a cycle")
+    return order
+
+
+def layout_coords(hidden: int) -> np.ndarray:
+    """Neuron coordinates (45 sensors, ``hidden`` hidden, 13 actuators) x
+    (u, v) as the reference's make_layout builds them (hypernet.py:64-74),
+    float64, flattened for evo_express_cppn."""
+    slots = np.linspace(-1.0, 1.0, 9)
+    subs = np.linspace(-1.0, 1.0, 5)
+    inputs = np.array([(u, v) for u in slots for v in subs], dtype=np.float64)
+    parts = [inputs]
+    if hidden > 0:
+        parts.append(np.stack([np.linspace(-1.0, 1.0, hidden), np.zeros(hidden)], axis=1))
+    parts.append(np.stack([np.linspace(-1.0, 1.0, 13), np.zeros(13)], axis=1))
+    return np.ascontiguousarray(np.vstack(parts), np.float64)
+
+
+def compile_programs(genomes):
+    """Flatten a batch of genomes into ``evo_express_cppn`` programs.
+
+    Per genome, nodes in ``topo_order``; node record (int32 x4):
+    ``[act_code | -1 for inputs, input_position | -1, edge_begin, edge_end]``
+    (edges are global indices into ``edge_src`` / ``edge_w``); incoming
+    edges of a node are its ENABLED connections in connection-list order
+    (the reference's summation order, hypernet.py:140-153), ``edge_src`` is
+    the source node's position in the genome's own node list.  ``outs``
+    holds the positions of the two output nodes in ascending id order
+    (weight signal, bias signal; hypernet.py:154-155).
+    Returns (node_off int32 [n+1], nodes int32 [N,4], edge_src int32 [E],
+    edge_w float64 [E], outs int32 [n,2]).
+    """
+    node_off = [0]
+    nodes, edge_src, edge_w, outs = [], [], [], []
+    for gnm in genomes:
+        order = topo_order(gnm)
+        pos = {nid: i for i, nid in enumerate(order)}
+        role = {n.id: n for n in gnm.nodes}
+        input_pos = {nid: i for i, nid in enumerate(sorted(n.id for n in gnm.nodes if n.role == "input"))}
+        if len(input_pos) != N_INPUTS:
+            raise ValueError("a pattern network needs exactly five inputs")
+        incoming: dict = {}
+        for c in gnm.connections:
+            if c.enabled:
+                incoming.setdefault(c.dst, []).append(c)
+        for nid in order:
+            nd = role[nid]
+            if nd.role == "input":
+                nodes.append((-1, input_pos[nid], len(edge_src), len(edge_src)))
+                continue
+            if nd.activation not in ACT_CODE:
+                raise ValueError(f"unknown activation {nd.activation!r}")
+            b = len(edge_src)
+            for c in incoming.get(nid, ()):
+                edge_src.append(pos[c.src])
+                edge_w.append(float(c.weight))
+            nodes.append((ACT_CODE[nd.activation], -1, b, len(edge_src)))
+        out_ids = sorted(n.id for n in gnm.nodes if n.role == "output")
+        if len(out_ids) != 2:
+            raise ValueError("a pattern network needs exactly two outputs")
+        outs.append((pos[out_ids[0]], pos[out_ids[1]]))
+        node_off.append(len(nodes))
+    return (np.asarray(node_off, np.int32), np.asarray(nodes, np.int32).reshape(-1, 4),
+            np.asarray(edge_src, np.int32), np.asarray(edge_w, np.float64), np.asarray(outs, np.int32).reshape(-1, 2))

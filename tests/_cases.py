@@ -53,3 +53,48 @@ def step_net(z, hidden, genomes=8):
     w2 = np.stack([z[f"w2_{i}"] for i in range(genomes)])
     b2 = np.stack([z[f"b2_{i}"] for i in range(genomes)])
     return orc.Net(hidden, w2, b2, w1, b1)
+
+
+# -- CPPN fixtures (tests/golden/make_golden_cppn.py) ----------------------------------
+
+
+def cppn_doc():
+    import json
+
+    with open(os.path.join(GOLDEN, "cppn_genomes.json")) as f:
+        return json.load(f)
+
+
+def genome_from_json(d):
+    from paper_2406_09654_b200 import neat
+
+    nodes = tuple(neat.NodeGene(int(n["id"]), n["role"], n["act"]) for n in d["nodes"])
+    conns = tuple(neat.ConnGene(int(c["innov"]), int(c["from"]), int(c["to"]), float(c["w"]), bool(c["on"]))
+                  for c in d["conns"])
+    return neat.CppnGenome(nodes, conns)
+
+
+def cppn_genomes():
+    doc = cppn_doc()
+    return [genome_from_json(g) for g in doc["genomes"]], doc
+
+
+def run_program(prog, gi, queries):
+    """Evaluate genome ``gi`` of a compile_programs() batch exactly as the
+    device kernel does (node records in order, edges summed as
+    total = total + w * v starting from 0.0, float64 activations)."""
+    node_off, nodes, esrc, ew, outs = prog
+    acts = [np.sin, lambda x: np.exp(-np.square(x)), lambda x: 1.0 / (1.0 + np.exp(-x)), np.tanh,
+            lambda x: x, np.abs]
+    q = np.asarray(queries, np.float64)
+    vals = []
+    for r in nodes[node_off[gi]:node_off[gi + 1]]:
+        act, ipos, b, e = (int(v) for v in r)
+        if act < 0:
+            vals.append(q[:, ipos])
+            continue
+        total = np.zeros(len(q))
+        for k in range(b, e):
+            total = total + ew[k] * vals[esrc[k]]
+        vals.append(acts[act](total))
+    return np.stack([vals[outs[gi, 0]], vals[outs[gi, 1]]], axis=1)
