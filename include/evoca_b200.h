@@ -165,6 +165,22 @@ EVO_API int evo_express_cppn(evo_ctx* ctx, int n, const int32_t* slots, const in
                              const int32_t* outs, const double* coords, double tau, double w_max,
                              void* stream);
 
+/* Field radiation (BASELINE config 3 extension).
+ * evo_select_cells: every occupied cell of the front genome plane, in
+ * ascending index order, takes the next double of the host Philox stream
+ * whose 128-bit key is (key_hi:key_lo) - NumPy's Philox4x64-10, i.e.
+ * np.random.Generator(np.random.Philox(key=k)).random(n_occupied) with k the
+ * rng.stream(seed, t, "field_radiation") key (rng.py:19-33) - and is
+ * selected iff u < p.  The selection stays on the device; parent_counts
+ * (capacity, may be NULL) receives the number of selected cells per slot.
+ * evo_remap_selected then moves each selected cell from slot g to
+ * slot_map[g] (-1 keeps it), e.g. to the children the host admitted.
+ * evo_read_selected copies the selected cells (ascending) for inspection. */
+EVO_API int evo_select_cells(evo_ctx* ctx, uint64_t key_lo, uint64_t key_hi, double p, int32_t* parent_counts,
+                             int64_t* n_selected);
+EVO_API int evo_read_selected(evo_ctx* ctx, int64_t capacity, int64_t* cells, int64_t* n);
+EVO_API int evo_remap_selected(evo_ctx* ctx, const int32_t* slot_map);
+
 /* Device pointers of a plane (halo exchange / interop).  which: 0 energy,
  * 1 infra, 2 comm (3 planes, stride = plane_stride), 3 genome, 4 rotation,
  * 5 mid infra, 6 mid genome, 7 mid proposal byte, 8 mid quantity, 9 census

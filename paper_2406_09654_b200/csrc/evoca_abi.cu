@@ -53,6 +53,14 @@ struct evo_ctx {
   float* ev_q = nullptr;
   int32_t* ev_def = nullptr;
   float* src_map = nullptr;
+  // field-radiation selection (allocated on first use)
+  int32_t* sel_list = nullptr;
+  int32_t* sel_chunk_cnt = nullptr;
+  long long* sel_chunk_off = nullptr;
+  unsigned long long* sel_n = nullptr;
+  int32_t* sel_parent = nullptr;
+  int32_t* sel_map = nullptr;
+  bool have_select = false;
   bool have_export = false, have_events = false, have_src_map = false;
   cudaStream_t stream = nullptr;
   std::vector<void*> allocs;
@@ -690,6 +698,62 @@ EVO_API int evo_express_cppn(evo_ctx* c, int n, const int32_t* slots, const int3
   if (e == cudaSuccess) e = cudaStreamSynchronize(st);
   cudaFree(dbuf);
   CK(e);
+  return 0;
+}
+
+EVO_API int evo_select_cells(evo_ctx* c, uint64_t key_lo, uint64_t key_hi, double p, int32_t* parent_counts,
+                             int64_t* n_selected) {
+  if (int r = check_ctx(c)) return r;
+  if (!(p >= 0.0 && p <= 1.0)) return fail(EVO_EINVAL, "selection probability must be in [0, 1]");
+  if (c->strip) return fail(EVO_EINVAL, "field selection ranks cells over the whole torus: single-context only");
+  const long long n = c->ncell();
+  if (!c->sel_list) {
+    cudaError_t e;
+    if ((e = c->alloc(&c->sel_list, (size_t)n)) != cudaSuccess ||
+        (e = c->alloc(&c->sel_chunk_cnt, (size_t)evo::select_chunks(n) + 1)) != cudaSuccess ||
+        (e = c->alloc(&c->sel_chunk_off, (size_t)evo::select_chunks(n) + 1)) != cudaSuccess ||
+        (e = c->alloc(&c->sel_n, 1)) != cudaSuccess || (e = c->alloc(&c->sel_parent, (size_t)c->cap)) != cudaSuccess ||
+        (e = c->alloc(&c->sel_map, (size_t)c->cap)) != cudaSuccess)
+      return fail((int)e, std::string("selection buffers: ") + cudaGetErrorString(e));
+  }
+  CK(evo::launch_select_cells(c->buf[c->front].gi + c->W, n, key_lo, key_hi, p, c->sel_chunk_cnt, c->sel_chunk_off,
+                              c->sel_list, c->sel_n, c->sel_parent, c->cap, c->stream));
+  c->have_select = true;
+  unsigned long long ns = 0;
+  CK(cudaMemcpyAsync(&ns, c->sel_n, sizeof(ns), cudaMemcpyDeviceToHost, c->stream));
+  if (parent_counts)
+    CK(cudaMemcpyAsync(parent_counts, c->sel_parent, (size_t)c->cap * 4, cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  if (n_selected) *n_selected = (int64_t)ns;
+  return 0;
+}
+
+EVO_API int evo_read_selected(evo_ctx* c, int64_t capacity, int64_t* cells, int64_t* n) {
+  if (int r = check_ctx(c)) return r;
+  if (!c->have_select) return fail(EVO_EINVAL, "no selection: call evo_select_cells first");
+  unsigned long long ns = 0;
+  CK(cudaMemcpy(&ns, c->sel_n, sizeof(ns), cudaMemcpyDeviceToHost));
+  if (n) *n = (int64_t)ns;
+  if (!cells) return 0;
+  if ((long long)ns > capacity) return fail(EVO_EINVAL, "cells buffer too small");
+  std::vector<int32_t> tmp(ns);
+  CK(cudaMemcpy(tmp.data(), c->sel_list, ns * 4, cudaMemcpyDeviceToHost));
+  std::sort(tmp.begin(), tmp.end());
+  for (size_t i = 0; i < tmp.size(); ++i) cells[i] = tmp[i];
+  return 0;
+}
+
+EVO_API int evo_remap_selected(evo_ctx* c, const int32_t* slot_map) {
+  if (int r = check_ctx(c)) return r;
+  if (!c->have_select) return fail(EVO_EINVAL, "no selection: call evo_select_cells first");
+  if (!slot_map) return fail(EVO_EINVAL, "null slot map");
+  for (int i = 0; i < c->cap; ++i)
+    if (slot_map[i] < -1 || slot_map[i] >= c->cap) return fail(EVO_EINVAL, "slot map entry outside the pool");
+  CK(cudaMemcpyAsync(c->sel_map, slot_map, (size_t)c->cap * 4, cudaMemcpyHostToDevice, c->stream));
+  CK(evo::launch_remap_selected(c->buf[c->front].gi + c->W, c->sel_list, c->sel_n, c->sel_map, c->ncell(), c->stream));
+  CK(evo::launch_refresh_ghosts(c->buf[c->front], c->geom(), c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  c->have_select = false;  // the selection is consumed
   return 0;
 }
 

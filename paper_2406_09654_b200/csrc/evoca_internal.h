@@ -123,6 +123,12 @@ struct CppnBatch {
   double tau, w_max;
 };
 
+int select_chunks(long long n);
+cudaError_t launch_select_cells(const int32_t* gi, long long n, unsigned long long k0, unsigned long long k1, double p,
+                                int32_t* chunk_cnt, long long* chunk_off, int32_t* list, unsigned long long* n_sel,
+                                int32_t* parent_cnt, int capacity, cudaStream_t st);
+cudaError_t launch_remap_selected(int32_t* gi, const int32_t* list, const unsigned long long* n_sel,
+                                  const int32_t* map, long long max_n, cudaStream_t st);
 int cppn_threads(int max_nodes);  // 0 -> program too large
 cudaError_t launch_express_cppn(const CppnBatch& b, const Params& net, float* wA, float* bA, float* wB, float* bB,
                                 cudaStream_t st);

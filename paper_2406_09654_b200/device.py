@@ -240,6 +240,28 @@ class DeviceSubstrate:
         check(self.lib.evo_express_cppn(self.ctx, len(slots), ptr(slots), ptr(node_off), ptr(nodes), ptr(esrc),
                                         ptr(ew), ptr(outs), ptr(coords), float(tau), float(w_max), _stream(stream)))
 
+    def select_cells(self, key: int, p: float):
+        """Field-radiation selection on the front genome plane
+        (evo_select_cells): returns (per-slot selected counts, n selected)."""
+        counts = np.zeros(self.capacity, np.int32)
+        n = C.c_int64()
+        lo, hi = int(key) & 0xFFFFFFFFFFFFFFFF, (int(key) >> 64) & 0xFFFFFFFFFFFFFFFF
+        check(self.lib.evo_select_cells(self.ctx, lo, hi, float(p), ptr(counts), C.byref(n)))
+        return counts, n.value
+
+    def read_selected(self) -> np.ndarray:
+        n = C.c_int64()
+        check(self.lib.evo_read_selected(self.ctx, 0, None, C.byref(n)))
+        cells = np.zeros(max(n.value, 1), np.int64)
+        check(self.lib.evo_read_selected(self.ctx, len(cells), ptr(cells), C.byref(n)))
+        return cells[:n.value]
+
+    def remap_selected(self, slot_map) -> None:
+        slot_map = np.ascontiguousarray(slot_map, np.int32)
+        if slot_map.shape != (self.capacity,):
+            raise ValueError("slot map needs one entry per pool slot")
+        check(self.lib.evo_remap_selected(self.ctx, ptr(slot_map)))
+
     def plane_ptr(self, which: str, buffer: int = 0):
         p = C.c_void_p()
         stride = C.c_int64()

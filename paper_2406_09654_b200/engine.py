@@ -62,12 +62,23 @@ class EvolutionRates:
 
 
 @dataclass
+class FieldRadiationConfig:
+    """BASELINE config-3 extension: every ``every`` steps
+    a fraction ``p`` of occupied cells moves to freshly mutated children of
+    their genomes (radiation.field_radiation).  0 disables it."""
+
+    every: int = 0
+    p: float = 0.01
+
+
+@dataclass
 class ExperimentConfig:
     grid: GridConfig = field(default_factory=GridConfig)
     seed: int = 0
     physics: PhysicsParams = field(default_factory=PhysicsParams)
     evolution: EvolutionRates = field(default_factory=EvolutionRates)
     hypernet: HypernetConfig = field(default_factory=HypernetConfig)
+    field_radiation: FieldRadiationConfig = field(default_factory=FieldRadiationConfig)
 
 
 @dataclass
@@ -121,11 +132,26 @@ class _Binding:
         ver = getattr(pool, "version", None)
         if ver is not None and ver == self.pool_version:
             return
-        changed = []
+        from .radiation import DeviceExpressed
+
+        changed, express = [], []
         for slot in range(self.capacity):
             p = pool.params(slot)
             if p is not None and self.param_ids[slot] is not p:
-                changed.append(slot)
+                if isinstance(p, DeviceExpressed):
+                    express.append(slot)
+                else:
+                    changed.append(slot)
+        if express:  # admitted pattern networks: one batched device expression
+            ps = [pool.params(s) for s in express]
+            by_expr = {}
+            for s, p in zip(express, ps):
+                by_expr.setdefault((p.tau, p.w_max), []).append((s, p))
+            for (tau, w_max), items in by_expr.items():
+                self.dev.express_cppn([s for s, _ in items], [p.genome for _, p in items], tau, w_max)
+                for s, p in items:
+                    p.bind(self.dev, s)
+                    self.param_ids[s] = p
         # upload contiguous runs of changed slots
         i = 0
         while i < len(changed):
@@ -147,8 +173,12 @@ def _hidden_of(state) -> int:
     if hidden is None:
         raise ValueError("config.hypernet.hidden_size is required")
     # a reference config with DirectParams in the pool means the direct net
+    from .radiation import DeviceExpressed
+
     for slot in range(int(state.pool.capacity)):
         p = state.pool.params(slot)
+        if isinstance(p, DeviceExpressed):
+            return p.hidden
         if p is not None:
             if isinstance(p, DirectParams) or (hasattr(p, "w") and not hasattr(p, "w1")):
                 return 0
@@ -259,6 +289,12 @@ def step(state) -> None:
     state.last_adoptions = int(adoptions)
     state.last_extinctions = len(newly_dead)
     b.device_ahead = False
+    fr = getattr(state.config, "field_radiation", None)
+    if fr is not None and fr.every > 0 and sub.step_counter % fr.every == 0:
+        from .radiation import field_radiation
+
+        field_radiation(state, sub.step_counter, fr.p)
+        _download_front(state)  # keep the host mirror current in host-resident mode
 
 
 def _download_front(state) -> None:
@@ -320,6 +356,11 @@ def run(state, steps: int, hooks=(), should_stop: Optional[Callable[[], bool]] =
         b.dev.step_raw(step_scalars(t, phys), t, source_map=phys.energy_source_map)
         sub.step_counter = t + 1
         b.device_ahead = True
+        fr = getattr(state.config, "field_radiation", None)
+        if fr is not None and fr.every > 0 and sub.step_counter % fr.every == 0:
+            from .radiation import field_radiation
+
+            field_radiation(state, sub.step_counter, fr.p)
         due = [h for h in hooks if sub.step_counter % h.every == 0]
         if due:
             _download_front(state)
@@ -394,6 +435,7 @@ def baseline_state(name: str = "c2", seed: int = 0, width: int | None = None, he
     g = genomes or cfg.genomes
     ec = ExperimentConfig(grid=GridConfig(w, h), seed=seed, hypernet=HypernetConfig(cfg.hidden))
     ec.physics.cycle_period = cfg.cycle_period
+    ec.field_radiation = FieldRadiationConfig(cfg.radiation_every, cfg.radiation_p or 0.01)
     sub = create_substrate(w, h)
     E, I, Cm, gi, rot = synth_arrays(h, w, g, seed, cfg.sparse_infra)
     f = sub.front
@@ -402,7 +444,15 @@ def baseline_state(name: str = "c2", seed: int = 0, width: int | None = None, he
     f.channels["communication"][:] = Cm
     f.genome_index[:] = gi
     f.rotation[:] = rot
-    pool = SlotPool(g)
+    cap = max(cfg.capacity, g)
+    pool = SlotPool(cap)
+    genomes = [None] * g
+    if cfg.radiation_every:
+        from .radiation import device_net_factory
+        from .synth import synth_genomes
+
+        genomes, pool.innovations = synth_genomes(g, seed)
+        pool.net_factory = device_net_factory(cfg.hidden)
     for i, p in enumerate(synth_params(g, cfg.hidden, seed)):
-        pool.install(i, p)
+        pool.install(i, p, genome=genomes[i])
     return SimState(substrate=sub, pool=pool, config=ec, master_seed=seed)

@@ -40,6 +40,7 @@ __all__ = [
     "compile_programs",
     "layout_coords",
     "stream",
+    "stream_key",
 ]
 
 ACTIVATIONS = ("sine", "gaussian", "sigmoid", "tanh", "identity", "abs")  # neuroevo.py:43
@@ -102,9 +103,10 @@ class EvolutionRates:
     toggle_enable_prob: float = 0.01
 
 
-def stream(master_seed: int, step: int, purpose: str, index: int = 0) -> np.random.Generator:
-    """Counter-based Philox stream keyed by a blake2b digest of the
-    derivation tuple (the reference's rng.stream, rng.py:19-33)."""
+def stream_key(master_seed: int, step: int, purpose: str, index: int = 0) -> int:
+    """128-bit Philox key of the derivation tuple: blake2b-128 of
+    (seed, step, len(purpose), purpose, index) (the reference's rng.stream,
+    rng.py:19-33)."""
     import hashlib
     import struct
 
@@ -112,8 +114,12 @@ def stream(master_seed: int, step: int, purpose: str, index: int = 0) -> np.rand
     tag = purpose.encode("utf-8")
     packed = (struct.pack("<QQ", master_seed & m, step & m) + struct.pack("<H", len(tag)) + tag
               + struct.pack("<Q", index & m))
-    key = int.from_bytes(hashlib.blake2b(packed, digest_size=16).digest(), "little")
-    return np.random.Generator(np.random.Philox(key=key))
+    return int.from_bytes(hashlib.blake2b(packed, digest_size=16).digest(), "little")
+
+
+def stream(master_seed: int, step: int, purpose: str, index: int = 0) -> np.random.Generator:
+    """Counter-based Philox stream of the derivation tuple (rng.py:19-33)."""
+    return np.random.Generator(np.random.Philox(key=stream_key(master_seed, step, purpose, index)))
 
 
 def _base_nodes():

@@ -27,13 +27,20 @@ class SlotRecord:
     birth_step: int
     death_step: Optional[int] = None
     peak_population: int = 0
+    parents: tuple = ()
 
 
 class SlotPool:
-    def __init__(self, capacity: int):
+    def __init__(self, capacity: int, net_factory=None, counter=None):
         if capacity < 1:
             raise ValueError("pool capacity must be positive")
+        from .neat import InnovationCounter
+
         self.capacity = capacity
+        self.net_factory = net_factory
+        self.innovations = counter if counter is not None else InnovationCounter()
+        self._genomes = [None] * capacity
+        self._death = np.full(capacity, -1, np.int64)
         self._params = [None] * capacity
         self._state = np.zeros(capacity, np.int8)  # 0 free, 1 live, 2 dead
         self._lineage = np.full(capacity, -1, np.int64)
@@ -41,11 +48,13 @@ class SlotPool:
         self.next_lineage_id = 0
         self.version = 0  # bumped on every params/liveness change
 
-    def install(self, slot: int, params, birth_step: int = 0) -> int:
-        """Put a parameter set in a slot and mark it live (admission without NEAT)."""
+    def install(self, slot: int, params, birth_step: int = 0, genome=None) -> int:
+        """Put a parameter set (and optionally its pattern network) in a slot
+        and mark it live (admission without NEAT)."""
         if not 0 <= slot < self.capacity:
             raise ValueError("slot outside the pool capacity")
         self._params[slot] = params
+        self._genomes[slot] = genome
         self._state[slot] = 1
         lid = self.next_lineage_id
         self.next_lineage_id += 1
@@ -56,6 +65,44 @@ class SlotPool:
 
     def params(self, slot: int):
         return self._params[slot]
+
+    def genome(self, slot: int):
+        g = self._genomes[slot]
+        if g is None:
+            raise KeyError(f"slot {slot} has no genome")
+        return g
+
+    def set_genome(self, slot: int, genome) -> None:
+        self._genomes[slot] = genome
+
+    # -- admission (GenomePool.can_admit / admit, neuroevo.py:451-487) ----------
+
+    def can_admit(self) -> bool:
+        return bool(np.any(self._state != 1))
+
+    def admit(self, genome, parents: tuple = (), birth_step: int = 0) -> Optional[int]:
+        """Lowest free slot, else evict the dead slot with the oldest death
+        step (lowest index on ties); None when every slot is live.  Params come
+        from ``net_factory(genome)`` (e.g. a device-expression placeholder)."""
+        free = np.flatnonzero(self._state == 0)
+        if len(free):
+            idx = int(free[0])
+        else:
+            dead = np.flatnonzero(self._state == 2)
+            if not len(dead):
+                return None
+            idx = int(dead[np.lexsort((dead, self._death[dead]))[0]])
+        params = self.net_factory(genome) if self.net_factory is not None else None
+        self._genomes[idx] = genome
+        self._params[idx] = params
+        self._state[idx] = 1
+        self._death[idx] = -1
+        lid = self.next_lineage_id
+        self.next_lineage_id += 1
+        self._lineage[idx] = lid
+        self.records[lid] = SlotRecord(lid, idx, birth_step, parents=tuple(parents))
+        self.version += 1
+        return idx
 
     def is_live(self, slot: int) -> bool:
         return 0 <= slot < self.capacity and self._state[slot] == 1
@@ -92,6 +139,7 @@ class SlotPool:
             rec = self.records[int(self._lineage[i])]
             if c == 0:
                 self._state[i] = 2
+                self._death[i] = step
                 rec.death_step = step
                 dead.append(int(i))
             elif c > rec.peak_population:
@@ -109,6 +157,7 @@ class SlotPool:
                 rec.peak_population = int(peak[i])
             if state[i] == 2:
                 self._state[i] = 2
+                self._death[i] = int(death_step[i])
                 rec.death_step = int(death_step[i])
                 dead.append(int(i))
         return dead

@@ -1,0 +1,117 @@
+"""Radiation feed on the device path.
+
+Host NEAT (mutation, crossover, pool admission) stays on the host
+(north_star (6)); what moves to the GPU is everything around it:
+
+* ``DeviceExpressed`` - the params object a pool's ``net_factory`` returns
+  for an admitted genome (GenomePool.admit, neuroevo.py:476).  The engine
+  turns every such slot into ONE batched ``evo_express_cppn`` launch (the
+  reference calls hypernet.generate_network per admission on the CPU,
+  hypernet.py:183-220); the host tables are fetched lazily, only if someone
+  reads ``.w1``/``.w`` etc.  ``use_device_expression(state)`` installs it, so
+  the reference's own ``apply_radiation`` (physics.py:346-392), run on the
+  device-compacted adoption events, admits children whose weights are
+  generated on the GPU.
+* ``field_radiation`` - the BASELINE config-3 extension:
+  every ``every`` steps, 1 % of occupied cells (device draw from the host
+  Philox stream ``rng.stream(seed, t, "field_radiation")``, rng.py:19-33) are
+  selected; one child per distinct parent slot is mutated on the host
+  (``neat.mutate`` with ``stream(seed, t, "mutate", parent)``), admitted, its
+  weights generated on the device, and the selected cells move to it.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from . import neat
+
+__all__ = ["DeviceExpressed", "device_net_factory", "use_device_expression", "stream_key", "field_radiation"]
+
+
+stream_key = neat.stream_key
+
+
+class DeviceExpressed:
+    """Dense params of a pattern network, generated on the device.
+
+    Reads of the table attributes (DenseParams ``w1, b1, w2, b2`` for a
+    hidden-layer substrate, DirectParams ``w, b`` for the direct one) pull
+    the slot's tables back with ``evo_get_params``."""
+
+    def __init__(self, genome, hidden: int, tau: float = 0.2, w_max: float = 3.0):
+        self.genome = genome
+        self.hidden = int(hidden)
+        self.tau = float(tau)
+        self.w_max = float(w_max)
+        self._dev = None
+        self._slot = None
+        self._tables = None
+
+    @property
+    def expressed(self) -> bool:
+        return self._dev is not None
+
+    def bind(self, dev, slot: int) -> None:
+        self._dev, self._slot, self._tables = dev, int(slot), None
+
+    def _fetch(self):
+        if self._tables is None:
+            if self._dev is None:
+                raise RuntimeError("params not generated yet: the engine expresses them at its next step")
+            w1, b1, w2, b2 = self._dev.get_params_arrays(self._slot, 1)
+            self._tables = (None if w1 is None else w1[0], None if b1 is None else b1[0], w2[0], b2[0])
+        return self._tables
+
+    def __getattr__(self, name):
+        # only the table attributes are synthesised; anything else is absent
+        if name in ("w1", "b1", "w2", "b2") and self.__dict__.get("hidden", 0) > 0:
+            return self._fetch()[("w1", "b1", "w2", "b2").index(name)]
+        if name in ("w", "b") and self.__dict__.get("hidden", 1) == 0:
+            return self._fetch()[2 if name == "w" else 3]
+        raise AttributeError(name)
+
+
+def device_net_factory(hidden: int, tau: float = 0.2, w_max: float = 3.0):
+    def factory(genome):
+        return DeviceExpressed(genome, hidden, tau, w_max)
+
+    return factory
+
+
+def use_device_expression(state, tau: float = 0.2, w_max: float = 3.0) -> None:
+    """Route the pool's admissions through the device CPPN kernel."""
+    from .engine import _hidden_of
+
+    state.pool.net_factory = device_net_factory(_hidden_of(state), tau, w_max)
+
+
+def field_radiation(state, t: int, p: float = 0.01, rates: neat.EvolutionRates | None = None,
+                    purpose: str = "field_radiation") -> dict:
+    """One config-3 radiation event on the state's device front (call between
+    steps).  Returns {"selected", "parents", "children"}."""
+    from .engine import _binding, _fold_census
+
+    b = _binding(state)
+    dev = b.dev
+    pool = state.pool
+    _fold_census(state)  # admission must see the device's deaths (slot states, peaks)
+    rates = rates or neat.EvolutionRates()
+    counts, n_sel = dev.select_cells(stream_key(state.master_seed, t, purpose), p)
+    parents = np.flatnonzero(counts)
+    slot_map = np.full(pool.capacity, -1, np.int32)
+    children = []
+    for par in parents:
+        par = int(par)
+        if not pool.can_admit():
+            break
+        child = neat.mutate(pool.genome(par), rates, neat.stream(state.master_seed, t, "mutate", par), pool.innovations)
+        slot = pool.admit(child, parents=(pool.lineage(par),), birth_step=t)
+        if slot is None:
+            break
+        slot_map[par] = slot
+        children.append(slot)
+    b.sync_params(pool)  # one batched evo_express_cppn for every new slot
+    dev.remap_selected(slot_map)
+    b.device_ahead = True
+    return {"selected": int(n_sel), "parents": len(parents), "children": len(children)}

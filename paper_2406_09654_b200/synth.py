@@ -18,7 +18,7 @@ import numpy as np
 
 from .hypernet import DenseParams, DirectParams
 
-__all__ = ["BaselineConfig", "BASELINE_CONFIGS", "synth_arrays", "synth_params"]
+__all__ = ["BaselineConfig", "BASELINE_CONFIGS", "synth_arrays", "synth_params", "synth_genomes"]
 
 
 @dataclass(frozen=True)
@@ -31,14 +31,18 @@ class BaselineConfig:
     steps: int
     sparse_infra: bool = False
     cycle_period: int = 20
+    capacity: int = 0          # pool capacity (0: = genomes)
+    radiation_every: int = 0   # field radiation period (config 3)
+    radiation_p: float = 0.0   # fraction of occupied cells irradiated
 
 
-# BASELINE.json "configs" (radiation of config 3 and the multi-GPU layouts of
-# configs 4/5 are handled by the callers).
+# BASELINE.json "configs" (the multi-GPU layouts of configs 4/5 are handled
+# by the callers; config 3's radiation by radiation.field_radiation).
 BASELINE_CONFIGS = {
     "c1": BaselineConfig("c1-64x64-g8-direct", 64, 64, 8, 0, 100),
     "c2": BaselineConfig("c2-1024x1024-g64-direct", 1024, 1024, 64, 0, 1000),
-    "c3": BaselineConfig("c3-4096x4096-g256-direct", 4096, 4096, 256, 0, 1000),
+    "c3": BaselineConfig("c3-4096x4096-g256-direct-rad50", 4096, 4096, 256, 0, 1000, capacity=2048,
+                         radiation_every=50, radiation_p=0.01),
     "c4": BaselineConfig("c4-16384x16384-g1024-direct", 16384, 16384, 1024, 0, 500),
     "c5": BaselineConfig("c5-32768x32768-g4096-h128", 32768, 32768, 4096, 128, 200, sparse_infra=True),
 }
@@ -68,3 +72,13 @@ def synth_params(genomes: int, hidden: int = 0, seed: int = 0):
         w2 = (g.standard_normal((13, hidden)) * 0.3).astype(np.float32)
         out.append(DenseParams(w1, np.zeros(hidden, np.float32), w2, np.zeros(13, np.float32)))
     return out
+
+
+def synth_genomes(genomes: int, seed: int = 0, counter=None):
+    """Config-3 pattern networks, one per initial slot, from default_rng(seed+2)
+    (neat.init_c3_genome)."""
+    from .neat import InnovationCounter, init_c3_genome
+
+    g = np.random.default_rng(seed + 2)
+    counter = counter if counter is not None else InnovationCounter()
+    return [init_c3_genome(g, counter) for _ in range(genomes)], counter
