@@ -61,6 +61,12 @@ struct evo_ctx {
   int32_t* sel_parent = nullptr;
   int32_t* sel_map = nullptr;
   bool have_select = false;
+  // tensor-core hidden-layer controller buffers (allocated on first use)
+  evo::HidBuffers hid = {};
+  int num_sms = 0;
+  // rows / flags evo_get_actions reads (act_out, or hid.act after a tensor-core step)
+  const float* exp_rows = nullptr;
+  const uint8_t* exp_flag = nullptr;
   bool have_export = false, have_events = false, have_src_map = false;
   cudaStream_t stream = nullptr;
   std::vector<void*> allocs;
@@ -208,6 +214,22 @@ int ensure_actions_out(evo_ctx* c) {
   if (c->act_out) return 0;
   CK(c->alloc(&c->act_out, (size_t)c->ncell() * evo::kActuators));
   CK(c->alloc(&c->act_out_flag, (size_t)c->ncell()));
+  return 0;
+}
+
+int ensure_hidden_tc(evo_ctx* c) {
+  if (c->hid.sens) return 0;
+  const size_t n = (size_t)c->ncell(), cap = (size_t)c->cap;
+  CK(c->alloc(&c->hid.counts, cap));
+  CK(c->alloc(&c->hid.offs, cap + 1));
+  CK(c->alloc(&c->hid.tiles, cap + 1));
+  CK(c->alloc(&c->hid.cursor, cap));
+  CK(c->alloc(&c->hid.n_tiles, 1));
+  CK(c->alloc(&c->hid.rowcell, n));
+  CK(c->alloc(&c->hid.act, n * evo::kActuators));
+  CK(c->alloc(&c->hid.flag, n));
+  CK(c->alloc(&c->hid.sens, n * 48));
+  if (!c->num_sms) CK(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, c->device));
   return 0;
 }
 
@@ -402,12 +424,23 @@ EVO_API int evo_pass1(evo_ctx* c, const evo_scalars* s, int64_t t, int phases, i
   if (!s) return fail(EVO_EINVAL, "null scalars");
   (void)t;
   const bool inject = flags & EVO_F_INJECT_ACTIONS;
-  const bool exp = (flags & EVO_F_EXPORT_ACTIONS) && !inject;
+  bool exp = (flags & EVO_F_EXPORT_ACTIONS) && !inject;
   if (inject && !c->act_in) return fail(EVO_EINVAL, "EVO_F_INJECT_ACTIONS without evo_set_actions");
-  if (exp) {
+  // hidden-layer nets run on the tensor cores (sense -> genome buckets ->
+  // tcgen05 3xTF32 MLP -> actuator rows), the physics as pass 1 with those rows
+  const bool tc_net = !inject && c->hidden > 0 && evo::hidden_tc_supported(c->hidden) &&
+                      !(flags & EVO_F_CUDA_CORE_NET);
+  if (exp && !tc_net) {
     if (int r = ensure_actions_out(c)) return r;
   }
-  c->have_export = exp;
+  if (tc_net) {
+    if (int r = ensure_hidden_tc(c)) return r;
+    CK(evo::launch_hidden_tc(c->hid, c->geom(), c->buf[c->front], c->params(), c->cap, c->num_sms,
+                             pick(c, stream)));
+  }
+  c->have_export = exp || tc_net;
+  c->exp_rows = tc_net ? c->hid.act : c->act_out;
+  c->exp_flag = tc_net ? c->hid.flag : c->act_out_flag;
   evo::Pass1Args a;
   a.g = c->geom();
   a.front = c->buf[c->front];
@@ -422,13 +455,13 @@ EVO_API int evo_pass1(evo_ctx* c, const evo_scalars* s, int64_t t, int phases, i
   a.s = to_scalars(*s);
   a.phases = phases;
   a.src_map = c->have_src_map ? c->src_map : nullptr;
-  a.act_in = c->act_in;
-  a.act_flag = c->act_in_flag;
+  a.act_in = tc_net ? c->hid.act : c->act_in;
+  a.act_flag = tc_net ? c->hid.flag : c->act_in_flag;
   a.act_out = c->act_out;
   a.act_out_flag = c->act_out_flag;
   a.capacity = c->cap;
   a.stats = c->census.stats;
-  CK(evo::launch_pass1(a, inject, exp, pick(c, stream)));
+  CK(evo::launch_pass1(a, inject || tc_net, exp && !tc_net, pick(c, stream)));
   return 0;
 }
 
@@ -521,14 +554,14 @@ EVO_API int evo_set_actions(evo_ctx* c, const int64_t* cells, int64_t n, const f
 EVO_API int evo_get_actions(evo_ctx* c, int64_t capacity, int64_t* cells, float* acts, int64_t* n) {
   if (int r = check_ctx(c)) return r;
   if (!n) return fail(EVO_EINVAL, "n is null");
-  if (!c->have_export || !c->act_out) return fail(EVO_EINVAL, "no exported actions (step with EVO_F_EXPORT_ACTIONS)");
+  if (!c->have_export || !c->exp_rows) return fail(EVO_EINVAL, "no exported actions (step with EVO_F_EXPORT_ACTIONS)");
   CK(cudaStreamSynchronize(c->stream));
   CK(cudaDeviceSynchronize());
   const long long nc = c->ncell();
   std::vector<uint8_t> flag((size_t)nc);
   std::vector<float> rows((size_t)nc * evo::kActuators);
-  CK(cudaMemcpy(flag.data(), c->act_out_flag, (size_t)nc, cudaMemcpyDeviceToHost));
-  CK(cudaMemcpy(rows.data(), c->act_out, rows.size() * 4, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(flag.data(), c->exp_flag, (size_t)nc, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(rows.data(), c->exp_rows, rows.size() * 4, cudaMemcpyDeviceToHost));
   int64_t m = 0;
   for (long long i = 0; i < nc; ++i) {
     if (!flag[(size_t)i]) continue;

@@ -123,6 +123,24 @@ struct CppnBatch {
   double tau, w_max;
 };
 
+// Hidden-layer controller on tcgen05 (evoca_hidden_tc.cu): per-step buffers.
+struct HidBuffers {
+  int32_t* counts;   // [cap]
+  int32_t* offs;     // [cap + 1]
+  int32_t* tiles;    // [cap + 1]
+  int32_t* cursor;   // [cap]
+  int32_t* n_tiles;  // [1]
+  float* sens;       // [ncell][48]
+  int32_t* rowcell;  // [ncell]
+  float* act;        // [ncell][13] actuator rows (consumed as injected actions)
+  uint8_t* flag;     // [ncell]
+};
+bool hidden_tc_supported(int hidden);
+int hidden_tc_nh(int hidden);
+size_t hidden_tc_smem(int hidden);
+cudaError_t launch_hidden_tc(const HidBuffers& b, const StepGeom& g, const Planes& front, const Params& net,
+                             int capacity, int num_sms, cudaStream_t st);
+
 int select_chunks(long long n);
 cudaError_t launch_select_cells(const int32_t* gi, long long n, unsigned long long k0, unsigned long long k1, double p,
                                 int32_t* chunk_cnt, long long* chunk_off, int32_t* list, unsigned long long* n_sel,

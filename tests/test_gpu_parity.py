@@ -448,3 +448,46 @@ def test_census_deaths_tracked_on_device():
     assert counts[5] == 0 and state[5] == 2 and death[5] == 1
     assert dev.read_stats()[1] >= 1
     assert (peak[:5] == counts[:5]).all()
+
+
+# -- hidden-layer controller on the tensor cores (tcgen05 3xTF32) ----------------------------
+
+
+def _actions(dev, t, params, flags=0):
+    dev.step_raw(physics.step_scalars(t, params), t, flags=_lib.F_EXPORT_ACTIONS | flags)
+    return dev.get_actions()
+
+
+@pytest.mark.parametrize("hidden,genomes,shape", [(128, 300, (96, 80)), (16, 7, (33, 70)), (64, 1, (40, 40)),
+                                                  (128, 2, (1, 300))])
+def test_tensor_core_net_vs_oracle_and_cuda_core(hidden, genomes, shape):
+    """BASELINE config-5 net shape (45->128 tanh->13, N(0,0.3), sparse infra)
+    and odd shapes: many genomes with 1-cell groups, a single genome spanning
+    several 128-row tiles with a partial last tile, a 1-row torus.  Device
+    actions vs the oracle's float64 forward within 1e-5 relative, and the
+    physics bit-exact given them; the CUDA-core FP32 path as a cross-check."""
+    h, w = shape
+    p0 = orc.synth_planes(h, w, genomes, seed=hidden + genomes, sparse_infra=True)
+    net = orc.synth_net(genomes, hidden, seed=3)
+    phys = orc.Phys(cycle_period=20)
+    params = oracle_phys_to_params(phys)
+    oa = orc.act(p0, net)
+    dev = make_dev(p0, genomes, net)
+    cells, acts = _actions(dev, 0, params)
+    assert np.array_equal(cells, oa.cells)
+    assert rel_err(acts, oa.a) <= TOL
+    ref = orc.step(p0, 0, net, phys, acts=orc.Actions(cells, acts))
+    assert download(dev).equal(ref.planes)
+    dev.close()
+    dev = make_dev(p0, genomes, net)
+    cells2, acts2 = _actions(dev, 0, params, _lib.F_CUDA_CORE_NET)
+    assert np.array_equal(cells2, cells) and rel_err(acts2, oa.a) <= TOL
+    dev.close()
+
+
+def test_tensor_core_net_free_running_matches_oracle():
+    """A few device-resident steps of a hidden-128 world against the oracle
+    (tier A per step with the device's own actions)."""
+    p0 = orc.synth_planes(64, 64, 40, seed=11, sparse_infra=True)
+    net = orc.synth_net(40, 128, seed=11)
+    _step_vs_oracle(p0, net, orc.Phys(cycle_period=20), steps=4)
