@@ -140,8 +140,8 @@ int create_impl(evo_ctx** out, int width, int height, long long row0, int hg, in
   if (hidden < 0 || hidden > 1024) return fail(EVO_EINVAL, "hidden size must be in [0, 1024]");
   if (hg < height || row0 < 0 || row0 + height > hg) return fail(EVO_EINVAL, "strip outside the global torus");
   if ((long long)width * hg >= 0xFFFFFFFFLL) return fail(EVO_EINVAL, "grid exceeds 2^32-1 cells");
-  if ((long long)(height + 2) * width >= (1LL << 31))
-    return fail(EVO_EINVAL, "strip exceeds 2^31 cells per plane: split it over more strips");
+  if ((long long)(height + 2) * width >= 0x7F800000LL)
+    return fail(EVO_EINVAL, "strip exceeds 2^31 - 2^23 cells per plane: split it over more strips");
   if (strip && height < 1) return fail(EVO_EINVAL, "strip needs at least one row");
   evo_ctx* c = new evo_ctx();
   c->device = device;
@@ -225,7 +225,8 @@ int ensure_hidden_tc(evo_ctx* c) {
   CK(c->alloc(&c->hid.tiles, cap + 1));
   CK(c->alloc(&c->hid.cursor, cap));
   CK(c->alloc(&c->hid.n_tiles, 1));
-  CK(c->alloc(&c->hid.rowcell, n));
+  CK(c->alloc(&c->hid.cta_hist, (size_t)evo::hidden_sort_ctas(c->ncell()) * cap));
+  CK(c->alloc(&c->hid.tile_slot, n / 128 + cap + 1));
   CK(c->alloc(&c->hid.act, n * evo::kActuators));
   CK(c->alloc(&c->hid.flag, n));
   CK(c->alloc(&c->hid.sens, n * 48));

@@ -44,17 +44,41 @@ constexpr int kTmemCols = 512;
 // matches (layer 1) or beats (layer 2) a sequential FP32 FMA chain.
 constexpr int kL1StepsPerAcc = 2;
 
-__global__ void k_hid_count(const int32_t* gi, long long n, int cap, int32_t* counts) {
+// Deterministic counting sort of the occupied cells by slot, without hot
+// global atomics: each CTA owns a contiguous chunk of kSortChunk cells,
+// histograms it in shared memory and writes the histogram out; a column scan
+// turns the per-CTA histograms into per-CTA row bases; the sense pass then
+// ranks cells inside the CTA with shared-memory atomics.
+constexpr int kSortChunk = 16384;
+constexpr int kSortThreads = 256;
+
+__global__ void k_hid_count(const int32_t* gi, long long n, int cap, int32_t* cta_hist) {
   extern __shared__ int hist[];
   for (int b = threadIdx.x; b < cap; b += blockDim.x) hist[b] = 0;
   __syncthreads();
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+  const long long c0 = (long long)blockIdx.x * kSortChunk, c1 = min(n, c0 + kSortChunk);
+  for (long long i = c0 + threadIdx.x; i < c1; i += blockDim.x) {
     const int g = gi[i];
     if (g >= 0) atomicAdd(&hist[g], 1);
   }
   __syncthreads();
-  for (int b = threadIdx.x; b < cap; b += blockDim.x)
-    if (hist[b]) atomicAdd(&counts[b], hist[b]);
+  int32_t* out = cta_hist + (size_t)blockIdx.x * cap;
+  for (int b = threadIdx.x; b < cap; b += blockDim.x) out[b] = hist[b];
+}
+
+// per slot: exclusive scan of the per-CTA counts over CTAs (in place) and the
+// slot total
+__global__ void k_hid_colscan(int32_t* cta_hist, int nctas, int cap, int32_t* counts) {
+  const int g = blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= cap) return;
+  int run = 0;
+  for (int c = 0; c < nctas; ++c) {
+    int32_t* p = cta_hist + (size_t)c * cap + g;
+    const int v = *p;
+    *p = run;
+    run += v;
+  }
+  counts[g] = run;
 }
 
 // exclusive scans of counts (cells) and ceil(counts / 128) (tiles); one CTA
@@ -103,42 +127,88 @@ __global__ void k_hid_scan(const int32_t* counts, int cap, int32_t* offs, int32_
   }
 }
 
-__global__ void k_hid_sense(const StepGeom g, const Planes f, const int32_t* offs, int32_t* cursor, float* sens,
-                            int32_t* rowcell, uint8_t* flag) {
-  const long long n = (long long)g.W * g.H;
-  const long long st = g.stride;
-  for (long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x; c < n; c += (long long)gridDim.x * blockDim.x) {
-    const int y = (int)(c / g.W), x = (int)(c - (long long)y * g.W);
-    const long long self = (long long)(y + 1) * g.W + x;
-    const int slot = f.gi[self];
-    if (slot < 0) {
-      flag[c] = 0;
-      continue;
-    }
-    const int rank = offs[slot] + atomicAdd(&cursor[slot], 1);
-    rowcell[rank] = (int32_t)c;
-    const int rot = f.rot[self];
-    float v[kK1];
+// Sensor rows.  Element 45 of a row carries the cell index (its bit
+// pattern; rows' pad columns meet zero weights, and index bits below
+// 0x7F800000 are finite floats, evo_create bounds the strip), so the net
+// kernel needs no separate row -> cell map.  Rows are assembled per warp in
+// shared memory and written out cooperatively (12 lanes per 192-byte row)
+// so that every store instruction covers whole 32-byte sectors.
+constexpr int kRowPitch = 49;  // floats per staged row (bank-conflict padding)
+
+__global__ void __launch_bounds__(kSortThreads) k_hid_sense(const StepGeom g, const Planes f, const int32_t* offs,
+                                                            const int32_t* cta_base, int cap, float* sens,
+                                                            uint8_t* flag) {
+  extern __shared__ int cursor[];  // [cap] then per-warp row staging
+  float* stage = reinterpret_cast<float*>(cursor + ((cap + 3) & ~3)) + (threadIdx.x >> 5) * 32 * kRowPitch;
+  const int32_t* base = cta_base + (size_t)blockIdx.x * cap;
+  for (int b = threadIdx.x; b < cap; b += blockDim.x) cursor[b] = __ldg(offs + b) + __ldg(base + b);
+  __syncthreads();
+  // 32-bit cell arithmetic: a strip holds < 2^31 cells (evo_create checks)
+  const int n = g.W * g.H;
+  const int st = (int)g.stride;
+  const int lane = threadIdx.x & 31;
+  const int c0 = blockIdx.x * kSortChunk, c1 = min(n, c0 + kSortChunk);
+  for (int cb = c0 + (threadIdx.x & ~31); cb < c1; cb += blockDim.x) {
+    const int c = cb + lane;
+    int rank = -1;
+    if (c < c1) {
+      const int y = c / g.W, x = c - y * g.W;
+      const int self = (y + 1) * g.W + x;
+      const int slot = f.gi[self];
+      if (slot < 0) {
+        flag[c] = 0;
+      } else {
+        rank = atomicAdd(&cursor[slot], 1);
+        const int rot = f.rot[self];
+        float* row = stage + lane * kRowPitch;
 #pragma unroll
-    for (int s = 0; s < 9; ++s) {
-      long long o = self;
-      if (s > 0) {
-        const int d = perm_dir(rot, s - 1);
-        int xx = x + dir_dx(d);
-        xx = xx < 0 ? xx + g.W : (xx >= g.W ? xx - g.W : xx);
-        o = (long long)(y + dir_dy(d) + 1) * g.W + xx;  // ghost rows -1 / H exist
+        for (int s = 0; s < 9; ++s) {
+          int o = self;
+          if (s > 0) {
+            const int d = perm_dir(rot, s - 1);
+            int xx = x + dir_dx(d);
+            xx = xx < 0 ? xx + g.W : (xx >= g.W ? xx - g.W : xx);
+            o = (y + dir_dy(d) + 1) * g.W + xx;  // ghost rows -1 / H exist
+          }
+          row[s * 5 + 0] = __ldg(f.E + o);
+          row[s * 5 + 1] = __ldg(f.I + o);
+          row[s * 5 + 2] = __ldg(f.C + o);
+          row[s * 5 + 3] = __ldg(f.C + st + o);
+          row[s * 5 + 4] = __ldg(f.C + 2 * st + o);
+        }
+        row[45] = __int_as_float(c);
+        row[46] = row[47] = 0.0f;
       }
-      v[s * 5 + 0] = __ldg(f.E + o);
-      v[s * 5 + 1] = __ldg(f.I + o);
-      v[s * 5 + 2] = __ldg(f.C + o);
-      v[s * 5 + 3] = __ldg(f.C + st + o);
-      v[s * 5 + 4] = __ldg(f.C + 2 * st + o);
     }
-    v[45] = v[46] = v[47] = 0.0f;
-    float4* dst = reinterpret_cast<float4*>(sens + (size_t)rank * kK1);
-#pragma unroll
-    for (int q = 0; q < kK1 / 4; ++q) dst[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+    __syncwarp();
+    // 32 rows x 12 16-byte chunks, lane-consecutive chunks of the same row
+    for (int i = lane; i < 32 * 12; i += 32) {
+      const int r = i / 12, part = i - r * 12;
+      const int rk = __shfl_sync(0xffffffffu, rank, r);
+      if (rk >= 0) {
+        const float* src = stage + r * kRowPitch + part * 4;
+        reinterpret_cast<float4*>(sens + (size_t)rk * kK1)[part] = make_float4(src[0], src[1], src[2], src[3]);
+      }
+    }
+    __syncwarp();
   }
+}
+
+// tanh(x) = 1 - 2 / (1 + 2^(2x log2 e)) with the SFU exp2 / reciprocal:
+// absolute error ~2e-7 (the hidden activations only enter the next dot
+// product, where absolute error is what counts), 2 MUFU + 3 FMA-pipe ops
+// instead of the libdevice tanhf sequence.
+__device__ __forceinline__ float tanh_sfu(float x) {
+  float t, r;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(t) : "f"(x * 2.8853900817779268f));
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(1.0f + t));
+  return fmaf(-2.0f, r, 1.0f);
+}
+
+__global__ void k_hid_tilemap(const int32_t* tiles, int cap, int32_t* tile_slot) {
+  const int g = blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= cap) return;
+  for (int t = tiles[g]; t < tiles[g + 1]; ++t) tile_slot[t] = g;
 }
 
 struct NetArgs {
@@ -147,9 +217,9 @@ struct NetArgs {
   const int32_t* offs;
   const int32_t* tiles;
   const int32_t* n_tiles;
+  const int32_t* tile_slot;
   int cap;
   const float* sens;
-  const int32_t* rowcell;
   float* act;
   uint8_t* flag;
 };
@@ -177,6 +247,7 @@ __global__ void __launch_bounds__(kNetThreads, 1) k_hid_net(const NetArgs a) {
   unsigned char* Alo = Ahi + a_bytes;
   __shared__ uint32_t tmem_base;
   __shared__ __align__(8) uint64_t bar;
+  __shared__ int cell_of_row[kRows];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 
   const int T = *a.n_tiles;
@@ -193,16 +264,24 @@ __global__ void __launch_bounds__(kNetThreads, 1) k_hid_net(const NetArgs a) {
   int cur = -1;
   const uint32_t id1 = tc::idesc_tf32(kRows, nh), id2 = tc::idesc_tf32(kRows, 16);
 
+  // tile t -> (slot, first row, rows): slot = last s with tiles[s] <= t
+  auto locate = [&](int t, int& slot, int& row0, int& nrows) {
+    slot = __ldg(a.tile_slot + t);
+    row0 = __ldg(a.offs + slot) + (t - __ldg(a.tiles + slot)) * kRows;
+    nrows = min(kRows, __ldg(a.offs + slot + 1) - row0);
+  };
+  // this thread's half sensor row of a tile (24 floats) into registers
+  const int ar = tid >> 1, ahalf = tid & 1;
+  float4 pf[6];
+  auto fetch = [&](int row0, int nrows) {
+    const float4* src = reinterpret_cast<const float4*>(a.sens + (size_t)(row0 + ar) * kK1) + ahalf * 6;
+#pragma unroll
+    for (int q = 0; q < 6; ++q) pf[q] = ar < nrows ? __ldg(src + q) : make_float4(0.f, 0.f, 0.f, 0.f);
+  };
+  int slot, row0, nrows;
+  locate(t0, slot, row0, nrows);
+  fetch(row0, nrows);
   for (int t = t0; t < t1; ++t) {
-    // slot of tile t: last s with tiles[s] <= t
-    int lo = 0, hi = a.cap;  // tiles[cap] = T > t
-    while (hi - lo > 1) {
-      const int mid = (lo + hi) >> 1;
-      if (__ldg(a.tiles + mid) <= t) lo = mid; else hi = mid;
-    }
-    const int slot = lo;
-    const int row0 = __ldg(a.offs + slot) + (t - __ldg(a.tiles + slot)) * kRows;
-    const int nrows = min(kRows, __ldg(a.offs + slot + 1) - row0);
     if (slot != cur) {  // stage the slot's weights (canonical K-major, split)
       cur = slot;
       const float* W1 = a.net.wA + (size_t)slot * kSensors * hp;
@@ -220,24 +299,25 @@ __global__ void __launch_bounds__(kNetThreads, 1) k_hid_net(const NetArgs a) {
       for (int h = tid; h < nh; h += kNetThreads) b1[h] = h < H ? __ldg(a.net.bA + (size_t)slot * hp + h) : 0.0f;
       if (tid < 16) b2[tid] = tid < kActuators ? __ldg(a.net.bB + (size_t)slot * kOutPad + tid) : 0.0f;
     }
-    // A1: 128 sensor rows, each thread half a row (24 floats)
-    {
-      const int r = tid >> 1, half = tid & 1;
-      const float4* src = reinterpret_cast<const float4*>(a.sens + (size_t)(row0 + r) * kK1) + half * 6;
-#pragma unroll
-      for (int q = 0; q < 6; ++q) {
-        const float4 v = r < nrows ? __ldg(src + q) : make_float4(0.f, 0.f, 0.f, 0.f);
-        const int k = (half * 6 + q) * 4;
-        float4 h4, l4;
-        tc::split_tf32(v.x, h4.x, l4.x);
-        tc::split_tf32(v.y, h4.y, l4.y);
-        tc::split_tf32(v.z, h4.z, l4.z);
-        tc::split_tf32(v.w, h4.w, l4.w);
-        const uint32_t off = tc::canon_off(r, k, kRows);
-        *reinterpret_cast<float4*>(Ahi + off) = h4;
-        *reinterpret_cast<float4*>(Alo + off) = l4;
-      }
+    // A1 from the prefetched registers (split, canonical layout); element 45
+    // (chunk 11, .y) is the row's cell index, element 46-47 zero
+    if (ahalf == 1) {
+      cell_of_row[ar] = __float_as_int(pf[5].y);
+      pf[5].y = 0.0f;
     }
+#pragma unroll
+    for (int q = 0; q < 6; ++q) {
+      const float4 v = pf[q];
+      float4 h4, l4;
+      tc::split_tf32(v.x, h4.x, l4.x);
+      tc::split_tf32(v.y, h4.y, l4.y);
+      tc::split_tf32(v.z, h4.z, l4.z);
+      tc::split_tf32(v.w, h4.w, l4.w);
+      const uint32_t off = tc::canon_off(ar, (ahalf * 6 + q) * 4, kRows);
+      *reinterpret_cast<float4*>(Ahi + off) = h4;
+      *reinterpret_cast<float4*>(Alo + off) = l4;
+    }
+    const int cur_nrows = nrows;
     tc::fence_async_smem();
     tc::fence_before();
     __syncthreads();
@@ -254,6 +334,10 @@ __global__ void __launch_bounds__(kNetThreads, 1) k_hid_net(const NetArgs a) {
         tc::mma_tf32(d, tc::smem_desc(ah + oa, lA, 128), tc::smem_desc(bh + ob, lB, 128), id1, 1);
       }
       tc::commit(&bar);
+    }
+    if (t + 1 < t1) {  // next tile's rows are in flight during this tile's MMAs and epilogues
+      locate(t + 1, slot, row0, nrows);
+      fetch(row0, nrows);
     }
     tc::mbar_wait(&bar, phase);
     phase ^= 1;
@@ -275,7 +359,7 @@ __global__ void __launch_bounds__(kNetThreads, 1) k_hid_net(const NetArgs a) {
         float4 h4[2], l4[2];
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
-          const float th = tanhf(__fadd_rn(v[j], b1[c0 + j]));
+          const float th = tanh_sfu(__fadd_rn(v[j], b1[c0 + j]));
           float hh, ll;
           tc::split_tf32(th, hh, ll);
           reinterpret_cast<float*>(h4)[j] = hh;
@@ -318,8 +402,8 @@ __global__ void __launch_bounds__(kNetThreads, 1) k_hid_net(const NetArgs a) {
 #pragma unroll
         for (int j = 0; j < 16; ++j) z[j] = __fadd_rn(z[j], p[j]);
       }
-      if (r < nrows) {
-        const int cell = __ldg(a.rowcell + row0 + r);
+      if (r < cur_nrows) {
+        const int cell = cell_of_row[r];
         float* dst = a.act + (size_t)cell * kActuators;
 #pragma unroll
         for (int j = 0; j < kActuators; ++j) dst[j] = squash(__fadd_rn(z[j], b2[j]));
@@ -336,6 +420,8 @@ __global__ void __launch_bounds__(kNetThreads, 1) k_hid_net(const NetArgs a) {
 
 }  // namespace
 
+int hidden_sort_ctas(long long ncell) { return (int)((ncell + kSortChunk - 1) / kSortChunk); }
+
 int hidden_tc_nh(int hidden) { return ((hidden + 15) / 16) * 16; }
 
 bool hidden_tc_supported(int hidden) { return hidden >= 1 && hidden_tc_nh(hidden) <= 128; }
@@ -350,13 +436,23 @@ size_t hidden_tc_smem(int hidden) {
 cudaError_t launch_hidden_tc(const HidBuffers& b, const StepGeom& g, const Planes& front, const Params& net,
                              int capacity, int num_sms, cudaStream_t st) {
   const long long n = (long long)g.W * g.H;
-  cudaError_t e = cudaMemsetAsync(b.counts, 0, (size_t)capacity * 4, st);
-  if (e != cudaSuccess) return e;
-  const int cgrid = (int)std::min<long long>((n + 255) / 256, (long long)num_sms * 4);
-  k_hid_count<<<cgrid, 256, (size_t)capacity * 4, st>>>(front.gi + g.W, n, capacity, b.counts);
+  const int nctas = hidden_sort_ctas(n);
+  const size_t hsmem = (size_t)capacity * 4;
+  cudaError_t e = cudaSuccess;
+  if (hsmem > 48 * 1024) {
+    e = cudaFuncSetAttribute(k_hid_count, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hsmem);
+    if (e != cudaSuccess) return e;
+  }
+  const size_t ssmem = (size_t)((capacity + 3) & ~3) * 4 + (size_t)(kSortThreads / 32) * 32 * kRowPitch * 4;
+  if (ssmem > 48 * 1024) {
+    e = cudaFuncSetAttribute(k_hid_sense, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssmem);
+    if (e != cudaSuccess) return e;
+  }
+  k_hid_count<<<nctas, kSortThreads, hsmem, st>>>(front.gi + g.W, n, capacity, b.cta_hist);
+  k_hid_colscan<<<(capacity + 255) / 256, 256, 0, st>>>(b.cta_hist, nctas, capacity, b.counts);
   k_hid_scan<<<1, 1024, 0, st>>>(b.counts, capacity, b.offs, b.tiles, b.cursor, b.n_tiles);
-  const int sgrid = (int)std::min<long long>((n + 255) / 256, (long long)num_sms * 16);
-  k_hid_sense<<<sgrid, 256, 0, st>>>(g, front, b.offs, b.cursor, b.sens, b.rowcell, b.flag);
+  k_hid_tilemap<<<(capacity + 255) / 256, 256, 0, st>>>(b.tiles, capacity, b.tile_slot);
+  k_hid_sense<<<nctas, kSortThreads, ssmem, st>>>(g, front, b.offs, b.cta_hist, capacity, b.sens, b.flag);
   NetArgs a;
   a.net = net;
   a.nh = hidden_tc_nh(net.hidden);
@@ -365,7 +461,7 @@ cudaError_t launch_hidden_tc(const HidBuffers& b, const StepGeom& g, const Plane
   a.n_tiles = b.n_tiles;
   a.cap = capacity;
   a.sens = b.sens;
-  a.rowcell = b.rowcell;
+  a.tile_slot = b.tile_slot;
   a.act = b.act;
   a.flag = b.flag;
   const size_t smem = hidden_tc_smem(net.hidden);

@@ -130,12 +130,14 @@ struct HidBuffers {
   int32_t* tiles;    // [cap + 1]
   int32_t* cursor;   // [cap]
   int32_t* n_tiles;  // [1]
+  int32_t* cta_hist;  // [sort CTAs][cap] per-CTA slot histograms -> row bases
   float* sens;       // [ncell][48]
-  int32_t* rowcell;  // [ncell]
+  int32_t* tile_slot;  // [ncell / 128 + cap] slot of each 128-row tile
   float* act;        // [ncell][13] actuator rows (consumed as injected actions)
   uint8_t* flag;     // [ncell]
 };
 bool hidden_tc_supported(int hidden);
+int hidden_sort_ctas(long long ncell);
 int hidden_tc_nh(int hidden);
 size_t hidden_tc_smem(int hidden);
 cudaError_t launch_hidden_tc(const HidBuffers& b, const StepGeom& g, const Planes& front, const Params& net,

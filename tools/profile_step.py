@@ -17,23 +17,37 @@ def main():
     ap.add_argument("--steps", type=int, default=6)
     ap.add_argument("--flush", action="store_true")
     ap.add_argument("--genomes", type=int, default=None)
+    ap.add_argument("--width", type=int, default=None)
+    ap.add_argument("--height", type=int, default=None)
+    ap.add_argument("--flags", type=int, default=0)
+    ap.add_argument("--time", action="store_true", help="CUDA-event time per step")
     args = ap.parse_args()
     import torch
 
     from paper_2406_09654_b200 import engine, physics
 
-    st = engine.baseline_state(args.config, genomes=args.genomes)
+    st = engine.baseline_state(args.config, genomes=args.genomes, width=args.width, height=args.height)
     dev = engine.device_of(st)
     st._evo_binding.sync_params(st.pool)
     dev.upload(st.substrate.front)
     s = torch.cuda.Stream()
     torch.cuda.set_stream(s)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda") if args.flush else None
+    times = []
     for t in range(args.steps):
         if flush is not None:
             flush.zero_()
-        dev.step_raw(physics.step_scalars(t, st.config.physics), t, stream=s.cuda_stream)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(s)
+        dev.step_raw(physics.step_scalars(t, st.config.physics), t, flags=args.flags, stream=s.cuda_stream)
+        e1.record(s)
+        times.append((e0, e1))
     torch.cuda.synchronize()
+    if args.time:
+        ms = [a.elapsed_time(b) for a, b in times]
+        n = st.substrate.width * st.substrate.height
+        best = min(ms[1:] or ms)
+        print(f"step ms: {[round(x, 3) for x in ms]}  best {best:.3f} ms  {n / best / 1e6:.2f} G cell-updates/s")
     print("adoptions", dev.read_stats())
     if os.environ.get("EVOCA_B200_LIB"):
         import ctypes as C
