@@ -182,6 +182,14 @@ EVO_API int evo_select_cells(evo_ctx* ctx, uint64_t key_lo, uint64_t key_hi, dou
 EVO_API int evo_read_selected(evo_ctx* ctx, int64_t capacity, int64_t* cells, int64_t* n);
 EVO_API int evo_remap_selected(evo_ctx* ctx, const int32_t* slot_map);
 
+/* Page-lock caller-owned host planes (cudaHostRegister) so that the
+ * upload/download copies of evo_upload_planes / evo_download_planes run as
+ * direct DMA at full link bandwidth; the substrate's front/back arrays live
+ * for the whole run (substrate.py:86-108), so the engine registers them once.
+ * Registering an already registered range is not an error. */
+EVO_API int evo_host_register(void* ptr, int64_t bytes);
+EVO_API int evo_host_unregister(void* ptr);
+
 /* Device pointers of a plane (halo exchange / interop).  which: 0 energy,
  * 1 infra, 2 comm (3 planes, stride = plane_stride), 3 genome, 4 rotation,
  * 5 mid infra, 6 mid genome, 7 mid proposal byte, 8 mid quantity, 9 census

@@ -791,6 +791,28 @@ EVO_API int evo_remap_selected(evo_ctx* c, const int32_t* slot_map) {
   return 0;
 }
 
+EVO_API int evo_host_register(void* p, int64_t bytes) {
+  if (!p || bytes <= 0) return fail(EVO_EINVAL, "empty host range");
+  cudaError_t e = cudaHostRegister(p, (size_t)bytes, cudaHostRegisterDefault);
+  if (e == cudaErrorHostMemoryAlreadyRegistered) {
+    cudaGetLastError();
+    return 0;
+  }
+  CK(e);
+  return 0;
+}
+
+EVO_API int evo_host_unregister(void* p) {
+  if (!p) return fail(EVO_EINVAL, "null pointer");
+  cudaError_t e = cudaHostUnregister(p);
+  if (e == cudaErrorHostMemoryNotRegistered) {
+    cudaGetLastError();
+    return 0;
+  }
+  CK(e);
+  return 0;
+}
+
 EVO_API int evo_plane_ptr(evo_ctx* c, int which, int buffer, void** ptr, int64_t* plane_stride) {
   if (!c || !ptr) return fail(EVO_EINVAL, "null argument");
   const evo::Planes& p = c->buf[(c->front ^ (buffer ? 1 : 0)) & 1];

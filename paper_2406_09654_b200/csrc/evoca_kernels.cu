@@ -675,16 +675,19 @@ __global__ void __launch_bounds__(kThreads2) k_resolve(const Pass2Args a) {
   for (int b = tid; b < a.capacity; b += kThreads2)
     if (hist[b]) atomicAdd(&a.census.counts[b], hist[b]);
   if (!a.run_census) return;
-  // last CTA: census epilogue (physics.py:395-404, neuroevo.py:521-542)
-  __threadfence();
+  // last CTA: census epilogue (physics.py:395-404, neuroevo.py:521-542).
+  // One cumulative release fence by thread 0 after the barrier publishes the
+  // whole CTA's count atomics before its ticket (a fence in every thread
+  // stalled every warp on a full memory drain).
   __syncthreads();
   if (tid == 0) {
+    asm volatile("fence.acq_rel.gpu;" ::: "memory");
     const unsigned ticket = atomicAdd(a.census.done, 1u);
     s_last = (ticket == gridDim.x - 1);
+    if (s_last) asm volatile("fence.acq_rel.gpu;" ::: "memory");
   }
   __syncthreads();
   if (!s_last) return;
-  __threadfence();
   int dead = 0;
   for (int b = tid; b < a.capacity; b += kThreads2) {
     const int c = atomicExch(&a.census.counts[b], 0);

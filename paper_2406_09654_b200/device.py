@@ -59,9 +59,13 @@ class DeviceSubstrate:
             check(self.lib.evo_create(C.byref(ctx), width, height, capacity, hidden, device))
         self.ctx = ctx
         self._src_map_id = None
+        self._pinned = {}
 
     # -- lifetime -------------------------------------------------------------
     def close(self) -> None:
+        for key in list(getattr(self, "_pinned", {})):
+            self.lib.evo_host_unregister(C.c_void_p(key))
+        self._pinned = {}
         if self.ctx:
             self.lib.evo_destroy(self.ctx)
             self.ctx = None
@@ -97,6 +101,20 @@ class DeviceSubstrate:
             if a is not None and not a.flags["C_CONTIGUOUS"]:
                 raise ValueError("download targets must be C-contiguous")
         check(self.lib.evo_download_planes(self.ctx, ptr(E), ptr(I), ptr(Cm), ptr(gi), ptr(rot), _stream(stream)))
+
+    def pin(self, planes) -> None:
+        """Page-lock a PlaneSet's arrays (evo_host_register) so that uploads
+        and downloads are direct DMA; the arrays are kept alive and unpinned
+        by close()."""
+        for a in _arrays_of(planes):
+            base = a
+            while isinstance(base, np.ndarray) and base.base is not None and isinstance(base.base, np.ndarray):
+                base = base.base
+            key = base.ctypes.data
+            if key in self._pinned:
+                continue
+            check(self.lib.evo_host_register(C.c_void_p(key), base.nbytes))
+            self._pinned[key] = base
 
     def upload(self, planes, stream=None) -> None:
         self.upload_arrays(*_arrays_of(planes), stream=stream)

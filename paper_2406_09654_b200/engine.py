@@ -127,6 +127,7 @@ class _Binding:
         self.param_ids = [None] * self.capacity
         self.pool_version = None
         self.device_ahead = False  # device front newer than the host mirror
+        self.pinned = False
 
     def sync_params(self, pool) -> None:
         ver = getattr(pool, "version", None)
@@ -259,6 +260,10 @@ def step(state) -> None:
     sub = state.substrate
     t = sub.step_counter
     b.sync_params(state.pool)
+    if not b.pinned:  # page-lock the host planes once: uploads/downloads become direct DMA
+        b.dev.pin(sub.front)
+        b.dev.pin(sub.back)
+        b.pinned = True
     if b.device_ahead:
         _download_front(state)
     b.dev.upload(sub.front)

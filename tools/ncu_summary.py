@@ -1,10 +1,11 @@
 """Summarise ncu reports for profiles/ (runs on the CPU box).
 
-    python tools/ncu_summary.py OUT_PREFIX REPORT.ncu-rep [REPORT2 ...]
+    python tools/ncu_summary.py [--config c2] OUT_PREFIX REPORT.ncu-rep [REPORT2 ...]
 
 Writes OUT_PREFIX.md (per-kernel duration, DRAM bytes, issue/pipe
 utilisation, shared-memory wavefronts, top stall reasons) and merges the
-per-launch DRAM traffic into profiles/ncu_traffic.json (read by bench.py).
+per-launch DRAM traffic into profiles/ncu_traffic.json under the config key
+(read by bench.py).
 """
 
 import csv
@@ -41,7 +42,11 @@ def raw(rep):
 
 
 def main():
-    prefix, reps = sys.argv[1], sys.argv[2:]
+    argv = sys.argv[1:]
+    config = "c2"
+    if argv[:1] == ["--config"]:
+        config, argv = argv[1], argv[2:]
+    prefix, reps = argv[0], argv[1:]
     lines = ["# ncu summary", ""]
     traffic = {}
     for rep in reps:
@@ -77,7 +82,8 @@ def main():
         f.write("\n".join(lines) + "\n")
     tpath = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "profiles", "ncu_traffic.json")
     old = json.load(open(tpath)) if os.path.exists(tpath) else {}
-    old.setdefault("per_kernel_dram_bytes_per_launch", {}).update(traffic)
+    old.pop("per_kernel_dram_bytes_per_launch", None)  # pre-config layout
+    old.setdefault(config, {}).setdefault("per_kernel_dram_bytes_per_launch", {}).update(traffic)
     with open(tpath, "w") as f:
         json.dump(old, f, indent=1)
     print(prefix + ".md")
