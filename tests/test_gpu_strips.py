@@ -8,11 +8,17 @@ import pytest
 
 from oracle import oracle as orc
 from paper_2406_09654_b200 import _lib, physics
-from paper_2406_09654_b200.hypernet import DirectParams
+from paper_2406_09654_b200.hypernet import DenseParams, DirectParams
 from paper_2406_09654_b200.strips import DeviceStrip, StripPlan, step_local
 from tests.test_gpu_parity import download, make_dev
 
 pytestmark = pytest.mark.gpu
+
+
+def _params(net):
+    if net.hidden == 0:
+        return [DirectParams(net.w2[i], net.b2[i]) for i in range(net.capacity)]
+    return [DenseParams(net.w1[i], net.b1[i], net.w2[i], net.b2[i]) for i in range(net.capacity)]
 
 
 def _strips(p, net, world):
@@ -20,8 +26,8 @@ def _strips(p, net, world):
     plan = StripPlan(H, W, world)
     strips = []
     for r in range(world):
-        s = DeviceStrip(plan, r, net.capacity, hidden=0)
-        s.dev.set_params([DirectParams(net.w2[i], net.b2[i]) for i in range(net.capacity)])
+        s = DeviceStrip(plan, r, net.capacity, hidden=net.hidden)
+        s.dev.set_params(_params(net))
         s.dev.set_slots(np.ones(net.capacity, np.int8))
         row0, h = plan.rows(r)
         s.dev.upload_arrays(p.E[row0:row0 + h], p.I[row0:row0 + h], p.C[:, row0:row0 + h],
@@ -70,6 +76,30 @@ def test_strips_match_single_context(world, shape):
         c_ref = ref.read_census()[0]
         for s in strips:
             assert np.array_equal(s.dev.read_census()[0], c_ref)
+    for s in strips:
+        s.dev.close()
+    ref.close()
+
+
+@pytest.mark.parametrize("world", [1, 2, 3])
+def test_strips_tensor_core_hidden_net(world):
+    """The config-5 net (45->128 tanh->13 on tcgen05) in strip mode: per-cell
+    results do not depend on the strip / bucket / tile placement, so 1-3
+    strips reproduce the single context bit for bit."""
+    import torch
+
+    H, W = 48, 40
+    p0 = orc.synth_planes(H, W, 24, seed=world, sparse_infra=True)
+    net = orc.synth_net(24, 128, seed=4)
+    ref = make_dev(p0, 24, net)
+    plan, strips = _strips(p0, net, world)
+    params = physics.PhysicsParams(cycle_period=20)
+    for t in range(3):
+        sc = physics.step_scalars(t, params)
+        ref.step_raw(sc, t)
+        step_local(strips, sc, t)
+        torch.cuda.synchronize()
+        assert _gather(plan, strips, p0).equal(download(ref)), f"world={world} t={t}"
     for s in strips:
         s.dev.close()
     ref.close()
