@@ -202,6 +202,8 @@ EVO_API int evo_plane_ptr(evo_ctx* ctx, int which, int buffer, void** ptr, int64
  * CTAs (0 bucketing, 1 controller, 2 physics tail, 3 halo commit, 4 setup);
  * non-zero only in a library built with -DEVO_PHASE_TIMING. */
 EVO_API int evo_debug_phase_cycles(uint64_t* out8, int reset);
+/* Same for the tensor-core hidden-layer kernel (8 phases of its tile loop). */
+EVO_API int evo_debug_hidden_cycles(uint64_t* out8, int reset);
 
 /* 64-bit FNV-1a continuation over host bytes (engine.digest, engine.py:283-315):
  * *out = fold(h, data[0..n)).  Host code, no device involved. */

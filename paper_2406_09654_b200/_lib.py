@@ -77,6 +77,7 @@ SIGNATURES = {
     "evo_host_unregister": [_P],
     "evo_fnv1a64": [C.c_uint64, _P, _I64, C.POINTER(C.c_uint64)],
     "evo_debug_phase_cycles": [_P, _I],
+    "evo_debug_hidden_cycles": [_P, _I],
 }
 RESTYPES = {"evo_last_error": C.c_char_p}
 

@@ -226,7 +226,7 @@ int ensure_hidden_tc(evo_ctx* c) {
   CK(c->alloc(&c->hid.cursor, cap));
   CK(c->alloc(&c->hid.n_tiles, 1));
   CK(c->alloc(&c->hid.cta_hist, (size_t)evo::hidden_sort_ctas(c->ncell()) * cap));
-  CK(c->alloc(&c->hid.tile_slot, n / 128 + cap + 1));
+  CK(c->alloc(&c->hid.tile_info, n / 128 + cap + 1));
   CK(c->alloc(&c->hid.act, n * evo::kActuators));
   CK(c->alloc(&c->hid.flag, n));
   CK(c->alloc(&c->hid.sens, n * 48));
@@ -838,6 +838,13 @@ EVO_API int evo_debug_phase_cycles(uint64_t* out8, int reset) {
   if (!out8) return fail(EVO_EINVAL, "null argument");
   CK(cudaDeviceSynchronize());
   CK(evo::debug_phase_cycles(reinterpret_cast<unsigned long long*>(out8), reset != 0));
+  return 0;
+}
+
+EVO_API int evo_debug_hidden_cycles(uint64_t* out8, int reset) {
+  if (!out8) return fail(EVO_EINVAL, "null argument");
+  CK(cudaDeviceSynchronize());
+  CK(evo::debug_hidden_cycles(reinterpret_cast<unsigned long long*>(out8), reset != 0));
   return 0;
 }
 

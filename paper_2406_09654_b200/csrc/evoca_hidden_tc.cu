@@ -29,6 +29,20 @@
 
 namespace evo {
 
+// Diagnostics build (-DEVO_PHASE_TIMING): per-phase cycle sums of k_hid_net
+// (thread 0 of each CTA), read with evo_debug_hidden_cycles.
+__device__ unsigned long long g_hid_cycles[8];
+#ifdef EVO_PHASE_TIMING
+#define HID_MARK(k)                                                  \
+  if (threadIdx.x == 0) {                                            \
+    const long long now = clock64();                                 \
+    atomicAdd(&g_hid_cycles[k], (unsigned long long)(now - t_mark)); \
+    t_mark = now;                                                    \
+  }
+#else
+#define HID_MARK(k)
+#endif
+
 namespace {
 
 constexpr int kRows = 128;   // MMA M: cells per tile
@@ -194,6 +208,15 @@ __global__ void __launch_bounds__(kSortThreads) k_hid_sense(const StepGeom g, co
   }
 }
 
+// x = hi + lo with hi = x truncated to TF32 (low 13 mantissa bits cleared)
+// and lo = x - hi exact in FP32 (the tensor core reads lo's top 11 bits:
+// error <= 2^-22 |x|, below the accumulation error, tools/microbench/
+// tc_split.cu); 2 instructions instead of two TF32 round-to-nearest cvts.
+__device__ __forceinline__ void split_fast(float x, float& hi, float& lo) {
+  hi = __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
+  lo = __fsub_rn(x, hi);
+}
+
 // tanh(x) = 1 - 2 / (1 + 2^(2x log2 e)) with the SFU exp2 / reciprocal:
 // absolute error ~2e-7 (the hidden activations only enter the next dot
 // product, where absolute error is what counts), 2 MUFU + 3 FMA-pipe ops
@@ -205,10 +228,15 @@ __device__ __forceinline__ float tanh_sfu(float x) {
   return fmaf(-2.0f, r, 1.0f);
 }
 
-__global__ void k_hid_tilemap(const int32_t* tiles, int cap, int32_t* tile_slot) {
+// per 128-row tile: {slot, first row, rows, 0} - one 16-byte load per tile
+__global__ void k_hid_tilemap(const int32_t* offs, const int32_t* tiles, int cap, int4* tile_info) {
   const int g = blockIdx.x * blockDim.x + threadIdx.x;
   if (g >= cap) return;
-  for (int t = tiles[g]; t < tiles[g + 1]; ++t) tile_slot[t] = g;
+  const int o0 = offs[g], o1 = offs[g + 1];
+  for (int t = tiles[g]; t < tiles[g + 1]; ++t) {
+    const int row0 = o0 + (t - tiles[g]) * kRows;
+    tile_info[t] = make_int4(g, row0, min(kRows, o1 - row0), 0);
+  }
 }
 
 struct NetArgs {
@@ -217,7 +245,7 @@ struct NetArgs {
   const int32_t* offs;
   const int32_t* tiles;
   const int32_t* n_tiles;
-  const int32_t* tile_slot;
+  const int4* tile_info;
   int cap;
   const float* sens;
   float* act;
@@ -231,23 +259,48 @@ __device__ __forceinline__ void put_split(unsigned char* hi, unsigned char* lo, 
   *reinterpret_cast<float*>(lo + off) = l;
 }
 
+// TMEM map (512 columns, lanes = the tile's 128 rows):
+//   [0, nh)      layer-1 accumulator 0 (K steps 0-2), then tanh(h) hi  (A of layer 2)
+//   [128, +nh)   layer-1 accumulator 1 (K steps 3-5), then tanh(h) lo
+//   [256, 512)   layer-2 accumulator sets, one per two K=8 steps (32 columns:
+//                hi.hi + lo.hi in 0-15, hi.lo in 16-31)
+// Epilogue 1 turns the two accumulators into h in place (each lane reads its
+// row's columns before writing them), so layer 2 reads its A operand from
+// TMEM (no shared-memory round trip) and only W2 (32 x 8 per step: hi and
+// lo rows) from shared memory.
+constexpr int kAccH = 128;    // TMEM column of layer-1 accumulator 1 / h lo
+constexpr int kD2 = 256;      // TMEM column of the layer-2 accumulators
+
+__device__ __forceinline__ void tmem_st8(uint32_t addr, const float v[8]) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(addr),
+               "r"(__float_as_uint(v[0])), "r"(__float_as_uint(v[1])), "r"(__float_as_uint(v[2])),
+               "r"(__float_as_uint(v[3])), "r"(__float_as_uint(v[4])), "r"(__float_as_uint(v[5])),
+               "r"(__float_as_uint(v[6])), "r"(__float_as_uint(v[7])));
+}
+
+__device__ __forceinline__ void mma_tf32_ta(uint32_t d_tmem, uint32_t a_tmem, uint64_t b, uint32_t idesc,
+                                            uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b), "r"(idesc), "r"(acc));
+}
+
 __global__ void __launch_bounds__(kNetThreads, 1) k_hid_net(const NetArgs a) {
   extern __shared__ __align__(1024) unsigned char smem[];
   const int nh = a.nh;
   const int H = a.net.hidden, hp = a.net.hpad;
   unsigned char* B1hi = smem;
   unsigned char* B1lo = B1hi + nh * kK1 * 4;
-  unsigned char* B2hi = B1lo + nh * kK1 * 4;
-  unsigned char* B2lo = B2hi + 16 * nh * 4;
-  float* b1 = reinterpret_cast<float*>(B2lo + 16 * nh * 4);
+  unsigned char* B2 = B1lo + nh * kK1 * 4;  // [W2 hi (16 rows) ; W2 lo (16 rows)] x nh, canonical R=32
+  float* b1 = reinterpret_cast<float*>(B2 + 32 * nh * 4);
   float* b2 = b1 + nh;
-  unsigned char* Ahi = reinterpret_cast<unsigned char*>(b2 + 16);
-  Ahi = reinterpret_cast<unsigned char*>(((uintptr_t)Ahi + 1023) & ~(uintptr_t)1023);
-  const int a_bytes = kRows * (nh > kK1 ? nh : kK1) * 4;
-  unsigned char* Alo = Ahi + a_bytes;
+  unsigned char* A1 = reinterpret_cast<unsigned char*>(((uintptr_t)(b2 + 16) + 1023) & ~(uintptr_t)1023);
+  constexpr int kA1Bytes = kRows * kK1 * 4;  // one of hi / lo
+  // A1 double buffer: buffer i at A1 + i * 2 * kA1Bytes (hi) and + kA1Bytes (lo)
   __shared__ uint32_t tmem_base;
-  __shared__ __align__(8) uint64_t bar;
-  __shared__ int cell_of_row[kRows];
+  __shared__ __align__(8) uint64_t bar1, bar2;
+  __shared__ int cell_of_row[2][kRows];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 
   const int T = *a.n_tiles;
@@ -255,170 +308,252 @@ __global__ void __launch_bounds__(kNetThreads, 1) k_hid_net(const NetArgs a) {
   const int t0 = blockIdx.x * per, t1 = min(T, t0 + per);
   if (t0 >= t1) return;
   if (warp == 0) tc::tmem_alloc<kTmemCols>(&tmem_base);
-  if (tid == 0) tc::mbar_init(&bar, 1);
+  if (tid == 0) {
+    tc::mbar_init(&bar1, 1);
+    tc::mbar_init(&bar2, 1);
+  }
   tc::fence_before();
   __syncthreads();
   tc::fence_after();
   const uint32_t tmem = tmem_base;
-  uint32_t phase = 0;
-  int cur = -1;
-  const uint32_t id1 = tc::idesc_tf32(kRows, nh), id2 = tc::idesc_tf32(kRows, 16);
+  uint32_t ph1 = 0, ph2 = 0;
+  const uint32_t id1 = tc::idesc_tf32(kRows, nh), id2 = tc::idesc_tf32(kRows, 16),
+                 id2w = tc::idesc_tf32(kRows, 32);
+  const bool issuer = tid == 4 * 32;  // warp 4 issues the MMAs (warps 0-3 run epilogue 2 meanwhile)
 
-  // tile t -> (slot, first row, rows): slot = last s with tiles[s] <= t
   auto locate = [&](int t, int& slot, int& row0, int& nrows) {
-    slot = __ldg(a.tile_slot + t);
-    row0 = __ldg(a.offs + slot) + (t - __ldg(a.tiles + slot)) * kRows;
-    nrows = min(kRows, __ldg(a.offs + slot + 1) - row0);
+    const int4 ti = __ldg(a.tile_info + t);
+    slot = ti.x;
+    row0 = ti.y;
+    nrows = ti.z;
   };
-  // this thread's half sensor row of a tile (24 floats) into registers
-  const int ar = tid >> 1, ahalf = tid & 1;
+  const int ar = tid >> 1, ahalf = tid & 1;  // this thread's half sensor row
   float4 pf[6];
   auto fetch = [&](int row0, int nrows) {
     const float4* src = reinterpret_cast<const float4*>(a.sens + (size_t)(row0 + ar) * kK1) + ahalf * 6;
 #pragma unroll
     for (int q = 0; q < 6; ++q) pf[q] = ar < nrows ? __ldg(src + q) : make_float4(0.f, 0.f, 0.f, 0.f);
   };
-  int slot, row0, nrows;
-  locate(t0, slot, row0, nrows);
-  fetch(row0, nrows);
-  for (int t = t0; t < t1; ++t) {
-    if (slot != cur) {  // stage the slot's weights (canonical K-major, split)
-      cur = slot;
-      const float* W1 = a.net.wA + (size_t)slot * kSensors * hp;
-      for (int i = tid; i < nh * kK1; i += kNetThreads) {
-        const int h = i % nh, k = i / nh;
-        const float w = (h < H && k < kSensors) ? __ldg(W1 + (size_t)k * hp + h) : 0.0f;
-        put_split(B1hi, B1lo, tc::canon_off(h, k, nh), w);
-      }
-      const float* W2 = a.net.wB + (size_t)slot * hp * kOutPad;
-      for (int i = tid; i < 16 * nh; i += kNetThreads) {
-        const int j = i & 15, h = i >> 4;
-        const float w = (h < H && j < kActuators) ? __ldg(W2 + (size_t)h * kOutPad + j) : 0.0f;
-        put_split(B2hi, B2lo, tc::canon_off(j, h, 16), w);
-      }
-      for (int h = tid; h < nh; h += kNetThreads) b1[h] = h < H ? __ldg(a.net.bA + (size_t)slot * hp + h) : 0.0f;
-      if (tid < 16) b2[tid] = tid < kActuators ? __ldg(a.net.bB + (size_t)slot * kOutPad + tid) : 0.0f;
-    }
-    // A1 from the prefetched registers (split, canonical layout); element 45
-    // (chunk 11, .y) is the row's cell index, element 46-47 zero
+  // split the prefetched half row into A1 buffer `buf` (canonical layout); element
+  // 45 of a row is its cell index
+  auto stage_a1 = [&](int buf) {
+    unsigned char* hi = A1 + buf * 2 * kA1Bytes;
+    unsigned char* lo = hi + kA1Bytes;
     if (ahalf == 1) {
-      cell_of_row[ar] = __float_as_int(pf[5].y);
+      cell_of_row[buf][ar] = __float_as_int(pf[5].y);
       pf[5].y = 0.0f;
     }
 #pragma unroll
     for (int q = 0; q < 6; ++q) {
       const float4 v = pf[q];
       float4 h4, l4;
-      tc::split_tf32(v.x, h4.x, l4.x);
-      tc::split_tf32(v.y, h4.y, l4.y);
-      tc::split_tf32(v.z, h4.z, l4.z);
-      tc::split_tf32(v.w, h4.w, l4.w);
+      split_fast(v.x, h4.x, l4.x);
+      split_fast(v.y, h4.y, l4.y);
+      split_fast(v.z, h4.z, l4.z);
+      split_fast(v.w, h4.w, l4.w);
       const uint32_t off = tc::canon_off(ar, (ahalf * 6 + q) * 4, kRows);
-      *reinterpret_cast<float4*>(Ahi + off) = h4;
-      *reinterpret_cast<float4*>(Alo + off) = l4;
+      *reinterpret_cast<float4*>(hi + off) = h4;
+      *reinterpret_cast<float4*>(lo + off) = l4;
     }
-    const int cur_nrows = nrows;
-    tc::fence_async_smem();
-    tc::fence_before();
-    __syncthreads();
-    tc::fence_after();
-    if (tid == 0) {
+  };
+  auto stage_weights = [&](int slot) {
+    const float* W1 = a.net.wA + (size_t)slot * kSensors * hp;
+    for (int i = tid; i < nh * kK1; i += kNetThreads) {
+      const int h = i % nh, k = i / nh;
+      const float w = (h < H && k < kSensors) ? __ldg(W1 + (size_t)k * hp + h) : 0.0f;
+      put_split(B1hi, B1lo, tc::canon_off(h, k, nh), w);
+    }
+    const float* W2 = a.net.wB + (size_t)slot * hp * kOutPad;
+    for (int i = tid; i < 16 * nh; i += kNetThreads) {
+      const int j = i & 15, h = i >> 4;
+      const float w = (h < H && j < kActuators) ? __ldg(W2 + (size_t)h * kOutPad + j) : 0.0f;
+      float hi, lo;
+      tc::split_tf32(w, hi, lo);
+      *reinterpret_cast<float*>(B2 + tc::canon_off(j, h, 32)) = hi;
+      *reinterpret_cast<float*>(B2 + tc::canon_off(16 + j, h, 32)) = lo;
+    }
+    for (int h = tid; h < nh; h += kNetThreads) b1[h] = h < H ? __ldg(a.net.bA + (size_t)slot * hp + h) : 0.0f;
+    if (tid < 16) b2[tid] = tid < kActuators ? __ldg(a.net.bB + (size_t)slot * kOutPad + tid) : 0.0f;
+  };
+  // layer 1 of the tile in A1 buffer `buf`: 6 K steps x (lo.hi, hi.lo, hi.hi),
+  // accumulator 0 for steps 0-2, accumulator 1 for steps 3-5
+  auto issue_l1 = [&](int buf) {
+    if (issuer) {
       const uint32_t lA = kRows * 16, lB = nh * 16;
-      const uint32_t ah = tc::smem_u32(Ahi), al = tc::smem_u32(Alo), bh = tc::smem_u32(B1hi), bl = tc::smem_u32(B1lo);
+      const uint32_t ah = tc::smem_u32(A1 + buf * 2 * kA1Bytes), al = ah + kA1Bytes;
+      const uint32_t bh = tc::smem_u32(B1hi), bl = tc::smem_u32(B1lo);
+      // the two accumulators interleaved (independent consecutive MMAs)
 #pragma unroll
-      for (int ks = 0; ks < kK1 / 8; ++ks) {
-        const uint32_t oa = 2 * ks * lA, ob = 2 * ks * lB;
-        const uint32_t d = tmem + (uint32_t)((ks / kL1StepsPerAcc) * nh);
-        tc::mma_tf32(d, tc::smem_desc(al + oa, lA, 128), tc::smem_desc(bh + ob, lB, 128), id1, ks % kL1StepsPerAcc);
-        tc::mma_tf32(d, tc::smem_desc(ah + oa, lA, 128), tc::smem_desc(bl + ob, lB, 128), id1, 1);
-        tc::mma_tf32(d, tc::smem_desc(ah + oa, lA, 128), tc::smem_desc(bh + ob, lB, 128), id1, 1);
-      }
-      tc::commit(&bar);
+      for (int j = 0; j < 3; ++j)
+#pragma unroll
+        for (int acc = 0; acc < 2; ++acc) {
+          const int ks = acc * 3 + j;
+          const uint32_t oa = 2 * ks * lA, ob = 2 * ks * lB;
+          const uint32_t d = tmem + (acc ? (uint32_t)kAccH : 0u);
+          tc::mma_tf32(d, tc::smem_desc(al + oa, lA, 128), tc::smem_desc(bh + ob, lB, 128), id1, j > 0);
+          tc::mma_tf32(d, tc::smem_desc(ah + oa, lA, 128), tc::smem_desc(bl + ob, lB, 128), id1, 1);
+          tc::mma_tf32(d, tc::smem_desc(ah + oa, lA, 128), tc::smem_desc(bh + ob, lB, 128), id1, 1);
+        }
+      tc::commit(&bar1);
     }
-    if (t + 1 < t1) {  // next tile's rows are in flight during this tile's MMAs and epilogues
-      locate(t + 1, slot, row0, nrows);
-      fetch(row0, nrows);
+  };
+
+  int slot, row0, nrows;
+  locate(t0, slot, row0, nrows);
+  fetch(row0, nrows);
+  int cur = slot;
+  stage_weights(cur);
+  stage_a1(0);
+  int nslot = slot, nrow0, nnrows;
+  if (t0 + 1 < t1) {
+    locate(t0 + 1, nslot, nrow0, nnrows);
+    fetch(nrow0, nnrows);
+  }
+  // tile info one more tile ahead, so fetch() never waits on it
+  int4 ti2 = t0 + 2 < t1 ? __ldg(a.tile_info + t0 + 2) : make_int4(0, 0, 0, 0);
+  tc::fence_async_smem();
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  issue_l1(0);
+  long long t_mark = clock64();
+  (void)t_mark;
+
+  for (int t = t0; t < t1; ++t) {
+    const int buf = (t - t0) & 1;
+    const int cur_nrows = nrows;
+    const bool has_next = t + 1 < t1;
+    // (a) next tile's rows into the other A1 buffer while layer 1 runs
+    if (has_next) stage_a1(buf ^ 1);
+    int n2slot = nslot, n2row0 = 0, n2nrows = 0;
+    if (t + 2 < t1) {
+      n2slot = ti2.x;
+      n2row0 = ti2.y;
+      n2nrows = ti2.z;
+      fetch(n2row0, n2nrows);
+      if (t + 3 < t1) ti2 = __ldg(a.tile_info + t + 3);
     }
-    tc::mbar_wait(&bar, phase);
-    phase ^= 1;
+    HID_MARK(0);
+    // (b) epilogue 1: z1 = acc0 + acc1 + b1 -> tanh -> h (hi, lo) in place in TMEM
+    tc::mbar_wait(&bar1, ph1);
+    ph1 ^= 1;
     tc::fence_after();
-    // epilogue 1: z1 + b1 -> tanh -> A2 (K = hidden), warps share lane quadrants
+    HID_MARK(1);
     {
-      const int q = warp & 3, r = q * 32 + lane;
+      const int q = warp & 3;
+      const uint32_t lb = tmem + ((uint32_t)(q * 32) << 16);
       const int c_begin = (warp >> 2) * (nh / 2), c_end = c_begin + nh / 2;
-      const uint32_t lane_base = tmem + ((uint32_t)(q * 32) << 16);
-      for (int c0 = c_begin; c0 < c_end; c0 += 8) {
-        float v[8], p[8];
-        tc::tmem_ld8(lane_base + c0, v);
+      for (int c0 = c_begin; c0 < c_end; c0 += 16) {
+        float v[16], p[16];
+        tc::tmem_ld16(lb + c0, v);
+        tc::tmem_ld16(lb + kAccH + c0, p);
+        float hh[16], ll[16];
 #pragma unroll
-        for (int g = 1; g < kK1 / 8 / kL1StepsPerAcc; ++g) {
-          tc::tmem_ld8(lane_base + g * nh + c0, p);
-#pragma unroll
-          for (int j = 0; j < 8; ++j) v[j] = __fadd_rn(v[j], p[j]);
+        for (int j = 0; j < 16; ++j) {
+          const float th = tanh_sfu(__fadd_rn(__fadd_rn(v[j], p[j]), b1[c0 + j]));
+          split_fast(th, hh[j], ll[j]);
         }
-        float4 h4[2], l4[2];
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          const float th = tanh_sfu(__fadd_rn(v[j], b1[c0 + j]));
-          float hh, ll;
-          tc::split_tf32(th, hh, ll);
-          reinterpret_cast<float*>(h4)[j] = hh;
-          reinterpret_cast<float*>(l4)[j] = ll;
-        }
-        *reinterpret_cast<float4*>(Ahi + tc::canon_off(r, c0, kRows)) = h4[0];
-        *reinterpret_cast<float4*>(Ahi + tc::canon_off(r, c0 + 4, kRows)) = h4[1];
-        *reinterpret_cast<float4*>(Alo + tc::canon_off(r, c0, kRows)) = l4[0];
-        *reinterpret_cast<float4*>(Alo + tc::canon_off(r, c0 + 4, kRows)) = l4[1];
+        tmem_st8(lb + c0, hh);
+        tmem_st8(lb + c0 + 8, hh + 8);
+        tmem_st8(lb + kAccH + c0, ll);
+        tmem_st8(lb + kAccH + c0 + 8, ll + 8);
       }
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
     }
-    tc::fence_async_smem();
+    HID_MARK(2);
     tc::fence_before();
     __syncthreads();
     tc::fence_after();
-    if (tid == 0) {
-      const uint32_t lA = kRows * 16, lB = 16 * 16;
-      const uint32_t ah = tc::smem_u32(Ahi), al = tc::smem_u32(Alo), bh = tc::smem_u32(B2hi), bl = tc::smem_u32(B2lo);
+    HID_MARK(3);
+    // (c) layer 2 from TMEM: A = h, B = W2.  Per K step two MMAs: h_hi x [W2 hi ;
+    //     W2 lo] (N = 32: hi.hi in columns 0-15, hi.lo in 16-31, h_hi read once)
+    //     and h_lo x W2 hi (N = 16, into columns 0-15); accumulator set g =
+    //     columns kD2 + 32 g holds K steps 2g, 2g+1.
+    if (issuer) {
+      const uint32_t lB = 32 * 16;
+      const uint32_t b = tc::smem_u32(B2);
       for (int ks = 0; ks < nh / 8; ++ks) {
-        const uint32_t oa = 2 * ks * lA, ob = 2 * ks * lB, d = tmem + (uint32_t)(ks * 16);
-        tc::mma_tf32(d, tc::smem_desc(al + oa, lA, 128), tc::smem_desc(bh + ob, lB, 128), id2, 0);
-        tc::mma_tf32(d, tc::smem_desc(ah + oa, lA, 128), tc::smem_desc(bl + ob, lB, 128), id2, 1);
-        tc::mma_tf32(d, tc::smem_desc(ah + oa, lA, 128), tc::smem_desc(bh + ob, lB, 128), id2, 1);
+        const uint32_t d = tmem + kD2 + (uint32_t)((ks >> 1) * 32);
+        const uint64_t desc = tc::smem_desc(b + 2 * ks * lB, lB, 128);
+        mma_tf32_ta(d, tmem + (uint32_t)(ks * 8), desc, id2w, ks & 1);  // initialises all 32 columns of a set
+        mma_tf32_ta(d, tmem + kAccH + (uint32_t)(ks * 8), desc, id2, 1);
       }
-      tc::commit(&bar);
+      tc::commit(&bar2);
     }
-    tc::mbar_wait(&bar, phase);
-    phase ^= 1;
-    tc::fence_after();
-    // epilogue 2: z2 + b2 -> sigmoid (hypernet.py:246-251) -> actuator row
-    if (warp < 4) {
-      const int r = warp * 32 + lane;
-      float z[16], p[16];
-      const uint32_t lane_base = tmem + ((uint32_t)(warp * 32) << 16);
-      tc::tmem_ld8(lane_base, z);
-      tc::tmem_ld8(lane_base + 8, z + 8);
-      for (int ks = 1; ks < nh / 8; ++ks) {
-        tc::tmem_ld8(lane_base + ks * 16, p);
-        tc::tmem_ld8(lane_base + ks * 16 + 8, p + 8);
+    float bias2[16];
 #pragma unroll
-        for (int j = 0; j < 16; ++j) z[j] = __fadd_rn(z[j], p[j]);
+    for (int j = 0; j < 16; ++j) bias2[j] = b2[j];
+    tc::mbar_wait(&bar2, ph2);
+    ph2 ^= 1;
+    tc::fence_after();
+    HID_MARK(4);
+    // (d) next tile's layer 1 (its weights first if the slot changes) runs
+    //     while this tile's second epilogue reads the layer-2 accumulators
+    if (has_next) {
+      if (nslot != cur) {
+        __syncthreads();  // every warp has read b2 above
+        cur = nslot;
+        stage_weights(cur);
+      }
+      tc::fence_async_smem();
+      tc::fence_before();
+      __syncthreads();
+      tc::fence_after();
+      issue_l1(buf ^ 1);
+    }
+    HID_MARK(5);
+    // (e) epilogue 2: sum the accumulator sets in k order, + b2, reference
+    //     sigmoid; warps w and w+4 share the rows of quadrant w, outputs 0-7 / 8-12
+    {
+      const int q = warp & 3, r = q * 32 + lane, jh = (warp >> 2) * 8;
+      const uint32_t lb = tmem + ((uint32_t)(q * 32) << 16) + kD2 + jh;
+      float z[8], pa[8], pb[8];
+      tc::tmem_ld8(lb, pa);
+      tc::tmem_ld8(lb + 16, pb);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) z[j] = __fadd_rn(pa[j], pb[j]);
+      for (int g = 1; g < nh / 16; ++g) {
+        tc::tmem_ld8(lb + g * 32, pa);
+        tc::tmem_ld8(lb + g * 32 + 16, pb);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) z[j] = __fadd_rn(z[j], __fadd_rn(pa[j], pb[j]));
       }
       if (r < cur_nrows) {
-        const int cell = cell_of_row[r];
-        float* dst = a.act + (size_t)cell * kActuators;
+        const int cell = cell_of_row[buf][r];
+        float* dst = a.act + (size_t)cell * kActuators + jh;
+        const int nj = jh == 0 ? 8 : kActuators - 8;
 #pragma unroll
-        for (int j = 0; j < kActuators; ++j) dst[j] = squash(__fadd_rn(z[j], b2[j]));
-        a.flag[cell] = 1;
+        for (int j = 0; j < 8; ++j)
+          if (j < nj) dst[j] = squash(__fadd_rn(z[j], bias2[jh + j]));
+        if (jh == 0) a.flag[cell] = 1;
       }
     }
+    HID_MARK(6);
     tc::fence_before();
     __syncthreads();
     tc::fence_after();
+    HID_MARK(7);
+    slot = nslot;
+    row0 = nrow0;
+    nrows = nnrows;
+    nslot = n2slot;
+    nrow0 = n2row0;
+    nnrows = n2nrows;
   }
   __syncthreads();
   if (warp == 0) tc::tmem_dealloc<kTmemCols>(tmem);
 }
 
 }  // namespace
+
+cudaError_t debug_hidden_cycles(unsigned long long* out, bool reset) {
+  cudaError_t e = cudaMemcpyFromSymbol(out, g_hid_cycles, sizeof(unsigned long long) * 8);
+  if (e == cudaSuccess && reset) {
+    unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    e = cudaMemcpyToSymbol(g_hid_cycles, z, sizeof(z));
+  }
+  return e;
+}
 
 int hidden_sort_ctas(long long ncell) { return (int)((ncell + kSortChunk - 1) / kSortChunk); }
 
@@ -428,9 +563,8 @@ bool hidden_tc_supported(int hidden) { return hidden >= 1 && hidden_tc_nh(hidden
 
 size_t hidden_tc_smem(int hidden) {
   const int nh = hidden_tc_nh(hidden);
-  const size_t fixed = (size_t)2 * nh * kK1 * 4 + (size_t)2 * 16 * nh * 4 + (size_t)(nh + 16) * 4;
-  const size_t a_bytes = (size_t)kRows * (nh > kK1 ? nh : kK1) * 4;
-  return ((fixed + 1023) & ~(size_t)1023) + 2 * a_bytes + 1024;  // + alignment slack
+  const size_t fixed = (size_t)2 * nh * kK1 * 4 + (size_t)32 * nh * 4 + (size_t)(nh + 16) * 4;
+  return ((fixed + 1023) & ~(size_t)1023) + (size_t)4 * kRows * kK1 * 4 + 1024;  // + alignment slack
 }
 
 cudaError_t launch_hidden_tc(const HidBuffers& b, const StepGeom& g, const Planes& front, const Params& net,
@@ -451,7 +585,7 @@ cudaError_t launch_hidden_tc(const HidBuffers& b, const StepGeom& g, const Plane
   k_hid_count<<<nctas, kSortThreads, hsmem, st>>>(front.gi + g.W, n, capacity, b.cta_hist);
   k_hid_colscan<<<(capacity + 255) / 256, 256, 0, st>>>(b.cta_hist, nctas, capacity, b.counts);
   k_hid_scan<<<1, 1024, 0, st>>>(b.counts, capacity, b.offs, b.tiles, b.cursor, b.n_tiles);
-  k_hid_tilemap<<<(capacity + 255) / 256, 256, 0, st>>>(b.tiles, capacity, b.tile_slot);
+  k_hid_tilemap<<<(capacity + 255) / 256, 256, 0, st>>>(b.offs, b.tiles, capacity, b.tile_info);
   k_hid_sense<<<nctas, kSortThreads, ssmem, st>>>(g, front, b.offs, b.cta_hist, capacity, b.sens, b.flag);
   NetArgs a;
   a.net = net;
@@ -461,7 +595,7 @@ cudaError_t launch_hidden_tc(const HidBuffers& b, const StepGeom& g, const Plane
   a.n_tiles = b.n_tiles;
   a.cap = capacity;
   a.sens = b.sens;
-  a.tile_slot = b.tile_slot;
+  a.tile_info = b.tile_info;
   a.act = b.act;
   a.flag = b.flag;
   const size_t smem = hidden_tc_smem(net.hidden);

@@ -132,7 +132,7 @@ struct HidBuffers {
   int32_t* n_tiles;  // [1]
   int32_t* cta_hist;  // [sort CTAs][cap] per-CTA slot histograms -> row bases
   float* sens;       // [ncell][48]
-  int32_t* tile_slot;  // [ncell / 128 + cap] slot of each 128-row tile
+  int4* tile_info;     // [ncell / 128 + cap] {slot, first row, rows, 0} per 128-row tile
   float* act;        // [ncell][13] actuator rows (consumed as injected actions)
   uint8_t* flag;     // [ncell]
 };
@@ -155,6 +155,7 @@ cudaError_t launch_express_cppn(const CppnBatch& b, const Params& net, float* wA
 cudaError_t launch_pass1(const Pass1Args& a, bool inject, bool export_actions, cudaStream_t st);
 cudaError_t launch_pass2(const Pass2Args& a, cudaStream_t st);
 cudaError_t debug_phase_cycles(unsigned long long* out, bool reset);
+cudaError_t debug_hidden_cycles(unsigned long long* out, bool reset);
 cudaError_t launch_census_finish(const Census& c, int capacity, long long t, cudaStream_t st);
 cudaError_t launch_refresh_ghosts(const Planes& p, const StepGeom& g, cudaStream_t st);
 cudaError_t launch_scatter_actions(float* act, uint8_t* flag, const int64_t* cells, const float* rows, long long n,

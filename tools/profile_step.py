@@ -65,6 +65,14 @@ def main():
                   f"{out[i] / args.steps / 148:10.0f} per CTA-step")
         if out[7]:
             print(f"distinct genome slots per controller warp-iteration: {out[6] / out[7]:.2f}")
+        hc = np.zeros(8, np.uint64)
+        _lib.check(_lib.load().evo_debug_hidden_cycles(_lib.ptr(hc), 1))
+        if hc.sum():
+            names = ["stage A1 + prefetch", "wait L1 MMA", "epilogue 1", "sync", "L2 issue + wait",
+                     "restage + L1 issue", "epilogue 2", "tile-end sync"]
+            tot = float(hc.sum())
+            for i, n in enumerate(names):
+                print(f"hid {n:22s} {hc[i] / tot * 100:5.1f}%  {hc[i] / 148 / args.steps:12.0f} cycles/CTA-step")
 
 
 if __name__ == "__main__":
