@@ -357,35 +357,51 @@ __global__ void __launch_bounds__(kThreadsP, 1) k_pass1_direct(const Pass1Args a
     asm volatile("cp.async.commit_group;" ::: "memory");
   }
   fill_slot_offsets(sm.slot_off);
+  int rank[kPreCells];
   {
     Prefetch pf;
     prefetch_tile(a, tile, tiles_x, pf);
     commit_tile(sm, pf);
+    for (int b = threadIdx.x; b < a.capacity; b += kThreadsP) sm.bins[b] = 0;
+    __syncthreads();
+    bucket_count<kThreadsP, kPreCells>(sm.bins, pf.gi, rank);
+    __syncthreads();
+    bucket_offsets<kThreadsP, 2 * kUnitP, kUnitP>(sm.bins, sm.scratch, sm.order, &sm.n_units, a.capacity);
+    __syncthreads();
+    bucket_scatter<kThreadsP, kPreCells>(sm.bins, pf.gi, rank, sm.order);
   }
   __syncthreads();
   long long t_mark = clock64();
   (void)t_mark;
   PHASE_MARK(4);
+  // Per tile: controller | physics + next tile's genome count (from its
+  // prefetch registers) | offsets | scatter + halo commit of the next tile.
   for (; tile < ntiles; tile += gridDim.x) {
     const int x0 = (tile % tiles_x) * kTileW;
     const int y0 = (tile / tiles_x) * kTileH;
     const int next = tile + gridDim.x;
     if (next < ntiles) prefetch_tile_l2(a, next, tiles_x);
-    bucket_by_genome<kThreadsP, kPreCells, 2 * kUnitP, kUnitP>(sm.bins, sm.scratch, sm.gi, sm.order, &sm.n_units, a.capacity);
-    PHASE_MARK(0);
+    for (int b = threadIdx.x; b < a.capacity; b += kThreadsP) sm.bins[b] = 0;  // for the next count
     if (kSmemW && tile == (int)blockIdx.x) {  // weight staging overlapped the first halo load + bucketing
       asm volatile("cp.async.wait_all;" ::: "memory");
       __syncthreads();
     }
+    PHASE_MARK(0);
     tile_controller<kExport, false, kThreadsP, kUnitP, kSmemW>(a, sm, x0, y0, sW12, sW1, sB);
     __syncthreads();
     PHASE_MARK(1);
     Prefetch pf;
     if (next < ntiles) prefetch_tile(a, next, tiles_x, pf);  // L2 hits by now
     tile_physics<false, kExport, kThreadsP>(a, sm, x0, y0);
+    if (next < ntiles) bucket_count<kThreadsP, kPreCells>(sm.bins, pf.gi, rank);
     __syncthreads();
     PHASE_MARK(2);
-    if (next < ntiles) commit_tile(sm, pf);
+    if (next < ntiles) {
+      bucket_offsets<kThreadsP, 2 * kUnitP, kUnitP>(sm.bins, sm.scratch, sm.order, &sm.n_units, a.capacity);
+      __syncthreads();
+      bucket_scatter<kThreadsP, kPreCells>(sm.bins, pf.gi, rank, sm.order);
+      commit_tile(sm, pf);
+    }
     __syncthreads();
     PHASE_MARK(3);
   }
