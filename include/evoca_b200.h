@@ -190,6 +190,17 @@ EVO_API int evo_remap_selected(evo_ctx* ctx, const int32_t* slot_map);
 EVO_API int evo_host_register(void* ptr, int64_t bytes);
 EVO_API int evo_host_unregister(void* ptr);
 
+/* Strip halo staging in one launch each (multi-GPU).
+ * which 0: the five sensed front planes (E, I, C0..C2) before pass 1;
+ * which 1: the pass-1 outputs pass 2 reads (post-death genome, shipped
+ * quantity, proposal byte widened to 32 bits).  Device buffers of
+ * 2 x row_words 32-bit words: pack writes [first row | last row], unpack
+ * reads [ghost row above | ghost row below]; the caller moves them between
+ * ranks (NCCL send/recv). */
+EVO_API int evo_halo_row_words(evo_ctx* ctx, int which, int64_t* row_words);
+EVO_API int evo_halo_pack(evo_ctx* ctx, int which, void* send, void* stream);
+EVO_API int evo_halo_unpack(evo_ctx* ctx, int which, const void* recv, void* stream);
+
 /* Device pointers of a plane (halo exchange / interop).  which: 0 energy,
  * 1 infra, 2 comm (3 planes, stride = plane_stride), 3 genome, 4 rotation,
  * 5 mid infra, 6 mid genome, 7 mid proposal byte, 8 mid quantity, 9 census

@@ -74,6 +74,9 @@ SIGNATURES = {
     "evo_express_cppn": [_P, _I, _P, _P, _P, _P, _P, _P, _P, C.c_double, C.c_double, _P],
     "evo_plane_ptr": [_P, _I, _I, C.POINTER(_P), C.POINTER(_I64)],
     "evo_host_register": [_P, _I64],
+    "evo_halo_row_words": [_P, _I, C.POINTER(_I64)],
+    "evo_halo_pack": [_P, _I, _P, _P],
+    "evo_halo_unpack": [_P, _I, _P, _P],
     "evo_host_unregister": [_P],
     "evo_fnv1a64": [C.c_uint64, _P, _I64, C.POINTER(C.c_uint64)],
     "evo_debug_phase_cycles": [_P, _I],

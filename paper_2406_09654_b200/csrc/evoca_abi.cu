@@ -813,6 +813,27 @@ EVO_API int evo_host_unregister(void* p) {
   return 0;
 }
 
+EVO_API int evo_halo_row_words(evo_ctx* c, int which, int64_t* words) {
+  if (int r = check_ctx(c)) return r;
+  if ((which != 0 && which != 1) || !words) return fail(EVO_EINVAL, "which must be 0 (front) or 1 (pass-1 outputs)");
+  *words = (int64_t)(which == 0 ? 5 : 3) * c->W;
+  return 0;
+}
+
+EVO_API int evo_halo_pack(evo_ctx* c, int which, void* send, void* stream) {
+  if (int r = check_ctx(c)) return r;
+  if ((which != 0 && which != 1) || !send) return fail(EVO_EINVAL, "bad halo pack arguments");
+  CK(evo::launch_halo(c->buf[c->front], c->mid, c->geom(), which, true, send, pick(c, stream)));
+  return 0;
+}
+
+EVO_API int evo_halo_unpack(evo_ctx* c, int which, const void* recv, void* stream) {
+  if (int r = check_ctx(c)) return r;
+  if ((which != 0 && which != 1) || !recv) return fail(EVO_EINVAL, "bad halo unpack arguments");
+  CK(evo::launch_halo(c->buf[c->front], c->mid, c->geom(), which, false, const_cast<void*>(recv), pick(c, stream)));
+  return 0;
+}
+
 EVO_API int evo_plane_ptr(evo_ctx* c, int which, int buffer, void** ptr, int64_t* plane_stride) {
   if (!c || !ptr) return fail(EVO_EINVAL, "null argument");
   const evo::Planes& p = c->buf[(c->front ^ (buffer ? 1 : 0)) & 1];

@@ -765,6 +765,49 @@ __global__ void k_refresh_ghosts(const Planes p, const StepGeom g) {
   }
 }
 
+// Strip halo staging (multi-GPU row strips).  which 0: the five sensed
+// front planes E, I, C0..C2 (f32); which 1: the pass-1 outputs a
+// neighbour's pass 2 reads - post-death genome (i32), shipped quantity (f32
+// bits), proposal byte (widened to a 32-bit word).  A buffer holds two rows
+// of `planes x W` 32-bit words: [0] = this strip's first row (pack) / the
+// ghost row above (unpack), [1] = last row / ghost row below.
+__global__ void k_halo_pack(const Planes f, const Mid m, const StepGeom g, int which, uint32_t* buf) {
+  const int np = which == 0 ? 5 : 3;
+  const int n = 2 * np * g.W;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int side = i / (np * g.W), r = i - side * np * g.W, pl = r / g.W, x = r - pl * g.W;
+    const long long o = plane_row(g, side ? g.H - 1 : 0) + x;
+    uint32_t v;
+    if (which == 0) {
+      const float* src = pl == 0 ? f.E : (pl == 1 ? f.I : f.C + (pl - 2) * g.stride);
+      v = __float_as_uint(src[o]);
+    } else {
+      v = pl == 0 ? (uint32_t)m.gi[o] : (pl == 1 ? __float_as_uint(m.q[o]) : (uint32_t)m.rp[o]);
+    }
+    buf[i] = v;
+  }
+}
+
+__global__ void k_halo_unpack(const Planes f, const Mid m, const StepGeom g, int which, const uint32_t* buf) {
+  const int np = which == 0 ? 5 : 3;
+  const int n = 2 * np * g.W;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int side = i / (np * g.W), r = i - side * np * g.W, pl = r / g.W, x = r - pl * g.W;
+    const long long o = plane_row(g, side ? g.H : -1) + x;
+    const uint32_t v = buf[i];
+    if (which == 0) {
+      float* dst = pl == 0 ? f.E : (pl == 1 ? f.I : f.C + (pl - 2) * g.stride);
+      dst[o] = __uint_as_float(v);
+    } else if (pl == 0) {
+      m.gi[o] = (int32_t)v;
+    } else if (pl == 1) {
+      m.q[o] = __uint_as_float(v);
+    } else {
+      m.rp[o] = (uint8_t)v;
+    }
+  }
+}
+
 __global__ void k_scatter_actions(float* act, uint8_t* flag, const int64_t* cells, const float* rows, long long n,
                                   long long ncell) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
@@ -886,6 +929,17 @@ cudaError_t launch_census_finish(const Census& c, int capacity, long long t, cud
 cudaError_t launch_refresh_ghosts(const Planes& p, const StepGeom& g, cudaStream_t st) {
   const int blocks = (g.W + 255) / 256;
   k_refresh_ghosts<<<blocks, 256, 0, st>>>(p, g);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_halo(const Planes& f, const Mid& m, const StepGeom& g, int which, bool pack, void* buf,
+                        cudaStream_t st) {
+  const int n = 2 * (which == 0 ? 5 : 3) * g.W;
+  const int blocks = (n + 255) / 256 > 1024 ? 1024 : (n + 255) / 256;
+  if (pack)
+    k_halo_pack<<<blocks, 256, 0, st>>>(f, m, g, which, static_cast<uint32_t*>(buf));
+  else
+    k_halo_unpack<<<blocks, 256, 0, st>>>(f, m, g, which, static_cast<const uint32_t*>(buf));
   return cudaGetLastError();
 }
 

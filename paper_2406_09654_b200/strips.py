@@ -136,40 +136,47 @@ class DeviceStrip:
     def _rows(self, plane):
         return plane[1], plane[self.h], plane[0], plane[self.h + 1]  # first, last, ghost top, ghost bottom
 
-    def exchange_front(self) -> None:
-        """Ghost rows of the sensed front planes (before pass 1)."""
+    def _halo_buffers(self, which: int):
+        """Persistent (2, planes * W) int32 device buffers: send [first; last]
+        rows, recv [ghost above; ghost below] (evo_halo_pack / _unpack)."""
         import torch
 
-        views = [self._rows(self._plane(w, 0, k, np.float32)) for w, k in self.FRONT]
-        first = torch.stack([v[0] for v in views])
-        last = torch.stack([v[1] for v in views])
-        gt = torch.empty_like(first)
-        gb = torch.empty_like(first)
-        self.comm.exchange(first, last, gt, gb)
-        for i, v in enumerate(views):
-            v[2].copy_(gt[i])
-            v[3].copy_(gb[i])
+        from ._lib import check
+
+        bufs = self.__dict__.setdefault("_halo", {})
+        if which not in bufs:
+            import ctypes as C
+
+            words = C.c_int64()
+            check(self.dev.lib.evo_halo_row_words(self.dev.ctx, which, C.byref(words)))
+            mk = lambda: torch.empty((2, words.value), dtype=torch.int32, device="cuda")  # noqa: E731
+            bufs[which] = (mk(), mk())
+        return bufs[which]
+
+    def _exchange(self, which: int) -> None:
+        import ctypes as C
+
+        import torch
+
+        from ._lib import check
+
+        from .device import _stream
+
+        send, recv = self._halo_buffers(which)
+        stream = _stream(torch.cuda.current_stream().cuda_stream)  # 0 -> the legacy default stream
+        check(self.dev.lib.evo_halo_pack(self.dev.ctx, which, C.c_void_p(send.data_ptr()), stream))
+        self.comm.exchange(send[0], send[1], recv[0], recv[1])
+        check(self.dev.lib.evo_halo_unpack(self.dev.ctx, which, C.c_void_p(recv.data_ptr()), stream))
+
+    def exchange_front(self) -> None:
+        """Ghost rows of the sensed front planes (before pass 1): one pack
+        launch, one batched NCCL send/recv pair per neighbour, one unpack."""
+        self._exchange(0)
 
     def exchange_mid(self) -> None:
         """Ghost rows of the pass-1 outputs pass 2 reads (proposal byte,
         quantity, post-death genome)."""
-        import torch
-
-        gi = self._rows(self._plane("mid_genome", 0, 0, np.int32))
-        q = self._rows(self._plane("mid_quantity", 0, 0, np.float32))
-        rp = self._rows(self._plane("mid_proposal", 0, 0, np.uint8))
-        # pack as int32 words: genome, bits(q), proposal
-        first = torch.stack([gi[0], q[0].view(torch.int32), rp[0].to(torch.int32)])
-        last = torch.stack([gi[1], q[1].view(torch.int32), rp[1].to(torch.int32)])
-        gt = torch.empty_like(first)
-        gb = torch.empty_like(first)
-        self.comm.exchange(first, last, gt, gb)
-        gi[2].copy_(gt[0])
-        gi[3].copy_(gb[0])
-        q[2].copy_(gt[1].view(torch.float32))
-        q[3].copy_(gb[1].view(torch.float32))
-        rp[2].copy_(gt[2].to(torch.uint8))
-        rp[3].copy_(gb[2].to(torch.uint8))
+        self._exchange(1)
 
     def front_rows(self):
         """(first, last, ghost_top, ghost_bottom) views of the sensed front planes, each (5, W)."""
@@ -190,8 +197,10 @@ class DeviceStrip:
         self.dev.pass1(scalars, t, flags=flags, stream=stream)
         self.exchange_mid()
         self.dev.pass2(t, flags=flags | _lib.F_NO_CENSUS, stream=stream)
-        ptr, _ = self.dev.plane_ptr("census_counts")
-        self.comm.sum_(cuda_view(ptr, (self.dev.capacity,), np.int32))
+        if not hasattr(self, "_counts"):
+            ptr, _ = self.dev.plane_ptr("census_counts")
+            self._counts = cuda_view(ptr, (self.dev.capacity,), np.int32)
+        self.comm.sum_(self._counts)
         self.dev.census_finish(t, stream=stream)
         self.dev.swap()
 
@@ -205,21 +214,31 @@ def step_local(strips, scalars, t: int, flags: int = 0) -> None:
 
     from . import _lib
 
+    import ctypes as C
+
+    from ._lib import check
+    from .device import _stream
+
     n = len(strips)
-
-    def ring(views_of):
-        views = [views_of(s) for s in strips]
-        for r in range(n):
-            up, down = views[(r - 1) % n], views[(r + 1) % n]
-            for k in range(len(views[r])):
-                views[r][k][2].copy_(up[k][1])    # ghost top <- upper neighbour's last row
-                views[r][k][3].copy_(down[k][0])  # ghost bottom <- lower neighbour's first row
-
     stream = torch.cuda.current_stream().cuda_stream
-    ring(lambda s: s.front_rows())
+    cstream = _stream(stream)  # 0 -> the legacy default stream, as the passes use
+
+    def ring(which):
+        bufs = [s._halo_buffers(which) for s in strips]
+        for s, (send, _) in zip(strips, bufs):
+            check(s.dev.lib.evo_halo_pack(s.dev.ctx, which, C.c_void_p(send.data_ptr()), cstream))
+        for r in range(n):
+            up, down = bufs[(r - 1) % n][0], bufs[(r + 1) % n][0]
+            recv = bufs[r][1]
+            recv[0].copy_(up[1])    # ghost above <- upper neighbour's last row
+            recv[1].copy_(down[0])  # ghost below <- lower neighbour's first row
+        for s, (_, recv) in zip(strips, bufs):
+            check(s.dev.lib.evo_halo_unpack(s.dev.ctx, which, C.c_void_p(recv.data_ptr()), cstream))
+
+    ring(0)
     for s in strips:
         s.dev.pass1(scalars, t, flags=flags, stream=stream)
-    ring(lambda s: s.mid_rows())
+    ring(1)
     for s in strips:
         s.dev.pass2(t, flags=flags | _lib.F_NO_CENSUS, stream=stream)
     counts = [cuda_view(s.dev.plane_ptr("census_counts")[0], (s.dev.capacity,), np.int32) for s in strips]
