@@ -84,3 +84,78 @@ def test_slot_pool_census_contract():
     assert dead2 == [1]
     assert p2.records[p2.lineage(1)].death_step == 10
     assert p2.record_for_slot(0).peak_population == 2
+
+
+# -- pool admission, device-expression placeholders, program linearisation --------------
+
+
+def test_slot_pool_admission_matches_reference_rules():
+    """GenomePool.admit (neuroevo.py:451-487): lowest free slot, else the dead
+    slot with the oldest death step (lowest index on ties), else None."""
+    from paper_2406_09654_b200 import neat
+
+    pool = SlotPool(4, net_factory=lambda g: ("params", g))
+    g = neat.init_genome(np.random.default_rng(0), pool.innovations)
+    assert [pool.admit(g, birth_step=0) for _ in range(4)] == [0, 1, 2, 3]
+    assert pool.admit(g) is None and not pool.can_admit()
+    # slots 2 and 1 die at steps 5 and 7, slot 3 at step 5 too
+    counts = np.array([9, 9, 0, 0])
+    pool.update_census(counts, 5)
+    pool.update_census(np.array([9, 0, 0, 0]), 7)
+    assert pool.can_admit()
+    assert pool.admit(g, parents=(0,), birth_step=8) == 2  # oldest death (5), lowest index of the tie
+    assert pool.admit(g, birth_step=8) == 3
+    assert pool.admit(g, birth_step=8) == 1
+    assert pool.admit(g) is None
+    assert pool.params(2) == ("params", g) and pool.genome(2) is g
+    assert pool.record_for_slot(2).parents == (0,)
+
+
+def test_device_expressed_placeholder_surface():
+    from paper_2406_09654_b200 import neat
+    from paper_2406_09654_b200.radiation import DeviceExpressed
+
+    g = neat.init_genome(np.random.default_rng(1), neat.InnovationCounter())
+    direct = DeviceExpressed(g, 0)
+    dense = DeviceExpressed(g, 16)
+    assert not hasattr(direct, "w1") and not hasattr(dense, "w")
+    with pytest.raises(RuntimeError):
+        _ = direct.w  # not generated yet: no silent host fallback
+    with pytest.raises(RuntimeError):
+        _ = dense.w1
+
+    class FakeDev:
+        def get_params_arrays(self, slot, n):
+            assert (slot, n) == (3, 1)
+            return None, None, np.full((1, 13, 45), 2.0, np.float32), np.zeros((1, 13), np.float32)
+
+    direct.bind(FakeDev(), 3)
+    assert direct.expressed and direct.w.shape == (13, 45) and float(direct.w[0, 0]) == 2.0
+
+
+def test_compile_programs_rejects_malformed_genomes():
+    from paper_2406_09654_b200 import neat
+
+    rng = np.random.default_rng(2)
+    g = neat.init_genome(rng, neat.InnovationCounter())
+    # a cycle in the full gene graph
+    h = neat.NodeGene(7, "hidden", "sine")
+    cyc = neat.CppnGenome(g.nodes + (h,), g.connections + (neat.ConnGene(99, 5, 7, 1.0, True),
+                                                            neat.ConnGene(100, 7, 5, 1.0, True)))
+    with pytest.raises(ValueError):
+        neat.compile_programs([cyc])
+    bad = neat.CppnGenome(tuple(n for n in g.nodes if n.id != 6), tuple(c for c in g.connections if c.dst != 6))
+    with pytest.raises(ValueError):
+        neat.compile_programs([bad])
+    node_off, nodes, esrc, ew, outs = neat.compile_programs([g, g])
+    assert node_off.tolist() == [0, 7, 14] and outs.tolist() == [[5, 6], [5, 6]]
+    assert len(esrc) == 20 and np.all(esrc < 7)
+
+
+def test_layout_coords_match_reference_layout():
+    from oracle import cppn as ocppn
+    from paper_2406_09654_b200 import neat
+
+    for hidden in (0, 16, 128):
+        inp, hid, out = ocppn.make_layout(hidden)
+        np.testing.assert_array_equal(neat.layout_coords(hidden), np.vstack([inp, hid, out]))
