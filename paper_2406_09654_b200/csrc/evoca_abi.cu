@@ -476,6 +476,7 @@ EVO_API int evo_pass2(evo_ctx* c, int64_t t, int flags, void* stream) {
   evo::Pass2Args a;
   a.g = c->geom();
   a.back = c->buf[c->front ^ 1];
+  a.rot_front = c->buf[c->front].rot;
   a.mid = c->mid;
   a.census = c->census;
   a.ev.src = rec ? c->ev_src : nullptr;

@@ -21,9 +21,10 @@ constexpr int kActuators = 13;
 constexpr int kOutPad = 16;              // 13 actuators padded to 4 float4
 constexpr int kMaxCapacity = 8192;       // device census bins per CTA (smem)
 
-// Proposal byte written by pass 1 (one per cell): bits 0-2 rotation (front),
-// bits 3-5 shipment direction, bit 6 = cell ships this step.
-constexpr uint8_t kShipBit = 0x40;
+// Proposal byte written by pass 1 (one per cell): one-hot shipment direction
+// (bit d set: the cell ships in direction d this step), 0 = no shipment.
+// Pass 2 finds the arrivals at a target by masking each neighbour's byte
+// with the one direction that points back at the target.
 
 struct Scalars {
   int mode;  // 0 none, 1 day, 2 night
@@ -100,6 +101,7 @@ struct Pass1Args {
 struct Pass2Args {
   StepGeom g;
   Planes back;  // writes I, gi, rot
+  const uint8_t* rot_front;  // pre-step rotation (pass 1 does not change it)
   Mid mid;
   Census census;
   Events ev;     // ev.src == nullptr -> not recorded

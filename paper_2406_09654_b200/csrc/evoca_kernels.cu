@@ -19,7 +19,7 @@
 //                   45->H(tanh)->13 reference net.
 //
 // Pass 2 (k_resolve, physics.py:286-343 + 395-404): each target cell PULLS
-// the shipments aimed at it from its 8 neighbours' proposal bytes.  Arrivals
+// the shipments aimed at it from its 8 neighbours' one-hot proposal bytes.  Arrivals
 // are ordered by the packed 64-bit key (bits(q) << 32) | (0xFFFFFFFF -
 // global_source_index), i.e. q descending then source ascending - the
 // reference's lexsort order - and summed sequentially in that order
@@ -428,6 +428,7 @@ constexpr int kWarps2 = kThreads2 / 32;
 
 struct WarpTile {
   uint8_t rp[kWtHalo];
+  uint8_t rot[kWtCells];
   float q[kWtHalo];
   int gi[kWtHalo];
   float inf[kWtCells];
@@ -467,10 +468,7 @@ __device__ __forceinline__ void ce_desc(u64& a, u64& b) {  // max first
 __device__ __forceinline__ unsigned arrival_mask(const WarpTile& wt, int ty, int tx) {
   unsigned m = 0;
 #pragma unroll
-  for (int d = 0; d < 8; ++d) {
-    const uint8_t rp = wt.rp[(ty + 1 - dir_dy(d)) * kWtHW + tx + 1 - dir_dx(d)];
-    m |= ((rp & 0x78u) == (unsigned)(kShipBit | (d << 3))) ? (1u << d) : 0u;
-  }
+  for (int d = 0; d < 8; ++d) m |= wt.rp[(ty + 1 - dir_dy(d)) * kWtHW + tx + 1 - dir_dx(d)] & (1u << d);
   return m;
 }
 
@@ -481,12 +479,12 @@ __device__ __forceinline__ unsigned arrival_mask(const WarpTile& wt, int ty, int
 // never executes predicated-off code of the other cases.
 template <bool kRecord, int KIND>
 __device__ __forceinline__ int resolve_cell(const Pass2Args& a, const WarpTile& wt, int ty, int tx, int y, int x,
-                                            unsigned m, int& adopted) {
+                                            unsigned m, int& adopted, bool edge_tile) {
   const StepGeom& g = a.g;
   const int hc = (ty + 1) * kWtHW + tx + 1;
   const float before = wt.inf[ty * kWtW + tx];
   const int own = wt.gi[hc];
-  const int r = wt.rp[hc] & 7;
+  const int r = wt.rot[ty * kWtW + tx];
   float acc = before;
   int gnew = own, rnew = r;
   bool adopt = false;
@@ -557,7 +555,7 @@ __device__ __forceinline__ int resolve_cell(const Pass2Args& a, const WarpTile& 
   a.back.I[o] = acc;
   a.back.gi[o] = gnew;
   a.back.rot[o] = (uint8_t)rnew;
-  if (g.own_ghosts && (y == 0 || y == g.H - 1)) {
+  if (edge_tile && (y == 0 || y == g.H - 1)) {  // warp-uniform pre-test per tile
     if (y == 0) {
       const unsigned og = (unsigned)((g.H + 1) * g.W + x);
       a.back.I[og] = acc;
@@ -592,6 +590,7 @@ __global__ void __launch_bounds__(kThreads2) k_resolve(const Pass2Args a) {
   for (int tile = blockIdx.x * kWarps2 + warp; tile < ntiles; tile += gridDim.x * kWarps2) {
     const int x0 = (tile % tiles_x) * kWtW;
     const int y0 = (tile / tiles_x) * kWtH;
+    const bool edge_tile = g.own_ghosts && (y0 == 0 || y0 + kWtH >= g.H);
     {
       // all staging loads of the warp tile issued before any shared store
       // halo column lane (x0-1+lane) of every halo row, plus halo columns 32
@@ -621,8 +620,13 @@ __global__ void __launch_bounds__(kThreads2) k_resolve(const Pass2Args a) {
         }
       }
       const int xi = min(x0 + lane, g.W - 1);
+      uint8_t vr[kWtH];
 #pragma unroll
-      for (int j = 0; j < kWtH; ++j) vi[j] = __ldg(a.mid.I + (unsigned)((min(y0 + j, g.H - 1) + 1) * g.W + xi));
+      for (int j = 0; j < kWtH; ++j) {
+        const unsigned o = (unsigned)((min(y0 + j, g.H - 1) + 1) * g.W + xi);
+        vi[j] = __ldg(a.mid.I + o);
+        vr[j] = __ldg(a.rot_front + o);
+      }
       __syncwarp();
 #pragma unroll
       for (int r = 0; r < kRows; ++r) {
@@ -636,7 +640,10 @@ __global__ void __launch_bounds__(kThreads2) k_resolve(const Pass2Args a) {
         }
       }
 #pragma unroll
-      for (int j = 0; j < kWtH; ++j) wt.inf[j * kWtW + lane] = vi[j];
+      for (int j = 0; j < kWtH; ++j) {
+        wt.inf[j * kWtW + lane] = vi[j];
+        wt.rot[j * kWtW + lane] = vr[j];
+      }
       __syncwarp();
     }
     // cells with <= 1 arrival resolve in place; the rest are queued so that
@@ -652,7 +659,7 @@ __global__ void __launch_bounds__(kThreads2) k_resolve(const Pass2Args a) {
       if (y < g.H && x < g.W) {
         const unsigned m = arrival_mask(wt, ty, tx);
         if ((m & (m - 1)) == 0) {
-          const int gn = resolve_cell<kRecord, 1>(a, wt, ty, tx, y, x, m, my_adopt);
+          const int gn = resolve_cell<kRecord, 1>(a, wt, ty, tx, y, x, m, my_adopt, edge_tile);
           key = (gn >= 0 && gn < a.capacity) ? gn : -1;
         } else {
           kind = __popc(m) == 2 ? 2 : 3;
@@ -672,14 +679,16 @@ __global__ void __launch_bounds__(kThreads2) k_resolve(const Pass2Args a) {
     for (int e = lane; e < n2; e += 32) {
       const int i = wt.queue[e];
       const int ty = i / kWtW, tx = i - ty * kWtW;
-      const int gn = resolve_cell<kRecord, 2>(a, wt, ty, tx, y0 + ty, x0 + tx, arrival_mask(wt, ty, tx), my_adopt);
+      const int gn = resolve_cell<kRecord, 2>(a, wt, ty, tx, y0 + ty, x0 + tx, arrival_mask(wt, ty, tx), my_adopt,
+                                              edge_tile);
       if (gn >= 0 && gn < a.capacity) atomicAdd(&hist[gn], 1);
     }
 #pragma unroll 1
     for (int e = lane; e < n3; e += 32) {
       const int i = wt.queue[kWtCells - 1 - e];
       const int ty = i / kWtW, tx = i - ty * kWtW;
-      const int gn = resolve_cell<kRecord, 3>(a, wt, ty, tx, y0 + ty, x0 + tx, arrival_mask(wt, ty, tx), my_adopt);
+      const int gn = resolve_cell<kRecord, 3>(a, wt, ty, tx, y0 + ty, x0 + tx, arrival_mask(wt, ty, tx), my_adopt,
+                                              edge_tile);
       if (gn >= 0 && gn < a.capacity) atomicAdd(&hist[gn], 1);
     }
     __syncwarp();
@@ -893,7 +902,10 @@ cudaError_t launch_pass2(const Pass2Args& a, cudaStream_t st) {
   // few CTAs, many warp tiles each: the per-CTA census flush (capacity
   // global atomics on shared addresses) and the completion ticket are
   // serialised in L2, so they must not scale with the grid
-  int grid = num_sms() * 8;
+#ifndef EVO_K2_GRID_FACTOR
+#define EVO_K2_GRID_FACTOR 8
+#endif
+  int grid = num_sms() * EVO_K2_GRID_FACTOR;
   const int need = (tiles + kWarps2 - 1) / kWarps2;
   if (grid > need) grid = need;
   const size_t smem = ((sizeof(WarpTile) * kWarps2 + 15) & ~(size_t)15) + (size_t)a.capacity * sizeof(int);
