@@ -225,7 +225,7 @@ int ensure_hidden_tc(evo_ctx* c) {
   CK(c->alloc(&c->hid.tiles, cap + 1));
   CK(c->alloc(&c->hid.cursor, cap));
   CK(c->alloc(&c->hid.n_tiles, 1));
-  CK(c->alloc(&c->hid.cta_hist, (size_t)evo::hidden_sort_ctas(c->ncell()) * cap));
+  CK(c->alloc(&c->hid.cta_hist, (size_t)evo::hidden_sort_ctas(c->W, c->H) * cap));
   CK(c->alloc(&c->hid.tile_info, n / 128 + cap + 1));
   CK(c->alloc(&c->hid.act, n * evo::kActuators));
   CK(c->alloc(&c->hid.flag, n));

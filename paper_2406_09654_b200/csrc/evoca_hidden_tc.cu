@@ -59,21 +59,28 @@ constexpr int kTmemCols = 512;
 constexpr int kL1StepsPerAcc = 2;
 
 // Deterministic counting sort of the occupied cells by slot, without hot
-// global atomics: each CTA owns a contiguous chunk of kSortChunk cells,
-// histograms it in shared memory and writes the histogram out; a column scan
-// turns the per-CTA histograms into per-CTA row bases; the sense pass then
-// ranks cells inside the CTA with shared-memory atomics.
-constexpr int kSortChunk = 16384;
+// global atomics: each CTA owns kSortTiles consecutive 32x32 tiles (tile
+// row-major order), histograms them in shared memory and writes the histogram
+// out; a column scan turns the per-CTA histograms into per-CTA row bases; the
+// sense pass then ranks cells inside the CTA with shared-memory atomics.
+constexpr int kSortTiles = 16;
 constexpr int kSortThreads = 256;
+constexpr int kST = 32;  // sort / sense tile edge
 
-__global__ void k_hid_count(const int32_t* gi, long long n, int cap, int32_t* cta_hist) {
+__global__ void k_hid_count(const StepGeom g, const int32_t* gi, int cap, int32_t* cta_hist) {
   extern __shared__ int hist[];
   for (int b = threadIdx.x; b < cap; b += blockDim.x) hist[b] = 0;
   __syncthreads();
-  const long long c0 = (long long)blockIdx.x * kSortChunk, c1 = min(n, c0 + kSortChunk);
-  for (long long i = c0 + threadIdx.x; i < c1; i += blockDim.x) {
-    const int g = gi[i];
-    if (g >= 0) atomicAdd(&hist[g], 1);
+  const int tiles_x = (g.W + kST - 1) / kST, ntiles = tiles_x * ((g.H + kST - 1) / kST);
+  const int t0 = blockIdx.x * kSortTiles, t1 = min(ntiles, t0 + kSortTiles);
+  for (int t = t0; t < t1; ++t) {
+    const int x0 = (t % tiles_x) * kST, y0 = (t / tiles_x) * kST;
+    for (int i = threadIdx.x; i < kST * kST; i += blockDim.x) {
+      const int y = y0 + i / kST, x = x0 + i % kST;
+      if (y >= g.H || x >= g.W) continue;
+      const int s = gi[(y + 1) * g.W + x];
+      if (s >= 0) atomicAdd(&hist[s], 1);
+    }
   }
   __syncthreads();
   int32_t* out = cta_hist + (size_t)blockIdx.x * cap;
@@ -81,18 +88,37 @@ __global__ void k_hid_count(const int32_t* gi, long long n, int cap, int32_t* ct
 }
 
 // per slot: exclusive scan of the per-CTA counts over CTAs (in place) and the
-// slot total
-__global__ void k_hid_colscan(int32_t* cta_hist, int nctas, int cap, int32_t* counts) {
-  const int g = blockIdx.x * blockDim.x + threadIdx.x;
-  if (g >= cap) return;
-  int run = 0;
-  for (int c = 0; c < nctas; ++c) {
-    int32_t* p = cta_hist + (size_t)c * cap + g;
-    const int v = *p;
-    *p = run;
-    run += v;
+// slot total.  One CTA per 32 slots: lane = slot (coalesced), warp w owns a
+// contiguous chunk of the sort CTAs; chunk sums are scanned across warps in
+// shared memory.
+__global__ void __launch_bounds__(1024) k_hid_colscan(int32_t* cta_hist, int nctas, int cap, int32_t* counts) {
+  __shared__ int part[32][33];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int g = blockIdx.x * 32 + lane;
+  const int per = (nctas + 31) / 32, c0 = w * per, c1 = min(nctas, c0 + per);
+  int sum = 0;
+  if (g < cap)
+    for (int c = c0; c < c1; ++c) sum += cta_hist[(size_t)c * cap + g];
+  part[w][lane] = sum;
+  __syncthreads();
+  if (w == 0) {
+    int run = 0;
+    for (int k = 0; k < 32; ++k) {
+      const int v = part[k][lane];
+      part[k][lane] = run;
+      run += v;
+    }
+    if (g < cap) counts[g] = run;
   }
-  counts[g] = run;
+  __syncthreads();
+  int run = part[w][lane];
+  if (g < cap)
+    for (int c = c0; c < c1; ++c) {
+      int32_t* p = cta_hist + (size_t)c * cap + g;
+      const int v = *p;
+      *p = run;
+      run += v;
+    }
 }
 
 // exclusive scans of counts (cells) and ceil(counts / 128) (tiles); one CTA
@@ -144,67 +170,95 @@ __global__ void k_hid_scan(const int32_t* counts, int cap, int32_t* offs, int32_
 // Sensor rows.  Element 45 of a row carries the cell index (its bit
 // pattern; rows' pad columns meet zero weights, and index bits below
 // 0x7F800000 are finite floats, evo_create bounds the strip), so the net
-// kernel needs no separate row -> cell map.  Rows are assembled per warp in
-// shared memory and written out cooperatively (12 lanes per 192-byte row)
-// so that every store instruction covers whole 32-byte sectors.
+// kernel needs no separate row -> cell map.  Per 32x32 tile the five sensed
+// planes' halo (34 x 34) is staged in shared memory with coalesced loads;
+// each warp assembles 32 rows from it and writes them out cooperatively (12
+// lanes per 192-byte row, whole sectors per store instruction).
 constexpr int kRowPitch = 49;  // floats per staged row (bank-conflict padding)
+constexpr int kSH = kST + 2;   // halo edge
+
+struct SenseSmem {
+  float pl[5][kSH * kSH];
+  int gi[kST * kST];
+  uint8_t rot[kST * kST];
+  float stage[kSortThreads / 32][32 * kRowPitch];
+};
+
+size_t sense_smem_bytes(int cap) { return sizeof(SenseSmem) + (size_t)((cap + 3) & ~3) * 4; }
 
 __global__ void __launch_bounds__(kSortThreads) k_hid_sense(const StepGeom g, const Planes f, const int32_t* offs,
                                                             const int32_t* cta_base, int cap, float* sens,
                                                             uint8_t* flag) {
-  extern __shared__ int cursor[];  // [cap] then per-warp row staging
-  float* stage = reinterpret_cast<float*>(cursor + ((cap + 3) & ~3)) + (threadIdx.x >> 5) * 32 * kRowPitch;
+  extern __shared__ __align__(16) unsigned char sraw[];
+  SenseSmem& sm = *reinterpret_cast<SenseSmem*>(sraw);
+  int* cursor = reinterpret_cast<int*>(sraw + sizeof(SenseSmem));
   const int32_t* base = cta_base + (size_t)blockIdx.x * cap;
   for (int b = threadIdx.x; b < cap; b += blockDim.x) cursor[b] = __ldg(offs + b) + __ldg(base + b);
-  __syncthreads();
-  // 32-bit cell arithmetic: a strip holds < 2^31 cells (evo_create checks)
-  const int n = g.W * g.H;
+  const int tiles_x = (g.W + kST - 1) / kST, ntiles = tiles_x * ((g.H + kST - 1) / kST);
+  const int t0 = blockIdx.x * kSortTiles, t1 = min(ntiles, t0 + kSortTiles);
   const int st = (int)g.stride;
-  const int lane = threadIdx.x & 31;
-  const int c0 = blockIdx.x * kSortChunk, c1 = min(n, c0 + kSortChunk);
-  for (int cb = c0 + (threadIdx.x & ~31); cb < c1; cb += blockDim.x) {
-    const int c = cb + lane;
-    int rank = -1;
-    if (c < c1) {
-      const int y = c / g.W, x = c - y * g.W;
-      const int self = (y + 1) * g.W + x;
-      const int slot = f.gi[self];
-      if (slot < 0) {
-        flag[c] = 0;
-      } else {
-        rank = atomicAdd(&cursor[slot], 1);
-        const int rot = f.rot[self];
-        float* row = stage + lane * kRowPitch;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  float* stage = sm.stage[warp];
+  for (int t = t0; t < t1; ++t) {
+    const int x0 = (t % tiles_x) * kST, y0 = (t / tiles_x) * kST;
+    __syncthreads();  // previous tile's readers are done (and cursor init on the first pass)
+    for (int i = threadIdx.x; i < kSH * kSH; i += blockDim.x) {
+      const int hy = i / kSH, hx = i - hy * kSH;
+      int y = y0 + hy - 1;
+      y = y > g.H ? g.H : y;  // beyond a partial tile: never read
+      int x = x0 + hx - 1;
+      x = x < 0 ? x + g.W : (x >= g.W ? x - g.W : x);
+      x = x >= g.W ? g.W - 1 : x;
+      const int o = (y + 1) * g.W + x;
+      sm.pl[0][i] = __ldg(f.E + o);
+      sm.pl[1][i] = __ldg(f.I + o);
+      sm.pl[2][i] = __ldg(f.C + o);
+      sm.pl[3][i] = __ldg(f.C + st + o);
+      sm.pl[4][i] = __ldg(f.C + 2 * st + o);
+    }
+    for (int i = threadIdx.x; i < kST * kST; i += blockDim.x) {
+      const int y = y0 + i / kST, x = x0 + i % kST;
+      const bool in = y < g.H && x < g.W;
+      const int o = (y + 1) * g.W + x;
+      sm.gi[i] = in ? __ldg(f.gi + o) : -1;
+      sm.rot[i] = in ? __ldg(f.rot + o) : 0;
+    }
+    __syncthreads();
+    for (int cb = warp * 32; cb < kST * kST; cb += blockDim.x) {
+      const int i = cb + lane, ty = i / kST, tx = i - ty * kST;
+      const int y = y0 + ty, x = x0 + tx;
+      const int slot = sm.gi[i];
+      int rank = -1;
+      if (y < g.H && x < g.W) {
+        const int c = y * g.W + x;
+        if (slot < 0) {
+          flag[c] = 0;
+        } else {
+          rank = atomicAdd(&cursor[slot], 1);
+          const int rot = sm.rot[i];
+          const int hb = (ty + 1) * kSH + tx + 1;
+          float* row = stage + lane * kRowPitch;
 #pragma unroll
-        for (int s = 0; s < 9; ++s) {
-          int o = self;
-          if (s > 0) {
-            const int d = perm_dir(rot, s - 1);
-            int xx = x + dir_dx(d);
-            xx = xx < 0 ? xx + g.W : (xx >= g.W ? xx - g.W : xx);
-            o = (y + dir_dy(d) + 1) * g.W + xx;  // ghost rows -1 / H exist
+          for (int s = 0; s < 9; ++s) {
+            const int hp = s == 0 ? hb : hb + dir_dy(perm_dir(rot, s - 1)) * kSH + dir_dx(perm_dir(rot, s - 1));
+#pragma unroll
+            for (int ch = 0; ch < 5; ++ch) row[s * 5 + ch] = sm.pl[ch][hp];
           }
-          row[s * 5 + 0] = __ldg(f.E + o);
-          row[s * 5 + 1] = __ldg(f.I + o);
-          row[s * 5 + 2] = __ldg(f.C + o);
-          row[s * 5 + 3] = __ldg(f.C + st + o);
-          row[s * 5 + 4] = __ldg(f.C + 2 * st + o);
+          row[45] = __int_as_float(c);
+          row[46] = row[47] = 0.0f;
         }
-        row[45] = __int_as_float(c);
-        row[46] = row[47] = 0.0f;
       }
-    }
-    __syncwarp();
-    // 32 rows x 12 16-byte chunks, lane-consecutive chunks of the same row
-    for (int i = lane; i < 32 * 12; i += 32) {
-      const int r = i / 12, part = i - r * 12;
-      const int rk = __shfl_sync(0xffffffffu, rank, r);
-      if (rk >= 0) {
-        const float* src = stage + r * kRowPitch + part * 4;
-        reinterpret_cast<float4*>(sens + (size_t)rk * kK1)[part] = make_float4(src[0], src[1], src[2], src[3]);
+      __syncwarp();
+      for (int k = lane; k < 32 * 12; k += 32) {  // 12 lanes per 192-byte row
+        const int r = k / 12, part = k - r * 12;
+        const int rk = __shfl_sync(0xffffffffu, rank, r);
+        if (rk >= 0) {
+          const float* src = stage + r * kRowPitch + part * 4;
+          reinterpret_cast<float4*>(sens + (size_t)rk * kK1)[part] = make_float4(src[0], src[1], src[2], src[3]);
+        }
       }
+      __syncwarp();
     }
-    __syncwarp();
   }
 }
 
@@ -555,7 +609,10 @@ cudaError_t debug_hidden_cycles(unsigned long long* out, bool reset) {
   return e;
 }
 
-int hidden_sort_ctas(long long ncell) { return (int)((ncell + kSortChunk - 1) / kSortChunk); }
+int hidden_sort_ctas(int W, int H) {
+  const int ntiles = ((W + kST - 1) / kST) * ((H + kST - 1) / kST);
+  return (ntiles + kSortTiles - 1) / kSortTiles;
+}
 
 int hidden_tc_nh(int hidden) { return ((hidden + 15) / 16) * 16; }
 
@@ -569,21 +626,20 @@ size_t hidden_tc_smem(int hidden) {
 
 cudaError_t launch_hidden_tc(const HidBuffers& b, const StepGeom& g, const Planes& front, const Params& net,
                              int capacity, int num_sms, cudaStream_t st) {
-  const long long n = (long long)g.W * g.H;
-  const int nctas = hidden_sort_ctas(n);
+  const int nctas = hidden_sort_ctas(g.W, g.H);
   const size_t hsmem = (size_t)capacity * 4;
+  const size_t ssmem = sense_smem_bytes(capacity);
   cudaError_t e = cudaSuccess;
   if (hsmem > 48 * 1024) {
     e = cudaFuncSetAttribute(k_hid_count, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hsmem);
     if (e != cudaSuccess) return e;
   }
-  const size_t ssmem = (size_t)((capacity + 3) & ~3) * 4 + (size_t)(kSortThreads / 32) * 32 * kRowPitch * 4;
   if (ssmem > 48 * 1024) {
     e = cudaFuncSetAttribute(k_hid_sense, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssmem);
     if (e != cudaSuccess) return e;
   }
-  k_hid_count<<<nctas, kSortThreads, hsmem, st>>>(front.gi + g.W, n, capacity, b.cta_hist);
-  k_hid_colscan<<<(capacity + 255) / 256, 256, 0, st>>>(b.cta_hist, nctas, capacity, b.counts);
+  k_hid_count<<<nctas, kSortThreads, hsmem, st>>>(g, front.gi, capacity, b.cta_hist);
+  k_hid_colscan<<<(capacity + 31) / 32, 1024, 0, st>>>(b.cta_hist, nctas, capacity, b.counts);
   k_hid_scan<<<1, 1024, 0, st>>>(b.counts, capacity, b.offs, b.tiles, b.cursor, b.n_tiles);
   k_hid_tilemap<<<(capacity + 255) / 256, 256, 0, st>>>(b.offs, b.tiles, capacity, b.tile_info);
   k_hid_sense<<<nctas, kSortThreads, ssmem, st>>>(g, front, b.offs, b.cta_hist, capacity, b.sens, b.flag);

@@ -139,7 +139,7 @@ struct HidBuffers {
   uint8_t* flag;     // [ncell]
 };
 bool hidden_tc_supported(int hidden);
-int hidden_sort_ctas(long long ncell);
+int hidden_sort_ctas(int W, int H);
 int hidden_tc_nh(int hidden);
 size_t hidden_tc_smem(int hidden);
 cudaError_t launch_hidden_tc(const HidBuffers& b, const StepGeom& g, const Planes& front, const Params& net,
