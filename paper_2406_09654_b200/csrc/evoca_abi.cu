@@ -67,6 +67,7 @@ struct evo_ctx {
   // rows / flags evo_get_actions reads (act_out, or hid.act after a tensor-core step)
   const float* exp_rows = nullptr;
   const uint8_t* exp_flag = nullptr;
+  const int32_t* exp_rank = nullptr;  // rank-indexed rows (genome-sorted paths)
   bool have_export = false, have_events = false, have_src_map = false;
   cudaStream_t stream = nullptr;
   std::vector<void*> allocs;
@@ -227,8 +228,9 @@ int ensure_hidden_tc(evo_ctx* c) {
   CK(c->alloc(&c->hid.n_tiles, 1));
   CK(c->alloc(&c->hid.cta_hist, (size_t)evo::hidden_sort_ctas(c->W, c->H) * cap));
   CK(c->alloc(&c->hid.tile_info, n / 128 + cap + 1));
-  CK(c->alloc(&c->hid.act, n * evo::kActuators));
-  CK(c->alloc(&c->hid.flag, n));
+  CK(c->alloc(&c->hid.act, n * 16));
+  CK(c->alloc(&c->hid.flag, 1));
+  CK(c->alloc(&c->hid.rank, n));
   CK(c->alloc(&c->hid.sens, n * 48));
   if (!c->num_sms) CK(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, c->device));
   return 0;
@@ -431,17 +433,23 @@ EVO_API int evo_pass1(evo_ctx* c, const evo_scalars* s, int64_t t, int phases, i
   // tcgen05 3xTF32 MLP -> actuator rows), the physics as pass 1 with those rows
   const bool tc_net = !inject && c->hidden > 0 && evo::hidden_tc_supported(c->hidden) &&
                       !(flags & EVO_F_CUDA_CORE_NET);
-  if (exp && !tc_net) {
+  // direct nets of large pools (weights do not fit next to the tile in shared
+  // memory): genome-sorted rows instead of per-tile weight fetches
+  const bool rows_net = !inject && c->hidden == 0 && c->cap > evo::kSmemWeightSlotsAbi &&
+                        !(flags & EVO_F_TILE_NET);
+  if (exp && !tc_net && !rows_net) {
     if (int r = ensure_actions_out(c)) return r;
   }
-  if (tc_net) {
+  if (tc_net || rows_net) {
     if (int r = ensure_hidden_tc(c)) return r;
     CK(evo::launch_hidden_tc(c->hid, c->geom(), c->buf[c->front], c->params(), c->cap, c->num_sms,
                              pick(c, stream)));
   }
-  c->have_export = exp || tc_net;
-  c->exp_rows = tc_net ? c->hid.act : c->act_out;
-  c->exp_flag = tc_net ? c->hid.flag : c->act_out_flag;
+  const bool via_rows = tc_net || rows_net;
+  c->have_export = exp || via_rows;
+  c->exp_rows = via_rows ? c->hid.act : c->act_out;
+  c->exp_flag = via_rows ? nullptr : c->act_out_flag;
+  c->exp_rank = via_rows ? c->hid.rank : nullptr;
   evo::Pass1Args a;
   a.g = c->geom();
   a.front = c->buf[c->front];
@@ -456,13 +464,14 @@ EVO_API int evo_pass1(evo_ctx* c, const evo_scalars* s, int64_t t, int phases, i
   a.s = to_scalars(*s);
   a.phases = phases;
   a.src_map = c->have_src_map ? c->src_map : nullptr;
-  a.act_in = tc_net ? c->hid.act : c->act_in;
-  a.act_flag = tc_net ? c->hid.flag : c->act_in_flag;
+  a.act_in = via_rows ? c->hid.act : c->act_in;
+  a.act_flag = via_rows ? nullptr : c->act_in_flag;
+  a.act_rank = via_rows ? c->hid.rank : nullptr;
   a.act_out = c->act_out;
   a.act_out_flag = c->act_out_flag;
   a.capacity = c->cap;
   a.stats = c->census.stats;
-  CK(evo::launch_pass1(a, inject || tc_net, exp && !tc_net, pick(c, stream)));
+  CK(evo::launch_pass1(a, inject || via_rows, exp && !via_rows, pick(c, stream)));
   return 0;
 }
 
@@ -562,9 +571,26 @@ EVO_API int evo_get_actions(evo_ctx* c, int64_t capacity, int64_t* cells, float*
   const long long nc = c->ncell();
   std::vector<uint8_t> flag((size_t)nc);
   std::vector<float> rows((size_t)nc * evo::kActuators);
+  int64_t m = 0;
+  if (c->exp_rank) {  // genome-sorted rows of 16 floats, located through the cell -> row map
+    std::vector<int32_t> rank((size_t)nc);
+    std::vector<float> srows((size_t)nc * 16);
+    CK(cudaMemcpy(rank.data(), c->exp_rank, (size_t)nc * 4, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(srows.data(), c->exp_rows, srows.size() * 4, cudaMemcpyDeviceToHost));
+    for (long long i = 0; i < nc; ++i) {
+      const int r = rank[(size_t)i];
+      if (r < 0) continue;
+      if (m < capacity) {
+        if (cells) cells[m] = i;
+        if (acts) std::memcpy(acts + m * evo::kActuators, srows.data() + (size_t)r * 16, evo::kActuators * 4);
+      }
+      ++m;
+    }
+    *n = m;
+    return 0;
+  }
   CK(cudaMemcpy(flag.data(), c->exp_flag, (size_t)nc, cudaMemcpyDeviceToHost));
   CK(cudaMemcpy(rows.data(), c->exp_rows, rows.size() * 4, cudaMemcpyDeviceToHost));
-  int64_t m = 0;
   for (long long i = 0; i < nc; ++i) {
     if (!flag[(size_t)i]) continue;
     if (m < capacity) {

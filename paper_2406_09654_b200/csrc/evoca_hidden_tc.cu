@@ -24,7 +24,7 @@
 
 #include <algorithm>
 
-#include "evoca_device.cuh"
+#include "evoca_net.cuh"
 #include "evoca_tc.cuh"
 
 namespace evo {
@@ -188,7 +188,7 @@ size_t sense_smem_bytes(int cap) { return sizeof(SenseSmem) + (size_t)((cap + 3)
 
 __global__ void __launch_bounds__(kSortThreads) k_hid_sense(const StepGeom g, const Planes f, const int32_t* offs,
                                                             const int32_t* cta_base, int cap, float* sens,
-                                                            uint8_t* flag) {
+                                                            int32_t* rank_of_cell) {
   extern __shared__ __align__(16) unsigned char sraw[];
   SenseSmem& sm = *reinterpret_cast<SenseSmem*>(sraw);
   int* cursor = reinterpret_cast<int*>(sraw + sizeof(SenseSmem));
@@ -231,9 +231,7 @@ __global__ void __launch_bounds__(kSortThreads) k_hid_sense(const StepGeom g, co
       int rank = -1;
       if (y < g.H && x < g.W) {
         const int c = y * g.W + x;
-        if (slot < 0) {
-          flag[c] = 0;
-        } else {
+        if (slot >= 0) {
           rank = atomicAdd(&cursor[slot], 1);
           const int rot = sm.rot[i];
           const int hb = (ty + 1) * kSH + tx + 1;
@@ -247,6 +245,7 @@ __global__ void __launch_bounds__(kSortThreads) k_hid_sense(const StepGeom g, co
           row[45] = __int_as_float(c);
           row[46] = row[47] = 0.0f;
         }
+        rank_of_cell[c] = rank;
       }
       __syncwarp();
       for (int k = lane; k < 32 * 12; k += 32) {  // 12 lanes per 192-byte row
@@ -302,8 +301,7 @@ struct NetArgs {
   const int4* tile_info;
   int cap;
   const float* sens;
-  float* act;
-  uint8_t* flag;
+  float* act;  // [rows][16]
 };
 
 __device__ __forceinline__ void put_split(unsigned char* hi, unsigned char* lo, uint32_t off, float x) {
@@ -354,7 +352,6 @@ __global__ void __launch_bounds__(kNetThreads, 1) k_hid_net(const NetArgs a) {
   // A1 double buffer: buffer i at A1 + i * 2 * kA1Bytes (hi) and + kA1Bytes (lo)
   __shared__ uint32_t tmem_base;
   __shared__ __align__(8) uint64_t bar1, bar2;
-  __shared__ int cell_of_row[2][kRows];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 
   const int T = *a.n_tiles;
@@ -393,10 +390,7 @@ __global__ void __launch_bounds__(kNetThreads, 1) k_hid_net(const NetArgs a) {
   auto stage_a1 = [&](int buf) {
     unsigned char* hi = A1 + buf * 2 * kA1Bytes;
     unsigned char* lo = hi + kA1Bytes;
-    if (ahalf == 1) {
-      cell_of_row[buf][ar] = __float_as_int(pf[5].y);
-      pf[5].y = 0.0f;
-    }
+    if (ahalf == 1) pf[5].y = 0.0f;  // element 45 carries the cell index
 #pragma unroll
     for (int q = 0; q < 6; ++q) {
       const float4 v = pf[q];
@@ -475,7 +469,7 @@ __global__ void __launch_bounds__(kNetThreads, 1) k_hid_net(const NetArgs a) {
 
   for (int t = t0; t < t1; ++t) {
     const int buf = (t - t0) & 1;
-    const int cur_nrows = nrows;
+    const int cur_nrows = nrows, cur_row0 = row0;
     const bool has_next = t + 1 < t1;
     // (a) next tile's rows into the other A1 buffer while layer 1 runs
     if (has_next) stage_a1(buf ^ 1);
@@ -497,7 +491,8 @@ __global__ void __launch_bounds__(kNetThreads, 1) k_hid_net(const NetArgs a) {
       const int q = warp & 3;
       const uint32_t lb = tmem + ((uint32_t)(q * 32) << 16);
       const int c_begin = (warp >> 2) * (nh / 2), c_end = c_begin + nh / 2;
-      for (int c0 = c_begin; c0 < c_end; c0 += 16) {
+      int c0 = c_begin;
+      for (; c0 + 16 <= c_end; c0 += 16) {  // 16-column chunks (each warp's half is a multiple of 8)
         float v[16], p[16];
         tc::tmem_ld16(lb + c0, v);
         tc::tmem_ld16(lb + kAccH + c0, p);
@@ -511,6 +506,19 @@ __global__ void __launch_bounds__(kNetThreads, 1) k_hid_net(const NetArgs a) {
         tmem_st8(lb + c0 + 8, hh + 8);
         tmem_st8(lb + kAccH + c0, ll);
         tmem_st8(lb + kAccH + c0 + 8, ll + 8);
+      }
+      if (c0 < c_end) {  // an 8-column tail
+        float v[8], p[8];
+        tc::tmem_ld8(lb + c0, v);
+        tc::tmem_ld8(lb + kAccH + c0, p);
+        float hh[8], ll[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const float th = tanh_sfu(__fadd_rn(__fadd_rn(v[j], p[j]), b1[c0 + j]));
+          split_fast(th, hh[j], ll[j]);
+        }
+        tmem_st8(lb + c0, hh);
+        tmem_st8(lb + kAccH + c0, ll);
       }
       asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
     }
@@ -572,14 +580,13 @@ __global__ void __launch_bounds__(kNetThreads, 1) k_hid_net(const NetArgs a) {
 #pragma unroll
         for (int j = 0; j < 8; ++j) z[j] = __fadd_rn(z[j], __fadd_rn(pa[j], pb[j]));
       }
-      if (r < cur_nrows) {
-        const int cell = cell_of_row[buf][r];
-        float* dst = a.act + (size_t)cell * kActuators + jh;
-        const int nj = jh == 0 ? 8 : kActuators - 8;
+      if (r < cur_nrows) {  // actuator row at its sorted position: 32-byte aligned halves, coalesced
+        float v[8];
 #pragma unroll
-        for (int j = 0; j < 8; ++j)
-          if (j < nj) dst[j] = squash(__fadd_rn(z[j], bias2[jh + j]));
-        if (jh == 0) a.flag[cell] = 1;
+        for (int j = 0; j < 8; ++j) v[j] = jh + j < kActuators ? squash(__fadd_rn(z[j], bias2[jh + j])) : 0.0f;
+        float4* dst = reinterpret_cast<float4*>(a.act + (size_t)(cur_row0 + r) * 16 + jh);
+        dst[0] = make_float4(v[0], v[1], v[2], v[3]);
+        dst[1] = make_float4(v[4], v[5], v[6], v[7]);
       }
     }
     HID_MARK(6);
@@ -596,6 +603,75 @@ __global__ void __launch_bounds__(kNetThreads, 1) k_hid_net(const NetArgs a) {
   }
   __syncthreads();
   if (warp == 0) tc::tmem_dealloc<kTmemCols>(tmem);
+}
+
+// Direct 45->13 controller over genome-sorted sensor rows (many-genome
+// pools, e.g. BASELINE configs 3-4 with 256-1024 genomes, where a 32x32 tile
+// holds ~1-4 cells per genome and per-tile weight fetches dominate).  A CTA
+// of 128 threads takes contiguous 128-row tiles (one genome each): the
+// genome's 2.4 KB of weights are staged in shared memory once per run of
+// tiles and every weight load is a warp-uniform broadcast; each thread loads
+// its whole 192-byte row up front (12 independent 16-byte loads in flight)
+// and runs the same packed FFMA2 chains, pairing and k order as the tile
+// kernel (net_direct_unit), so results are bit-identical to it.
+constexpr int kDrThreads = 128;
+
+__global__ void __launch_bounds__(kDrThreads) k_direct_rows(const NetArgs a) {
+  __shared__ __align__(16) float W12[kSensors * 12];
+  __shared__ __align__(16) float W1[48];
+  __shared__ __align__(16) float Bs[kOutPad];
+  const int T = *a.n_tiles;
+  const int per = (T + gridDim.x - 1) / gridDim.x;
+  const int t0 = blockIdx.x * per, t1 = min(T, t0 + per);
+  int cur = -1;
+  for (int t = t0; t < t1; ++t) {
+    const int4 ti = __ldg(a.tile_info + t);
+    const bool valid = (int)threadIdx.x < ti.z;
+    float4 xr[12];
+    const float4* row = reinterpret_cast<const float4*>(a.sens + (size_t)(ti.y + (valid ? threadIdx.x : 0)) * kK1);
+#pragma unroll
+    for (int q = 0; q < 12; ++q) xr[q] = __ldg(row + q);
+    if (ti.x != cur) {
+      __syncthreads();
+      cur = ti.x;
+      const float* w12 = a.net.wA + (size_t)cur * kSensors * 12;
+      for (int i = threadIdx.x; i < kSensors * 12; i += kDrThreads) W12[i] = __ldg(w12 + i);
+      for (int i = threadIdx.x; i < kSensors; i += kDrThreads) W1[i] = __ldg(a.net.wB + (size_t)cur * kSensors + i);
+      if (threadIdx.x < kOutPad) Bs[threadIdx.x] = __ldg(a.net.bA + (size_t)cur * kOutPad + threadIdx.x);
+      __syncthreads();
+    }
+    u64 acc[6] = {0ull, 0ull, 0ull, 0ull, 0ull, 0ull};
+    float acc12 = 0.0f;
+#pragma unroll
+    for (int k = 0; k < kSensors; ++k) {
+      const float4 c4 = xr[k >> 2];
+      const float x = (k & 3) == 0 ? c4.x : ((k & 3) == 1 ? c4.y : ((k & 3) == 2 ? c4.z : c4.w));
+      const float4* w4 = reinterpret_cast<const float4*>(W12 + k * 12);
+      const float4 wa = w4[0], wb = w4[1], wc = w4[2];
+      ffma2(acc[0], x, pk2(wa.x, wa.y));
+      ffma2(acc[1], x, pk2(wa.z, wa.w));
+      ffma2(acc[2], x, pk2(wb.x, wb.y));
+      ffma2(acc[3], x, pk2(wb.z, wb.w));
+      ffma2(acc[4], x, pk2(wc.x, wc.y));
+      ffma2(acc[5], x, pk2(wc.z, wc.w));
+      acc12 = fmaf(x, W1[k], acc12);
+    }
+    if (valid) {  // the actuator row at its sorted position (64 bytes, coalesced across the warp)
+      float v[16];
+#pragma unroll
+      for (int p = 0; p < 6; ++p) {
+        float lo, hi;
+        up2(acc[p], lo, hi);
+        v[2 * p] = squash(__fadd_rn(lo, Bs[2 * p]));
+        v[2 * p + 1] = squash(__fadd_rn(hi, Bs[2 * p + 1]));
+      }
+      v[12] = squash(__fadd_rn(acc12, Bs[12]));
+      v[13] = v[14] = v[15] = 0.0f;
+      float4* dst = reinterpret_cast<float4*>(a.act + (size_t)(ti.y + threadIdx.x) * 16);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) dst[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+    }
+  }
 }
 
 }  // namespace
@@ -642,10 +718,10 @@ cudaError_t launch_hidden_tc(const HidBuffers& b, const StepGeom& g, const Plane
   k_hid_colscan<<<(capacity + 31) / 32, 1024, 0, st>>>(b.cta_hist, nctas, capacity, b.counts);
   k_hid_scan<<<1, 1024, 0, st>>>(b.counts, capacity, b.offs, b.tiles, b.cursor, b.n_tiles);
   k_hid_tilemap<<<(capacity + 255) / 256, 256, 0, st>>>(b.offs, b.tiles, capacity, b.tile_info);
-  k_hid_sense<<<nctas, kSortThreads, ssmem, st>>>(g, front, b.offs, b.cta_hist, capacity, b.sens, b.flag);
+  k_hid_sense<<<nctas, kSortThreads, ssmem, st>>>(g, front, b.offs, b.cta_hist, capacity, b.sens, b.rank);
   NetArgs a;
   a.net = net;
-  a.nh = hidden_tc_nh(net.hidden);
+  a.nh = net.hidden > 0 ? hidden_tc_nh(net.hidden) : 0;
   a.offs = b.offs;
   a.tiles = b.tiles;
   a.n_tiles = b.n_tiles;
@@ -653,7 +729,10 @@ cudaError_t launch_hidden_tc(const HidBuffers& b, const StepGeom& g, const Plane
   a.sens = b.sens;
   a.tile_info = b.tile_info;
   a.act = b.act;
-  a.flag = b.flag;
+  if (net.hidden == 0) {
+    k_direct_rows<<<num_sms * 12, kDrThreads, 0, st>>>(a);
+    return cudaGetLastError();
+  }
   const size_t smem = hidden_tc_smem(net.hidden);
   e = cudaFuncSetAttribute(k_hid_net, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;

@@ -20,6 +20,7 @@ constexpr int kSensors = 45;             // hypernet.py:35-38
 constexpr int kActuators = 13;
 constexpr int kOutPad = 16;              // 13 actuators padded to 4 float4
 constexpr int kMaxCapacity = 8192;       // device census bins per CTA (smem)
+constexpr int kSmemWeightSlotsAbi = 68;  // largest pool the tile kernel keeps in shared memory
 
 // Proposal byte written by pass 1 (one per cell): one-hot shipment direction
 // (bit d set: the cell ships in direction d this step), 0 = no shipment.
@@ -90,8 +91,9 @@ struct Pass1Args {
   Scalars s;
   int phases;
   const float* src_map;      // nullable, (H,W)
-  const float* act_in;       // inject: (H*W,13)
+  const float* act_in;       // inject: (H*W,13), or with act_rank: rank-ordered rows of 16
   const uint8_t* act_flag;   // inject: (H*W)
+  const int32_t* act_rank;   // nullable: row of each cell in act_in (-1 = no actions)
   float* act_out;            // export: (H*W,13)
   uint8_t* act_out_flag;     // export: (H*W)
   int capacity;
@@ -135,8 +137,9 @@ struct HidBuffers {
   int32_t* cta_hist;  // [sort CTAs][cap] per-CTA slot histograms -> row bases
   float* sens;       // [ncell][48]
   int4* tile_info;     // [ncell / 128 + cap] {slot, first row, rows, 0} per 128-row tile
-  float* act;        // [ncell][13] actuator rows (consumed as injected actions)
-  uint8_t* flag;     // [ncell]
+  float* act;        // [ncell][16] actuator rows in sorted-row order (13 used)
+  uint8_t* flag;     // unused by the row paths (kept for layout stability)
+  int32_t* rank;     // [ncell] sorted row of each cell, -1 = empty
 };
 bool hidden_tc_supported(int hidden);
 int hidden_sort_ctas(int W, int H);

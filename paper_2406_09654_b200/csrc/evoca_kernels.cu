@@ -80,9 +80,16 @@ __device__ __forceinline__ void tile_physics(const Pass1Args& a, const SM& sm, i
     CellAct ac{};
     if (kExport && st.slot < 0) a.act_out_flag[cell] = 0;
     if (kInject) {
-      ac.acted = a.act_flag[cell] != 0;
+      const float* row;
+      if (a.act_rank) {  // rows of the genome-sorted paths, 16 floats each
+        const int r = a.act_rank[cell];
+        ac.acted = r >= 0;
+        row = a.act_in + (size_t)(r >= 0 ? r : 0) * 16;
+      } else {
+        ac.acted = a.act_flag[cell] != 0;
+        row = a.act_in + cell * kActuators;
+      }
       if (ac.acted) {
-        const float* row = a.act_in + cell * kActuators;
         ac.inv = row[0];
         ac.liq = row[1];
         ac.m0 = row[2];
@@ -408,7 +415,7 @@ __global__ void __launch_bounds__(kThreadsP, 1) k_pass1_direct(const Pass1Args a
 }
 
 // Largest pool whose weight tables fit in shared memory next to the tile.
-constexpr int kSmemWeightSlots = 68;
+constexpr int kSmemWeightSlots = kSmemWeightSlotsAbi;
 constexpr size_t weight_smem_bytes(int capacity) {
   return ((size_t)capacity * (kSensors * 12 + kOutPad) + (((size_t)capacity * kSensors + 3) & ~(size_t)3)) * sizeof(float);
 }

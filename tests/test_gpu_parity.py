@@ -491,3 +491,26 @@ def test_tensor_core_net_free_running_matches_oracle():
     p0 = orc.synth_planes(64, 64, 40, seed=11, sparse_infra=True)
     net = orc.synth_net(40, 128, seed=11)
     _step_vs_oracle(p0, net, orc.Phys(cycle_period=20), steps=4)
+
+
+@pytest.mark.parametrize("genomes,shape", [(300, (96, 80)), (1024, (64, 64)), (90, (1, 500))])
+def test_genome_sorted_direct_path_matches_tile_path(genomes, shape):
+    """Pools larger than the tile kernel's shared-memory weight table (68
+    slots) run the direct net over genome-sorted sensor rows; per-cell
+    arithmetic (FFMA2 pairing, k order, bias, sigmoid) is the tile kernel's,
+    so both paths give bit-identical states, and tier A holds vs the oracle."""
+    h, w = shape
+    p0 = orc.synth_planes(h, w, genomes, seed=genomes)
+    net = orc.synth_net(genomes, 0, seed=5)
+    phys = orc.Phys(cycle_period=20)
+    params = oracle_phys_to_params(phys)
+    a = make_dev(p0, genomes, net)
+    b = make_dev(p0, genomes, net)
+    for t in range(3):
+        sc = physics.step_scalars(t, params)
+        a.step_raw(sc, t, flags=_lib.F_EXPORT_ACTIONS)
+        b.step_raw(sc, t, flags=_lib.F_TILE_NET)
+        assert download(a).equal(download(b)), f"t={t}"
+    a.close()
+    b.close()
+    _step_vs_oracle(p0, net, phys, steps=2)
