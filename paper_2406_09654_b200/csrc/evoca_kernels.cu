@@ -28,6 +28,8 @@
 // plane feeds a shared-memory census histogram; the last CTA to finish
 // publishes counts and retires slots (neuroevo.py:521-542).
 
+#include <algorithm>
+
 #include "evoca_net.cuh"
 
 namespace evo {
@@ -50,6 +52,40 @@ __device__ __forceinline__ void zero_stats(const Pass1Args& a) {
   if (blockIdx.x == 0 && threadIdx.x == 0 && a.stats) {
     a.stats[0] = 0;
     a.stats[1] = 0;
+  }
+}
+
+// Pass 1 of the genome-sorted paths (tensor-core hidden nets, large-pool
+// direct nets): the actions already sit in rank-ordered rows, so the physics
+// tail runs per cell straight from the planes - coalesced state reads, one
+// 64-byte actuator row read per occupied cell, coalesced stores - with no
+// shared-memory staging.
+__global__ void __launch_bounds__(256) k_physics_rows(const Pass1Args a) {
+  zero_stats(a);
+  const StepGeom& g = a.g;
+  const int n = g.W * g.H;
+  const unsigned st = (unsigned)g.stride;
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < n; c += gridDim.x * blockDim.x) {
+    const int y = c / g.W, x = c - y * g.W;
+    const unsigned o = (unsigned)((y + 1) * g.W + x);
+    const CellState cs{__ldg(a.front.E + o), __ldg(a.front.I + o), __ldg(a.front.C + o),
+                       __ldg(a.front.C + st + o), __ldg(a.front.C + 2 * st + o), __ldg(a.front.gi + o),
+                       (int)__ldg(a.front.rot + o)};
+    CellAct ac{};
+    const int r = __ldg(a.act_rank + c);
+    ac.acted = r >= 0;
+    if (ac.acted) {
+      const float4* row = reinterpret_cast<const float4*>(a.act_in + (size_t)r * 16);
+      const float4 r0 = __ldg(row), r1 = __ldg(row + 1), r2 = __ldg(row + 2), r3 = __ldg(row + 3);
+      ac.inv = r0.x;
+      ac.liq = r0.y;
+      ac.m0 = r0.z;
+      ac.m1 = r0.w;
+      ac.m2 = r1.x;
+      const float ex[8] = {r1.y, r1.z, r1.w, r2.x, r2.y, r2.z, r2.w, r3.x};
+      explore_argmax(ex, ac.kstar, ac.xmax);
+    }
+    store_pass1(a, y, x, cell_physics(a.s, a.phases, a.src_map, c, cs, ac));
   }
 }
 
@@ -896,6 +932,12 @@ static cudaError_t launch_direct(const Pass1Args& a, cudaStream_t st) {
 }
 
 cudaError_t launch_pass1(const Pass1Args& a, bool inject, bool export_actions, cudaStream_t st) {
+  if (inject && a.act_rank) {
+    const long long n = (long long)a.g.W * a.g.H;
+    const int grid = (int)std::min<long long>((n + 255) / 256, (long long)num_sms() * 8);
+    k_physics_rows<<<grid, 256, 0, st>>>(a);
+    return cudaGetLastError();
+  }
   if (inject) return launch_generic<true, false, false>(a, st);
   if (a.net.hidden > 0)
     return export_actions ? launch_generic<false, true, true>(a, st) : launch_generic<false, false, true>(a, st);
