@@ -443,7 +443,7 @@ EVO_API int evo_pass1(evo_ctx* c, const evo_scalars* s, int64_t t, int phases, i
   if (tc_net || rows_net) {
     if (int r = ensure_hidden_tc(c)) return r;
     CK(evo::launch_hidden_tc(c->hid, c->geom(), c->buf[c->front], c->params(), c->cap, c->num_sms,
-                             pick(c, stream)));
+                             /*decided=*/!exp, pick(c, stream)));
   }
   const bool via_rows = tc_net || rows_net;
   c->have_export = exp || via_rows;
@@ -467,6 +467,7 @@ EVO_API int evo_pass1(evo_ctx* c, const evo_scalars* s, int64_t t, int phases, i
   a.act_in = via_rows ? c->hid.act : c->act_in;
   a.act_flag = via_rows ? nullptr : c->act_in_flag;
   a.act_rank = via_rows ? c->hid.rank : nullptr;
+  a.act_decided = via_rows && c->hidden == 0 && !exp ? 1 : 0;
   a.act_out = c->act_out;
   a.act_out_flag = c->act_out_flag;
   a.capacity = c->cap;

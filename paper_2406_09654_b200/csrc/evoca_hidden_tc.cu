@@ -301,7 +301,8 @@ struct NetArgs {
   const int4* tile_info;
   int cap;
   const float* sens;
-  float* act;  // [rows][16]
+  float* act;  // [rows][16], or [rows][8] decided rows (direct nets, no export)
+  int decided;
 };
 
 __device__ __forceinline__ void put_split(unsigned char* hi, unsigned char* lo, uint32_t off, float x) {
@@ -656,20 +657,32 @@ __global__ void __launch_bounds__(kDrThreads) k_direct_rows(const NetArgs a) {
       ffma2(acc[5], x, pk2(wc.z, wc.w));
       acc12 = fmaf(x, W1[k], acc12);
     }
-    if (valid) {  // the actuator row at its sorted position (64 bytes, coalesced across the warp)
-      float v[16];
+    if (valid) {  // the actuator row at its sorted position (coalesced across the warp)
+      float z[13];
 #pragma unroll
       for (int p = 0; p < 6; ++p) {
         float lo, hi;
         up2(acc[p], lo, hi);
-        v[2 * p] = squash(__fadd_rn(lo, Bs[2 * p]));
-        v[2 * p + 1] = squash(__fadd_rn(hi, Bs[2 * p + 1]));
+        z[2 * p] = __fadd_rn(lo, Bs[2 * p]);
+        z[2 * p + 1] = __fadd_rn(hi, Bs[2 * p + 1]);
       }
-      v[12] = squash(__fadd_rn(acc12, Bs[12]));
-      v[13] = v[14] = v[15] = 0.0f;
-      float4* dst = reinterpret_cast<float4*>(a.act + (size_t)(ti.y + threadIdx.x) * 16);
+      z[12] = __fadd_rn(acc12, Bs[12]);
+      if (a.decided) {  // 32 bytes: the physics needs only these (explore_pick is exact)
+        int ks;
+        float xm;
+        explore_pick(z + 5, ks, xm);
+        float4* dst = reinterpret_cast<float4*>(a.act + (size_t)(ti.y + threadIdx.x) * 8);
+        dst[0] = make_float4(squash(z[0]), squash(z[1]), squash(z[2]), squash(z[3]));
+        dst[1] = make_float4(squash(z[4]), xm, __int_as_float(ks), 0.0f);
+      } else {
+        float v[16];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) dst[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+        for (int j = 0; j < 13; ++j) v[j] = squash(z[j]);
+        v[13] = v[14] = v[15] = 0.0f;
+        float4* dst = reinterpret_cast<float4*>(a.act + (size_t)(ti.y + threadIdx.x) * 16);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) dst[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+      }
     }
   }
 }
@@ -701,7 +714,7 @@ size_t hidden_tc_smem(int hidden) {
 }
 
 cudaError_t launch_hidden_tc(const HidBuffers& b, const StepGeom& g, const Planes& front, const Params& net,
-                             int capacity, int num_sms, cudaStream_t st) {
+                             int capacity, int num_sms, bool decided, cudaStream_t st) {
   const int nctas = hidden_sort_ctas(g.W, g.H);
   const size_t hsmem = (size_t)capacity * 4;
   const size_t ssmem = sense_smem_bytes(capacity);
@@ -729,6 +742,7 @@ cudaError_t launch_hidden_tc(const HidBuffers& b, const StepGeom& g, const Plane
   a.sens = b.sens;
   a.tile_info = b.tile_info;
   a.act = b.act;
+  a.decided = decided && net.hidden == 0 ? 1 : 0;
   if (net.hidden == 0) {
     k_direct_rows<<<num_sms * 12, kDrThreads, 0, st>>>(a);
     return cudaGetLastError();

@@ -94,6 +94,8 @@ struct Pass1Args {
   const float* act_in;       // inject: (H*W,13), or with act_rank: rank-ordered rows of 16
   const uint8_t* act_flag;   // inject: (H*W)
   const int32_t* act_rank;   // nullable: row of each cell in act_in (-1 = no actions)
+  int act_decided;           // with act_rank: 1 -> 8-float decided rows {inv, liq, m0..m2, xmax, kstar, 0},
+                             // 0 -> 16-float rows of the 13 squashed actuators
   float* act_out;            // export: (H*W,13)
   uint8_t* act_out_flag;     // export: (H*W)
   int capacity;
@@ -146,7 +148,7 @@ int hidden_sort_ctas(int W, int H);
 int hidden_tc_nh(int hidden);
 size_t hidden_tc_smem(int hidden);
 cudaError_t launch_hidden_tc(const HidBuffers& b, const StepGeom& g, const Planes& front, const Params& net,
-                             int capacity, int num_sms, cudaStream_t st);
+                             int capacity, int num_sms, bool decided, cudaStream_t st);
 
 int select_chunks(long long n);
 cudaError_t launch_select_cells(const int32_t* gi, long long n, unsigned long long k0, unsigned long long k1, double p,

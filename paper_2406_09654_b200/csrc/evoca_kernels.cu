@@ -74,7 +74,17 @@ __global__ void __launch_bounds__(256) k_physics_rows(const Pass1Args a) {
     CellAct ac{};
     const int r = __ldg(a.act_rank + c);
     ac.acted = r >= 0;
-    if (ac.acted) {
+    if (ac.acted && a.act_decided) {
+      const float4* row = reinterpret_cast<const float4*>(a.act_in + (size_t)r * 8);
+      const float4 r0 = __ldg(row), r1 = __ldg(row + 1);
+      ac.inv = r0.x;
+      ac.liq = r0.y;
+      ac.m0 = r0.z;
+      ac.m1 = r0.w;
+      ac.m2 = r1.x;
+      ac.xmax = r1.y;
+      ac.kstar = __float_as_int(r1.z);
+    } else if (ac.acted) {
       const float4* row = reinterpret_cast<const float4*>(a.act_in + (size_t)r * 16);
       const float4 r0 = __ldg(row), r1 = __ldg(row + 1), r2 = __ldg(row + 2), r3 = __ldg(row + 3);
       ac.inv = r0.x;

@@ -504,13 +504,17 @@ def test_genome_sorted_direct_path_matches_tile_path(genomes, shape):
     net = orc.synth_net(genomes, 0, seed=5)
     phys = orc.Phys(cycle_period=20)
     params = oracle_phys_to_params(phys)
-    a = make_dev(p0, genomes, net)
-    b = make_dev(p0, genomes, net)
+    a = make_dev(p0, genomes, net)  # genome-sorted rows, 8-float decided rows
+    b = make_dev(p0, genomes, net)  # per-tile kernel
+    c = make_dev(p0, genomes, net)  # genome-sorted rows, full 13-actuator rows (export)
     for t in range(3):
         sc = physics.step_scalars(t, params)
-        a.step_raw(sc, t, flags=_lib.F_EXPORT_ACTIONS)
+        a.step_raw(sc, t)
         b.step_raw(sc, t, flags=_lib.F_TILE_NET)
-        assert download(a).equal(download(b)), f"t={t}"
-    a.close()
-    b.close()
+        c.step_raw(sc, t, flags=_lib.F_EXPORT_ACTIONS)
+        want = download(b)
+        assert download(a).equal(want), f"t={t}"
+        assert download(c).equal(want), f"t={t}"
+    for d in (a, b, c):
+        d.close()
     _step_vs_oracle(p0, net, phys, steps=2)
