@@ -615,63 +615,102 @@ __global__ void __launch_bounds__(kNetThreads, 1) k_hid_net(const NetArgs a) {
 // its whole 192-byte row up front (12 independent 16-byte loads in flight)
 // and runs the same packed FFMA2 chains, pairing and k order as the tile
 // kernel (net_direct_unit), so results are bit-identical to it.
-constexpr int kDrThreads = 128;
+constexpr int kDrThreads = 64;   // two rows per thread: every weight broadcast feeds two FMA chains
+constexpr int kDrPitch = 52;  // floats per staged row: 16-byte aligned, conflict-free LDS.128 per lane
+
+__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(tc::smem_u32(smem_dst)), "l"(gsrc) : "memory");
+}
 
 __global__ void __launch_bounds__(kDrThreads) k_direct_rows(const NetArgs a) {
-  __shared__ __align__(16) float W12[kSensors * 12];
-  __shared__ __align__(16) float W1[48];
-  __shared__ __align__(16) float Bs[kOutPad];
+  extern __shared__ __align__(16) float dsm[];
+  float* W12 = dsm;                        // [45][12]
+  float* W1 = W12 + kSensors * 12;         // [48]
+  float* Bs = W1 + 48;                     // [16]
+  float* rows = Bs + kOutPad;              // 2 x [128][kDrPitch]
   const int T = *a.n_tiles;
   const int per = (T + gridDim.x - 1) / gridDim.x;
   const int t0 = blockIdx.x * per, t1 = min(T, t0 + per);
+  if (t0 >= t1) return;
+  // rows of tile t into buffer b: 128 x 12 sixteen-byte copies, 12 per thread
+  auto stage = [&](int t, int b) {
+    const int4 ti = __ldg(a.tile_info + t);
+    float* dst = rows + b * kRows * kDrPitch;
+    for (int i = threadIdx.x; i < kRows * 12; i += kDrThreads) {
+      const int r = i / 12, part = i - r * 12;
+      if (r < ti.z) cp_async16(dst + r * kDrPitch + part * 4, a.sens + (size_t)(ti.y + r) * kK1 + part * 4);
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  stage(t0, 0);
   int cur = -1;
   for (int t = t0; t < t1; ++t) {
+    const int b = (t - t0) & 1;
     const int4 ti = __ldg(a.tile_info + t);
-    const bool valid = (int)threadIdx.x < ti.z;
-    float4 xr[12];
-    const float4* row = reinterpret_cast<const float4*>(a.sens + (size_t)(ti.y + (valid ? threadIdx.x : 0)) * kK1);
-#pragma unroll
-    for (int q = 0; q < 12; ++q) xr[q] = __ldg(row + q);
+    if (t + 1 < t1) {
+      stage(t + 1, b ^ 1);
+      asm volatile("cp.async.wait_group 1;" ::: "memory");
+    } else {
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
+    }
     if (ti.x != cur) {
-      __syncthreads();
       cur = ti.x;
       const float* w12 = a.net.wA + (size_t)cur * kSensors * 12;
       for (int i = threadIdx.x; i < kSensors * 12; i += kDrThreads) W12[i] = __ldg(w12 + i);
       for (int i = threadIdx.x; i < kSensors; i += kDrThreads) W1[i] = __ldg(a.net.wB + (size_t)cur * kSensors + i);
       if (threadIdx.x < kOutPad) Bs[threadIdx.x] = __ldg(a.net.bA + (size_t)cur * kOutPad + threadIdx.x);
-      __syncthreads();
     }
-    u64 acc[6] = {0ull, 0ull, 0ull, 0ull, 0ull, 0ull};
-    float acc12 = 0.0f;
+    __syncthreads();  // this tile's rows (and weights) visible to all threads
+    const float* rbase = rows + b * kRows * kDrPitch;
+    const float4* row0 = reinterpret_cast<const float4*>(rbase + threadIdx.x * kDrPitch);
+    const float4* row1 = reinterpret_cast<const float4*>(rbase + (threadIdx.x + kDrThreads) * kDrPitch);
+    u64 acc[2][6];
+    float acc12[2] = {0.0f, 0.0f};
+#pragma unroll
+    for (int c = 0; c < 2; ++c)
+#pragma unroll
+      for (int p = 0; p < 6; ++p) acc[c][p] = 0ull;
+    float4 c0 = row0[0], c1 = row1[0];
 #pragma unroll
     for (int k = 0; k < kSensors; ++k) {
-      const float4 c4 = xr[k >> 2];
-      const float x = (k & 3) == 0 ? c4.x : ((k & 3) == 1 ? c4.y : ((k & 3) == 2 ? c4.z : c4.w));
+      if ((k & 3) == 0 && k > 0) {
+        c0 = row0[k >> 2];
+        c1 = row1[k >> 2];
+      }
+      const int j = k & 3;
+      const float x0 = j == 0 ? c0.x : (j == 1 ? c0.y : (j == 2 ? c0.z : c0.w));
+      const float x1 = j == 0 ? c1.x : (j == 1 ? c1.y : (j == 2 ? c1.z : c1.w));
       const float4* w4 = reinterpret_cast<const float4*>(W12 + k * 12);
       const float4 wa = w4[0], wb = w4[1], wc = w4[2];
-      ffma2(acc[0], x, pk2(wa.x, wa.y));
-      ffma2(acc[1], x, pk2(wa.z, wa.w));
-      ffma2(acc[2], x, pk2(wb.x, wb.y));
-      ffma2(acc[3], x, pk2(wb.z, wb.w));
-      ffma2(acc[4], x, pk2(wc.x, wc.y));
-      ffma2(acc[5], x, pk2(wc.z, wc.w));
-      acc12 = fmaf(x, W1[k], acc12);
+      const u64 wp[6] = {pk2(wa.x, wa.y), pk2(wa.z, wa.w), pk2(wb.x, wb.y),
+                         pk2(wb.z, wb.w), pk2(wc.x, wc.y), pk2(wc.z, wc.w)};
+      const float w12 = W1[k];
+#pragma unroll
+      for (int p = 0; p < 6; ++p) {
+        ffma2(acc[0][p], x0, wp[p]);
+        ffma2(acc[1][p], x1, wp[p]);
+      }
+      acc12[0] = fmaf(x0, w12, acc12[0]);
+      acc12[1] = fmaf(x1, w12, acc12[1]);
     }
-    if (valid) {  // the actuator row at its sorted position (coalesced across the warp)
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+      const int r = threadIdx.x + c * kDrThreads;
+      if (r >= ti.z) continue;
       float z[13];
 #pragma unroll
       for (int p = 0; p < 6; ++p) {
         float lo, hi;
-        up2(acc[p], lo, hi);
+        up2(acc[c][p], lo, hi);
         z[2 * p] = __fadd_rn(lo, Bs[2 * p]);
         z[2 * p + 1] = __fadd_rn(hi, Bs[2 * p + 1]);
       }
-      z[12] = __fadd_rn(acc12, Bs[12]);
+      z[12] = __fadd_rn(acc12[c], Bs[12]);
       if (a.decided) {  // 32 bytes: the physics needs only these (explore_pick is exact)
         int ks;
         float xm;
         explore_pick(z + 5, ks, xm);
-        float4* dst = reinterpret_cast<float4*>(a.act + (size_t)(ti.y + threadIdx.x) * 8);
+        float4* dst = reinterpret_cast<float4*>(a.act + (size_t)(ti.y + r) * 8);
         dst[0] = make_float4(squash(z[0]), squash(z[1]), squash(z[2]), squash(z[3]));
         dst[1] = make_float4(squash(z[4]), xm, __int_as_float(ks), 0.0f);
       } else {
@@ -679,13 +718,16 @@ __global__ void __launch_bounds__(kDrThreads) k_direct_rows(const NetArgs a) {
 #pragma unroll
         for (int j = 0; j < 13; ++j) v[j] = squash(z[j]);
         v[13] = v[14] = v[15] = 0.0f;
-        float4* dst = reinterpret_cast<float4*>(a.act + (size_t)(ti.y + threadIdx.x) * 16);
+        float4* dst = reinterpret_cast<float4*>(a.act + (size_t)(ti.y + r) * 16);
 #pragma unroll
         for (int q = 0; q < 4; ++q) dst[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
       }
     }
+    __syncthreads();  // buffer b and the weights are free for the next stage / restage
   }
 }
+
+size_t direct_rows_smem() { return (size_t)(kSensors * 12 + 48 + kOutPad + 2 * kRows * kDrPitch) * sizeof(float); }
 
 }  // namespace
 
@@ -744,7 +786,10 @@ cudaError_t launch_hidden_tc(const HidBuffers& b, const StepGeom& g, const Plane
   a.act = b.act;
   a.decided = decided && net.hidden == 0 ? 1 : 0;
   if (net.hidden == 0) {
-    k_direct_rows<<<num_sms * 12, kDrThreads, 0, st>>>(a);
+    const size_t dsm = direct_rows_smem();
+    e = cudaFuncSetAttribute(k_direct_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm);
+    if (e != cudaSuccess) return e;
+    k_direct_rows<<<num_sms * 4, kDrThreads, dsm, st>>>(a);  // 4 x 53 KB of staged rows per SM
     return cudaGetLastError();
   }
   const size_t smem = hidden_tc_smem(net.hidden);
