@@ -144,6 +144,8 @@ def run_ours(args, rank, world, local):
     dev.upload(state.substrate.front)
     dev.sync()
 
+    radiate = (not strips) and cfg.radiation_every > 0  # config 3: field radiation every 50 steps, amortised
+
     def one_step(sc, t, e0=None, e1=None, e2=None):
         if e0 is not None:
             e0.record(stream)
@@ -157,9 +159,15 @@ def run_ours(args, rank, world, local):
         if e1 is not None:
             e1.record(stream)
         dev.pass2(t, stream=sh)
+        dev.swap()
+        if radiate and (t + 1) % cfg.radiation_every == 0:
+            from paper_2406_09654_b200 import radiation
+
+            state.substrate.step_counter = t + 1
+            stream.synchronize()  # the radiation calls run on the context's own stream
+            radiation.field_radiation(state, t + 1, cfg.radiation_p)  # host NEAT + device selection/expression
         if e2 is not None:
             e2.record(stream)
-        dev.swap()
 
     t = 0
     for _ in range(args.warmup):
@@ -208,6 +216,14 @@ def run_ours(args, rank, world, local):
 
     if rank != 0:
         return None
+    # which pass-1 pipeline the library ran (evo_pass1): per-tile fused kernel
+    # for small direct pools, genome-sorted rows otherwise
+    rows_path = cfg.hidden > 0 or max(cfg.capacity, cfg.genomes) > 68
+    p1_name = ("pass 1, genome-sorted rows (sort, sense, "
+               + ("tcgen05 3xTF32 MLP" if cfg.hidden else "CUDA-core net") + ", physics)") if rows_path else \
+        "k_pass1_direct (pass 1: sense+net+physics)"
+    launches_per_step = (8 if rows_path else 2) + (5 if strips else 0)  # strips: halo pack/unpack x2, census epilogue
+    n_rad = sum(1 for i in range(args.steps) if radiate and (t - args.steps + i + 1) % cfg.radiation_every == 0)
     hbm, hbm_kind, pk = peaks()
     step_s = total_ms / 1e3 / args.steps
     value = ncell * world / step_s
@@ -243,7 +259,7 @@ def run_ours(args, rank, world, local):
                    "parallelism": (f"row strips x{world} over a {cfg.height * world}x{cfg.width} torus, NCCL halo "
                                    "exchange + census all_reduce per step") if strips else "single GPU"},
         "roofline": {
-            "kernel": "k_pass1_direct (pass 1, dominant)" if not strips else "strip step",
+            "kernel": (p1_name + ", dominant") if not strips else "strip step",
             "bound": "hbm",
             "achieved": (ncell * BYTES_PER_CELL_PASS1 / k1_s / 1e9) if not strips else achieved_gbs,
             "peak": hbm,
@@ -256,19 +272,20 @@ def run_ours(args, rank, world, local):
             "step": {"achieved": achieved_gbs, "frac": achieved_gbs / hbm,
                      "algorithmic_bytes_per_cell": BYTES_PER_CELL},
             "kernels": [
-                {"name": "k_pass1_direct (pass 1: sense+net+physics)" if not strips else
+                {"name": p1_name if not strips else
                  "strip step (exchanges + pass 1 + pass 2 + census)", "ms": k1_s * 1e3, "share": k1 / total_ms,
                  "fp32_tflops": ncell * FLOP_PER_CELL_DIRECT / k1_s / 1e12 if cfg.hidden == 0 else None,
                  "fp32_peak_tflops_derived": fp32_peak},
-                {"name": "k_resolve (pass 2: explore resolve+adoption+census)", "ms": k2_s * 1e3,
-                 "share": k2 / total_ms},
+                {"name": "k_resolve (pass 2: explore resolve+adoption+census)"
+                 + (" + field radiation every %d steps" % cfg.radiation_every if radiate else ""),
+                 "ms": k2_s * 1e3, "share": k2 / total_ms},
             ],
         },
         "e2e": {"value": ncell * world * e2e_steps / e2e_s, "unit": "cell-updates/s",
                 "api": "paper_2406_09654_b200.engine.step(state) on host-resident planes",
                 "h2d_bytes_per_step": ncell * 25 + state.pool.capacity * 9,
                 "d2h_bytes_per_step": ncell * 25 + state.pool.capacity * 4 + 16},
-        "gpu_launches": (3 if strips else 2) * args.steps,
+        "gpu_launches": launches_per_step * args.steps + 6 * n_rad,
         "clocks": clk,
         "adoptions_last_step": int(adoptions),
     }
