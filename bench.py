@@ -196,19 +196,52 @@ def run_ours(args, rank, world, local):
         total_ms = float(tt.item())
     adoptions, _ = dev.read_stats()
 
-    # e2e through the public API: engine.step on a host-resident state
-    # (upload of the front planes, both passes, download of the new planes,
-    # census read-back and host pool update, every step).
-    e2e_state = engine.baseline_state(args.config, seed=args.seed + rank)
-    engine.device_of(e2e_state, device=local)
+    # e2e through the public API with host-resident planes, every step: H2D of
+    # the front planes, the step, D2H of the new planes, census read-back.
+    # One GPU: engine.step (the reference's drop-in entry point).  N GPUs: each
+    # rank's row strip through DeviceStrip (halo exchanges + census
+    # all_reduce inside), with its own page-locked host planes.
     e2e_steps = max(3, min(args.steps, 20))
-    engine.step(e2e_state)  # warm
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    for _ in range(e2e_steps):
-        engine.step(e2e_state)
-    torch.cuda.synchronize()
-    e2e_s = time.perf_counter() - t0
+    if strips:
+        row0, h = plan.rows(rank)
+        hf = state.substrate.front
+        E = np.ascontiguousarray(hf.channels["energy"][0][:h])
+        I = np.ascontiguousarray(hf.channels["infrastructure"][0][:h])
+        Cm = np.ascontiguousarray(hf.channels["communication"][:, :h])
+        gi = np.ascontiguousarray(hf.genome_index[:h])
+        rot = np.ascontiguousarray(hf.rotation[:h])
+        for arr in (E, I, Cm, gi, rot):
+            dev.lib.evo_host_register(arr.ctypes.data_as(__import__("ctypes").c_void_p), arr.nbytes)
+
+        def e2e_step(t):
+            dev.upload_arrays(E, I, Cm, gi, rot)
+            strip.step(physics.step_scalars(t, phys), t)
+            dev.download_arrays(E, I, Cm, gi, rot)
+            dev.read_census()
+
+        e2e_step(0)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for i in range(e2e_steps):
+            e2e_step(i + 1)
+        torch.cuda.synchronize()
+        e2e_s = time.perf_counter() - t0
+        for arr in (E, I, Cm, gi, rot):
+            dev.lib.evo_host_unregister(arr.ctypes.data_as(__import__("ctypes").c_void_p))
+        e2e_api = "DeviceStrip.step with evo_upload_planes / evo_download_planes of the rank's strip"
+        e2e_cells = h * cfg.width
+    else:
+        e2e_state = engine.baseline_state(args.config, seed=args.seed + rank)
+        engine.device_of(e2e_state, device=local)
+        engine.step(e2e_state)  # warm
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(e2e_steps):
+            engine.step(e2e_state)
+        torch.cuda.synchronize()
+        e2e_s = time.perf_counter() - t0
+        e2e_api = "paper_2406_09654_b200.engine.step(state) on host-resident planes"
+        e2e_cells = ncell
     if world > 1:
         tt = torch.tensor([e2e_s], device="cuda", dtype=torch.float64)
         torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
@@ -276,15 +309,16 @@ def run_ours(args, rank, world, local):
                  "strip step (exchanges + pass 1 + pass 2 + census)", "ms": k1_s * 1e3, "share": k1 / total_ms,
                  "fp32_tflops": ncell * FLOP_PER_CELL_DIRECT / k1_s / 1e12 if cfg.hidden == 0 else None,
                  "fp32_peak_tflops_derived": fp32_peak},
+            ] + ([] if strips else [
                 {"name": "k_resolve (pass 2: explore resolve+adoption+census)"
                  + (" + field radiation every %d steps" % cfg.radiation_every if radiate else ""),
                  "ms": k2_s * 1e3, "share": k2 / total_ms},
-            ],
+            ]),
         },
         "e2e": {"value": ncell * world * e2e_steps / e2e_s, "unit": "cell-updates/s",
-                "api": "paper_2406_09654_b200.engine.step(state) on host-resident planes",
-                "h2d_bytes_per_step": ncell * 25 + state.pool.capacity * 9,
-                "d2h_bytes_per_step": ncell * 25 + state.pool.capacity * 4 + 16},
+                "api": e2e_api,
+                "h2d_bytes_per_step": (e2e_cells * 25 + state.pool.capacity * 9) * world,
+                "d2h_bytes_per_step": (e2e_cells * 25 + state.pool.capacity * 4 + 16) * world},
         "gpu_launches": launches_per_step * args.steps + 6 * n_rad,
         "clocks": clk,
         "adoptions_last_step": int(adoptions),
