@@ -4,23 +4,26 @@
 // and the fused physics tail, per 32x32 tile.  The tile plus its 1-cell Moore
 // halo of the five sensed front planes (E, I, C0..C2) is staged in shared
 // memory; occupied cells are bucketed by genome slot inside the CTA (counting
-// sort, groups padded to cell quads) so that each thread evaluates four cells
-// of ONE genome and every weight fetched feeds four fixed-order fp32 FMA
-// chains.  Sensors are gathered from shared memory in the rotation order
-// PERM[rot] (physics.py:48-62, engine.py:164-177) and never touch HBM.
-// Actions land in shared memory in spatial order; the physics tail then runs
-// in spatial order with coalesced stores, using only __f*_rn intrinsics (no
-// FMA contraction) in the reference's op order so that, given the same
-// actions, results are bit-identical to NumPy.
-//   k_pass1_direct  hot path: persistent CTA per SM, direct 45->13 net with
-//                   packed FFMA2 (fma.rn.f32x2), weights L1-resident, next
-//                   tile's halo prefetched into registers during compute.
-//   k_pass1_generic parity / hidden-layer path: injected actions, the
-//                   45->H(tanh)->13 reference net.
+// sort, each genome group padded to an even number of two-cell units) so
+// that each thread evaluates two cells of ONE genome and every weight loaded
+// feeds two fixed-order fp32 FMA chains.  Sensors are gathered from shared
+// memory in the rotation order PERM[rot] (physics.py:48-62,
+// engine.py:164-177) and never touch HBM.  Actions land in shared memory in
+// spatial order; the physics tail then runs in spatial order with coalesced
+// stores, using only __f*_rn intrinsics (no FMA contraction) in the
+// reference's op order so that, given the same actions, results are
+// bit-identical to NumPy.
+//   k_pass1_direct  hot path (direct 45->13 net, pools <= 68 slots):
+//                   persistent CTA per SM, weight table resident in shared
+//                   memory, packed FFMA2 (fma.rn.f32x2), next tile's halo
+//                   prefetched into L2 and registers during compute.
+//   k_pass1_generic injected actions (parity tier A / the phase-function API)
+//                   and the CUDA-core 45->H(tanh)->13 net.
+//   k_physics_rows  physics of the genome-sorted paths (evoca_hidden_tc.cu).
 //
 // Pass 2 (k_resolve, physics.py:286-343 + 395-404): each target cell PULLS
-// the shipments aimed at it from its 8 neighbours' one-hot proposal bytes.  Arrivals
-// are ordered by the packed 64-bit key (bits(q) << 32) | (0xFFFFFFFF -
+// the shipments aimed at it from its 8 neighbours' one-hot proposal bytes.
+// Arrivals are ordered by the packed 64-bit key (bits(q) << 32) | (0xFFFFFFFF -
 // global_source_index), i.e. q descending then source ascending - the
 // reference's lexsort order - and summed sequentially in that order
 // (bit-exact, deterministic, no atomics); the maximal key is the winner,
