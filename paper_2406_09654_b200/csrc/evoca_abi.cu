@@ -229,7 +229,6 @@ int ensure_hidden_tc(evo_ctx* c) {
   CK(c->alloc(&c->hid.cta_hist, (size_t)evo::hidden_sort_ctas(c->W, c->H) * cap));
   CK(c->alloc(&c->hid.tile_info, n / 128 + cap + 1));
   CK(c->alloc(&c->hid.act, n * 16));
-  CK(c->alloc(&c->hid.flag, 1));
   CK(c->alloc(&c->hid.rank, n));
   CK(c->alloc(&c->hid.sens, n * 48));
   if (!c->num_sms) CK(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, c->device));

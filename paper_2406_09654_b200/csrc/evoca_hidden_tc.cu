@@ -51,12 +51,11 @@ constexpr int kNetThreads = 256;
 constexpr int kTmemCols = 512;
 // The TF32 MMA accumulates in TMEM with less than FP32 rounding accuracy
 // (tools/microbench/tc_split.cu: rms error 3x an FP32 FMA chain, whatever the
-// operand split).  Partial sums therefore go to separate accumulators - one
-// per two K=8 steps in layer 1 (3 x nh columns), one per K step in layer 2
-// (nh/8 x 16 columns, reusing layer 1's columns once its epilogue has read
-// them) - and are added in FP32 on the CUDA cores in k order: accuracy then
-// matches (layer 1) or beats (layer 2) a sequential FP32 FMA chain.
-constexpr int kL1StepsPerAcc = 2;
+// operand split).  Partial sums therefore go to separate accumulators - two
+// of three K=8 steps each in layer 1, one per two K steps in layer 2 (see the
+// TMEM map at k_hid_net) - and are added in FP32 on the CUDA cores in k order;
+// H=128 actions stay within 4e-6 of the float64 oracle (the CUDA-core FP32
+// net: 4.8e-6).
 
 // Deterministic counting sort of the occupied cells by slot, without hot
 // global atomics: each CTA owns kSortTiles consecutive 32x32 tiles (tile

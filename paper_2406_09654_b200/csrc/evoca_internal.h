@@ -139,8 +139,7 @@ struct HidBuffers {
   int32_t* cta_hist;  // [sort CTAs][cap] per-CTA slot histograms -> row bases
   float* sens;       // [ncell][48]
   int4* tile_info;     // [ncell / 128 + cap] {slot, first row, rows, 0} per 128-row tile
-  float* act;        // [ncell][16] actuator rows in sorted-row order (13 used)
-  uint8_t* flag;     // unused by the row paths (kept for layout stability)
+  float* act;        // [ncell][16] (or [ncell][8] decided) actuator rows in sorted-row order
   int32_t* rank;     // [ncell] sorted row of each cell, -1 = empty
 };
 bool hidden_tc_supported(int hidden);
