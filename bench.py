@@ -240,7 +240,7 @@ def run_ours(args, rank, world, local):
             engine.step(e2e_state)
         torch.cuda.synchronize()
         e2e_s = time.perf_counter() - t0
-        e2e_api = "paper_2406_09654_b200.engine.step(state) on host-resident planes"
+        e2e_api = "paper_2406_09654_b200.engine.step(state) on host-resident planes (evo_step_host, banded H2D/step/D2H)"
         e2e_cells = ncell
     if world > 1:
         tt = torch.tensor([e2e_s], device="cuda", dtype=torch.float64)

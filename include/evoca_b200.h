@@ -113,6 +113,22 @@ EVO_API int evo_set_source_map(evo_ctx* ctx, const float* map);
  * sense + net + energy + invest/liquidate + comm + explore proposal (pass 1),
  * explore resolve + adoption + census (pass 2), front/back swap. */
 EVO_API int evo_step(evo_ctx* ctx, const evo_scalars* s, int64_t t, int phases, int flags, void* stream);
+/* One step of a HOST-resident state, the drop-in for engine.step on a
+ * SimState whose planes live in host memory (engine.py:233-248 on the
+ * reference's numpy double buffer, substrate.py:52-110): uploads the front planes
+ * (E, I, C as (3,H,W), genome_index, rotation), steps, and writes the new
+ * planes to the *_out arrays, pipelined over `bands` row bands (0 = auto) so
+ * the host->device copy, the two passes and the device->host copy overlap.
+ * Genome / rotation ranges are checked on the device (EVO_EINVAL, outputs
+ * undefined, device state not advanced).  Optional outputs: the census counts
+ * (capacity int32; not with EVO_F_NO_CENSUS) and {adoptions, extinctions}.
+ * Flags: 0 or EVO_F_RECORD_EVENTS | EVO_F_NO_CENSUS (host radiation).  The
+ * call returns once the outputs are written; `stream` orders it after prior
+ * work.  Host planes should be page-locked (evo_host_register) for DMA. */
+EVO_API int evo_step_host(evo_ctx* ctx, const evo_scalars* s, int64_t t, int flags, const float* E, const float* I,
+                          const float* C, const int32_t* gi, const uint8_t* rot, float* E_out, float* I_out,
+                          float* C_out, int32_t* gi_out, uint8_t* rot_out, int32_t* counts, int64_t* stats,
+                          int bands, void* stream);
 /* k consecutive steps t0..t0+k-1 with per-step scalars s[0..k-1]. */
 EVO_API int evo_run(evo_ctx* ctx, const evo_scalars* s, int64_t t0, int k, void* stream);
 /* The two launches of a step, for halo exchange between them (multi-GPU) and

@@ -8,6 +8,8 @@
 #include <cuda_runtime.h>
 
 #include <cstdio>
+#include <cstdlib>
+#include <chrono>
 #include <algorithm>
 #include <cstring>
 #include <string>
@@ -70,6 +72,14 @@ struct evo_ctx {
   const int32_t* exp_rank = nullptr;  // rank-indexed rows (genome-sorted paths)
   bool have_export = false, have_events = false, have_src_map = false;
   cudaStream_t stream = nullptr;
+  // host-pipelined step (evo_step_host; created on first use)
+  static constexpr int kMaxBands = 64;
+  cudaStream_t s_in = nullptr, s_out = nullptr;
+  cudaEvent_t ev_start = nullptr, ev_out = nullptr, ev_in[kMaxBands] = {}, ev_p2[kMaxBands + 2] = {};
+  static constexpr size_t kTraceEvents = 512;
+  cudaEvent_t tev[kTraceEvents] = {};
+  int* bad = nullptr;
+  unsigned char* h_stage = nullptr;  // pinned: bad flag, stats, census counts
   std::vector<void*> allocs;
 
   long long ncell() const { return (long long)W * H; }
@@ -166,11 +176,16 @@ int create_impl(evo_ctx** out, int width, int height, long long row0, int hg, in
   e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
   if (e != cudaSuccess) return bail(e, "cudaStreamCreate");
   const size_t n = (size_t)c->stride;
+  // E, I, C0..C2 and the genome plane of a buffer are one block of six
+  // equally spaced 4-byte planes, so a row band of all six moves between host
+  // and device in one 2-D copy when the host planes are laid out alike
   for (int b = 0; b < 2; ++b) {
-    if ((e = c->alloc(&c->buf[b].E, n)) != cudaSuccess) return bail(e, "alloc E");
-    if ((e = c->alloc(&c->buf[b].I, n)) != cudaSuccess) return bail(e, "alloc I");
-    if ((e = c->alloc(&c->buf[b].C, 3 * n)) != cudaSuccess) return bail(e, "alloc C");
-    if ((e = c->alloc(&c->buf[b].gi, n)) != cudaSuccess) return bail(e, "alloc gi");
+    float* blk = nullptr;
+    if ((e = c->alloc(&blk, 6 * n)) != cudaSuccess) return bail(e, "alloc planes");
+    c->buf[b].E = blk;
+    c->buf[b].I = blk + n;
+    c->buf[b].C = blk + 2 * n;
+    c->buf[b].gi = reinterpret_cast<int32_t*>(blk + 5 * n);
     if ((e = c->alloc(&c->buf[b].rot, n)) != cudaSuccess) return bail(e, "alloc rot");
   }
   if ((e = cudaMemset(c->buf[0].gi, 0xFF, n * sizeof(int32_t))) != cudaSuccess) return bail(e, "memset gi");
@@ -243,6 +258,142 @@ int ensure_events(evo_ctx* c) {
   return 0;
 }
 
+int ensure_pipe(evo_ctx* c) {
+  if (c->s_in) return 0;
+  CK(cudaStreamCreateWithFlags(&c->s_in, cudaStreamNonBlocking));
+  CK(cudaStreamCreateWithFlags(&c->s_out, cudaStreamNonBlocking));
+  CK(cudaEventCreateWithFlags(&c->ev_start, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&c->ev_out, cudaEventDisableTiming));
+  for (cudaEvent_t& e : c->ev_in) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  for (cudaEvent_t& e : c->ev_p2) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  if (std::getenv("EVO_PIPE_TRACE"))
+    for (size_t i = 0; i < evo_ctx::kTraceEvents; ++i) CK(cudaEventCreate(&c->tev[i]));
+  CK(c->alloc(&c->bad, 1));
+  CK(cudaHostAlloc(reinterpret_cast<void**>(&c->h_stage), 32 + (size_t)c->cap * 4, cudaHostAllocDefault));
+  return 0;
+}
+
+// A run of rows of the strip viewed as a strip of its own: plane pointers
+// shifted by `off` = first row * W so that the view's ghost rows are the
+// neighbouring real rows (row-band pipelining of evo_step_host).
+struct View {
+  evo::StepGeom g;
+  evo::Planes front, back;
+  evo::Mid mid;
+  long long off;
+};
+
+evo::Planes shifted(const evo::Planes& p, long long o) {
+  evo::Planes q;
+  q.E = p.E + o;
+  q.I = p.I + o;
+  q.C = p.C + o;
+  q.gi = p.gi + o;
+  q.rot = p.rot + o;
+  return q;
+}
+
+View full_view(const evo_ctx* c) {
+  View v;
+  v.g = c->geom();
+  v.front = c->buf[c->front];
+  v.back = c->buf[c->front ^ 1];
+  v.mid = c->mid;
+  v.off = 0;
+  return v;
+}
+
+View band_view(const evo_ctx* c, int r0, int rows) {
+  View v = full_view(c);
+  const long long o = (long long)r0 * c->W;
+  v.g.H = rows;
+  v.g.row0 = c->row0 + r0;
+  v.g.own_ghosts = 0;
+  v.front = shifted(v.front, o);
+  v.back = shifted(v.back, o);
+  v.mid.I += o;
+  v.mid.gi += o;
+  v.mid.rp += o;
+  v.mid.q += o;
+  v.off = o;
+  return v;
+}
+
+int pass1_view(evo_ctx* c, const View& v, const evo_scalars* s, int phases, int flags, long long* stats,
+               cudaStream_t st) {
+  if (!s) return fail(EVO_EINVAL, "null scalars");
+  const bool inject = flags & EVO_F_INJECT_ACTIONS;
+  bool exp = (flags & EVO_F_EXPORT_ACTIONS) && !inject;
+  if (inject && !c->act_in) return fail(EVO_EINVAL, "EVO_F_INJECT_ACTIONS without evo_set_actions");
+  if ((inject || exp) && v.off != 0) return fail(EVO_EINVAL, "action injection/export needs a whole-strip pass");
+  // hidden-layer nets run on the tensor cores (sense -> genome buckets ->
+  // tcgen05 3xTF32 MLP -> actuator rows), the physics as pass 1 with those rows
+  const bool tc_net = !inject && c->hidden > 0 && evo::hidden_tc_supported(c->hidden) &&
+                      !(flags & EVO_F_CUDA_CORE_NET);
+  // direct nets of large pools (weights do not fit next to the tile in shared
+  // memory): genome-sorted rows instead of per-tile weight fetches
+  const bool rows_net = !inject && c->hidden == 0 && c->cap > evo::kSmemWeightSlotsAbi &&
+                        !(flags & EVO_F_TILE_NET);
+  if (exp && !tc_net && !rows_net) {
+    if (int r = ensure_actions_out(c)) return r;
+  }
+  if (tc_net || rows_net) {
+    if (int r = ensure_hidden_tc(c)) return r;
+    CK(evo::launch_hidden_tc(c->hid, v.g, v.front, c->params(), c->cap, c->num_sms, /*decided=*/!exp, st));
+  }
+  const bool via_rows = tc_net || rows_net;
+  c->have_export = exp || via_rows;
+  c->exp_rows = via_rows ? c->hid.act : c->act_out;
+  c->exp_flag = via_rows ? nullptr : c->act_out_flag;
+  c->exp_rank = via_rows ? c->hid.rank : nullptr;
+  evo::Pass1Args a;
+  a.g = v.g;
+  a.front = v.front;
+  a.back = v.back;
+  a.mid = v.mid;
+  a.net.hidden = c->hidden;
+  a.net.hpad = c->hpad;
+  a.net.wA = c->wA;
+  a.net.bA = c->bA;
+  a.net.wB = c->wB;
+  a.net.bB = c->bB;
+  a.s = to_scalars(*s);
+  a.phases = phases;
+  a.src_map = c->have_src_map ? c->src_map + v.off : nullptr;
+  a.act_in = via_rows ? c->hid.act : c->act_in;
+  a.act_flag = via_rows ? nullptr : c->act_in_flag;
+  a.act_rank = via_rows ? c->hid.rank : nullptr;
+  a.act_decided = via_rows && c->hidden == 0 && !exp ? 1 : 0;
+  a.act_out = c->act_out;
+  a.act_out_flag = c->act_out_flag;
+  a.capacity = c->cap;
+  a.stats = stats;
+  CK(evo::launch_pass1(a, inject || via_rows, exp && !via_rows, st));
+  return 0;
+}
+
+int pass2_view(evo_ctx* c, const View& v, int64_t t, int flags, int run_census, cudaStream_t st) {
+  const bool rec = flags & EVO_F_RECORD_EVENTS;
+  if (rec) {
+    if (int r = ensure_events(c)) return r;
+  }
+  c->have_events = rec;
+  evo::Pass2Args a;
+  a.g = v.g;
+  a.back = v.back;
+  a.rot_front = v.front.rot;
+  a.mid = v.mid;
+  a.census = c->census;
+  a.ev.src = rec ? c->ev_src + v.off : nullptr;
+  a.ev.q = rec ? c->ev_q + v.off : nullptr;
+  a.ev.def = rec ? c->ev_def + v.off : nullptr;
+  a.capacity = c->cap;
+  a.run_census = run_census;
+  a.t = t;
+  CK(evo::launch_pass2(a, st));
+  return 0;
+}
+
 }  // namespace
 
 extern "C" {
@@ -264,6 +415,19 @@ EVO_API int evo_destroy(evo_ctx* c) {
   if (!c) return 0;
   cudaSetDevice(c->device);
   cudaStreamSynchronize(c->stream);
+  if (c->s_in) {
+    cudaStreamSynchronize(c->s_in);
+    cudaStreamSynchronize(c->s_out);
+    cudaStreamDestroy(c->s_in);
+    cudaStreamDestroy(c->s_out);
+    cudaEventDestroy(c->ev_start);
+    cudaEventDestroy(c->ev_out);
+    for (cudaEvent_t e : c->ev_in) cudaEventDestroy(e);
+    for (cudaEvent_t e : c->ev_p2) cudaEventDestroy(e);
+    cudaFreeHost(c->h_stage);
+    for (size_t i = 0; i < evo_ctx::kTraceEvents; ++i)
+      if (c->tev[i]) cudaEventDestroy(c->tev[i]);
+  }
   for (void* p : c->allocs) cudaFree(p);
   cudaStreamDestroy(c->stream);
   delete c;
@@ -423,79 +587,13 @@ EVO_API int evo_set_source_map(evo_ctx* c, const float* map) {
 
 EVO_API int evo_pass1(evo_ctx* c, const evo_scalars* s, int64_t t, int phases, int flags, void* stream) {
   if (int r = check_ctx(c)) return r;
-  if (!s) return fail(EVO_EINVAL, "null scalars");
   (void)t;
-  const bool inject = flags & EVO_F_INJECT_ACTIONS;
-  bool exp = (flags & EVO_F_EXPORT_ACTIONS) && !inject;
-  if (inject && !c->act_in) return fail(EVO_EINVAL, "EVO_F_INJECT_ACTIONS without evo_set_actions");
-  // hidden-layer nets run on the tensor cores (sense -> genome buckets ->
-  // tcgen05 3xTF32 MLP -> actuator rows), the physics as pass 1 with those rows
-  const bool tc_net = !inject && c->hidden > 0 && evo::hidden_tc_supported(c->hidden) &&
-                      !(flags & EVO_F_CUDA_CORE_NET);
-  // direct nets of large pools (weights do not fit next to the tile in shared
-  // memory): genome-sorted rows instead of per-tile weight fetches
-  const bool rows_net = !inject && c->hidden == 0 && c->cap > evo::kSmemWeightSlotsAbi &&
-                        !(flags & EVO_F_TILE_NET);
-  if (exp && !tc_net && !rows_net) {
-    if (int r = ensure_actions_out(c)) return r;
-  }
-  if (tc_net || rows_net) {
-    if (int r = ensure_hidden_tc(c)) return r;
-    CK(evo::launch_hidden_tc(c->hid, c->geom(), c->buf[c->front], c->params(), c->cap, c->num_sms,
-                             /*decided=*/!exp, pick(c, stream)));
-  }
-  const bool via_rows = tc_net || rows_net;
-  c->have_export = exp || via_rows;
-  c->exp_rows = via_rows ? c->hid.act : c->act_out;
-  c->exp_flag = via_rows ? nullptr : c->act_out_flag;
-  c->exp_rank = via_rows ? c->hid.rank : nullptr;
-  evo::Pass1Args a;
-  a.g = c->geom();
-  a.front = c->buf[c->front];
-  a.back = c->buf[c->front ^ 1];
-  a.mid = c->mid;
-  a.net.hidden = c->hidden;
-  a.net.hpad = c->hpad;
-  a.net.wA = c->wA;
-  a.net.bA = c->bA;
-  a.net.wB = c->wB;
-  a.net.bB = c->bB;
-  a.s = to_scalars(*s);
-  a.phases = phases;
-  a.src_map = c->have_src_map ? c->src_map : nullptr;
-  a.act_in = via_rows ? c->hid.act : c->act_in;
-  a.act_flag = via_rows ? nullptr : c->act_in_flag;
-  a.act_rank = via_rows ? c->hid.rank : nullptr;
-  a.act_decided = via_rows && c->hidden == 0 && !exp ? 1 : 0;
-  a.act_out = c->act_out;
-  a.act_out_flag = c->act_out_flag;
-  a.capacity = c->cap;
-  a.stats = c->census.stats;
-  CK(evo::launch_pass1(a, inject || via_rows, exp && !via_rows, pick(c, stream)));
-  return 0;
+  return pass1_view(c, full_view(c), s, phases, flags, c->census.stats, pick(c, stream));
 }
 
 EVO_API int evo_pass2(evo_ctx* c, int64_t t, int flags, void* stream) {
   if (int r = check_ctx(c)) return r;
-  const bool rec = flags & EVO_F_RECORD_EVENTS;
-  if (rec) {
-    if (int r = ensure_events(c)) return r;
-  }
-  c->have_events = rec;
-  evo::Pass2Args a;
-  a.g = c->geom();
-  a.back = c->buf[c->front ^ 1];
-  a.rot_front = c->buf[c->front].rot;
-  a.mid = c->mid;
-  a.census = c->census;
-  a.ev.src = rec ? c->ev_src : nullptr;
-  a.ev.q = c->ev_q;
-  a.ev.def = c->ev_def;
-  a.capacity = c->cap;
-  a.run_census = (flags & EVO_F_NO_CENSUS) ? 0 : 1;
-  a.t = t;
-  CK(evo::launch_pass2(a, pick(c, stream)));
-  return 0;
+  return pass2_view(c, full_view(c), t, flags, (flags & EVO_F_NO_CENSUS) ? 0 : 1, pick(c, stream));
 }
 
 EVO_API int evo_census_finish(evo_ctx* c, int64_t t, void* stream) {
@@ -515,6 +613,186 @@ EVO_API int evo_step(evo_ctx* c, const evo_scalars* s, int64_t t, int phases, in
   if (int r = evo_pass1(c, s, t, phases, flags, stream)) return r;
   if (int r = evo_pass2(c, t, flags, stream)) return r;
   return evo_swap(c);
+}
+
+EVO_API int evo_step_host(evo_ctx* c, const evo_scalars* s, int64_t t, int flags, const float* E, const float* I,
+                          const float* C, const int32_t* gi, const uint8_t* rot, float* E_out, float* I_out,
+                          float* C_out, int32_t* gi_out, uint8_t* rot_out, int32_t* counts, int64_t* stats,
+                          int bands, void* stream) {
+  if (int r = check_ctx(c)) return r;
+  if (c->strip) return fail(EVO_EINVAL, "evo_step_host steps a single-strip context");
+  if (!s) return fail(EVO_EINVAL, "null scalars");
+  if (!E || !I || !C || !gi || !rot || !E_out || !I_out || !C_out || !gi_out || !rot_out)
+    return fail(EVO_EINVAL, "null plane pointer");
+  if (flags & (EVO_F_INJECT_ACTIONS | EVO_F_EXPORT_ACTIONS))
+    return fail(EVO_EINVAL, "action injection/export is not available in the host-pipelined step");
+  if (int r = ensure_pipe(c)) return r;
+  if (c->hidden > 0 || c->cap > evo::kSmemWeightSlotsAbi) {
+    if (int r = ensure_hidden_tc(c)) return r;
+  }
+  if ((flags & EVO_F_RECORD_EVENTS)) {
+    if (int r = ensure_events(c)) return r;
+  }
+  const int W = c->W, H = c->H;
+  const long long n = c->ncell();
+  // Row bands.  Band nb-1 is the last 32 rows and is uploaded first (it holds
+  // the torus row above row 0); bands 0..nb-2 split the rest in whole 32-row
+  // tiles.  Pass 1 chunk b = rows [R_b - 32, R_{b+1} - 32) needs only bands
+  // <= b; pass 2 chunk b = rows [R_b - 33, R_{b+1} - 33) needs only pass-1
+  // chunks <= b; row 0 and the last chunk close the seam at the end.
+  int nb = bands > 0 ? bands : 4;
+  nb = std::min(nb, evo_ctx::kMaxBands);
+  if (H - 32 < 64) nb = 1;
+  std::vector<int> R;  // band starts, R[nb] = H
+  if (nb == 1) {
+    R = {0, H};
+  } else {
+    const int main_rows = H - 32;
+    int per = (main_rows + (nb - 1) - 1) / (nb - 1);
+    per = std::max(64, (per + 31) / 32 * 32);
+    for (int r0 = 0; r0 < main_rows; r0 += per) R.push_back(r0);
+    R.push_back(H - 32);
+    R.push_back(H);
+    nb = (int)R.size() - 1;
+  }
+  const cudaStream_t st = pick(c, stream);
+  // EVO_PIPE_TRACE=1: per-band timeline on stderr (diagnostics)
+  static const bool trace = std::getenv("EVO_PIPE_TRACE") != nullptr;
+  std::vector<std::string> tname;
+  auto markn = [&](cudaStream_t q, const std::string& nm) {
+    if (!trace || tname.size() >= evo_ctx::kTraceEvents) return;
+    cudaEventRecord(c->tev[tname.size()], q);
+    tname.push_back(nm);
+  };
+  const evo::Planes F = c->buf[c->front], B = c->buf[c->front ^ 1];
+  const size_t pitch = (size_t)c->stride * 4, hpitch = (size_t)n * 4;
+  // host planes E, I, C0..C2, genome equally spaced (this package's PlaneSet
+  // allocates them as one block): one 2-D copy per band instead of five
+  auto block6 = [&](const void* e, const void* i, const void* cc, const void* g) {
+    const char* b0 = static_cast<const char*>(e);
+    return static_cast<const char*>(i) == b0 + hpitch && static_cast<const char*>(cc) == b0 + 2 * hpitch &&
+           static_cast<const char*>(g) == b0 + 5 * hpitch;
+  };
+  const bool in6 = block6(E, I, C, gi), out6 = block6(E_out, I_out, C_out, gi_out);
+  auto h2d = [&](int b) -> int {
+    const size_t o = (size_t)(R[b] + 1) * W, h = (size_t)R[b] * W, m = (size_t)(R[b + 1] - R[b]) * W;
+    if (in6) {
+      CK(cudaMemcpy2DAsync(F.E + o, pitch, E + h, hpitch, m * 4, 6, cudaMemcpyHostToDevice, c->s_in));
+    } else {
+      CK(cudaMemcpyAsync(F.E + o, E + h, m * 4, cudaMemcpyHostToDevice, c->s_in));
+      CK(cudaMemcpyAsync(F.I + o, I + h, m * 4, cudaMemcpyHostToDevice, c->s_in));
+      CK(cudaMemcpy2DAsync(F.C + o, pitch, C + h, hpitch, m * 4, 3, cudaMemcpyHostToDevice, c->s_in));
+      CK(cudaMemcpyAsync(F.gi + o, gi + h, m * 4, cudaMemcpyHostToDevice, c->s_in));
+    }
+    CK(cudaMemcpyAsync(F.rot + o, rot + h, m, cudaMemcpyHostToDevice, c->s_in));
+    CK(cudaEventRecord(c->ev_in[b], c->s_in));
+    markn(c->s_in, "h2d " + std::to_string(b));
+    return 0;
+  };
+  auto check = [&](int b) -> int {
+    const size_t o = (size_t)(R[b] + 1) * W, m = (size_t)(R[b + 1] - R[b]) * W;
+    CK(evo::launch_check_cells(F.gi + o, F.rot + o, (long long)m, c->cap, c->bad, st));
+    return 0;
+  };
+  int n_out = 0;
+  auto d2h = [&](int r0, int r1) -> int {
+    if (r1 <= r0) return 0;
+    const size_t o = (size_t)(r0 + 1) * W, h = (size_t)r0 * W, m = (size_t)(r1 - r0) * W;
+    const int k = n_out++;
+    CK(cudaEventRecord(c->ev_p2[k], st));
+    CK(cudaStreamWaitEvent(c->s_out, c->ev_p2[k], 0));
+    if (out6) {
+      CK(cudaMemcpy2DAsync(E_out + h, hpitch, B.E + o, pitch, m * 4, 6, cudaMemcpyDeviceToHost, c->s_out));
+      CK(cudaMemcpyAsync(rot_out + h, B.rot + o, m, cudaMemcpyDeviceToHost, c->s_out));
+    } else {
+      CK(cudaMemcpyAsync(E_out + h, B.E + o, m * 4, cudaMemcpyDeviceToHost, c->s_out));
+      CK(cudaMemcpyAsync(I_out + h, B.I + o, m * 4, cudaMemcpyDeviceToHost, c->s_out));
+      CK(cudaMemcpy2DAsync(C_out + h, hpitch, B.C + o, pitch, m * 4, 3, cudaMemcpyDeviceToHost, c->s_out));
+      CK(cudaMemcpyAsync(gi_out + h, B.gi + o, m * 4, cudaMemcpyDeviceToHost, c->s_out));
+      CK(cudaMemcpyAsync(rot_out + h, B.rot + o, m, cudaMemcpyDeviceToHost, c->s_out));
+    }
+    markn(c->s_out, "d2h " + std::to_string(r0) + "-" + std::to_string(r1));
+    return 0;
+  };
+  auto p1 = [&](int r0, int r1) -> int {
+    if (r1 <= r0) return 0;
+    if (int r = pass1_view(c, band_view(c, r0, r1 - r0), s, EVO_PH_ALL, flags, r0 == 0 ? c->census.stats : nullptr,
+                           st))
+      return r;
+    markn(st, "pass1 " + std::to_string(r0) + "-" + std::to_string(r1));
+    return 0;
+  };
+  auto p2 = [&](int r0, int r1) -> int {
+    if (r1 <= r0) return 0;
+    if (int r = pass2_view(c, band_view(c, r0, r1 - r0), t, flags, 0, st)) return r;
+    markn(st, "pass2 " + std::to_string(r0) + "-" + std::to_string(r1));
+    return d2h(r0, r1);
+  };
+  const bool census = !(flags & EVO_F_NO_CENSUS);
+  const auto host_t0 = std::chrono::steady_clock::now();
+  markn(st, "start");
+  CK(cudaEventRecord(c->ev_start, st));
+  CK(cudaStreamWaitEvent(c->s_in, c->ev_start, 0));
+  CK(cudaStreamWaitEvent(c->s_out, c->ev_start, 0));
+  CK(cudaMemsetAsync(c->bad, 0, sizeof(int), st));
+  // uploads: the seam band first, then bands 0..nb-2
+  if (nb > 1) {
+    if (int r = h2d(nb - 1)) return r;
+  }
+  for (int b = 0; b < std::max(1, nb - 1); ++b)
+    if (int r = h2d(b)) return r;
+  if (nb == 1) {
+    CK(cudaStreamWaitEvent(st, c->ev_in[0], 0));
+    if (int r = check(0)) return r;
+    CK(evo::launch_refresh_ghosts(F, c->geom(), st));
+    if (int r = p1(0, H)) return r;
+    CK(evo::launch_wrap_mid(c->mid, c->geom(), st));
+    if (int r = p2(0, H)) return r;
+  } else {
+    for (int b = 0; b < nb - 1; ++b) {
+      CK(cudaStreamWaitEvent(st, c->ev_in[b], 0));
+      if (b == 0) {
+        if (int r = check(nb - 1)) return r;
+      }
+      if (int r = check(b)) return r;
+      if (b == 0) CK(evo::launch_refresh_ghosts(F, c->geom(), st));  // rows -1 and H from rows H-1 and 0
+      if (int r = p1(b == 0 ? 0 : R[b] - 32, R[b + 1] - 32)) return r;
+      if (int r = p2(b == 0 ? 1 : R[b] - 33, R[b + 1] - 33)) return r;
+    }
+    if (int r = p1(R[nb - 1] - 32, H)) return r;
+    CK(evo::launch_wrap_mid(c->mid, c->geom(), st));
+    if (int r = p2(R[nb - 1] - 33, H)) return r;
+    if (int r = p2(0, 1)) return r;
+  }
+  if (census) CK(evo::launch_census_finish(c->census, c->cap, t, st));
+  CK(evo::launch_refresh_ghosts(B, c->geom(), st));  // device-resident steps may follow
+  CK(cudaMemcpyAsync(c->h_stage, c->bad, sizeof(int), cudaMemcpyDeviceToHost, st));
+  if (stats) CK(cudaMemcpyAsync(c->h_stage + 8, c->census.stats, 16, cudaMemcpyDeviceToHost, st));
+  if (counts && census)
+    CK(cudaMemcpyAsync(c->h_stage + 32, c->census.counts_last, (size_t)c->cap * 4, cudaMemcpyDeviceToHost, st));
+  CK(cudaEventRecord(c->ev_out, c->s_out));
+  CK(cudaStreamWaitEvent(st, c->ev_out, 0));
+  const auto host_t1 = std::chrono::steady_clock::now();
+  CK(cudaStreamSynchronize(st));
+  if (trace) {
+    std::fprintf(stderr, "[pipe] host enqueue %.3f ms\n",
+                 std::chrono::duration<double, std::milli>(host_t1 - host_t0).count());
+    for (size_t i = 0; i < tname.size(); ++i) {
+      float ms = 0;
+      const cudaError_t e = cudaEventElapsedTime(&ms, c->tev[0], c->tev[i]);
+      std::fprintf(stderr, "%s%s %.3f%s", i ? ", " : "[pipe] ", tname[i].c_str(), ms, e ? "(err)" : "");
+    }
+    std::fprintf(stderr, " in6=%d out6=%d\n", (int)in6, (int)out6);
+  }
+  c->have_export = false;
+  int bad_flag;
+  std::memcpy(&bad_flag, c->h_stage, sizeof(int));
+  if (bad_flag)
+    return fail(EVO_EINVAL, "genome_index outside [-1, capacity) or rotation > 7 in the uploaded planes");
+  if (stats) std::memcpy(stats, c->h_stage + 8, 16);
+  if (counts && census) std::memcpy(counts, c->h_stage + 32, (size_t)c->cap * 4);
+  c->front ^= 1;
+  return 0;
 }
 
 EVO_API int evo_run(evo_ctx* c, const evo_scalars* s, int64_t t0, int k, void* stream) {
@@ -820,7 +1098,7 @@ EVO_API int evo_remap_selected(evo_ctx* c, const int32_t* slot_map) {
 
 EVO_API int evo_host_register(void* p, int64_t bytes) {
   if (!p || bytes <= 0) return fail(EVO_EINVAL, "empty host range");
-  cudaError_t e = cudaHostRegister(p, (size_t)bytes, cudaHostRegisterDefault);
+  cudaError_t e = cudaHostRegister(p, (size_t)bytes, cudaHostRegisterMapped | cudaHostRegisterPortable);
   if (e == cudaErrorHostMemoryAlreadyRegistered) {
     cudaGetLastError();
     return 0;

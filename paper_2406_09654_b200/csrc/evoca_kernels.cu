@@ -175,11 +175,16 @@ __device__ __forceinline__ void tile_controller(const Pass1Args& a, SM& sm, int 
   const int nu = sm.n_units;
   for (int q = threadIdx.x; q < nu; q += THREADS) {
     unsigned short ord[U];
+    if constexpr (U % 2 == 0) {
 #pragma unroll
-    for (int c = 0; c < U; c += 2) {  // order entries are 16-bit, read in 32-bit pairs
-      const unsigned w = reinterpret_cast<const unsigned*>(sm.order)[(q * U + c) >> 1];
-      ord[c] = (unsigned short)(w & 0xFFFFu);
-      ord[(c + 1) % U] = (unsigned short)(w >> 16);
+      for (int c = 0; c < U; c += 2) {  // order entries are 16-bit, read in 32-bit pairs
+        const unsigned w = reinterpret_cast<const unsigned*>(sm.order)[(q * U + c) >> 1];
+        ord[c] = (unsigned short)(w & 0xFFFFu);
+        ord[c + 1] = (unsigned short)(w >> 16);
+      }
+    } else {
+#pragma unroll
+      for (int c = 0; c < U; ++c) ord[c] = sm.order[q * U + c];
     }
     if (ord[0] == 0xFFFF) continue;  // a pure padding unit (groups padded past U cells)
     int pos[U], hb[U], rot[U];
@@ -277,7 +282,10 @@ __global__ void __launch_bounds__(kThreads1, 2) k_pass1_generic(const Pass1Args 
 // Pass 1, hot path: persistent, direct net, FFMA2
 
 constexpr int kThreadsP = 640;  // >= units of a tile for pools <= 64 slots: one controller round
-constexpr int kUnitP = 2;       // cells per thread in the controller (a same-genome pair)
+#ifndef EVO_UNIT_CELLS
+#define EVO_UNIT_CELLS 2
+#endif
+constexpr int kUnitP = EVO_UNIT_CELLS;  // cells per thread in the controller (same genome)
 constexpr int kPreHalo = (kHaloCells + kThreadsP - 1) / kThreadsP;
 constexpr int kPreCells = (kTileCells + kThreadsP - 1) / kThreadsP;
 
@@ -830,6 +838,44 @@ __global__ void k_refresh_ghosts(const Planes p, const StepGeom g) {
   }
 }
 
+// Row-band (host-pipelined) steps of a single strip: the bands run as
+// strips of one context whose ghost rows are the neighbouring bands' real
+// rows, so only the torus seam needs the pass-1 outputs pass 2 reads
+// (post-death genome, shipped quantity, proposal byte) wrapped.
+__global__ void k_wrap_mid(const Mid m, const StepGeom g) {
+  for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < g.W; x += gridDim.x * blockDim.x) {
+    const long long top = plane_row(g, -1) + x, last = plane_row(g, g.H - 1) + x;
+    const long long bot = plane_row(g, g.H) + x, first = plane_row(g, 0) + x;
+    m.gi[top] = m.gi[last];
+    m.gi[bot] = m.gi[first];
+    m.q[top] = m.q[last];
+    m.q[bot] = m.q[first];
+    m.rp[top] = m.rp[last];
+    m.rp[bot] = m.rp[first];
+  }
+}
+
+// Range check of uploaded genome / rotation planes (the host upload's
+// ValueError, done on the device so the host never scans the planes):
+// out-of-range entries are cleared (genome -1, rotation & 7) so no kernel
+// indexes outside the tables, and *bad is set; the host reports the error.
+__global__ void k_check_cells(int32_t* gi, uint8_t* rot, long long n, int capacity, int* bad) {
+  int b = 0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const int g = gi[i];
+    if (g < -1 || g >= capacity) {
+      gi[i] = -1;
+      b = 1;
+    }
+    const uint8_t r = rot[i];
+    if (r > 7) {
+      rot[i] = r & 7;
+      b = 1;
+    }
+  }
+  if (__any_sync(0xffffffffu, b) && (threadIdx.x & 31) == 0) atomicOr(bad, 1);
+}
+
 // Strip halo staging (multi-GPU row strips).  which 0: the five sensed
 // front planes E, I, C0..C2 (f32); which 1: the pass-1 outputs a
 // neighbour's pass 2 reads - post-death genome (i32), shipped quantity (f32
@@ -1003,6 +1049,20 @@ cudaError_t launch_census_finish(const Census& c, int capacity, long long t, cud
 cudaError_t launch_refresh_ghosts(const Planes& p, const StepGeom& g, cudaStream_t st) {
   const int blocks = (g.W + 255) / 256;
   k_refresh_ghosts<<<blocks, 256, 0, st>>>(p, g);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_wrap_mid(const Mid& m, const StepGeom& g, cudaStream_t st) {
+  const int blocks = (g.W + 255) / 256;
+  k_wrap_mid<<<blocks, 256, 0, st>>>(m, g);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_check_cells(int32_t* gi, uint8_t* rot, long long n, int capacity, int* bad, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  long long blocks = (n + 1023) / 1024;
+  if (blocks > 1184) blocks = 1184;
+  k_check_cells<<<(int)blocks, 256, 0, st>>>(gi, rot, n, capacity, bad);
   return cudaGetLastError();
 }
 

@@ -96,6 +96,30 @@ class DeviceSubstrate:
         self._keep = (E, I, Cm, gi, rot)  # keep alive across async copies
         check(self.lib.evo_upload_planes(self.ctx, ptr(E), ptr(I), ptr(Cm), ptr(gi), ptr(rot), _stream(stream)))
 
+    def step_host(self, front, back, scalars, t: int, flags: int = 0, bands: int = 0, source_map=None,
+                  stream=None):
+        """One step of host-resident planes (evo_step_host): uploads `front`,
+        steps, writes the new planes into `back`, pipelined over row bands.
+        Returns (census counts or None, adoptions, extinctions)."""
+        if self.strip:
+            raise ValueError("step_host steps a single-strip context")
+        src = [np.ascontiguousarray(a) for a in _arrays_of(front)]
+        self._check_shapes(*src)
+        dst = list(_arrays_of(back))
+        self._check_shapes(*dst)
+        for a in dst:
+            if not a.flags["C_CONTIGUOUS"] or not a.flags["WRITEABLE"]:
+                raise ValueError("step_host targets must be writeable C-contiguous arrays")
+        if source_map is not None or self._src_map_id is not None:
+            if source_map is None or id(source_map) != self._src_map_id:
+                self.set_source_map(source_map)
+        census = not (flags & _lib.F_NO_CENSUS)
+        counts = np.empty(self.capacity, np.int32) if census else None
+        st = np.zeros(2, np.int64)
+        check(self.lib.evo_step_host(self.ctx, C.byref(scalars), int(t), int(flags), *(ptr(a) for a in src),
+                                     *(ptr(a) for a in dst), ptr(counts), ptr(st), int(bands), _stream(stream)))
+        return counts, int(st[0]), int(st[1])
+
     def download_arrays(self, E, I, Cm, gi, rot, stream=None) -> None:
         for a in (E, I, Cm, gi, rot):
             if a is not None and not a.flags["C_CONTIGUOUS"]:

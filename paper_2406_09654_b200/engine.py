@@ -266,13 +266,13 @@ def step(state) -> None:
         b.pinned = True
     if b.device_ahead:
         _download_front(state)
-    b.dev.upload(sub.front)
     phys = state.config.physics
     rad = _radiation_active(state)
     flags = (_lib.F_RECORD_EVENTS | _lib.F_NO_CENSUS) if rad else 0
-    b.dev.step_raw(step_scalars(t, phys), t, flags=flags, source_map=phys.energy_source_map)
-    b.dev.download(sub.back)
-    adoptions, _ = b.dev.read_stats()
+    # upload front -> pass 1 -> pass 2 -> download into back, pipelined over
+    # row bands inside the library (evo_step_host)
+    counts, adoptions, _ = b.dev.step_host(sub.front, sub.back, step_scalars(t, phys), t, flags=flags,
+                                           source_map=phys.energy_source_map)
     if rad:
         events = b.dev.read_events()
         if len(events):
@@ -288,7 +288,6 @@ def step(state) -> None:
         b.pool_version = None
         b.sync_params(state.pool)
     else:
-        counts, _, _, _ = b.dev.read_census()
         newly_dead = state.pool.update_census(counts, t + 1)
     sub.swap_buffers()
     state.last_adoptions = int(adoptions)
