@@ -11,6 +11,9 @@ Drop-in for /root/reference/pkg/src/evoca/engine.py:
   * ``build_action_field(state)`` - device sense + controller, exported as an
     ``ActionField`` (engine.py:193-230).
   * ``digest(state)`` - FNV-1a over the front planes (engine.py:301-315).
+  * ``new_state(config)`` / ``seed_initial_population`` (engine.py:94-139),
+    ``gather_sensors`` (engine.py:142-161), ``describe_params`` /
+    ``validate_param`` / ``apply_param`` live steering (engine.py:321-390).
 Host NEAT radiation (physics.apply_radiation, physics.py:346-392) stays on
 the host; when its probabilities are non-zero the engine records adoption
 events on the device and hands them to a host callback per step.
@@ -34,11 +37,15 @@ from .synth import BASELINE_CONFIGS, synth_arrays, synth_params
 
 __all__ = [
     "GridConfig", "HypernetConfig", "EvolutionRates", "ExperimentConfig",
-    "SimState", "Hook", "baseline_state", "step", "run", "build_action_field", "digest",
+    "SimState", "Hook", "baseline_state", "new_state", "seed_initial_population", "gather_sensors", "step",
+    "run", "build_action_field", "digest", "describe_params", "validate_param", "apply_param",
     "device_of", "sync_to_host",
 ]
 
 log = logging.getLogger(__name__)
+
+
+DEFAULT_POOL_CAPACITY = 512  # neuroevo.py:50
 
 
 @dataclass
@@ -46,19 +53,57 @@ class GridConfig:
     width: int = 256
     height: int = 256
 
+    def validate(self) -> None:  # config.py:32-36
+        if self.width < 4:
+            raise ValueError("grid.width must be >= 4")
+        if self.height < 4:
+            raise ValueError("grid.height must be >= 4")
+
 
 @dataclass
 class HypernetConfig:
     hidden_size: int = 16  # 0 selects the BASELINE direct 45->13 controller
+    tau: float = 0.2
+    w_max: float = 3.0
+
+    def validate(self) -> None:  # config.py:45-51 (hidden 0 = the direct-net extension)
+        if self.hidden_size < 0:
+            raise ValueError("hypernet.hidden_size must be >= 0")
+        if not 0.0 <= self.tau < 1.0:
+            raise ValueError("hypernet.tau must be in [0, 1)")
+        if self.w_max <= 0:
+            raise ValueError("hypernet.w_max must be positive")
 
 
 @dataclass
 class EvolutionRates:
-    """The two rates the step consults (neuroevo.py:170-203); NEAT's
-    mutation rates live with the host genetics."""
+    """neuroevo.py:170-203.  The radiation probabilities default to 0 here
+    (the BASELINE configurations run without host NEAT radiation); set the
+    reference's 0.02 / 0.2 to restore its default evolution."""
 
+    weight_perturb_prob: float = 0.8
+    weight_perturb_sigma: float = 0.5
+    weight_reset_prob: float = 0.05
+    add_connection_prob: float = 0.05
+    add_node_prob: float = 0.03
+    toggle_enable_prob: float = 0.01
+    c1: float = 1.0
+    c2: float = 1.0
+    c3: float = 0.4
     p_radiation: float = 0.0
     p_merge: float = 0.0
+
+    def validate(self) -> None:  # neuroevo.py:186-203
+        for name in ("weight_perturb_prob", "weight_reset_prob", "add_connection_prob", "add_node_prob",
+                     "toggle_enable_prob", "p_radiation", "p_merge"):
+            v = getattr(self, name)
+            if not 0.0 <= v <= 1.0:
+                raise ValueError(f"{name} must be in [0, 1], got {v}")
+        if self.weight_perturb_sigma <= 0:
+            raise ValueError("weight_perturb_sigma must be positive")
+        for name in ("c1", "c2", "c3"):
+            if getattr(self, name) < 0:
+                raise ValueError(f"{name} must be non-negative")
 
 
 @dataclass
@@ -70,15 +115,37 @@ class FieldRadiationConfig:
     every: int = 0
     p: float = 0.01
 
+    def validate(self) -> None:
+        if self.every < 0:
+            raise ValueError("field_radiation.every must be >= 0")
+        if not 0.0 <= self.p <= 1.0:
+            raise ValueError("field_radiation.p must be in [0, 1]")
+
 
 @dataclass
 class ExperimentConfig:
     grid: GridConfig = field(default_factory=GridConfig)
     seed: int = 0
+    initial_population: int = 64
     physics: PhysicsParams = field(default_factory=PhysicsParams)
     evolution: EvolutionRates = field(default_factory=EvolutionRates)
     hypernet: HypernetConfig = field(default_factory=HypernetConfig)
     field_radiation: FieldRadiationConfig = field(default_factory=FieldRadiationConfig)
+
+    def validate(self) -> None:  # config.py:104-121
+        self.grid.validate()
+        self.physics.validate()
+        self.evolution.validate()
+        self.hypernet.validate()
+        self.field_radiation.validate()
+        if self.seed < 0:
+            raise ValueError("seed must be >= 0")
+        if self.initial_population < 0:
+            raise ValueError("initial_population must be >= 0")
+        if self.initial_population > DEFAULT_POOL_CAPACITY:
+            raise ValueError(f"initial_population must be <= {DEFAULT_POOL_CAPACITY}")
+        if self.initial_population > self.grid.width * self.grid.height:
+            raise ValueError("initial_population must fit on the grid")
 
 
 @dataclass
@@ -424,6 +491,159 @@ def digest(state) -> int:
         buf = np.ascontiguousarray(a).view(np.uint8).reshape(-1)
         _lib.check(lib.evo_fnv1a64(h.value, _lib.ptr(buf), buf.size, C.byref(h)))
     return int(h.value)
+
+
+# -- state construction (engine.py:94-139) -------------------------------------------
+
+
+def new_state(config: ExperimentConfig, workers: int = 1, seed_population: bool = True) -> SimState:
+    """A ready-to-run state from a validated config (engine.py:94-107).  The
+    pool's net factory defers expression to the device: admitted genomes are
+    expressed in one batched CPPN launch (evo_express_cppn) when the state
+    first steps, bit-identical to the reference's generate_network."""
+    from .radiation import device_net_factory
+
+    hyper = config.hypernet
+    sub = create_substrate(config.grid.width, config.grid.height)
+    pool = SlotPool(DEFAULT_POOL_CAPACITY, net_factory=device_net_factory(hyper.hidden_size, hyper.tau, hyper.w_max))
+    state = SimState(substrate=sub, pool=pool, config=config, master_seed=config.seed, workers=workers)
+    if seed_population and config.initial_population > 0:
+        seed_initial_population(state, config.initial_population)
+    return state
+
+
+def seed_initial_population(state, count: int) -> None:
+    """Scatter fresh organisms onto distinct front cells (engine.py:110-139):
+    placement and headings from the "seed_cells" stream, each genome from its
+    own "init_genome" stream, energy = infrastructure = 1."""
+    from .neat import init_genome, stream
+
+    sub = state.substrate
+    if count > state.pool.capacity:
+        raise ValueError("initial population exceeds pool capacity")
+    if count > sub.width * sub.height:
+        raise ValueError("initial population exceeds cell count")
+    sync_to_host(state)
+    t = sub.step_counter
+    g = stream(state.master_seed, t, "seed_cells")
+    cells = g.choice(sub.width * sub.height, size=count, replace=False)
+    rots = g.integers(0, 8, size=count)
+    front = sub.front
+    gi = front.genome_index.reshape(-1)
+    energy = front.channels["energy"][0].reshape(-1)
+    infra = front.channels["infrastructure"][0].reshape(-1)
+    rot = front.rotation.reshape(-1)
+    for i in range(count):
+        genome = init_genome(stream(state.master_seed, t, "init_genome", i), state.pool.innovations)
+        slot = state.pool.admit(genome, parents=(), birth_step=t)
+        if slot is None:
+            raise RuntimeError("pool rejected a seed genome")
+        c = int(cells[i])
+        gi[c] = slot
+        energy[c] = 1.0
+        infra[c] = 1.0
+        rot[c] = rots[i]
+
+
+def gather_sensors(sub, x: int, y: int) -> np.ndarray:
+    """Scalar sensor vector of one cell (engine.py:142-161): self then the
+    eight neighbours in the cell's rotation order, channels E, I, C0..C2.
+    (The device builds these vectors in shared memory; this host version is
+    the reference's per-cell helper over the host front planes.)"""
+    from .physics import KERNEL_OFFSETS, PERM_TABLE
+
+    w, h = sub.width, sub.height
+    front = sub.front
+    planes = (front.channels["energy"][0], front.channels["infrastructure"][0], front.channels["communication"][0],
+              front.channels["communication"][1], front.channels["communication"][2])
+    r = int(front.rotation[y, x])
+    out = np.empty(45, np.float32)
+    coords = [(x, y)] + [((x + int(KERNEL_OFFSETS[j, 0])) % w, (y + int(KERNEL_OFFSETS[j, 1])) % h)
+                         for j in PERM_TABLE[r]]
+    for s, (cx, cy) in enumerate(coords):
+        for ch, p in enumerate(planes):
+            out[s * 5 + ch] = p[cy, cx]
+    return out
+
+
+# -- live parameter steering (engine.py:321-390) -------------------------------------
+
+_PARAM_RANGES: dict[str, tuple[float, float]] = {
+    "physics.cycle_amplitude": (0.0, 2.0),
+    "physics.cycle_period": (2, 100000),
+    "physics.drain_fraction": (0.0, 1.0),
+    "physics.invest_rate": (0.0, 10.0),
+    "physics.liquidate_rate": (0.0, 10.0),
+    "physics.invest_efficiency": (0.0, 1.0),
+    "physics.liquidate_efficiency": (0.0, 1.0),
+    "physics.explore_fraction": (0.0, 1.0),
+    "physics.upkeep": (0.0, 1.0),
+    "physics.decay_on_starvation": (0.0, 1.0),
+    "physics.death_threshold": (0.0, 1.0),
+    "evolution.weight_perturb_prob": (0.0, 1.0),
+    "evolution.weight_perturb_sigma": (1e-6, 5.0),
+    "evolution.weight_reset_prob": (0.0, 1.0),
+    "evolution.add_connection_prob": (0.0, 1.0),
+    "evolution.add_node_prob": (0.0, 1.0),
+    "evolution.toggle_enable_prob": (0.0, 1.0),
+    "evolution.c1": (0.0, 10.0),
+    "evolution.c2": (0.0, 10.0),
+    "evolution.c3": (0.0, 10.0),
+    "evolution.p_radiation": (0.0, 1.0),
+    "evolution.p_merge": (0.0, 1.0),
+    "hypernet.tau": (0.0, 0.99),
+    "hypernet.w_max": (0.1, 10.0),
+}
+_INT_PARAMS = {"physics.cycle_period"}
+
+
+def describe_params(state) -> list[dict]:
+    """Steerable parameters with current values and ranges (engine.py:351-358)."""
+    items = []
+    for path, (lo, hi) in _PARAM_RANGES.items():
+        section, name = path.split(".")
+        items.append({"path": path, "value": getattr(getattr(state.config, section), name), "min": lo, "max": hi})
+    return items
+
+
+def validate_param(path: str, value):
+    """Check a steering request without touching any state (engine.py:361-376)."""
+    if path not in _PARAM_RANGES:
+        raise ValueError(f"unknown parameter {path!r}")
+    lo, hi = _PARAM_RANGES[path]
+    if isinstance(value, bool) or not isinstance(value, (int, float)):
+        raise ValueError(f"{path} expects a number")
+    if path in _INT_PARAMS:
+        if value != int(value):
+            raise ValueError(f"{path} must be an integer")
+        value = int(value)
+    else:
+        value = float(value)
+    if not lo <= value <= hi:
+        raise ValueError(f"{path} must be in [{lo}, {hi}]")
+    return value
+
+
+def apply_param(state, path: str, value) -> None:
+    """Set one steerable parameter (engine.py:379-390).  Physics scalars are
+    recomputed from the config at every step, so the next device step (or the
+    next step of a device-resident run) uses the new value without a sync;
+    hypernet tau / w_max apply to genomes expressed from now on."""
+    value = validate_param(path, value)
+    section, name = path.split(".")
+    obj = getattr(state.config, section)
+    old = getattr(obj, name)
+    setattr(obj, name, value)
+    try:
+        obj.validate()
+    except ValueError:
+        setattr(obj, name, old)
+        raise
+    if section == "hypernet" and isinstance(state.pool, SlotPool):
+        from .radiation import device_net_factory
+
+        hyper = state.config.hypernet
+        state.pool.net_factory = device_net_factory(_hidden_of(state), hyper.tau, hyper.w_max)
 
 
 # -- BASELINE synthetic states -------------------------------------------------------
