@@ -129,6 +129,11 @@ EVO_API int evo_step_host(evo_ctx* ctx, const evo_scalars* s, int64_t t, int fla
                           const float* C, const int32_t* gi, const uint8_t* rot, float* E_out, float* I_out,
                           float* C_out, int32_t* gi_out, uint8_t* rot_out, int32_t* counts, int64_t* stats,
                           int bands, void* stream);
+/* RGBA frame of the device front buffer (substrate.py:147-165 render_rgb):
+ * rgba = H*W*4 bytes, row-major; bit-identical to the reference's numpy
+ * frame; moves 4 B/cell to the host instead of the 25 B/cell planes. */
+EVO_API int evo_render_rgb(evo_ctx* ctx, double norm_energy, double norm_infrastructure, uint8_t* rgba,
+                           void* stream);
 /* k consecutive steps t0..t0+k-1 with per-step scalars s[0..k-1]. */
 EVO_API int evo_run(evo_ctx* ctx, const evo_scalars* s, int64_t t0, int k, void* stream);
 /* The two launches of a step, for halo exchange between them (multi-GPU) and

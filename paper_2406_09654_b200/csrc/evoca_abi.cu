@@ -78,6 +78,7 @@ struct evo_ctx {
   cudaEvent_t ev_start = nullptr, ev_out = nullptr, ev_in[kMaxBands] = {}, ev_p2[kMaxBands + 2] = {};
   static constexpr size_t kTraceEvents = 512;
   cudaEvent_t tev[kTraceEvents] = {};
+  uint32_t* rgba = nullptr;  // render target (evo_render_rgb; allocated on first use)
   int* bad = nullptr;
   unsigned char* h_stage = nullptr;  // pinned: bad flag, stats, census counts
   std::vector<void*> allocs;
@@ -792,6 +793,18 @@ EVO_API int evo_step_host(evo_ctx* c, const evo_scalars* s, int64_t t, int flags
   if (stats) std::memcpy(stats, c->h_stage + 8, 16);
   if (counts && census) std::memcpy(counts, c->h_stage + 32, (size_t)c->cap * 4);
   c->front ^= 1;
+  return 0;
+}
+
+EVO_API int evo_render_rgb(evo_ctx* c, double norm_energy, double norm_infrastructure, uint8_t* rgba, void* stream) {
+  if (int r = check_ctx(c)) return r;
+  if (!rgba) return fail(EVO_EINVAL, "null frame pointer");
+  if (!(norm_energy != 0.0) || !(norm_infrastructure != 0.0)) return fail(EVO_EINVAL, "display norms must be non-zero");
+  if (!c->rgba) CK(c->alloc(&c->rgba, (size_t)c->ncell()));
+  cudaStream_t st = pick(c, stream);
+  CK(evo::launch_render_rgb(c->buf[c->front], c->geom(), norm_energy, norm_infrastructure, c->rgba, st));
+  CK(cudaMemcpyAsync(rgba, c->rgba, (size_t)c->ncell() * 4, cudaMemcpyDeviceToHost, st));
+  if (!stream) CK(cudaStreamSynchronize(st));
   return 0;
 }
 

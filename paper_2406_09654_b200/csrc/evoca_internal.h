@@ -164,6 +164,8 @@ cudaError_t debug_phase_cycles(unsigned long long* out, bool reset);
 cudaError_t debug_hidden_cycles(unsigned long long* out, bool reset);
 cudaError_t launch_census_finish(const Census& c, int capacity, long long t, cudaStream_t st);
 cudaError_t launch_refresh_ghosts(const Planes& p, const StepGeom& g, cudaStream_t st);
+cudaError_t launch_render_rgb(const Planes& f, const StepGeom& g, double norm_e, double norm_i, uint32_t* out,
+                              cudaStream_t st);
 cudaError_t launch_wrap_mid(const Mid& m, const StepGeom& g, cudaStream_t st);
 cudaError_t launch_check_cells(int32_t* gi, uint8_t* rot, long long n, int capacity, int* bad, cudaStream_t st);
 cudaError_t launch_halo(const Planes& f, const Mid& m, const StepGeom& g, int which, bool pack, void* buf,

@@ -855,6 +855,31 @@ __global__ void k_wrap_mid(const Mid m, const StepGeom g) {
   }
 }
 
+// RGBA frame of the front buffer (substrate.py:147-165): red = energy and
+// green = infrastructure scaled by their display norms, clamped to [0, 1],
+// x255, rounded half-to-even; blue = the genome slot's golden-ratio hue
+// (slot * 0.6180339887498949 mod 1, 0 when empty); alpha 255.  All in f64 with
+// the reference's operation order (a true division by the norm), so frames
+// are bit-identical to numpy's; 12 B read + 4 B written per cell.
+__device__ __forceinline__ unsigned render_channel(double v) {
+  v = v < 0.0 ? 0.0 : (v > 1.0 ? 1.0 : v);  // np.clip (NaN passes through)
+  v = rint(v * 255.0);
+  return v == v ? (unsigned)v : 0u;
+}
+
+__global__ void k_render_rgb(const Planes f, const StepGeom g, double norm_e, double norm_i, uint32_t* out) {
+  const long long n = (long long)g.W * g.H;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const long long o = g.W + i;  // skip ghost row -1
+    const unsigned r = render_channel((double)f.E[o] / norm_e);
+    const unsigned gr = render_channel((double)f.I[o] / norm_i);
+    const int slot = f.gi[o];
+    const double hue = slot < 0 ? 0.0 : fmod((double)slot * 0.6180339887498949, 1.0);
+    const unsigned b = (unsigned)rint(hue * 255.0);
+    out[i] = r | (gr << 8) | (b << 16) | (255u << 24);
+  }
+}
+
 // Range check of uploaded genome / rotation planes (the host upload's
 // ValueError, done on the device so the host never scans the planes):
 // out-of-range entries are cleared (genome -1, rotation & 7) so no kernel
@@ -1055,6 +1080,14 @@ cudaError_t launch_refresh_ghosts(const Planes& p, const StepGeom& g, cudaStream
 cudaError_t launch_wrap_mid(const Mid& m, const StepGeom& g, cudaStream_t st) {
   const int blocks = (g.W + 255) / 256;
   k_wrap_mid<<<blocks, 256, 0, st>>>(m, g);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_render_rgb(const Planes& f, const StepGeom& g, double norm_e, double norm_i, uint32_t* out,
+                              cudaStream_t st) {
+  const long long n = (long long)g.W * g.H;
+  const int blocks = (int)std::min<long long>((n + 255) / 256, (long long)num_sms() * 16);
+  k_render_rgb<<<blocks, 256, 0, st>>>(f, g, norm_e, norm_i, out);
   return cudaGetLastError();
 }
 

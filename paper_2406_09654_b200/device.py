@@ -120,6 +120,12 @@ class DeviceSubstrate:
                                      *(ptr(a) for a in dst), ptr(counts), ptr(st), int(bands), _stream(stream)))
         return counts, int(st[0]), int(st[1])
 
+    def render_rgb(self, norm_energy: float = 1.0, norm_infrastructure: float = 1.0) -> np.ndarray:
+        """(H, W, 4) uint8 RGBA frame of the device front (evo_render_rgb)."""
+        px = np.empty((self.height, self.width, 4), np.uint8)
+        check(self.lib.evo_render_rgb(self.ctx, float(norm_energy), float(norm_infrastructure), ptr(px), None))
+        return px
+
     def download_arrays(self, E, I, Cm, gi, rot, stream=None) -> None:
         for a in (E, I, Cm, gi, rot):
             if a is not None and not a.flags["C_CONTIGUOUS"]:

@@ -38,7 +38,7 @@ from .synth import BASELINE_CONFIGS, synth_arrays, synth_params
 __all__ = [
     "GridConfig", "HypernetConfig", "EvolutionRates", "ExperimentConfig",
     "SimState", "Hook", "baseline_state", "new_state", "seed_initial_population", "gather_sensors", "step",
-    "run", "build_action_field", "digest", "describe_params", "validate_param", "apply_param",
+    "run", "build_action_field", "digest", "describe_params", "validate_param", "apply_param", "render_rgb",
     "device_of", "sync_to_host",
 ]
 
@@ -176,8 +176,13 @@ class SimState:
 
 @dataclass(frozen=True)
 class Hook:
+    """engine.py:87-91.  ``device=True`` (extension): the hook only uses
+    device-side views (``render_rgb``, ``last_adoptions``) and fires during a
+    device-resident ``run`` without downloading the planes."""
+
     every: int
     fn: Callable
+    device: bool = False
 
 
 # -- device binding -------------------------------------------------------------
@@ -433,6 +438,12 @@ def run(state, steps: int, hooks=(), should_stop: Optional[Callable[[], bool]] =
 
             field_radiation(state, sub.step_counter, fr.p)
         due = [h for h in hooks if sub.step_counter % h.every == 0]
+        dev_due = [h for h in due if getattr(h, "device", False)]
+        due = [h for h in due if not getattr(h, "device", False)]
+        if dev_due:
+            adoptions, extinctions = b.dev.read_stats()
+            state.last_adoptions, state.last_extinctions = int(adoptions), int(extinctions)
+            _fire(state, dev_due)
         if due:
             _download_front(state)
             adoptions, extinctions = b.dev.read_stats()
@@ -644,6 +655,23 @@ def apply_param(state, path: str, value) -> None:
 
         hyper = state.config.hypernet
         state.pool.net_factory = device_net_factory(_hidden_of(state), hyper.tau, hyper.w_max)
+
+
+def render_rgb(state, norm_energy: float = 1.0, norm_infrastructure: float = 1.0):
+    """RGBA frame of the state's front buffer (substrate.py:147-165).  When the
+    newest planes are on the device (a device-resident run) the frame is
+    rendered there and only 4 B/cell come back; otherwise the host mirror is
+    rendered.  Both are bit-identical to the reference's frame."""
+    from .substrate import RgbFrame
+    from .substrate import render_rgb as host_render
+
+    if norm_energy == 0 or norm_infrastructure == 0:
+        raise ValueError("display norms must be non-zero")
+    b = getattr(state, "_evo_binding", None)
+    sub = state.substrate
+    if b is not None and b.device_ahead:
+        return RgbFrame(sub.width, sub.height, b.dev.render_rgb(norm_energy, norm_infrastructure))
+    return host_render(sub, norm_energy, norm_infrastructure)
 
 
 # -- BASELINE synthetic states -------------------------------------------------------

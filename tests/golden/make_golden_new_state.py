@@ -8,7 +8,8 @@ Writes new_state_cases.npz: for a few configs, the reference new_state()
 front planes (seed_initial_population placement, headings, stocks), the
 innovation counter after seeding, and every seeded slot's expressed
 DenseParams (reference generate_network via the pool's net factory); plus
-reference gather_sensors vectors for a few cells of a random state.
+reference gather_sensors vectors for a few cells of a random state; reference
+render_rgb frames (substrate.py:147-165) of a random state at three norms.
 """
 
 from __future__ import annotations
@@ -66,6 +67,16 @@ def main():
     cells = [(0, 0), (8, 6), (4, 3), (8, 0), (0, 6)]
     out["gs_cells"] = np.array(cells, np.int64)
     out["gs_out"] = np.stack([reng.gather_sensors(st.substrate, x, y) for x, y in cells])
+    # render_rgb on a state with out-of-range stocks, empty cells and large slots
+    from evoca.substrate import render_rgb
+
+    f.channels["energy"][0] = (g.standard_normal((7, 9)) * 2).astype(np.float32)
+    f.channels["energy"][0][0, :3] = [np.float32(0.5 / 255), np.float32(1.5 / 255), np.float32(2.5 / 255)]
+    f.channels["infrastructure"][0] = g.random((7, 9), dtype=np.float32) * 3
+    f.genome_index[:] = g.integers(-1, 4096, (7, 9)).astype(np.int32)
+    out["rgb_E"], out["rgb_I"], out["rgb_gi"] = f.plane("energy").copy(), f.plane("infrastructure").copy(), f.genome_index.copy()
+    out["rgb_norms"] = np.array([[1.0, 1.0], [2.5, 0.7], [0.3, 3.0]])
+    out["rgb_px"] = np.stack([render_rgb(st.substrate, a, b).pixels for a, b in out["rgb_norms"]])
     np.savez_compressed(os.path.join(HERE, "new_state_cases.npz"), **out)
     print("wrote", len(out), "arrays")
 

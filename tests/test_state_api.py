@@ -126,3 +126,65 @@ def test_new_state_device_expression_matches_reference(k):
     engine.step(st)
     engine.run(st, 3)
     assert st.t == 4
+
+
+def _rgb_substrate():
+    sub = create_substrate(9, 7)
+    sub.front.channels["energy"][0] = GOLD["rgb_E"]
+    sub.front.channels["infrastructure"][0] = GOLD["rgb_I"]
+    sub.front.genome_index[:] = GOLD["rgb_gi"]
+    return sub
+
+
+def test_render_rgb_host_matches_reference():
+    from paper_2406_09654_b200.substrate import render_rgb
+
+    sub = _rgb_substrate()
+    for (ne, ni), want in zip(GOLD["rgb_norms"], GOLD["rgb_px"]):
+        assert np.array_equal(render_rgb(sub, ne, ni).pixels, want)
+
+
+@pytest.mark.gpu
+def test_render_rgb_device_matches_reference():
+    from oracle import oracle as orc
+    from paper_2406_09654_b200.device import DeviceSubstrate
+    from paper_2406_09654_b200.substrate import render_rgb
+
+    sub = _rgb_substrate()
+    dev = DeviceSubstrate(9, 7, 4096)
+    dev.upload(sub.front)
+    for (ne, ni), want in zip(GOLD["rgb_norms"], GOLD["rgb_px"]):
+        assert np.array_equal(dev.render_rgb(ne, ni), want)
+    dev.close()
+    # a larger random state (rounding ties, empty cells, big slots), device vs host
+    H, W = 300, 257
+    p = orc.synth_planes(H, W, 500, seed=3)
+    p.E[:] = (np.random.default_rng(1).standard_normal((H, W)) * 1.5).astype(np.float32)
+    p.E[0, :256] = (np.arange(256, dtype=np.float32) + np.float32(0.5)) / np.float32(255)
+    p.gi[np.random.default_rng(2).random((H, W)) < 0.2] = -1
+    big = create_substrate(W, H)
+    big.front.channels["energy"][0], big.front.channels["infrastructure"][0] = p.E, p.I
+    big.front.genome_index[:] = p.gi
+    dev = DeviceSubstrate(W, H, 500)
+    dev.upload(p)
+    for ne, ni in ((1.0, 1.0), (0.37, 5.0)):
+        assert np.array_equal(dev.render_rgb(ne, ni), render_rgb(big, ne, ni).pixels)
+    dev.close()
+
+
+@pytest.mark.gpu
+def test_device_hook_renders_without_download():
+    cfg = engine.ExperimentConfig(grid=engine.GridConfig(64, 48), initial_population=40, seed=4)
+    st = engine.new_state(cfg)
+    frames = []
+
+    def grab(s):
+        assert engine._binding(s).device_ahead  # no download happened for this hook
+        frames.append((s.t, engine.render_rgb(s).pixels.copy()))
+
+    engine.run(st, 6, hooks=[engine.Hook(3, grab, device=True)])
+    assert [t for t, _ in frames] == [3, 6]
+    # the last frame equals the host render of the final (downloaded) state
+    from paper_2406_09654_b200.substrate import render_rgb
+
+    assert np.array_equal(frames[-1][1], render_rgb(st.substrate).pixels)
