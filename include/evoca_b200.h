@@ -134,6 +134,17 @@ EVO_API int evo_step_host(evo_ctx* ctx, const evo_scalars* s, int64_t t, int fla
  * frame; moves 4 B/cell to the host instead of the 25 B/cell planes. */
 EVO_API int evo_render_rgb(evo_ctx* ctx, double norm_energy, double norm_infrastructure, uint8_t* rgba,
                            void* stream);
+/* Multi-scale complexity inputs of one front plane (metrics.py:57-103
+ * msc_of_substrate; plane 0 energy, 1 infrastructure, 2..4 communication):
+ * the centre power-of-two crop's block-mean pyramid and its overlaps as
+ * correctly rounded exact sums, squares[k] = fsum over scale k of f_k^2 and
+ * cross[k] = fsum of f_k * f_{k+1} (distinct products, k = 0..k_max); the
+ * reference's overlap is ldexp(sum, 2k) / side^2.  n_scales <= 0: all
+ * scales.  squares needs 32 entries, cross 31. */
+EVO_API int evo_msc(evo_ctx* ctx, int plane, int n_scales, double* squares, double* cross, int* side, int* k_max);
+/* float64 totals of the front energy / infrastructure planes in numpy's
+ * summation order (metrics.py:200-213 census: plane.sum(dtype=float64)). */
+EVO_API int evo_plane_sums(evo_ctx* ctx, double* energy, double* infrastructure);
 /* k consecutive steps t0..t0+k-1 with per-step scalars s[0..k-1]. */
 EVO_API int evo_run(evo_ctx* ctx, const evo_scalars* s, int64_t t0, int k, void* stream);
 /* The two launches of a step, for halo exchange between them (multi-GPU) and

@@ -21,7 +21,8 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 INCLUDE = os.path.join(ROOT, "include")
 LIB = os.path.join(PKG, "libevoca_b200.so")
-SOURCES = ["evoca_kernels.cu", "evoca_hidden_tc.cu", "evoca_cppn.cu", "evoca_radiation.cu", "evoca_abi.cu"]
+SOURCES = ["evoca_kernels.cu", "evoca_hidden_tc.cu", "evoca_cppn.cu", "evoca_radiation.cu", "evoca_metrics.cu",
+           "evoca_abi.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

@@ -79,6 +79,8 @@ struct evo_ctx {
   static constexpr size_t kTraceEvents = 512;
   cudaEvent_t tev[kTraceEvents] = {};
   uint32_t* rgba = nullptr;  // render target (evo_render_rgb; allocated on first use)
+  double* msc_work = nullptr;  // block-mean pyramid + results (evo_msc / evo_plane_sums)
+  long long* msc_acc = nullptr;
   int* bad = nullptr;
   unsigned char* h_stage = nullptr;  // pinned: bad flag, stats, census counts
   std::vector<void*> allocs;
@@ -805,6 +807,56 @@ EVO_API int evo_render_rgb(evo_ctx* c, double norm_energy, double norm_infrastru
   CK(evo::launch_render_rgb(c->buf[c->front], c->geom(), norm_energy, norm_infrastructure, c->rgba, st));
   CK(cudaMemcpyAsync(rgba, c->rgba, (size_t)c->ncell() * 4, cudaMemcpyDeviceToHost, st));
   if (!stream) CK(cudaStreamSynchronize(st));
+  return 0;
+}
+
+int ensure_metrics(evo_ctx* c) {
+  if (c->msc_work) return 0;
+  const int side = evo::msc_side(c->W, c->H);
+  const long long chunks = evo::plane_sum_chunks(c->ncell());
+  CK(c->alloc(&c->msc_work, (size_t)(evo::msc_workspace_doubles(side) + 64 + chunks + 2)));
+  CK(c->alloc(&c->msc_acc, (size_t)evo::msc_digits() * 64));
+  return 0;
+}
+
+EVO_API int evo_msc(evo_ctx* c, int plane, int n_scales, double* squares, double* cross, int* side, int* k_max) {
+  if (int r = check_ctx(c)) return r;
+  if (c->strip) return fail(EVO_EINVAL, "evo_msc needs a single-strip context");
+  if (plane < 0 || plane > 4) return fail(EVO_EINVAL, "plane must be 0 (energy), 1 (infrastructure) or 2..4 (communication)");
+  if (!squares || !cross || !side || !k_max) return fail(EVO_EINVAL, "null output pointer");
+  const int sd = evo::msc_side(c->W, c->H);
+  if (sd < 2) return fail(EVO_EINVAL, "field side must be a power of two >= 2");
+  if (int r = ensure_metrics(c)) return r;
+  const evo::Planes& f = c->buf[c->front];
+  const float* p = plane == 0 ? f.E : (plane == 1 ? f.I : f.C + (plane - 2) * c->stride);
+  double* out = c->msc_work + evo::msc_workspace_doubles(sd);
+  int km = 0;
+  CK(evo::launch_msc(p, c->W, c->H, n_scales, c->msc_work, c->msc_acc, out, &km, c->stream));
+  double host[64];
+  CK(cudaMemcpyAsync(host, out, sizeof(double) * (2 * km + 1), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  for (int k = 0; k <= km; ++k) squares[k] = host[k];
+  for (int k = 0; k < km; ++k) cross[k] = host[km + 1 + k];
+  *side = sd;
+  *k_max = km;
+  return 0;
+}
+
+EVO_API int evo_plane_sums(evo_ctx* c, double* energy, double* infrastructure) {
+  if (int r = check_ctx(c)) return r;
+  if (c->strip) return fail(EVO_EINVAL, "evo_plane_sums needs a single-strip context");
+  if (int r = ensure_metrics(c)) return r;
+  const int sd = evo::msc_side(c->W, c->H);
+  double* res = c->msc_work + evo::msc_workspace_doubles(sd) + 64;
+  double* chunks = res + 2;
+  const evo::Planes& f = c->buf[c->front];
+  CK(evo::launch_plane_sum(f.E + c->W, c->ncell(), chunks, res, c->stream));
+  CK(evo::launch_plane_sum(f.I + c->W, c->ncell(), chunks, res + 1, c->stream));
+  double host[2];
+  CK(cudaMemcpyAsync(host, res, sizeof(host), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  if (energy) *energy = host[0];
+  if (infrastructure) *infrastructure = host[1];
   return 0;
 }
 

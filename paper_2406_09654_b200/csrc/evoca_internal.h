@@ -166,6 +166,14 @@ cudaError_t launch_census_finish(const Census& c, int capacity, long long t, cud
 cudaError_t launch_refresh_ghosts(const Planes& p, const StepGeom& g, cudaStream_t st);
 cudaError_t launch_render_rgb(const Planes& f, const StepGeom& g, double norm_e, double norm_i, uint32_t* out,
                               cudaStream_t st);
+// observables (evoca_metrics.cu)
+int msc_side(int W, int H);
+long long msc_workspace_doubles(int side);
+int msc_digits();
+cudaError_t launch_msc(const float* plane, int W, int H, int n_scales, double* work, long long* accs, double* out,
+                       int* k_max_out, cudaStream_t st);
+long long plane_sum_chunks(long long n);
+cudaError_t launch_plane_sum(const float* plane, long long n, double* chunks, double* out, cudaStream_t st);
 cudaError_t launch_wrap_mid(const Mid& m, const StepGeom& g, cudaStream_t st);
 cudaError_t launch_check_cells(int32_t* gi, uint8_t* rot, long long n, int capacity, int* bad, cudaStream_t st);
 cudaError_t launch_halo(const Planes& f, const Mid& m, const StepGeom& g, int which, bool pack, void* buf,

@@ -131,6 +131,10 @@ class SlotPool:
             out[i] = self.records[int(self._lineage[i])].peak_population
         return out
 
+    def deaths_at(self, step: int) -> list[int]:
+        """Lineages whose recorded death step is ``step`` (neuroevo.py:544-545)."""
+        return [r.lineage_id for r in self.records.values() if r.death_step == step]
+
     def update_census(self, counts, step: int) -> list[int]:
         """Same contract as GenomePool.update_census (neuroevo.py:521-542)."""
         dead = []

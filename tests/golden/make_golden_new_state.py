@@ -77,6 +77,28 @@ def main():
     out["rgb_E"], out["rgb_I"], out["rgb_gi"] = f.plane("energy").copy(), f.plane("infrastructure").copy(), f.genome_index.copy()
     out["rgb_norms"] = np.array([[1.0, 1.0], [2.5, 0.7], [0.3, 3.0]])
     out["rgb_px"] = np.stack([render_rgb(st.substrate, a, b).pixels for a, b in out["rgb_norms"]])
+    # multi-scale complexity (metrics.py:57-103) and census plane totals
+    from evoca import metrics as rmet
+    from evoca.substrate import create_substrate
+
+    for k, (w, h) in enumerate([(37, 50), (64, 64), (130, 70)]):
+        sub = create_substrate(w, h)
+        f = sub.front
+        f.channels["energy"][0] = np.exp(g.standard_normal((h, w)) * 2).astype(np.float32)
+        inf = g.random((h, w), dtype=np.float32)
+        inf[g.random((h, w)) < 0.9] = 0
+        f.channels["infrastructure"][0] = inf
+        f.channels["communication"][:] = g.standard_normal((3, h, w)).astype(np.float32)
+        out[f"msc{k}_E"], out[f"msc{k}_I"] = f.plane("energy").copy(), f.plane("infrastructure").copy()
+        out[f"msc{k}_C"] = f.channels["communication"].copy()
+        for name, sb in (("energy", 0), ("infrastructure", 0), ("communication", 1)):
+            rep = rmet.msc_of_substrate(sub, name, sb)
+            out[f"msc{k}_{name}{sb}"] = np.array(list(rep.contributions) + [rep.total, rep.side])
+        out[f"msc{k}_sums"] = np.array([float(f.plane("energy").sum(dtype=np.float64)),
+                                        float(f.plane("infrastructure").sum(dtype=np.float64))])
+        side = 1 << min(h.bit_length() - 1, w.bit_length() - 1)
+        rep = rmet.msc(f.plane("energy")[:side, :side], n_scales=2)
+        out[f"msc{k}_E_n2"] = np.array(list(rep.contributions) + [rep.total, rep.side])
     np.savez_compressed(os.path.join(HERE, "new_state_cases.npz"), **out)
     print("wrote", len(out), "arrays")
 
