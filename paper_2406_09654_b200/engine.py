@@ -36,7 +36,8 @@ from .substrate import Substrate, create_substrate
 from .synth import BASELINE_CONFIGS, synth_arrays, synth_params
 
 __all__ = [
-    "GridConfig", "HypernetConfig", "EvolutionRates", "ExperimentConfig",
+    "GridConfig", "HypernetConfig", "EvolutionRates", "RunConfig", "ServeConfig", "FieldRadiationConfig",
+    "ExperimentConfig", "config_to_dict", "parse_config",
     "SimState", "Hook", "baseline_state", "new_state", "seed_initial_population", "gather_sensors", "step",
     "run", "build_action_field", "digest", "describe_params", "validate_param", "apply_param", "render_rgb",
     "device_of", "sync_to_host",
@@ -107,6 +108,48 @@ class EvolutionRates:
 
 
 @dataclass
+class RunConfig:
+    """config.py:55-72 (CLI cadence; carried for config/snapshot fidelity)."""
+
+    steps: int = 1000
+    metrics_every: int = 100
+    snapshot_every: int = 0
+    frame_every: int = 100
+
+    def validate(self) -> None:
+        if self.steps < 0:
+            raise ValueError("run.steps must be >= 0")
+        for name in ("metrics_every", "snapshot_every", "frame_every"):
+            if getattr(self, name) < 0:
+                raise ValueError(f"run.{name} must be >= 0")
+        if self.metrics_every == 0:
+            raise ValueError("run.metrics_every must be >= 1")
+        if self.frame_every == 0:
+            raise ValueError("run.frame_every must be >= 1")
+
+
+@dataclass
+class ServeConfig:
+    """config.py:74-90 (steering server; carried for config/snapshot fidelity)."""
+
+    host: str = "127.0.0.1"
+    port: int = 8765
+    frame_fps: float = 10.0
+    telemetry_fps: float = 2.0
+    max_steps_per_second: float = 0.0
+
+    def validate(self) -> None:
+        if not 0 <= self.port <= 65535:
+            raise ValueError("serve.port must be in [0, 65535]")
+        if self.frame_fps <= 0:
+            raise ValueError("serve.frame_fps must be positive")
+        if self.telemetry_fps <= 0:
+            raise ValueError("serve.telemetry_fps must be positive")
+        if self.max_steps_per_second < 0:
+            raise ValueError("serve.max_steps_per_second must be >= 0")
+
+
+@dataclass
 class FieldRadiationConfig:
     """BASELINE config-3 extension: every ``every`` steps
     a fraction ``p`` of occupied cells moves to freshly mutated children of
@@ -130,6 +173,8 @@ class ExperimentConfig:
     physics: PhysicsParams = field(default_factory=PhysicsParams)
     evolution: EvolutionRates = field(default_factory=EvolutionRates)
     hypernet: HypernetConfig = field(default_factory=HypernetConfig)
+    run: RunConfig = field(default_factory=RunConfig)
+    serve: ServeConfig = field(default_factory=ServeConfig)
     field_radiation: FieldRadiationConfig = field(default_factory=FieldRadiationConfig)
 
     def validate(self) -> None:  # config.py:104-121
@@ -137,6 +182,8 @@ class ExperimentConfig:
         self.physics.validate()
         self.evolution.validate()
         self.hypernet.validate()
+        self.run.validate()
+        self.serve.validate()
         self.field_radiation.validate()
         if self.seed < 0:
             raise ValueError("seed must be >= 0")
@@ -183,6 +230,72 @@ class Hook:
     every: int
     fn: Callable
     device: bool = False
+
+
+_SECTIONS = {"grid": GridConfig, "physics": PhysicsParams, "evolution": EvolutionRates, "hypernet": HypernetConfig,
+             "run": RunConfig, "serve": ServeConfig, "field_radiation": FieldRadiationConfig}
+_SCALAR_KEYS = ("seed", "initial_population")
+
+
+def _coerce(path: str, default, value):  # config.py:133-151
+    if isinstance(default, bool):
+        if not isinstance(value, bool):
+            raise ValueError(f"{path} must be a boolean")
+        return value
+    if isinstance(default, int):
+        if not isinstance(value, int) or isinstance(value, bool):
+            raise ValueError(f"{path} must be an integer")
+        return value
+    if isinstance(default, float):
+        if not isinstance(value, (int, float)) or isinstance(value, bool):
+            raise ValueError(f"{path} must be a number")
+        return float(value)
+    if isinstance(default, str):
+        if not isinstance(value, str):
+            raise ValueError(f"{path} must be a string")
+        return value
+    return value
+
+
+def parse_config(data: dict) -> ExperimentConfig:
+    """Build and validate a config from a parsed JSON object (config.py:164-183);
+    also accepts this package's ``field_radiation`` section."""
+    if not isinstance(data, dict):
+        raise ValueError("config root must be an object")
+    cfg = ExperimentConfig()
+    for key, value in data.items():
+        if key in _SECTIONS:
+            if not isinstance(value, dict):
+                raise ValueError(f"{key} must be an object")
+            if key == "physics" and "energy_source_map" in value:
+                raise ValueError("physics.energy_source_map is not configurable from file")
+            obj = _SECTIONS[key]()
+            known = set(vars(obj))
+            for k, v in value.items():
+                if k not in known:
+                    raise ValueError(f"unknown key {key}.{k}")
+                setattr(obj, k, _coerce(f"{key}.{k}", getattr(obj, k), v))
+            setattr(cfg, key, obj)
+        elif key in _SCALAR_KEYS:
+            setattr(cfg, key, _coerce(key, getattr(cfg, key), value))
+        else:
+            raise ValueError(f"unknown key {key}")
+    cfg.validate()
+    return cfg
+
+
+def config_to_dict(cfg) -> dict:
+    """JSON-ready dict that parse_config round-trips (config.py:194-198); the
+    field-radiation extension is written only when enabled, so other configs
+    stay loadable by the reference."""
+    from dataclasses import asdict
+
+    out = asdict(cfg)
+    out["physics"].pop("energy_source_map", None)
+    fr = out.get("field_radiation")
+    if fr is not None and not fr.get("every"):
+        out.pop("field_radiation")
+    return out
 
 
 # -- device binding -------------------------------------------------------------
