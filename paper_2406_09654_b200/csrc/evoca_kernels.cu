@@ -522,13 +522,6 @@ __device__ __forceinline__ Arrival arrival(const StepGeom& g, const WarpTile& wt
   return r;
 }
 
-__device__ __forceinline__ void ce_desc(u64& a, u64& b) {  // max first
-  const u64 hi = a > b ? a : b;
-  const u64 lo = a > b ? b : a;
-  a = hi;
-  b = lo;
-}
-
 __device__ __forceinline__ unsigned arrival_mask(const WarpTile& wt, int ty, int tx) {
   unsigned m = 0;
 #pragma unroll
@@ -576,29 +569,59 @@ __device__ __forceinline__ int resolve_cell(const Pass2Args& a, const WarpTile& 
       win = (u64)__float_as_uint(first0 ? q0 : q1) << 32;
       if (kRecord) win = arrival(g, wt, y, x, ty, tx, wd).key;
     } else {
-      // general: keys for all eight directions (absent = 0), sorting network
-      // (Batcher odd-even merge, 19 comparators), sequential sum
-      u64 k[8];
+      // general (>= 3 arrivals).  Quantities are >= 0, so their f32 bit
+      // patterns order like the values; equal quantities add identically in
+      // any order, so the sum only needs the quantities sorted descending
+      // (32-bit min/max network, 19 comparators) and the source index only
+      // breaks ties for the winner.  Present zero quantities sort last and
+      // add +0 (which only turns a -0 sum into +0).
+      unsigned qb[8];
+      unsigned qmax = 0, zeros = 0;
 #pragma unroll
-      for (int d = 0; d < 8; ++d) k[d] = (m & (1u << d)) ? arrival(g, wt, y, x, ty, tx, d).key : 0ull;
-      win = 0;
-      wd = 0;
+      for (int d = 0; d < 8; ++d) {
+        const bool pres = (m >> d) & 1u;
+        const unsigned b = pres ? __float_as_uint(__fadd_rn(wt.q[(ty + 1 - dir_dy(d)) * kWtHW + tx + 1 - dir_dx(d)],
+                                                            0.0f))
+                                : 0u;
+        qb[d] = b;
+        qmax = max(qmax, b);
+        zeros |= (pres && b == 0u) ? 1u : 0u;
+      }
+      unsigned tie = 0;
 #pragma unroll
-      for (int d = 0; d < 8; ++d)
-        if (k[d] > win) {
-          win = k[d];
-          wd = d;
+      for (int d = 0; d < 8; ++d) tie |= ((m >> d) & 1u) && qb[d] == qmax ? (1u << d) : 0u;
+      wd = __ffs(tie) - 1;
+      if (tie & (tie - 1)) {  // exact tie on the maximum: lowest global source wins
+        u64 best = arrival(g, wt, y, x, ty, tx, wd).key;
+        for (unsigned rest = tie & (tie - 1); rest; rest &= rest - 1) {
+          const int d = __ffs(rest) - 1;
+          const u64 k = arrival(g, wt, y, x, ty, tx, d).key;
+          if (k > best) {
+            best = k;
+            wd = d;
+          }
         }
+      }
       wh = (ty + 1 - dir_dy(wd)) * kWtHW + tx + 1 - dir_dx(wd);
-      ce_desc(k[0], k[1]); ce_desc(k[2], k[3]); ce_desc(k[4], k[5]); ce_desc(k[6], k[7]);
-      ce_desc(k[0], k[2]); ce_desc(k[1], k[3]); ce_desc(k[4], k[6]); ce_desc(k[5], k[7]);
-      ce_desc(k[1], k[2]); ce_desc(k[5], k[6]);
-      ce_desc(k[0], k[4]); ce_desc(k[1], k[5]); ce_desc(k[2], k[6]); ce_desc(k[3], k[7]);
-      ce_desc(k[2], k[4]); ce_desc(k[3], k[5]);
-      ce_desc(k[1], k[2]); ce_desc(k[3], k[4]); ce_desc(k[5], k[6]);
+      win = (u64)qmax << 32;
+      if (kRecord) win = arrival(g, wt, y, x, ty, tx, wd).key;
+#define EVO_CE(a, b)                 \
+  {                                  \
+    const unsigned hi = max(a, b);   \
+    b = min(a, b);                   \
+    a = hi;                          \
+  }
+      EVO_CE(qb[0], qb[1]) EVO_CE(qb[2], qb[3]) EVO_CE(qb[4], qb[5]) EVO_CE(qb[6], qb[7])
+      EVO_CE(qb[0], qb[2]) EVO_CE(qb[1], qb[3]) EVO_CE(qb[4], qb[6]) EVO_CE(qb[5], qb[7])
+      EVO_CE(qb[1], qb[2]) EVO_CE(qb[5], qb[6])
+      EVO_CE(qb[0], qb[4]) EVO_CE(qb[1], qb[5]) EVO_CE(qb[2], qb[6]) EVO_CE(qb[3], qb[7])
+      EVO_CE(qb[2], qb[4]) EVO_CE(qb[3], qb[5])
+      EVO_CE(qb[1], qb[2]) EVO_CE(qb[3], qb[4]) EVO_CE(qb[5], qb[6])
+#undef EVO_CE
 #pragma unroll
       for (int i = 0; i < 8; ++i)
-        if (k[i]) acc = __fadd_rn(acc, __uint_as_float((unsigned)(k[i] >> 32)));
+        if (qb[i]) acc = __fadd_rn(acc, __uint_as_float(qb[i]));
+      if (zeros) acc = __fadd_rn(acc, 0.0f);
     }
     const float qw = __uint_as_float((unsigned)(win >> 32));
     if (qw > before) {  // physics.py:325
