@@ -10,16 +10,19 @@
 //   k_hid_scan   cell offsets and 128-row tile offsets per slot
 //   k_hid_sense  sensor vectors (engine.py:164-177 order, 45 + 3 zero pad)
 //                written to the slot's row range, one 192-byte row per cell
-//   k_hid_net    persistent CTA per SM: per tile, A (128 x 48 sensors) and the
-//                slot's W1 / W2 staged in shared memory in the UMMA canonical
-//                K-major layout, z1 = A.W1^T by tcgen05.mma kind::tf32 into
-//                TMEM, epilogue z1 + b1 -> tanh -> shared memory, z2 = h.W2^T
-//                by a second MMA chain, epilogue z2 + b2 -> the reference
-//                sigmoid sequence -> the cell's actuator row.
-// FP32 accuracy from TF32 units: every operand is split x = hi + lo (both
-// TF32) and each product accumulates lo.hi + hi.lo + hi.hi in the FP32 TMEM
-// accumulator ("3xTF32"; measured max |err| / sum|a.b| = 3.6e-7,
-// tools/microbench/tc_tf32.cu).  The physics then runs as pass 1 with these
+//   k_hid_net    persistent CTA per SM: per 128-row tile (one genome), A
+//                (128 x 48 sensors) and the slot's W1 staged in shared
+//                memory in the UMMA canonical K-major layout, z1 = A.W1^T by
+//                tcgen05.mma kind::tf32 into one of two TMEM accumulator
+//                buffers (the next tile's layer 1 runs during this tile's
+//                epilogue); epilogue z1 + b1 -> tanh -> z2 = h.W2^T in FP32
+//                FMAs -> + b2 -> the reference sigmoid sequence -> the
+//                cell's actuator row.
+// FP32 accuracy from TF32 units (layer 1): every operand is split x = hi +
+// lo (both TF32) and each product accumulates lo.hi + hi.lo + hi.hi in the
+// FP32 TMEM accumulator ("3xTF32"; measured max |err| / sum|a.b| = 3.6e-7,
+// tools/microbench/tc_tf32.cu).  Layer 2 is fmaf-chained FP32 in hidden-unit
+// order per quarter, the four quarter sums added in order.  The physics then runs as pass 1 with these
 // actions injected (bit-exact physics given the actions).
 
 #include <algorithm>
@@ -47,15 +50,14 @@ namespace {
 
 constexpr int kRows = 128;   // MMA M: cells per tile
 constexpr int kK1 = 48;      // 45 sensors padded to the TF32 K granularity (8)
-constexpr int kNetThreads = 256;
+constexpr int kNetThreads = 512;  // 16 warps: four per TMEM lane quadrant
 constexpr int kTmemCols = 512;
 // The TF32 MMA accumulates in TMEM with less than FP32 rounding accuracy
 // (tools/microbench/tc_split.cu: rms error 3x an FP32 FMA chain, whatever the
-// operand split).  Partial sums therefore go to separate accumulators - two
-// of three K=8 steps each in layer 1, one per two K steps in layer 2 (see the
-// TMEM map at k_hid_net) - and are added in FP32 on the CUDA cores in k order;
-// H=128 actions stay within 4e-6 of the float64 oracle (the CUDA-core FP32
-// net: 4.8e-6).
+// operand split).  Layer-1 partial sums therefore go to two accumulators
+// (three K=8 steps each, see the TMEM map at k_hid_net) added in FP32 on the
+// CUDA cores in k order; actions stay within the 1e-5 relative tier-B
+// tolerance of the float64 oracle (test_tensor_core_net_vs_oracle_and_cuda_core).
 
 // Deterministic counting sort of the occupied cells by slot, without hot
 // global atomics: each CTA owns kSortTiles consecutive 32x32 tiles (tile
@@ -311,32 +313,17 @@ __device__ __forceinline__ void put_split(unsigned char* hi, unsigned char* lo, 
   *reinterpret_cast<float*>(lo + off) = l;
 }
 
-// TMEM map (512 columns, lanes = the tile's 128 rows):
-//   [0, nh)      layer-1 accumulator 0 (K steps 0-2), then tanh(h) hi  (A of layer 2)
-//   [128, +nh)   layer-1 accumulator 1 (K steps 3-5), then tanh(h) lo
-//   [256, 512)   layer-2 accumulator sets, one per two K=8 steps (32 columns:
-//                hi.hi + lo.hi in 0-15, hi.lo in 16-31)
-// Epilogue 1 turns the two accumulators into h in place (each lane reads its
-// row's columns before writing them), so layer 2 reads its A operand from
-// TMEM (no shared-memory round trip) and only W2 (32 x 8 per step: hi and
-// lo rows) from shared memory.
-constexpr int kAccH = 128;    // TMEM column of layer-1 accumulator 1 / h lo
-constexpr int kD2 = 256;      // TMEM column of the layer-2 accumulators
-
-__device__ __forceinline__ void tmem_st8(uint32_t addr, const float v[8]) {
-  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(addr),
-               "r"(__float_as_uint(v[0])), "r"(__float_as_uint(v[1])), "r"(__float_as_uint(v[2])),
-               "r"(__float_as_uint(v[3])), "r"(__float_as_uint(v[4])), "r"(__float_as_uint(v[5])),
-               "r"(__float_as_uint(v[6])), "r"(__float_as_uint(v[7])));
-}
-
-__device__ __forceinline__ void mma_tf32_ta(uint32_t d_tmem, uint32_t a_tmem, uint64_t b, uint32_t idesc,
-                                            uint32_t acc) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(d_tmem),
-      "r"(a_tmem), "l"(b), "r"(idesc), "r"(acc));
-}
+// TMEM map (512 columns, lanes = the tile's 128 rows): two layer-1
+// accumulator buffers, one per tile in flight; buffer b at columns
+// [256 b, 256 b + 2 nh): accumulator 0 (K steps 0-2) in the first nh columns,
+// accumulator 1 (K steps 3-5) in the next nh.  Layer 2 (45->H->13: H x 13
+// MACs per cell, N = 13) runs on the CUDA cores inside the tanh epilogue:
+// as 13-column tensor-core MMAs it was issue-bound (32 tcgen05.mma of
+// ~60 issue cycles each per tile, tools/microbench/tc_rate.cu), and keeping
+// it off the tensor core frees the TMEM that lets the next tile's layer 1 run
+// during this tile's epilogue.
+constexpr int kAccBuf = 256;  // TMEM columns per layer-1 accumulator buffer
+constexpr int kXPitch = 4 * kActuators + 1;  // exchange row: 4 quarter sums x 13, odd pitch
 
 __global__ void __launch_bounds__(kNetThreads, 1) k_hid_net(const NetArgs a) {
   extern __shared__ __align__(1024) unsigned char smem[];
@@ -344,14 +331,15 @@ __global__ void __launch_bounds__(kNetThreads, 1) k_hid_net(const NetArgs a) {
   const int H = a.net.hidden, hp = a.net.hpad;
   unsigned char* B1hi = smem;
   unsigned char* B1lo = B1hi + nh * kK1 * 4;
-  unsigned char* B2 = B1lo + nh * kK1 * 4;  // [W2 hi (16 rows) ; W2 lo (16 rows)] x nh, canonical R=32
-  float* b1 = reinterpret_cast<float*>(B2 + 32 * nh * 4);
+  float* W2s = reinterpret_cast<float*>(B1lo + nh * kK1 * 4);  // [nh][16]: W2^T rows
+  float* b1 = W2s + nh * 16;
   float* b2 = b1 + nh;
-  unsigned char* A1 = reinterpret_cast<unsigned char*>(((uintptr_t)(b2 + 16) + 1023) & ~(uintptr_t)1023);
+  float* xbuf = b2 + 16;  // [kRows][kXPitch] quarter-sum exchange (odd pitch: conflict-free)
+  unsigned char* A1 = reinterpret_cast<unsigned char*>(((uintptr_t)(xbuf + kRows * kXPitch) + 1023) & ~(uintptr_t)1023);
   constexpr int kA1Bytes = kRows * kK1 * 4;  // one of hi / lo
   // A1 double buffer: buffer i at A1 + i * 2 * kA1Bytes (hi) and + kA1Bytes (lo)
   __shared__ uint32_t tmem_base;
-  __shared__ __align__(8) uint64_t bar1, bar2;
+  __shared__ __align__(8) uint64_t bar[2];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 
   const int T = *a.n_tiles;
@@ -360,46 +348,41 @@ __global__ void __launch_bounds__(kNetThreads, 1) k_hid_net(const NetArgs a) {
   if (t0 >= t1) return;
   if (warp == 0) tc::tmem_alloc<kTmemCols>(&tmem_base);
   if (tid == 0) {
-    tc::mbar_init(&bar1, 1);
-    tc::mbar_init(&bar2, 1);
+    tc::mbar_init(&bar[0], 1);
+    tc::mbar_init(&bar[1], 1);
   }
   tc::fence_before();
   __syncthreads();
   tc::fence_after();
   const uint32_t tmem = tmem_base;
-  uint32_t ph1 = 0, ph2 = 0;
-  const uint32_t id1 = tc::idesc_tf32(kRows, nh), id2 = tc::idesc_tf32(kRows, 16),
-                 id2w = tc::idesc_tf32(kRows, 32);
-  const bool issuer = tid == 4 * 32;  // warp 4 issues the MMAs (warps 0-3 run epilogue 2 meanwhile)
+  uint32_t ph0 = 0u, ph1 = 0u;
+  const uint32_t id1 = tc::idesc_tf32(kRows, nh);
+  const bool issuer = tid == 4 * 32;
 
-  auto locate = [&](int t, int& slot, int& row0, int& nrows) {
-    const int4 ti = __ldg(a.tile_info + t);
-    slot = ti.x;
-    row0 = ti.y;
-    nrows = ti.z;
-  };
-  const int ar = tid >> 1, ahalf = tid & 1;  // this thread's half sensor row
-  float4 pf[6];
-  auto fetch = [&](int row0, int nrows) {
-    const float4* src = reinterpret_cast<const float4*>(a.sens + (size_t)(row0 + ar) * kK1) + ahalf * 6;
+  const int ar = tid >> 2, aq = tid & 3;  // this thread's quarter sensor row (staging)
+  float4 pf[3];
+  auto fetch = [&](const int4 ti) {
+    const float4* src = reinterpret_cast<const float4*>(a.sens + (size_t)(ti.y + ar) * kK1) + aq * 3;
 #pragma unroll
-    for (int q = 0; q < 6; ++q) pf[q] = ar < nrows ? __ldg(src + q) : make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int q = 0; q < 3; ++q) pf[q] = ar < ti.z ? __ldg(src + q) : make_float4(0.f, 0.f, 0.f, 0.f);
   };
-  // split the prefetched half row into A1 buffer `buf` (canonical layout); element
-  // 45 of a row is its cell index
+  // split the prefetched quarter row into A1 buffer `buf` (canonical
+  // layout); element 45 of a row is its cell index
   auto stage_a1 = [&](int buf) {
     unsigned char* hi = A1 + buf * 2 * kA1Bytes;
     unsigned char* lo = hi + kA1Bytes;
-    if (ahalf == 1) pf[5].y = 0.0f;  // element 45 carries the cell index
 #pragma unroll
-    for (int q = 0; q < 6; ++q) {
-      const float4 v = pf[q];
+    for (int q = 0; q < 3; ++q) {
+      float4 v = pf[q];
+      // (never written back into pf: a modified component made the compiler
+      // copy it right after its load, exposing the whole load latency)
+      if (q == 2 && aq == 3) v.y = 0.0f;
       float4 h4, l4;
       split_fast(v.x, h4.x, l4.x);
       split_fast(v.y, h4.y, l4.y);
       split_fast(v.z, h4.z, l4.z);
       split_fast(v.w, h4.w, l4.w);
-      const uint32_t off = tc::canon_off(ar, (ahalf * 6 + q) * 4, kRows);
+      const uint32_t off = tc::canon_off(ar, (aq * 3 + q) * 4, kRows);
       *reinterpret_cast<float4*>(hi + off) = h4;
       *reinterpret_cast<float4*>(lo + off) = l4;
     }
@@ -414,51 +397,50 @@ __global__ void __launch_bounds__(kNetThreads, 1) k_hid_net(const NetArgs a) {
     const float* W2 = a.net.wB + (size_t)slot * hp * kOutPad;
     for (int i = tid; i < 16 * nh; i += kNetThreads) {
       const int j = i & 15, h = i >> 4;
-      const float w = (h < H && j < kActuators) ? __ldg(W2 + (size_t)h * kOutPad + j) : 0.0f;
-      float hi, lo;
-      tc::split_tf32(w, hi, lo);
-      *reinterpret_cast<float*>(B2 + tc::canon_off(j, h, 32)) = hi;
-      *reinterpret_cast<float*>(B2 + tc::canon_off(16 + j, h, 32)) = lo;
+      W2s[i] = (h < H && j < kActuators) ? __ldg(W2 + (size_t)h * kOutPad + j) : 0.0f;
     }
     for (int h = tid; h < nh; h += kNetThreads) b1[h] = h < H ? __ldg(a.net.bA + (size_t)slot * hp + h) : 0.0f;
     if (tid < 16) b2[tid] = tid < kActuators ? __ldg(a.net.bB + (size_t)slot * kOutPad + tid) : 0.0f;
   };
-  // layer 1 of the tile in A1 buffer `buf`: 6 K steps x (lo.hi, hi.lo, hi.hi),
-  // accumulator 0 for steps 0-2, accumulator 1 for steps 3-5
+  // layer 1 of the tile in A1 buffer `buf` into TMEM buffer `buf`: 6 K steps x
+  // (lo.hi, hi.lo, hi.hi), accumulator 0 for steps 0-2, accumulator 1 for 3-5
   auto issue_l1 = [&](int buf) {
     if (issuer) {
       const uint32_t lA = kRows * 16, lB = nh * 16;
       const uint32_t ah = tc::smem_u32(A1 + buf * 2 * kA1Bytes), al = ah + kA1Bytes;
       const uint32_t bh = tc::smem_u32(B1hi), bl = tc::smem_u32(B1lo);
-      // the two accumulators interleaved (independent consecutive MMAs)
+      const uint32_t tb = tmem + (uint32_t)(buf * kAccBuf);
 #pragma unroll
       for (int j = 0; j < 3; ++j)
 #pragma unroll
         for (int acc = 0; acc < 2; ++acc) {
           const int ks = acc * 3 + j;
           const uint32_t oa = 2 * ks * lA, ob = 2 * ks * lB;
-          const uint32_t d = tmem + (acc ? (uint32_t)kAccH : 0u);
+          const uint32_t d = tb + (acc ? (uint32_t)nh : 0u);
           tc::mma_tf32(d, tc::smem_desc(al + oa, lA, 128), tc::smem_desc(bh + ob, lB, 128), id1, j > 0);
           tc::mma_tf32(d, tc::smem_desc(ah + oa, lA, 128), tc::smem_desc(bl + ob, lB, 128), id1, 1);
           tc::mma_tf32(d, tc::smem_desc(ah + oa, lA, 128), tc::smem_desc(bh + ob, lB, 128), id1, 1);
         }
-      tc::commit(&bar1);
+      tc::commit(&bar[buf]);
     }
   };
 
-  int slot, row0, nrows;
-  locate(t0, slot, row0, nrows);
-  fetch(row0, nrows);
-  int cur = slot;
+  // tile infos t, t + 1, t + 2, t + 3 ride along in registers, so that no
+  // row fetch waits on a dependent tile-info load
+  const int4 z4 = make_int4(0, 0, 0, 0);
+  int4 ti0 = __ldg(a.tile_info + t0);
+  int4 ti1 = t0 + 1 < t1 ? __ldg(a.tile_info + t0 + 1) : z4;
+  int4 ti2 = t0 + 2 < t1 ? __ldg(a.tile_info + t0 + 2) : z4;
+  int4 ti3 = t0 + 3 < t1 ? __ldg(a.tile_info + t0 + 3) : z4;
+  int cur = ti0.x;
+  fetch(ti0);
   stage_weights(cur);
   stage_a1(0);
-  int nslot = slot, nrow0, nnrows;
   if (t0 + 1 < t1) {
-    locate(t0 + 1, nslot, nrow0, nnrows);
-    fetch(nrow0, nnrows);
+    fetch(ti1);
+    stage_a1(1);
   }
-  // tile info one more tile ahead, so fetch() never waits on it
-  int4 ti2 = t0 + 2 < t1 ? __ldg(a.tile_info + t0 + 2) : make_int4(0, 0, 0, 0);
+  if (t0 + 2 < t1) fetch(ti2);
   tc::fence_async_smem();
   tc::fence_before();
   __syncthreads();
@@ -467,139 +449,128 @@ __global__ void __launch_bounds__(kNetThreads, 1) k_hid_net(const NetArgs a) {
   long long t_mark = clock64();
   (void)t_mark;
 
+  const int q = warp & 3, qt = warp >> 2;  // TMEM lane quadrant, hidden-unit quarter
+  const int r = q * 32 + lane;               // this thread's tile row (TMEM lane)
+  const int c_begin = qt * (nh / 4), c_end = c_begin + nh / 4;
   for (int t = t0; t < t1; ++t) {
     const int buf = (t - t0) & 1;
-    const int cur_nrows = nrows, cur_row0 = row0;
+    const int4 ti = ti0;
     const bool has_next = t + 1 < t1;
-    // (a) next tile's rows into the other A1 buffer while layer 1 runs
-    if (has_next) stage_a1(buf ^ 1);
-    int n2slot = nslot, n2row0 = 0, n2nrows = 0;
-    if (t + 2 < t1) {
-      n2slot = ti2.x;
-      n2row0 = ti2.y;
-      n2nrows = ti2.z;
-      fetch(n2row0, n2nrows);
-      if (t + 3 < t1) ti2 = __ldg(a.tile_info + t + 3);
-    }
+    const int next_slot = has_next ? ti1.x : cur;
+    ti0 = ti1;
+    ti1 = ti2;
+    ti2 = ti3;
+    ti3 = t + 4 < t1 ? __ldg(a.tile_info + t + 4) : z4;
+    // (a) the next tile's layer 1 (same genome: its weights are resident) runs
+    //     on the tensor core during this tile's epilogue
+    const bool early = has_next && next_slot == cur;
+    if (early) issue_l1(buf ^ 1);
     HID_MARK(0);
-    // (b) epilogue 1: z1 = acc0 + acc1 + b1 -> tanh -> h (hi, lo) in place in TMEM
-    tc::mbar_wait(&bar1, ph1);
-    ph1 ^= 1;
+    tc::mbar_wait(&bar[buf], buf ? ph1 : ph0);
+    if (buf) ph1 ^= 1u; else ph0 ^= 1u;
     tc::fence_after();
     HID_MARK(1);
-    {
-      const int q = warp & 3;
-      const uint32_t lb = tmem + ((uint32_t)(q * 32) << 16);
-      const int c_begin = (warp >> 2) * (nh / 2), c_end = c_begin + nh / 2;
-      int c0 = c_begin;
-      for (; c0 + 16 <= c_end; c0 += 16) {  // 16-column chunks (each warp's half is a multiple of 8)
-        float v[16], p[16];
-        tc::tmem_ld16(lb + c0, v);
-        tc::tmem_ld16(lb + kAccH + c0, p);
-        float hh[16], ll[16];
-#pragma unroll
-        for (int j = 0; j < 16; ++j) {
-          const float th = tanh_sfu(__fadd_rn(__fadd_rn(v[j], p[j]), b1[c0 + j]));
-          split_fast(th, hh[j], ll[j]);
-        }
-        tmem_st8(lb + c0, hh);
-        tmem_st8(lb + c0 + 8, hh + 8);
-        tmem_st8(lb + kAccH + c0, ll);
-        tmem_st8(lb + kAccH + c0 + 8, ll + 8);
-      }
-      if (c0 < c_end) {  // an 8-column tail
-        float v[8], p[8];
-        tc::tmem_ld8(lb + c0, v);
-        tc::tmem_ld8(lb + kAccH + c0, p);
-        float hh[8], ll[8];
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          const float th = tanh_sfu(__fadd_rn(__fadd_rn(v[j], p[j]), b1[c0 + j]));
-          split_fast(th, hh[j], ll[j]);
-        }
-        tmem_st8(lb + c0, hh);
-        tmem_st8(lb + kAccH + c0, ll);
-      }
-      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-    }
+    // (b) rows of tile t + 2 into this tile's A1 buffer (its layer 1 is done),
+    //     then the rows of tile t + 3 into registers
+    if (t + 2 < t1) stage_a1(buf);
+    if (t + 3 < t1) fetch(ti2);  // (shifted: ti2 now holds tile t + 3)
     HID_MARK(2);
+    // (c) epilogue: z1 = acc0 + acc1 + b1 -> tanh -> z2 += h W2 (FP32, h
+    //     ascending) over this thread's quarter of the hidden units
+    {
+      const uint32_t lb = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(buf * kAccBuf);
+      u64 z2p[6];
+      float z12 = 0.0f;
+#pragma unroll
+      for (int p = 0; p < 6; ++p) z2p[p] = 0ull;
+      auto column = [&](int h, float s) {
+        const float th = tanh_sfu(__fadd_rn(s, b1[h]));
+        const float4* w4 = reinterpret_cast<const float4*>(W2s + h * 16);
+        const float4 wa = w4[0], wb = w4[1], wc = w4[2], wd = w4[3];
+        ffma2(z2p[0], th, pk2(wa.x, wa.y));
+        ffma2(z2p[1], th, pk2(wa.z, wa.w));
+        ffma2(z2p[2], th, pk2(wb.x, wb.y));
+        ffma2(z2p[3], th, pk2(wb.z, wb.w));
+        ffma2(z2p[4], th, pk2(wc.x, wc.y));
+        ffma2(z2p[5], th, pk2(wc.z, wc.w));
+        z12 = fmaf(th, wd.x, z12);
+      };
+      uint32_t v[16], pv[16];
+      int c0 = c_begin;
+      if (c0 + 16 <= c_end) {
+        tc::tmem_ld16_nw(lb + c0, v);
+        tc::tmem_ld16_nw(lb + nh + c0, pv);
+      }
+      for (; c0 + 16 <= c_end; c0 += 16) {  // 16-column chunks, the next chunk's loads in flight
+        tc::tmem_wait_ld();
+        tc::reg_fence(v);
+        tc::reg_fence(pv);
+        float sum[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) sum[j] = __fadd_rn(__uint_as_float(v[j]), __uint_as_float(pv[j]));
+        if (c0 + 32 <= c_end) {
+          tc::tmem_ld16_nw(lb + c0 + 16, v);
+          tc::tmem_ld16_nw(lb + nh + c0 + 16, pv);
+        }
+#pragma unroll
+        for (int j = 0; j < 16; ++j) column(c0 + j, sum[j]);
+      }
+      for (; c0 < c_end; c0 += 4) {  // 4-column tail (nh / 4 is a multiple of 4)
+        uint32_t va[4], pa[4];
+        tc::tmem_ld4_nw(lb + c0, va);
+        tc::tmem_ld4_nw(lb + nh + c0, pa);
+        tc::tmem_wait_ld();
+        tc::reg_fence(va);
+        tc::reg_fence(pa);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) column(c0 + j, __fadd_rn(__uint_as_float(va[j]), __uint_as_float(pa[j])));
+      }
+      float z2[kActuators];
+#pragma unroll
+      for (int p = 0; p < 6; ++p) up2(z2p[p], z2[2 * p], z2[2 * p + 1]);
+      z2[12] = z12;
+      // (d) quarter sums through shared memory; thread quarter qt finishes
+      //     outputs 4 qt .. 4 qt + 3 as ((q0 + q1) + q2) + q3 + b2
+      float* xr = xbuf + r * kXPitch;
+#pragma unroll
+      for (int j = 0; j < kActuators; ++j) xr[qt * kActuators + j] = z2[j];
+      HID_MARK(3);
+      __syncthreads();
+      HID_MARK(4);
+      const int jh = qt * 4;
+      if (r < ti.z) {  // actuator row at its sorted position: 16-byte quarters, coalesced
+        float o[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int jj = jh + j;
+          if (jj < kActuators) {
+            float zz = __fadd_rn(xr[jj], xr[kActuators + jj]);
+            zz = __fadd_rn(zz, xr[2 * kActuators + jj]);
+            zz = __fadd_rn(zz, xr[3 * kActuators + jj]);
+            o[j] = squash(__fadd_rn(zz, b2[jj]));
+          } else {
+            o[j] = 0.0f;
+          }
+        }
+        reinterpret_cast<float4*>(a.act + (size_t)(ti.y + r) * 16)[qt] = make_float4(o[0], o[1], o[2], o[3]);
+      }
+    }
+    HID_MARK(5);
+    // (e) end of tile: TMEM buffer, exchange rows and staged A1 free / visible
+    tc::fence_async_smem();
     tc::fence_before();
     __syncthreads();
     tc::fence_after();
-    HID_MARK(3);
-    // (c) layer 2 from TMEM: A = h, B = W2.  Per K step two MMAs: h_hi x [W2 hi ;
-    //     W2 lo] (N = 32: hi.hi in columns 0-15, hi.lo in 16-31, h_hi read once)
-    //     and h_lo x W2 hi (N = 16, into columns 0-15); accumulator set g =
-    //     columns kD2 + 32 g holds K steps 2g, 2g+1.
-    if (issuer) {
-      const uint32_t lB = 32 * 16;
-      const uint32_t b = tc::smem_u32(B2);
-      for (int ks = 0; ks < nh / 8; ++ks) {
-        const uint32_t d = tmem + kD2 + (uint32_t)((ks >> 1) * 32);
-        const uint64_t desc = tc::smem_desc(b + 2 * ks * lB, lB, 128);
-        mma_tf32_ta(d, tmem + (uint32_t)(ks * 8), desc, id2w, ks & 1);  // initialises all 32 columns of a set
-        mma_tf32_ta(d, tmem + kAccH + (uint32_t)(ks * 8), desc, id2, 1);
-      }
-      tc::commit(&bar2);
-    }
-    float bias2[16];
-#pragma unroll
-    for (int j = 0; j < 16; ++j) bias2[j] = b2[j];
-    tc::mbar_wait(&bar2, ph2);
-    ph2 ^= 1;
-    tc::fence_after();
-    HID_MARK(4);
-    // (d) next tile's layer 1 (its weights first if the slot changes) runs
-    //     while this tile's second epilogue reads the layer-2 accumulators
-    if (has_next) {
-      if (nslot != cur) {
-        __syncthreads();  // every warp has read b2 above
-        cur = nslot;
-        stage_weights(cur);
-      }
+    if (has_next && !early) {  // genome change: restage the weights, then layer 1
+      cur = next_slot;
+      stage_weights(cur);
       tc::fence_async_smem();
       tc::fence_before();
       __syncthreads();
       tc::fence_after();
       issue_l1(buf ^ 1);
     }
-    HID_MARK(5);
-    // (e) epilogue 2: sum the accumulator sets in k order, + b2, reference
-    //     sigmoid; warps w and w+4 share the rows of quadrant w, outputs 0-7 / 8-12
-    {
-      const int q = warp & 3, r = q * 32 + lane, jh = (warp >> 2) * 8;
-      const uint32_t lb = tmem + ((uint32_t)(q * 32) << 16) + kD2 + jh;
-      float z[8], pa[8], pb[8];
-      tc::tmem_ld8(lb, pa);
-      tc::tmem_ld8(lb + 16, pb);
-#pragma unroll
-      for (int j = 0; j < 8; ++j) z[j] = __fadd_rn(pa[j], pb[j]);
-      for (int g = 1; g < nh / 16; ++g) {
-        tc::tmem_ld8(lb + g * 32, pa);
-        tc::tmem_ld8(lb + g * 32 + 16, pb);
-#pragma unroll
-        for (int j = 0; j < 8; ++j) z[j] = __fadd_rn(z[j], __fadd_rn(pa[j], pb[j]));
-      }
-      if (r < cur_nrows) {  // actuator row at its sorted position: 32-byte aligned halves, coalesced
-        float v[8];
-#pragma unroll
-        for (int j = 0; j < 8; ++j) v[j] = jh + j < kActuators ? squash(__fadd_rn(z[j], bias2[jh + j])) : 0.0f;
-        float4* dst = reinterpret_cast<float4*>(a.act + (size_t)(cur_row0 + r) * 16 + jh);
-        dst[0] = make_float4(v[0], v[1], v[2], v[3]);
-        dst[1] = make_float4(v[4], v[5], v[6], v[7]);
-      }
-    }
     HID_MARK(6);
-    tc::fence_before();
-    __syncthreads();
-    tc::fence_after();
-    HID_MARK(7);
-    slot = nslot;
-    row0 = nrow0;
-    nrows = nnrows;
-    nslot = n2slot;
-    nrow0 = n2row0;
-    nnrows = n2nrows;
   }
   __syncthreads();
   if (warp == 0) tc::tmem_dealloc<kTmemCols>(tmem);
@@ -750,7 +721,7 @@ bool hidden_tc_supported(int hidden) { return hidden >= 1 && hidden_tc_nh(hidden
 
 size_t hidden_tc_smem(int hidden) {
   const int nh = hidden_tc_nh(hidden);
-  const size_t fixed = (size_t)2 * nh * kK1 * 4 + (size_t)32 * nh * 4 + (size_t)(nh + 16) * 4;
+  const size_t fixed = (size_t)2 * nh * kK1 * 4 + (size_t)16 * nh * 4 + (size_t)(nh + 16) * 4 + (size_t)kRows * kXPitch * 4;
   return ((fixed + 1023) & ~(size_t)1023) + (size_t)4 * kRows * kK1 * 4 + 1024;  // + alignment slack
 }
 

@@ -793,8 +793,13 @@ __global__ void __launch_bounds__(kThreads2) k_resolve(const Pass2Args a) {
   if (lane == 0 && my_adopt) atomicAdd(&s_adopt, my_adopt);
   __syncthreads();
   if (tid == 0 && s_adopt) atomicAdd((unsigned long long*)&a.census.stats[0], (unsigned long long)s_adopt);
+#ifndef EVO_DIAG_NO_FLUSH
   for (int b = tid; b < a.capacity; b += kThreads2)
     if (hist[b]) atomicAdd(&a.census.counts[b], hist[b]);
+#endif
+#ifdef EVO_DIAG_NO_TICKET  // diagnostics builds only: census not finished
+  return;
+#endif
   if (!a.run_census) return;
   // last CTA: census epilogue (physics.py:395-404, neuroevo.py:521-542).
   // One cumulative release fence by thread 0 after the barrier publishes the
@@ -1062,13 +1067,23 @@ cudaError_t launch_pass1(const Pass1Args& a, bool inject, bool export_actions, c
   return export_actions ? launch_direct<true, false>(a, st) : launch_direct<false, false>(a, st);
 }
 
-cudaError_t launch_pass2(const Pass2Args& a, cudaStream_t st) {
+cudaError_t launch_census_finish(const Census& c, int capacity, long long t, cudaStream_t st);
+
+cudaError_t launch_pass2(const Pass2Args& a_in, cudaStream_t st) {
+  Pass2Args a = a_in;
+#ifdef EVO_K2_SPLIT_CENSUS
+  // census epilogue as its own launch instead of the last-CTA ticket: the
+  // ticket's per-CTA GPU-scope fence costs ~4 us of k_resolve, the extra
+  // launch about the same (measured), so the ticket stays the default
+  const bool finish = a.run_census != 0;
+  a.run_census = 0;
+#endif
   const int tiles = ((a.g.W + kWtW - 1) / kWtW) * ((a.g.H + kWtH - 1) / kWtH);
   // few CTAs, many warp tiles each: the per-CTA census flush (capacity
   // global atomics on shared addresses) and the completion ticket are
   // serialised in L2, so they must not scale with the grid
 #ifndef EVO_K2_GRID_FACTOR
-#define EVO_K2_GRID_FACTOR 8
+#define EVO_K2_GRID_FACTOR 4
 #endif
   int grid = num_sms() * EVO_K2_GRID_FACTOR;
   const int need = (tiles + kWarps2 - 1) / kWarps2;
@@ -1085,6 +1100,13 @@ cudaError_t launch_pass2(const Pass2Args& a, cudaStream_t st) {
     if (e != cudaSuccess) return e;
     k_resolve<false><<<grid, kThreads2, smem, st>>>(a);
   }
+#ifdef EVO_K2_SPLIT_CENSUS
+  if (finish) {
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    return launch_census_finish(a.census, a.capacity, a.t, st);
+  }
+#endif
   return cudaGetLastError();
 }
 

@@ -68,8 +68,8 @@ def main():
         hc = np.zeros(8, np.uint64)
         _lib.check(_lib.load().evo_debug_hidden_cycles(_lib.ptr(hc), 1))
         if hc.sum():
-            names = ["stage A1 + prefetch", "wait L1 MMA", "epilogue 1", "sync", "L2 issue + wait",
-                     "restage + L1 issue", "epilogue 2", "tile-end sync"]
+            names = ["tile end + L1 issue", "wait L1 MMA", "stage A1 + fetch", "epilogue (tanh, layer 2)",
+                     "exchange sync", "finish + store", "tile-end sync + restage", "-"]
             tot = float(hc.sum())
             for i, n in enumerate(names):
                 print(f"hid {n:22s} {hc[i] / tot * 100:5.1f}%  {hc[i] / 148 / args.steps:12.0f} cycles/CTA-step")
