@@ -46,6 +46,11 @@ struct evo_ctx {
   int front = 0;
   evo::Mid mid = {};
   float *wA = nullptr, *bA = nullptr, *wB = nullptr, *bB = nullptr;
+  // direct nets of pools <= kMmaSlots: fragment-order copy for the mma.sync
+  // tile kernel (EVO_F_MMA_NET), rebuilt on the stream before the next such
+  // pass 1 after any weight write
+  float* wF = nullptr;
+  bool frag_stale = true;
   evo::Census census = {};
   float* act_in = nullptr;
   uint8_t* act_in_flag = nullptr;
@@ -94,6 +99,7 @@ struct evo_ctx {
     p.bA = bA;
     p.wB = wB;
     p.bB = bB;
+    p.wF = nullptr;
     return p;
   }
   evo::StepGeom geom() const {
@@ -203,6 +209,8 @@ int create_impl(evo_ctx** out, int width, int height, long long row0, int hg, in
     if ((e = c->alloc(&c->wA, cap * evo::kSensors * 12)) != cudaSuccess) return bail(e, "alloc w");
     if ((e = c->alloc(&c->wB, (cap * evo::kSensors + 3) / 4 * 4)) != cudaSuccess) return bail(e, "alloc w");
     if ((e = c->alloc(&c->bA, cap * evo::kOutPad)) != cudaSuccess) return bail(e, "alloc b");
+    if (capacity <= evo::kMmaSlots && (e = c->alloc(&c->wF, cap * evo::kFragGenome)) != cudaSuccess)
+      return bail(e, "alloc wF");
   } else {
     if ((e = c->alloc(&c->wA, cap * evo::kSensors * c->hpad)) != cudaSuccess) return bail(e, "alloc w1");
     if ((e = c->alloc(&c->bA, cap * c->hpad)) != cudaSuccess) return bail(e, "alloc b1");
@@ -360,6 +368,14 @@ int pass1_view(evo_ctx* c, const View& v, const evo_scalars* s, int phases, int 
   a.net.bA = c->bA;
   a.net.wB = c->wB;
   a.net.bB = c->bB;
+  a.net.wF = nullptr;
+  if (c->wF && !inject && !via_rows && (flags & EVO_F_MMA_NET)) {
+    if (c->frag_stale) {
+      CK(evo::launch_frag_relayout(c->params(), c->cap, c->wF, st));
+      c->frag_stale = false;
+    }
+    a.net.wF = c->wF;
+  }
   a.s = to_scalars(*s);
   a.phases = phases;
   a.src_map = c->have_src_map ? c->src_map + v.off : nullptr;
@@ -499,6 +515,7 @@ EVO_API int evo_set_params(evo_ctx* c, int slot0, int n, const float* w1, const 
     CK(cudaMemcpy(c->wA + (size_t)slot0 * evo::kSensors * 12, w12.data(), w12.size() * 4, cudaMemcpyHostToDevice));
     CK(cudaMemcpy(c->wB + (size_t)slot0 * evo::kSensors, w1.data(), w1.size() * 4, cudaMemcpyHostToDevice));
     CK(cudaMemcpy(c->bA + (size_t)slot0 * evo::kOutPad, bt.data(), bt.size() * 4, cudaMemcpyHostToDevice));
+    c->frag_stale = true;
     return 0;
   }
   const int hp = c->hpad;
@@ -1099,6 +1116,7 @@ EVO_API int evo_express_cppn(evo_ctx* c, int n, const int32_t* slots, const int3
   put(coords, (size_t)ncoord * 8);
   cudaError_t e = cudaMemcpyAsync(dbuf, h.data(), h.size(), cudaMemcpyHostToDevice, st);
   if (e == cudaSuccess) e = evo::launch_express_cppn(b, c->params(), c->wA, c->bA, c->wB, c->bB, st);
+  c->frag_stale = true;
   if (e == cudaSuccess) e = cudaStreamSynchronize(st);
   cudaFree(dbuf);
   CK(e);

@@ -21,6 +21,11 @@ constexpr int kActuators = 13;
 constexpr int kOutPad = 16;              // 13 actuators padded to 4 float4
 constexpr int kMaxCapacity = 8192;       // device census bins per CTA (smem)
 constexpr int kSmemWeightSlotsAbi = 68;  // largest pool the tile kernel keeps in shared memory
+// Tensor-core direct net (k_pass1_mma): per-genome weights in mma.sync A-fragment
+// order, 6 K-steps x (lanes 0-19: 4 floats, lanes 20-31: 2 floats) + bias[16].
+constexpr int kMmaSlots = 64;            // largest pool k_pass1_mma keeps in shared memory
+constexpr int kFragStep = 20 * 4 + 12 * 2;
+constexpr int kFragGenome = 6 * kFragStep + 16;
 
 // Proposal byte written by pass 1 (one per cell): one-hot shipment direction
 // (bit d set: the cell ships in direction d this step), 0 = no shipment.
@@ -57,6 +62,7 @@ struct Params {
   const float* bA;  // direct: bias [cap][16];     hidden: b1 [cap][hpad]
   const float* wB;  // direct: W1 [cap][45] (actuator 12); hidden: W2^T [cap][hpad][16]
   const float* bB;  // hidden: b2 [cap][16]
+  const float* wF;  // direct, pools <= kMmaSlots: fragment-order table [cap][kFragGenome] (or null)
 };
 
 struct Census {
@@ -159,6 +165,7 @@ int cppn_threads(int max_nodes);  // 0 -> program too large
 cudaError_t launch_express_cppn(const CppnBatch& b, const Params& net, float* wA, float* bA, float* wB, float* bB,
                                 cudaStream_t st);
 cudaError_t launch_pass1(const Pass1Args& a, bool inject, bool export_actions, cudaStream_t st);
+cudaError_t launch_frag_relayout(const Params& net, int capacity, float* wF, cudaStream_t st);
 cudaError_t launch_pass2(const Pass2Args& a, cudaStream_t st);
 cudaError_t debug_phase_cycles(unsigned long long* out, bool reset);
 cudaError_t debug_hidden_cycles(unsigned long long* out, bool reset);

@@ -295,7 +295,6 @@ constexpr int kThreadsP = 640;  // >= units of a tile for pools <= 64 slots: one
 #define EVO_UNIT_CELLS 2
 #endif
 constexpr int kUnitP = EVO_UNIT_CELLS;  // cells per thread in the controller (same genome)
-constexpr int kPreHalo = (kHaloCells + kThreadsP - 1) / kThreadsP;
 constexpr int kPreCells = (kTileCells + kThreadsP - 1) / kThreadsP;
 
 struct DirectSmem {
@@ -313,13 +312,19 @@ struct DirectSmem {
   int bins[1];  // capacity ints (dynamic tail)
 };
 
-struct Prefetch {
-  float v[kPreHalo][5];
-  int gi[kPreCells];
-  int rot[kPreCells];
+template <int THREADS>
+struct PrefetchT {
+  static constexpr int kHalo = (kHaloCells + THREADS - 1) / THREADS;
+  static constexpr int kCells = (kTileCells + THREADS - 1) / THREADS;
+  float v[kHalo][5];
+  int gi[kCells];
+  int rot[kCells];
 };
+using Prefetch = PrefetchT<kThreadsP>;
 
-__device__ __forceinline__ void prefetch_tile(const Pass1Args& a, int tile, int tiles_x, Prefetch& pf) {
+template <int THREADS>
+__device__ __forceinline__ void prefetch_tile(const Pass1Args& a, int tile, int tiles_x, PrefetchT<THREADS>& pf) {
+  constexpr int kPreHalo = PrefetchT<THREADS>::kHalo, kPreCells = PrefetchT<THREADS>::kCells;
   const StepGeom& g = a.g;
   const int tid = threadIdx.x;
   const int x0 = (tile % tiles_x) * kTileW;
@@ -327,7 +332,7 @@ __device__ __forceinline__ void prefetch_tile(const Pass1Args& a, int tile, int 
   const unsigned st = (unsigned)g.stride;
 #pragma unroll
   for (int j = 0; j < kPreHalo; ++j) {
-    const int i = tid + j * kThreadsP;
+    const int i = tid + j * THREADS;
     if (i < kHaloCells) {
       const unsigned o = halo_src(g, x0, y0, i);
       pf.v[j][0] = ld_na(a.front.E + o);
@@ -339,7 +344,7 @@ __device__ __forceinline__ void prefetch_tile(const Pass1Args& a, int tile, int 
   }
 #pragma unroll
   for (int j = 0; j < kPreCells; ++j) {
-    const int i = tid + j * kThreadsP;
+    const int i = tid + j * THREADS;
     const int ty = i / kTileW, tx = i - ty * kTileW;
     const int y = y0 + ty, x = x0 + tx;
     const bool in = (i < kTileCells) && (y < g.H) && (x < g.W);
@@ -349,11 +354,13 @@ __device__ __forceinline__ void prefetch_tile(const Pass1Args& a, int tile, int 
   }
 }
 
-__device__ __forceinline__ void commit_tile(DirectSmem& sm, const Prefetch& pf) {
+template <int THREADS, typename SM>
+__device__ __forceinline__ void commit_tile(SM& sm, const PrefetchT<THREADS>& pf) {
+  constexpr int kPreHalo = PrefetchT<THREADS>::kHalo, kPreCells = PrefetchT<THREADS>::kCells;
   const int tid = threadIdx.x;
 #pragma unroll
   for (int j = 0; j < kPreHalo; ++j) {
-    const int i = tid + j * kThreadsP;
+    const int i = tid + j * THREADS;
     if (i < kHaloCells) {
       sm.eic[i] = make_float4(pf.v[j][0], pf.v[j][1], pf.v[j][2], pf.v[j][3]);
       sm.c2[i] = pf.v[j][4];
@@ -361,7 +368,7 @@ __device__ __forceinline__ void commit_tile(DirectSmem& sm, const Prefetch& pf) 
   }
 #pragma unroll
   for (int j = 0; j < kPreCells; ++j) {
-    const int i = tid + j * kThreadsP;
+    const int i = tid + j * THREADS;
     if (i < kTileCells) {
       sm.gi[i] = pf.gi[j];
       sm.rot[i] = (uint8_t)pf.rot[j];
@@ -371,13 +378,14 @@ __device__ __forceinline__ void commit_tile(DirectSmem& sm, const Prefetch& pf) 
 
 // L2 prefetch of a tile's halo rows (5 planes) and interior genome/rotation
 // rows: no registers, issued a whole tile ahead of the register loads.
+template <int THREADS = kThreadsP>
 __device__ __forceinline__ void prefetch_tile_l2(const Pass1Args& a, int tile, int tiles_x) {
   const StepGeom& g = a.g;
   const int x0 = (tile % tiles_x) * kTileW;
   const int y0 = (tile / tiles_x) * kTileH;
   // per plane row: [x0-1, x0+33) -> at most 2 x 128-byte lines (floats)
   constexpr int kLines = kHaloH * 2;  // per float plane
-  for (int i = threadIdx.x; i < kLines * 5 + kTileH * 2; i += kThreadsP) {
+  for (int i = threadIdx.x; i < kLines * 5 + kTileH * 2; i += THREADS) {
     const char* p;
     if (i < kLines * 5) {
       const int plane = i / kLines, r = (i - plane * kLines) >> 1, half = i & 1;
@@ -399,9 +407,10 @@ __device__ __forceinline__ void prefetch_tile_l2(const Pass1Args& a, int tile, i
 }
 
 // Asynchronous copy of the slot weight tables into shared memory (16-byte cp.async).
+template <int THREADS = kThreadsP>
 __device__ __forceinline__ void stage_weights(float* dst, const float* src, int nfloats) {
   const unsigned sbase = (unsigned)__cvta_generic_to_shared(dst);
-  for (int i = threadIdx.x * 4; i < nfloats; i += kThreadsP * 4)
+  for (int i = threadIdx.x * 4; i < nfloats; i += THREADS * 4)
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sbase + i * 4), "l"(src + i));
 }
 
@@ -484,6 +493,304 @@ __global__ void __launch_bounds__(kThreadsP, 1) k_pass1_direct(const Pass1Args a
 constexpr int kSmemWeightSlots = kSmemWeightSlotsAbi;
 constexpr size_t weight_smem_bytes(int capacity) {
   return ((size_t)capacity * (kSensors * 12 + kOutPad) + (((size_t)capacity * kSensors + 3) & ~(size_t)3)) * sizeof(float);
+}
+
+// ---------------------------------------------------------------------------
+// Pass 1, direct net as mma.sync m16n8k8 TF32 (EVO_F_MMA_NET; a measured
+// alternative, not the default: on config 2 it runs the step in 157 us against
+// the FFMA2 kernel's 115 us - 81M warp instructions per launch against 43M,
+// because per 8-cell block every lane splits its 12 sensor values, computes 12
+// rotated addresses and squashes 2-4 outputs, ~3x the sigmoid evaluations of
+// the pruned per-cell epilogue)
+//
+// The 45->13 contraction of an 8-cell block of one genome is D[16 x 8] =
+// W[16 outputs x 48] . S[48 x 8 cells]: outputs on M (13 of 16 rows used),
+// cells on N, so genome groups are padded to 8 cells (not 16).  fp32
+// accuracy from the 3xTF32 split x = hi + lo: hi.hi into one accumulator
+// (bias-initialised), hi.lo + lo.hi into a second, summed in FP32 (the TF32
+// MMA accumulates with worse than FP32 rounding, tools/microbench/tc_split.cu).
+// The K order is permuted so that lane (r = lane/4, q = lane%4) loads
+// channel q of the 9 Moore slots straight from the interleaved halo tile
+// (one 16-byte {E, I, C0, C1} chunk per cell and slot is read by the cell's
+// four lanes) plus three C2 values:
+//   K-steps 0-3: rows 8j+q -> slot 2j channel q, 8j+4+q -> slot 2j+1 channel q
+//   K-step 4:    32+q -> slot 8 channel q,      36+q -> slot q channel C2
+//   K-step 5:    40+q -> slot 4+q channel C2,   44+q -> slot 8 C2 (q = 0), pad
+// Weights live in shared memory in A-fragment order (k_frag_relayout), loaded
+// into registers (split hi/lo) when a warp's block changes genome; warps walk
+// contiguous ranges of blocks.  Epilogue: each lane squashes its outputs (the
+// reference sigmoid sequence), the explore argmax (first-max over squashed
+// values) is a 3-step shuffle reduction over the 8 lanes of a cell pair.
+
+constexpr int kThreadsM = 512;
+constexpr int kWarpsM = kThreadsM / 32;
+constexpr int kOrderM = (kTileCells + kMmaSlots * 7 + 7) & ~7;
+
+struct MmaSmem {
+  float4 eic[kHaloCells];
+  float c2[kHaloCells];
+  int gi[kTileCells];
+  uint8_t rot[kTileCells];
+  unsigned short order[kOrderM];
+  int scratch[kThreadsM / 32];
+  int n_units;
+  union {
+    ActSmem act;
+  } u;
+  int bins[kMmaSlots];
+};
+
+// logical K row -> physical sensor index slot*5 + channel (-1: padding)
+__host__ __device__ constexpr int mma_k_phys(int kk) {
+  const int j = kk >> 3, h = (kk >> 2) & 1, q = kk & 3;
+  return j < 4 ? (2 * j + h) * 5 + q
+               : (j == 4 ? (h == 0 ? 40 + q : q * 5 + 4) : (h == 0 ? (4 + q) * 5 + 4 : (q == 0 ? 44 : -1)));
+}
+
+// Compact direct weights (W12 [cap][45][12], W1 [cap][45], bias [cap][16])
+// -> fragment-order table [cap][kFragGenome].
+__global__ void k_frag_relayout(const Params net, int capacity, float* wF) {
+  const int n = capacity * kFragGenome;
+  for (int d = blockIdx.x * blockDim.x + threadIdx.x; d < n; d += gridDim.x * blockDim.x) {
+    const int g = d / kFragGenome, e = d - g * kFragGenome;
+    float v = 0.0f;
+    if (e >= 6 * kFragStep) {
+      v = net.bA[(size_t)g * kOutPad + (e - 6 * kFragStep)];
+    } else {
+      const int j = e / kFragStep, r2 = e - j * kFragStep;
+      int lane, comp;
+      if (r2 < 80) {
+        lane = r2 >> 2;
+        comp = r2 & 3;
+      } else {
+        lane = 20 + ((r2 - 80) >> 1);
+        comp = ((r2 - 80) & 1) * 2;  // a0, a2
+      }
+      const int o = (lane >> 2) + ((comp & 1) ? 8 : 0);
+      const int kk = 8 * j + (lane & 3) + ((comp & 2) ? 4 : 0);
+      const int ph = mma_k_phys(kk);
+      if (ph >= 0 && o < kActuators)
+        v = o < 12 ? net.wA[((size_t)g * kSensors + ph) * 12 + o] : net.wB[(size_t)g * kSensors + ph];
+    }
+    wF[d] = v;
+  }
+}
+
+// x = hi + lo with hi exactly TF32 (11 significant bits, rounded to nearest)
+// by Veltkamp splitting on the FMA pipe (cvt.rna.tf32 runs on the slow XU
+// pipe, which bound the first version of this kernel): t = x * (2^13 + 1),
+// hi = t - (t - x), lo = x - hi exact (<= 12 significant bits; the MMA reads
+// its top 11, an error <= 2^-22 |x|).
+__device__ __forceinline__ void split_tf32(float x, unsigned& hi, unsigned& lo) {
+  const float t = __fmul_rn(x, 8193.0f);
+  const float h = __fsub_rn(t, __fsub_rn(t, x));
+  hi = __float_as_uint(h);
+  lo = __float_as_uint(__fsub_rn(x, h));
+}
+__device__ __forceinline__ void mma_tf32(float (&d)[4], const unsigned (&a)[4], unsigned b0, unsigned b1) {
+  asm("mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ float lds_f32(unsigned addr) {
+  float r;
+  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(r) : "r"(addr));
+  return r;
+}
+
+// halo-tile offset (biased by +64) of Moore slot s for rotation rot, from the
+// byte-rotated direction pack
+__device__ __forceinline__ unsigned long long rotated_offsets(int rot) {
+  const unsigned long long p = kHaloOffPack;
+  const int sh = 8 * rot;
+  return sh ? (p >> sh) | (p << (64 - sh)) : p;
+}
+
+template <bool kExport>
+__device__ __forceinline__ void tile_controller_mma(const Pass1Args& a, MmaSmem& sm, const float* sF, int x0,
+                                                    int y0) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int r = lane >> 2, q = lane & 3;
+  const int nblk = sm.n_units;
+  const int b_begin = warp * nblk / kWarpsM, b_end = (warp + 1) * nblk / kWarpsM;
+  // lane constants: rotation deltas of C2 slots q and 4+q (slot 0 has none)
+  const int dq1 = (int)((kDeltaPack >> (4 * ((q + 7) & 7))) & 7u);  // slot q (q >= 1): delta index q-1
+  const int dq2 = (int)((kDeltaPack >> (4 * (q + 3))) & 7u);        // slot 4+q: delta index 3+q
+  const unsigned eic_base = (unsigned)__cvta_generic_to_shared(sm.eic) + 4u * q;
+  const unsigned c2_base = (unsigned)__cvta_generic_to_shared(sm.c2);
+  const bool lo_lane = lane < 20;  // rows r and r+8 (r+8 <= 12); lanes 20-31 hold rows 5-7 only
+  const float* fr_base = sF + (lo_lane ? lane * 4 : 80 + (lane - 20) * 2);
+  unsigned ah[6][4], al[6][4];
+  float bias0 = 0.0f, bias1 = 0.0f;
+  int cur = -1;
+  float* actf = reinterpret_cast<float*>(&sm.u.act);
+  for (int b = b_begin; b < b_end; ++b) {
+    const unsigned short* ob = sm.order + b * 8;
+    const int p0 = ob[0];
+    const int slot = sm.gi[p0];
+    if (slot != cur) {  // warp-uniform: reload this genome's fragments
+      cur = slot;
+      const float* fg = fr_base + (size_t)slot * kFragGenome;
+#pragma unroll
+      for (int j = 0; j < 6; ++j) {
+        float w[4];
+        if (lo_lane) {
+          const float4 v = *reinterpret_cast<const float4*>(fg + j * kFragStep);
+          w[0] = v.x, w[1] = v.y, w[2] = v.z, w[3] = v.w;
+        } else {
+          const float2 v = *reinterpret_cast<const float2*>(fg + j * kFragStep);
+          w[0] = v.x, w[1] = 0.0f, w[2] = v.y, w[3] = 0.0f;
+        }
+#pragma unroll
+        for (int c = 0; c < 4; ++c) split_tf32(w[c], ah[j][c], al[j][c]);
+      }
+      const float* bg = sF + (size_t)slot * kFragGenome + 6 * kFragStep;
+      bias0 = bg[r];
+      bias1 = bg[r + 8];
+    }
+    // sensors of cell r (padding entries read cell p0; their results are dropped)
+    const int pr = ob[r];
+    const int pc = pr == 0xFFFF ? p0 : pr;
+    const int ty = pc >> 5, tx = pc & 31;
+    const int hb = (ty + 1) * kHaloW + tx + 1 - 64;
+    const unsigned long long rp = rotated_offsets(sm.rot[pc]);
+    int nbr[9];
+    nbr[0] = hb + 64;
+#pragma unroll
+    for (int s = 1; s < 9; ++s) nbr[s] = hb + (int)((rp >> (8 * ((kDeltaPack >> (4 * (s - 1))) & 7u))) & 0xFFu);
+    float v[12];
+#pragma unroll
+    for (int s = 0; s < 9; ++s) v[s] = lds_f32(eic_base + 16u * (unsigned)nbr[s]);
+    const int nq1 = q == 0 ? hb + 64 : hb + (int)((rp >> (8 * dq1)) & 0xFFu);
+    const int nq2 = hb + (int)((rp >> (8 * dq2)) & 0xFFu);
+    v[9] = lds_f32(c2_base + 4u * (unsigned)nq1);
+    v[10] = lds_f32(c2_base + 4u * (unsigned)nq2);
+    v[11] = q == 0 ? lds_f32(c2_base + 4u * (unsigned)nbr[8]) : 0.0f;
+    float dh[4] = {bias0, bias0, bias1, bias1};
+    float dc[4] = {0.0f, 0.0f, 0.0f, 0.0f}, dd[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+#pragma unroll
+    for (int j = 0; j < 6; ++j) {
+      unsigned bh0, bl0, bh1, bl1;
+      split_tf32(v[2 * j], bh0, bl0);
+      split_tf32(v[2 * j + 1], bh1, bl1);
+      mma_tf32(dh, ah[j], bh0, bh1);
+      mma_tf32(dc, ah[j], bl0, bl1);
+      mma_tf32(dd, al[j], bh0, bh1);
+    }
+    float z[4];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) z[c] = __fadd_rn(dh[c], __fadd_rn(dc[c], dd[c]));
+    // z[0], z[1]: output r of cells 2q, 2q+1; z[2], z[3]: output r+8
+    const unsigned pair = *reinterpret_cast<const unsigned*>(ob + 2 * q);
+    const int pa = (int)(pair & 0xFFFFu), pb = (int)(pair >> 16);
+    const bool act_lane = r < 5;
+    float sa = squash(act_lane ? z[2] : z[0]);
+    float sb = squash(act_lane ? z[3] : z[1]);
+    int ea = act_lane ? r + 3 : r - 5;
+    int eb = ea;
+    float ua = 0.0f, ub = 0.0f;
+    if (act_lane) {
+      ua = squash(z[0]);
+      ub = squash(z[1]);
+    }
+    if (kExport) {  // all 13 squashed actuators of the exported cells
+      const int oa = act_lane ? r : -1;  // action output held in ua/ub
+      const int ox = ea + 5;             // explore output held in sa/sb
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        const int p = c ? pb : pa;
+        if (p == 0xFFFF) continue;
+        const int ty2 = p >> 5, tx2 = p - (ty2 << 5);
+        const long long cell = (long long)(y0 + ty2) * a.g.W + (x0 + tx2);
+        float* dst = a.act_out + cell * kActuators;
+        if (oa >= 0) dst[oa] = c ? ub : ua;
+        dst[ox] = c ? sb : sa;
+        if (r == 0) a.act_out_flag[cell] = 1;
+      }
+    }
+#pragma unroll
+    for (int m = 4; m <= 16; m <<= 1) {
+      const float oa = __shfl_xor_sync(0xFFFFFFFFu, sa, m), ob2 = __shfl_xor_sync(0xFFFFFFFFu, sb, m);
+      const int xa = __shfl_xor_sync(0xFFFFFFFFu, ea, m), xb = __shfl_xor_sync(0xFFFFFFFFu, eb, m);
+      if (oa > sa || (oa == sa && xa < ea)) sa = oa, ea = xa;
+      if (ob2 > sb || (ob2 == sb && xb < eb)) sb = ob2, eb = xb;
+    }
+    if (pa != 0xFFFF) {
+      if (act_lane) actf[r * kTileCells + pa] = ua;
+      if (r == 5) {
+        actf[5 * kTileCells + pa] = sa;
+        sm.u.act.kstar[pa] = (uint8_t)ea;
+      }
+    }
+    if (pb != 0xFFFF) {
+      if (act_lane) actf[r * kTileCells + pb] = ub;
+      if (r == 6) {
+        actf[5 * kTileCells + pb] = sb;
+        sm.u.act.kstar[pb] = (uint8_t)eb;
+      }
+    }
+  }
+}
+
+template <bool kExport>
+__global__ void __launch_bounds__(kThreadsM, 1) k_pass1_mma(const Pass1Args a) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  MmaSmem& sm = *reinterpret_cast<MmaSmem*>(smem_raw);
+  const StepGeom& g = a.g;
+  const int tiles_x = (g.W + kTileW - 1) / kTileW;
+  const int ntiles = tiles_x * ((g.H + kTileH - 1) / kTileH);
+  zero_stats(a);
+  int tile = blockIdx.x;
+  if (tile >= ntiles) return;
+  float* sF = reinterpret_cast<float*>(smem_raw + ((sizeof(MmaSmem) + 15) & ~(size_t)15));
+  stage_weights<kThreadsM>(sF, a.net.wF, a.capacity * kFragGenome);
+  asm volatile("cp.async.commit_group;" ::: "memory");
+  using PF = PrefetchT<kThreadsM>;
+  constexpr int kPreCellsM = PF::kCells;
+  int rank[kPreCellsM];
+  {
+    PF pf;
+    prefetch_tile(a, tile, tiles_x, pf);
+    commit_tile(sm, pf);
+    for (int b = threadIdx.x; b < a.capacity; b += kThreadsM) sm.bins[b] = 0;
+    __syncthreads();
+    bucket_count<kThreadsM, kPreCellsM>(sm.bins, pf.gi, rank);
+    __syncthreads();
+    bucket_offsets<kThreadsM, 8, 8>(sm.bins, sm.scratch, sm.order, &sm.n_units, a.capacity);
+    __syncthreads();
+    bucket_scatter<kThreadsM, kPreCellsM>(sm.bins, pf.gi, rank, sm.order);
+  }
+  asm volatile("cp.async.wait_all;" ::: "memory");
+  __syncthreads();
+  long long t_mark = clock64();
+  (void)t_mark;
+  PHASE_MARK(4);
+  for (; tile < ntiles; tile += gridDim.x) {
+    const int x0 = (tile % tiles_x) * kTileW;
+    const int y0 = (tile / tiles_x) * kTileH;
+    const int next = tile + gridDim.x;
+    if (next < ntiles) prefetch_tile_l2<kThreadsM>(a, next, tiles_x);
+    for (int b = threadIdx.x; b < a.capacity; b += kThreadsM) sm.bins[b] = 0;  // for the next count
+    PHASE_MARK(0);
+    tile_controller_mma<kExport>(a, sm, sF, x0, y0);
+    __syncthreads();
+    PHASE_MARK(1);
+    PF pf;
+    if (next < ntiles) prefetch_tile(a, next, tiles_x, pf);
+    tile_physics<false, kExport, kThreadsM>(a, sm, x0, y0);
+    if (next < ntiles) bucket_count<kThreadsM, kPreCellsM>(sm.bins, pf.gi, rank);
+    __syncthreads();
+    PHASE_MARK(2);
+    if (next < ntiles) {
+      bucket_offsets<kThreadsM, 8, 8>(sm.bins, sm.scratch, sm.order, &sm.n_units, a.capacity);
+      __syncthreads();
+      bucket_scatter<kThreadsM, kPreCellsM>(sm.bins, pf.gi, rank, sm.order);
+      commit_tile(sm, pf);
+    }
+    __syncthreads();
+    PHASE_MARK(3);
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -1052,6 +1359,24 @@ static cudaError_t launch_direct(const Pass1Args& a, cudaStream_t st) {
   return cudaGetLastError();
 }
 
+template <bool E>
+static cudaError_t launch_mma(const Pass1Args& a, cudaStream_t st) {
+  const size_t smem = ((sizeof(MmaSmem) + 15) & ~(size_t)15) + (size_t)a.capacity * kFragGenome * sizeof(float);
+  static int configured = 0;
+  cudaError_t e = set_smem(k_pass1_mma<E>, smem, configured);
+  if (e != cudaSuccess) return e;
+  const int tiles = ((a.g.W + kTileW - 1) / kTileW) * ((a.g.H + kTileH - 1) / kTileH);
+  const int grid = tiles < num_sms() ? tiles : num_sms();
+  k_pass1_mma<E><<<grid, kThreadsM, smem, st>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_frag_relayout(const Params& net, int capacity, float* wF, cudaStream_t st) {
+  const int n = capacity * kFragGenome;
+  k_frag_relayout<<<(n + 255) / 256, 256, 0, st>>>(net, capacity, wF);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_pass1(const Pass1Args& a, bool inject, bool export_actions, cudaStream_t st) {
   if (inject && a.act_rank) {
     const long long n = (long long)a.g.W * a.g.H;
@@ -1062,6 +1387,8 @@ cudaError_t launch_pass1(const Pass1Args& a, bool inject, bool export_actions, c
   if (inject) return launch_generic<true, false, false>(a, st);
   if (a.net.hidden > 0)
     return export_actions ? launch_generic<false, true, true>(a, st) : launch_generic<false, false, true>(a, st);
+  if (a.net.wF && a.capacity <= kMmaSlots)
+    return export_actions ? launch_mma<true>(a, st) : launch_mma<false>(a, st);
   if (a.capacity <= kSmemWeightSlots)
     return export_actions ? launch_direct<true, true>(a, st) : launch_direct<false, true>(a, st);
   return export_actions ? launch_direct<true, false>(a, st) : launch_direct<false, false>(a, st);

@@ -518,3 +518,60 @@ def test_genome_sorted_direct_path_matches_tile_path(genomes, shape):
     for d in (a, b, c):
         d.close()
     _step_vs_oracle(p0, net, phys, steps=2)
+
+
+# -- direct net on the tensor cores (k_pass1_mma, mma.sync 3xTF32) ---------------------------
+
+
+@pytest.mark.parametrize("genomes,shape,hole", [(64, (96, 80), False), (8, (64, 64), False), (1, (40, 33), False),
+                                                 (64, (1, 300), False), (13, (70, 35), True), (64, (128, 128), True)])
+def test_mma_direct_net_vs_oracle_and_ffma(genomes, shape, hole):
+    """EVO_F_MMA_NET runs the direct 45->13 net of pools <= 64 slots as
+    mma.sync m16n8k8 TF32 (3xTF32 split, 8-cell genome blocks; a measured
+    alternative to the default FFMA2 tile kernel): device actions vs the
+    oracle within 1e-5 relative, explore argmax and physics tier A given them,
+    the export and decided variants bit-identical, the default path within
+    the same tolerance.  Shapes: full pools, a single genome, a 1-row torus,
+    partial tiles, unoccupied slots."""
+    h, w = shape
+    p0 = orc.synth_planes(h, w, genomes, seed=genomes * 7 + h)
+    if hole:  # a live slot without cells
+        p0.gi[p0.gi == 3] = 4
+    live = None
+    net = orc.synth_net(genomes, 0, seed=genomes + 1)
+    phys = orc.Phys(cycle_period=20)
+    params = oracle_phys_to_params(phys)
+    oa = orc.act(p0, net)
+    dev = make_dev(p0, genomes, net, live=live)
+    cells, acts = _actions(dev, 0, params, _lib.F_MMA_NET)
+    assert np.array_equal(cells, oa.cells)
+    assert rel_err(acts, oa.a) <= TOL
+    ref = orc.step(p0, 0, net, phys, acts=orc.Actions(cells, acts))
+    got = download(dev)
+    assert got.equal(ref.planes)
+    dev.close()
+    dev = make_dev(p0, genomes, net, live=live)  # decided (non-export) variant
+    dev.step_raw(physics.step_scalars(0, params), 0, flags=_lib.F_MMA_NET)
+    assert download(dev).equal(got)
+    dev.close()
+    dev = make_dev(p0, genomes, net, live=live)
+    cells2, acts2 = _actions(dev, 0, params)
+    assert np.array_equal(cells2, cells) and rel_err(acts2, oa.a) <= TOL
+    dev.close()
+
+
+def test_mma_direct_net_follows_parameter_updates():
+    """The fragment-order weight copy is rebuilt after evo_set_params: a step
+    after replacing the nets uses the new weights."""
+    p0 = orc.synth_planes(48, 48, 16, seed=21)
+    net_a = orc.synth_net(16, 0, seed=1)
+    net_b = orc.synth_net(16, 0, seed=2)
+    params = oracle_phys_to_params(orc.Phys(cycle_period=20))
+    dev = make_dev(p0, 16, net_a)
+    _actions(dev, 0, params, _lib.F_MMA_NET)
+    dev.set_params(net_params(net_b))
+    dev.upload(p0)
+    cells, acts = _actions(dev, 0, params, _lib.F_MMA_NET)
+    oa = orc.act(p0, net_b)
+    assert np.array_equal(cells, oa.cells) and rel_err(acts, oa.a) <= TOL
+    dev.close()
