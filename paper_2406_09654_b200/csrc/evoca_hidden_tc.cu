@@ -187,7 +187,7 @@ struct SenseSmem {
 
 size_t sense_smem_bytes(int cap) { return sizeof(SenseSmem) + (size_t)((cap + 3) & ~3) * 4; }
 
-__global__ void __launch_bounds__(kSortThreads) k_hid_sense(const StepGeom g, const Planes f, const int32_t* offs,
+__global__ void __launch_bounds__(kSortThreads, 2) k_hid_sense(const StepGeom g, const Planes f, const int32_t* offs,
                                                             const int32_t* cta_base, int cap, float* sens,
                                                             int32_t* rank_of_cell) {
   extern __shared__ __align__(16) unsigned char sraw[];
@@ -200,31 +200,61 @@ __global__ void __launch_bounds__(kSortThreads) k_hid_sense(const StepGeom g, co
   const int st = (int)g.stride;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   float* stage = sm.stage[warp];
-  for (int t = t0; t < t1; ++t) {
+  // the next tile's halo planes, genome and rotation are loaded into
+  // registers while the current tile's rows are assembled and stored
+  constexpr int kPH = (kSH * kSH + kSortThreads - 1) / kSortThreads;
+  constexpr int kPC = (kST * kST) / kSortThreads;
+  float pv[kPH][5];
+  int pg[kPC], pr[kPC];
+  auto load_tile = [&](int t) {
     const int x0 = (t % tiles_x) * kST, y0 = (t / tiles_x) * kST;
-    __syncthreads();  // previous tile's readers are done (and cursor init on the first pass)
-    for (int i = threadIdx.x; i < kSH * kSH; i += blockDim.x) {
-      const int hy = i / kSH, hx = i - hy * kSH;
-      int y = y0 + hy - 1;
-      y = y > g.H ? g.H : y;  // beyond a partial tile: never read
-      int x = x0 + hx - 1;
-      x = x < 0 ? x + g.W : (x >= g.W ? x - g.W : x);
-      x = x >= g.W ? g.W - 1 : x;
-      const int o = (y + 1) * g.W + x;
-      sm.pl[0][i] = __ldg(f.E + o);
-      sm.pl[1][i] = __ldg(f.I + o);
-      sm.pl[2][i] = __ldg(f.C + o);
-      sm.pl[3][i] = __ldg(f.C + st + o);
-      sm.pl[4][i] = __ldg(f.C + 2 * st + o);
+#pragma unroll
+    for (int j = 0; j < kPH; ++j) {
+      const int i = threadIdx.x + j * kSortThreads;
+      if (i < kSH * kSH) {
+        const int hy = i / kSH, hx = i - hy * kSH;
+        int y = y0 + hy - 1;
+        y = y > g.H ? g.H : y;  // beyond a partial tile: never read
+        int x = x0 + hx - 1;
+        x = x < 0 ? x + g.W : (x >= g.W ? x - g.W : x);
+        x = x >= g.W ? g.W - 1 : x;
+        const int o = (y + 1) * g.W + x;
+        pv[j][0] = __ldg(f.E + o);
+        pv[j][1] = __ldg(f.I + o);
+        pv[j][2] = __ldg(f.C + o);
+        pv[j][3] = __ldg(f.C + st + o);
+        pv[j][4] = __ldg(f.C + 2 * st + o);
+      }
     }
-    for (int i = threadIdx.x; i < kST * kST; i += blockDim.x) {
+#pragma unroll
+    for (int j = 0; j < kPC; ++j) {
+      const int i = threadIdx.x + j * kSortThreads;
       const int y = y0 + i / kST, x = x0 + i % kST;
       const bool in = y < g.H && x < g.W;
       const int o = (y + 1) * g.W + x;
-      sm.gi[i] = in ? __ldg(f.gi + o) : -1;
-      sm.rot[i] = in ? __ldg(f.rot + o) : 0;
+      pg[j] = in ? __ldg(f.gi + o) : -1;
+      pr[j] = in ? (int)__ldg(f.rot + o) : 0;
+    }
+  };
+  if (t0 < t1) load_tile(t0);
+  for (int t = t0; t < t1; ++t) {
+    const int x0 = (t % tiles_x) * kST, y0 = (t / tiles_x) * kST;
+    __syncthreads();  // previous tile's readers are done (and cursor init on the first pass)
+#pragma unroll
+    for (int j = 0; j < kPH; ++j) {
+      const int i = threadIdx.x + j * kSortThreads;
+      if (i < kSH * kSH)
+#pragma unroll
+        for (int ch = 0; ch < 5; ++ch) sm.pl[ch][i] = pv[j][ch];
+    }
+#pragma unroll
+    for (int j = 0; j < kPC; ++j) {
+      const int i = threadIdx.x + j * kSortThreads;
+      sm.gi[i] = pg[j];
+      sm.rot[i] = (uint8_t)pr[j];
     }
     __syncthreads();
+    if (t + 1 < t1) load_tile(t + 1);
     for (int cb = warp * 32; cb < kST * kST; cb += blockDim.x) {
       const int i = cb + lane, ty = i / kST, tx = i - ty * kST;
       const int y = y0 + ty, x = x0 + tx;
@@ -283,14 +313,20 @@ __device__ __forceinline__ float tanh_sfu(float x) {
 }
 
 // per 128-row tile: {slot, first row, rows, 0} - one 16-byte load per tile
-__global__ void k_hid_tilemap(const int32_t* offs, const int32_t* tiles, int cap, int4* tile_info) {
-  const int g = blockIdx.x * blockDim.x + threadIdx.x;
-  if (g >= cap) return;
-  const int o0 = offs[g], o1 = offs[g + 1];
-  for (int t = tiles[g]; t < tiles[g + 1]; ++t) {
-    const int row0 = o0 + (t - tiles[g]) * kRows;
-    tile_info[t] = make_int4(g, row0, min(kRows, o1 - row0), 0);
+// tile -> {slot, first row, rows}: one thread per tile, slot found by binary
+// search over the per-slot tile offsets (a per-slot loop serialised ~500
+// tiles per thread on config 3)
+__global__ void k_hid_tilemap(const int32_t* offs, const int32_t* tiles, int cap, const int32_t* n_tiles,
+                              int4* tile_info) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= *n_tiles) return;
+  int lo = 0, hi = cap;  // largest g with tiles[g] <= t (tiles[cap] = n_tiles > t)
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (__ldg(tiles + mid) <= t) lo = mid; else hi = mid;
   }
+  const int row0 = __ldg(offs + lo) + (t - __ldg(tiles + lo)) * kRows;
+  tile_info[t] = make_int4(lo, row0, min(kRows, __ldg(offs + lo + 1) - row0), 0);
 }
 
 struct NetArgs {
@@ -578,78 +614,74 @@ __global__ void __launch_bounds__(kNetThreads, 1) k_hid_net(const NetArgs a) {
 
 // Direct 45->13 controller over genome-sorted sensor rows (many-genome
 // pools, e.g. BASELINE configs 3-4 with 256-1024 genomes, where a 32x32 tile
-// holds ~1-4 cells per genome and per-tile weight fetches dominate).  A CTA
-// of 128 threads takes contiguous 128-row tiles (one genome each): the
-// genome's 2.4 KB of weights are staged in shared memory once per run of
-// tiles and every weight load is a warp-uniform broadcast; each thread loads
-// its whole 192-byte row up front (12 independent 16-byte loads in flight)
-// and runs the same packed FFMA2 chains, pairing and k order as the tile
-// kernel (net_direct_unit), so results are bit-identical to it.
-constexpr int kDrThreads = 64;   // two rows per thread: every weight broadcast feeds two FMA chains
-constexpr int kDrPitch = 52;  // floats per staged row: 16-byte aligned, conflict-free LDS.128 per lane
+// holds ~1-4 cells per genome and per-tile weight fetches dominate).  Each
+// WARP takes contiguous 64-row half-tiles (one genome each): the genome's
+// 2.4 KB of weights are staged in a warp-private shared buffer once per run
+// of half-tiles (every weight load a warp-uniform broadcast); each lane
+// streams its two 192-byte rows straight from global memory into registers,
+// kDrDepth 16-byte chunks per row in flight (no shared-memory staging, so
+// 16 warps fit per SM instead of the 8 that double-buffered 53 KB row tiles
+// allowed), and runs the same packed FFMA2 chains, pairing and k order as the
+// tile kernel (net_direct_unit), so results are bit-identical to it.
+constexpr int kDrWarps = 4;
+constexpr int kDrThreads = kDrWarps * 32;
+constexpr int kDrDepth = 6;     // 16-byte chunks per row in flight
+constexpr int kDrW = kSensors * 12 + 48 + kOutPad;  // W12 [45][12] | W1 [48] | bias [16]
 
-__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(tc::smem_u32(smem_dst)), "l"(gsrc) : "memory");
+__device__ __forceinline__ float4 ld_row16(const float4* p) {
+  float4 r;
+  asm volatile("ld.global.nc.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w) : "l"(p));
+  return r;
 }
 
-__global__ void __launch_bounds__(kDrThreads) k_direct_rows(const NetArgs a) {
-  extern __shared__ __align__(16) float dsm[];
-  float* W12 = dsm;                        // [45][12]
-  float* W1 = W12 + kSensors * 12;         // [48]
-  float* Bs = W1 + 48;                     // [16]
-  float* rows = Bs + kOutPad;              // 2 x [128][kDrPitch]
-  const int T = *a.n_tiles;
-  const int per = (T + gridDim.x - 1) / gridDim.x;
-  const int t0 = blockIdx.x * per, t1 = min(T, t0 + per);
-  if (t0 >= t1) return;
-  // rows of tile t into buffer b: 128 x 12 sixteen-byte copies, 12 per thread
-  auto stage = [&](int t, int b) {
-    const int4 ti = __ldg(a.tile_info + t);
-    float* dst = rows + b * kRows * kDrPitch;
-    for (int i = threadIdx.x; i < kRows * 12; i += kDrThreads) {
-      const int r = i / 12, part = i - r * 12;
-      if (r < ti.z) cp_async16(dst + r * kDrPitch + part * 4, a.sens + (size_t)(ti.y + r) * kK1 + part * 4);
-    }
-    asm volatile("cp.async.commit_group;" ::: "memory");
-  };
-  stage(t0, 0);
+__global__ void __launch_bounds__(kDrThreads, 4) k_direct_rows(const NetArgs a) {
+  __shared__ __align__(16) float wsm[kDrWarps][kDrW];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  float* W12 = wsm[warp];
+  float* W1 = W12 + kSensors * 12;
+  float* Bs = W1 + 48;
+  const int H = 2 * *a.n_tiles;  // 64-row half-tiles
+  const int nw = gridDim.x * kDrWarps, gw = blockIdx.x * kDrWarps + warp;
+  const int per = (H + nw - 1) / nw;
+  const int h0 = gw * per, h1 = min(H, h0 + per);
   int cur = -1;
-  for (int t = t0; t < t1; ++t) {
-    const int b = (t - t0) & 1;
-    const int4 ti = __ldg(a.tile_info + t);
-    if (t + 1 < t1) {
-      stage(t + 1, b ^ 1);
-      asm volatile("cp.async.wait_group 1;" ::: "memory");
-    } else {
-      asm volatile("cp.async.wait_group 0;" ::: "memory");
-    }
+  for (int h = h0; h < h1; ++h) {
+    const int4 ti = __ldg(a.tile_info + (h >> 1));
+    const int rb = (h & 1) * 64;
+    if (rb >= ti.z) continue;  // warp-uniform: empty second half
     if (ti.x != cur) {
       cur = ti.x;
-      const float* w12 = a.net.wA + (size_t)cur * kSensors * 12;
-      for (int i = threadIdx.x; i < kSensors * 12; i += kDrThreads) W12[i] = __ldg(w12 + i);
-      for (int i = threadIdx.x; i < kSensors; i += kDrThreads) W1[i] = __ldg(a.net.wB + (size_t)cur * kSensors + i);
-      if (threadIdx.x < kOutPad) Bs[threadIdx.x] = __ldg(a.net.bA + (size_t)cur * kOutPad + threadIdx.x);
+      __syncwarp();
+      const float4* w12 = reinterpret_cast<const float4*>(a.net.wA + (size_t)cur * kSensors * 12);
+      for (int i = lane; i < kSensors * 3; i += 32) reinterpret_cast<float4*>(W12)[i] = __ldg(w12 + i);
+      for (int i = lane; i < kSensors; i += 32) W1[i] = __ldg(a.net.wB + (size_t)cur * kSensors + i);
+      if (lane < kOutPad) Bs[lane] = __ldg(a.net.bA + (size_t)cur * kOutPad + lane);
+      __syncwarp();
     }
-    __syncthreads();  // this tile's rows (and weights) visible to all threads
-    const float* rbase = rows + b * kRows * kDrPitch;
-    const float4* row0 = reinterpret_cast<const float4*>(rbase + threadIdx.x * kDrPitch);
-    const float4* row1 = reinterpret_cast<const float4*>(rbase + (threadIdx.x + kDrThreads) * kDrPitch);
+    const int r0 = rb + lane, r1 = rb + lane + 32;
+    const float4* g0 = reinterpret_cast<const float4*>(a.sens + (size_t)(ti.y + (r0 < ti.z ? r0 : 0)) * kK1);
+    const float4* g1 = reinterpret_cast<const float4*>(a.sens + (size_t)(ti.y + (r1 < ti.z ? r1 : 0)) * kK1);
+    float4 q0[12], q1[12];
+#pragma unroll
+    for (int c = 0; c < kDrDepth; ++c) {
+      q0[c] = ld_row16(g0 + c);
+      q1[c] = ld_row16(g1 + c);
+    }
     u64 acc[2][6];
     float acc12[2] = {0.0f, 0.0f};
 #pragma unroll
     for (int c = 0; c < 2; ++c)
 #pragma unroll
       for (int p = 0; p < 6; ++p) acc[c][p] = 0ull;
-    float4 c0 = row0[0], c1 = row1[0];
 #pragma unroll
     for (int k = 0; k < kSensors; ++k) {
-      if ((k & 3) == 0 && k > 0) {
-        c0 = row0[k >> 2];
-        c1 = row1[k >> 2];
+      const int ch = k >> 2, j = k & 3;
+      if (j == 0 && ch + kDrDepth < 12) {  // refill the chunk pipeline
+        q0[ch + kDrDepth] = ld_row16(g0 + ch + kDrDepth);
+        q1[ch + kDrDepth] = ld_row16(g1 + ch + kDrDepth);
       }
-      const int j = k & 3;
-      const float x0 = j == 0 ? c0.x : (j == 1 ? c0.y : (j == 2 ? c0.z : c0.w));
-      const float x1 = j == 0 ? c1.x : (j == 1 ? c1.y : (j == 2 ? c1.z : c1.w));
+      const float x0 = j == 0 ? q0[ch].x : (j == 1 ? q0[ch].y : (j == 2 ? q0[ch].z : q0[ch].w));
+      const float x1 = j == 0 ? q1[ch].x : (j == 1 ? q1[ch].y : (j == 2 ? q1[ch].z : q1[ch].w));
       const float4* w4 = reinterpret_cast<const float4*>(W12 + k * 12);
       const float4 wa = w4[0], wb = w4[1], wc = w4[2];
       const u64 wp[6] = {pk2(wa.x, wa.y), pk2(wa.z, wa.w), pk2(wb.x, wb.y),
@@ -665,7 +697,7 @@ __global__ void __launch_bounds__(kDrThreads) k_direct_rows(const NetArgs a) {
     }
 #pragma unroll
     for (int c = 0; c < 2; ++c) {
-      const int r = threadIdx.x + c * kDrThreads;
+      const int r = c ? r1 : r0;
       if (r >= ti.z) continue;
       float z[13];
 #pragma unroll
@@ -693,11 +725,10 @@ __global__ void __launch_bounds__(kDrThreads) k_direct_rows(const NetArgs a) {
         for (int q = 0; q < 4; ++q) dst[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
       }
     }
-    __syncthreads();  // buffer b and the weights are free for the next stage / restage
   }
 }
 
-size_t direct_rows_smem() { return (size_t)(kSensors * 12 + 48 + kOutPad + 2 * kRows * kDrPitch) * sizeof(float); }
+
 
 }  // namespace
 
@@ -742,7 +773,11 @@ cudaError_t launch_hidden_tc(const HidBuffers& b, const StepGeom& g, const Plane
   k_hid_count<<<nctas, kSortThreads, hsmem, st>>>(g, front.gi, capacity, b.cta_hist);
   k_hid_colscan<<<(capacity + 31) / 32, 1024, 0, st>>>(b.cta_hist, nctas, capacity, b.counts);
   k_hid_scan<<<1, 1024, 0, st>>>(b.counts, capacity, b.offs, b.tiles, b.cursor, b.n_tiles);
-  k_hid_tilemap<<<(capacity + 255) / 256, 256, 0, st>>>(b.offs, b.tiles, capacity, b.tile_info);
+  {
+    const long long max_tiles = ((long long)g.W * g.H + kRows - 1) / kRows + capacity;
+    k_hid_tilemap<<<(unsigned)((max_tiles + 255) / 256), 256, 0, st>>>(b.offs, b.tiles, capacity, b.n_tiles,
+                                                                       b.tile_info);
+  }
   k_hid_sense<<<nctas, kSortThreads, ssmem, st>>>(g, front, b.offs, b.cta_hist, capacity, b.sens, b.rank);
   NetArgs a;
   a.net = net;
@@ -756,10 +791,7 @@ cudaError_t launch_hidden_tc(const HidBuffers& b, const StepGeom& g, const Plane
   a.act = b.act;
   a.decided = decided && net.hidden == 0 ? 1 : 0;
   if (net.hidden == 0) {
-    const size_t dsm = direct_rows_smem();
-    e = cudaFuncSetAttribute(k_direct_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm);
-    if (e != cudaSuccess) return e;
-    k_direct_rows<<<num_sms * 4, kDrThreads, dsm, st>>>(a);  // 4 x 53 KB of staged rows per SM
+    k_direct_rows<<<num_sms * 4, kDrThreads, 0, st>>>(a);  // 16 warps per SM, one wave
     return cudaGetLastError();
   }
   const size_t smem = hidden_tc_smem(net.hidden);
