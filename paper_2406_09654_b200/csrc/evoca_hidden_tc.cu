@@ -619,18 +619,25 @@ __global__ void __launch_bounds__(kNetThreads, 1) k_hid_net(const NetArgs a) {
 // 2.4 KB of weights are staged in a warp-private shared buffer once per run
 // of half-tiles (every weight load a warp-uniform broadcast); each lane
 // streams its two 192-byte rows straight from global memory into registers,
-// kDrDepth 16-byte chunks per row in flight (no shared-memory staging, so
+// kDrDepth whole 32-byte sectors per row in flight (LDG.256; no shared-memory staging, so
 // 16 warps fit per SM instead of the 8 that double-buffered 53 KB row tiles
 // allowed), and runs the same packed FFMA2 chains, pairing and k order as the
 // tile kernel (net_direct_unit), so results are bit-identical to it.
 constexpr int kDrWarps = 4;
 constexpr int kDrThreads = kDrWarps * 32;
-constexpr int kDrDepth = 6;     // 16-byte chunks per row in flight
+constexpr int kDrDepth = 3;     // 32-byte chunks (whole sectors) per row in flight
 constexpr int kDrW = kSensors * 12 + 48 + kOutPad;  // W12 [45][12] | W1 [48] | bias [16]
 
-__device__ __forceinline__ float4 ld_row16(const float4* p) {
-  float4 r;
-  asm volatile("ld.global.nc.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w) : "l"(p));
+struct f8 {
+  float v[8];
+};
+// one whole 32-byte sector per lane (LDG.256)
+__device__ __forceinline__ f8 ld_row32(const float* p) {
+  f8 r;
+  asm volatile("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=f"(r.v[0]), "=f"(r.v[1]), "=f"(r.v[2]), "=f"(r.v[3]), "=f"(r.v[4]), "=f"(r.v[5]), "=f"(r.v[6]),
+                 "=f"(r.v[7])
+               : "l"(p));
   return r;
 }
 
@@ -659,13 +666,13 @@ __global__ void __launch_bounds__(kDrThreads, 4) k_direct_rows(const NetArgs a) 
       __syncwarp();
     }
     const int r0 = rb + lane, r1 = rb + lane + 32;
-    const float4* g0 = reinterpret_cast<const float4*>(a.sens + (size_t)(ti.y + (r0 < ti.z ? r0 : 0)) * kK1);
-    const float4* g1 = reinterpret_cast<const float4*>(a.sens + (size_t)(ti.y + (r1 < ti.z ? r1 : 0)) * kK1);
-    float4 q0[12], q1[12];
+    const float* g0 = a.sens + (size_t)(ti.y + (r0 < ti.z ? r0 : 0)) * kK1;
+    const float* g1 = a.sens + (size_t)(ti.y + (r1 < ti.z ? r1 : 0)) * kK1;
+    f8 q0[6], q1[6];
 #pragma unroll
     for (int c = 0; c < kDrDepth; ++c) {
-      q0[c] = ld_row16(g0 + c);
-      q1[c] = ld_row16(g1 + c);
+      q0[c] = ld_row32(g0 + 8 * c);
+      q1[c] = ld_row32(g1 + 8 * c);
     }
     u64 acc[2][6];
     float acc12[2] = {0.0f, 0.0f};
@@ -675,13 +682,13 @@ __global__ void __launch_bounds__(kDrThreads, 4) k_direct_rows(const NetArgs a) 
       for (int p = 0; p < 6; ++p) acc[c][p] = 0ull;
 #pragma unroll
     for (int k = 0; k < kSensors; ++k) {
-      const int ch = k >> 2, j = k & 3;
-      if (j == 0 && ch + kDrDepth < 12) {  // refill the chunk pipeline
-        q0[ch + kDrDepth] = ld_row16(g0 + ch + kDrDepth);
-        q1[ch + kDrDepth] = ld_row16(g1 + ch + kDrDepth);
+      const int ch = k >> 3, j = k & 7;
+      if (j == 0 && ch + kDrDepth < 6) {  // refill the sector pipeline
+        q0[ch + kDrDepth] = ld_row32(g0 + 8 * (ch + kDrDepth));
+        q1[ch + kDrDepth] = ld_row32(g1 + 8 * (ch + kDrDepth));
       }
-      const float x0 = j == 0 ? q0[ch].x : (j == 1 ? q0[ch].y : (j == 2 ? q0[ch].z : q0[ch].w));
-      const float x1 = j == 0 ? q1[ch].x : (j == 1 ? q1[ch].y : (j == 2 ? q1[ch].z : q1[ch].w));
+      const float x0 = q0[ch].v[j];
+      const float x1 = q1[ch].v[j];
       const float4* w4 = reinterpret_cast<const float4*>(W12 + k * 12);
       const float4 wa = w4[0], wb = w4[1], wc = w4[2];
       const u64 wp[6] = {pk2(wa.x, wa.y), pk2(wa.z, wa.w), pk2(wb.x, wb.y),
