@@ -63,42 +63,89 @@ __device__ __forceinline__ void zero_stats(const Pass1Args& a) {
 // tail runs per cell straight from the planes - coalesced state reads, one
 // 64-byte actuator row read per occupied cell, coalesced stores - with no
 // shared-memory staging.
+__device__ __forceinline__ CellAct row_actions(const Pass1Args& a, int r) {
+  CellAct ac{};
+  ac.acted = r >= 0;
+  if (ac.acted && a.act_decided) {  // one 32-byte sector: {inv, liq, m0, m1, m2, xmax, kstar, 0}
+    float v[8];
+    asm volatile("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]), "=f"(v[4]), "=f"(v[5]), "=f"(v[6]), "=f"(v[7])
+                 : "l"(a.act_in + (size_t)r * 8));
+    ac.inv = v[0];
+    ac.liq = v[1];
+    ac.m0 = v[2];
+    ac.m1 = v[3];
+    ac.m2 = v[4];
+    ac.xmax = v[5];
+    ac.kstar = __float_as_int(v[6]);
+  } else if (ac.acted) {
+    const float4* row = reinterpret_cast<const float4*>(a.act_in + (size_t)r * 16);
+    const float4 r0 = __ldg(row), r1 = __ldg(row + 1), r2 = __ldg(row + 2), r3 = __ldg(row + 3);
+    ac.inv = r0.x;
+    ac.liq = r0.y;
+    ac.m0 = r0.z;
+    ac.m1 = r0.w;
+    ac.m2 = r1.x;
+    const float ex[8] = {r1.y, r1.z, r1.w, r2.x, r2.y, r2.z, r2.w, r3.x};
+    explore_argmax(ex, ac.kstar, ac.xmax);
+  }
+  return ac;
+}
+
+// Four consecutive cells per thread (W % 4 == 0): 16-byte plane loads and
+// stores, one load instruction per plane per four cells (the per-cell
+// version was LSU-queue bound: lg_throttle 28 %, long_scoreboard 60 %).
 __global__ void __launch_bounds__(256) k_physics_rows(const Pass1Args a) {
   zero_stats(a);
   const StepGeom& g = a.g;
   const int n = g.W * g.H;
   const unsigned st = (unsigned)g.stride;
+  if ((g.W & 3) == 0) {
+    for (int c0 = (blockIdx.x * blockDim.x + threadIdx.x) * 4; c0 < n; c0 += gridDim.x * blockDim.x * 4) {
+      const int y = c0 / g.W, x = c0 - y * g.W;
+      const unsigned o = (unsigned)((y + 1) * g.W + x);
+      const float4 E = __ldg(reinterpret_cast<const float4*>(a.front.E + o));
+      const float4 I = __ldg(reinterpret_cast<const float4*>(a.front.I + o));
+      const float4 C0 = __ldg(reinterpret_cast<const float4*>(a.front.C + o));
+      const float4 C1 = __ldg(reinterpret_cast<const float4*>(a.front.C + st + o));
+      const float4 C2 = __ldg(reinterpret_cast<const float4*>(a.front.C + 2 * st + o));
+      const int4 G = __ldg(reinterpret_cast<const int4*>(a.front.gi + o));
+      const unsigned R = __ldg(reinterpret_cast<const unsigned*>(a.front.rot + o));
+      const int4 RK = __ldg(reinterpret_cast<const int4*>(a.act_rank + c0));
+      const float e[4] = {E.x, E.y, E.z, E.w}, in[4] = {I.x, I.y, I.z, I.w};
+      const float c0v[4] = {C0.x, C0.y, C0.z, C0.w}, c1v[4] = {C1.x, C1.y, C1.z, C1.w},
+                  c2v[4] = {C2.x, C2.y, C2.z, C2.w};
+      const int gv[4] = {G.x, G.y, G.z, G.w}, rk[4] = {RK.x, RK.y, RK.z, RK.w};
+      CellOut out[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const CellState cs{e[j], in[j], c0v[j], c1v[j], c2v[j], gv[j], (int)((R >> (8 * j)) & 0xFFu)};
+        out[j] = cell_physics(a.s, a.phases, a.src_map, c0 + j, cs, row_actions(a, rk[j]));
+      }
+      if (g.own_ghosts && (y == 0 || y == g.H - 1)) {  // seam rows: per-cell stores with the wrapped copies
+#pragma unroll
+        for (int j = 0; j < 4; ++j) store_pass1(a, y, x + j, out[j]);
+        continue;
+      }
+      *reinterpret_cast<float4*>(a.back.E + o) = make_float4(out[0].e, out[1].e, out[2].e, out[3].e);
+      *reinterpret_cast<float4*>(a.back.C + o) = make_float4(out[0].c0, out[1].c0, out[2].c0, out[3].c0);
+      *reinterpret_cast<float4*>(a.back.C + st + o) = make_float4(out[0].c1, out[1].c1, out[2].c1, out[3].c1);
+      *reinterpret_cast<float4*>(a.back.C + 2 * st + o) = make_float4(out[0].c2, out[1].c2, out[2].c2, out[3].c2);
+      *reinterpret_cast<float4*>(a.mid.I + o) = make_float4(out[0].inf, out[1].inf, out[2].inf, out[3].inf);
+      *reinterpret_cast<int4*>(a.mid.gi + o) = make_int4(out[0].slot, out[1].slot, out[2].slot, out[3].slot);
+      *reinterpret_cast<unsigned*>(a.mid.rp + o) =
+          (unsigned)out[0].rp | ((unsigned)out[1].rp << 8) | ((unsigned)out[2].rp << 16) | ((unsigned)out[3].rp << 24);
+      *reinterpret_cast<float4*>(a.mid.q + o) = make_float4(out[0].q, out[1].q, out[2].q, out[3].q);
+    }
+    return;
+  }
   for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < n; c += gridDim.x * blockDim.x) {
     const int y = c / g.W, x = c - y * g.W;
     const unsigned o = (unsigned)((y + 1) * g.W + x);
     const CellState cs{__ldg(a.front.E + o), __ldg(a.front.I + o), __ldg(a.front.C + o),
                        __ldg(a.front.C + st + o), __ldg(a.front.C + 2 * st + o), __ldg(a.front.gi + o),
                        (int)__ldg(a.front.rot + o)};
-    CellAct ac{};
-    const int r = __ldg(a.act_rank + c);
-    ac.acted = r >= 0;
-    if (ac.acted && a.act_decided) {
-      const float4* row = reinterpret_cast<const float4*>(a.act_in + (size_t)r * 8);
-      const float4 r0 = __ldg(row), r1 = __ldg(row + 1);
-      ac.inv = r0.x;
-      ac.liq = r0.y;
-      ac.m0 = r0.z;
-      ac.m1 = r0.w;
-      ac.m2 = r1.x;
-      ac.xmax = r1.y;
-      ac.kstar = __float_as_int(r1.z);
-    } else if (ac.acted) {
-      const float4* row = reinterpret_cast<const float4*>(a.act_in + (size_t)r * 16);
-      const float4 r0 = __ldg(row), r1 = __ldg(row + 1), r2 = __ldg(row + 2), r3 = __ldg(row + 3);
-      ac.inv = r0.x;
-      ac.liq = r0.y;
-      ac.m0 = r0.z;
-      ac.m1 = r0.w;
-      ac.m2 = r1.x;
-      const float ex[8] = {r1.y, r1.z, r1.w, r2.x, r2.y, r2.z, r2.w, r3.x};
-      explore_argmax(ex, ac.kstar, ac.xmax);
-    }
-    store_pass1(a, y, x, cell_physics(a.s, a.phases, a.src_map, c, cs, ac));
+    store_pass1(a, y, x, cell_physics(a.s, a.phases, a.src_map, c, cs, row_actions(a, __ldg(a.act_rank + c))));
   }
 }
 
