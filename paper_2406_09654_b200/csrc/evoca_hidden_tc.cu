@@ -175,11 +175,12 @@ __global__ void k_hid_scan(const int32_t* counts, int cap, int32_t* offs, int32_
 // planes' halo (34 x 34) is staged in shared memory with coalesced loads;
 // each warp assembles 32 rows from it and writes them out cooperatively (12
 // lanes per 192-byte row, whole sectors per store instruction).
-constexpr int kRowPitch = 49;  // floats per staged row (bank-conflict padding)
+constexpr int kRowPitch = 52;  // floats per staged row: 16-byte rows, 13 x 16 B apart (conflict-free STS/LDS.128)
 constexpr int kSH = kST + 2;   // halo edge
 
 struct SenseSmem {
-  float pl[5][kSH * kSH];
+  float4 eic[kSH * kSH];  // {E, I, C0, C1} interleaved: one LDS.128 per Moore slot
+  float c2[kSH * kSH];
   int gi[kST * kST];
   uint8_t rot[kST * kST];
   float stage[kSortThreads / 32][32 * kRowPitch];
@@ -245,7 +246,10 @@ __global__ void __launch_bounds__(kSortThreads, 2) k_hid_sense(const StepGeom g,
       const int i = threadIdx.x + j * kSortThreads;
       if (i < kSH * kSH)
 #pragma unroll
-        for (int ch = 0; ch < 5; ++ch) sm.pl[ch][i] = pv[j][ch];
+      {
+        sm.eic[i] = make_float4(pv[j][0], pv[j][1], pv[j][2], pv[j][3]);
+        sm.c2[i] = pv[j][4];
+      }
     }
 #pragma unroll
     for (int j = 0; j < kPC; ++j) {
@@ -266,15 +270,23 @@ __global__ void __launch_bounds__(kSortThreads, 2) k_hid_sense(const StepGeom g,
           rank = atomicAdd(&cursor[slot], 1);
           const int rot = sm.rot[i];
           const int hb = (ty + 1) * kSH + tx + 1;
-          float* row = stage + lane * kRowPitch;
+          float v[kK1];
 #pragma unroll
           for (int s = 0; s < 9; ++s) {
             const int hp = s == 0 ? hb : hb + dir_dy(perm_dir(rot, s - 1)) * kSH + dir_dx(perm_dir(rot, s - 1));
-#pragma unroll
-            for (int ch = 0; ch < 5; ++ch) row[s * 5 + ch] = sm.pl[ch][hp];
+            const float4 q = sm.eic[hp];
+            v[s * 5 + 0] = q.x;
+            v[s * 5 + 1] = q.y;
+            v[s * 5 + 2] = q.z;
+            v[s * 5 + 3] = q.w;
+            v[s * 5 + 4] = sm.c2[hp];
           }
-          row[45] = __int_as_float(c);
-          row[46] = row[47] = 0.0f;
+          v[45] = __int_as_float(c);
+          v[46] = v[47] = 0.0f;
+          float4* row = reinterpret_cast<float4*>(stage + lane * kRowPitch);
+#pragma unroll
+          for (int part = 0; part < 12; ++part)
+            row[part] = make_float4(v[4 * part], v[4 * part + 1], v[4 * part + 2], v[4 * part + 3]);
         }
         rank_of_cell[c] = rank;
       }
@@ -283,8 +295,8 @@ __global__ void __launch_bounds__(kSortThreads, 2) k_hid_sense(const StepGeom g,
         const int r = k / 12, part = k - r * 12;
         const int rk = __shfl_sync(0xffffffffu, rank, r);
         if (rk >= 0) {
-          const float* src = stage + r * kRowPitch + part * 4;
-          reinterpret_cast<float4*>(sens + (size_t)rk * kK1)[part] = make_float4(src[0], src[1], src[2], src[3]);
+          reinterpret_cast<float4*>(sens + (size_t)rk * kK1)[part] =
+              *reinterpret_cast<const float4*>(stage + r * kRowPitch + part * 4);
         }
       }
       __syncwarp();
