@@ -56,3 +56,15 @@ def test_fnv_matches_oracle_digest():
         buf = np.ascontiguousarray(a).view(np.uint8).reshape(-1)
         assert lib.evo_fnv1a64(h.value, _lib.ptr(buf), buf.size, C.byref(h)) == 0
     assert h.value == orc.digest(p)
+
+
+def test_flag_and_phase_constants_match_the_header():
+    """Every EVO_F_* / EVO_PH_* the header defines has the same value in the
+    ctypes layer (F_* / PH_* in _lib)."""
+    text = open(HEADER).read()
+    defs = dict(re.findall(r"#define\s+EVO_((?:F|PH)_\w+)\s+(\d+)", text))
+    assert {"F_INJECT_ACTIONS", "F_EXPORT_ACTIONS", "F_MMA_NET", "F_TILE_NET"} <= set(defs)
+    for name, value in defs.items():
+        if hasattr(_lib, name):
+            assert getattr(_lib, name) == int(value), name
+    assert all(hasattr(_lib, n) for n in defs if n.startswith("F_")), "a header flag is missing in _lib"
