@@ -1022,7 +1022,13 @@ __device__ __forceinline__ int resolve_cell(const Pass2Args& a, const WarpTile& 
 }
 
 template <bool kRecord>
-__global__ void __launch_bounds__(kThreads2) k_resolve(const Pass2Args a) {
+// 4 resident CTAs per SM (64 registers, no spills): the 4 x num_sms grid is
+// one wave; at 80 registers only 3 fitted and the last quarter of the grid ran
+// as a tail (k_resolve 22.5 -> 20.9 us on config 2, config 3 step 2.44 -> 2.40 ms)
+#ifndef EVO_K2_MIN_BLOCKS
+#define EVO_K2_MIN_BLOCKS 4
+#endif
+__global__ void __launch_bounds__(kThreads2, EVO_K2_MIN_BLOCKS) k_resolve(const Pass2Args a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   WarpTile* wts = reinterpret_cast<WarpTile*>(smem_raw);
   int* hist = reinterpret_cast<int*>(smem_raw + ((sizeof(WarpTile) * kWarps2 + 15) & ~(size_t)15));
