@@ -3,22 +3,27 @@ cell-updates/sec of the full step, and % of the HBM roofline).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl ours|reference]
 
-Workload (BASELINE.json configs[1]): 1024x1024 torus, 64 genomes, direct
-45->13 controller, synthetic seeded state (paper_2406_09654_b200/synth.py).
-A step = one full substrate update (pass 1 + pass 2).  Each timed step is
-bracketed by CUDA events on the launching stream, with an L2 flush (a 256 MiB
-memset, twice the 126 MB L2) before it and outside the timed interval, so the
-52 MB state is read from HBM every step.  Multi-GPU: one process per GPU
-(torchrun); the torus grows with the GPU count ((1024*N) x 1024, weak
-scaling) and is split into row strips, one per GPU, with NCCL halo exchanges
-and a census all_reduce inside every timed step (paper_2406_09654_b200/
-strips.py); the slowest rank's time is reported.  --strips forces that path
-on one GPU.
+Workload (default, the largest single-GPU BASELINE.json configuration,
+configs[2]): 4096x4096 torus, 256 genomes (pool capacity 2048), direct
+45->13 controller, field radiation every 50 steps (1 % of occupied cells move
+to host-mutated children whose weights the device expresses); synthetic
+seeded state (paper_2406_09654_b200/synth.py).  The timed window is placed so
+that it contains one radiation step (or one per 50 steps for >= 50 steps).
+--config c2 / c4 / c5 select the other BASELINE configurations.
+A step = one full substrate update (pass 1 + pass 2, plus the radiation
+event on its steps).  Each timed step is bracketed by CUDA events on the
+launching stream, with an L2 flush (a 256 MiB memset, twice the 126 MB L2)
+before it and outside the timed interval, so the state (839 MB for config 3,
+52 MB for config 2) is read from HBM every step.  Multi-GPU: one process per
+GPU (torchrun); the torus grows with the GPU count ((H*N) x W, weak scaling)
+and is split into row strips, one per GPU, with NCCL halo exchanges and a
+census all_reduce inside every timed step (paper_2406_09654_b200/strips.py);
+the slowest rank's time is reported.  --strips forces that path on one GPU.
 
 --impl reference times the reference algorithm on the host cores: the
 oracle port (oracle/oracle.py; the reference is pure Python and cannot be
-compiled), each step a bounded sample (a 512x512 or 256x256 window of the
-same workload) so the run stays within minutes.
+compiled), each step a bounded sample (a 1024x1024 window of the same
+workload - all of config 2 - or 512x512 for runs over 100 steps) so the run stays within minutes.
 """
 
 from __future__ import annotations
@@ -169,7 +174,13 @@ def run_ours(args, rank, world, local):
         if e2 is not None:
             e2.record(stream)
 
+    # config 3's field radiation fires after every step t with (t+1) % 50 == 0;
+    # start the clock so that one such step falls in the middle of the timed
+    # window (windows of >= 50 steps hold one per 50 steps anyway)
     t = 0
+    if radiate:
+        every = cfg.radiation_every
+        t = (every - 1 - min(args.steps, every) // 2 - args.warmup) % every
     for _ in range(args.warmup):
         flush.zero_()
         one_step(physics.step_scalars(t, phys), t)
@@ -289,6 +300,7 @@ def run_ours(args, rank, world, local):
         "config": {"workload": cfg.name, "grid": [cfg.height, cfg.width], "genomes": cfg.genomes,
                    "net": "45->13 direct" if cfg.hidden == 0 else f"45->{cfg.hidden}->13",
                    "cells_per_gpu": ncell, "l2": "flushed before every timed step (256 MiB memset)",
+                   "radiation_steps_timed": n_rad,
                    "parallelism": (f"row strips x{world} over a {cfg.height * world}x{cfg.width} torus, NCCL halo "
                                    "exchange + census all_reduce per step") if strips else "single GPU"},
         "roofline": {
@@ -330,13 +342,15 @@ def run_ours(args, rank, world, local):
 
 def cpu_baseline(config: str, budget_s: float = 15.0, side: int | None = None, steps: int | None = None):
     """The oracle port (numpy + numba, like the reference) on the host cores,
-    on a bounded sample of the workload."""
+    on a bounded sample of the workload: SURVEY.md §8d runs config 2 whole
+    and the larger configs as 1024x1024 slices with the same distributions
+    and genome counts."""
     from oracle import oracle as orc
     from paper_2406_09654_b200.synth import BASELINE_CONFIGS
 
     cfg = BASELINE_CONFIGS[config]
-    side_h = min(cfg.height, side or 512)
-    side_w = min(cfg.width, side or 512)
+    side_h = min(cfg.height, side or 1024)
+    side_w = min(cfg.width, side or 1024)
     p = orc.synth_planes(side_h, side_w, cfg.genomes, seed=0, sparse_infra=cfg.sparse_infra)
     net = orc.synth_net(cfg.genomes, cfg.hidden, seed=0)
     phys = orc.Phys(cycle_period=cfg.cycle_period)
@@ -357,7 +371,7 @@ def cpu_baseline(config: str, budget_s: float = 15.0, side: int | None = None, s
 def run_reference(args, rank, world):
     if rank != 0:
         return None
-    side = 512 if args.steps <= 200 else 256
+    side = 1024 if args.steps <= 100 else 512
     from paper_2406_09654_b200.synth import BASELINE_CONFIGS
 
     cfg = BASELINE_CONFIGS[args.config]
@@ -389,7 +403,7 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--config", default="c2")
+    ap.add_argument("--config", default="c3")
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")

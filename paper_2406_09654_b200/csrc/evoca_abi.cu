@@ -784,7 +784,10 @@ EVO_API int evo_step_host(evo_ctx* c, const evo_scalars* s, int64_t t, int flags
     if (int r = p2(R[nb - 1] - 33, H)) return r;
     if (int r = p2(0, 1)) return r;
   }
-  if (census) CK(evo::launch_census_finish(c->census, c->cap, t, st));
+  // the census epilogue (slot deaths) only runs on accepted planes: with
+  // *bad set it just clears the counts, so a rejected step leaves the
+  // slot table as it was
+  if (census) CK(evo::launch_census_finish(c->census, c->cap, t, st, c->bad));
   CK(evo::launch_refresh_ghosts(B, c->geom(), st));  // device-resident steps may follow
   CK(cudaMemcpyAsync(c->h_stage, c->bad, sizeof(int), cudaMemcpyDeviceToHost, st));
   if (stats) CK(cudaMemcpyAsync(c->h_stage + 8, c->census.stats, 16, cudaMemcpyDeviceToHost, st));

@@ -169,7 +169,8 @@ cudaError_t launch_frag_relayout(const Params& net, int capacity, float* wF, cud
 cudaError_t launch_pass2(const Pass2Args& a, cudaStream_t st);
 cudaError_t debug_phase_cycles(unsigned long long* out, bool reset);
 cudaError_t debug_hidden_cycles(unsigned long long* out, bool reset);
-cudaError_t launch_census_finish(const Census& c, int capacity, long long t, cudaStream_t st);
+cudaError_t launch_census_finish(const Census& c, int capacity, long long t, cudaStream_t st,
+                                 const int* skip = nullptr);
 cudaError_t launch_refresh_ghosts(const Planes& p, const StepGeom& g, cudaStream_t st);
 cudaError_t launch_render_rgb(const Planes& f, const StepGeom& g, double norm_e, double norm_i, uint32_t* out,
                               cudaStream_t st);

@@ -1194,12 +1194,16 @@ __global__ void __launch_bounds__(kThreads2, EVO_K2_MIN_BLOCKS) k_resolve(const 
 }
 
 
-// Census epilogue as its own launch (strip mode: after the cross-rank sum of counts).
-__global__ void k_census_finish(const Census c, int capacity, long long t) {
+// Census epilogue as its own launch (strip mode: after the cross-rank sum of
+// counts).  A set *skip (rejected host planes, evo_step_host) only clears
+// the accumulators: slot states are left as they were before the step.
+__global__ void k_census_finish(const Census c, int capacity, long long t, const int* skip) {
+  const bool discard = skip && *skip;
   int dead = 0;
   for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < capacity; b += gridDim.x * blockDim.x) {
     const int n = c.counts[b];
     c.counts[b] = 0;
+    if (discard) continue;
     c.counts_last[b] = n;
     if (c.state[b] == 1) {
       if (n == 0) {
@@ -1360,19 +1364,36 @@ __global__ void k_patch_genomes(int32_t* gi, int W, const int64_t* cells, const 
 // ---------------------------------------------------------------------------
 // launchers
 
-static int g_num_sms = 0;
+// Per-device launch configuration: the SM count and every kernel's opted-in
+// dynamic shared-memory size are properties of the device (context), so they
+// are cached per device ordinal - a process may drive several GPUs.
+constexpr int kMaxDevices = 64;
+static int current_device() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  return dev >= 0 && dev < kMaxDevices ? dev : 0;
+}
 static int num_sms() {
-  if (!g_num_sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
-    if (g_num_sms <= 0) g_num_sms = 148;
+  static int sms[kMaxDevices] = {0};
+  const int dev = current_device();
+  if (!sms[dev]) {
+    int n = 0;
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    sms[dev] = n > 0 ? n : 148;
   }
-  return g_num_sms;
+  return sms[dev];
 }
 
+struct SmemOptIn {
+  int bytes[kMaxDevices] = {0};
+};
+// Raise `kernel`'s dynamic shared-memory limit on the current device if
+// `smem` exceeds what was configured there; *first is set when this device
+// configures the kernel for the first time.
 template <typename K>
-static cudaError_t set_smem(K kernel, size_t smem, int& configured) {
+static cudaError_t set_smem(K kernel, size_t smem, SmemOptIn& cfg, bool* first = nullptr) {
+  int& configured = cfg.bytes[current_device()];
+  if (first) *first = configured == 0;
   if ((int)smem <= configured) return cudaSuccess;
   cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e == cudaSuccess) configured = (int)smem;
@@ -1382,8 +1403,8 @@ static cudaError_t set_smem(K kernel, size_t smem, int& configured) {
 template <bool I, bool E, bool H>
 static cudaError_t launch_generic(const Pass1Args& a, cudaStream_t st) {
   const size_t smem = sizeof(GenericSmem) + (size_t)a.capacity * sizeof(int);
-  static int configured = 0;
-  cudaError_t e = set_smem(k_pass1_generic<I, E, H>, smem, configured);
+  static SmemOptIn cfg;
+  cudaError_t e = set_smem(k_pass1_generic<I, E, H>, smem, cfg);
   if (e != cudaSuccess) return e;
   const int tiles = ((a.g.W + kTileW - 1) / kTileW) * ((a.g.H + kTileH - 1) / kTileH);
   k_pass1_generic<I, E, H><<<tiles, kThreads1, smem, st>>>(a);
@@ -1394,10 +1415,11 @@ template <bool E, bool S>
 static cudaError_t launch_direct(const Pass1Args& a, cudaStream_t st) {
   size_t smem = sizeof(DirectSmem) + (size_t)a.capacity * sizeof(int);
   if (S) smem = ((smem + 15) & ~(size_t)15) + weight_smem_bytes(a.capacity);
-  static int configured = 0;
-  if ((int)smem > configured) {
-    cudaError_t e = set_smem(k_pass1_direct<E, S>, smem, configured);
-    if (e != cudaSuccess) return e;
+  static SmemOptIn cfg;
+  bool first = false;
+  cudaError_t e = set_smem(k_pass1_direct<E, S>, smem, cfg, &first);
+  if (e != cudaSuccess) return e;
+  if (first) {
     if (!S) {
       // smallest shared-memory carveout that holds one CTA: the rest of the
       // 256 KB per SM stays L1, where the per-genome weight table lives.
@@ -1415,8 +1437,8 @@ static cudaError_t launch_direct(const Pass1Args& a, cudaStream_t st) {
 template <bool E>
 static cudaError_t launch_mma(const Pass1Args& a, cudaStream_t st) {
   const size_t smem = ((sizeof(MmaSmem) + 15) & ~(size_t)15) + (size_t)a.capacity * kFragGenome * sizeof(float);
-  static int configured = 0;
-  cudaError_t e = set_smem(k_pass1_mma<E>, smem, configured);
+  static SmemOptIn cfg;
+  cudaError_t e = set_smem(k_pass1_mma<E>, smem, cfg);
   if (e != cudaSuccess) return e;
   const int tiles = ((a.g.W + kTileW - 1) / kTileW) * ((a.g.H + kTileH - 1) / kTileH);
   const int grid = tiles < num_sms() ? tiles : num_sms();
@@ -1447,7 +1469,7 @@ cudaError_t launch_pass1(const Pass1Args& a, bool inject, bool export_actions, c
   return export_actions ? launch_direct<true, false>(a, st) : launch_direct<false, false>(a, st);
 }
 
-cudaError_t launch_census_finish(const Census& c, int capacity, long long t, cudaStream_t st);
+cudaError_t launch_census_finish(const Census& c, int capacity, long long t, cudaStream_t st, const int* skip);
 
 cudaError_t launch_pass2(const Pass2Args& a_in, cudaStream_t st) {
   Pass2Args a = a_in;
@@ -1470,12 +1492,12 @@ cudaError_t launch_pass2(const Pass2Args& a_in, cudaStream_t st) {
   if (grid > need) grid = need;
   const size_t smem = ((sizeof(WarpTile) * kWarps2 + 15) & ~(size_t)15) + (size_t)a.capacity * sizeof(int);
   if (a.ev.src) {
-    static int cfg = 0;
+    static SmemOptIn cfg;
     cudaError_t e = set_smem(k_resolve<true>, smem, cfg);
     if (e != cudaSuccess) return e;
     k_resolve<true><<<grid, kThreads2, smem, st>>>(a);
   } else {
-    static int cfg = 0;
+    static SmemOptIn cfg;
     cudaError_t e = set_smem(k_resolve<false>, smem, cfg);
     if (e != cudaSuccess) return e;
     k_resolve<false><<<grid, kThreads2, smem, st>>>(a);
@@ -1484,7 +1506,7 @@ cudaError_t launch_pass2(const Pass2Args& a_in, cudaStream_t st) {
   if (finish) {
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
-    return launch_census_finish(a.census, a.capacity, a.t, st);
+    return launch_census_finish(a.census, a.capacity, a.t, st, nullptr);
   }
 #endif
   return cudaGetLastError();
@@ -1499,9 +1521,9 @@ cudaError_t debug_phase_cycles(unsigned long long* out, bool reset) {
   return e;
 }
 
-cudaError_t launch_census_finish(const Census& c, int capacity, long long t, cudaStream_t st) {
+cudaError_t launch_census_finish(const Census& c, int capacity, long long t, cudaStream_t st, const int* skip) {
   const int blocks = (capacity + 255) / 256;
-  k_census_finish<<<blocks, 256, 0, st>>>(c, capacity, t);
+  k_census_finish<<<blocks, 256, 0, st>>>(c, capacity, t, skip);
   return cudaGetLastError();
 }
 

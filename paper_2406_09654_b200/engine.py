@@ -78,9 +78,9 @@ class HypernetConfig:
 
 @dataclass
 class EvolutionRates:
-    """neuroevo.py:170-203.  The radiation probabilities default to 0 here
-    (the BASELINE configurations run without host NEAT radiation); set the
-    reference's 0.02 / 0.2 to restore its default evolution."""
+    """neuroevo.py:170-203, with the reference's defaults (p_radiation 0.02,
+    p_merge 0.2: adoption-driven radiation is on unless a config turns it
+    off; the BASELINE synthetic configurations set both to 0)."""
 
     weight_perturb_prob: float = 0.8
     weight_perturb_sigma: float = 0.5
@@ -91,8 +91,8 @@ class EvolutionRates:
     c1: float = 1.0
     c2: float = 1.0
     c3: float = 0.4
-    p_radiation: float = 0.0
-    p_merge: float = 0.0
+    p_radiation: float = 0.02
+    p_merge: float = 0.2
 
     def validate(self) -> None:  # neuroevo.py:186-203
         for name in ("weight_perturb_prob", "weight_reset_prob", "add_connection_prob", "add_node_prob",
@@ -423,17 +423,13 @@ def _radiation_active(state) -> bool:
 
 
 def _radiation_fn(state):
+    """The host radiation callback: ``state.radiation`` if set, else this
+    package's restatement of physics.apply_radiation (radiation.py)."""
     if getattr(state, "radiation", None) is not None:
         return state.radiation
-    try:  # the reference's host NEAT, when installed alongside
-        from evoca.physics import apply_radiation  # type: ignore
+    from .radiation import apply_radiation
 
-        return apply_radiation
-    except Exception as exc:  # pragma: no cover - depends on the host install
-        raise NotImplementedError(
-            "radiation is enabled but no host NEAT callback is available: set state.radiation "
-            "or install the reference package"
-        ) from exc
+    return apply_radiation
 
 
 # -- the drop-in step -------------------------------------------------------------
@@ -499,8 +495,9 @@ def _fold_census(state) -> None:
     counts, st, death, peak = b.dev.read_census()
     pool = state.pool
     if isinstance(pool, SlotPool):
+        # the device already holds these slot states; pool.version is not
+        # bumped, so changes the host made since the last sync stay pending
         pool.apply_device_census(st, death, peak)
-        b.pool_version = pool.version
         return
     # foreign pool (e.g. the reference GenomePool): replay update_census in
     # death-step order, feeding each slot's peak so peaks update identically
@@ -798,7 +795,8 @@ def baseline_state(name: str = "c2", seed: int = 0, width: int | None = None, he
     w = width or cfg.width
     h = height or cfg.height
     g = genomes or cfg.genomes
-    ec = ExperimentConfig(grid=GridConfig(w, h), seed=seed, hypernet=HypernetConfig(cfg.hidden))
+    ec = ExperimentConfig(grid=GridConfig(w, h), seed=seed, hypernet=HypernetConfig(cfg.hidden),
+                          evolution=EvolutionRates(p_radiation=0.0, p_merge=0.0))  # SURVEY.md §8d notes
     ec.physics.cycle_period = cfg.cycle_period
     ec.field_radiation = FieldRadiationConfig(cfg.radiation_every, cfg.radiation_p or 0.01)
     sub = create_substrate(w, h)

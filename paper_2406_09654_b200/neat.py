@@ -11,6 +11,8 @@ kernel:
   (neuroevo.py:233-299: weight reset/perturb, toggles, add-connection,
   add-node, in that fixed order and draw order), so a given Philox stream
   yields the same child (pinned by tests/golden/cppn_cases.npz);
+* ``crossover`` - recombination of two parents (neuroevo.py:329-351) in the
+  reference's draw order (pinned by tests/golden/radiation_steps.npz);
 * ``init_genome`` (neuroevo.py:212-230) and ``init_c3_genome``, the
   BASELINE config-3 pattern network (4 coordinate inputs -> 8 hidden
   sin/gauss/tanh nodes -> weight output, weights N(0,1); SURVEY.md §8d C3);
@@ -36,6 +38,7 @@ __all__ = [
     "init_genome",
     "init_c3_genome",
     "mutate",
+    "crossover",
     "topo_order",
     "compile_programs",
     "layout_coords",
@@ -211,6 +214,48 @@ def mutate(genome, rates: EvolutionRates, rng: np.random.Generator, counter: Inn
             conns.append(ConnGene(counter.new_innovation(), old.src, nid, 1.0, True))
             conns.append(ConnGene(counter.new_innovation(), nid, old.dst, old.weight, True))
     return CppnGenome(tuple(nodes), tuple(conns))
+
+
+def _paired_genes(a, b):
+    """Innovation-ordered walk over two connection lists (both are kept in
+    ascending innovation order by mutate): yields (gene of a | None, gene of
+    b | None), both set for a matching innovation (neuroevo.py:304-326)."""
+    ca, cb = a.connections, b.connections
+    i = j = 0
+    while i < len(ca) or j < len(cb):
+        ka = ca[i].innovation if i < len(ca) else None
+        kb = cb[j].innovation if j < len(cb) else None
+        if kb is None or (ka is not None and ka < kb):
+            yield ca[i], None
+            i += 1
+        elif ka is None or kb < ka:
+            yield None, cb[j]
+            j += 1
+        else:
+            yield ca[i], cb[j]
+            i += 1
+            j += 1
+
+
+def crossover(fitter, other, rng: np.random.Generator) -> CppnGenome:
+    """Child of two genomes, ``fitter`` first (neuroevo.py:329-351), with the
+    reference's draw order: for every gene of the fitter parent, a matching
+    gene first draws which parent's weight to take (< 0.5: the fitter's);
+    then any gene disabled in a parent draws once more and stays disabled
+    unless that draw is >= 0.75.  Genes only the other parent has are
+    dropped, so the child keeps the fitter's node and edge sets."""
+    genes = []
+    for mine, theirs in _paired_genes(fitter, other):
+        if mine is None:
+            continue
+        if theirs is None:
+            weight, was_off = mine.weight, not mine.enabled
+        else:
+            weight = mine.weight if rng.random() < 0.5 else theirs.weight
+            was_off = not (mine.enabled and theirs.enabled)
+        enabled = True if not was_off else bool(rng.random() >= 0.75)
+        genes.append(replace(mine, weight=weight, enabled=enabled))
+    return CppnGenome(fitter.nodes, tuple(genes))
 
 
 def topo_order(genome) -> list:

@@ -12,6 +12,13 @@ Host NEAT (mutation, crossover, pool admission) stays on the host
   the reference's own ``apply_radiation`` (physics.py:346-392), run on the
   device-compacted adoption events, admits children whose weights are
   generated on the GPU.
+* ``apply_radiation`` - the reference's adoption-driven radiation
+  (physics.py:346-392) owned by this package: per device-compacted adoption
+  event (ascending target), a merge roll and a mutation roll from the step's
+  "radiation" stream, then ``neat.crossover`` / ``neat.mutate`` from the
+  event's own "merge" / "mutate" stream, pool admission and installation of
+  the child at the target.  The engine calls it whenever p_radiation or
+  p_merge is non-zero (engine.py:244 in the reference).
 * ``field_radiation`` - the BASELINE config-3 extension:
   every ``every`` steps, 1 % of occupied cells (device draw from the host
   Philox stream ``rng.stream(seed, t, "field_radiation")``, rng.py:19-33) are
@@ -26,7 +33,8 @@ import numpy as np
 
 from . import neat
 
-__all__ = ["DeviceExpressed", "device_net_factory", "use_device_expression", "stream_key", "field_radiation"]
+__all__ = ["DeviceExpressed", "device_net_factory", "use_device_expression", "stream_key", "apply_radiation",
+           "field_radiation"]
 
 
 stream_key = neat.stream_key
@@ -84,6 +92,46 @@ def use_device_expression(state, tau: float = 0.2, w_max: float = 3.0) -> None:
     from .engine import _hidden_of
 
     state.pool.net_factory = device_net_factory(_hidden_of(state), tau, w_max)
+
+
+def apply_radiation(events, pool, rates, planes, master_seed: int, step: int) -> None:
+    """Adoption-driven radiation on a host genome plane (physics.py:346-392).
+
+    ``events``: AdoptionEvents of the step in ascending target order;
+    ``pool``: a slot pool with ``live_mask / can_admit / admit / genome /
+    lineage / innovations`` (SlotPool or the reference's GenomePool);
+    ``rates``: ``p_merge``, ``p_radiation`` and the mutation rates;
+    ``planes``: the PlaneSet whose genome plane receives the children (the
+    back buffer, before the census).  Decisions are taken for all events
+    first (the liveness of the defenders as it was when the step began), then
+    children are admitted in target order until the pool is full."""
+    n = len(events)
+    if n == 0:
+        return
+    merge_roll, mutate_roll = neat.stream(master_seed, step, "radiation").random((2, n))
+    winner = np.asarray(events.winner_slot, np.int64)
+    defender = np.asarray(events.defender_slot, np.int64)
+    live = np.asarray(pool.live_mask(), bool)
+    merge_ok = (defender >= 0) & (defender != winner)
+    merge_ok[merge_ok] = live[defender[merge_ok]]
+    merge = merge_ok & (merge_roll < rates.p_merge)
+    mutation = ~merge & (mutate_roll < rates.p_radiation)
+    cells = planes.genome_index.reshape(-1)
+    for k in np.flatnonzero(merge | mutation):
+        if not pool.can_admit():
+            break  # admissions only fill slots within one call
+        tgt, win = int(events.target[k]), int(winner[k])
+        if merge[k]:
+            dfd = int(defender[k])
+            child = neat.crossover(pool.genome(win), pool.genome(dfd), neat.stream(master_seed, step, "merge", tgt))
+            parents = (pool.lineage(win), pool.lineage(dfd))
+        else:
+            child = neat.mutate(pool.genome(win), rates, neat.stream(master_seed, step, "mutate", tgt),
+                                pool.innovations)
+            parents = (pool.lineage(win),)
+        slot = pool.admit(child, parents=parents, birth_step=step + 1)
+        if slot is not None:
+            cells[tgt] = slot
 
 
 def field_radiation(state, t: int, p: float = 0.01, rates: neat.EvolutionRates | None = None,

@@ -1,0 +1,224 @@
+"""Adoption-driven radiation (reference physics.apply_radiation,
+physics.py:346-392, with crossover neuroevo.py:329-351 and GenomePool.admit
+neuroevo.py:458-487) owned by this package, pinned to reference steps run
+with p_radiation 0.02 / p_merge 0.2 (tests/golden/make_golden_radiation.py).
+
+* CPU: the package's apply_radiation + census on the reference's own events
+  reproduce the reference's genome plane, pool slots, lineages, phylogeny
+  records, innovation counter and every admitted child genome, step by step.
+* GPU (tier A): the device step with the reference's actions injected emits
+  the reference's adoption events; with this package's host radiation the
+  post-step planes and pool equal the reference's bit for bit.
+* GPU (free running): ``engine.step`` itself (host-resident state, device
+  sense + net + physics, host radiation, device CPPN expression of the
+  children) keeps genome/rotation planes and the pool identical to the
+  reference's; continuous planes within 1e-5."""
+
+import json
+import os
+
+import numpy as np
+import pytest
+
+from paper_2406_09654_b200 import engine, neat, radiation
+from paper_2406_09654_b200.physics import AdoptionEvents
+from paper_2406_09654_b200.pool import SlotPool
+from paper_2406_09654_b200.substrate import create_substrate
+from tests import _cases as CS
+
+CASES = ("sparse", "dense")
+
+
+def _genome(d):
+    return neat.CppnGenome(tuple(neat.NodeGene(int(i), r, a) for i, r, a in d["nodes"]),
+                           tuple(neat.ConnGene(int(n), int(s), int(t), float(w), bool(e))
+                                 for n, s, t, w, e in d["connections"]))
+
+
+def _golden():
+    z = CS.load("radiation_steps.npz")
+    with open(os.path.join(CS.GOLDEN, "radiation_genomes.json")) as f:
+        g = json.load(f)
+    return z, g
+
+
+def _pool(z, g, case, net_factory=None):
+    pool = SlotPool(int(z[case + "_capacity"]), net_factory=net_factory,
+                    counter=neat.InnovationCounter(*g[case]["innovation"]))
+    for gd in g[case]["initial"]:
+        pool.admit(_genome(gd), parents=(), birth_step=0)
+    return pool
+
+
+def _events(rows):
+    r = np.asarray(rows, np.float64).reshape(-1, 6)
+    return AdoptionEvents(r[:, 0].astype(np.int64), r[:, 1].astype(np.int64), r[:, 2].astype(np.int32),
+                          r[:, 3].astype(np.int32), r[:, 4].astype(np.int64), r[:, 5].astype(np.float32))
+
+
+def _records(pool):
+    rows = []
+    for lid in sorted(pool.records):
+        r = pool.records[lid]
+        par = tuple(r.parents)
+        rows.append([lid, r.slot, r.birth_step, -1 if r.death_step is None else r.death_step, r.peak_population,
+                     par[0] if len(par) > 0 else -1, par[1] if len(par) > 1 else -1, len(par)])
+    return np.asarray(rows, np.int64)
+
+
+def _check_pool(pool, z, g, case, k, lineage_before):
+    sk = f"{case}_s{k:02d}_"
+    assert np.array_equal(pool.slot_states(), z[sk + "pool_state"])
+    assert np.array_equal(pool._lineage, z[sk + "pool_lineage"])
+    assert np.array_equal(pool._death, z[sk + "pool_death"])
+    assert np.array_equal(_records(pool), z[sk + "records"])
+    assert [pool.innovations.next_innovation, pool.innovations.next_node_id] == z[sk + "innovation"].tolist()
+    admitted = g[case]["admitted"][k]
+    assert [lid for lid, _, _ in admitted] == list(range(lineage_before, pool.next_lineage_id))
+    for lid, slot, gd in admitted:
+        assert pool.records[lid].slot == slot
+        assert pool.genome(slot) == _genome(gd)
+
+
+def _census(pool, gi, t):
+    counts = np.bincount(gi[gi >= 0], minlength=pool.capacity)
+    return pool.update_census(counts, t + 1)
+
+
+@pytest.mark.parametrize("case", CASES)
+def test_apply_radiation_matches_reference(case):
+    z, g = _golden()
+    pool = _pool(z, g, case)
+    rates = engine.EvolutionRates()
+    assert [rates.p_radiation, rates.p_merge] == z[case + "_rates"].tolist()
+    seed = int(z[case + "_seed"])
+    merges = mutations = 0
+    for k in range(int(z[case + "_steps"])):
+        sk = f"{case}_s{k:02d}_"
+        planes = create_substrate(64, 64).back
+        planes.genome_index[:] = z[sk + "gi_pre_rad"]
+        ev = _events(z[sk + "events"])
+        before = pool.next_lineage_id
+        radiation.apply_radiation(ev, pool, rates, planes, seed, k)
+        for lid in range(before, pool.next_lineage_id):
+            if len(pool.records[lid].parents) == 2:
+                merges += 1
+            else:
+                mutations += 1
+        dead = _census(pool, planes.genome_index, k)
+        assert np.array_equal(planes.genome_index, z[sk + "post_gi"])
+        assert len(dead) == int(z[sk + "stats"][1])
+        _check_pool(pool, z, g, case, k, before)
+    assert mutations > 0
+    if case == "dense":
+        assert merges > 0
+
+
+def test_crossover_draw_order():
+    """A disabled gene draws a second uniform; matching genes draw the parent."""
+    c = neat.InnovationCounter()
+    a = neat.init_genome(np.random.default_rng(1), c)
+    b = neat.init_genome(np.random.default_rng(2), neat.InnovationCounter())
+    b = neat.CppnGenome(b.nodes, tuple(x if i != 3 else neat.ConnGene(x.innovation, x.src, x.dst, x.weight, False)
+                                       for i, x in enumerate(b.connections)))
+    rng = np.random.default_rng(9)
+    child = neat.crossover(a, b, rng)
+    rng2 = np.random.default_rng(9)
+    draws = []
+    for i in range(len(a.connections)):
+        draws.append(rng2.random())
+        if i == 3:
+            draws.append(rng2.random())
+    pick = [draws[i + (1 if i > 3 else 0)] for i in range(len(a.connections))]
+    for i, gene in enumerate(child.connections):
+        src = a.connections[i] if pick[i] < 0.5 else b.connections[i]
+        assert gene.weight == src.weight
+        assert gene.enabled == (i != 3 or draws[4] >= 0.75)
+    assert child.nodes == a.nodes
+
+
+# -- device -----------------------------------------------------------------------------
+
+
+def _front(sub, z, key):
+    f = sub.front
+    f.channels["energy"][0] = z[key + "E"]
+    f.channels["infrastructure"][0] = z[key + "I"]
+    f.channels["communication"][:] = z[key + "C"]
+    f.genome_index[:] = z[key + "gi"]
+    f.rotation[:] = z[key + "rot"]
+
+
+def _same_planes(ps, z, key, exact=True):
+    vals = (ps.channels["energy"][0], ps.channels["infrastructure"][0], ps.channels["communication"])
+    refs = (z[key + "E"], z[key + "I"], z[key + "C"])
+    for v, r in zip(vals, refs):
+        if exact:
+            assert np.array_equal(v.view(np.uint32), r.view(np.uint32))
+        else:
+            assert np.all(np.abs(v.astype(np.float64) - r) <= 1e-5 * np.maximum(np.abs(r), 1.0))
+    assert np.array_equal(ps.genome_index, z[key + "gi"])
+    assert np.array_equal(ps.rotation, z[key + "rot"])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("case", CASES)
+def test_device_radiation_steps_tier_a(case):
+    from paper_2406_09654_b200 import _lib, physics
+    from paper_2406_09654_b200.device import DeviceSubstrate
+
+    z, g = _golden()
+    pool = _pool(z, g, case)
+    rates = engine.EvolutionRates()
+    seed = int(z[case + "_seed"])
+    sub = create_substrate(64, 64)
+    _front(sub, z, case + "_pre_")
+    dev = DeviceSubstrate(64, 64, pool.capacity, hidden=0)
+    phys = physics.PhysicsParams()
+    try:
+        for k in range(int(z[case + "_steps"])):
+            sk = f"{case}_s{k:02d}_"
+            dev.set_slots(pool.slot_states())
+            dev.upload(sub.front)
+            dev.set_actions(z[sk + "cells"], z[sk + "acts"])
+            dev.step_raw(physics.step_scalars(k, phys), k,
+                         flags=_lib.F_INJECT_ACTIONS | _lib.F_RECORD_EVENTS | _lib.F_NO_CENSUS)
+            ev = dev.read_events()
+            ref_ev = np.asarray(z[sk + "events"], np.float64).reshape(-1, 6)
+            got = np.stack([ev.target, ev.source, ev.winner_slot, ev.defender_slot, ev.direction,
+                            ev.quantity.astype(np.float64)], axis=1) if len(ev) else np.zeros((0, 6))
+            assert np.array_equal(got, ref_ev)
+            back = sub.back
+            dev.download(back)
+            assert np.array_equal(back.genome_index, z[sk + "gi_pre_rad"])
+            before = pool.next_lineage_id
+            radiation.apply_radiation(ev, pool, rates, back, seed, k)
+            _census(pool, back.genome_index, k)
+            dev.census_finish(k)
+            sub.swap_buffers()
+            _same_planes(sub.front, z, sk + "post_")
+            _check_pool(pool, z, g, case, k, before)
+    finally:
+        dev.close()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("case", CASES)
+def test_engine_step_free_running_with_radiation(case):
+    """engine.step end to end (host-resident planes) with the reference's
+    default evolution; children's weights come from the device CPPN kernel."""
+    z, g = _golden()
+    hidden = 16
+    pool = _pool(z, g, case, net_factory=radiation.device_net_factory(hidden))
+    cfg = engine.ExperimentConfig(grid=engine.GridConfig(64, 64), seed=int(z[case + "_seed"]))
+    sub = create_substrate(64, 64)
+    _front(sub, z, case + "_pre_")
+    state = engine.SimState(substrate=sub, pool=pool, config=cfg, master_seed=int(z[case + "_seed"]))
+    for k in range(int(z[case + "_steps"])):
+        sk = f"{case}_s{k:02d}_"
+        before = pool.next_lineage_id
+        engine.step(state)
+        _same_planes(sub.front, z, sk + "post_", exact=False)
+        _check_pool(pool, z, g, case, k, before)
+        assert state.last_adoptions == int(z[sk + "stats"][0])
+        assert state.last_extinctions == int(z[sk + "stats"][1])

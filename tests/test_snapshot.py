@@ -72,3 +72,21 @@ def test_device_state_snapshot_resumes_exactly(tmp_path):
         snapshot.save_snapshot(b, tmp_path / "b2.crls")
         snapshot.save_snapshot(a, tmp_path / "a2.crls")
         assert (tmp_path / "b2.crls").read_bytes() == (tmp_path / "a2.crls").read_bytes()
+
+
+@pytest.mark.gpu
+def test_fresh_state_snapshot_at_step_zero(tmp_path):
+    """A fresh new_state saves before its first step (the reference saves at
+    step 0): the deferred seed networks are expressed on the device for the
+    snapshot, and the loaded copy steps identically."""
+    cfg = engine.ExperimentConfig(grid=engine.GridConfig(32, 24), seed=5, initial_population=12)
+    a = engine.new_state(cfg)
+    path = tmp_path / "fresh.crls"
+    snapshot.save_snapshot(a, path)
+    b = snapshot.load_snapshot(path)
+    assert b.t == 0 and engine.digest(a) == engine.digest(b)
+    for s in range(12):
+        assert np.array_equal(a.pool.params(s).w1, b.pool.params(s).w1)
+    engine.run(a, 3)
+    engine.run(b, 3)
+    assert engine.digest(a) == engine.digest(b)
