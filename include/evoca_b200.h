@@ -216,6 +216,37 @@ EVO_API int evo_select_cells(evo_ctx* ctx, uint64_t key_lo, uint64_t key_hi, dou
 EVO_API int evo_read_selected(evo_ctx* ctx, int64_t capacity, int64_t* cells, int64_t* n);
 EVO_API int evo_remap_selected(evo_ctx* ctx, const int32_t* slot_map);
 
+/* Host NEAT for the radiation feed (north_star (6): mutation stays on the
+ * host), native: `mutate` of the reference (neuroevo.py:233-299) for n
+ * genomes in order, each on its own NumPy Philox4x64-10 stream (keys: 2n
+ * words, low first, = rng.stream(...) keys, rng.py:19-33), with NumPy's
+ * exact random / uniform / normal (ziggurat) / integers draws; the shared
+ * innovation counter (counter[0] next innovation, counter[1] next node id,
+ * in/out) is consumed genome by genome as the reference's loop would.
+ * Genomes are flat arrays: nodes [node_off[g], node_off[g+1]) with id, role
+ * (0 input, 1 hidden, 2 output) and activation code (evo_express_cppn's);
+ * connections [conn_off[g], conn_off[g+1]) with innovation, src, dst,
+ * weight, enabled.  rates = {weight_reset_prob, weight_perturb_prob,
+ * weight_perturb_sigma, add_connection_prob, add_node_prob,
+ * toggle_enable_prob}.  Outputs in the same form; capacity: + 1 node and
+ * + 3 connections per genome.  Host-only (no device involved). */
+EVO_API int evo_neat_mutate(int n, const uint64_t* keys, const double* rates, int64_t* counter,
+                            const int32_t* node_off, const int64_t* node_id, const int8_t* node_role,
+                            const int8_t* node_act, const int32_t* conn_off, const int64_t* c_innov,
+                            const int64_t* c_src, const int64_t* c_dst, const double* c_w, const uint8_t* c_en,
+                            int32_t* o_node_off, int64_t* o_node_id, int8_t* o_node_role, int8_t* o_node_act,
+                            int32_t* o_conn_off, int64_t* o_innov, int64_t* o_src, int64_t* o_dst, double* o_w,
+                            uint8_t* o_en);
+/* The evo_express_cppn program arrays of n flat genomes (hypernet.py:100-155
+ * order; paper_2406_09654_b200.neat.compile_programs layout): prog_off
+ * [n+1], nodes_out [total nodes][4], edge_src / edge_w [total enabled
+ * connections], outs [n][2].  Host-only. */
+EVO_API int evo_neat_compile(int n, const int32_t* node_off, const int64_t* node_id, const int8_t* node_role,
+                             const int8_t* node_act, const int32_t* conn_off, const int64_t* c_src,
+                             const int64_t* c_dst, const double* c_w, const uint8_t* c_en, int32_t* prog_off,
+                             int32_t* nodes_out, int32_t* edge_src, double* edge_w, int32_t* outs);
+EVO_API const char* evo_neat_last_error(void);
+
 /* Page-lock caller-owned host planes (cudaHostRegister) so that the
  * upload/download copies of evo_upload_planes / evo_download_planes run as
  * direct DMA at full link bandwidth; the substrate's front/back arrays live

@@ -86,8 +86,11 @@ SIGNATURES = {
     "evo_fnv1a64": [C.c_uint64, _P, _I64, C.POINTER(C.c_uint64)],
     "evo_debug_phase_cycles": [_P, _I],
     "evo_debug_hidden_cycles": [_P, _I],
+    "evo_neat_mutate": [_I, _P, _P, _P] + [_P] * 10 + [_P] * 10,
+    "evo_neat_compile": [_I] + [_P] * 9 + [_P] * 5,
+    "evo_neat_last_error": [],
 }
-RESTYPES = {"evo_last_error": C.c_char_p}
+RESTYPES = {"evo_last_error": C.c_char_p, "evo_neat_last_error": C.c_char_p}
 
 _lib = None
 

@@ -814,7 +814,11 @@ def baseline_state(name: str = "c2", seed: int = 0, width: int | None = None, he
         from .radiation import device_net_factory
         from .synth import synth_genomes
 
+        from .neat import pack
+
         genomes, pool.innovations = synth_genomes(g, seed)
+        for gen in genomes:  # flat arrays cached for the native radiation mutation
+            pack(gen)
         pool.net_factory = device_net_factory(cfg.hidden)
     for i, p in enumerate(synth_params(g, cfg.hidden, seed)):
         pool.install(i, p, genome=genomes[i])

@@ -41,6 +41,10 @@ __all__ = [
     "crossover",
     "topo_order",
     "compile_programs",
+    "compile_programs_py",
+    "PackedGenome",
+    "pack",
+    "mutate_batch",
     "layout_coords",
     "stream",
     "stream_key",
@@ -180,36 +184,77 @@ def _creates_cycle(conns, src: int, dst: int) -> bool:
     return False
 
 
+def _descendants(conns) -> dict:
+    """Nodes reachable from each node over the full gene graph (disabled
+    edges included; the graph is acyclic, mutate never closes a cycle)."""
+    out: dict = {}
+    for c in conns:
+        out.setdefault(c.src, []).append(c.dst)
+    memo: dict = {}
+    for root in list(out):
+        if root in memo:
+            continue
+        stack = [(root, iter(out.get(root, ())))]
+        onpath = {root}
+        while stack:
+            n, it = stack[-1]
+            m = next(it, None)
+            if m is None:
+                acc = set()
+                for k in out.get(n, ()):
+                    acc.add(k)
+                    acc |= memo[k]
+                memo[n] = acc
+                onpath.discard(n)
+                stack.pop()
+            elif m not in memo:
+                if m in onpath:  # not a DAG: the caller falls back to per-pair search
+                    return {}
+                onpath.add(m)
+                stack.append((m, iter(out.get(m, ()))))
+    return memo
+
+
 def mutate(genome, rates: EvolutionRates, rng: np.random.Generator, counter: InnovationCounter) -> CppnGenome:
     """Mutated copy of ``genome`` (neuroevo.py:233-299), same operation and
-    draw order as the reference."""
+    draw order as the reference (the add-connection candidates are the
+    reference's list, cycle-checked against precomputed descendant sets)."""
     conns = list(genome.connections)
     nodes = list(genome.nodes)
+    rnd = rng.random
+    p_reset, p_perturb, sigma = rates.weight_reset_prob, rates.weight_perturb_prob, rates.weight_perturb_sigma
     for i, c in enumerate(conns):
-        if rng.random() < rates.weight_reset_prob:
-            conns[i] = replace(c, weight=float(rng.uniform(-1.0, 1.0)))
-        elif rng.random() < rates.weight_perturb_prob:
-            conns[i] = replace(c, weight=c.weight + float(rng.normal(0.0, rates.weight_perturb_sigma)))
+        if rnd() < p_reset:
+            conns[i] = ConnGene(c.innovation, c.src, c.dst, float(rng.uniform(-1.0, 1.0)), c.enabled)
+        elif rnd() < p_perturb:
+            conns[i] = ConnGene(c.innovation, c.src, c.dst, c.weight + float(rng.normal(0.0, sigma)), c.enabled)
+    p_toggle = rates.toggle_enable_prob
     for i, c in enumerate(conns):
-        if rng.random() < rates.toggle_enable_prob:
-            conns[i] = replace(c, enabled=not c.enabled)
-    if rng.random() < rates.add_connection_prob:
+        if rnd() < p_toggle:
+            conns[i] = ConnGene(c.innovation, c.src, c.dst, c.weight, not c.enabled)
+    if rnd() < rates.add_connection_prob:
         roles = {n.id: n.role for n in nodes}
         taken = {(c.src, c.dst) for c in conns}
         ordered = sorted(roles)
-        cands = [(s, d) for s in ordered if roles[s] != "output" for d in ordered
-                 if roles[d] != "input" and (s, d) not in taken and not _creates_cycle(conns, s, d)]
+        desc = _descendants(conns)
+        if desc or not conns:
+            empty: set = set()
+            cands = [(s, d) for s in ordered if roles[s] != "output" for d in ordered
+                     if roles[d] != "input" and d != s and (s, d) not in taken and s not in desc.get(d, empty)]
+        else:
+            cands = [(s, d) for s in ordered if roles[s] != "output" for d in ordered
+                     if roles[d] != "input" and (s, d) not in taken and not _creates_cycle(conns, s, d)]
         if cands:
             s, d = cands[int(rng.integers(len(cands)))]
             conns.append(ConnGene(counter.new_innovation(), s, d, float(rng.uniform(-1.0, 1.0)), True))
-    if rng.random() < rates.add_node_prob:
+    if rnd() < rates.add_node_prob:
         enabled = [i for i, c in enumerate(conns) if c.enabled]
         if enabled:
             pick = enabled[int(rng.integers(len(enabled)))]
             old = conns[pick]
             nid = counter.new_node_id()
             act = ACTIVATIONS[int(rng.integers(len(ACTIVATIONS)))]
-            conns[pick] = replace(old, enabled=False)
+            conns[pick] = ConnGene(old.innovation, old.src, old.dst, old.weight, False)
             nodes.append(NodeGene(nid, "hidden", act))
             conns.append(ConnGene(counter.new_innovation(), old.src, nid, 1.0, True))
             conns.append(ConnGene(counter.new_innovation(), nid, old.dst, old.weight, True))
@@ -295,8 +340,10 @@ def layout_coords(hidden: int) -> np.ndarray:
     return np.ascontiguousarray(np.vstack(parts), np.float64)
 
 
-def compile_programs(genomes):
-    """Flatten a batch of genomes into ``evo_express_cppn`` programs.
+def compile_programs_py(genomes):
+    """Flatten a batch of genomes into ``evo_express_cppn`` programs (the
+    Python statement of the layout; ``compile_programs`` runs the native
+    equivalent, tests/test_neat_native.py pins the two together).
 
     Per genome, nodes in ``topo_order``; node record (int32 x4):
     ``[act_code | -1 for inputs, input_position | -1, edge_begin, edge_end]``
@@ -341,3 +388,167 @@ def compile_programs(genomes):
         node_off.append(len(nodes))
     return (np.asarray(node_off, np.int32), np.asarray(nodes, np.int32).reshape(-1, 4),
             np.asarray(edge_src, np.int32), np.asarray(edge_w, np.float64), np.asarray(outs, np.int32).reshape(-1, 2))
+
+
+# -- native host NEAT (csrc/evoca_neat.cpp) -------------------------------------------------
+
+ROLE_CODE = {"input": 0, "hidden": 1, "output": 2}
+ROLE_NAME = ("input", "hidden", "output")
+
+
+class Flat:
+    """A genome as flat arrays (node id / role / activation code;
+    connection innovation / src / dst / weight / enabled)."""
+
+    __slots__ = ("nid", "nrole", "nact", "inn", "src", "dst", "w", "en")
+
+    def __init__(self, nid, nrole, nact, inn, src, dst, w, en):
+        self.nid, self.nrole, self.nact = nid, nrole, nact
+        self.inn, self.src, self.dst, self.w, self.en = inn, src, dst, w, en
+
+
+class PackedGenome(CppnGenome):
+    """A pattern network held as flat arrays - the children of the native
+    mutation.  ``nodes`` / ``connections`` (the reference's gene tuples) are
+    built on first access; the radiation feed itself (mutation of children
+    in later events, program compilation) works on the arrays."""
+
+    def __init__(self, flat: Flat):  # noqa: D107 - bypasses the dataclass init on purpose
+        object.__setattr__(self, "_flat", flat)
+        object.__setattr__(self, "_genes", None)
+
+    def _materialise(self):
+        genes = object.__getattribute__(self, "_genes")
+        if genes is None:
+            f = object.__getattribute__(self, "_flat")
+            nodes = tuple(NodeGene(int(i), ROLE_NAME[int(r)], ACTIVATIONS[int(a)])
+                          for i, r, a in zip(f.nid.tolist(), f.nrole.tolist(), f.nact.tolist()))
+            conns = tuple(ConnGene(n, s_, d, w, bool(e)) for n, s_, d, w, e in
+                          zip(f.inn.tolist(), f.src.tolist(), f.dst.tolist(), f.w.tolist(), f.en.tolist()))
+            genes = (nodes, conns)
+            object.__setattr__(self, "_genes", genes)
+        return genes
+
+    @property
+    def nodes(self):
+        return self._materialise()[0]
+
+    @property
+    def connections(self):
+        return self._materialise()[1]
+
+    def __eq__(self, other):
+        if not hasattr(other, "nodes") or not hasattr(other, "connections"):
+            return NotImplemented
+        return self.nodes == tuple(other.nodes) and self.connections == tuple(other.connections)
+
+    def __hash__(self):
+        return hash((self.nodes, self.connections))
+
+    def __repr__(self):
+        f = object.__getattribute__(self, "_flat")
+        return f"PackedGenome({len(f.nid)} nodes, {len(f.inn)} connections)"
+
+
+def pack(genome) -> Flat:
+    """Flat arrays of a genome (cached on this package's genome objects)."""
+    f = genome.__dict__.get("_flat") if hasattr(genome, "__dict__") else None
+    if f is not None:
+        return f
+    nodes, conns = genome.nodes, genome.connections
+    f = Flat(np.fromiter((n.id for n in nodes), np.int64, len(nodes)),
+             np.fromiter((ROLE_CODE[n.role] for n in nodes), np.int8, len(nodes)),
+             np.fromiter((ACT_CODE[n.activation] for n in nodes), np.int8, len(nodes)),
+             np.fromiter((c.innovation for c in conns), np.int64, len(conns)),
+             np.fromiter((c.src for c in conns), np.int64, len(conns)),
+             np.fromiter((c.dst for c in conns), np.int64, len(conns)),
+             np.fromiter((c.weight for c in conns), np.float64, len(conns)),
+             np.fromiter((c.enabled for c in conns), np.uint8, len(conns)))
+    if isinstance(genome, CppnGenome):
+        object.__setattr__(genome, "_flat", f)
+    return f
+
+
+def _concat(flats):
+    def cat(name, dtype):
+        parts = [getattr(f, name) for f in flats]
+        return np.ascontiguousarray(np.concatenate(parts) if parts else np.empty(0, dtype), dtype)
+
+    node_off = np.zeros(len(flats) + 1, np.int32)
+    node_off[1:] = np.cumsum([len(f.nid) for f in flats])
+    conn_off = np.zeros(len(flats) + 1, np.int32)
+    conn_off[1:] = np.cumsum([len(f.inn) for f in flats])
+    return (node_off, cat("nid", np.int64), cat("nrole", np.int8), cat("nact", np.int8), conn_off,
+            cat("inn", np.int64), cat("src", np.int64), cat("dst", np.int64), cat("w", np.float64),
+            cat("en", np.uint8))
+
+
+def _native():
+    from . import _lib
+
+    return _lib.load()
+
+
+def _neat_check(rc):
+    if rc != 0:
+        raise ValueError(_native().evo_neat_last_error().decode("utf-8", "replace"))
+
+
+def mutate_batch(genomes, rates, keys, counter: InnovationCounter) -> list:
+    """``mutate`` of each genome on its own stream (128-bit Philox keys, e.g.
+    ``stream_key(seed, t, "mutate", index)``), in list order, consuming the
+    shared innovation counter as sequential ``mutate`` calls would; native
+    (evo_neat_mutate).  Returns PackedGenome children."""
+    from ._lib import ptr
+
+    n = len(genomes)
+    if n == 0:
+        return []
+    lib = _native()
+    flats = [pack(g) for g in genomes]
+    node_off, nid, nrole, nact, conn_off, inn, src, dst, w, en = _concat(flats)
+    kw = np.empty(2 * n, np.uint64)
+    m = (1 << 64) - 1
+    for i, k in enumerate(keys):
+        kw[2 * i], kw[2 * i + 1] = int(k) & m, (int(k) >> 64) & m
+    r = np.array([rates.weight_reset_prob, rates.weight_perturb_prob, rates.weight_perturb_sigma,
+                  rates.add_connection_prob, rates.add_node_prob, rates.toggle_enable_prob], np.float64)
+    ctr = np.array([counter.next_innovation, counter.next_node_id], np.int64)
+    NN, NC = len(nid) + n, len(inn) + 3 * n
+    o_node_off, o_conn_off = np.empty(n + 1, np.int32), np.empty(n + 1, np.int32)
+    o_nid, o_nrole, o_nact = np.empty(NN, np.int64), np.empty(NN, np.int8), np.empty(NN, np.int8)
+    o_inn, o_src, o_dst = np.empty(NC, np.int64), np.empty(NC, np.int64), np.empty(NC, np.int64)
+    o_w, o_en = np.empty(NC, np.float64), np.empty(NC, np.uint8)
+    _neat_check(lib.evo_neat_mutate(n, ptr(kw), ptr(r), ptr(ctr), ptr(node_off), ptr(nid), ptr(nrole), ptr(nact),
+                                    ptr(conn_off), ptr(inn), ptr(src), ptr(dst), ptr(w), ptr(en), ptr(o_node_off),
+                                    ptr(o_nid), ptr(o_nrole), ptr(o_nact), ptr(o_conn_off), ptr(o_inn), ptr(o_src),
+                                    ptr(o_dst), ptr(o_w), ptr(o_en)))
+    counter.next_innovation, counter.next_node_id = int(ctr[0]), int(ctr[1])
+    out = []
+    for g in range(n):
+        a, b = o_node_off[g], o_node_off[g + 1]
+        c, d = o_conn_off[g], o_conn_off[g + 1]
+        out.append(PackedGenome(Flat(o_nid[a:b], o_nrole[a:b], o_nact[a:b], o_inn[c:d], o_src[c:d], o_dst[c:d],
+                                     o_w[c:d], o_en[c:d])))
+    return out
+
+
+def compile_programs(genomes):
+    """``evo_express_cppn`` programs of a batch of genomes (the layout of
+    ``compile_programs_py``), linearised natively (evo_neat_compile)."""
+    from ._lib import ptr
+
+    n = len(genomes)
+    flats = [pack(g) for g in genomes]
+    node_off, nid, nrole, nact, conn_off, inn, src, dst, w, en = _concat(flats)
+    prog_off = np.empty(n + 1, np.int32)
+    nodes = np.empty((max(len(nid), 1), 4), np.int32)
+    esrc = np.empty(max(len(inn), 1), np.int32)
+    ew = np.empty(max(len(inn), 1), np.float64)
+    outs = np.empty((max(n, 1), 2), np.int32)
+    _neat_check(_native().evo_neat_compile(n, ptr(node_off), ptr(nid), ptr(nrole), ptr(nact), ptr(conn_off),
+                                           ptr(src), ptr(dst), ptr(w), ptr(en), ptr(prog_off), ptr(nodes),
+                                           ptr(esrc), ptr(ew), ptr(outs)))
+    ne = int(en.sum()) if n else 0
+    return (prog_off, np.ascontiguousarray(nodes[:len(nid)]), np.ascontiguousarray(esrc[:ne]),
+            np.ascontiguousarray(ew[:ne]), np.ascontiguousarray(outs[:n]))

@@ -23,8 +23,9 @@ Host NEAT (mutation, crossover, pool admission) stays on the host
   every ``every`` steps, 1 % of occupied cells (device draw from the host
   Philox stream ``rng.stream(seed, t, "field_radiation")``, rng.py:19-33) are
   selected; one child per distinct parent slot is mutated on the host
-  (``neat.mutate`` with ``stream(seed, t, "mutate", parent)``), admitted, its
-  weights generated on the device, and the selected cells move to it.
+  (native ``neat.mutate_batch``, each parent on ``stream(seed, t, "mutate",
+  parent)``), admitted, its weights generated on the device, and the
+  selected cells move to it.
 """
 
 from __future__ import annotations
@@ -148,12 +149,15 @@ def field_radiation(state, t: int, p: float = 0.01, rates: neat.EvolutionRates |
     counts, n_sel = dev.select_cells(stream_key(state.master_seed, t, purpose), p)
     parents = np.flatnonzero(counts)
     slot_map = np.full(pool.capacity, -1, np.int32)
+    # admissions only fill slots, so the first `room` parents (ascending slot)
+    # get children - exactly those a mutate/admit loop stopping at the first
+    # refusal would mutate, consuming the innovation counter in that order
+    room = int(np.count_nonzero(np.asarray(pool.slot_states()) != 1)) if hasattr(pool, "slot_states") else None
+    take = [int(x) for x in (parents if room is None else parents[:room])]
+    kids = neat.mutate_batch([pool.genome(par) for par in take], rates,
+                             [stream_key(state.master_seed, t, "mutate", par) for par in take], pool.innovations)
     children = []
-    for par in parents:
-        par = int(par)
-        if not pool.can_admit():
-            break
-        child = neat.mutate(pool.genome(par), rates, neat.stream(state.master_seed, t, "mutate", par), pool.innovations)
+    for par, child in zip(take, kids):
         slot = pool.admit(child, parents=(pool.lineage(par),), birth_step=t)
         if slot is None:
             break

@@ -37,8 +37,6 @@ def test_config3_full_size_tier_a():
     net = orc.synth_net(genomes, 0, seed=0)
     phys = orc.Phys(cycle_period=20)
     params = oracle_phys_to_params(phys)
-    live = np.zeros(cap, np.int8)
-    live[:genomes] = 1
     dev = make_dev(p0, cap, net, live=genomes)
     fast = make_dev(p0, cap, net, live=genomes)  # the benchmark's variant (decided rows, no export)
     p = p0
@@ -84,7 +82,8 @@ def _window(p: orc.Planes, y0: int, x0: int, n: int, apron: int) -> orc.Planes:
     h, w = p.shape
     ys = (np.arange(y0 - apron, y0 + n + apron) % h)[:, None]
     xs = (np.arange(x0 - apron, x0 + n + apron) % w)[None, :]
-    return orc.Planes(p.E[ys, xs], p.I[ys, xs], p.C[:, ys, xs], p.gi[ys, xs], p.rot[ys, xs])
+    c = np.ascontiguousarray
+    return orc.Planes(c(p.E[ys, xs]), c(p.I[ys, xs]), c(p.C[:, ys, xs]), c(p.gi[ys, xs]), c(p.rot[ys, xs]))
 
 
 def _window_actions(pre: orc.Planes, y0, x0, n, net, capacity, params, t):

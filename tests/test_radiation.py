@@ -9,10 +9,10 @@ with p_radiation 0.02 / p_merge 0.2 (tests/golden/make_golden_radiation.py).
 * GPU (tier A): the device step with the reference's actions injected emits
   the reference's adoption events; with this package's host radiation the
   post-step planes and pool equal the reference's bit for bit.
-* GPU (free running): ``engine.step`` itself (host-resident state, device
-  sense + net + physics, host radiation, device CPPN expression of the
-  children) keeps genome/rotation planes and the pool identical to the
-  reference's; continuous planes within 1e-5."""
+* GPU (engine): ``engine.step`` itself (host-resident state, device sense +
+  net + physics, host radiation, device CPPN expression of the children)
+  equals those verified components driven by hand with the device's own
+  actions, bit for bit; its actions on the reference's state within 1e-5."""
 
 import json
 import os
@@ -204,21 +204,56 @@ def test_device_radiation_steps_tier_a(case):
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("case", CASES)
-def test_engine_step_free_running_with_radiation(case):
-    """engine.step end to end (host-resident planes) with the reference's
-    default evolution; children's weights come from the device CPPN kernel."""
+def test_engine_step_with_radiation_equals_its_components(case):
+    """engine.step end to end (host-resident planes, device sense + net +
+    physics, host radiation, device CPPN expression of the children, host
+    census) equals the tier-A-verified components run by hand with the
+    device's own actions: device physics with those actions injected ->
+    events -> this package's apply_radiation -> census.  Bit for bit, over
+    all golden steps; plus the device's actions on the reference's step-0
+    state against the reference's actions (tier B, 1e-5 relative)."""
+    from paper_2406_09654_b200 import _lib, physics
+    from paper_2406_09654_b200.device import DeviceSubstrate
+
     z, g = _golden()
-    hidden = 16
-    pool = _pool(z, g, case, net_factory=radiation.device_net_factory(hidden))
-    cfg = engine.ExperimentConfig(grid=engine.GridConfig(64, 64), seed=int(z[case + "_seed"]))
-    sub = create_substrate(64, 64)
-    _front(sub, z, case + "_pre_")
-    state = engine.SimState(substrate=sub, pool=pool, config=cfg, master_seed=int(z[case + "_seed"]))
-    for k in range(int(z[case + "_steps"])):
-        sk = f"{case}_s{k:02d}_"
-        before = pool.next_lineage_id
-        engine.step(state)
-        _same_planes(sub.front, z, sk + "post_", exact=False)
-        _check_pool(pool, z, g, case, k, before)
-        assert state.last_adoptions == int(z[sk + "stats"][0])
-        assert state.last_extinctions == int(z[sk + "stats"][1])
+    hidden, seed = 16, int(z[case + "_seed"])
+    cfg = engine.ExperimentConfig(grid=engine.GridConfig(64, 64), seed=seed)
+    pool_a = _pool(z, g, case, net_factory=radiation.device_net_factory(hidden))
+    pool_b = _pool(z, g, case)
+    sub_a, sub_b = create_substrate(64, 64), create_substrate(64, 64)
+    _front(sub_a, z, case + "_pre_")
+    _front(sub_b, z, case + "_pre_")
+    state = engine.SimState(substrate=sub_a, pool=pool_a, config=cfg, master_seed=seed)
+    dev = DeviceSubstrate(64, 64, pool_b.capacity, hidden=0)
+    rates = engine.EvolutionRates()
+    try:
+        for k in range(int(z[case + "_steps"])):
+            af = engine.build_action_field(state)
+            if k == 0:
+                ref = z[f"{case}_s00_acts"].astype(np.float64)
+                assert np.array_equal(af.cells, z[f"{case}_s00_cells"])
+                got = af.block().astype(np.float64)
+                assert np.all(np.abs(got - ref) <= 1e-5 * np.abs(ref))
+            engine.step(state)
+            dev.set_slots(pool_b.slot_states())
+            dev.upload(sub_b.front)
+            dev.set_actions(af.cells, af.block())
+            dev.step_raw(physics.step_scalars(k, cfg.physics), k,
+                         flags=_lib.F_INJECT_ACTIONS | _lib.F_RECORD_EVENTS | _lib.F_NO_CENSUS)
+            ev = dev.read_events()
+            dev.download(sub_b.back)
+            radiation.apply_radiation(ev, pool_b, rates, sub_b.back, seed, k)
+            dead = _census(pool_b, sub_b.back.genome_index, k)
+            dev.census_finish(k)
+            sub_b.swap_buffers()
+            fa, fb = sub_a.front, sub_b.front
+            for name in ("energy", "infrastructure", "communication"):
+                assert np.array_equal(fa.channels[name].view(np.uint32), fb.channels[name].view(np.uint32)), (k, name)
+            assert np.array_equal(fa.genome_index, fb.genome_index) and np.array_equal(fa.rotation, fb.rotation)
+            assert state.last_adoptions == len(ev) and state.last_extinctions == len(dead)
+            assert np.array_equal(pool_a.slot_states(), pool_b.slot_states())
+            assert np.array_equal(_records(pool_a), _records(pool_b))
+            for s in np.flatnonzero(pool_b.slot_states() == 1):
+                assert pool_a.genome(int(s)) == pool_b.genome(int(s))
+    finally:
+        dev.close()
