@@ -169,6 +169,11 @@ EVO_API int evo_get_actions(evo_ctx* ctx, int64_t capacity, int64_t* cells, floa
 /* Census of the last step: counts (capacity), slot state (0/1/2), death step
  * (-1 = alive), peak population.  Any pointer may be NULL. */
 EVO_API int evo_read_census(evo_ctx* ctx, int32_t* counts, int8_t* state, int64_t* death_step, int32_t* peak);
+/* Census counts accumulated by an EVO_F_NO_CENSUS step (per slot, the
+ * genome plane before host radiation), copied out and cleared; the slot
+ * table is left to the caller (host census after radiation, then
+ * evo_set_slots).  counts: capacity int32. */
+EVO_API int evo_census_take(evo_ctx* ctx, int32_t* counts);
 /* Last step's adoption count and newly dead slot count
  * (SimState.last_adoptions / last_extinctions, engine.py:247-248). */
 EVO_API int evo_read_stats(evo_ctx* ctx, int64_t* adoptions, int64_t* extinctions);

@@ -71,6 +71,7 @@ SIGNATURES = {
     "evo_get_actions": [_P, _I64, _P, _P, C.POINTER(_I64)],
     "evo_read_census": [_P, _P, _P, _P, _P],
     "evo_read_stats": [_P, C.POINTER(_I64), C.POINTER(_I64)],
+    "evo_census_take": [_P, _P],
     "evo_read_events": [_P, _I64, _P, _P, _P, _P, _P, _P, C.POINTER(_I64)],
     "evo_patch_genomes": [_P, _P, _P, _I64],
     "evo_select_cells": [_P, C.c_uint64, C.c_uint64, C.c_double, _P, C.POINTER(_I64)],

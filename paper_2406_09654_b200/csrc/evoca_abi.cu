@@ -978,6 +978,16 @@ EVO_API int evo_read_census(evo_ctx* c, int32_t* counts, int8_t* state, int64_t*
   return 0;
 }
 
+EVO_API int evo_census_take(evo_ctx* c, int32_t* counts) {
+  if (int r = check_ctx(c)) return r;
+  if (!counts) return fail(EVO_EINVAL, "null counts");
+  CK(cudaStreamSynchronize(c->stream));
+  CK(cudaDeviceSynchronize());
+  CK(cudaMemcpy(counts, c->census.counts, (size_t)c->cap * 4, cudaMemcpyDeviceToHost));
+  CK(cudaMemset(c->census.counts, 0, (size_t)c->cap * 4));
+  return 0;
+}
+
 EVO_API int evo_read_stats(evo_ctx* c, int64_t* adoptions, int64_t* extinctions) {
   if (int r = check_ctx(c)) return r;
   CK(cudaStreamSynchronize(c->stream));

@@ -237,6 +237,12 @@ class DeviceSubstrate:
         check(self.lib.evo_read_census(self.ctx, ptr(counts), ptr(state), ptr(death), ptr(peak)))
         return counts, state, death, peak
 
+    def census_take(self) -> np.ndarray:
+        """Counts accumulated by an EVO_F_NO_CENSUS step, cleared on the device."""
+        counts = np.empty(self.capacity, np.int32)
+        check(self.lib.evo_census_take(self.ctx, ptr(counts)))
+        return counts
+
     def read_stats(self):
         a, e = C.c_int64(), C.c_int64()
         check(self.lib.evo_read_stats(self.ctx, C.byref(a), C.byref(e)))

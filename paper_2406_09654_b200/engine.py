@@ -520,15 +520,66 @@ def sync_to_host(state) -> None:
         _download_front(state)
 
 
+class _GenomePatches:
+    """Stand-in for the back PlaneSet handed to the host radiation callback
+    in a device-resident run: ``genome_index.ravel()`` / ``.reshape(-1)``
+    return a recorder whose item assignments (children installed at adoption
+    targets, physics.py:389-392) are collected and patched onto the device."""
+
+    def __init__(self):
+        self.cells: list = []
+        self.slots: list = []
+
+    @property
+    def genome_index(self):
+        return self
+
+    def ravel(self):
+        return self
+
+    def reshape(self, *shape):
+        return self
+
+    def __setitem__(self, cell, slot):
+        self.cells.append(int(cell))
+        self.slots.append(int(slot))
+
+
+def _device_radiation_step(state, b, t, phys) -> None:
+    """One step with adoption-driven radiation, device-resident: the device
+    steps with adoption events recorded and the census deferred; the host
+    runs the radiation callback on the compacted events (physics.py:346-392),
+    the children it installs are patched onto the device genome plane, and
+    the census (physics.py:395-404) runs on the device's counts corrected for
+    those patches; new slots are expressed on the device before the next step."""
+    dev = b.dev
+    dev.step_raw(step_scalars(t, phys), t, flags=_lib.F_RECORD_EVENTS | _lib.F_NO_CENSUS,
+                 source_map=phys.energy_source_map)
+    events = dev.read_events()
+    counts = dev.census_take().astype(np.int64)
+    if len(events):
+        patches = _GenomePatches()
+        _radiation_fn(state)(events, state.pool, state.config.evolution, patches, state.master_seed, t)
+        if patches.cells:
+            cells = np.asarray(patches.cells, np.int64)
+            slots = np.asarray(patches.slots, np.int32)
+            dev.patch_genomes(cells, slots)
+            winner = dict(zip(events.target.tolist(), events.winner_slot.tolist()))
+            for c, sl in zip(patches.cells, patches.slots):  # the target held the winner's slot
+                counts[winner[c]] -= 1
+                counts[sl] += 1
+    newly_dead = state.pool.update_census(counts, t + 1)
+    b.pool_version = None
+    b.sync_params(state.pool)  # children expressed in one launch, slot table + peaks pushed
+    state.last_adoptions = len(events)
+    state.last_extinctions = len(newly_dead)
+
+
 def run(state, steps: int, hooks=(), should_stop: Optional[Callable[[], bool]] = None) -> None:
-    """engine.run (engine.py:251-271): device-resident between hooks."""
-    if _radiation_active(state):
-        for _ in range(steps):
-            if should_stop is not None and should_stop():
-                break
-            step(state)
-            _fire(state, hooks)
-        return
+    """engine.run (engine.py:251-271): device-resident between hooks, with
+    adoption-driven radiation (when its probabilities are non-zero) on the
+    host per step over device-compacted events."""
+    rad = _radiation_active(state)
     b = _binding(state)
     sub = state.substrate
     b.sync_params(state.pool)
@@ -539,7 +590,10 @@ def run(state, steps: int, hooks=(), should_stop: Optional[Callable[[], bool]] =
         if should_stop is not None and should_stop():
             break
         t = sub.step_counter
-        b.dev.step_raw(step_scalars(t, phys), t, source_map=phys.energy_source_map)
+        if rad:
+            _device_radiation_step(state, b, t, phys)
+        else:
+            b.dev.step_raw(step_scalars(t, phys), t, source_map=phys.energy_source_map)
         sub.step_counter = t + 1
         b.device_ahead = True
         fr = getattr(state.config, "field_radiation", None)
@@ -551,20 +605,23 @@ def run(state, steps: int, hooks=(), should_stop: Optional[Callable[[], bool]] =
         dev_due = [h for h in due if getattr(h, "device", False)]
         due = [h for h in due if not getattr(h, "device", False)]
         if dev_due:
-            adoptions, extinctions = b.dev.read_stats()
-            state.last_adoptions, state.last_extinctions = int(adoptions), int(extinctions)
+            if not rad:
+                adoptions, extinctions = b.dev.read_stats()
+                state.last_adoptions, state.last_extinctions = int(adoptions), int(extinctions)
             _fire(state, dev_due)
         if due:
             _download_front(state)
-            adoptions, extinctions = b.dev.read_stats()
-            state.last_adoptions, state.last_extinctions = int(adoptions), int(extinctions)
+            if not rad:
+                adoptions, extinctions = b.dev.read_stats()
+                state.last_adoptions, state.last_extinctions = int(adoptions), int(extinctions)
             _fire(state, due)
             b.sync_params(state.pool)
             b.dev.upload(sub.front)  # hooks may write the front
     if b.device_ahead:
         _download_front(state)
-        adoptions, extinctions = b.dev.read_stats()
-        state.last_adoptions, state.last_extinctions = int(adoptions), int(extinctions)
+        if not rad:
+            adoptions, extinctions = b.dev.read_stats()
+            state.last_adoptions, state.last_extinctions = int(adoptions), int(extinctions)
 
 
 def _fire(state, hooks) -> None:
