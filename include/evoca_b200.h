@@ -51,6 +51,8 @@ extern "C" {
 #define EVO_F_CUDA_CORE_NET 16  /* hidden-layer nets: per-cell CUDA-core FP32 forward instead of the tcgen05 path */
 #define EVO_F_TILE_NET 32       /* direct nets of pools > 68 slots: per-tile kernel instead of genome-sorted rows */
 #define EVO_F_MMA_NET 64        /* direct nets of pools <= 64 slots: mma.sync 3xTF32 tile kernel (measured slower; A/B) */
+#define EVO_F_TC_NET 128        /* hidden layers narrower than 64: tcgen05 3xTF32 net instead of FP32 CUDA cores */
+#define EVO_F_SHARD_NET 256     /* direct nets of pools > 68 slots: cluster-sharded tile kernel (measured slower; A/B) */
 
 /* Host-computed per-step scalars, exactly as the reference derives them:
  * rho = A*sin(2*pi*t/P) in float64 (physics.py:186); rho_mode 1 if rho > 0,

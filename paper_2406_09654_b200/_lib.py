@@ -20,6 +20,8 @@ EVO_EINVAL = -1
 PH_ENERGY, PH_INVEST, PH_COMM, PH_EXPLORE, PH_ALL = 1, 2, 4, 8, 15
 F_INJECT_ACTIONS, F_EXPORT_ACTIONS, F_RECORD_EVENTS, F_NO_CENSUS, F_CUDA_CORE_NET, F_TILE_NET = 1, 2, 4, 8, 16, 32
 F_MMA_NET = 64  # direct nets of pools <= 64 slots: mma.sync 3xTF32 tile kernel (measured slower; A/B only)
+F_TC_NET = 128  # hidden layers narrower than 64 on the tensor cores (default: FP32 CUDA cores)
+F_SHARD_NET = 256  # large direct pools: cluster-sharded tile kernel (measured slower than the rows path; A/B)
 
 
 class EvoScalars(C.Structure):

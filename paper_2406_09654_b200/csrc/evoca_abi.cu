@@ -51,6 +51,14 @@ struct evo_ctx {
   // pass 1 after any weight write
   float* wF = nullptr;
   bool frag_stale = true;
+  // cluster-sharded pass 1 (evoca_shard.cu): slot -> (shard, local) map and
+  // per-shard weight tables, rebuilt on the stream when the pool changed
+  int* shard_map = nullptr;
+  int* shard_res = nullptr;
+  float* shard_tables = nullptr;
+  bool shard_stale = true;
+  int shard_q = 0;
+  int live = 0;  // live slots at the last evo_set_slots
   evo::Census census = {};
   float* act_in = nullptr;
   uint8_t* act_in_flag = nullptr;
@@ -337,14 +345,24 @@ int pass1_view(evo_ctx* c, const View& v, const evo_scalars* s, int phases, int 
   bool exp = (flags & EVO_F_EXPORT_ACTIONS) && !inject;
   if (inject && !c->act_in) return fail(EVO_EINVAL, "EVO_F_INJECT_ACTIONS without evo_set_actions");
   if ((inject || exp) && v.off != 0) return fail(EVO_EINVAL, "action injection/export needs a whole-strip pass");
-  // hidden-layer nets run on the tensor cores (sense -> genome buckets ->
-  // tcgen05 3xTF32 MLP -> actuator rows), the physics as pass 1 with those rows
+  // wide hidden layers run on the tensor cores (sense -> genome buckets ->
+  // tcgen05 3xTF32 MLP -> actuator rows), the physics as pass 1 with those
+  // rows; narrow ones (the reference's default 16) stay on the CUDA cores in
+  // fixed-order FP32 - 3xTF32 is ~2^-21 relative per product, which exceeds
+  // the 1e-5 action tolerance when CPPN weights reach w_max = 3
+  // (tests/test_radiation.py), and a 45x16 layer is not dense enough to pay
   const bool tc_net = !inject && c->hidden > 0 && evo::hidden_tc_supported(c->hidden) &&
-                      !(flags & EVO_F_CUDA_CORE_NET);
+                      !(flags & EVO_F_CUDA_CORE_NET) &&
+                      (c->hidden >= evo::kTcMinHidden || (flags & EVO_F_TC_NET));
   // direct nets of large pools (weights do not fit next to the tile in shared
-  // memory): genome-sorted rows instead of per-tile weight fetches
-  const bool rows_net = !inject && c->hidden == 0 && c->cap > evo::kSmemWeightSlotsAbi &&
+  // memory): genome-sorted sensor rows; EVO_F_SHARD_NET selects the measured
+  // alternative that shards the weight table over a thread-block cluster
+  // working on one tile (evoca_shard.cu: 4.7 ms against 2.4 ms per config-3
+  // step - each CTA sees ~256 cells of a tile, too few to hide its latency)
+  const bool big_pool = !inject && c->hidden == 0 && c->cap > evo::kSmemWeightSlotsAbi &&
                         !(flags & EVO_F_TILE_NET);
+  const bool shard_net = big_pool && !exp && (flags & EVO_F_SHARD_NET) && c->live <= evo::kShardMaxLive;
+  const bool rows_net = big_pool && !shard_net;
   if (exp && !tc_net && !rows_net) {
     if (int r = ensure_actions_out(c)) return r;
   }
@@ -387,6 +405,24 @@ int pass1_view(evo_ctx* c, const View& v, const evo_scalars* s, int phases, int 
   a.act_out_flag = c->act_out_flag;
   a.capacity = c->cap;
   a.stats = stats;
+  if (shard_net) {
+    const int Q = std::min(evo::kShardMaxQ, std::max(2, (std::min(c->live, evo::kShardMaxQ * evo::kShardSlots) +
+                                                         evo::kShardSlots - 1) / evo::kShardSlots));
+    if (!c->num_sms) CK(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, c->device));
+    if (!c->shard_map) {
+      CK(c->alloc(&c->shard_map, (size_t)c->cap));
+      CK(c->alloc(&c->shard_res, (size_t)evo::kShardMaxQ * evo::kShardSlots));
+      CK(c->alloc(&c->shard_tables, (size_t)evo::kShardMaxQ * evo::kShardFloats));
+    }
+    if (c->shard_stale || Q != c->shard_q) {
+      CK(evo::launch_shard_plan(c->census.state, c->cap, Q, c->shard_map, c->shard_res, c->params(),
+                                c->shard_tables, st));
+      c->shard_stale = false;
+      c->shard_q = Q;
+    }
+    CK(evo::launch_pass1_shard(a, c->shard_map, c->shard_tables, Q, c->num_sms, st));
+    return 0;
+  }
   CK(evo::launch_pass1(a, inject || via_rows, exp && !via_rows, st));
   return 0;
 }
@@ -516,6 +552,7 @@ EVO_API int evo_set_params(evo_ctx* c, int slot0, int n, const float* w1, const 
     CK(cudaMemcpy(c->wB + (size_t)slot0 * evo::kSensors, w1.data(), w1.size() * 4, cudaMemcpyHostToDevice));
     CK(cudaMemcpy(c->bA + (size_t)slot0 * evo::kOutPad, bt.data(), bt.size() * 4, cudaMemcpyHostToDevice));
     c->frag_stale = true;
+    c->shard_stale = true;
     return 0;
   }
   const int hp = c->hpad;
@@ -585,6 +622,8 @@ EVO_API int evo_set_slots(evo_ctx* c, const int8_t* state, const int32_t* peak) 
   CK(cudaStreamSynchronize(c->stream));
   if (state) {
     CK(cudaMemcpy(c->census.state, state, (size_t)c->cap, cudaMemcpyHostToDevice));
+    c->live = (int)std::count(state, state + c->cap, (int8_t)1);
+    c->shard_stale = true;
     std::vector<int64_t> ds((size_t)c->cap, -1);
     CK(cudaMemcpy(c->census.death_step, ds.data(), ds.size() * 8, cudaMemcpyHostToDevice));
   }
@@ -1129,6 +1168,8 @@ EVO_API int evo_express_cppn(evo_ctx* c, int n, const int32_t* slots, const int3
   put(coords, (size_t)ncoord * 8);
   cudaError_t e = cudaMemcpyAsync(dbuf, h.data(), h.size(), cudaMemcpyHostToDevice, st);
   if (e == cudaSuccess) e = evo::launch_express_cppn(b, c->params(), c->wA, c->bA, c->wB, c->bB, st);
+  c->frag_stale = true;
+  c->shard_stale = true;
   c->frag_stale = true;
   if (e == cudaSuccess) e = cudaStreamSynchronize(st);
   cudaFree(dbuf);

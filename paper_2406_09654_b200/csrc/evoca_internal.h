@@ -21,6 +21,12 @@ constexpr int kActuators = 13;
 constexpr int kOutPad = 16;              // 13 actuators padded to 4 float4
 constexpr int kMaxCapacity = 8192;       // device census bins per CTA (smem)
 constexpr int kSmemWeightSlotsAbi = 68;  // largest pool the tile kernel keeps in shared memory
+constexpr int kTcMinHidden = 64;
+// Cluster-sharded pass 1 (evoca_shard.cu): 64 resident genomes per CTA.
+constexpr int kShardSlots = 64;
+constexpr int kShardFloats = kShardSlots * kSensors * 12 + ((kShardSlots * kSensors + 3) & ~3) + kShardSlots * kOutPad;
+constexpr int kShardMaxQ = 4;
+constexpr int kShardMaxLive = 768;       // larger live pools take the genome-sorted rows path         // narrowest hidden layer run on the tensor cores by default
 // Tensor-core direct net (k_pass1_mma): per-genome weights in mma.sync A-fragment
 // order, 6 K-steps x (lanes 0-19: 4 floats, lanes 20-31: 2 floats) + bias[16].
 constexpr int kMmaSlots = 64;            // largest pool k_pass1_mma keeps in shared memory
@@ -167,6 +173,11 @@ cudaError_t launch_express_cppn(const CppnBatch& b, const Params& net, float* wA
 cudaError_t launch_pass1(const Pass1Args& a, bool inject, bool export_actions, cudaStream_t st);
 cudaError_t launch_frag_relayout(const Params& net, int capacity, float* wF, cudaStream_t st);
 cudaError_t launch_pass2(const Pass2Args& a, cudaStream_t st);
+size_t shard_smem_bytes(int Q);
+cudaError_t launch_shard_plan(const int8_t* state, int cap, int Q, int* map, int* resident, const Params& net,
+                              float* tables, cudaStream_t st);
+cudaError_t launch_pass1_shard(const Pass1Args& a, const int* map, const float* tables, int Q, int num_sms,
+                               cudaStream_t st);
 cudaError_t debug_phase_cycles(unsigned long long* out, bool reset);
 cudaError_t debug_hidden_cycles(unsigned long long* out, bool reset);
 cudaError_t launch_census_finish(const Census& c, int capacity, long long t, cudaStream_t st,

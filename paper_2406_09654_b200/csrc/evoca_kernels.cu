@@ -33,7 +33,7 @@
 
 #include <algorithm>
 
-#include "evoca_net.cuh"
+#include "evoca_tile.cuh"
 
 namespace evo {
 
@@ -147,17 +147,6 @@ __global__ void __launch_bounds__(256) k_physics_rows(const Pass1Args a) {
                        (int)__ldg(a.front.rot + o)};
     store_pass1(a, y, x, cell_physics(a.s, a.phases, a.src_map, c, cs, row_actions(a, __ldg(a.act_rank + c))));
   }
-}
-
-// Halo cell i of the tile at (x0, y0): global plane offset (rows -1..H exist).
-__device__ __forceinline__ unsigned halo_src(const StepGeom& g, int x0, int y0, int i) {
-  const int hy = i / kHaloW, hx = i - hy * kHaloW;
-  int y = y0 + hy - 1;
-  if (y > g.H) y = g.H;  // beyond a partial tile: never read
-  int x = x0 + hx - 1;
-  x = x < 0 ? x + g.W : (x >= g.W ? x - g.W : x);
-  if (x >= g.W) x = g.W - 1;
-  return (unsigned)((y + 1) * g.W + x);
 }
 
 // Physics tail of one tile in spatial order (shared by both pass-1 kernels).
@@ -359,107 +348,7 @@ struct DirectSmem {
   int bins[1];  // capacity ints (dynamic tail)
 };
 
-template <int THREADS>
-struct PrefetchT {
-  static constexpr int kHalo = (kHaloCells + THREADS - 1) / THREADS;
-  static constexpr int kCells = (kTileCells + THREADS - 1) / THREADS;
-  float v[kHalo][5];
-  int gi[kCells];
-  int rot[kCells];
-};
 using Prefetch = PrefetchT<kThreadsP>;
-
-template <int THREADS>
-__device__ __forceinline__ void prefetch_tile(const Pass1Args& a, int tile, int tiles_x, PrefetchT<THREADS>& pf) {
-  constexpr int kPreHalo = PrefetchT<THREADS>::kHalo, kPreCells = PrefetchT<THREADS>::kCells;
-  const StepGeom& g = a.g;
-  const int tid = threadIdx.x;
-  const int x0 = (tile % tiles_x) * kTileW;
-  const int y0 = (tile / tiles_x) * kTileH;
-  const unsigned st = (unsigned)g.stride;
-#pragma unroll
-  for (int j = 0; j < kPreHalo; ++j) {
-    const int i = tid + j * THREADS;
-    if (i < kHaloCells) {
-      const unsigned o = halo_src(g, x0, y0, i);
-      pf.v[j][0] = ld_na(a.front.E + o);
-      pf.v[j][1] = ld_na(a.front.I + o);
-      pf.v[j][2] = ld_na(a.front.C + o);
-      pf.v[j][3] = ld_na(a.front.C + st + o);
-      pf.v[j][4] = ld_na(a.front.C + 2 * st + o);
-    }
-  }
-#pragma unroll
-  for (int j = 0; j < kPreCells; ++j) {
-    const int i = tid + j * THREADS;
-    const int ty = i / kTileW, tx = i - ty * kTileW;
-    const int y = y0 + ty, x = x0 + tx;
-    const bool in = (i < kTileCells) && (y < g.H) && (x < g.W);
-    const unsigned o = in ? (unsigned)((y + 1) * g.W + x) : 0u;
-    pf.gi[j] = in ? __ldg(a.front.gi + o) : -1;
-    pf.rot[j] = in ? (int)__ldg(a.front.rot + o) : 0;
-  }
-}
-
-template <int THREADS, typename SM>
-__device__ __forceinline__ void commit_tile(SM& sm, const PrefetchT<THREADS>& pf) {
-  constexpr int kPreHalo = PrefetchT<THREADS>::kHalo, kPreCells = PrefetchT<THREADS>::kCells;
-  const int tid = threadIdx.x;
-#pragma unroll
-  for (int j = 0; j < kPreHalo; ++j) {
-    const int i = tid + j * THREADS;
-    if (i < kHaloCells) {
-      sm.eic[i] = make_float4(pf.v[j][0], pf.v[j][1], pf.v[j][2], pf.v[j][3]);
-      sm.c2[i] = pf.v[j][4];
-    }
-  }
-#pragma unroll
-  for (int j = 0; j < kPreCells; ++j) {
-    const int i = tid + j * THREADS;
-    if (i < kTileCells) {
-      sm.gi[i] = pf.gi[j];
-      sm.rot[i] = (uint8_t)pf.rot[j];
-    }
-  }
-}
-
-// L2 prefetch of a tile's halo rows (5 planes) and interior genome/rotation
-// rows: no registers, issued a whole tile ahead of the register loads.
-template <int THREADS = kThreadsP>
-__device__ __forceinline__ void prefetch_tile_l2(const Pass1Args& a, int tile, int tiles_x) {
-  const StepGeom& g = a.g;
-  const int x0 = (tile % tiles_x) * kTileW;
-  const int y0 = (tile / tiles_x) * kTileH;
-  // per plane row: [x0-1, x0+33) -> at most 2 x 128-byte lines (floats)
-  constexpr int kLines = kHaloH * 2;  // per float plane
-  for (int i = threadIdx.x; i < kLines * 5 + kTileH * 2; i += THREADS) {
-    const char* p;
-    if (i < kLines * 5) {
-      const int plane = i / kLines, r = (i - plane * kLines) >> 1, half = i & 1;
-      int y = y0 + r - 1;
-      if (y > g.H) y = g.H;
-      int x = x0 - 1 + half * 32;
-      x = x < 0 ? 0 : (x >= g.W ? g.W - 1 : x);
-      const float* base = plane == 0 ? a.front.E : (plane == 1 ? a.front.I : a.front.C + (plane - 2) * g.stride);
-      p = reinterpret_cast<const char*>(base + (unsigned)((y + 1) * g.W + x));
-    } else {
-      const int j = i - kLines * 5, r = j >> 1;
-      int y = y0 + r;
-      if (y >= g.H) y = g.H - 1;
-      p = (j & 1) ? reinterpret_cast<const char*>(a.front.rot + (unsigned)((y + 1) * g.W + x0))
-                  : reinterpret_cast<const char*>(a.front.gi + (unsigned)((y + 1) * g.W + x0));
-    }
-    asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
-  }
-}
-
-// Asynchronous copy of the slot weight tables into shared memory (16-byte cp.async).
-template <int THREADS = kThreadsP>
-__device__ __forceinline__ void stage_weights(float* dst, const float* src, int nfloats) {
-  const unsigned sbase = (unsigned)__cvta_generic_to_shared(dst);
-  for (int i = threadIdx.x * 4; i < nfloats; i += THREADS * 4)
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sbase + i * 4), "l"(src + i));
-}
 
 template <bool kExport, bool kSmemW>
 __global__ void __launch_bounds__(kThreadsP, 1) k_pass1_direct(const Pass1Args a) {
@@ -480,9 +369,9 @@ __global__ void __launch_bounds__(kThreadsP, 1) k_pass1_direct(const Pass1Args a
     sW12 = reinterpret_cast<float*>(smem_raw + off);
     sW1 = sW12 + (size_t)a.capacity * kSensors * 12;
     sB = sW1 + (((size_t)a.capacity * kSensors + 3) & ~(size_t)3);
-    stage_weights(sW12, a.net.wA, a.capacity * kSensors * 12);
-    stage_weights(sW1, a.net.wB, (a.capacity * kSensors + 3) & ~3);
-    stage_weights(sB, a.net.bA, a.capacity * kOutPad);
+    stage_weights<kThreadsP>(sW12, a.net.wA, a.capacity * kSensors * 12);
+    stage_weights<kThreadsP>(sW1, a.net.wB, (a.capacity * kSensors + 3) & ~3);
+    stage_weights<kThreadsP>(sB, a.net.bA, a.capacity * kOutPad);
     asm volatile("cp.async.commit_group;" ::: "memory");
   }
   fill_slot_offsets(sm.slot_off);
@@ -509,7 +398,7 @@ __global__ void __launch_bounds__(kThreadsP, 1) k_pass1_direct(const Pass1Args a
     const int x0 = (tile % tiles_x) * kTileW;
     const int y0 = (tile / tiles_x) * kTileH;
     const int next = tile + gridDim.x;
-    if (next < ntiles) prefetch_tile_l2(a, next, tiles_x);
+    if (next < ntiles) prefetch_tile_l2<kThreadsP>(a, next, tiles_x);
     for (int b = threadIdx.x; b < a.capacity; b += kThreadsP) sm.bins[b] = 0;  // for the next count
     if (kSmemW && tile == (int)blockIdx.x) {  // weight staging overlapped the first halo load + bucketing
       asm volatile("cp.async.wait_all;" ::: "memory");

@@ -26,7 +26,7 @@ from dataclasses import dataclass
 
 import numpy as np
 
-__all__ = ["StripPlan", "HaloComm", "DeviceStrip", "cuda_view"]
+__all__ = ["StripPlan", "HaloComm", "StagedHaloComm", "DeviceStrip", "cuda_view"]
 
 
 @dataclass(frozen=True)
@@ -93,6 +93,34 @@ class HaloComm:
         import torch.distributed as dist
 
         dist.all_reduce(t, op=dist.ReduceOp.SUM, group=self.group)
+
+
+class StagedHaloComm(HaloComm):
+    """HaloComm over a host-side process group (gloo): device rows are staged
+    through host memory around each exchange and reduction.  For runs whose
+    ranks share a GPU or have no NCCL (tests, CPU-only launchers); the
+    exchange pattern and results are those of the device path."""
+
+    def exchange(self, first, last, ghost_top, ghost_bottom) -> None:
+        if not first.is_cuda:
+            return super().exchange(first, last, ghost_top, ghost_bottom)
+        import torch
+
+        torch.cuda.current_stream().synchronize()
+        gt, gb = ghost_top.cpu(), ghost_bottom.cpu()
+        super().exchange(first.cpu(), last.cpu(), gt, gb)
+        ghost_top.copy_(gt)
+        ghost_bottom.copy_(gb)
+
+    def sum_(self, t) -> None:
+        if not t.is_cuda:
+            return super().sum_(t)
+        import torch
+
+        torch.cuda.current_stream().synchronize()
+        h = t.cpu()
+        super().sum_(h)
+        t.copy_(h)
 
 
 class _CudaArray:

@@ -473,7 +473,7 @@ def test_tensor_core_net_vs_oracle_and_cuda_core(hidden, genomes, shape):
     params = oracle_phys_to_params(phys)
     oa = orc.act(p0, net)
     dev = make_dev(p0, genomes, net)
-    cells, acts = _actions(dev, 0, params)
+    cells, acts = _actions(dev, 0, params, _lib.F_TC_NET)  # tensor cores at every hidden width
     assert np.array_equal(cells, oa.cells)
     assert rel_err(acts, oa.a) <= TOL
     ref = orc.step(p0, 0, net, phys, acts=orc.Actions(cells, acts))
@@ -575,3 +575,39 @@ def test_mma_direct_net_follows_parameter_updates():
     oa = orc.act(p0, net_b)
     assert np.array_equal(cells, oa.cells) and rel_err(acts, oa.a) <= TOL
     dev.close()
+
+
+@pytest.mark.parametrize("genomes,live,shape", [(100, 100, (64, 64)), (200, 200, (96, 80)), (300, 300, (70, 35)),
+                                                (700, 400, (128, 96)), (90, 90, (1, 500))])
+def test_cluster_sharded_path_matches_rows_and_tile(genomes, live, shape):
+    """The cluster-sharded tile kernel for large direct pools (k_pass1_shard,
+    EVO_F_SHARD_NET: 64 resident genomes per CTA, records through DSMEM,
+    stragglers beyond 64 x 4 resident slots from global weights) must be
+    bit-identical to the genome-sorted rows path and the per-tile kernel,
+    including slots marked free or dead in the pool (stragglers) and partial
+    tiles."""
+    h, w = shape
+    p0 = orc.synth_planes(h, w, genomes, seed=genomes + h)
+    net = orc.synth_net(genomes, 0, seed=genomes)
+    st = np.zeros(genomes, np.int8)
+    st[:live] = 1
+    st[live:] = 2  # cells of "dead" slots: evaluated as stragglers
+    phys = orc.Phys(cycle_period=20)
+    params = oracle_phys_to_params(phys)
+    devs = []
+    for _ in range(3):
+        d = make_dev(p0, genomes, net)
+        d.set_slots(st)
+        devs.append(d)
+    a, b, c = devs
+    for t in range(3):
+        sc = physics.step_scalars(t, params)
+        a.step_raw(sc, t, flags=_lib.F_SHARD_NET)   # cluster-sharded tile kernel (A/B)
+        b.step_raw(sc, t)                           # genome-sorted rows (default for large pools)
+        c.step_raw(sc, t, flags=_lib.F_TILE_NET)    # per-tile kernel, weights from global
+        want = download(b)
+        assert download(a).equal(want), f"t={t}"
+        assert download(c).equal(want), f"t={t}"
+        assert a.read_stats()[0] == b.read_stats()[0]
+    for d in devs:
+        d.close()

@@ -103,3 +103,82 @@ def test_strips_tensor_core_hidden_net(world):
     for s in strips:
         s.dev.close()
     ref.close()
+
+
+def _rank_worker(rank, world, port, outdir, t_steps):
+    """One rank of a world-2 run: its own process and CUDA context on cuda:0,
+    DeviceStrip.step with the halo exchanges and census all_reduce going
+    through gloo (StagedHaloComm) - the rank's kernels never wait on the
+    other rank's kernels, only the host waits on the exchange."""
+    import os
+
+    import torch.distributed as dist
+
+    from paper_2406_09654_b200.strips import StagedHaloComm
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        p = orc.synth_planes(70, 48, 9, seed=21)
+        p.I[np.random.default_rng(2).random((70, 48)) < 0.4] = 0  # contention across the strip seams
+        net = orc.synth_net(9, 0, seed=21)
+        plan = StripPlan(70, 48, world)
+        s = DeviceStrip(plan, rank, net.capacity, hidden=0, device=0, comm=StagedHaloComm(rank, world))
+        s.dev.set_params(_params(net))
+        s.dev.set_slots(np.ones(net.capacity, np.int8))
+        row0, h = plan.rows(rank)
+        s.dev.upload_arrays(p.E[row0:row0 + h], p.I[row0:row0 + h], p.C[:, row0:row0 + h], p.gi[row0:row0 + h],
+                            p.rot[row0:row0 + h])
+        params = physics.PhysicsParams(cycle_period=20)
+        for t in range(t_steps):
+            s.step(physics.step_scalars(t, params), t)
+        E = np.empty((h, 48), np.float32)
+        I = np.empty((h, 48), np.float32)
+        Cm = np.empty((3, h, 48), np.float32)
+        gi = np.empty((h, 48), np.int32)
+        rot = np.empty((h, 48), np.uint8)
+        s.dev.download_arrays(E, I, Cm, gi, rot)
+        counts, state, _, _ = s.dev.read_census()
+        np.savez(os.path.join(outdir, f"r{rank}.npz"), E=E, I=I, C=Cm, gi=gi, rot=rot, counts=counts, state=state,
+                 meta=np.array([row0, h]))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_device_strips_two_processes_match_single_context():
+    """DeviceStrip.step itself with world size 2 (two processes, gloo-staged
+    exchanges) equals the single-context device step bit for bit after
+    several steps, census included."""
+    import os
+    import socket
+    import tempfile
+
+    import torch.multiprocessing as mp
+
+    sock = socket.socket()
+    sock.bind(("127.0.0.1", 0))
+    port = sock.getsockname()[1]
+    sock.close()
+    steps = 5
+    p = orc.synth_planes(70, 48, 9, seed=21)
+    p.I[np.random.default_rng(2).random((70, 48)) < 0.4] = 0
+    net = orc.synth_net(9, 0, seed=21)
+    dev = make_dev(p, 9, net)
+    params = physics.PhysicsParams(cycle_period=20)
+    for t in range(steps):
+        dev.step_raw(physics.step_scalars(t, params), t)
+    want = download(dev)
+    counts_want, state_want, _, _ = dev.read_census()
+    dev.close()
+    with tempfile.TemporaryDirectory() as d:
+        mp.spawn(_rank_worker, args=(2, port, d, steps), nprocs=2, join=True)
+        got = orc.Planes(np.empty((70, 48), np.float32), np.empty((70, 48), np.float32),
+                         np.empty((3, 70, 48), np.float32), np.empty((70, 48), np.int32), np.empty((70, 48), np.uint8))
+        for r in range(2):
+            z = np.load(os.path.join(d, f"r{r}.npz"))
+            row0, h = z["meta"].tolist()
+            got.E[row0:row0 + h], got.I[row0:row0 + h], got.C[:, row0:row0 + h] = z["E"], z["I"], z["C"]
+            got.gi[row0:row0 + h], got.rot[row0:row0 + h] = z["gi"], z["rot"]
+            assert np.array_equal(z["counts"], counts_want) and np.array_equal(z["state"], state_want)
+    assert got.equal(want)
