@@ -1360,8 +1360,16 @@ cudaError_t launch_pass1(const Pass1Args& a, bool inject, bool export_actions, c
 
 cudaError_t launch_census_finish(const Census& c, int capacity, long long t, cudaStream_t st, const int* skip);
 
+cudaError_t launch_resolve_rows(const Pass2Args& a, int num_sms, cudaStream_t st);
+
 cudaError_t launch_pass2(const Pass2Args& a_in, cudaStream_t st) {
   Pass2Args a = a_in;
+#ifdef EVO_K2_STREAM
+  // measured alternative (evoca_resolve.cu): the register-window streaming
+  // form - 9.0 warp instructions per cell against 9.6 here, 0.24 ms against
+  // 0.22 ms on config 3 and 49 us against 24 us on config 2
+  return launch_resolve_rows(a, num_sms(), st);
+#endif
 #ifdef EVO_K2_SPLIT_CENSUS
   // census epilogue as its own launch instead of the last-CTA ticket: the
   // ticket's per-CTA GPU-scope fence costs ~4 us of k_resolve, the extra

@@ -104,6 +104,32 @@ class SlotPool:
         self.version += 1
         return idx
 
+    def admit_batch(self, genomes, parents, birth_step: int = 0) -> list:
+        """``admit`` of each genome in order (same slot choice: lowest free
+        slot, then the dead slot with the oldest death step, lowest index on
+        ties; stops at the first refusal), with the slot search done once
+        for the batch.  ``parents``: one tuple per genome.  Returns the slots."""
+        free = np.flatnonzero(self._state == 0)
+        dead = np.flatnonzero(self._state == 2)
+        dead = dead[np.lexsort((dead, self._death[dead]))]
+        order = np.concatenate([free, dead])[:len(genomes)]
+        out = []
+        for idx, genome, par in zip(order.tolist(), genomes, parents):
+            params = self.net_factory(genome) if self.net_factory is not None else None
+            self._genomes[idx] = genome
+            self._params[idx] = params
+            lid = self.next_lineage_id
+            self.next_lineage_id += 1
+            self._lineage[idx] = lid
+            self.records[lid] = SlotRecord(lid, idx, birth_step, parents=tuple(par))
+            out.append(idx)
+        if out:
+            sel = np.asarray(out, np.int64)
+            self._state[sel] = 1
+            self._death[sel] = -1
+            self.version += 1
+        return out
+
     def is_live(self, slot: int) -> bool:
         return 0 <= slot < self.capacity and self._state[slot] == 1
 

@@ -156,13 +156,17 @@ def field_radiation(state, t: int, p: float = 0.01, rates: neat.EvolutionRates |
     take = [int(x) for x in (parents if room is None else parents[:room])]
     kids = neat.mutate_batch([pool.genome(par) for par in take], rates,
                              [stream_key(state.master_seed, t, "mutate", par) for par in take], pool.innovations)
-    children = []
-    for par, child in zip(take, kids):
-        slot = pool.admit(child, parents=(pool.lineage(par),), birth_step=t)
-        if slot is None:
-            break
-        slot_map[par] = slot
-        children.append(slot)
+    if hasattr(pool, "admit_batch"):
+        children = pool.admit_batch(kids, [(pool.lineage(par),) for par in take], birth_step=t)
+        slot_map[np.asarray(take[:len(children)], np.int64)] = children
+    else:
+        children = []
+        for par, child in zip(take, kids):
+            slot = pool.admit(child, parents=(pool.lineage(par),), birth_step=t)
+            if slot is None:
+                break
+            slot_map[par] = slot
+            children.append(slot)
     b.sync_params(pool)  # one batched evo_express_cppn for every new slot
     dev.remap_selected(slot_map)
     b.device_ahead = True

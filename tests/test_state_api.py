@@ -188,3 +188,30 @@ def test_device_hook_renders_without_download():
     from paper_2406_09654_b200.substrate import render_rgb
 
     assert np.array_equal(frames[-1][1], render_rgb(st.substrate).pixels)
+
+
+def test_slot_pool_admit_batch_equals_sequential_admit():
+    from paper_2406_09654_b200.pool import SlotPool
+
+    def fresh():
+        p = SlotPool(12)
+        for i in range(12):
+            p.install(i, None, birth_step=0)
+        p._state[[1, 4, 5, 9]] = 2
+        p._death[[1, 4, 5, 9]] = [7, 3, 7, 1]
+        p._state[[2, 10]] = 0
+        return p
+
+    a, b = fresh(), fresh()
+    genomes = [object() for _ in range(8)]
+    got = a.admit_batch(genomes, [(i,) for i in range(8)], birth_step=5)
+    want = []
+    for i, gnm in enumerate(genomes):
+        s = b.admit(gnm, parents=(i,), birth_step=5)
+        if s is None:
+            break
+        want.append(s)
+    assert got == want == [2, 10, 9, 4, 1, 5]
+    assert np.array_equal(a.slot_states(), b.slot_states()) and np.array_equal(a._death, b._death)
+    assert [(r.slot, r.parents, r.birth_step) for r in a.records.values()] == \
+        [(r.slot, r.parents, r.birth_step) for r in b.records.values()]
