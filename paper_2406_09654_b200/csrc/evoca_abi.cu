@@ -127,13 +127,30 @@ struct evo_ctx {
     if (e != cudaSuccess) return e;
     allocs.push_back(v);
     *p = static_cast<T*>(v);
-    return cudaMemset(v, 0, count * sizeof(T) > 0 ? count * sizeof(T) : 16);
+    // the legacy default stream does not order against the context's
+    // non-blocking streams: zero synchronously before anything can use it
+    e = cudaMemset(v, 0, count * sizeof(T) > 0 ? count * sizeof(T) : 16);
+    return e == cudaSuccess ? cudaDeviceSynchronize() : e;
   }
 };
 
 namespace {
 
 cudaStream_t pick(evo_ctx* c, void* s) { return s ? static_cast<cudaStream_t>(s) : c->stream; }
+
+// Host <-> device copies of the ABI's small tables, ordered on the context's
+// stream and complete on return.  (The legacy default stream does not order
+// against the context's non-blocking streams, and a pageable host->device
+// cudaMemcpy may return before its DMA has landed: a copy into the census
+// table raced the next step's kernels.)
+cudaError_t copy_sync(evo_ctx* c, void* dst, const void* src, size_t bytes, cudaMemcpyKind kind) {
+  cudaError_t e = cudaMemcpyAsync(dst, src, bytes, kind, c->stream);
+  return e == cudaSuccess ? cudaStreamSynchronize(c->stream) : e;
+}
+cudaError_t zero_sync(evo_ctx* c, void* dst, int value, size_t bytes) {
+  cudaError_t e = cudaMemsetAsync(dst, value, bytes, c->stream);
+  return e == cudaSuccess ? cudaStreamSynchronize(c->stream) : e;
+}
 
 int check_ctx(evo_ctx* c) {
   if (!c) return fail(EVO_EINVAL, "null context");
@@ -548,9 +565,9 @@ EVO_API int evo_set_params(evo_ctx* c, int slot0, int n, const float* w1, const 
         }
         bt[(size_t)s * evo::kOutPad + j] = b2[(size_t)s * evo::kActuators + j];
       }
-    CK(cudaMemcpy(c->wA + (size_t)slot0 * evo::kSensors * 12, w12.data(), w12.size() * 4, cudaMemcpyHostToDevice));
-    CK(cudaMemcpy(c->wB + (size_t)slot0 * evo::kSensors, w1.data(), w1.size() * 4, cudaMemcpyHostToDevice));
-    CK(cudaMemcpy(c->bA + (size_t)slot0 * evo::kOutPad, bt.data(), bt.size() * 4, cudaMemcpyHostToDevice));
+    CK(copy_sync(c, c->wA + (size_t)slot0 * evo::kSensors * 12, w12.data(), w12.size() * 4, cudaMemcpyHostToDevice));
+    CK(copy_sync(c, c->wB + (size_t)slot0 * evo::kSensors, w1.data(), w1.size() * 4, cudaMemcpyHostToDevice));
+    CK(copy_sync(c, c->bA + (size_t)slot0 * evo::kOutPad, bt.data(), bt.size() * 4, cudaMemcpyHostToDevice));
     c->frag_stale = true;
     c->shard_stale = true;
     return 0;
@@ -568,10 +585,10 @@ EVO_API int evo_set_params(evo_ctx* c, int slot0, int n, const float* w1, const 
     }
     for (int j = 0; j < evo::kActuators; ++j) B2[(size_t)s * evo::kOutPad + j] = b2[(size_t)s * evo::kActuators + j];
   }
-  CK(cudaMemcpy(c->wA + (size_t)slot0 * evo::kSensors * hp, W1.data(), W1.size() * 4, cudaMemcpyHostToDevice));
-  CK(cudaMemcpy(c->bA + (size_t)slot0 * hp, B1.data(), B1.size() * 4, cudaMemcpyHostToDevice));
-  CK(cudaMemcpy(c->wB + (size_t)slot0 * hp * evo::kOutPad, W2.data(), W2.size() * 4, cudaMemcpyHostToDevice));
-  CK(cudaMemcpy(c->bB + (size_t)slot0 * evo::kOutPad, B2.data(), B2.size() * 4, cudaMemcpyHostToDevice));
+  CK(copy_sync(c, c->wA + (size_t)slot0 * evo::kSensors * hp, W1.data(), W1.size() * 4, cudaMemcpyHostToDevice));
+  CK(copy_sync(c, c->bA + (size_t)slot0 * hp, B1.data(), B1.size() * 4, cudaMemcpyHostToDevice));
+  CK(copy_sync(c, c->wB + (size_t)slot0 * hp * evo::kOutPad, W2.data(), W2.size() * 4, cudaMemcpyHostToDevice));
+  CK(copy_sync(c, c->bB + (size_t)slot0 * evo::kOutPad, B2.data(), B2.size() * 4, cudaMemcpyHostToDevice));
   return 0;
 }
 
@@ -585,9 +602,9 @@ EVO_API int evo_get_params(evo_ctx* c, int slot0, int n, float* w1, float* b1, f
   CK(cudaStreamSynchronize(c->stream));
   if (H == 0) {
     std::vector<float> w12((size_t)n * evo::kSensors * 12), wl((size_t)n * evo::kSensors), bt((size_t)n * evo::kOutPad);
-    CK(cudaMemcpy(w12.data(), c->wA + (size_t)slot0 * evo::kSensors * 12, w12.size() * 4, cudaMemcpyDeviceToHost));
-    CK(cudaMemcpy(wl.data(), c->wB + (size_t)slot0 * evo::kSensors, wl.size() * 4, cudaMemcpyDeviceToHost));
-    CK(cudaMemcpy(bt.data(), c->bA + (size_t)slot0 * evo::kOutPad, bt.size() * 4, cudaMemcpyDeviceToHost));
+    CK(copy_sync(c, w12.data(), c->wA + (size_t)slot0 * evo::kSensors * 12, w12.size() * 4, cudaMemcpyDeviceToHost));
+    CK(copy_sync(c, wl.data(), c->wB + (size_t)slot0 * evo::kSensors, wl.size() * 4, cudaMemcpyDeviceToHost));
+    CK(copy_sync(c, bt.data(), c->bA + (size_t)slot0 * evo::kOutPad, bt.size() * 4, cudaMemcpyDeviceToHost));
     for (int s = 0; s < n; ++s)
       for (int j = 0; j < evo::kActuators; ++j) {
         for (int k = 0; k < evo::kSensors; ++k)
@@ -600,10 +617,10 @@ EVO_API int evo_get_params(evo_ctx* c, int slot0, int n, float* w1, float* b1, f
   const int hp = c->hpad;
   std::vector<float> W1((size_t)n * evo::kSensors * hp), B1((size_t)n * hp);
   std::vector<float> W2((size_t)n * hp * evo::kOutPad), B2((size_t)n * evo::kOutPad);
-  CK(cudaMemcpy(W1.data(), c->wA + (size_t)slot0 * evo::kSensors * hp, W1.size() * 4, cudaMemcpyDeviceToHost));
-  CK(cudaMemcpy(B1.data(), c->bA + (size_t)slot0 * hp, B1.size() * 4, cudaMemcpyDeviceToHost));
-  CK(cudaMemcpy(W2.data(), c->wB + (size_t)slot0 * hp * evo::kOutPad, W2.size() * 4, cudaMemcpyDeviceToHost));
-  CK(cudaMemcpy(B2.data(), c->bB + (size_t)slot0 * evo::kOutPad, B2.size() * 4, cudaMemcpyDeviceToHost));
+  CK(copy_sync(c, W1.data(), c->wA + (size_t)slot0 * evo::kSensors * hp, W1.size() * 4, cudaMemcpyDeviceToHost));
+  CK(copy_sync(c, B1.data(), c->bA + (size_t)slot0 * hp, B1.size() * 4, cudaMemcpyDeviceToHost));
+  CK(copy_sync(c, W2.data(), c->wB + (size_t)slot0 * hp * evo::kOutPad, W2.size() * 4, cudaMemcpyDeviceToHost));
+  CK(copy_sync(c, B2.data(), c->bB + (size_t)slot0 * evo::kOutPad, B2.size() * 4, cudaMemcpyDeviceToHost));
   for (int s = 0; s < n; ++s) {
     for (int h = 0; h < H; ++h) {
       for (int k = 0; k < evo::kSensors; ++k)
@@ -621,13 +638,13 @@ EVO_API int evo_set_slots(evo_ctx* c, const int8_t* state, const int32_t* peak) 
   if (int r = check_ctx(c)) return r;
   CK(cudaStreamSynchronize(c->stream));
   if (state) {
-    CK(cudaMemcpy(c->census.state, state, (size_t)c->cap, cudaMemcpyHostToDevice));
+    CK(copy_sync(c, c->census.state, state, (size_t)c->cap, cudaMemcpyHostToDevice));
     c->live = (int)std::count(state, state + c->cap, (int8_t)1);
     c->shard_stale = true;
     std::vector<int64_t> ds((size_t)c->cap, -1);
-    CK(cudaMemcpy(c->census.death_step, ds.data(), ds.size() * 8, cudaMemcpyHostToDevice));
+    CK(copy_sync(c, c->census.death_step, ds.data(), ds.size() * 8, cudaMemcpyHostToDevice));
   }
-  if (peak) CK(cudaMemcpy(c->census.peak, peak, (size_t)c->cap * 4, cudaMemcpyHostToDevice));
+  if (peak) CK(copy_sync(c, c->census.peak, peak, (size_t)c->cap * 4, cudaMemcpyHostToDevice));
   return 0;
 }
 
@@ -639,7 +656,7 @@ EVO_API int evo_set_source_map(evo_ctx* c, const float* map) {
     return 0;
   }
   if (!c->src_map) CK(c->alloc(&c->src_map, (size_t)c->ncell()));
-  CK(cudaMemcpy(c->src_map, map, (size_t)c->ncell() * 4, cudaMemcpyHostToDevice));
+  CK(copy_sync(c, c->src_map, map, (size_t)c->ncell() * 4, cudaMemcpyHostToDevice));
   c->have_src_map = true;
   return 0;
 }
@@ -948,14 +965,14 @@ EVO_API int evo_set_actions(evo_ctx* c, const int64_t* cells, int64_t n, const f
   for (int64_t i = 0; i < n; ++i)
     if (cells[i] < 0 || cells[i] >= nc) return fail(EVO_EINVAL, "action cell index out of range");
   CK(cudaStreamSynchronize(c->stream));
-  CK(cudaMemset(c->act_in_flag, 0, (size_t)nc));
+  CK(zero_sync(c, c->act_in_flag, 0, (size_t)nc));
   if (n == 0) return 0;
   int64_t* dcells = nullptr;
   float* drows = nullptr;
   CK(cudaMalloc(&dcells, (size_t)n * 8));
   cudaError_t e = cudaMalloc(&drows, (size_t)n * evo::kActuators * 4);
-  if (e == cudaSuccess) e = cudaMemcpy(dcells, cells, (size_t)n * 8, cudaMemcpyHostToDevice);
-  if (e == cudaSuccess) e = cudaMemcpy(drows, acts, (size_t)n * evo::kActuators * 4, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = copy_sync(c, dcells, cells, (size_t)n * 8, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = copy_sync(c, drows, acts, (size_t)n * evo::kActuators * 4, cudaMemcpyHostToDevice);
   if (e == cudaSuccess) e = evo::launch_scatter_actions(c->act_in, c->act_in_flag, dcells, drows, n, nc, c->stream);
   if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
   cudaFree(dcells);
@@ -977,8 +994,8 @@ EVO_API int evo_get_actions(evo_ctx* c, int64_t capacity, int64_t* cells, float*
   if (c->exp_rank) {  // genome-sorted rows of 16 floats, located through the cell -> row map
     std::vector<int32_t> rank((size_t)nc);
     std::vector<float> srows((size_t)nc * 16);
-    CK(cudaMemcpy(rank.data(), c->exp_rank, (size_t)nc * 4, cudaMemcpyDeviceToHost));
-    CK(cudaMemcpy(srows.data(), c->exp_rows, srows.size() * 4, cudaMemcpyDeviceToHost));
+    CK(copy_sync(c, rank.data(), c->exp_rank, (size_t)nc * 4, cudaMemcpyDeviceToHost));
+    CK(copy_sync(c, srows.data(), c->exp_rows, srows.size() * 4, cudaMemcpyDeviceToHost));
     for (long long i = 0; i < nc; ++i) {
       const int r = rank[(size_t)i];
       if (r < 0) continue;
@@ -991,8 +1008,8 @@ EVO_API int evo_get_actions(evo_ctx* c, int64_t capacity, int64_t* cells, float*
     *n = m;
     return 0;
   }
-  CK(cudaMemcpy(flag.data(), c->exp_flag, (size_t)nc, cudaMemcpyDeviceToHost));
-  CK(cudaMemcpy(rows.data(), c->exp_rows, rows.size() * 4, cudaMemcpyDeviceToHost));
+  CK(copy_sync(c, flag.data(), c->exp_flag, (size_t)nc, cudaMemcpyDeviceToHost));
+  CK(copy_sync(c, rows.data(), c->exp_rows, rows.size() * 4, cudaMemcpyDeviceToHost));
   for (long long i = 0; i < nc; ++i) {
     if (!flag[(size_t)i]) continue;
     if (m < capacity) {
@@ -1010,10 +1027,10 @@ EVO_API int evo_read_census(evo_ctx* c, int32_t* counts, int8_t* state, int64_t*
   CK(cudaStreamSynchronize(c->stream));
   CK(cudaDeviceSynchronize());
   const size_t cap = (size_t)c->cap;
-  if (counts) CK(cudaMemcpy(counts, c->census.counts_last, cap * 4, cudaMemcpyDeviceToHost));
-  if (state) CK(cudaMemcpy(state, c->census.state, cap, cudaMemcpyDeviceToHost));
-  if (death_step) CK(cudaMemcpy(death_step, c->census.death_step, cap * 8, cudaMemcpyDeviceToHost));
-  if (peak) CK(cudaMemcpy(peak, c->census.peak, cap * 4, cudaMemcpyDeviceToHost));
+  if (counts) CK(copy_sync(c, counts, c->census.counts_last, cap * 4, cudaMemcpyDeviceToHost));
+  if (state) CK(copy_sync(c, state, c->census.state, cap, cudaMemcpyDeviceToHost));
+  if (death_step) CK(copy_sync(c, death_step, c->census.death_step, cap * 8, cudaMemcpyDeviceToHost));
+  if (peak) CK(copy_sync(c, peak, c->census.peak, cap * 4, cudaMemcpyDeviceToHost));
   return 0;
 }
 
@@ -1022,8 +1039,9 @@ EVO_API int evo_census_take(evo_ctx* c, int32_t* counts) {
   if (!counts) return fail(EVO_EINVAL, "null counts");
   CK(cudaStreamSynchronize(c->stream));
   CK(cudaDeviceSynchronize());
-  CK(cudaMemcpy(counts, c->census.counts, (size_t)c->cap * 4, cudaMemcpyDeviceToHost));
-  CK(cudaMemset(c->census.counts, 0, (size_t)c->cap * 4));
+  CK(copy_sync(c, counts, c->census.counts, (size_t)c->cap * 4, cudaMemcpyDeviceToHost));
+  CK(cudaMemsetAsync(c->census.counts, 0, (size_t)c->cap * 4, c->stream));  // ordered before the next step
+  CK(cudaStreamSynchronize(c->stream));
   return 0;
 }
 
@@ -1032,7 +1050,7 @@ EVO_API int evo_read_stats(evo_ctx* c, int64_t* adoptions, int64_t* extinctions)
   CK(cudaStreamSynchronize(c->stream));
   CK(cudaDeviceSynchronize());
   long long st[2];
-  CK(cudaMemcpy(st, c->census.stats, sizeof(st), cudaMemcpyDeviceToHost));
+  CK(copy_sync(c, st, c->census.stats, sizeof(st), cudaMemcpyDeviceToHost));
   if (adoptions) *adoptions = st[0];
   if (extinctions) *extinctions = st[1];
   return 0;
@@ -1052,11 +1070,11 @@ EVO_API int evo_read_events(evo_ctx* c, int64_t capacity, int64_t* target, int64
   std::vector<uint8_t> rot((size_t)nc);
   // events belong to the step that produced the current front buffer
   const evo::Planes& p = c->buf[c->front];
-  CK(cudaMemcpy(src.data(), c->ev_src, (size_t)nc * 8, cudaMemcpyDeviceToHost));
-  CK(cudaMemcpy(q.data(), c->ev_q, (size_t)nc * 4, cudaMemcpyDeviceToHost));
-  CK(cudaMemcpy(def.data(), c->ev_def, (size_t)nc * 4, cudaMemcpyDeviceToHost));
-  CK(cudaMemcpy(gi.data(), p.gi + c->W, (size_t)nc * 4, cudaMemcpyDeviceToHost));
-  CK(cudaMemcpy(rot.data(), p.rot + c->W, (size_t)nc, cudaMemcpyDeviceToHost));
+  CK(copy_sync(c, src.data(), c->ev_src, (size_t)nc * 8, cudaMemcpyDeviceToHost));
+  CK(copy_sync(c, q.data(), c->ev_q, (size_t)nc * 4, cudaMemcpyDeviceToHost));
+  CK(copy_sync(c, def.data(), c->ev_def, (size_t)nc * 4, cudaMemcpyDeviceToHost));
+  CK(copy_sync(c, gi.data(), p.gi + c->W, (size_t)nc * 4, cudaMemcpyDeviceToHost));
+  CK(copy_sync(c, rot.data(), p.rot + c->W, (size_t)nc, cudaMemcpyDeviceToHost));
   int64_t k = 0;
   for (long long i = 0; i < nc; ++i) {
     if (src[(size_t)i] < 0) continue;
@@ -1088,8 +1106,8 @@ EVO_API int evo_patch_genomes(evo_ctx* c, const int64_t* cells, const int32_t* s
   int32_t* ds = nullptr;
   CK(cudaMalloc(&dc, (size_t)n * 8));
   cudaError_t e = cudaMalloc(&ds, (size_t)n * 4);
-  if (e == cudaSuccess) e = cudaMemcpy(dc, cells, (size_t)n * 8, cudaMemcpyHostToDevice);
-  if (e == cudaSuccess) e = cudaMemcpy(ds, slots, (size_t)n * 4, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = copy_sync(c, dc, cells, (size_t)n * 8, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = copy_sync(c, ds, slots, (size_t)n * 4, cudaMemcpyHostToDevice);
   if (e == cudaSuccess) e = evo::launch_patch_genomes(c->buf[c->front].gi, c->W, dc, ds, n, c->stream);
   if (e == cudaSuccess && !c->strip) e = evo::launch_refresh_ghosts(c->buf[c->front], c->geom(), c->stream);
   if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
@@ -1208,12 +1226,12 @@ EVO_API int evo_read_selected(evo_ctx* c, int64_t capacity, int64_t* cells, int6
   if (int r = check_ctx(c)) return r;
   if (!c->have_select) return fail(EVO_EINVAL, "no selection: call evo_select_cells first");
   unsigned long long ns = 0;
-  CK(cudaMemcpy(&ns, c->sel_n, sizeof(ns), cudaMemcpyDeviceToHost));
+  CK(copy_sync(c, &ns, c->sel_n, sizeof(ns), cudaMemcpyDeviceToHost));
   if (n) *n = (int64_t)ns;
   if (!cells) return 0;
   if ((long long)ns > capacity) return fail(EVO_EINVAL, "cells buffer too small");
   std::vector<int32_t> tmp(ns);
-  CK(cudaMemcpy(tmp.data(), c->sel_list, ns * 4, cudaMemcpyDeviceToHost));
+  CK(copy_sync(c, tmp.data(), c->sel_list, ns * 4, cudaMemcpyDeviceToHost));
   std::sort(tmp.begin(), tmp.end());
   for (size_t i = 0; i < tmp.size(); ++i) cells[i] = tmp[i];
   return 0;
