@@ -263,9 +263,9 @@ def run_ours(args, rank, world, local):
     # which pass-1 pipeline the library ran (evo_pass1): per-tile fused kernel
     # for small direct pools, genome-sorted rows otherwise
     rows_path = cfg.hidden > 0 or max(cfg.capacity, cfg.genomes) > 68
-    p1_name = ("pass 1, genome-sorted rows (sort, sense, "
-               + ("tcgen05 3xTF32 MLP" if cfg.hidden else "CUDA-core net") + ", physics)") if rows_path else \
-        "k_pass1_direct (pass 1: sense+net+physics)"
+    p1_name = ("pass-1 pipeline on genome-sorted rows (7 launches: sort x4, k_hid_sense, "
+               + ("k_hid_net tcgen05 3xTF32 MLP" if cfg.hidden else "k_direct_rows CUDA-core net")
+               + ", k_physics_rows)") if rows_path else "k_pass1_direct (pass 1: sense+net+physics)"
     launches_per_step = (8 if rows_path else 2) + (5 if strips else 0)  # strips: halo pack/unpack x2, census epilogue
     n_rad = sum(1 for i in range(args.steps) if radiate and (t - args.steps + i + 1) % cfg.radiation_every == 0)
     hbm, hbm_kind, pk = peaks()
@@ -273,12 +273,20 @@ def run_ours(args, rank, world, local):
     value = ncell * world / step_s
     achieved_gbs = ncell * BYTES_PER_CELL / step_s / 1e9
     k1_s, k2_s = k1 / 1e3 / args.steps, k2 / 1e3 / args.steps
-    traffic = None  # dram read+write bytes per launch of the dominant kernel, from an ncu --set full capture
+    # DRAM read + write bytes of the dominant launch(es) per step, from an ncu
+    # capture of this workload (profiles/ncu_traffic.json, tools/traffic_json.py):
+    # the pass-1 pipeline's total on the genome-sorted rows path, the fused
+    # kernel's on the tile path
+    traffic = None
     prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(prof) and not strips:
         try:
-            per = json.load(open(prof)).get(args.config, {}).get("per_kernel_dram_bytes_per_launch", {})
-            traffic = next((v for k, v in per.items() if "k_pass1_direct" in k), None)
+            rec = json.load(open(prof)).get(args.config, {})
+            if rows_path:
+                traffic = rec.get("pass1_dram_bytes_per_step")
+            else:
+                per = rec.get("per_kernel_dram_bytes_per_launch", {})
+                traffic = next((v for k, v in per.items() if "k_pass1_direct" in k), None)
         except Exception:
             traffic = None
     clk = clocks.summary()
@@ -312,6 +320,7 @@ def run_ours(args, rank, world, local):
             "unit": "GB/s",
             "frac": ((ncell * BYTES_PER_CELL_PASS1 / k1_s / 1e9) if not strips else achieved_gbs) / hbm,
             "traffic": traffic,
+            "traffic_over_algorithmic": (traffic / (ncell * BYTES_PER_CELL_PASS1)) if traffic else None,
             "algorithmic_bytes_per_cell": BYTES_PER_CELL_PASS1 if not strips else BYTES_PER_CELL,
             "units_per_launch": ncell,
             "step": {"achieved": achieved_gbs, "frac": achieved_gbs / hbm,
