@@ -313,6 +313,12 @@ class _Binding:
         self.pool_version = None
         self.device_ahead = False  # device front newer than the host mirror
         self.pinned = False
+        fr = getattr(state.config, "field_radiation", None)
+        if fr is not None and fr.every > 0:
+            # field radiation selects cells on the device every `every` steps:
+            # allocate its buffers now (a zero-probability selection) rather
+            # than inside the first radiation step
+            self.dev.select_cells(0, 0.0)
 
     def sync_params(self, pool) -> None:
         ver = getattr(pool, "version", None)
