@@ -1,11 +1,11 @@
 """Summarise ncu reports for profiles/ (runs on the CPU box).
 
-    python tools/ncu_summary.py [--config c2] OUT_PREFIX REPORT.ncu-rep [REPORT2 ...]
+    python tools/ncu_summary.py OUT_PREFIX REPORT.ncu-rep [REPORT2 ...]
 
-Writes OUT_PREFIX.md (per-kernel duration, DRAM bytes, issue/pipe
-utilisation, shared-memory wavefronts, top stall reasons) and merges the
-per-launch DRAM traffic into profiles/ncu_traffic.json under the config key
-(read by bench.py).
+Writes OUT_PREFIX.md: per-kernel duration, DRAM bytes, issue / pipe
+utilisation (FMA, LSU, tensor), shared-memory wavefronts and conflicts,
+occupancy, top stall reasons.  (profiles/ncu_traffic.json, which bench.py
+reads, is written from launch lists by tools/traffic_json.py.)
 """
 
 import csv
@@ -28,6 +28,11 @@ KEYS = [
     ("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed", "smem wavefront util %"),
     ("l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum", "smem bank conflicts"),
     ("dram__throughput.avg.pct_of_peak_sustained_elapsed", "DRAM throughput %"),
+    ("sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active", "tensor pipe active %"),
+    ("sm__inst_executed_pipe_uniform.avg.pct_of_peak_sustained_active", "uniform pipe %"),
+    ("sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active", "ALU pipe active %"),
+    ("sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active", "FMA pipe active %"),
+    ("lts__t_bytes.sum", "L2 bytes"),
     ("launch__registers_per_thread", "registers/thread"),
     ("launch__grid_size", "grid"),
     ("launch__block_size", "block"),
@@ -43,12 +48,8 @@ def raw(rep):
 
 def main():
     argv = sys.argv[1:]
-    config = "c2"
-    if argv[:1] == ["--config"]:
-        config, argv = argv[1], argv[2:]
     prefix, reps = argv[0], argv[1:]
     lines = ["# ncu summary", ""]
-    traffic = {}
     for rep in reps:
         hdr, units, rows = raw(rep)
         lines.append(f"## {os.path.basename(rep)}")
@@ -71,21 +72,9 @@ def main():
             tot = sum(st.values()) or 1.0
             top = sorted(st.items(), key=lambda x: -x[1])[:6]
             lines.append("- top stall reasons: " + ", ".join(f"{k} {v / tot * 100:.1f}%" for k, v in top))
-            if "dram__bytes_read.sum" in vals:
-                b = 0.0
-                for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
-                    v, u = vals[k]
-                    b += float(v) * SCALE.get(u, 1.0)
-                traffic[name] = b
             lines.append("")
     with open(prefix + ".md", "w") as f:
         f.write("\n".join(lines) + "\n")
-    tpath = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "profiles", "ncu_traffic.json")
-    old = json.load(open(tpath)) if os.path.exists(tpath) else {}
-    old.pop("per_kernel_dram_bytes_per_launch", None)  # pre-config layout
-    old.setdefault(config, {}).setdefault("per_kernel_dram_bytes_per_launch", {}).update(traffic)
-    with open(tpath, "w") as f:
-        json.dump(old, f, indent=1)
     print(prefix + ".md")
 
 
