@@ -388,7 +388,8 @@ int pass1_view(evo_ctx* c, const View& v, const evo_scalars* s, int phases, int 
     CK(evo::launch_hidden_tc(c->hid, v.g, v.front, c->params(), c->cap, c->num_sms, /*decided=*/!exp, st));
   }
   const bool via_rows = tc_net || rows_net;
-  c->have_export = exp || via_rows;
+  const bool decided = via_rows && c->hidden == 0 && !exp;  // 8-float records at the cell index
+  c->have_export = exp || (via_rows && !decided);
   c->exp_rows = via_rows ? c->hid.act : c->act_out;
   c->exp_flag = via_rows ? nullptr : c->act_out_flag;
   c->exp_rank = via_rows ? c->hid.rank : nullptr;
@@ -417,7 +418,7 @@ int pass1_view(evo_ctx* c, const View& v, const evo_scalars* s, int phases, int 
   a.act_in = via_rows ? c->hid.act : c->act_in;
   a.act_flag = via_rows ? nullptr : c->act_in_flag;
   a.act_rank = via_rows ? c->hid.rank : nullptr;
-  a.act_decided = via_rows && c->hidden == 0 && !exp ? 1 : 0;
+  a.act_decided = decided ? 1 : 0;
   a.act_out = c->act_out;
   a.act_out_flag = c->act_out_flag;
   a.capacity = c->cap;

@@ -288,7 +288,7 @@ __global__ void __launch_bounds__(kSortThreads, 2) k_hid_sense(const StepGeom g,
           for (int part = 0; part < 12; ++part)
             row[part] = make_float4(v[4 * part], v[4 * part + 1], v[4 * part + 2], v[4 * part + 3]);
         }
-        rank_of_cell[c] = rank;
+        if (rank_of_cell) rank_of_cell[c] = rank;
       }
       __syncwarp();
       for (int k = lane; k < 32 * 12; k += 32) {  // 12 lanes per 192-byte row
@@ -663,11 +663,36 @@ __global__ void __launch_bounds__(kDrThreads, 4) k_direct_rows(const NetArgs a) 
   const int nw = gridDim.x * kDrWarps, gw = blockIdx.x * kDrWarps + warp;
   const int per = (H + nw - 1) / nw;
   const int h0 = gw * per, h1 = min(H, h0 + per);
+  // next non-empty half-tile at or after h (empty second halves of short
+  // tiles are skipped; warp-uniform)
+  auto advance = [&](int h, int4& ti) {
+    for (; h < h1; ++h) {
+      ti = __ldg(a.tile_info + (h >> 1));
+      if ((h & 1) * 64 < ti.z) break;
+    }
+    return h;
+  };
+  auto row_ptr = [&](const int4& ti, int h, int r) {
+    const int rr = (h & 1) * 64 + r;
+    return a.sens + (size_t)(ti.y + (rr < ti.z ? rr : 0)) * kK1;
+  };
   int cur = -1;
-  for (int h = h0; h < h1; ++h) {
-    const int4 ti = __ldg(a.tile_info + (h >> 1));
-    const int rb = (h & 1) * 64;
-    if (rb >= ti.z) continue;  // warp-uniform: empty second half
+  int4 ti = make_int4(0, 0, 0, 0);
+  int h = advance(h0, ti);
+  f8 q0[6], q1[6];
+  if (h < h1) {  // the first half-tile's leading sectors; later ones are
+                 // issued during the previous half-tile's last chunks
+    const float* g0 = row_ptr(ti, h, lane);
+    const float* g1 = row_ptr(ti, h, lane + 32);
+#pragma unroll
+    for (int c = 0; c < kDrDepth; ++c) {
+      q0[c] = ld_row32(g0 + 8 * c);
+      q1[c] = ld_row32(g1 + 8 * c);
+    }
+  }
+  while (h < h1) {
+    int4 tn = ti;
+    const int hn = advance(h + 1, tn);
     if (ti.x != cur) {
       cur = ti.x;
       __syncwarp();
@@ -677,15 +702,13 @@ __global__ void __launch_bounds__(kDrThreads, 4) k_direct_rows(const NetArgs a) 
       if (lane < kOutPad) Bs[lane] = __ldg(a.net.bA + (size_t)cur * kOutPad + lane);
       __syncwarp();
     }
+    const int rb = (h & 1) * 64;
     const int r0 = rb + lane, r1 = rb + lane + 32;
-    const float* g0 = a.sens + (size_t)(ti.y + (r0 < ti.z ? r0 : 0)) * kK1;
-    const float* g1 = a.sens + (size_t)(ti.y + (r1 < ti.z ? r1 : 0)) * kK1;
-    f8 q0[6], q1[6];
-#pragma unroll
-    for (int c = 0; c < kDrDepth; ++c) {
-      q0[c] = ld_row32(g0 + 8 * c);
-      q1[c] = ld_row32(g1 + 8 * c);
-    }
+    const float* g0 = row_ptr(ti, h, lane);
+    const float* g1 = row_ptr(ti, h, lane + 32);
+    const bool more = hn < h1;
+    const float* n0 = row_ptr(tn, hn, lane);
+    const float* n1 = row_ptr(tn, hn, lane + 32);
     u64 acc[2][6];
     float acc12[2] = {0.0f, 0.0f};
 #pragma unroll
@@ -698,6 +721,10 @@ __global__ void __launch_bounds__(kDrThreads, 4) k_direct_rows(const NetArgs a) 
       if (j == 0 && ch + kDrDepth < 6) {  // refill the sector pipeline
         q0[ch + kDrDepth] = ld_row32(g0 + 8 * (ch + kDrDepth));
         q1[ch + kDrDepth] = ld_row32(g1 + 8 * (ch + kDrDepth));
+      }
+      if (j == 0 && ch >= 6 - kDrDepth && more) {  // the next half-tile's leading sectors
+        q0[ch - (6 - kDrDepth)] = ld_row32(n0 + 8 * (ch - (6 - kDrDepth)));
+        q1[ch - (6 - kDrDepth)] = ld_row32(n1 + 8 * (ch - (6 - kDrDepth)));
       }
       const float x0 = q0[ch].v[j];
       const float x1 = q1[ch].v[j];
@@ -727,13 +754,17 @@ __global__ void __launch_bounds__(kDrThreads, 4) k_direct_rows(const NetArgs a) 
         z[2 * p + 1] = __fadd_rn(hi, Bs[2 * p + 1]);
       }
       z[12] = __fadd_rn(acc12[c], Bs[12]);
-      if (a.decided) {  // 32 bytes: the physics needs only these (explore_pick is exact)
+      if (a.decided) {  // 32 bytes at the cell's index: the physics needs only these (explore_pick is exact)
         int ks;
         float xm;
         explore_pick(z + 5, ks, xm);
-        float4* dst = reinterpret_cast<float4*>(a.act + (size_t)(ti.y + r) * 8);
-        dst[0] = make_float4(squash(z[0]), squash(z[1]), squash(z[2]), squash(z[3]));
-        dst[1] = make_float4(squash(z[4]), xm, __int_as_float(ks), 0.0f);
+        const int cell = __float_as_int(c ? q1[5].v[5] : q0[5].v[5]);  // row element 45
+        // one whole-sector store per record (STG.256): scattered cells, so
+        // every store instruction is 32 sectors and their count is the cost
+        asm volatile("st.global.v8.f32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(a.act + (size_t)cell * 8),
+                     "f"(squash(z[0])), "f"(squash(z[1])), "f"(squash(z[2])), "f"(squash(z[3])), "f"(squash(z[4])),
+                     "f"(xm), "f"(__int_as_float(ks)), "f"(0.0f)
+                     : "memory");
       } else {
         float v[16];
 #pragma unroll
@@ -744,6 +775,8 @@ __global__ void __launch_bounds__(kDrThreads, 4) k_direct_rows(const NetArgs a) 
         for (int q = 0; q < 4; ++q) dst[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
       }
     }
+    h = hn;
+    ti = tn;
   }
 }
 
@@ -797,7 +830,9 @@ cudaError_t launch_hidden_tc(const HidBuffers& b, const StepGeom& g, const Plane
     k_hid_tilemap<<<(unsigned)((max_tiles + 255) / 256), 256, 0, st>>>(b.offs, b.tiles, capacity, b.n_tiles,
                                                                        b.tile_info);
   }
-  k_hid_sense<<<nctas, kSortThreads, ssmem, st>>>(g, front, b.offs, b.cta_hist, capacity, b.sens, b.rank);
+  // decided records of direct nets land at the cell index: no cell -> row map
+  int32_t* rank = decided && net.hidden == 0 ? nullptr : b.rank;
+  k_hid_sense<<<nctas, kSortThreads, ssmem, st>>>(g, front, b.offs, b.cta_hist, capacity, b.sens, rank);
   NetArgs a;
   a.net = net;
   a.nh = net.hidden > 0 ? hidden_tc_nh(net.hidden) : 0;

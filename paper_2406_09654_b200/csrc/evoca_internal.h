@@ -106,8 +106,9 @@ struct Pass1Args {
   const float* act_in;       // inject: (H*W,13), or with act_rank: rank-ordered rows of 16
   const uint8_t* act_flag;   // inject: (H*W)
   const int32_t* act_rank;   // nullable: row of each cell in act_in (-1 = no actions)
-  int act_decided;           // with act_rank: 1 -> 8-float decided rows {inv, liq, m0..m2, xmax, kstar, 0},
-                             // 0 -> 16-float rows of the 13 squashed actuators
+  int act_decided;           // with act_rank: 1 -> 8-float decided records {inv, liq, m0..m2, xmax, kstar, 0}
+                             // at each occupied CELL's index (spatial order; act_rank unused),
+                             // 0 -> 16-float rows of the 13 squashed actuators at the cell's rank
   float* act_out;            // export: (H*W,13)
   uint8_t* act_out_flag;     // export: (H*W)
   int capacity;
@@ -151,7 +152,7 @@ struct HidBuffers {
   int32_t* cta_hist;  // [sort CTAs][cap] per-CTA slot histograms -> row bases
   float* sens;       // [ncell][48]
   int4* tile_info;     // [ncell / 128 + cap] {slot, first row, rows, 0} per 128-row tile
-  float* act;        // [ncell][16] (or [ncell][8] decided) actuator rows in sorted-row order
+  float* act;        // [ncell][16] actuator rows in sorted-row order, or [ncell][8] decided records in cell order
   int32_t* rank;     // [ncell] sorted row of each cell, -1 = empty
 };
 bool hidden_tc_supported(int hidden);

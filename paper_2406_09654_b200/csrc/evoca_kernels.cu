@@ -66,7 +66,7 @@ __device__ __forceinline__ void zero_stats(const Pass1Args& a) {
 __device__ __forceinline__ CellAct row_actions(const Pass1Args& a, int r) {
   CellAct ac{};
   ac.acted = r >= 0;
-  if (ac.acted && a.act_decided) {  // one 32-byte sector: {inv, liq, m0, m1, m2, xmax, kstar, 0}
+  if (ac.acted && a.act_decided) {  // one 32-byte sector at the cell index: {inv, liq, m0, m1, m2, xmax, kstar, 0}
     float v[8];
     asm volatile("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
                  : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]), "=f"(v[4]), "=f"(v[5]), "=f"(v[6]), "=f"(v[7])
@@ -95,6 +95,9 @@ __device__ __forceinline__ CellAct row_actions(const Pass1Args& a, int r) {
 // Four consecutive cells per thread (W % 4 == 0): 16-byte plane loads and
 // stores, one load instruction per plane per four cells (the per-cell
 // version was LSU-queue bound: lg_throttle 28 %, long_scoreboard 60 %).
+// Direct nets write their decided records at the cell's own index, so those
+// reads are coalesced too (rows at the sorted rank made this kernel
+// gather-bound: long_scoreboard 83 %).
 __global__ void __launch_bounds__(256) k_physics_rows(const Pass1Args a) {
   zero_stats(a);
   const StepGeom& g = a.g;
@@ -111,7 +114,9 @@ __global__ void __launch_bounds__(256) k_physics_rows(const Pass1Args a) {
       const float4 C2 = __ldg(reinterpret_cast<const float4*>(a.front.C + 2 * st + o));
       const int4 G = __ldg(reinterpret_cast<const int4*>(a.front.gi + o));
       const unsigned R = __ldg(reinterpret_cast<const unsigned*>(a.front.rot + o));
-      const int4 RK = __ldg(reinterpret_cast<const int4*>(a.act_rank + c0));
+      const int4 RK = a.act_decided ? make_int4(G.x >= 0 ? c0 : -1, G.y >= 0 ? c0 + 1 : -1, G.z >= 0 ? c0 + 2 : -1,
+                                                G.w >= 0 ? c0 + 3 : -1)
+                                    : __ldg(reinterpret_cast<const int4*>(a.act_rank + c0));
       const float e[4] = {E.x, E.y, E.z, E.w}, in[4] = {I.x, I.y, I.z, I.w};
       const float c0v[4] = {C0.x, C0.y, C0.z, C0.w}, c1v[4] = {C1.x, C1.y, C1.z, C1.w},
                   c2v[4] = {C2.x, C2.y, C2.z, C2.w};
@@ -145,7 +150,8 @@ __global__ void __launch_bounds__(256) k_physics_rows(const Pass1Args a) {
     const CellState cs{__ldg(a.front.E + o), __ldg(a.front.I + o), __ldg(a.front.C + o),
                        __ldg(a.front.C + st + o), __ldg(a.front.C + 2 * st + o), __ldg(a.front.gi + o),
                        (int)__ldg(a.front.rot + o)};
-    store_pass1(a, y, x, cell_physics(a.s, a.phases, a.src_map, c, cs, row_actions(a, __ldg(a.act_rank + c))));
+    const int r = a.act_decided ? (cs.slot >= 0 ? c : -1) : __ldg(a.act_rank + c);
+    store_pass1(a, y, x, cell_physics(a.s, a.phases, a.src_map, c, cs, row_actions(a, r)));
   }
 }
 

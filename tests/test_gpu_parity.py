@@ -515,6 +515,9 @@ def test_genome_sorted_direct_path_matches_tile_path(genomes, shape):
         want = download(b)
         assert download(a).equal(want), f"t={t}"
         assert download(c).equal(want), f"t={t}"
+    # the decided records of a non-export step are not actuator rows
+    with pytest.raises(ValueError):
+        a.get_actions()
     for d in (a, b, c):
         d.close()
     _step_vs_oracle(p0, net, phys, steps=2)
