@@ -53,6 +53,9 @@ extern "C" {
 #define EVO_F_MMA_NET 64        /* direct nets of pools <= 64 slots: mma.sync 3xTF32 tile kernel (measured slower; A/B) */
 #define EVO_F_TC_NET 128        /* hidden layers narrower than 64: tcgen05 3xTF32 net instead of FP32 CUDA cores */
 #define EVO_F_SHARD_NET 256     /* direct nets of pools > 68 slots: cluster-sharded tile kernel (measured slower; A/B) */
+#define EVO_F_ROWS_NET 512      /* direct nets of pools > 68 slots: genome-sorted sensor rows in HBM (round-2 path; A/B) */
+#define EVO_F_GATHER_NET 1024   /* direct nets of pools <= 68 slots: the large-pool gather path instead of the tile kernel (A/B) */
+#define EVO_F_TC_DIRECT 2048    /* gather path: the direct net as tcgen05 3xTF32 MMAs (A in TMEM) instead of FFMA2 warps */
 
 /* Host-computed per-step scalars, exactly as the reference derives them:
  * rho = A*sin(2*pi*t/P) in float64 (physics.py:186); rho_mode 1 if rho > 0,

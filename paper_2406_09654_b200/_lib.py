@@ -22,6 +22,9 @@ F_INJECT_ACTIONS, F_EXPORT_ACTIONS, F_RECORD_EVENTS, F_NO_CENSUS, F_CUDA_CORE_NE
 F_MMA_NET = 64  # direct nets of pools <= 64 slots: mma.sync 3xTF32 tile kernel (measured slower; A/B only)
 F_TC_NET = 128  # hidden layers narrower than 64 on the tensor cores (default: FP32 CUDA cores)
 F_SHARD_NET = 256  # large direct pools: cluster-sharded tile kernel (measured slower than the rows path; A/B)
+F_ROWS_NET = 512  # large direct pools: genome-sorted sensor rows through HBM (the round-2 path; A/B)
+F_GATHER_NET = 1024  # pools <= 68 slots: the large-pool gather path instead of the tile kernel (A/B)
+F_TC_DIRECT = 2048  # gather path: direct net on tcgen05 (3xTF32, A in TMEM) instead of FFMA2 warps
 
 
 class EvoScalars(C.Structure):

@@ -22,7 +22,7 @@ CSRC = os.path.join(PKG, "csrc")
 INCLUDE = os.path.join(ROOT, "include")
 LIB = os.path.join(PKG, "libevoca_b200.so")
 SOURCES = ["evoca_kernels.cu", "evoca_hidden_tc.cu", "evoca_cppn.cu", "evoca_radiation.cu", "evoca_metrics.cu",
-           "evoca_shard.cu", "evoca_resolve.cu", "evoca_abi.cu", "evoca_neat.cpp"]
+           "evoca_shard.cu", "evoca_gather.cu", "evoca_resolve.cu", "evoca_abi.cu", "evoca_neat.cpp"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

@@ -78,6 +78,7 @@ struct evo_ctx {
   bool have_select = false;
   // tensor-core hidden-layer controller buffers (allocated on first use)
   evo::HidBuffers hid = {};
+  evo::GatherBuffers gat = {};  // large-pool direct nets by gather (allocated on first use)
   int num_sms = 0;
   // rows / flags evo_get_actions reads (act_out, or hid.act after a tensor-core step)
   const float* exp_rows = nullptr;
@@ -269,7 +270,37 @@ int ensure_actions_out(evo_ctx* c) {
   return 0;
 }
 
+// actuator rows / decided records and the cell -> row map shared by every
+// genome-sorted path
+int ensure_sorted_out(evo_ctx* c) {
+  if (c->hid.act) return 0;
+  const size_t n = (size_t)c->ncell();
+  CK(c->alloc(&c->hid.act, n * 16));
+  CK(c->alloc(&c->hid.rank, n));
+  if (!c->num_sms) CK(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, c->device));
+  return 0;
+}
+
+int ensure_gather(evo_ctx* c) {
+  if (int r = ensure_sorted_out(c)) return r;
+  if (c->gat.tex) return 0;
+  const evo::GatherSizes z = evo::gather_sizes(c->W, c->H, c->cap, c->num_sms);
+  const size_t n = (size_t)c->ncell(), nb = (size_t)z.nbands, bins = (size_t)z.bins;
+  CK(c->alloc(&c->gat.tex, ((size_t)c->H + 2) * c->W * 8));
+  CK(c->alloc(&c->gat.band_hist, nb * bins));
+  CK(c->alloc(&c->gat.goff, nb * (bins + 1)));
+  CK(c->alloc(&c->gat.ght, nb * (bins + 1)));
+  CK(c->alloc(&c->gat.cursor, nb * bins));
+  CK(c->alloc(&c->gat.band_tot, nb * 2));
+  CK(c->alloc(&c->gat.band_base, nb * 2 + 2));
+  CK(c->alloc(&c->gat.n_ht, 2));
+  CK(c->alloc(&c->gat.sorted, n));
+  CK(c->alloc(&c->gat.info, (size_t)z.max_ht));
+  return 0;
+}
+
 int ensure_hidden_tc(evo_ctx* c) {
+  if (int r = ensure_sorted_out(c)) return r;
   if (c->hid.sens) return 0;
   const size_t n = (size_t)c->ncell(), cap = (size_t)c->cap;
   CK(c->alloc(&c->hid.counts, cap));
@@ -279,10 +310,7 @@ int ensure_hidden_tc(evo_ctx* c) {
   CK(c->alloc(&c->hid.n_tiles, 1));
   CK(c->alloc(&c->hid.cta_hist, (size_t)evo::hidden_sort_ctas(c->W, c->H) * cap));
   CK(c->alloc(&c->hid.tile_info, n / 128 + cap + 1));
-  CK(c->alloc(&c->hid.act, n * 16));
-  CK(c->alloc(&c->hid.rank, n));
   CK(c->alloc(&c->hid.sens, n * 48));
-  if (!c->num_sms) CK(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, c->device));
   return 0;
 }
 
@@ -372,22 +400,33 @@ int pass1_view(evo_ctx* c, const View& v, const evo_scalars* s, int phases, int 
                       !(flags & EVO_F_CUDA_CORE_NET) &&
                       (c->hidden >= evo::kTcMinHidden || (flags & EVO_F_TC_NET));
   // direct nets of large pools (weights do not fit next to the tile in shared
-  // memory): genome-sorted sensor rows; EVO_F_SHARD_NET selects the measured
+  // memory): cells sorted by (row band, slot, rotation), each warp gathering
+  // its cells' Moore neighbourhoods from an L2-resident sense texture
+  // (evoca_gather.cu); EVO_F_ROWS_NET selects the earlier genome-sorted
+  // sensor rows written to HBM (evoca_hidden_tc.cu); EVO_F_SHARD_NET the measured
   // alternative that shards the weight table over a thread-block cluster
   // working on one tile (evoca_shard.cu: 4.7 ms against 2.4 ms per config-3
   // step - each CTA sees ~256 cells of a tile, too few to hide its latency)
-  const bool big_pool = !inject && c->hidden == 0 && c->cap > evo::kSmemWeightSlotsAbi &&
+  const bool big_pool = !inject && c->hidden == 0 &&
+                        (c->cap > evo::kSmemWeightSlotsAbi || (flags & EVO_F_GATHER_NET)) &&
                         !(flags & EVO_F_TILE_NET);
   const bool shard_net = big_pool && !exp && (flags & EVO_F_SHARD_NET) && c->live <= evo::kShardMaxLive;
-  const bool rows_net = big_pool && !shard_net;
-  if (exp && !tc_net && !rows_net) {
+  const bool gather_net = big_pool && !shard_net && !(flags & EVO_F_ROWS_NET) &&
+                          evo::gather_supported(c->W, c->H, c->cap);
+  const bool rows_net = big_pool && !shard_net && !gather_net;
+  if (exp && !tc_net && !rows_net && !gather_net) {
     if (int r = ensure_actions_out(c)) return r;
   }
   if (tc_net || rows_net) {
     if (int r = ensure_hidden_tc(c)) return r;
     CK(evo::launch_hidden_tc(c->hid, v.g, v.front, c->params(), c->cap, c->num_sms, /*decided=*/!exp, st));
   }
-  const bool via_rows = tc_net || rows_net;
+  if (gather_net) {  // rows (export) or decided records at the cell index; rank = identity for occupied cells
+    if (int r = ensure_gather(c)) return r;
+    CK(evo::launch_direct_gather(c->gat, v.g, v.front, c->params(), c->cap, c->num_sms,
+                                 (flags & EVO_F_TC_DIRECT) != 0, exp, c->hid.act, c->hid.rank, st));
+  }
+  const bool via_rows = tc_net || rows_net || gather_net;
   const bool decided = via_rows && c->hidden == 0 && !exp;  // 8-float records at the cell index
   c->have_export = exp || (via_rows && !decided);
   c->exp_rows = via_rows ? c->hid.act : c->act_out;
@@ -705,7 +744,9 @@ EVO_API int evo_step_host(evo_ctx* c, const evo_scalars* s, int64_t t, int flags
     return fail(EVO_EINVAL, "action injection/export is not available in the host-pipelined step");
   if (int r = ensure_pipe(c)) return r;
   if (c->hidden > 0 || c->cap > evo::kSmemWeightSlotsAbi) {
-    if (int r = ensure_hidden_tc(c)) return r;
+    const bool gather = c->hidden == 0 && !(flags & (EVO_F_ROWS_NET | EVO_F_TILE_NET | EVO_F_SHARD_NET)) &&
+                        evo::gather_supported(c->W, c->H, c->cap);
+    if (int r = gather ? ensure_gather(c) : ensure_hidden_tc(c)) return r;
   }
   if ((flags & EVO_F_RECORD_EVENTS)) {
     if (int r = ensure_events(c)) return r;

@@ -155,6 +155,30 @@ struct HidBuffers {
   float* act;        // [ncell][16] actuator rows in sorted-row order, or [ncell][8] decided records in cell order
   int32_t* rank;     // [ncell] sorted row of each cell, -1 = empty
 };
+// Direct nets of large pools by gather (evoca_gather.cu): per-step buffers.
+constexpr int kGatherMaxCap = 2048;  // (slot, rotation) histogram of 16 K bins in shared memory
+struct GatherBuffers {
+  float* tex;          // [(H + 2) * W][8] sense records {E, I, C0, C1, C2, 0, 0, 0}
+  int32_t* band_hist;  // [nbands][bins] (zero between steps)
+  int32_t* goff;       // [nbands][bins + 1] group cell offsets within the band
+  int32_t* ght;        // [nbands][bins + 1] group half-tile offsets within the band
+  int32_t* cursor;     // [nbands][bins]
+  int32_t* band_tot;   // [nbands][2]
+  int32_t* band_base;  // [nbands + 1][2]
+  int32_t* n_ht;       // [2]: half-tiles, gather work counter
+  uint32_t* sorted;    // [ncell] (y << 16) | x by (band, slot, rotation)
+  int4* info;          // [max_ht] {slot * 8 + rot, first, cells, 0}
+};
+struct GatherSizes {
+  int nbands, bins;
+  long long max_ht;
+};
+bool gather_supported(int W, int H, int cap);
+GatherSizes gather_sizes(int W, int H, int cap, int num_sms);
+cudaError_t launch_direct_gather(const GatherBuffers& b, const StepGeom& g, const Planes& front, const Params& net,
+                                 int cap, int num_sms, bool tc, bool export_rows, float* act, int32_t* rank,
+                                 cudaStream_t st);
+
 bool hidden_tc_supported(int hidden);
 int hidden_sort_ctas(int W, int H);
 int hidden_tc_nh(int hidden);

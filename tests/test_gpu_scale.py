@@ -39,16 +39,19 @@ def test_config3_full_size_tier_a():
     params = oracle_phys_to_params(phys)
     dev = make_dev(p0, cap, net, live=genomes)
     fast = make_dev(p0, cap, net, live=genomes)  # the benchmark's variant (decided rows, no export)
+    rows = make_dev(p0, cap, net, live=genomes)  # sensor rows through HBM (EVO_F_ROWS_NET)
     p = p0
     for t in range(2):
         sc = physics.step_scalars(t, params)
         dev.step_raw(sc, t, flags=_lib.F_EXPORT_ACTIONS | _lib.F_RECORD_EVENTS)
         fast.step_raw(sc, t)
+        rows.step_raw(sc, t, flags=_lib.F_ROWS_NET)
         cells, acts = dev.get_actions()
         ref = orc.step(p, t, net, phys, acts=orc.Actions(cells, acts))
         got = download(dev)
         assert got.equal(ref.planes), f"t={t}"
         assert download(fast).equal(got), f"t={t}"
+        assert download(rows).equal(got), f"t={t}"
         assert events_rows(dev.read_events()) == [tuple(map(float, r)) for r in ref.events.rows()], f"t={t}"
         counts = dev.read_census()[0]
         assert np.array_equal(counts[:genomes], ref.counts[:genomes]) and not counts[genomes:].any()
@@ -58,6 +61,7 @@ def test_config3_full_size_tier_a():
         p = got
     dev.close()
     fast.close()
+    rows.close()
 
 
 def test_config2_nonexport_kernel_equals_export():
