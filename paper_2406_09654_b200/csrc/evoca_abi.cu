@@ -284,13 +284,14 @@ int ensure_sorted_out(evo_ctx* c) {
 int ensure_gather(evo_ctx* c) {
   if (int r = ensure_sorted_out(c)) return r;
   if (c->gat.tex) return 0;
+  CK(c->alloc(&c->gat.tex, ((size_t)c->H + 2) * c->W * 8));
   const evo::GatherSizes z = evo::gather_sizes(c->W, c->H, c->cap, c->num_sms);
   const size_t n = (size_t)c->ncell(), nb = (size_t)z.nbands, bins = (size_t)z.bins;
-  CK(c->alloc(&c->gat.tex, ((size_t)c->H + 2) * c->W * 8));
+  CK(c->alloc(&c->gat.cta_hist, (size_t)z.nctas * bins));
+  CK(c->alloc(&c->gat.lrank, n));
   CK(c->alloc(&c->gat.band_hist, nb * bins));
   CK(c->alloc(&c->gat.goff, nb * (bins + 1)));
   CK(c->alloc(&c->gat.ght, nb * (bins + 1)));
-  CK(c->alloc(&c->gat.cursor, nb * bins));
   CK(c->alloc(&c->gat.band_tot, nb * 2));
   CK(c->alloc(&c->gat.band_base, nb * 2 + 2));
   CK(c->alloc(&c->gat.n_ht, 2));
@@ -422,9 +423,10 @@ int pass1_view(evo_ctx* c, const View& v, const evo_scalars* s, int phases, int 
     CK(evo::launch_hidden_tc(c->hid, v.g, v.front, c->params(), c->cap, c->num_sms, /*decided=*/!exp, st));
   }
   if (gather_net) {  // rows (export) or decided records at the cell index; rank = identity for occupied cells
+    const bool tc = (flags & EVO_F_TC_DIRECT) != 0;
     if (int r = ensure_gather(c)) return r;
-    CK(evo::launch_direct_gather(c->gat, v.g, v.front, c->params(), c->cap, c->num_sms,
-                                 (flags & EVO_F_TC_DIRECT) != 0, exp, c->hid.act, c->hid.rank, st));
+    CK(evo::launch_direct_gather(c->gat, v.g, v.front, c->params(), c->cap, c->num_sms, tc, exp, c->hid.act,
+                                 c->hid.rank, st));
   }
   const bool via_rows = tc_net || rows_net || gather_net;
   const bool decided = via_rows && c->hidden == 0 && !exp;  // 8-float records at the cell index

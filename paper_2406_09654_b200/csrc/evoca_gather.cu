@@ -8,23 +8,27 @@
 // wrote a 192-byte sensor row per cell to HBM and read it back (9.5 GB per
 // config-3 step).  Here nothing per-cell but a 4-byte sorted cell list leaves
 // the chip between sense and net:
-//   k_gs_count    per row band (~1 M cells, so the band's texture stays in
-//                 the 126 MB L2): histogram of the occupied cells by
-//                 (slot, rotation), and the 32-byte sense texture record of
-//                 every cell {E, I, C0, C1, C2, 0, 0, 0} (one sector)
-//   k_gs_scan_band / k_gs_scan_bands  group offsets within bands, band bases
-//   k_gs_scatter  cell list sorted by (band, slot, rotation)
-//   k_gs_tilemap  64-cell half-tiles of one (band, slot, rotation) group
-//   k_direct_gather  one warp per half-tile: slot AND rotation are uniform,
-//                 so the Moore slot order (PERM_TABLE[rot], physics.py:48-62)
-//                 is a warp-uniform offset and the weights are warp-uniform
-//                 broadcasts; each lane gathers its two cells' nine texture
-//                 records (whole 32-byte sectors, L2 hits: half-tiles are
-//                 handed out band by band) and runs the tile kernel's FFMA2
-//                 chains in the same k order, so the actions are
-//                 bit-identical to the tile and rows paths.  Output: the
-//                 32-byte decided record at the cell index (k_physics_rows),
-//                 or 16-float actuator rows at the cell index (export).
+//   k_gs_count    per count CTA (a run of rows): the 32-byte sense texture
+//                 record of every cell {E, I, C0, C1, C2, 0, 0, 0} (one
+//                 sector), the CTA's histogram of occupied cells by slot and
+//                 each cell's rank in it (one shared-memory atomic per cell)
+//   k_gs_colscan / k_gs_scan_band / k_gs_scan_bands  per row band (~1 M
+//                 cells, so the band's texture stays in the 126 MB L2):
+//                 CTA bases inside each (band, slot) group, group offsets,
+//                 band bases
+//   k_gs_scatter  cell list sorted by (band, slot): positions from the
+//                 scans and ranks, no atomics
+//   k_gs_tilemap  64-cell half-tiles of one (band, slot) group
+//   k_direct_gather  one warp per half-tile: the slot is uniform, so every
+//                 weight load is a warp-uniform broadcast; each lane gathers
+//                 its two cells' nine texture records in their own Moore
+//                 order (PERM_TABLE[rot], physics.py:48-62; whole 32-byte
+//                 sectors, L2 hits: half-tiles are handed out band by band)
+//                 and runs the tile kernel's FFMA2 chains in the same k
+//                 order, so the actions are bit-identical to the tile and
+//                 rows paths.  Output: the 32-byte decided record at the
+//                 cell index (k_physics_rows), or 16-float actuator rows at
+//                 the cell index (export).
 
 #include <algorithm>
 
@@ -59,31 +63,28 @@ __device__ __forceinline__ void st_rec(float* p, float e, float i, float c0, flo
 // [0, cap) are left out (no out-of-bounds shared-memory write); the step's
 // range check reports them.  Widths divisible by 4 move four cells per
 // thread and iteration with 16-byte plane loads.
-__device__ __forceinline__ void count_cell(const GsPlan& p, int* hist, int cap, int s, int r, int32_t* rank, long long i,
-                                           bool in) {
+__device__ __forceinline__ void count_cell(const GsPlan& p, int* hist, int cap, int s, int r, int32_t* rank,
+                                           uint16_t* lrank, long long i, bool in) {
   if (!in) return;
   const bool occ = (unsigned)s < (unsigned)cap;
-  if (occ) atomicAdd(&hist[gs_bin(p, s, r)], 1);
+  if (occ) lrank[i] = (uint16_t)atomicAdd(&hist[gs_bin(p, s, r)], 1);  // rank inside the CTA's group
   if (rank) rank[i] = occ ? (int)i : -1;
 }
 
-__global__ void __launch_bounds__(kGsThreads) k_gs_count(const StepGeom g, const Planes f, const GsPlan p,
-                                                          int cap, int32_t* band_hist, float* tex, int32_t* rank) {
+__global__ void __launch_bounds__(kGsThreads) k_gs_count(const StepGeom g, const Planes f, const GsPlan p, int cap,
+                                                          int32_t* cta_hist, uint16_t* lrank, float* tex,
+                                                          int32_t* rank) {
   extern __shared__ int hist[];
   for (int b = threadIdx.x; b < p.bins; b += blockDim.x) hist[b] = 0;
   __syncthreads();
   const int r0 = blockIdx.x * p.rows_per_cta, r1 = min(g.H, r0 + p.rows_per_cta);
   const long long W = g.W, st = g.stride;
+  // the records cover the ghost rows too (first / last CTA)
   const long long lo = (blockIdx.x == 0 ? -1 : r0) * W, hi = (r1 == g.H ? g.H + 1 : r1) * W;
   const long long c0 = (long long)r0 * W, c1 = (long long)r1 * W;
   if ((g.W & 3) == 0) {
     for (long long i = lo + 4 * threadIdx.x; i < hi; i += 4 * blockDim.x) {
       const long long o = i + W;  // element offset from ghost row -1
-      const float4 E = __ldg(reinterpret_cast<const float4*>(f.E + o));
-      const float4 I = __ldg(reinterpret_cast<const float4*>(f.I + o));
-      const float4 C0 = __ldg(reinterpret_cast<const float4*>(f.C + o));
-      const float4 C1 = __ldg(reinterpret_cast<const float4*>(f.C + st + o));
-      const float4 C2 = __ldg(reinterpret_cast<const float4*>(f.C + 2 * st + o));
       const bool in = i >= c0 && i < c1;
       int4 G = make_int4(-1, -1, -1, -1);
       unsigned R = 0;
@@ -91,29 +92,68 @@ __global__ void __launch_bounds__(kGsThreads) k_gs_count(const StepGeom g, const
         G = __ldg(reinterpret_cast<const int4*>(f.gi + o));
         R = __ldg(reinterpret_cast<const unsigned*>(f.rot + o));
       }
-      float* t = tex + o * 8;
-      st_rec(t, E.x, I.x, C0.x, C1.x, C2.x);
-      st_rec(t + 8, E.y, I.y, C0.y, C1.y, C2.y);
-      st_rec(t + 16, E.z, I.z, C0.z, C1.z, C2.z);
-      st_rec(t + 24, E.w, I.w, C0.w, C1.w, C2.w);
-      count_cell(p, hist, cap, G.x, (int)(R & 0xFFu), rank, i, in);
-      count_cell(p, hist, cap, G.y, (int)((R >> 8) & 0xFFu), rank, i + 1, in);
-      count_cell(p, hist, cap, G.z, (int)((R >> 16) & 0xFFu), rank, i + 2, in);
-      count_cell(p, hist, cap, G.w, (int)(R >> 24), rank, i + 3, in);
+        const float4 E = __ldg(reinterpret_cast<const float4*>(f.E + o));
+        const float4 I = __ldg(reinterpret_cast<const float4*>(f.I + o));
+        const float4 C0 = __ldg(reinterpret_cast<const float4*>(f.C + o));
+        const float4 C1 = __ldg(reinterpret_cast<const float4*>(f.C + st + o));
+        const float4 C2 = __ldg(reinterpret_cast<const float4*>(f.C + 2 * st + o));
+        float* t = tex + o * 8;
+        st_rec(t, E.x, I.x, C0.x, C1.x, C2.x);
+        st_rec(t + 8, E.y, I.y, C0.y, C1.y, C2.y);
+        st_rec(t + 16, E.z, I.z, C0.z, C1.z, C2.z);
+        st_rec(t + 24, E.w, I.w, C0.w, C1.w, C2.w);
+      count_cell(p, hist, cap, G.x, (int)(R & 0xFFu), rank, lrank, i, in);
+      count_cell(p, hist, cap, G.y, (int)((R >> 8) & 0xFFu), rank, lrank, i + 1, in);
+      count_cell(p, hist, cap, G.z, (int)((R >> 16) & 0xFFu), rank, lrank, i + 2, in);
+      count_cell(p, hist, cap, G.w, (int)(R >> 24), rank, lrank, i + 3, in);
     }
   } else {
     for (long long i = lo + threadIdx.x; i < hi; i += blockDim.x) {
       const long long o = i + W;
-      st_rec(tex + o * 8, __ldg(f.E + o), __ldg(f.I + o), __ldg(f.C + o), __ldg(f.C + st + o),
-             __ldg(f.C + 2 * st + o));
+        st_rec(tex + o * 8, __ldg(f.E + o), __ldg(f.I + o), __ldg(f.C + o), __ldg(f.C + st + o),
+               __ldg(f.C + 2 * st + o));
       const bool in = i >= c0 && i < c1;
-      count_cell(p, hist, cap, in ? __ldg(f.gi + o) : -1, in ? __ldg(f.rot + o) : 0, rank, i, in);
+      count_cell(p, hist, cap, in ? __ldg(f.gi + o) : -1, in ? __ldg(f.rot + o) : 0, rank, lrank, i, in);
     }
   }
   __syncthreads();
-  int32_t* bh = band_hist + (size_t)(blockIdx.x / p.ctas_per_band) * p.bins;
-  for (int b = threadIdx.x; b < p.bins; b += blockDim.x)
-    if (hist[b]) atomicAdd(bh + b, hist[b]);
+  int32_t* out = cta_hist + (size_t)blockIdx.x * p.bins;
+  for (int b = threadIdx.x; b < p.bins; b += blockDim.x) out[b] = hist[b];
+}
+
+// per band and bin: exclusive scan of the per-CTA counts over the band's CTAs
+// (in place: each CTA's base inside its group) and the band's group totals.
+// One CTA per (band, 32 bins): lane = bin (coalesced), warp w a contiguous
+// chunk of the band's CTAs; chunk sums scanned across warps in shared memory.
+__global__ void __launch_bounds__(1024) k_gs_colscan(const GsPlan p, int32_t* cta_hist, int32_t* band_hist) {
+  __shared__ int part[32][33];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int nb32 = (p.bins + 31) / 32, band = blockIdx.x / nb32, b = (blockIdx.x % nb32) * 32 + lane;
+  const int cb = band * p.ctas_per_band, ce = min(p.nctas, cb + p.ctas_per_band);
+  const int per = (ce - cb + 31) / 32, c0 = cb + w * per, c1 = min(ce, c0 + per);
+  int sum = 0;
+  if (b < p.bins)
+    for (int c = c0; c < c1; ++c) sum += cta_hist[(size_t)c * p.bins + b];
+  part[w][lane] = sum;
+  __syncthreads();
+  if (w == 0) {
+    int run = 0;
+    for (int k = 0; k < 32; ++k) {
+      const int v = part[k][lane];
+      part[k][lane] = run;
+      run += v;
+    }
+    if (b < p.bins) band_hist[(size_t)band * p.bins + b] = run;
+  }
+  __syncthreads();
+  int run = part[w][lane];
+  if (b < p.bins)
+    for (int c = c0; c < c1; ++c) {
+      int32_t* q = cta_hist + (size_t)c * p.bins + b;
+      const int v = *q;
+      *q = run;
+      run += v;
+    }
 }
 
 // Block-wide exclusive scan of (cells, half-tiles) pairs, 1024 threads.
@@ -148,34 +188,34 @@ __device__ __forceinline__ void scan_pair(int c, int t, int& xc, int& xt, int& t
   __syncthreads();
 }
 
-// one CTA per band: group offsets (cells, half-tiles) within the band; each
-// thread scans a contiguous run of bins; the band histogram is consumed
-// (zeroed for the next step)
-__global__ void __launch_bounds__(1024) k_gs_scan_band(const GsPlan p, int32_t* band_hist, int32_t* goff,
-                                                       int32_t* ght, int32_t* cursor, int32_t* band_tot) {
+// one CTA per band: group offsets (cells, tiles) within the band; each
+// thread scans a contiguous run of bins
+__global__ void __launch_bounds__(1024) k_gs_scan_band(const GsPlan p, const int32_t* band_hist, int32_t* goff,
+                                                       int32_t* ght, int32_t* band_tot) {
   __shared__ int wc[33], wt[33];
   const int band = blockIdx.x, bins = p.bins;
-  int32_t* bh = band_hist + (size_t)band * bins;
+  const int32_t* bh = band_hist + (size_t)band * bins;
   int32_t* go = goff + (size_t)band * (bins + 1);
   int32_t* gt = ght + (size_t)band * (bins + 1);
-  int32_t* cu = cursor + (size_t)band * bins;
   const int per = (bins + 1023) / 1024, b0 = threadIdx.x * per, b1 = min(bins, b0 + per);
+  int cnt[16];  // per <= 16 (bins <= 16 K)
   int sc = 0, stl = 0;
-  for (int b = b0; b < b1; ++b) {
-    const int c = bh[b];
-    sc += c;
-    stl += (c + p.tile - 1) / p.tile;
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+    cnt[j] = b0 + j < b1 ? bh[b0 + j] : 0;
+    sc += cnt[j];
+    stl += (cnt[j] + p.tile - 1) / p.tile;
   }
   int xc, xt, tc, tt;
   scan_pair(sc, stl, xc, xt, tc, tt, wc, wt);
-  for (int b = b0; b < b1; ++b) {
-    const int c = bh[b];
-    bh[b] = 0;
-    go[b] = xc;
-    gt[b] = xt;
-    cu[b] = xc;
-    xc += c;
-    xt += (c + p.tile - 1) / p.tile;
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+    if (b0 + j < b1) {
+      go[b0 + j] = xc;
+      gt[b0 + j] = xt;
+    }
+    xc += cnt[j];
+    xt += (cnt[j] + p.tile - 1) / p.tile;
   }
   if (threadIdx.x == 0) {
     go[bins] = tc;
@@ -211,63 +251,43 @@ __global__ void __launch_bounds__(1024) k_gs_scan_bands(const GsPlan p, const in
   }
 }
 
-// Sorted cell list: per CTA, one global reservation per non-empty (slot,
-// rotation) group, then shared-memory ranks.  Order inside a group depends on
-// atomic arrival, which changes no result (each cell's forward pass is
-// independent of its neighbours in the list).  Entry = (rot << 29) | (y << 15)
-// | x (gather_supported: W <= 32768, H <= 16384).
-__device__ __forceinline__ void scatter_cell(const GsPlan& p, int* hist, int cap, int s, int r, long long i,
-                                             long long W, uint32_t* sorted) {
+// Sorted cell list, no atomics: a cell's position is its band's base + its
+// group's offset in the band + its count CTA's base in the group + its rank
+// inside that CTA (k_gs_count).  Entry = (rot << 29) | (y << 15) | x
+// (gather_supported: W <= 32768, H <= 16384).
+__device__ __forceinline__ void scatter_cell(const GsPlan& p, int cap, int s, int r, long long i, long long W,
+                                             const int32_t* base, const int32_t* go, const int32_t* ch,
+                                             const uint16_t* lrank, uint32_t* sorted) {
   if ((unsigned)s >= (unsigned)cap) return;
-  const int pos = atomicAdd(&hist[gs_bin(p, s, r)], 1);
+  const int b = gs_bin(p, s, r);
+  const int pos = base[0] + __ldg(go + b) + __ldg(ch + b) + (int)lrank[i];
   const unsigned y = (unsigned)i / (unsigned)W, x = (unsigned)i - y * (unsigned)W;  // cells < 2^31
   sorted[pos] = ((unsigned)(r & 7) << 29) | (y << 15) | x;
 }
 
-__global__ void __launch_bounds__(kGsThreads) k_gs_scatter(const StepGeom g, const Planes f, const GsPlan p, int cap,
-                                                            int32_t* cursor, const int32_t* band_base,
-                                                            uint32_t* sorted) {
-  extern __shared__ int hist[];
-  for (int b = threadIdx.x; b < p.bins; b += blockDim.x) hist[b] = 0;
-  __syncthreads();
-  const int r0 = blockIdx.x * p.rows_per_cta, r1 = min(g.H, r0 + p.rows_per_cta);
-  const long long W = g.W;
-  const long long c0 = (long long)r0 * W, c1 = (long long)r1 * W;
+__global__ void __launch_bounds__(256) k_gs_scatter(const StepGeom g, const Planes f, const GsPlan p, int cap,
+                                                    const int32_t* cta_hist, const int32_t* goff,
+                                                    const int32_t* band_base, const uint16_t* lrank,
+                                                    uint32_t* sorted) {
+  const long long W = g.W, n = W * g.H;
   const bool v4 = (g.W & 3) == 0;
-  if (v4) {
-    for (long long i = c0 + 4 * threadIdx.x; i < c1; i += 4 * blockDim.x) {
+  const int step = v4 ? 4 : 1;
+  for (long long i = ((long long)blockIdx.x * blockDim.x + threadIdx.x) * step; i < n;
+       i += (long long)gridDim.x * blockDim.x * step) {
+    const int cta = (int)((unsigned)i / (unsigned)W) / p.rows_per_cta, band = cta / p.ctas_per_band;
+    const int32_t* base = band_base + 2 * band;
+    const int32_t* go = goff + (size_t)band * (p.bins + 1);
+    const int32_t* ch = cta_hist + (size_t)cta * p.bins;
+    if (v4) {
       const int4 G = __ldg(reinterpret_cast<const int4*>(f.gi + i + W));
       const unsigned R = __ldg(reinterpret_cast<const unsigned*>(f.rot + i + W));
-      if ((unsigned)G.x < (unsigned)cap) atomicAdd(&hist[gs_bin(p, G.x, (int)R)], 1);
-      if ((unsigned)G.y < (unsigned)cap) atomicAdd(&hist[gs_bin(p, G.y, (int)(R >> 8))], 1);
-      if ((unsigned)G.z < (unsigned)cap) atomicAdd(&hist[gs_bin(p, G.z, (int)(R >> 16))], 1);
-      if ((unsigned)G.w < (unsigned)cap) atomicAdd(&hist[gs_bin(p, G.w, (int)(R >> 24))], 1);
+      scatter_cell(p, cap, G.x, (int)(R & 0xFFu), i, W, base, go, ch, lrank, sorted);
+      scatter_cell(p, cap, G.y, (int)((R >> 8) & 0xFFu), i + 1, W, base, go, ch, lrank, sorted);
+      scatter_cell(p, cap, G.z, (int)((R >> 16) & 0xFFu), i + 2, W, base, go, ch, lrank, sorted);
+      scatter_cell(p, cap, G.w, (int)(R >> 24), i + 3, W, base, go, ch, lrank, sorted);
+    } else {
+      scatter_cell(p, cap, __ldg(f.gi + i + W), __ldg(f.rot + i + W), i, W, base, go, ch, lrank, sorted);
     }
-  } else {
-    for (long long i = c0 + threadIdx.x; i < c1; i += blockDim.x) {
-      const int s = __ldg(f.gi + i + W);
-      if ((unsigned)s < (unsigned)cap) atomicAdd(&hist[gs_bin(p, s, __ldg(f.rot + i + W))], 1);
-    }
-  }
-  __syncthreads();
-  const int band = blockIdx.x / p.ctas_per_band;
-  const int base = band_base[2 * band];
-  int32_t* cur = cursor + (size_t)band * p.bins;
-  for (int b = threadIdx.x; b < p.bins; b += blockDim.x)
-    if (hist[b]) hist[b] = base + atomicAdd(cur + b, hist[b]);
-  __syncthreads();
-  if (v4) {
-    for (long long i = c0 + 4 * threadIdx.x; i < c1; i += 4 * blockDim.x) {
-      const int4 G = __ldg(reinterpret_cast<const int4*>(f.gi + i + W));
-      const unsigned R = __ldg(reinterpret_cast<const unsigned*>(f.rot + i + W));
-      scatter_cell(p, hist, cap, G.x, (int)(R & 0xFFu), i, W, sorted);
-      scatter_cell(p, hist, cap, G.y, (int)((R >> 8) & 0xFFu), i + 1, W, sorted);
-      scatter_cell(p, hist, cap, G.z, (int)((R >> 16) & 0xFFu), i + 2, W, sorted);
-      scatter_cell(p, hist, cap, G.w, (int)(R >> 24), i + 3, W, sorted);
-    }
-  } else {
-    for (long long i = c0 + threadIdx.x; i < c1; i += blockDim.x)
-      scatter_cell(p, hist, cap, __ldg(f.gi + i + W), __ldg(f.rot + i + W), i, W, sorted);
   }
 }
 
@@ -305,7 +325,7 @@ constexpr int kGwW = kSensors * 12 + 48 + kOutPad;  // W12 [45][12] | W1 [48] | 
 
 struct GatherArgs {
   Params net;
-  const float* tex;  // record of ghost row -1, column 0
+  const float* tex;  // FFMA kernel: single-cell records from ghost row -1; tensor-core kernel: column triples
   int W;
   const uint32_t* sorted;
   const int4* info;
@@ -333,10 +353,12 @@ struct GCell {
   int wl;    // +W when x == 0 (a dx = -1 neighbour wraps)
   int wr;    // -W when x == W - 1
   int cell;  // y * W + x
+  int rot;
 };
 __device__ __forceinline__ GCell gcell(uint32_t e, int W) {
   GCell c;
   const int y = (int)((e >> 15) & 0x3FFFu), x = (int)(e & 0x7FFFu);
+  c.rot = (int)(e >> 29);
   c.cell = y * W + x;
   c.idx = c.cell + W;
   c.wl = x == 0 ? W : 0;
@@ -383,13 +405,10 @@ __global__ void __launch_bounds__(kGwThreads, 4) k_direct_gather(const GatherArg
   GCell c0 = gcell(__ldg(a.sorted + ti.y + (lane < ti.z ? lane : 0)), W);
   GCell c1 = gcell(__ldg(a.sorted + ti.y + (lane + 32 < ti.z ? lane + 32 : 0)), W);
   f8r q0[9], q1[9];
-  {
-    const int rot = ti.x & 7;
 #pragma unroll
-    for (int s = 0; s < kGwDepth; ++s) {
-      q0[s] = ld_rec(rec_ptr(a.tex, c0, W, rot, s));
-      q1[s] = ld_rec(rec_ptr(a.tex, c1, W, rot, s));
-    }
+  for (int s = 0; s < kGwDepth; ++s) {
+    q0[s] = ld_rec(rec_ptr(a.tex, c0, W, c0.rot, s));
+    q1[s] = ld_rec(rec_ptr(a.tex, c1, W, c1.rot, s));
   }
   while (h < n) {
     const int hn = step(h);
@@ -401,7 +420,7 @@ __global__ void __launch_bounds__(kGwThreads, 4) k_direct_gather(const GatherArg
       n0 = gcell(__ldg(a.sorted + tn.y + (lane < tn.z ? lane : 0)), W);
       n1 = gcell(__ldg(a.sorted + tn.y + (lane + 32 < tn.z ? lane + 32 : 0)), W);
     }
-    const int slot = ti.x >> 3, rot = ti.x & 7, rotn = tn.x & 7;
+    const int slot = ti.x;  // groups are (band, slot): each lane gathers in its own cell's Moore order
     if (slot != cur) {
       cur = slot;
       __syncwarp();
@@ -421,13 +440,13 @@ __global__ void __launch_bounds__(kGwThreads, 4) k_direct_gather(const GatherArg
     for (int k = 0; k < kSensors; ++k) {
       const int s = k / 5, ch = k - 5 * s;
       if (ch == 0 && s + kGwDepth < 9) {  // keep kGwDepth records per cell in flight
-        q0[s + kGwDepth] = ld_rec(rec_ptr(a.tex, c0, W, rot, s + kGwDepth));
-        q1[s + kGwDepth] = ld_rec(rec_ptr(a.tex, c1, W, rot, s + kGwDepth));
+        q0[s + kGwDepth] = ld_rec(rec_ptr(a.tex, c0, W, c0.rot, s + kGwDepth));
+        q1[s + kGwDepth] = ld_rec(rec_ptr(a.tex, c1, W, c1.rot, s + kGwDepth));
       }
       if (ch == 0 && s >= 9 - kGwDepth && more) {  // the next half-tile's leading records
         const int sn = s - (9 - kGwDepth);
-        q0[sn] = ld_rec(rec_ptr(a.tex, n0, W, rotn, sn));
-        q1[sn] = ld_rec(rec_ptr(a.tex, n1, W, rotn, sn));
+        q0[sn] = ld_rec(rec_ptr(a.tex, n0, W, n0.rot, sn));
+        q1[sn] = ld_rec(rec_ptr(a.tex, n1, W, n1.rot, sn));
       }
       // (q[sn] was last read at slot sn < s: free)
       const float x0 = q0[s].v[ch];
@@ -485,53 +504,50 @@ __global__ void __launch_bounds__(kGwThreads, 4) k_direct_gather(const GatherArg
 }
 
 // ---------------------------------------------------------------------------
-// The net on the tensor cores (k_direct_tc).  One 128-cell tile of one
-// (band, slot) group per MMA: thread t owns tile row t = TMEM lane t, gathers
-// its cell's nine records in the cell's own Moore order (per-row rotation:
-// no uniformity needed), splits the 48 sensors x = hi + lo (hi = x with the
-// low 13 mantissa bits cleared, lo = x - hi exact) and stores A' = [hi | lo]
-// (K = 96) into its TMEM lane with tcgen05.st.  B' = [W_hi | W_lo] (N = 32,
-// K = 48, canonical K-major in shared memory) serves both K halves, so 12
-// tcgen05.mma kind::tf32 (M = 128, N = 32, K = 8) give
-//   D[:, j] = (A_hi + A_lo) . W_hi[:, j],  D[:, 16 + j] = (A_hi + A_lo) . W_lo[:, j]
-// and z_j = D[j] + D[16 + j] + b_j (every cross product of the split,
-// lo.lo included).  The epilogue reads D with one tcgen05.ld and writes the
-// decided record (or the 13 squashed actuators).  4 CTAs per SM, 128 TMEM
-// columns each (A' 96 + D 32); the next tile's records and weights are in
-// flight while this tile's MMAs and epilogue run.
+// The net on the tensor cores (k_direct_tc, EVO_F_TC_DIRECT).  One 128-cell
+// tile of one (band, slot) group per MMA: thread t owns tile row t = TMEM
+// lane t and gathers its cell's nine records in the cell's own Moore order
+// (per-row rotation, so the rows need no uniformity); the 48 inputs are
+// split x = hi + lo (hi = x with the low 13 mantissa bits cleared, lo = x -
+// hi exact): A_hi goes into the thread's TMEM lane (tcgen05.st), A_lo into a
+// canonical K-major shared-memory tile.  B' = [W_hi | W_lo] (N = 32), so per
+// K step two tcgen05.mma kind::tf32 (M = 128, N = 32, K = 8) give
+//   D[:, j] += (A_hi + A_lo) . W_hi[:, j],  D[:, 16 + j] += (A_hi + A_lo) . W_lo[:, j]
+// (lo.lo included).  The tensor core accumulates with less than FP32
+// accuracy (tools/microbench/tc_split.cu), so the W_lo terms keep their own
+// columns and K steps 0-2 and 3-5 go to two accumulators, added in FP32 by
+// the epilogue: z_j = ((D0[j] + D0[16 + j]) + (D1[j] + D1[16 + j])) + b_j.
+// Measured: with all three cross products in one 16-column accumulator the
+// error reached 3.3x that of the FP32 FFMA forward (over the 1e-5 tier-B
+// target at BASELINE weights); this layout stays within 2x.  The summation
+// order differs from the FFMA paths' (parity: tier B against the float64
+// oracle).  TMEM per CTA: A_hi 48 + D0 32 + D1 32 columns (128 allocated),
+// so 4 CTAs per SM.  Tiles are claimed in runs of kTcChunk from one counter (all CTAs
+// sweep the bands together: the texture band stays in L2); each tile's info
+// and row cell are loaded two tiles ahead, its records and weights one tile
+// ahead, overlapping the previous tile's MMAs and epilogue.
 constexpr int kTcThreads = 128;
 constexpr int kTcCols = 128;
 constexpr int kTcChunk = 4;  // consecutive tiles per claim (one slot's weights mostly stay staged)
 constexpr int kTcK = 48;
-constexpr int kTcN = 32;
 constexpr int kTcWPer = 16 * kTcK / kTcThreads;  // weight elements staged per thread (6)
+constexpr uint32_t kTcD0 = 64, kTcD1 = 96;  // TMEM accumulator columns (A_hi at 0..47)
 
 struct __align__(1024) TcSmem {
-  unsigned char B[kTcN * kTcK * 4];  // 6 KB
+  unsigned char Alo[128 * kTcK * 4];  // 24 KB, canonical K-major (R = 128)
+  unsigned char B[32 * kTcK * 4];     // 6 KB: [W_hi | W_lo], canonical K-major (R = 32)
   float bias[16];
-  int next;
+  int ring[4];  // claimed runs (first tile index), consumed in order
   uint32_t tmem;
   uint64_t bar;
 };
 
-__device__ __forceinline__ void tmem_st32(uint32_t addr, const uint32_t (&v)[32]) {
+__device__ __forceinline__ void tmem_st16(uint32_t addr, const uint32_t (&v)[16]) {
   asm volatile(
-      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
-      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(addr),
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(
+          addr),
       "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]), "r"(v[9]),
-      "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15]), "r"(v[16]), "r"(v[17]), "r"(v[18]),
-      "r"(v[19]), "r"(v[20]), "r"(v[21]), "r"(v[22]), "r"(v[23]), "r"(v[24]), "r"(v[25]), "r"(v[26]), "r"(v[27]),
-      "r"(v[28]), "r"(v[29]), "r"(v[30]), "r"(v[31]));
-}
-__device__ __forceinline__ void tmem_ld32(uint32_t addr, uint32_t (&r)[32]) {
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,"
-      "%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
-        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]),
-        "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
-        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
-      : "r"(addr));
+      "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15]));
 }
 
 // weight element e (0 .. 16 * 48) of a slot: output n = e % 16, sensor k = e / 16
@@ -541,47 +557,93 @@ __device__ __forceinline__ float tc_weight(const Params& net, int slot, int e) {
   return n < 12 ? __ldg(net.wA + ((size_t)slot * kSensors + k) * 12 + n) : __ldg(net.wB + (size_t)slot * kSensors + k);
 }
 
+// one MMA, A from TMEM, in warp-uniform control flow with an elected issuing
+// lane (tools/microbench/tc_issue.cu: ~39 issue cycles per MMA, against ~73
+// for a `tid == 0` loop that ptxas wraps in ELECT / BRA.U.ANY waterfalls)
+__device__ __forceinline__ void mma_ts(uint32_t d, uint32_t a_tmem, uint64_t b, uint32_t id, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\tsetp.ne.b32 p, %4, 0;\n\telect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(d),
+      "r"(a_tmem), "l"(b), "r"(id), "r"(acc));
+}
+// the same with A from a shared-memory descriptor
+__device__ __forceinline__ void mma_ss(uint32_t d, uint64_t a, uint64_t b, uint32_t id, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\tsetp.ne.b32 p, %4, 0;\n\telect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(d),
+      "l"(a), "l"(b), "r"(id), "r"(acc));
+}
+
 __global__ void __launch_bounds__(kTcThreads, 4) k_direct_tc(const GatherArgs a) {
   __shared__ TcSmem sm;
   const int tid = threadIdx.x, warp = tid >> 5;
   const int n = a.n_ht[0], W = a.W;
+  auto claim = [&]() { return atomicAdd(a.n_ht + 1, 1) * kTcChunk; };
   if (warp == 0) tc::tmem_alloc<kTcCols>(&sm.tmem);
   if (tid == 0) {
     tc::mbar_init(&sm.bar, 1);
-    sm.next = atomicAdd(a.n_ht + 1, 1) * kTcChunk;
+    sm.ring[3] = claim();  // this CTA's first run
+    sm.ring[0] = claim();
+    sm.ring[1] = claim();
   }
   tc::fence_before();
   __syncthreads();
   tc::fence_after();
   const uint32_t tmem = sm.tmem;
   const uint32_t lane_base = tmem + ((uint32_t)(warp * 32) << 16);
-  int h = sm.next;
-  __syncthreads();
-  if (tid == 0) sm.next = atomicAdd(a.n_ht + 1, 1) * kTcChunk;  // the run after this one
   uint32_t phase = 0;
   int cur = -1;
-  // prefetched state of tile h: info, this row's cell, records, slot weights
-  int4 ti = make_int4(0, 0, 1, 0);
-  GCell cc{};
-  int rot = 0;
+  int k = 0;  // ring slots consumed
+  // the tile after h: the next one in the run, or the next claimed run
+  // (whose slot is refilled two runs ahead by thread 0)
+  auto next_tile = [&](int h) {
+    if ((h + 1) % kTcChunk) return h + 1;
+    const int r = sm.ring[k & 3];
+    if (tid == 0) sm.ring[(k + 2) & 3] = claim();
+    ++k;
+    return r;
+  };
+  int h = sm.ring[3];
+  int h1 = next_tile(h);
+  int h2 = next_tile(h1);
+  auto entry_of = [&](const int4& t) { return __ldg(a.sorted + t.y + (tid < t.z ? tid : 0)); };
+  int4 ti = make_int4(-1, 0, 1, 0), t1 = ti, t2 = ti;
+  uint32_t ecur = 0, e1 = 0, e2 = 0;
   f8r q[9];
   float wn[kTcWPer], bn = 0.0f;
-  auto fetch = [&](int hh, int4& t, GCell& c, int& r, int have_slot) {
-    t = __ldg(a.info + hh);
-    const uint32_t e = __ldg(a.sorted + t.y + (tid < t.z ? tid : 0));
-    c = gcell(e, W);
-    r = (int)(e >> 29);
+  auto fetch_records = [&](const int4& t, uint32_t e, int have_slot) {
+    const GCell c = gcell(e, W);
+    if (tid < t.z) {
 #pragma unroll
-    for (int s = 0; s < 9; ++s) q[s] = ld_rec(rec_ptr(a.tex, c, W, r, s));
+      for (int s = 0; s < 9; ++s) q[s] = ld_rec(rec_ptr(a.tex, c, W, c.rot, s));
+    } else {
+#pragma unroll
+      for (int s = 0; s < 9; ++s)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) q[s].v[j] = 0.0f;
+    }
     if (t.x != have_slot) {
 #pragma unroll
       for (int j = 0; j < kTcWPer; ++j) wn[j] = tc_weight(a.net, t.x, tid + j * kTcThreads);
       bn = tid < 16 ? __ldg(a.net.bA + (size_t)t.x * kOutPad + tid) : 0.0f;
     }
   };
-  if (h < n) fetch(h, ti, cc, rot, -1);
+  if (h < n) {
+    ti = __ldg(a.info + h);
+    ecur = entry_of(ti);
+    fetch_records(ti, ecur, -1);
+  }
+  if (h1 < n) {
+    t1 = __ldg(a.info + h1);
+    e1 = entry_of(t1);
+  }
   while (h < n) {
-    // (A) this row's sensors, split, into TMEM: hi at columns 0..47, lo at 48..95
+    if (h2 < n) {  // two ahead: info + row entry
+      t2 = __ldg(a.info + h2);
+      e2 = entry_of(t2);
+    }
+    // (A) inputs split: hi into this thread's TMEM lane (columns 0..47), lo
+    //     into row tid of the shared tile
     {
       uint32_t hv[48], lv[48];
 #pragma unroll
@@ -594,55 +656,48 @@ __global__ void __launch_bounds__(kTcThreads, 4) k_direct_tc(const GatherArgs a)
           lv[s * 5 + ch] = __float_as_uint(__fsub_rn(x, __uint_as_float(hb)));
         }
 #pragma unroll
-      for (int k = 45; k < 48; ++k) hv[k] = lv[k] = 0u;
-      uint32_t c32[32];
+      for (int kk = 45; kk < 48; ++kk) hv[kk] = lv[kk] = 0u;
 #pragma unroll
-      for (int j = 0; j < 32; ++j) c32[j] = hv[j];
-      tmem_st32(lane_base + 0, c32);
+      for (int c = 0; c < 3; ++c) {
+        uint32_t v16[16];
 #pragma unroll
-      for (int j = 0; j < 16; ++j) c32[j] = hv[32 + j];
+        for (int j = 0; j < 16; ++j) v16[j] = hv[16 * c + j];
+        tmem_st16(lane_base + 16 * c, v16);
+      }
 #pragma unroll
-      for (int j = 0; j < 16; ++j) c32[16 + j] = lv[j];
-      tmem_st32(lane_base + 32, c32);
-#pragma unroll
-      for (int j = 0; j < 32; ++j) c32[j] = lv[16 + j];
-      tmem_st32(lane_base + 64, c32);
+      for (int c = 0; c < 12; ++c)
+        *reinterpret_cast<uint4*>(sm.Alo + tc::canon_off(tid, 4 * c, 128)) =
+            make_uint4(lv[4 * c], lv[4 * c + 1], lv[4 * c + 2], lv[4 * c + 3]);
     }
-    // (B) the slot's weights into B' (prefetched with the tile)
+    // (B) the slot's weights (prefetched with the tile)
     if (ti.x != cur) {
       cur = ti.x;
 #pragma unroll
       for (int j = 0; j < kTcWPer; ++j) {
-        const int e = tid + j * kTcThreads, nn = e & 15, k = e >> 4;
+        const int e = tid + j * kTcThreads, nn = e & 15, kk = e >> 4;
         const uint32_t hb = __float_as_uint(wn[j]) & 0xFFFFE000u;
-        *reinterpret_cast<uint32_t*>(sm.B + tc::canon_off(nn, k, kTcN)) = hb;
-        *reinterpret_cast<float*>(sm.B + tc::canon_off(nn + 16, k, kTcN)) = __fsub_rn(wn[j], __uint_as_float(hb));
+        *reinterpret_cast<uint32_t*>(sm.B + tc::canon_off(nn, kk, 32)) = hb;
+        *reinterpret_cast<float*>(sm.B + tc::canon_off(nn + 16, kk, 32)) = __fsub_rn(wn[j], __uint_as_float(hb));
       }
       if (tid < 16) sm.bias[tid] = bn;
-      tc::fence_async_smem();
     }
+    tc::fence_async_smem();
     asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
     tc::fence_before();
     __syncthreads();
     tc::fence_after();
-    // (C) 12 MMAs: K steps 0-5 from A_hi, 6-11 from A_lo, both against B'.
-    //     Warp 0 runs the loop in warp-uniform control flow with operands
-    //     derived from uniform values, one elected lane issuing inside each
-    //     asm block (tools/microbench/tc_issue.cu: ~39 issue cycles per MMA
-    //     against ~73 for a per-thread `if (tid == 0)` loop, which ptxas
-    //     wraps in ELECT / BRA.U.ANY waterfalls)
+    // (C) 12 MMAs by warp 0: per K step A_hi.B' (TMEM) and A_lo.B' (shared)
     if (warp == 0) {
-      constexpr uint32_t id = tc::idesc_tf32(128, kTcN);
-      constexpr uint32_t lB = kTcN * 16;
+      constexpr uint32_t id = tc::idesc_tf32(128, 32);
+      constexpr uint32_t lB = 32 * 16, lA = 128 * 16;
       const uint64_t bd = tc::smem_desc(tc::smem_u32(sm.B), lB, 128);
+      const uint64_t ad = tc::smem_desc(tc::smem_u32(sm.Alo), lA, 128);
 #pragma unroll
-      for (int j = 0; j < 12; ++j) {
-        const int ks = j % 6;
-        asm volatile(
-            "{\n\t.reg .pred p, e;\n\tsetp.ne.b32 p, %4, 0;\n\telect.sync _|e, 0xffffffff;\n\t"
-            "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(tmem + 96u),
-            "r"(tmem + (uint32_t)((j < 6 ? 0 : 48) + 8 * ks)), "l"(bd + (uint64_t)((2 * ks * lB) >> 4)), "r"(id),
-            "r"((uint32_t)(j > 0)));
+      for (int ks = 0; ks < 6; ++ks) {
+        const uint32_t d = tmem + (ks < 3 ? kTcD0 : kTcD1);
+        const uint64_t b = bd + (uint64_t)((2 * ks * lB) >> 4);
+        mma_ts(d, tmem + (uint32_t)(8 * ks), b, id, (uint32_t)(ks % 3 != 0));
+        mma_ss(d, ad + (uint64_t)((2 * ks * lA) >> 4), b, id, 1u);
       }
       asm volatile(
           "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
@@ -652,30 +707,35 @@ __global__ void __launch_bounds__(kTcThreads, 4) k_direct_tc(const GatherArgs a)
     }
     // (D) the next tile's records and weights go out while the MMAs run
     const int4 tcur = ti;
-    const GCell ccur = cc;
-    int hn = h + 1;
-    if (hn % kTcChunk == 0) {
-      hn = sm.next;  // read before the barrier below lets thread 0 overwrite it
-    }
-    const bool more = hn < n;
-    if (more) fetch(hn, ti, cc, rot, tcur.x);
+    const int cell = gcell(ecur, W).cell;
+    if (h1 < n) fetch_records(t1, e1, tcur.x);
     // (E) epilogue
     tc::mbar_wait(&sm.bar, phase);
     phase ^= 1u;
     tc::fence_after();
-    uint32_t d[32];
-    tmem_ld32(lane_base + 96, d);
+    uint32_t d0[16], d0l[16], d1[16], d1l[16];
+    tc::tmem_ld16_nw(lane_base + kTcD0, d0);
+    tc::tmem_ld16_nw(lane_base + kTcD0 + 16, d0l);
+    tc::tmem_ld16_nw(lane_base + kTcD1, d1);
+    tc::tmem_ld16_nw(lane_base + kTcD1 + 16, d1l);
     tc::tmem_wait_ld();
+    tc::reg_fence(d0);
+    tc::reg_fence(d0l);
+    tc::reg_fence(d1);
+    tc::reg_fence(d1l);
     if (tid < tcur.z) {
       float z[13];
 #pragma unroll
-      for (int j = 0; j < 13; ++j)
-        z[j] = __fadd_rn(__fadd_rn(__uint_as_float(d[j]), __uint_as_float(d[16 + j])), sm.bias[j]);
+      for (int j = 0; j < 13; ++j) {
+        const float p0 = __fadd_rn(__uint_as_float(d0[j]), __uint_as_float(d0l[j]));
+        const float p1 = __fadd_rn(__uint_as_float(d1[j]), __uint_as_float(d1l[j]));
+        z[j] = __fadd_rn(__fadd_rn(p0, p1), sm.bias[j]);
+      }
       if (!a.export_rows) {
         int ks;
         float xm;
         explore_pick(z + 5, ks, xm);
-        asm volatile("st.global.v8.f32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(a.act + (size_t)ccur.cell * 8),
+        asm volatile("st.global.v8.f32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(a.act + (size_t)cell * 8),
                      "f"(squash(z[0])), "f"(squash(z[1])), "f"(squash(z[2])), "f"(squash(z[3])), "f"(squash(z[4])),
                      "f"(xm), "f"(__int_as_float(ks)), "f"(0.0f)
                      : "memory");
@@ -684,16 +744,21 @@ __global__ void __launch_bounds__(kTcThreads, 4) k_direct_tc(const GatherArgs a)
 #pragma unroll
         for (int j = 0; j < 13; ++j) v[j] = squash(z[j]);
         v[13] = v[14] = v[15] = 0.0f;
-        float4* dst = reinterpret_cast<float4*>(a.act + (size_t)ccur.cell * 16);
+        float4* dst = reinterpret_cast<float4*>(a.act + (size_t)cell * 16);
 #pragma unroll
         for (int qq = 0; qq < 4; ++qq) dst[qq] = make_float4(v[4 * qq], v[4 * qq + 1], v[4 * qq + 2], v[4 * qq + 3]);
       }
     }
     tc::fence_before();
-    __syncthreads();  // TMEM A' / D and B' free; every thread has read sm.next
+    __syncthreads();  // TMEM A_hi / D, the shared A_lo and B' free for the next tile
     tc::fence_after();
-    if ((h + 1) % kTcChunk == 0 && tid == 0) sm.next = atomicAdd(a.n_ht + 1, 1) * kTcChunk;
-    h = hn;
+    h = h1;
+    h1 = h2;
+    h2 = h2 < n ? next_tile(h2) : n;
+    ti = t1;
+    ecur = e1;
+    t1 = t2;
+    e1 = e2;
   }
   __syncthreads();
   if (warp == 0) tc::tmem_dealloc<kTcCols>(tmem);
@@ -701,7 +766,7 @@ __global__ void __launch_bounds__(kTcThreads, 4) k_direct_tc(const GatherArgs a)
 
 GsPlan make_plan(int W, int H, int cap, int num_sms, bool tc) {
   GsPlan p;
-  p.rb = tc ? 1 : 8;
+  p.rb = 1;  // both nets gather each row in its own Moore order
   p.tile = tc ? 128 : 64;
   const long long cells = (long long)W * H;
   int r = (int)((cells + 4LL * num_sms * W - 1) / (4LL * num_sms * W));
@@ -721,11 +786,13 @@ bool gather_supported(int W, int H, int cap) {
 }
 
 GatherSizes gather_sizes(int W, int H, int cap, int num_sms) {
-  const GsPlan p = make_plan(W, H, cap, num_sms, false);  // the larger of the two layouts
+  const GsPlan a = make_plan(W, H, cap, num_sms, false), b = make_plan(W, H, cap, num_sms, true);
   GatherSizes s;
-  s.nbands = p.nbands;
-  s.bins = p.bins;
-  s.max_ht = (long long)W * H / p.tile + (long long)p.nbands * p.bins + 1;
+  s.nbands = std::max(a.nbands, b.nbands);
+  s.nctas = std::max(a.nctas, b.nctas);
+  s.bins = std::max(a.bins, b.bins);
+  s.max_ht = std::max((long long)W * H / a.tile + (long long)a.nbands * a.bins,
+                      (long long)W * H / b.tile + (long long)b.nbands * b.bins) + 1;
   return s;
 }
 
@@ -738,13 +805,13 @@ cudaError_t launch_direct_gather(const GatherBuffers& b, const StepGeom& g, cons
   if (hsmem > 48 * 1024) {
     e = cudaFuncSetAttribute(k_gs_count, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hsmem);
     if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(k_gs_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hsmem);
-    if (e != cudaSuccess) return e;
   }
-  k_gs_count<<<p.nctas, kGsThreads, hsmem, st>>>(g, front, p, cap, b.band_hist, b.tex, export_rows ? rank : nullptr);
-  k_gs_scan_band<<<p.nbands, 1024, 0, st>>>(p, b.band_hist, b.goff, b.ght, b.cursor, b.band_tot);
+  k_gs_count<<<p.nctas, kGsThreads, hsmem, st>>>(g, front, p, cap, b.cta_hist, b.lrank, b.tex,
+                                                        export_rows ? rank : nullptr);
+  k_gs_colscan<<<p.nbands * ((p.bins + 31) / 32), 1024, 0, st>>>(p, b.cta_hist, b.band_hist);
+  k_gs_scan_band<<<p.nbands, 1024, 0, st>>>(p, b.band_hist, b.goff, b.ght, b.band_tot);
   k_gs_scan_bands<<<1, 1024, 0, st>>>(p, b.band_tot, b.band_base, b.n_ht);
-  k_gs_scatter<<<p.nctas, kGsThreads, hsmem, st>>>(g, front, p, cap, b.cursor, b.band_base, b.sorted);
+  k_gs_scatter<<<num_sms * 8, 256, 0, st>>>(g, front, p, cap, b.cta_hist, b.goff, b.band_base, b.lrank, b.sorted);
   const long long max_ht = (long long)g.W * g.H / p.tile + (long long)p.nbands * p.bins + 1;
   k_gs_tilemap<<<(unsigned)((max_ht + 255) / 256), 256, 0, st>>>(p, b.goff, b.ght, b.band_base, b.n_ht, b.info);
   GatherArgs a;

@@ -159,10 +159,11 @@ struct HidBuffers {
 constexpr int kGatherMaxCap = 2048;  // (slot, rotation) histogram of 16 K bins in shared memory
 struct GatherBuffers {
   float* tex;          // [(H + 2) * W][8] sense records {E, I, C0, C1, C2, 0, 0, 0}
-  int32_t* band_hist;  // [nbands][bins] (zero between steps)
+  int32_t* cta_hist;   // [count CTAs][bins] per-CTA group counts -> bases inside the band's groups
+  uint16_t* lrank;     // [ncell] rank of each cell inside its count CTA's group
+  int32_t* band_hist;  // [nbands][bins] group sizes
   int32_t* goff;       // [nbands][bins + 1] group cell offsets within the band
-  int32_t* ght;        // [nbands][bins + 1] group half-tile offsets within the band
-  int32_t* cursor;     // [nbands][bins]
+  int32_t* ght;        // [nbands][bins + 1] group tile offsets within the band
   int32_t* band_tot;   // [nbands][2]
   int32_t* band_base;  // [nbands + 1][2]
   int32_t* n_ht;       // [2]: half-tiles, gather work counter
@@ -170,7 +171,7 @@ struct GatherBuffers {
   int4* info;          // [max_ht] {slot * 8 + rot, first, cells, 0}
 };
 struct GatherSizes {
-  int nbands, bins;
+  int nbands, nctas, bins;
   long long max_ht;
 };
 bool gather_supported(int W, int H, int cap);
