@@ -260,13 +260,24 @@ def run_ours(args, rank, world, local):
 
     if rank != 0:
         return None
-    # which pass-1 pipeline the library ran (evo_pass1): per-tile fused kernel
-    # for small direct pools, genome-sorted rows otherwise
-    rows_path = cfg.hidden > 0 or max(cfg.capacity, cfg.genomes) > 68
-    p1_name = ("pass-1 pipeline on genome-sorted rows (7 launches: sort x4, k_hid_sense, "
-               + ("k_hid_net tcgen05 3xTF32 MLP" if cfg.hidden else "k_direct_rows CUDA-core net")
-               + ", k_physics_rows)") if rows_path else "k_pass1_direct (pass 1: sense+net+physics)"
-    launches_per_step = (8 if rows_path else 2) + (5 if strips else 0)  # strips: halo pack/unpack x2, census epilogue
+    # which pass-1 pipeline the library ran (evo_pass1): the
+    # per-tile fused kernel for small direct pools, the gather path for large
+    # direct pools, genome-sorted rows + tcgen05 for hidden-layer nets
+    cap = max(cfg.capacity, cfg.genomes)
+    if cfg.hidden > 0:
+        p1_name = ("pass-1 pipeline on genome-sorted rows (7 launches: sort x4, k_hid_sense, "
+                   "k_hid_net tcgen05 3xTF32 MLP, k_physics_rows)")
+        launches_per_step = 8
+    elif cap > 68:
+        p1_name = ("pass-1 pipeline, gather path (8 launches: k_gs_count sense texture + slot ranks, "
+                   "k_gs_colscan, k_gs_scan_band, k_gs_scan_bands, k_gs_scatter, k_gs_tilemap, "
+                   "k_direct_gather FFMA2 net, k_physics_rows)")
+        launches_per_step = 9
+    else:
+        p1_name = "k_pass1_direct (pass 1: sense+net+physics)"
+        launches_per_step = 2
+    rows_path = cap > 68 or cfg.hidden > 0
+    launches_per_step += 5 if strips else 0  # strips: halo pack/unpack x2, census epilogue
     n_rad = sum(1 for i in range(args.steps) if radiate and (t - args.steps + i + 1) % cfg.radiation_every == 0)
     hbm, hbm_kind, pk = peaks()
     step_s = total_ms / 1e3 / args.steps
@@ -275,8 +286,8 @@ def run_ours(args, rank, world, local):
     k1_s, k2_s = k1 / 1e3 / args.steps, k2 / 1e3 / args.steps
     # DRAM read + write bytes of the dominant launch(es) per step, from an ncu
     # capture of this workload (profiles/ncu_traffic.json, tools/traffic_json.py):
-    # the pass-1 pipeline's total on the genome-sorted rows path, the fused
-    # kernel's on the tile path
+    # the pass-1 pipeline's total on the gather / genome-sorted paths, the
+    # fused kernel's on the tile path
     traffic = None
     prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(prof) and not strips:

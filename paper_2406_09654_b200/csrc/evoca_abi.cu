@@ -423,9 +423,9 @@ int pass1_view(evo_ctx* c, const View& v, const evo_scalars* s, int phases, int 
     CK(evo::launch_hidden_tc(c->hid, v.g, v.front, c->params(), c->cap, c->num_sms, /*decided=*/!exp, st));
   }
   if (gather_net) {  // rows (export) or decided records at the cell index; rank = identity for occupied cells
-    const bool tc = (flags & EVO_F_TC_DIRECT) != 0;
+    const int variant = (flags & EVO_F_TC_DIRECT) ? evo::kGatherTc : evo::kGatherFfma2;
     if (int r = ensure_gather(c)) return r;
-    CK(evo::launch_direct_gather(c->gat, v.g, v.front, c->params(), c->cap, c->num_sms, tc, exp, c->hid.act,
+    CK(evo::launch_direct_gather(c->gat, v.g, v.front, c->params(), c->cap, c->num_sms, variant, exp, c->hid.act,
                                  c->hid.rank, st));
   }
   const bool via_rows = tc_net || rows_net || gather_net;

@@ -319,7 +319,6 @@ __global__ void k_gs_tilemap(const GsPlan p, const int32_t* goff, const int32_t*
 // the net
 constexpr int kGwWarps = 4;
 constexpr int kGwThreads = kGwWarps * 32;
-constexpr int kGwDepth = 3;  // Moore-slot records per cell in flight
 constexpr int kGwChunk = 8;  // consecutive half-tiles per warp turn (band locality: one turn of all warps ~1.2 M cells)
 constexpr int kGwW = kSensors * 12 + 48 + kOutPad;  // W12 [45][12] | W1 [48] | bias [16]
 
@@ -374,16 +373,23 @@ __device__ __forceinline__ const float* rec_ptr(const float* tex, const GCell& c
   return tex + (size_t)i * 8;
 }
 
-__global__ void __launch_bounds__(kGwThreads, 4) k_direct_gather(const GatherArgs a) {
+// C cells per lane (a warp takes a tile of 32 C cells of one slot); D Moore
+// records per cell in flight.  C = 2, D = 3: 16 warps per SM (four resident
+// CTAs).  Measured: C = 4 (half the weight broadcasts per cell, 12 warps per
+// SM, 168 registers) took 1.54 ms against 1.05 ms on config 3 - fewer,
+// larger tiles in flight spread over more of the band and the DRAM reads of
+// the texture doubled.
+template <int C, int D>
+__global__ void __launch_bounds__(kGwThreads, C == 2 ? 4 : 3) k_direct_gather(const GatherArgs a) {
   __shared__ __align__(16) float wsm[kGwWarps][kGwW];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   float* W12 = wsm[warp];
   float* W1 = W12 + kSensors * 12;
   float* Bs = W1 + 48;
   const int n = a.n_ht[0], W = a.W;
-  // Half-tiles are handed out in runs of kGwChunk from one counter, so all
-  // warps work on neighbouring runs: the texture band they gather from and
-  // the records they write stay in L2.  The run after next is claimed when a
+  // Tiles are handed out in runs of kGwChunk from one counter, so all warps
+  // work on neighbouring runs: the texture band they gather from and the
+  // records they write stay in L2.  The run after next is claimed when a
   // run starts, hiding the atomic's latency.
   auto claim = [&]() {
     int v = 0;
@@ -400,25 +406,32 @@ __global__ void __launch_bounds__(kGwThreads, 4) k_direct_gather(const GatherArg
     queued = claim();
     return q;
   };
+  auto cells_of = [&](const int4& t, GCell (&c)[C]) {
+#pragma unroll
+    for (int j = 0; j < C; ++j) {
+      const int r = lane + 32 * j;
+      c[j] = gcell(__ldg(a.sorted + t.y + (r < t.z ? r : 0)), W);
+    }
+  };
   int cur = -1;
   int4 ti = __ldg(a.info + h);
-  GCell c0 = gcell(__ldg(a.sorted + ti.y + (lane < ti.z ? lane : 0)), W);
-  GCell c1 = gcell(__ldg(a.sorted + ti.y + (lane + 32 < ti.z ? lane + 32 : 0)), W);
-  f8r q0[9], q1[9];
+  GCell cc[C];
+  cells_of(ti, cc);
+  f8r q[C][9];
 #pragma unroll
-  for (int s = 0; s < kGwDepth; ++s) {
-    q0[s] = ld_rec(rec_ptr(a.tex, c0, W, c0.rot, s));
-    q1[s] = ld_rec(rec_ptr(a.tex, c1, W, c1.rot, s));
-  }
+  for (int s = 0; s < D; ++s)
+#pragma unroll
+    for (int j = 0; j < C; ++j) q[j][s] = ld_rec(rec_ptr(a.tex, cc[j], W, cc[j].rot, s));
   while (h < n) {
     const int hn = step(h);
     const bool more = hn < n;
     int4 tn = make_int4(0, 0, 1, 0);
-    GCell n0 = c0, n1 = c1;
+    GCell nc[C];
+#pragma unroll
+    for (int j = 0; j < C; ++j) nc[j] = cc[j];
     if (more) {
       tn = __ldg(a.info + hn);
-      n0 = gcell(__ldg(a.sorted + tn.y + (lane < tn.z ? lane : 0)), W);
-      n1 = gcell(__ldg(a.sorted + tn.y + (lane + 32 < tn.z ? lane + 32 : 0)), W);
+      cells_of(tn, nc);
     }
     const int slot = ti.x;  // groups are (band, slot): each lane gathers in its own cell's Moore order
     if (slot != cur) {
@@ -430,43 +443,42 @@ __global__ void __launch_bounds__(kGwThreads, 4) k_direct_gather(const GatherArg
       if (lane < kOutPad) Bs[lane] = __ldg(a.net.bA + (size_t)cur * kOutPad + lane);
       __syncwarp();
     }
-    u64 acc[2][6];
-    float acc12[2] = {0.0f, 0.0f};
+    u64 acc[C][6];
+    float acc12[C];
 #pragma unroll
-    for (int c = 0; c < 2; ++c)
+    for (int c = 0; c < C; ++c) {
+      acc12[c] = 0.0f;
 #pragma unroll
       for (int p = 0; p < 6; ++p) acc[c][p] = 0ull;
+    }
 #pragma unroll
     for (int k = 0; k < kSensors; ++k) {
       const int s = k / 5, ch = k - 5 * s;
-      if (ch == 0 && s + kGwDepth < 9) {  // keep kGwDepth records per cell in flight
-        q0[s + kGwDepth] = ld_rec(rec_ptr(a.tex, c0, W, c0.rot, s + kGwDepth));
-        q1[s + kGwDepth] = ld_rec(rec_ptr(a.tex, c1, W, c1.rot, s + kGwDepth));
+      if (ch == 0 && s + D < 9) {  // keep D records per cell in flight
+#pragma unroll
+        for (int j = 0; j < C; ++j) q[j][s + D] = ld_rec(rec_ptr(a.tex, cc[j], W, cc[j].rot, s + D));
       }
-      if (ch == 0 && s >= 9 - kGwDepth && more) {  // the next half-tile's leading records
-        const int sn = s - (9 - kGwDepth);
-        q0[sn] = ld_rec(rec_ptr(a.tex, n0, W, n0.rot, sn));
-        q1[sn] = ld_rec(rec_ptr(a.tex, n1, W, n1.rot, sn));
+      if (ch == 0 && s >= 9 - D && more) {  // the next tile's leading records (q[j][sn] was last read at slot sn < s)
+        const int sn = s - (9 - D);
+#pragma unroll
+        for (int j = 0; j < C; ++j) q[j][sn] = ld_rec(rec_ptr(a.tex, nc[j], W, nc[j].rot, sn));
       }
-      // (q[sn] was last read at slot sn < s: free)
-      const float x0 = q0[s].v[ch];
-      const float x1 = q1[s].v[ch];
       const float4* w4 = reinterpret_cast<const float4*>(W12 + k * 12);
       const float4 wa = w4[0], wb = w4[1], wc = w4[2];
       const u64 wp[6] = {pk2(wa.x, wa.y), pk2(wa.z, wa.w), pk2(wb.x, wb.y),
                          pk2(wb.z, wb.w), pk2(wc.x, wc.y), pk2(wc.z, wc.w)};
       const float w12 = W1[k];
 #pragma unroll
-      for (int p = 0; p < 6; ++p) {
-        ffma2(acc[0][p], x0, wp[p]);
-        ffma2(acc[1][p], x1, wp[p]);
+      for (int c = 0; c < C; ++c) {
+        const float x = q[c][s].v[ch];
+#pragma unroll
+        for (int p = 0; p < 6; ++p) ffma2(acc[c][p], x, wp[p]);
+        acc12[c] = fmaf(x, w12, acc12[c]);
       }
-      acc12[0] = fmaf(x0, w12, acc12[0]);
-      acc12[1] = fmaf(x1, w12, acc12[1]);
     }
 #pragma unroll
-    for (int c = 0; c < 2; ++c) {
-      const int r = c ? lane + 32 : lane;
+    for (int c = 0; c < C; ++c) {
+      const int r = lane + 32 * c;
       if (r >= ti.z) continue;
       float z[13];
 #pragma unroll
@@ -477,7 +489,7 @@ __global__ void __launch_bounds__(kGwThreads, 4) k_direct_gather(const GatherArg
         z[2 * p + 1] = __fadd_rn(hi, Bs[2 * p + 1]);
       }
       z[12] = __fadd_rn(acc12[c], Bs[12]);
-      const int cell = c ? c1.cell : c0.cell;
+      const int cell = cc[c].cell;
       if (!a.export_rows) {  // 32 bytes at the cell index (explore_pick is exact)
         int ks;
         float xm;
@@ -493,13 +505,13 @@ __global__ void __launch_bounds__(kGwThreads, 4) k_direct_gather(const GatherArg
         v[13] = v[14] = v[15] = 0.0f;
         float4* dst = reinterpret_cast<float4*>(a.act + (size_t)cell * 16);
 #pragma unroll
-        for (int q = 0; q < 4; ++q) dst[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+        for (int qq = 0; qq < 4; ++qq) dst[qq] = make_float4(v[4 * qq], v[4 * qq + 1], v[4 * qq + 2], v[4 * qq + 3]);
       }
     }
     h = hn;
     ti = tn;
-    c0 = n0;
-    c1 = n1;
+#pragma unroll
+    for (int j = 0; j < C; ++j) cc[j] = nc[j];
   }
 }
 
@@ -764,10 +776,10 @@ __global__ void __launch_bounds__(kTcThreads, 4) k_direct_tc(const GatherArgs a)
   if (warp == 0) tc::tmem_dealloc<kTcCols>(tmem);
 }
 
-GsPlan make_plan(int W, int H, int cap, int num_sms, bool tc) {
+GsPlan make_plan(int W, int H, int cap, int num_sms, int tile) {
   GsPlan p;
   p.rb = 1;  // both nets gather each row in its own Moore order
-  p.tile = tc ? 128 : 64;
+  p.tile = tile;
   const long long cells = (long long)W * H;
   int r = (int)((cells + 4LL * num_sms * W - 1) / (4LL * num_sms * W));
   r = std::max(1, std::min(r, std::max(1, 65536 / W)));
@@ -786,7 +798,7 @@ bool gather_supported(int W, int H, int cap) {
 }
 
 GatherSizes gather_sizes(int W, int H, int cap, int num_sms) {
-  const GsPlan a = make_plan(W, H, cap, num_sms, false), b = make_plan(W, H, cap, num_sms, true);
+  const GsPlan a = make_plan(W, H, cap, num_sms, 64), b = make_plan(W, H, cap, num_sms, 128);
   GatherSizes s;
   s.nbands = std::max(a.nbands, b.nbands);
   s.nctas = std::max(a.nctas, b.nctas);
@@ -797,9 +809,10 @@ GatherSizes gather_sizes(int W, int H, int cap, int num_sms) {
 }
 
 cudaError_t launch_direct_gather(const GatherBuffers& b, const StepGeom& g, const Planes& front, const Params& net,
-                                 int cap, int num_sms, bool tc, bool export_rows, float* act, int32_t* rank,
+                                 int cap, int num_sms, int variant, bool export_rows, float* act, int32_t* rank,
                                  cudaStream_t st) {
-  const GsPlan p = make_plan(g.W, g.H, cap, num_sms, tc);
+  const bool tc = variant == kGatherTc;
+  const GsPlan p = make_plan(g.W, g.H, cap, num_sms, tc ? 128 : 64);
   const size_t hsmem = (size_t)p.bins * 4;
   cudaError_t e = cudaSuccess;
   if (hsmem > 48 * 1024) {
@@ -826,7 +839,7 @@ cudaError_t launch_direct_gather(const GatherBuffers& b, const StepGeom& g, cons
   if (tc)
     k_direct_tc<<<num_sms * 4, kTcThreads, 0, st>>>(a);  // 4 CTAs per SM, 128 TMEM columns each
   else
-    k_direct_gather<<<num_sms * 4, kGwThreads, 0, st>>>(a);  // 16 warps per SM, one wave
+    k_direct_gather<2, 3><<<num_sms * 4, kGwThreads, 0, st>>>(a);  // 16 warps per SM, one wave
   return cudaGetLastError();
 }
 

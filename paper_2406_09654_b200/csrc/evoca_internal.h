@@ -176,8 +176,9 @@ struct GatherSizes {
 };
 bool gather_supported(int W, int H, int cap);
 GatherSizes gather_sizes(int W, int H, int cap, int num_sms);
+constexpr int kGatherFfma2 = 0, kGatherTc = 2;  // net variants of the gather path
 cudaError_t launch_direct_gather(const GatherBuffers& b, const StepGeom& g, const Planes& front, const Params& net,
-                                 int cap, int num_sms, bool tc, bool export_rows, float* act, int32_t* rank,
+                                 int cap, int num_sms, int variant, bool export_rows, float* act, int32_t* rank,
                                  cudaStream_t st);
 
 bool hidden_tc_supported(int hidden);
