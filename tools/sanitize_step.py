@@ -3,8 +3,8 @@ compute-sanitizer (memcheck / racecheck / synccheck, one tool per run):
 
     compute-sanitizer --tool racecheck python tools/sanitize_step.py
 
-Paths: the per-tile direct kernel (export and not), genome-sorted rows for a
-large direct pool, the cluster-sharded tile kernel, the hidden-layer net on
+Paths: the per-tile direct kernel (export and not), the gather path (FFMA2
+and tcgen05 nets) and genome-sorted rows for a large direct pool, the cluster-sharded tile kernel, the hidden-layer net on
 the tensor cores and on the CUDA cores, injected actions, pass 2 with events,
 strips with halo exchange, the CPPN expression kernel, field-radiation
 selection / remap, render, MSC and plane sums; 64x64 and 256x256."""
@@ -53,7 +53,8 @@ def main():
     ex, rec = _lib.F_EXPORT_ACTIONS, _lib.F_RECORD_EVENTS
     for n in (64, 256):
         world(n, 8, 0, [0, ex | rec, _lib.F_MMA_NET])                           # per-tile direct kernel
-        world(n, 300, 0, [0, ex, _lib.F_SHARD_NET, _lib.F_TILE_NET])           # rows / sharded / tile
+        world(n, 300, 0, [0, ex, _lib.F_TC_DIRECT, _lib.F_TC_DIRECT | ex,      # gather (FFMA2 / tcgen05)
+                          _lib.F_ROWS_NET, _lib.F_SHARD_NET, _lib.F_TILE_NET])   # rows / sharded / tile
         world(n, 20, 128, [0, ex, _lib.F_CUDA_CORE_NET])                        # tcgen05 hidden net
         world(n, 6, 16, [0, _lib.F_TC_NET])                                     # narrow hidden layer
     # strips (halo pack / unpack, census finish)
