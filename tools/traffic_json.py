@@ -32,19 +32,29 @@ def launches(path):
     return [per[i] for i in order]
 
 
+RADIATION = ("k_occ_count", "k_chunk_scan", "k_select", "k_express_cppn", "k_remap", "k_check_cells")
+
+
+def _bytes(r):
+    return r.get("dram__bytes_read.sum", 0.0) + r.get("dram__bytes_write.sum", 0.0)
+
+
 def summarise(path):
-    ls = launches(path)
+    ls = [r for r in launches(path) if "k_" in r["name"] and not any(k in r["name"] for k in RADIATION)]
     last = {}
     for rec in ls:
-        last[rec["name"]] = rec.get("dram__bytes_read.sum", 0.0) + rec.get("dram__bytes_write.sum", 0.0)
-    # one step: the launches between the last two pass-2 launches
+        last[rec["name"]] = _bytes(rec)
+    # one full-size step: of the stretches between consecutive pass-2 launches
+    # (the bench's e2e steps run in row bands, smaller), the median
     p2 = [i for i, r in enumerate(ls) if "k_resolve" in r["name"]]
-    step = ls[p2[-2] + 1:p2[-1] + 1] if len(p2) >= 2 else ls
-    p1 = sum(r.get("dram__bytes_read.sum", 0) + r.get("dram__bytes_write.sum", 0) for r in step
-             if "k_resolve" not in r["name"])
-    return {"per_kernel_dram_bytes_per_launch": last, "pass1_dram_bytes_per_step": p1,
-            "pass2_dram_bytes_per_step": sum(r.get("dram__bytes_read.sum", 0) + r.get("dram__bytes_write.sum", 0)
-                                             for r in step if "k_resolve" in r["name"]),
+    steps = [ls[a + 1:b + 1] for a, b in zip(p2[:-1], p2[1:])] or [ls]
+    tot = [sum(_bytes(r) for r in st) for st in steps]
+    full = sorted((t, i) for i, t in enumerate(tot) if t >= 0.5 * max(tot))
+    step = steps[full[len(full) // 2][1]]  # the median full-size step
+    p1 = sum(_bytes(r) for r in step if "k_resolve" not in r["name"])
+    return {"per_kernel_dram_bytes_per_launch": {r["name"]: _bytes(r) for r in step},
+            "pass1_dram_bytes_per_step": p1,
+            "pass2_dram_bytes_per_step": sum(_bytes(r) for r in step if "k_resolve" in r["name"]),
             "source": os.path.basename(path)}
 
 
