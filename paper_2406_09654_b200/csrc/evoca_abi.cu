@@ -420,7 +420,8 @@ int pass1_view(evo_ctx* c, const View& v, const evo_scalars* s, int phases, int 
   }
   if (tc_net || rows_net) {
     if (int r = ensure_hidden_tc(c)) return r;
-    CK(evo::launch_hidden_tc(c->hid, v.g, v.front, c->params(), c->cap, c->num_sms, /*decided=*/!exp, st));
+    CK(evo::launch_hidden_tc(c->hid, v.g, v.front, c->params(), c->cap, c->num_sms, /*decided=*/!exp,
+                             (flags & EVO_F_L2_CUDA_CORE) != 0, st));
   }
   if (gather_net) {  // rows (export) or decided records at the cell index; rank = identity for occupied cells
     const int variant = (flags & EVO_F_TC_DIRECT) ? evo::kGatherTc : evo::kGatherFfma2;

@@ -624,6 +624,287 @@ __global__ void __launch_bounds__(kNetThreads, 1) k_hid_net(const NetArgs a) {
   if (warp == 0) tc::tmem_dealloc<kTmemCols>(tmem);
 }
 
+// Both layers on the tensor core (k_hid_net2, the default for hidden sizes
+// the TMEM map below holds; EVO_F_L2_CUDA_CORE selects k_hid_net).  Per
+// 128-row tile (one genome), 512 threads, one CTA per SM, TMEM:
+//   [0, nh)        layer-1 accumulator 0 (K steps 0-2), then h_hi in place
+//   [nh, 2 nh)     layer-1 accumulator 1 (K steps 3-5), then h_lo in place
+//   [256 + 32 i, 288 + 32 i)  layer-2 accumulator i = 0..3 (a quarter of
+//                  the hidden K steps each)
+// (1) layer 1 as in k_hid_net (3xTF32: lo.hi + hi.lo + hi.hi, A and B in
+//     shared memory); (2) epilogue 1: each thread (row r = TMEM lane, hidden
+//     quarter qt) reads its 2 x nh/4 accumulator columns, z1 = acc0 + acc1 +
+//     b1, h = tanh(z1), split h = hi + lo (hi = h with the low 13 mantissa
+//     bits cleared) and writes h_hi / h_lo over the columns it read
+//     (tcgen05.st; each thread owns those lane/column cells); (3) layer 2:
+//     A = h_hi / h_lo from TMEM, B = [W2_hi | W2_lo] (N = 32, K = nh) in
+//     shared memory, two MMAs per K step (lo.lo included) into the
+//     accumulator of its half of the hidden units (kL2Acc = 2); (4) as soon
+//     as layer 2 has read h, the next tile's layer 1 goes out and the
+//     epilogue 2 (four warps: z2_j = the partial sums (W2_hi and W2_lo
+//     columns added first) in order + b2_j, the reference sigmoid sequence,
+//     the actuator row) overlaps it.
+// Accuracy (test_tensor_core_net_vs_oracle_and_cuda_core, H = 128): actions
+// 7.8e-6 from the float64 oracle against 2.9e-6 with layer 2 in FP32 FMAs;
+// four accumulators gave 6.6e-6 (0.3 ms slower per config-5 step), lo
+// rounded to nearest TF32 (cvt.rna, on the saturated conversion pipe) 6.8e-6
+// (0.4 ms slower): the error is the tensor core's own rounding inside each
+// K = 8 step, not the split or the accumulation length.  Layer 2 on the CUDA cores (k_hid_net)
+//     was bound by the W2 broadcasts from shared memory (each lane receives
+//     its own copy; 57 % of the tile in the epilogue, round-1 phase timing).
+constexpr uint32_t kL2 = 256;  // layer-2 accumulators: kL2Acc x 32 columns
+constexpr int kL2Acc = 2;
+
+__device__ __forceinline__ void tmem_st4(uint32_t addr, uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1,%2,%3,%4};" ::"r"(addr), "r"(a0), "r"(a1), "r"(a2),
+               "r"(a3));
+}
+__device__ __forceinline__ void mma_ts(uint32_t d, uint32_t a_tmem, uint64_t b, uint32_t id, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\tsetp.ne.b32 p, %4, 0;\n\telect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(d),
+      "r"(a_tmem), "l"(b), "r"(id), "r"(acc));
+}
+__device__ __forceinline__ void mma_ss_e(uint32_t d, uint64_t a, uint64_t b, uint32_t id, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\tsetp.ne.b32 p, %4, 0;\n\telect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(d),
+      "l"(a), "l"(b), "r"(id), "r"(acc));
+}
+__device__ __forceinline__ void commit_e(uint64_t* bar) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}\n" ::"r"(tc::smem_u32(bar))
+      : "memory");
+}
+
+size_t hidden_tc2_smem(int hidden) {
+  const int nh = hidden_tc_nh(hidden);
+  const size_t fixed = (size_t)2 * nh * kK1 * 4 + (size_t)32 * nh * 4 + (size_t)(nh + 16) * 4;
+  return ((fixed + 1023) & ~(size_t)1023) + (size_t)4 * kRows * kK1 * 4 + 1024;
+}
+
+__global__ void __launch_bounds__(kNetThreads, 1) k_hid_net2(const NetArgs a) {
+  extern __shared__ __align__(1024) unsigned char smem[];
+  const int nh = a.nh;
+  const int H = a.net.hidden, hp = a.net.hpad;
+  unsigned char* B1hi = smem;
+  unsigned char* B1lo = B1hi + nh * kK1 * 4;
+  unsigned char* B2 = B1lo + nh * kK1 * 4;  // [W2_hi | W2_lo]: N = 32, K = nh, canonical
+  float* b1 = reinterpret_cast<float*>(B2 + 32 * nh * 4);
+  float* b2 = b1 + nh;
+  unsigned char* A1 = reinterpret_cast<unsigned char*>(((uintptr_t)(b2 + 16) + 1023) & ~(uintptr_t)1023);
+  constexpr int kA1Bytes = kRows * kK1 * 4;  // one of hi / lo; buffer i at A1 + i * 2 * kA1Bytes
+  __shared__ uint32_t tmem_base;
+  __shared__ __align__(8) uint64_t bar[2];  // 0: layer 1 done, 1: layer 2 done
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+
+  const int T = *a.n_tiles;
+  const int per = (T + gridDim.x - 1) / gridDim.x;
+  const int t0 = blockIdx.x * per, t1 = min(T, t0 + per);
+  if (t0 >= t1) return;
+  if (warp == 0) tc::tmem_alloc<kTmemCols>(&tmem_base);
+  if (tid == 0) {
+    tc::mbar_init(&bar[0], 1);
+    tc::mbar_init(&bar[1], 1);
+  }
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  const uint32_t tmem = tmem_base;
+  uint32_t ph0 = 0u, ph1 = 0u;
+  const uint32_t id1 = tc::idesc_tf32(kRows, nh), id2 = tc::idesc_tf32(kRows, 32);
+
+  const int ar = tid >> 2, aq = tid & 3;  // staging: this thread's quarter sensor row
+  float4 pf[3];
+  auto fetch = [&](const int4 ti) {
+    const float4* src = reinterpret_cast<const float4*>(a.sens + (size_t)(ti.y + ar) * kK1) + aq * 3;
+#pragma unroll
+    for (int q = 0; q < 3; ++q) pf[q] = ar < ti.z ? __ldg(src + q) : make_float4(0.f, 0.f, 0.f, 0.f);
+  };
+  auto stage_a1 = [&](int buf) {
+    unsigned char* hi = A1 + buf * 2 * kA1Bytes;
+    unsigned char* lo = hi + kA1Bytes;
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+      float4 v = pf[q];
+      if (q == 2 && aq == 3) v.y = 0.0f;  // element 45 is the cell index
+      float4 h4, l4;
+      split_fast(v.x, h4.x, l4.x);
+      split_fast(v.y, h4.y, l4.y);
+      split_fast(v.z, h4.z, l4.z);
+      split_fast(v.w, h4.w, l4.w);
+      const uint32_t off = tc::canon_off(ar, (aq * 3 + q) * 4, kRows);
+      *reinterpret_cast<float4*>(hi + off) = h4;
+      *reinterpret_cast<float4*>(lo + off) = l4;
+    }
+  };
+  auto stage_weights = [&](int slot) {
+    const float* W1 = a.net.wA + (size_t)slot * kSensors * hp;
+    for (int i = tid; i < nh * kK1; i += kNetThreads) {
+      const int h = i % nh, k = i / nh;
+      const float w = (h < H && k < kSensors) ? __ldg(W1 + (size_t)k * hp + h) : 0.0f;
+      put_split(B1hi, B1lo, tc::canon_off(h, k, nh), w);
+    }
+    const float* W2 = a.net.wB + (size_t)slot * hp * kOutPad;  // W2^T [hp][16]
+    for (int i = tid; i < 16 * nh; i += kNetThreads) {
+      const int j = i & 15, h = i >> 4;
+      const float w = (h < H && j < kActuators) ? __ldg(W2 + (size_t)h * kOutPad + j) : 0.0f;
+      float wh, wl;
+      split_fast(w, wh, wl);
+      *reinterpret_cast<float*>(B2 + tc::canon_off(j, h, 32)) = wh;
+      *reinterpret_cast<float*>(B2 + tc::canon_off(16 + j, h, 32)) = wl;
+    }
+    for (int h = tid; h < nh; h += kNetThreads) b1[h] = h < H ? __ldg(a.net.bA + (size_t)slot * hp + h) : 0.0f;
+    if (tid < 16) b2[tid] = tid < kActuators ? __ldg(a.net.bB + (size_t)slot * kOutPad + tid) : 0.0f;
+  };
+  // warp 0 issues (uniform control flow, one elected lane per MMA)
+  auto issue_l1 = [&](int buf) {
+    if (warp == 0) {
+      const uint32_t lA = kRows * 16, lB = nh * 16;
+      const uint64_t ah = tc::smem_desc(tc::smem_u32(A1 + buf * 2 * kA1Bytes), lA, 128);
+      const uint64_t al = tc::smem_desc(tc::smem_u32(A1 + buf * 2 * kA1Bytes + kA1Bytes), lA, 128);
+      const uint64_t bh = tc::smem_desc(tc::smem_u32(B1hi), lB, 128);
+      const uint64_t bl = tc::smem_desc(tc::smem_u32(B1lo), lB, 128);
+#pragma unroll
+      for (int j = 0; j < 3; ++j)
+#pragma unroll
+        for (int acc = 0; acc < 2; ++acc) {
+          const int ks = acc * 3 + j;
+          const uint64_t oa = (uint64_t)((2 * ks * lA) >> 4), ob = (uint64_t)((2 * ks * lB) >> 4);
+          const uint32_t d = tmem + (acc ? (uint32_t)nh : 0u);
+          mma_ss_e(d, al + oa, bh + ob, id1, j > 0);
+          mma_ss_e(d, ah + oa, bl + ob, id1, 1u);
+          mma_ss_e(d, ah + oa, bh + ob, id1, 1u);
+        }
+      commit_e(&bar[0]);
+    }
+  };
+  auto issue_l2 = [&]() {
+    if (warp == 0) {
+      const uint32_t lB = 32 * 16;
+      const uint64_t bd = tc::smem_desc(tc::smem_u32(B2), lB, 128);
+      const int nks = nh / 8, quarter = nks / kL2Acc;  // nh is a multiple of 32 here
+      for (int ks = 0; ks < nks; ++ks) {
+        const uint32_t d = tmem + kL2 + 32u * (uint32_t)(ks / quarter);
+        const uint64_t b = bd + (uint64_t)((2 * ks * lB) >> 4);
+        mma_ts(d, tmem + (uint32_t)(8 * ks), b, id2, (uint32_t)(ks % quarter != 0));
+        mma_ts(d, tmem + (uint32_t)(nh + 8 * ks), b, id2, 1u);
+      }
+      commit_e(&bar[1]);
+    }
+  };
+  auto sync_tc = [&]() {
+    tc::fence_before();
+    __syncthreads();
+    tc::fence_after();
+  };
+
+  const int4 z4 = make_int4(0, 0, 0, 0);
+  int4 ti0 = __ldg(a.tile_info + t0);
+  int4 ti1 = t0 + 1 < t1 ? __ldg(a.tile_info + t0 + 1) : z4;
+  int4 ti2 = t0 + 2 < t1 ? __ldg(a.tile_info + t0 + 2) : z4;
+  int cur = ti0.x;
+  fetch(ti0);
+  stage_weights(cur);
+  stage_a1(0);
+  if (t0 + 1 < t1) fetch(ti1);
+  tc::fence_async_smem();
+  sync_tc();
+  issue_l1(0);
+  const int q = warp & 3, qt = warp >> 2;
+  const int r = q * 32 + lane;  // this thread's tile row (TMEM lane)
+  const uint32_t lb = tmem + ((uint32_t)(q * 32) << 16);
+  const int c_begin = qt * (nh / 4), c_end = c_begin + nh / 4;
+  for (int t = t0; t < t1; ++t) {
+    const int buf = (t - t0) & 1;
+    const int4 ti = ti0;
+    const bool has_next = t + 1 < t1;
+    const int next_slot = has_next ? ti1.x : cur;
+    // (a) the next tile's rows into the other A1 buffer (its layer 1 reads
+    //     it after this tile's layer 2), the one after into registers
+    if (has_next) stage_a1(buf ^ 1);
+    if (t + 2 < t1) fetch(ti2);
+    ti0 = ti1;
+    ti1 = ti2;
+    ti2 = t + 3 < t1 ? __ldg(a.tile_info + t + 3) : z4;
+    // (b) epilogue 1: h = tanh(acc0 + acc1 + b1) over this thread's quarter,
+    //     written back split over the columns it read
+    tc::mbar_wait(&bar[0], ph0);
+    ph0 ^= 1u;
+    tc::fence_after();
+    for (int c0 = c_begin; c0 < c_end; c0 += 4) {
+      uint32_t va[4], vb[4];
+      tc::tmem_ld4_nw(lb + c0, va);
+      tc::tmem_ld4_nw(lb + nh + c0, vb);
+      tc::tmem_wait_ld();
+      tc::reg_fence(va);
+      tc::reg_fence(vb);
+      uint32_t hh[4], hl[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float h = tanh_sfu(__fadd_rn(__fadd_rn(__uint_as_float(va[j]), __uint_as_float(vb[j])), b1[c0 + j]));
+        float x, y;
+        split_fast(h, x, y);
+        hh[j] = __float_as_uint(x);
+        hl[j] = __float_as_uint(y);
+      }
+      tmem_st4(lb + c0, hh[0], hh[1], hh[2], hh[3]);
+      tmem_st4(lb + nh + c0, hl[0], hl[1], hl[2], hl[3]);
+    }
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+    tc::fence_async_smem();  // the next A1 buffer staged in (a)
+    sync_tc();
+    // (c) layer 2 of this tile
+    issue_l2();
+    // (d) layer 2 has read h once it completes: the next tile's layer 1
+    tc::mbar_wait(&bar[1], ph1);
+    ph1 ^= 1u;
+    tc::fence_after();
+    float bias2[kActuators];  // this tile's b2, read before a restage replaces it
+#pragma unroll
+    for (int j = 0; j < kActuators; ++j) bias2[j] = b2[j];
+    if (has_next && next_slot != cur) {  // genome change: restage every table first
+      sync_tc();
+      cur = next_slot;
+      stage_weights(cur);
+      tc::fence_async_smem();
+      sync_tc();
+    }
+    if (has_next) issue_l1(buf ^ 1);
+    // (e) epilogue 2 (one warp per lane quadrant) overlapping that layer 1
+    if (qt == 0) {
+      float zs[kActuators];
+#pragma unroll
+      for (int i = 0; i < kL2Acc; ++i) {
+        uint32_t dh[16], dl[16];
+        tc::tmem_ld16_nw(lb + kL2 + 32 * i, dh);
+        tc::tmem_ld16_nw(lb + kL2 + 32 * i + 16, dl);
+        tc::tmem_wait_ld();
+        tc::reg_fence(dh);
+        tc::reg_fence(dl);
+#pragma unroll
+        for (int j = 0; j < kActuators; ++j) {
+          const float p = __fadd_rn(__uint_as_float(dh[j]), __uint_as_float(dl[j]));
+          zs[j] = i ? __fadd_rn(zs[j], p) : p;
+        }
+      }
+      if (r < ti.z) {
+        float o[16];
+#pragma unroll
+        for (int j = 0; j < kActuators; ++j) o[j] = squash(__fadd_rn(zs[j], bias2[j]));
+        o[13] = o[14] = o[15] = 0.0f;
+        float4* dst = reinterpret_cast<float4*>(a.act + (size_t)(ti.y + r) * 16);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) dst[j] = make_float4(o[4 * j], o[4 * j + 1], o[4 * j + 2], o[4 * j + 3]);
+      }
+      tc::fence_before();  // the layer-2 columns are read before the next layer 2 (after the next epilogue 1's barrier)
+    }
+  }
+  __syncthreads();
+  if (warp == 0) tc::tmem_dealloc<kTmemCols>(tmem);
+}
+
 // Direct 45->13 controller over genome-sorted sensor rows (many-genome
 // pools, e.g. BASELINE configs 3-4 with 256-1024 genomes, where a 32x32 tile
 // holds ~1-4 cells per genome and per-tile weight fetches dominate).  Each
@@ -809,7 +1090,7 @@ size_t hidden_tc_smem(int hidden) {
 }
 
 cudaError_t launch_hidden_tc(const HidBuffers& b, const StepGeom& g, const Planes& front, const Params& net,
-                             int capacity, int num_sms, bool decided, cudaStream_t st) {
+                             int capacity, int num_sms, bool decided, bool l2_cuda_core, cudaStream_t st) {
   const int nctas = hidden_sort_ctas(g.W, g.H);
   const size_t hsmem = (size_t)capacity * 4;
   const size_t ssmem = sense_smem_bytes(capacity);
@@ -846,6 +1127,13 @@ cudaError_t launch_hidden_tc(const HidBuffers& b, const StepGeom& g, const Plane
   a.decided = decided && net.hidden == 0 ? 1 : 0;
   if (net.hidden == 0) {
     k_direct_rows<<<num_sms * 4, kDrThreads, 0, st>>>(a);  // 16 warps per SM, one wave
+    return cudaGetLastError();
+  }
+  if (!l2_cuda_core && hidden_tc_nh(net.hidden) <= 128 && hidden_tc_nh(net.hidden) % 32 == 0) {
+    const size_t smem = hidden_tc2_smem(net.hidden);
+    e = cudaFuncSetAttribute(k_hid_net2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    k_hid_net2<<<num_sms, kNetThreads, smem, st>>>(a);
     return cudaGetLastError();
   }
   const size_t smem = hidden_tc_smem(net.hidden);

@@ -186,7 +186,7 @@ int hidden_sort_ctas(int W, int H);
 int hidden_tc_nh(int hidden);
 size_t hidden_tc_smem(int hidden);
 cudaError_t launch_hidden_tc(const HidBuffers& b, const StepGeom& g, const Planes& front, const Params& net,
-                             int capacity, int num_sms, bool decided, cudaStream_t st);
+                             int capacity, int num_sms, bool decided, bool l2_cuda_core, cudaStream_t st);
 
 int select_chunks(long long n);
 cudaError_t launch_select_cells(const int32_t* gi, long long n, unsigned long long k0, unsigned long long k1, double p,

@@ -473,15 +473,21 @@ def test_tensor_core_net_vs_oracle_and_cuda_core(hidden, genomes, shape):
     params = oracle_phys_to_params(phys)
     oa = orc.act(p0, net)
     dev = make_dev(p0, genomes, net)
-    cells, acts = _actions(dev, 0, params, _lib.F_TC_NET)  # tensor cores at every hidden width
+    cells, acts = _actions(dev, 0, params, _lib.F_TC_NET)  # tensor cores at every hidden width (both layers)
     assert np.array_equal(cells, oa.cells)
-    assert rel_err(acts, oa.a) <= TOL
+    err_tc = rel_err(acts, oa.a)
+    assert err_tc <= TOL
     ref = orc.step(p0, 0, net, phys, acts=orc.Actions(cells, acts))
     assert download(dev).equal(ref.planes)
+    dev.close()
+    dev = make_dev(p0, genomes, net)  # layer 2 on the CUDA cores (the round-2 kernel)
+    cells3, acts3 = _actions(dev, 0, params, _lib.F_TC_NET | _lib.F_L2_CUDA_CORE)
+    assert np.array_equal(cells3, cells) and rel_err(acts3, oa.a) <= TOL
     dev.close()
     dev = make_dev(p0, genomes, net)
     cells2, acts2 = _actions(dev, 0, params, _lib.F_CUDA_CORE_NET)
     assert np.array_equal(cells2, cells) and rel_err(acts2, oa.a) <= TOL
+    print(f"H={hidden}: tcgen05 x2 {err_tc:.3g}, layer 2 FFMA {rel_err(acts3, oa.a):.3g}, FP32 {rel_err(acts2, oa.a):.3g}")
     dev.close()
 
 
