@@ -54,7 +54,7 @@ extern "C" {
 #define EVO_F_TC_NET 128        /* hidden layers narrower than 64: tcgen05 3xTF32 net instead of FP32 CUDA cores */
 #define EVO_F_SHARD_NET 256     /* direct nets of pools > 68 slots: cluster-sharded tile kernel (measured slower; A/B) */
 #define EVO_F_ROWS_NET 512      /* direct nets of pools > 68 slots: genome-sorted sensor rows in HBM (round-2 path; A/B) */
-#define EVO_F_GATHER_NET 1024   /* direct nets of pools <= 68 slots: the large-pool gather path instead of the tile kernel (A/B) */
+#define EVO_F_GATHER_NET 1024   /* the gather path for direct pools <= 68 slots and for tensor-core hidden nets (A/B) */
 #define EVO_F_TC_DIRECT 2048    /* gather path: the direct net as tcgen05 3xTF32 MMAs (A in TMEM) instead of FFMA2 warps */
 #define EVO_F_L2_CUDA_CORE 4096 /* tensor-core hidden net: layer 2 as FP32 FMAs on the CUDA cores (round-2 kernel; A/B) */
 

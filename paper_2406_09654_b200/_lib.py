@@ -23,7 +23,7 @@ F_MMA_NET = 64  # direct nets of pools <= 64 slots: mma.sync 3xTF32 tile kernel 
 F_TC_NET = 128  # hidden layers narrower than 64 on the tensor cores (default: FP32 CUDA cores)
 F_SHARD_NET = 256  # large direct pools: cluster-sharded tile kernel (measured slower than the rows path; A/B)
 F_ROWS_NET = 512  # large direct pools: genome-sorted sensor rows through HBM (the round-2 path; A/B)
-F_GATHER_NET = 1024  # pools <= 68 slots: the large-pool gather path instead of the tile kernel (A/B)
+F_GATHER_NET = 1024  # the gather path for direct pools <= 68 slots and for tensor-core hidden nets (A/B)
 F_TC_DIRECT = 2048  # gather path: direct net on tcgen05 (3xTF32, A in TMEM) instead of FFMA2 warps
 F_L2_CUDA_CORE = 4096  # tensor-core hidden net: layer 2 on the CUDA cores (round-2 kernel; A/B)
 

@@ -418,10 +418,23 @@ int pass1_view(evo_ctx* c, const View& v, const evo_scalars* s, int phases, int 
   if (exp && !tc_net && !rows_net && !gather_net) {
     if (int r = ensure_actions_out(c)) return r;
   }
-  if (tc_net || rows_net) {
+  // hidden-layer nets on the tensor cores: genome-sorted sensor rows; with
+  // EVO_F_GATHER_NET over the gather sort instead (cells by (band, slot),
+  // Moore records from the sense texture, actuator rows at the cell index) -
+  // measured slower on config 5 (9.8 ms against 3.7 ms per net): with 4096
+  // genomes a (band, slot) group is two tiles, so the 64 KB of split
+  // weights are restaged every other tile
+  const bool hid_gather = tc_net && (flags & EVO_F_GATHER_NET) && !(flags & (EVO_F_ROWS_NET | EVO_F_L2_CUDA_CORE)) &&
+                          evo::hidden_gather_supported(c->hidden) && evo::gather_supported(c->W, c->H, c->cap);
+  if ((tc_net && !hid_gather) || rows_net) {
     if (int r = ensure_hidden_tc(c)) return r;
     CK(evo::launch_hidden_tc(c->hid, v.g, v.front, c->params(), c->cap, c->num_sms, /*decided=*/!exp,
                              (flags & EVO_F_L2_CUDA_CORE) != 0, st));
+  }
+  if (hid_gather) {
+    if (int r = ensure_gather(c)) return r;
+    CK(evo::launch_gather_sort(c->gat, v.g, v.front, c->cap, c->num_sms, 128, /*one_band=*/false, c->hid.rank, st));
+    CK(evo::launch_hidden_gather(c->gat, v.g, c->params(), c->cap, c->num_sms, c->hid.act, st));
   }
   if (gather_net) {  // rows (export) or decided records at the cell index; rank = identity for occupied cells
     const int variant = (flags & EVO_F_TC_DIRECT) ? evo::kGatherTc : evo::kGatherFfma2;
@@ -747,8 +760,9 @@ EVO_API int evo_step_host(evo_ctx* c, const evo_scalars* s, int64_t t, int flags
     return fail(EVO_EINVAL, "action injection/export is not available in the host-pipelined step");
   if (int r = ensure_pipe(c)) return r;
   if (c->hidden > 0 || c->cap > evo::kSmemWeightSlotsAbi) {
-    const bool gather = c->hidden == 0 && !(flags & (EVO_F_ROWS_NET | EVO_F_TILE_NET | EVO_F_SHARD_NET)) &&
-                        evo::gather_supported(c->W, c->H, c->cap);
+    const bool gather = !(flags & (EVO_F_ROWS_NET | EVO_F_TILE_NET | EVO_F_SHARD_NET)) &&
+                        evo::gather_supported(c->W, c->H, c->cap) &&
+                        (c->hidden == 0 || ((flags & EVO_F_GATHER_NET) && evo::hidden_gather_supported(c->hidden)));
     if (int r = gather ? ensure_gather(c) : ensure_hidden_tc(c)) return r;
   }
   if ((flags & EVO_F_RECORD_EVENTS)) {

@@ -32,12 +32,15 @@
 
 #include <algorithm>
 
+#include "evoca_gather.cuh"
 #include "evoca_net.cuh"
 #include "evoca_tc.cuh"
 
 namespace evo {
 
 namespace {
+
+using namespace gs;
 
 constexpr int kGsThreads = 512;  // count / scatter CTA
 // GsPlan.rb: bins per slot (8 = one per rotation for the FFMA warp kernel,
@@ -332,46 +335,6 @@ struct GatherArgs {
   float* act;
   int export_rows;  // 0: 8-float decided records, 1: 16-float actuator rows (cell index)
 };
-
-struct f8r {
-  float v[8];
-};
-__device__ __forceinline__ f8r ld_rec(const float* p) {
-  f8r r;
-  asm volatile("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-               : "=f"(r.v[0]), "=f"(r.v[1]), "=f"(r.v[2]), "=f"(r.v[3]), "=f"(r.v[4]), "=f"(r.v[5]), "=f"(r.v[6]),
-                 "=f"(r.v[7])
-               : "l"(p));
-  return r;
-}
-
-// one lane's cell of a half-tile: texture index of its centre record and
-// the wrap corrections for x - 1 / x + 1 on the torus seam
-struct GCell {
-  int idx;   // (y + 1) * W + x
-  int wl;    // +W when x == 0 (a dx = -1 neighbour wraps)
-  int wr;    // -W when x == W - 1
-  int cell;  // y * W + x
-  int rot;
-};
-__device__ __forceinline__ GCell gcell(uint32_t e, int W) {
-  GCell c;
-  const int y = (int)((e >> 15) & 0x3FFFu), x = (int)(e & 0x7FFFu);
-  c.rot = (int)(e >> 29);
-  c.cell = y * W + x;
-  c.idx = c.cell + W;
-  c.wl = x == 0 ? W : 0;
-  c.wr = x == W - 1 ? -W : 0;
-  return c;
-}
-// Moore slot s of a (rot)-group: texture offset dy * W + dx and dx
-__device__ __forceinline__ int slot_dx(int rot, int s) { return s == 0 ? 0 : dir_dx(perm_dir(rot, s - 1)); }
-__device__ __forceinline__ int slot_dy(int rot, int s) { return s == 0 ? 0 : dir_dy(perm_dir(rot, s - 1)); }
-__device__ __forceinline__ const float* rec_ptr(const float* tex, const GCell& c, int W, int rot, int s) {
-  const int dx = slot_dx(rot, s), dy = slot_dy(rot, s);
-  const int i = c.idx + dy * W + dx + (dx < 0 ? c.wl : 0) + (dx > 0 ? c.wr : 0);
-  return tex + (size_t)i * 8;
-}
 
 // C cells per lane (a warp takes a tile of 32 C cells of one slot); D Moore
 // records per cell in flight.  C = 2, D = 3: 16 warps per SM (four resident
@@ -776,7 +739,7 @@ __global__ void __launch_bounds__(kTcThreads, 4) k_direct_tc(const GatherArgs a)
   if (warp == 0) tc::tmem_dealloc<kTcCols>(tmem);
 }
 
-GsPlan make_plan(int W, int H, int cap, int num_sms, int tile) {
+GsPlan make_plan(int W, int H, int cap, int num_sms, int tile, long long band_cells = kGsBandCells) {
   GsPlan p;
   p.rb = 1;  // both nets gather each row in its own Moore order
   p.tile = tile;
@@ -784,7 +747,7 @@ GsPlan make_plan(int W, int H, int cap, int num_sms, int tile) {
   int r = (int)((cells + 4LL * num_sms * W - 1) / (4LL * num_sms * W));
   r = std::max(1, std::min(r, std::max(1, 65536 / W)));
   p.rows_per_cta = r;
-  p.ctas_per_band = std::max(1, (int)(kGsBandCells / ((long long)r * W)));
+  p.ctas_per_band = (int)std::max(1LL, std::min((long long)(H + r - 1) / r, band_cells / ((long long)r * W)));
   p.nctas = (H + r - 1) / r;
   p.nbands = (p.nctas + p.ctas_per_band - 1) / p.ctas_per_band;
   p.bins = cap * p.rb;
@@ -808,25 +771,30 @@ GatherSizes gather_sizes(int W, int H, int cap, int num_sms) {
   return s;
 }
 
-cudaError_t launch_direct_gather(const GatherBuffers& b, const StepGeom& g, const Planes& front, const Params& net,
-                                 int cap, int num_sms, int variant, bool export_rows, float* act, int32_t* rank,
-                                 cudaStream_t st) {
-  const bool tc = variant == kGatherTc;
-  const GsPlan p = make_plan(g.W, g.H, cap, num_sms, tc ? 128 : 64);
+cudaError_t launch_gather_sort(const GatherBuffers& b, const StepGeom& g, const Planes& front, int cap, int num_sms,
+                               int tile, bool one_band, int32_t* rank, cudaStream_t st) {
+  const GsPlan p = make_plan(g.W, g.H, cap, num_sms, tile, one_band ? (long long)g.W * g.H : kGsBandCells);
   const size_t hsmem = (size_t)p.bins * 4;
-  cudaError_t e = cudaSuccess;
   if (hsmem > 48 * 1024) {
-    e = cudaFuncSetAttribute(k_gs_count, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hsmem);
+    cudaError_t e = cudaFuncSetAttribute(k_gs_count, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hsmem);
     if (e != cudaSuccess) return e;
   }
-  k_gs_count<<<p.nctas, kGsThreads, hsmem, st>>>(g, front, p, cap, b.cta_hist, b.lrank, b.tex,
-                                                        export_rows ? rank : nullptr);
+  k_gs_count<<<p.nctas, kGsThreads, hsmem, st>>>(g, front, p, cap, b.cta_hist, b.lrank, b.tex, rank);
   k_gs_colscan<<<p.nbands * ((p.bins + 31) / 32), 1024, 0, st>>>(p, b.cta_hist, b.band_hist);
   k_gs_scan_band<<<p.nbands, 1024, 0, st>>>(p, b.band_hist, b.goff, b.ght, b.band_tot);
   k_gs_scan_bands<<<1, 1024, 0, st>>>(p, b.band_tot, b.band_base, b.n_ht);
   k_gs_scatter<<<num_sms * 8, 256, 0, st>>>(g, front, p, cap, b.cta_hist, b.goff, b.band_base, b.lrank, b.sorted);
   const long long max_ht = (long long)g.W * g.H / p.tile + (long long)p.nbands * p.bins + 1;
   k_gs_tilemap<<<(unsigned)((max_ht + 255) / 256), 256, 0, st>>>(p, b.goff, b.ght, b.band_base, b.n_ht, b.info);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_direct_gather(const GatherBuffers& b, const StepGeom& g, const Planes& front, const Params& net,
+                                 int cap, int num_sms, int variant, bool export_rows, float* act, int32_t* rank,
+                                 cudaStream_t st) {
+  const bool tc = variant == kGatherTc;
+  cudaError_t e = launch_gather_sort(b, g, front, cap, num_sms, tc ? 128 : 64, false, export_rows ? rank : nullptr, st);
+  if (e != cudaSuccess) return e;
   GatherArgs a;
   a.net = net;
   a.tex = b.tex;

@@ -27,6 +27,7 @@
 
 #include <algorithm>
 
+#include "evoca_gather.cuh"
 #include "evoca_net.cuh"
 #include "evoca_tc.cuh"
 
@@ -352,6 +353,11 @@ struct NetArgs {
   const float* sens;
   float* act;  // [rows][16], or [rows][8] decided rows (direct nets, no export)
   int decided;
+  // gather form (k_hid_net2<true>): sorted cell list and sense texture
+  // instead of sensor rows; actuator rows land at the cell index
+  const uint32_t* sorted;
+  const float* tex;
+  int W;
 };
 
 __device__ __forceinline__ void put_split(unsigned char* hi, unsigned char* lo, uint32_t off, float x) {
@@ -653,6 +659,7 @@ __global__ void __launch_bounds__(kNetThreads, 1) k_hid_net(const NetArgs a) {
 //     was bound by the W2 broadcasts from shared memory (each lane receives
 //     its own copy; 57 % of the tile in the epilogue, round-1 phase timing).
 constexpr uint32_t kL2 = 256;  // layer-2 accumulators: kL2Acc x 32 columns
+constexpr int kHgRun = 2;     // gather form: consecutive tiles per claim
 constexpr int kL2Acc = 2;
 
 __device__ __forceinline__ void tmem_st4(uint32_t addr, uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3) {
@@ -684,6 +691,7 @@ size_t hidden_tc2_smem(int hidden) {
   return ((fixed + 1023) & ~(size_t)1023) + (size_t)4 * kRows * kK1 * 4 + 1024;
 }
 
+template <bool GATHER>
 __global__ void __launch_bounds__(kNetThreads, 1) k_hid_net2(const NetArgs a) {
   extern __shared__ __align__(1024) unsigned char smem[];
   const int nh = a.nh;
@@ -699,10 +707,41 @@ __global__ void __launch_bounds__(kNetThreads, 1) k_hid_net2(const NetArgs a) {
   __shared__ __align__(8) uint64_t bar[2];  // 0: layer 1 done, 1: layer 2 done
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 
-  const int T = *a.n_tiles;
-  const int per = (T + gridDim.x - 1) / gridDim.x;
-  const int t0 = blockIdx.x * per, t1 = min(T, t0 + per);
-  if (t0 >= t1) return;
+  // Tile sequence.  Rows form: one contiguous range per CTA (a genome's
+  // tiles stay together, its tables staged once).  Gather form: runs of
+  // kHgRun tiles claimed from one counter, so all CTAs sweep the row bands
+  // together and the band's texture stays in L2 (a contiguous range per CTA
+  // would gather from every band at once: 9.2 ms against 3.7 ms per
+  // config-5 net); the run after next is claimed two runs ahead (ring).
+  __shared__ int ring[4];
+  const int T = a.n_tiles[0];
+  int32_t* const counter = const_cast<int32_t*>(a.n_tiles) + 1;  // gather form: n_ht[1], zeroed by the sort
+  int t = 0, tend = T, k = 0;
+  if (GATHER) {
+    if (tid == 0) {
+      ring[3] = atomicAdd(counter, 1) * kHgRun;
+      ring[0] = atomicAdd(counter, 1) * kHgRun;
+      ring[1] = atomicAdd(counter, 1) * kHgRun;
+    }
+    __syncthreads();
+    t = ring[3];
+  } else {
+    const int per = (T + gridDim.x - 1) / gridDim.x;
+    t = blockIdx.x * per;
+    tend = min(T, t + per);
+  }
+  // the tile after u (T = none); thread 0 refills the ring slot two runs
+  // ahead of the one consumed (read only after >= kHgRun barriers)
+  auto next_tile = [&](int u) {
+    if (u >= tend) return T;
+    if (!GATHER) return u + 1 < tend ? u + 1 : T;
+    if ((u + 1) % kHgRun) return u + 1 < T ? u + 1 : T;
+    const int nx = ring[k & 3];
+    if (tid == 0) ring[(k + 2) & 3] = atomicAdd(counter, 1) * kHgRun;
+    ++k;
+    return nx < T ? nx : T;
+  };
+  if (t >= tend) return;
   if (warp == 0) tc::tmem_alloc<kTmemCols>(&tmem_base);
   if (tid == 0) {
     tc::mbar_init(&bar[0], 1);
@@ -715,20 +754,60 @@ __global__ void __launch_bounds__(kNetThreads, 1) k_hid_net2(const NetArgs a) {
   uint32_t ph0 = 0u, ph1 = 0u;
   const uint32_t id1 = tc::idesc_tf32(kRows, nh), id2 = tc::idesc_tf32(kRows, 32);
 
-  const int ar = tid >> 2, aq = tid & 3;  // staging: this thread's quarter sensor row
+  const int ar = tid >> 2, aq = tid & 3;  // staging: this thread's quarter sensor row (k = 12 aq .. 12 aq + 11)
   float4 pf[3];
+  // gather form: the Moore records this quarter row needs (Moore slots
+  // sb .. sb + 3 of the cell's own order; k = 5 s + ch)
+  gs::f8r rec[4];
+  const int sb = aq == 0 ? 0 : aq == 1 ? 2 : aq == 2 ? 4 : 7;
   auto fetch = [&](const int4 ti) {
-    const float4* src = reinterpret_cast<const float4*>(a.sens + (size_t)(ti.y + ar) * kK1) + aq * 3;
+    if (GATHER) {
+      const gs::GCell c = gs::gcell(__ldg(a.sorted + ti.y + (ar < ti.z ? ar : 0)), a.W);
 #pragma unroll
-    for (int q = 0; q < 3; ++q) pf[q] = ar < ti.z ? __ldg(src + q) : make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int j = 0; j < 4; ++j)
+        if (sb + j <= 8) rec[j] = gs::ld_rec(gs::rec_ptr(a.tex, c, a.W, c.rot, sb + j));
+    } else {
+      const float4* src = reinterpret_cast<const float4*>(a.sens + (size_t)(ti.y + ar) * kK1) + aq * 3;
+#pragma unroll
+      for (int q = 0; q < 3; ++q) pf[q] = ar < ti.z ? __ldg(src + q) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+  };
+  // the quarter row from the records (selects, no divergence: the four
+  // quarters of a row sit on neighbouring lanes)
+  auto assemble = [&]() {
+    float v[12];
+#pragma unroll
+    for (int kk = 0; kk < 12; ++kk) {
+      float x0, x1, x2, x3;
+      {  // aq = 0: k = kk
+        const int k = kk, s = k / 5;
+        x0 = rec[s - 0].v[k % 5];
+      }
+      {  // aq = 1: k = 12 + kk
+        const int k = 12 + kk, s = k / 5;
+        x1 = rec[s - 2].v[k % 5];
+      }
+      {  // aq = 2: k = 24 + kk
+        const int k = 24 + kk, s = k / 5;
+        x2 = rec[s - 4].v[k % 5];
+      }
+      {  // aq = 3: k = 36 + kk (45 .. 47 pad)
+        const int k = 36 + kk, s = k / 5;
+        x3 = k < kSensors ? rec[s - 7].v[k % 5] : 0.0f;
+      }
+      v[kk] = aq == 0 ? x0 : aq == 1 ? x1 : aq == 2 ? x2 : x3;
+    }
+#pragma unroll
+    for (int q = 0; q < 3; ++q) pf[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
   };
   auto stage_a1 = [&](int buf) {
     unsigned char* hi = A1 + buf * 2 * kA1Bytes;
     unsigned char* lo = hi + kA1Bytes;
+    if (GATHER) assemble();
 #pragma unroll
     for (int q = 0; q < 3; ++q) {
       float4 v = pf[q];
-      if (q == 2 && aq == 3) v.y = 0.0f;  // element 45 is the cell index
+      if (!GATHER && q == 2 && aq == 3) v.y = 0.0f;  // element 45 of a sensor row is the cell index
       float4 h4, l4;
       split_fast(v.x, h4.x, l4.x);
       split_fast(v.y, h4.y, l4.y);
@@ -801,14 +880,15 @@ __global__ void __launch_bounds__(kNetThreads, 1) k_hid_net2(const NetArgs a) {
   };
 
   const int4 z4 = make_int4(0, 0, 0, 0);
-  int4 ti0 = __ldg(a.tile_info + t0);
-  int4 ti1 = t0 + 1 < t1 ? __ldg(a.tile_info + t0 + 1) : z4;
-  int4 ti2 = t0 + 2 < t1 ? __ldg(a.tile_info + t0 + 2) : z4;
+  int u1 = next_tile(t), u2 = next_tile(u1);
+  int4 ti0 = __ldg(a.tile_info + t);
+  int4 ti1 = u1 < T ? __ldg(a.tile_info + u1) : z4;
+  int4 ti2 = u2 < T ? __ldg(a.tile_info + u2) : z4;
   int cur = ti0.x;
   fetch(ti0);
   stage_weights(cur);
   stage_a1(0);
-  if (t0 + 1 < t1) fetch(ti1);
+  if (u1 < T) fetch(ti1);
   tc::fence_async_smem();
   sync_tc();
   issue_l1(0);
@@ -816,18 +896,19 @@ __global__ void __launch_bounds__(kNetThreads, 1) k_hid_net2(const NetArgs a) {
   const int r = q * 32 + lane;  // this thread's tile row (TMEM lane)
   const uint32_t lb = tmem + ((uint32_t)(q * 32) << 16);
   const int c_begin = qt * (nh / 4), c_end = c_begin + nh / 4;
-  for (int t = t0; t < t1; ++t) {
-    const int buf = (t - t0) & 1;
+  int buf = 0;
+  while (t < T) {
     const int4 ti = ti0;
-    const bool has_next = t + 1 < t1;
+    const bool has_next = u1 < T;
     const int next_slot = has_next ? ti1.x : cur;
     // (a) the next tile's rows into the other A1 buffer (its layer 1 reads
     //     it after this tile's layer 2), the one after into registers
     if (has_next) stage_a1(buf ^ 1);
-    if (t + 2 < t1) fetch(ti2);
+    if (u2 < T) fetch(ti2);
+    const int u3 = next_tile(u2);
     ti0 = ti1;
     ti1 = ti2;
-    ti2 = t + 3 < t1 ? __ldg(a.tile_info + t + 3) : z4;
+    ti2 = u3 < T ? __ldg(a.tile_info + u3) : z4;
     // (b) epilogue 1: h = tanh(acc0 + acc1 + b1) over this thread's quarter,
     //     written back split over the columns it read
     tc::mbar_wait(&bar[0], ph0);
@@ -894,12 +975,17 @@ __global__ void __launch_bounds__(kNetThreads, 1) k_hid_net2(const NetArgs a) {
 #pragma unroll
         for (int j = 0; j < kActuators; ++j) o[j] = squash(__fadd_rn(zs[j], bias2[j]));
         o[13] = o[14] = o[15] = 0.0f;
-        float4* dst = reinterpret_cast<float4*>(a.act + (size_t)(ti.y + r) * 16);
+        const size_t row = GATHER ? (size_t)gs::gcell(__ldg(a.sorted + ti.y + r), a.W).cell : (size_t)(ti.y + r);
+        float4* dst = reinterpret_cast<float4*>(a.act + row * 16);
 #pragma unroll
         for (int j = 0; j < 4; ++j) dst[j] = make_float4(o[4 * j], o[4 * j + 1], o[4 * j + 2], o[4 * j + 3]);
       }
       tc::fence_before();  // the layer-2 columns are read before the next layer 2 (after the next epilogue 1's barrier)
     }
+    t = u1;
+    u1 = u2;
+    u2 = u3;
+    buf ^= 1;
   }
   __syncthreads();
   if (warp == 0) tc::tmem_dealloc<kTmemCols>(tmem);
@@ -1089,6 +1175,30 @@ size_t hidden_tc_smem(int hidden) {
   return ((fixed + 1023) & ~(size_t)1023) + (size_t)4 * kRows * kK1 * 4 + 1024;  // + alignment slack
 }
 
+bool hidden_gather_supported(int hidden) {
+  const int nh = hidden_tc_nh(hidden);
+  return hidden >= 1 && nh <= 128 && nh % 32 == 0;
+}
+
+cudaError_t launch_hidden_gather(const GatherBuffers& b, const StepGeom& g, const Params& net, int cap, int num_sms,
+                                 float* act, cudaStream_t st) {
+  NetArgs a{};
+  a.net = net;
+  a.nh = hidden_tc_nh(net.hidden);
+  a.n_tiles = b.n_ht;
+  a.tile_info = b.info;
+  a.cap = cap;
+  a.act = act;
+  a.sorted = b.sorted;
+  a.tex = b.tex;
+  a.W = g.W;
+  const size_t smem = hidden_tc2_smem(net.hidden);
+  cudaError_t e = cudaFuncSetAttribute(k_hid_net2<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  k_hid_net2<true><<<num_sms, kNetThreads, smem, st>>>(a);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_hidden_tc(const HidBuffers& b, const StepGeom& g, const Planes& front, const Params& net,
                              int capacity, int num_sms, bool decided, bool l2_cuda_core, cudaStream_t st) {
   const int nctas = hidden_sort_ctas(g.W, g.H);
@@ -1131,9 +1241,9 @@ cudaError_t launch_hidden_tc(const HidBuffers& b, const StepGeom& g, const Plane
   }
   if (!l2_cuda_core && hidden_tc_nh(net.hidden) <= 128 && hidden_tc_nh(net.hidden) % 32 == 0) {
     const size_t smem = hidden_tc2_smem(net.hidden);
-    e = cudaFuncSetAttribute(k_hid_net2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    e = cudaFuncSetAttribute(k_hid_net2<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    k_hid_net2<<<num_sms, kNetThreads, smem, st>>>(a);
+    k_hid_net2<false><<<num_sms, kNetThreads, smem, st>>>(a);
     return cudaGetLastError();
   }
   const size_t smem = hidden_tc_smem(net.hidden);

@@ -156,7 +156,7 @@ struct HidBuffers {
   int32_t* rank;     // [ncell] sorted row of each cell, -1 = empty
 };
 // Direct nets of large pools by gather (evoca_gather.cu): per-step buffers.
-constexpr int kGatherMaxCap = 2048;  // (slot, rotation) histogram of 16 K bins in shared memory
+constexpr int kGatherMaxCap = 8192;  // per-CTA slot histogram in shared memory (32 KB)
 struct GatherBuffers {
   float* tex;          // [(H + 2) * W][8] sense records {E, I, C0, C1, C2, 0, 0, 0}
   int32_t* cta_hist;   // [count CTAs][bins] per-CTA group counts -> bases inside the band's groups
@@ -177,6 +177,15 @@ struct GatherSizes {
 bool gather_supported(int W, int H, int cap);
 GatherSizes gather_sizes(int W, int H, int cap, int num_sms);
 constexpr int kGatherFfma2 = 0, kGatherTc = 2;  // net variants of the gather path
+// cells sorted by (row band, slot) (one band: by slot over the whole strip),
+// the sense texture, `tile`-cell tiles; rank (nullable): cell -> cell for
+// occupied cells, -1 otherwise
+cudaError_t launch_gather_sort(const GatherBuffers& b, const StepGeom& g, const Planes& front, int cap, int num_sms,
+                               int tile, bool one_band, int32_t* rank, cudaStream_t st);
+// hidden-layer net (k_hid_net2) over the gather sort: rows at the cell index
+cudaError_t launch_hidden_gather(const GatherBuffers& b, const StepGeom& g, const Params& net, int cap, int num_sms,
+                                 float* act, cudaStream_t st);
+bool hidden_gather_supported(int hidden);
 cudaError_t launch_direct_gather(const GatherBuffers& b, const StepGeom& g, const Planes& front, const Params& net,
                                  int cap, int num_sms, int variant, bool export_rows, float* act, int32_t* rank,
                                  cudaStream_t st);

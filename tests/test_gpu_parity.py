@@ -484,6 +484,12 @@ def test_tensor_core_net_vs_oracle_and_cuda_core(hidden, genomes, shape):
     cells3, acts3 = _actions(dev, 0, params, _lib.F_TC_NET | _lib.F_L2_CUDA_CORE)
     assert np.array_equal(cells3, cells) and rel_err(acts3, oa.a) <= TOL
     dev.close()
+    dev = make_dev(p0, genomes, net)  # the same tcgen05 net over the gather sort instead of sensor rows
+    cells4, acts4 = _actions(dev, 0, params, _lib.F_TC_NET | _lib.F_GATHER_NET)
+    assert np.array_equal(cells4, cells) and np.array_equal(acts4, acts)
+    ref4 = orc.step(p0, 0, net, phys, acts=orc.Actions(cells4, acts4))
+    assert download(dev).equal(ref4.planes)
+    dev.close()
     dev = make_dev(p0, genomes, net)
     cells2, acts2 = _actions(dev, 0, params, _lib.F_CUDA_CORE_NET)
     assert np.array_equal(cells2, cells) and rel_err(acts2, oa.a) <= TOL
