@@ -342,7 +342,7 @@ struct GatherArgs {
 // SM, 168 registers) took 1.54 ms against 1.05 ms on config 3 - fewer,
 // larger tiles in flight spread over more of the band and the DRAM reads of
 // the texture doubled.
-template <int C, int D>
+template <int C, int D, bool EXPORT>
 __global__ void __launch_bounds__(kGwThreads, C == 2 ? 4 : 3) k_direct_gather(const GatherArgs a) {
   __shared__ __align__(16) float wsm[kGwWarps][kGwW];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -421,7 +421,8 @@ __global__ void __launch_bounds__(kGwThreads, C == 2 ? 4 : 3) k_direct_gather(co
 #pragma unroll
         for (int j = 0; j < C; ++j) q[j][s + D] = ld_rec(rec_ptr(a.tex, cc[j], W, cc[j].rot, s + D));
       }
-      if (ch == 0 && s >= 9 - D && more) {  // the next tile's leading records (q[j][sn] was last read at slot sn < s)
+      if (ch == 0 && s >= 9 - D) {  // the next tile's leading records (q[j][sn] was last read at slot sn < s);
+                                     // unconditional (the last tile reloads its own cells): one copy of the loop body
         const int sn = s - (9 - D);
 #pragma unroll
         for (int j = 0; j < C; ++j) q[j][sn] = ld_rec(rec_ptr(a.tex, nc[j], W, nc[j].rot, sn));
@@ -453,7 +454,7 @@ __global__ void __launch_bounds__(kGwThreads, C == 2 ? 4 : 3) k_direct_gather(co
       }
       z[12] = __fadd_rn(acc12[c], Bs[12]);
       const int cell = cc[c].cell;
-      if (!a.export_rows) {  // 32 bytes at the cell index (explore_pick is exact)
+      if (!EXPORT) {  // 32 bytes at the cell index (explore_pick is exact)
         int ks;
         float xm;
         explore_pick(z + 5, ks, xm);
@@ -806,8 +807,10 @@ cudaError_t launch_direct_gather(const GatherBuffers& b, const StepGeom& g, cons
   a.export_rows = export_rows ? 1 : 0;
   if (tc)
     k_direct_tc<<<num_sms * 4, kTcThreads, 0, st>>>(a);  // 4 CTAs per SM, 128 TMEM columns each
+  else if (export_rows)
+    k_direct_gather<2, 3, true><<<num_sms * 4, kGwThreads, 0, st>>>(a);
   else
-    k_direct_gather<2, 3><<<num_sms * 4, kGwThreads, 0, st>>>(a);  // 16 warps per SM, one wave
+    k_direct_gather<2, 3, false><<<num_sms * 4, kGwThreads, 0, st>>>(a);  // 16 warps per SM, one wave
   return cudaGetLastError();
 }
 
