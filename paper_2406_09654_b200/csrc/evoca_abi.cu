@@ -79,6 +79,10 @@ struct evo_ctx {
   // tensor-core hidden-layer controller buffers (allocated on first use)
   evo::HidBuffers hid = {};
   evo::GatherBuffers gat = {};  // large-pool direct nets by gather (allocated on first use)
+  // TMA maps of the texture build for each plane buffer (whole-strip steps;
+  // built with the gather buffers, 0 = not available -> the LSU kernel)
+  evo::GatherMaps* gmaps = nullptr;  // [2], 64-byte aligned host memory
+  bool have_gmaps = false;
   int num_sms = 0;
   // rows / flags evo_get_actions reads (act_out, or hid.act after a tensor-core step)
   const float* exp_rows = nullptr;
@@ -285,6 +289,13 @@ int ensure_gather(evo_ctx* c) {
   if (int r = ensure_sorted_out(c)) return r;
   if (c->gat.tex) return 0;
   CK(c->alloc(&c->gat.tex, ((size_t)c->H + 2) * c->W * 8));
+  if (!c->gmaps) {
+    void* m = nullptr;
+    if (posix_memalign(&m, 128, 2 * sizeof(evo::GatherMaps)) != 0) return fail(EVO_EINVAL, "out of host memory");
+    c->gmaps = static_cast<evo::GatherMaps*>(m);
+  }
+  c->have_gmaps = !std::getenv("EVO_NO_TMA") && evo::make_gather_maps(c->buf[0], c->geom(), c->gat.tex, &c->gmaps[0]) &&
+                  evo::make_gather_maps(c->buf[1], c->geom(), c->gat.tex, &c->gmaps[1]);
   const evo::GatherSizes z = evo::gather_sizes(c->W, c->H, c->cap, c->num_sms);
   const size_t n = (size_t)c->ncell(), nb = (size_t)z.nbands, bins = (size_t)z.bins;
   CK(c->alloc(&c->gat.cta_hist, (size_t)z.nctas * bins));
@@ -439,8 +450,11 @@ int pass1_view(evo_ctx* c, const View& v, const evo_scalars* s, int phases, int 
   if (gather_net) {  // rows (export) or decided records at the cell index; rank = identity for occupied cells
     const int variant = (flags & EVO_F_TC_DIRECT) ? evo::kGatherTc : evo::kGatherFfma2;
     if (int r = ensure_gather(c)) return r;
+    // TMA texture build for whole-strip steps (band views of evo_step_host
+    // shift the planes: the LSU kernel)
+    const evo::GatherMaps* maps = (c->have_gmaps && v.off == 0) ? &c->gmaps[c->front] : nullptr;
     CK(evo::launch_direct_gather(c->gat, v.g, v.front, c->params(), c->cap, c->num_sms, variant, exp, c->hid.act,
-                                 c->hid.rank, st));
+                                 c->hid.rank, st, maps));
   }
   const bool via_rows = tc_net || rows_net || gather_net;
   const bool decided = via_rows && c->hidden == 0 && !exp;  // 8-float records at the cell index
@@ -557,6 +571,7 @@ EVO_API int evo_destroy(evo_ctx* c) {
       if (c->tev[i]) cudaEventDestroy(c->tev[i]);
   }
   for (void* p : c->allocs) cudaFree(p);
+  free(c->gmaps);
   cudaStreamDestroy(c->stream);
   delete c;
   return 0;

@@ -159,6 +159,114 @@ __global__ void __launch_bounds__(1024) k_gs_colscan(const GsPlan p, int32_t* ct
     }
 }
 
+// The same texture build and slot ranking through TMA (the default when the
+// step covers the whole strip): per CTA a two-stage pipeline over 256-cell
+// row chunks - thread 0 issues the chunk's six plane boxes (E, I, C0, C1, C2,
+// genome; cp.async.bulk.tensor, mbarrier complete_tx) one chunk ahead, every
+// thread turns its cell into a record in shared memory and ranks it, and
+// thread 0 writes the chunk's 256 records back with one TMA store.
+constexpr int kTmThreads = 256;
+constexpr int kTmChunk = 256;  // cells per box (one row)
+
+struct __align__(128) TmStage {
+  float pl[5][kTmChunk];
+  int32_t gi[kTmChunk];
+  float rec[kTmChunk * 8];
+};
+
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* m, int x, int y, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          (uint32_t)__cvta_generic_to_shared(dst)),
+      "l"((uint64_t)m), "r"(x), "r"(y), "r"((uint32_t)__cvta_generic_to_shared(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tma_store_3d(const CUtensorMap* m, const void* src, int c, int x, int y) {
+  asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"((uint64_t)m),
+               "r"(c), "r"(x), "r"(y), "r"((uint32_t)__cvta_generic_to_shared(src))
+               : "memory");
+}
+
+__global__ void __launch_bounds__(kTmThreads) k_gs_count_tma(const StepGeom g, const __grid_constant__ GatherMaps maps,
+                                                            const GsPlan p, int cap, int32_t* cta_hist,
+                                                            uint16_t* lrank, int32_t* rank) {
+  extern __shared__ __align__(128) unsigned char dsm[];
+  TmStage* stg = reinterpret_cast<TmStage*>(dsm);  // 2 stages
+  int* hist = reinterpret_cast<int*>(dsm + 2 * sizeof(TmStage));
+  __shared__ __align__(8) uint64_t full[2];
+  const int tid = threadIdx.x;
+  for (int b = tid; b < p.bins; b += kTmThreads) hist[b] = 0;
+  const int r0 = blockIdx.x * p.rows_per_cta, r1 = min(g.H, r0 + p.rows_per_cta);
+  // tensor rows (0 = ghost row -1): this CTA's rows, plus the ghost rows on
+  // the first / last CTA (records only)
+  const int y_lo = blockIdx.x == 0 ? 0 : r0 + 1, y_hi = r1 == g.H ? g.H + 2 : r1 + 1;
+  const int per_row = (g.W + kTmChunk - 1) / kTmChunk;
+  const int nchunks = (y_hi - y_lo) * per_row;
+  if (tid == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"((uint32_t)__cvta_generic_to_shared(&full[0])));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"((uint32_t)__cvta_generic_to_shared(&full[1])));
+    asm volatile("fence.mbarrier_init.release.cluster;");
+  }
+  __syncthreads();
+  auto issue = [&](int c) {  // thread 0: chunk c's six boxes into stage c & 1
+    TmStage& s = stg[c & 1];
+    const int ty = y_lo + c / per_row, x0 = (c % per_row) * kTmChunk;
+    uint64_t* bar = &full[c & 1];
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
+                     (uint32_t)__cvta_generic_to_shared(bar)),
+                 "r"(6 * kTmChunk * 4)
+                 : "memory");
+#pragma unroll
+    for (int k = 0; k < 5; ++k) tma_load_2d(s.pl[k], &maps.plane[k], x0, ty, bar);
+    tma_load_2d(s.gi, &maps.plane[5], x0, ty, bar);
+  };
+  if (tid == 0 && nchunks > 0) issue(0);
+  uint32_t ph[2] = {0u, 0u};
+  for (int c = 0; c < nchunks; ++c) {
+    const int sb = c & 1;
+    TmStage& s = stg[sb];
+    if (tid == 0 && c + 1 < nchunks) issue(c + 1);  // its stage was read before the last barrier
+    {
+      const uint32_t b = (uint32_t)__cvta_generic_to_shared(&full[sb]);
+      uint32_t done = 0;
+      while (!done)
+        asm volatile(
+            "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}\n"
+            : "=r"(done)
+            : "r"(b), "r"(ph[sb])
+            : "memory");
+      ph[sb] ^= 1u;
+    }
+    const int ty = y_lo + c / per_row, x = (c % per_row) * kTmChunk + tid;
+    // the record (two 16-byte halves; lanes 32 bytes apart)
+    float4* rp = reinterpret_cast<float4*>(s.rec + tid * 8);
+    rp[0] = make_float4(s.pl[0][tid], s.pl[1][tid], s.pl[2][tid], s.pl[3][tid]);
+    rp[1] = make_float4(s.pl[4][tid], 0.0f, 0.0f, 0.0f);
+    const int y = ty - 1;  // strip row
+    if (x < g.W && y >= r0 && y < r1) {
+      const long long i = (long long)y * g.W + x;
+      const int sl = s.gi[tid];
+      const bool occ = (unsigned)sl < (unsigned)cap;
+      if (occ) lrank[i] = (uint16_t)atomicAdd(&hist[gs_bin(p, sl, 0)], 1);
+      if (rank) rank[i] = occ ? (int)i : -1;
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncthreads();
+    if (tid == 0) {
+      tma_store_3d(&maps.tex, s.rec, 0, (c % per_row) * kTmChunk, ty);
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      // the store issued one chunk ago has read its stage: that stage's
+      // record buffer is written again by the next chunk
+      asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+    }
+    __syncthreads();
+  }
+  if (tid == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+  __syncthreads();
+  int32_t* out = cta_hist + (size_t)blockIdx.x * p.bins;
+  for (int b = tid; b < p.bins; b += kTmThreads) out[b] = hist[b];
+}
+
 // Block-wide exclusive scan of (cells, half-tiles) pairs, 1024 threads.
 __device__ __forceinline__ void scan_pair(int c, int t, int& xc, int& xt, int& tot_c, int& tot_t, int* wc, int* wt) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -757,6 +865,40 @@ GsPlan make_plan(int W, int H, int cap, int num_sms, int tile, long long band_ce
 
 }  // namespace
 
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no
+// link-time libcuda dependency)
+bool make_gather_maps(const Planes& f, const StepGeom& g, float* tex, GatherMaps* out) {
+  using Encode = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+  static Encode encode = nullptr;
+  if (!encode) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !fn)
+      return false;
+    encode = reinterpret_cast<Encode>(fn);
+  }
+  if ((g.W * 4) % 16 != 0) return false;  // TMA row pitch: a multiple of 16 bytes
+  const cuuint64_t dims[2] = {(cuuint64_t)g.W, (cuuint64_t)g.H + 2};
+  const cuuint64_t pitch[1] = {(cuuint64_t)g.W * 4};
+  const cuuint32_t box[2] = {kTmChunk, 1}, es[2] = {1, 1};
+  const void* base[6] = {f.E, f.I, f.C, f.C + g.stride, f.C + 2 * g.stride, f.gi};
+  for (int k = 0; k < 6; ++k)
+    if (encode(&out->plane[k], k == 5 ? CU_TENSOR_MAP_DATA_TYPE_INT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
+               const_cast<void*>(base[k]), dims, pitch, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+               CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return false;
+  const cuuint64_t tdims[3] = {8, (cuuint64_t)g.W, (cuuint64_t)g.H + 2};
+  const cuuint64_t tpitch[2] = {32, (cuuint64_t)g.W * 32};
+  const cuuint32_t tbox[3] = {8, kTmChunk, 1}, tes[3] = {1, 1, 1};
+  return encode(&out->tex, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, tex, tdims, tpitch, tbox, tes,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 bool gather_supported(int W, int H, int cap) {
   return cap <= kGatherMaxCap && W >= 2 && W <= 32768 && H <= 16384 && (long long)W * H < (1LL << 31);
 }
@@ -773,14 +915,21 @@ GatherSizes gather_sizes(int W, int H, int cap, int num_sms) {
 }
 
 cudaError_t launch_gather_sort(const GatherBuffers& b, const StepGeom& g, const Planes& front, int cap, int num_sms,
-                               int tile, bool one_band, int32_t* rank, cudaStream_t st) {
+                               int tile, bool one_band, int32_t* rank, cudaStream_t st, const GatherMaps* maps) {
   const GsPlan p = make_plan(g.W, g.H, cap, num_sms, tile, one_band ? (long long)g.W * g.H : kGsBandCells);
-  const size_t hsmem = (size_t)p.bins * 4;
-  if (hsmem > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(k_gs_count, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hsmem);
+  if (maps) {
+    const size_t smem = 2 * sizeof(TmStage) + (size_t)p.bins * 4;
+    cudaError_t e = cudaFuncSetAttribute(k_gs_count_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
+    k_gs_count_tma<<<p.nctas, kTmThreads, smem, st>>>(g, *maps, p, cap, b.cta_hist, b.lrank, rank);
+  } else {
+    const size_t hsmem = (size_t)p.bins * 4;
+    if (hsmem > 48 * 1024) {
+      cudaError_t e = cudaFuncSetAttribute(k_gs_count, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hsmem);
+      if (e != cudaSuccess) return e;
+    }
+    k_gs_count<<<p.nctas, kGsThreads, hsmem, st>>>(g, front, p, cap, b.cta_hist, b.lrank, b.tex, rank);
   }
-  k_gs_count<<<p.nctas, kGsThreads, hsmem, st>>>(g, front, p, cap, b.cta_hist, b.lrank, b.tex, rank);
   k_gs_colscan<<<p.nbands * ((p.bins + 31) / 32), 1024, 0, st>>>(p, b.cta_hist, b.band_hist);
   k_gs_scan_band<<<p.nbands, 1024, 0, st>>>(p, b.band_hist, b.goff, b.ght, b.band_tot);
   k_gs_scan_bands<<<1, 1024, 0, st>>>(p, b.band_tot, b.band_base, b.n_ht);
@@ -792,9 +941,10 @@ cudaError_t launch_gather_sort(const GatherBuffers& b, const StepGeom& g, const 
 
 cudaError_t launch_direct_gather(const GatherBuffers& b, const StepGeom& g, const Planes& front, const Params& net,
                                  int cap, int num_sms, int variant, bool export_rows, float* act, int32_t* rank,
-                                 cudaStream_t st) {
+                                 cudaStream_t st, const GatherMaps* maps) {
   const bool tc = variant == kGatherTc;
-  cudaError_t e = launch_gather_sort(b, g, front, cap, num_sms, tc ? 128 : 64, false, export_rows ? rank : nullptr, st);
+  cudaError_t e =
+      launch_gather_sort(b, g, front, cap, num_sms, tc ? 128 : 64, false, export_rows ? rank : nullptr, st, maps);
   if (e != cudaSuccess) return e;
   GatherArgs a;
   a.net = net;

@@ -1,6 +1,7 @@
 // Internal declarations shared by the kernels and the C ABI layer.
 #pragma once
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -167,9 +168,17 @@ struct GatherBuffers {
   int32_t* band_tot;   // [nbands][2]
   int32_t* band_base;  // [nbands + 1][2]
   int32_t* n_ht;       // [2]: half-tiles, gather work counter
-  uint32_t* sorted;    // [ncell] (y << 16) | x by (band, slot, rotation)
-  int4* info;          // [max_ht] {slot * 8 + rot, first, cells, 0}
+  uint32_t* sorted;    // [ncell] (rot << 29) | (y << 15) | x by (band, slot)
+  int4* info;          // [max_ht] {slot, first, cells, 0}
 };
+// TMA tensor maps of one plane buffer for the texture build (k_gs_count_tma):
+// E, I, C0, C1, C2 (f32) and the genome plane (i32), each 2-D [H + 2][W] from
+// ghost row -1, box 256 x 1; the texture 3-D [H + 2][W][8], box 8 x 256 x 1
+struct GatherMaps {
+  CUtensorMap plane[6];
+  CUtensorMap tex;
+};
+bool make_gather_maps(const Planes& f, const StepGeom& g, float* tex, GatherMaps* out);
 struct GatherSizes {
   int nbands, nctas, bins;
   long long max_ht;
@@ -181,14 +190,15 @@ constexpr int kGatherFfma2 = 0, kGatherTc = 2;  // net variants of the gather pa
 // the sense texture, `tile`-cell tiles; rank (nullable): cell -> cell for
 // occupied cells, -1 otherwise
 cudaError_t launch_gather_sort(const GatherBuffers& b, const StepGeom& g, const Planes& front, int cap, int num_sms,
-                               int tile, bool one_band, int32_t* rank, cudaStream_t st);
+                               int tile, bool one_band, int32_t* rank, cudaStream_t st,
+                               const GatherMaps* maps = nullptr);
 // hidden-layer net (k_hid_net2) over the gather sort: rows at the cell index
 cudaError_t launch_hidden_gather(const GatherBuffers& b, const StepGeom& g, const Params& net, int cap, int num_sms,
                                  float* act, cudaStream_t st);
 bool hidden_gather_supported(int hidden);
 cudaError_t launch_direct_gather(const GatherBuffers& b, const StepGeom& g, const Planes& front, const Params& net,
                                  int cap, int num_sms, int variant, bool export_rows, float* act, int32_t* rank,
-                                 cudaStream_t st);
+                                 cudaStream_t st, const GatherMaps* maps = nullptr);
 
 bool hidden_tc_supported(int hidden);
 int hidden_sort_ctas(int W, int H);
