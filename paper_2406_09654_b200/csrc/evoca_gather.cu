@@ -377,28 +377,55 @@ __device__ __forceinline__ void scatter_cell(const GsPlan& p, int cap, int s, in
 }
 
 __global__ void __launch_bounds__(256) k_gs_scatter(const StepGeom g, const Planes f, const GsPlan p, int cap,
-                                                    const int32_t* cta_hist, const int32_t* goff,
-                                                    const int32_t* band_base, const uint16_t* lrank,
-                                                    uint32_t* sorted) {
+                                                    const int32_t* __restrict__ cta_hist,
+                                                    const int32_t* __restrict__ goff,
+                                                    const int32_t* __restrict__ band_base,
+                                                    const uint16_t* __restrict__ lrank, uint32_t* __restrict__ sorted) {
   const long long W = g.W, n = W * g.H;
-  const bool v4 = (g.W & 3) == 0;
-  const int step = v4 ? 4 : 1;
-  for (long long i = ((long long)blockIdx.x * blockDim.x + threadIdx.x) * step; i < n;
-       i += (long long)gridDim.x * blockDim.x * step) {
-    const int cta = (int)((unsigned)i / (unsigned)W) / p.rows_per_cta, band = cta / p.ctas_per_band;
-    const int32_t* base = band_base + 2 * band;
-    const int32_t* go = goff + (size_t)band * (p.bins + 1);
-    const int32_t* ch = cta_hist + (size_t)cta * p.bins;
-    if (v4) {
-      const int4 G = __ldg(reinterpret_cast<const int4*>(f.gi + i + W));
-      const unsigned R = __ldg(reinterpret_cast<const unsigned*>(f.rot + i + W));
-      scatter_cell(p, cap, G.x, (int)(R & 0xFFu), i, W, base, go, ch, lrank, sorted);
-      scatter_cell(p, cap, G.y, (int)((R >> 8) & 0xFFu), i + 1, W, base, go, ch, lrank, sorted);
-      scatter_cell(p, cap, G.z, (int)((R >> 16) & 0xFFu), i + 2, W, base, go, ch, lrank, sorted);
-      scatter_cell(p, cap, G.w, (int)(R >> 24), i + 3, W, base, go, ch, lrank, sorted);
-    } else {
-      scatter_cell(p, cap, __ldg(f.gi + i + W), __ldg(f.rot + i + W), i, W, base, go, ch, lrank, sorted);
+  if ((g.W & 3) == 0) {
+    // eight cells per thread and iteration: every load of both quads (planes,
+    // ranks, then the group / CTA bases) is issued before any store, so the
+    // two dependent load rounds are paid once per eight cells
+    for (long long i0 = ((long long)blockIdx.x * blockDim.x + threadIdx.x) * 8; i0 < n;
+         i0 += (long long)gridDim.x * blockDim.x * 8) {
+      int sl[8], rt[8], rk[8], pos[8];
+      bool ok[8];
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const long long i = i0 + 4 * q;
+        const bool in = i < n;
+        const int4 G = in ? __ldg(reinterpret_cast<const int4*>(f.gi + i + W)) : make_int4(-1, -1, -1, -1);
+        const unsigned R = in ? __ldg(reinterpret_cast<const unsigned*>(f.rot + i + W)) : 0u;
+        const uint2 L = in ? __ldg(reinterpret_cast<const uint2*>(lrank + i)) : make_uint2(0u, 0u);
+        sl[4 * q] = G.x, sl[4 * q + 1] = G.y, sl[4 * q + 2] = G.z, sl[4 * q + 3] = G.w;
+        rt[4 * q] = (int)(R & 0xFFu), rt[4 * q + 1] = (int)((R >> 8) & 0xFFu), rt[4 * q + 2] = (int)((R >> 16) & 0xFFu),
+        rt[4 * q + 3] = (int)(R >> 24);
+        rk[4 * q] = (int)(L.x & 0xFFFFu), rk[4 * q + 1] = (int)(L.x >> 16), rk[4 * q + 2] = (int)(L.y & 0xFFFFu),
+        rk[4 * q + 3] = (int)(L.y >> 16);
+      }
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const long long i = i0 + j;
+        ok[j] = i < n && (unsigned)sl[j] < (unsigned)cap;
+        const int cta = (int)((unsigned)(ok[j] ? i : 0) / (unsigned)W) / p.rows_per_cta, band = cta / p.ctas_per_band;
+        const int b = ok[j] ? gs_bin(p, sl[j], rt[j]) : 0;
+        pos[j] = __ldg(band_base + 2 * band) + __ldg(goff + (size_t)band * (p.bins + 1) + b) +
+                 __ldg(cta_hist + (size_t)cta * p.bins + b) + rk[j];
+      }
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        if (ok[j]) {
+          const long long i = i0 + j;
+          const unsigned y = (unsigned)i / (unsigned)W, x = (unsigned)i - y * (unsigned)W;  // cells < 2^31
+          sorted[pos[j]] = ((unsigned)(rt[j] & 7) << 29) | (y << 15) | x;
+        }
     }
+    return;
+  }
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const int cta = (int)((unsigned)i / (unsigned)W) / p.rows_per_cta, band = cta / p.ctas_per_band;
+    scatter_cell(p, cap, __ldg(f.gi + i + W), __ldg(f.rot + i + W), i, W, band_base + 2 * band,
+                 goff + (size_t)band * (p.bins + 1), cta_hist + (size_t)cta * p.bins, lrank, sorted);
   }
 }
 
