@@ -515,7 +515,7 @@ __global__ void __launch_bounds__(kGwThreads, C == 2 ? 4 : 3) k_direct_gather(co
   int4 ti = __ldg(a.info + h);
   GCell cc[C];
   cells_of(ti, cc);
-  f8r q[C][9];
+  f8r q[C][3];  // ring of the D = 3 Moore records in flight per cell
 #pragma unroll
   for (int s = 0; s < D; ++s)
 #pragma unroll
@@ -549,30 +549,38 @@ __global__ void __launch_bounds__(kGwThreads, C == 2 ? 4 : 3) k_direct_gather(co
 #pragma unroll
       for (int p = 0; p < 6; ++p) acc[c][p] = 0ull;
     }
+    // nine Moore slots in three rolled rounds of three (a third of the code
+    // of the fully unrolled loop: no_instructions stalls); ring slot j holds
+    // Moore slot 3 i + j, refilled with slot 3 i + j + 3 (or the next tile's
+    // slot j) as soon as it is consumed
+    static_assert(D == 3, "the rolled slot loop keeps three records per cell in flight");
+#pragma unroll 1
+    for (int i = 0; i < 3; ++i) {
 #pragma unroll
-    for (int k = 0; k < kSensors; ++k) {
-      const int s = k / 5, ch = k - 5 * s;
-      if (ch == 0 && s + D < 9) {  // keep D records per cell in flight
+      for (int j = 0; j < 3; ++j) {
+        const int s = 3 * i + j;
 #pragma unroll
-        for (int j = 0; j < C; ++j) q[j][s + D] = ld_rec(rec_ptr(a.tex, cc[j], W, cc[j].rot, s + D));
-      }
-      if (ch == 0 && s >= 9 - D) {  // the next tile's leading records (q[j][sn] was last read at slot sn < s);
-                                     // unconditional (the last tile reloads its own cells): one copy of the loop body
-        const int sn = s - (9 - D);
+        for (int ch = 0; ch < 5; ++ch) {
+          const int k = 5 * s + ch;
+          const float4* w4 = reinterpret_cast<const float4*>(W12 + k * 12);
+          const float4 wa = w4[0], wb = w4[1], wc = w4[2];
+          const u64 wp[6] = {pk2(wa.x, wa.y), pk2(wa.z, wa.w), pk2(wb.x, wb.y),
+                             pk2(wb.z, wb.w), pk2(wc.x, wc.y), pk2(wc.z, wc.w)};
+          const float w12 = W1[k];
 #pragma unroll
-        for (int j = 0; j < C; ++j) q[j][sn] = ld_rec(rec_ptr(a.tex, nc[j], W, nc[j].rot, sn));
-      }
-      const float4* w4 = reinterpret_cast<const float4*>(W12 + k * 12);
-      const float4 wa = w4[0], wb = w4[1], wc = w4[2];
-      const u64 wp[6] = {pk2(wa.x, wa.y), pk2(wa.z, wa.w), pk2(wb.x, wb.y),
-                         pk2(wb.z, wb.w), pk2(wc.x, wc.y), pk2(wc.z, wc.w)};
-      const float w12 = W1[k];
+          for (int c = 0; c < C; ++c) {
+            const float x = q[c][j].v[ch];
 #pragma unroll
-      for (int c = 0; c < C; ++c) {
-        const float x = q[c][s].v[ch];
+            for (int p = 0; p < 6; ++p) ffma2(acc[c][p], x, wp[p]);
+            acc12[c] = fmaf(x, w12, acc12[c]);
+          }
+        }
+        // refill (unconditional for the next tile: the last tile reloads its
+        // own cells, which keeps a single copy of the loop body)
 #pragma unroll
-        for (int p = 0; p < 6; ++p) ffma2(acc[c][p], x, wp[p]);
-        acc12[c] = fmaf(x, w12, acc12[c]);
+        for (int c = 0; c < C; ++c)
+          q[c][j] = i < 2 ? ld_rec(rec_ptr(a.tex, cc[c], W, cc[c].rot, s + 3))
+                          : ld_rec(rec_ptr(a.tex, nc[c], W, nc[c].rot, j));
       }
     }
 #pragma unroll
