@@ -790,7 +790,10 @@ EVO_API int evo_step_host(evo_ctx* c, const evo_scalars* s, int64_t t, int flags
   // tiles.  Pass 1 chunk b = rows [R_b - 32, R_{b+1} - 32) needs only bands
   // <= b; pass 2 chunk b = rows [R_b - 33, R_{b+1} - 33) needs only pass-1
   // chunks <= b; row 0 and the last chunk close the seam at the end.
-  int nb = bands > 0 ? bands : 4;
+  // default: ~1.4 M cells per band, 4..12 bands (config 3 measured 12.9 /
+  // 11.7 / 11.2 / 11.6 ms per step at 4 / 8 / 12 / 16 bands, tools/e2e_bands.py;
+  // config 2 keeps 4)
+  int nb = bands > 0 ? bands : (int)std::max(4LL, std::min(12LL, n / 1400000));
   nb = std::min(nb, evo_ctx::kMaxBands);
   if (H - 32 < 64) nb = 1;
   std::vector<int> R;  // band starts, R[nb] = H
