@@ -51,6 +51,10 @@ struct evo_ctx {
   // pass 1 after any weight write
   float* wF = nullptr;
   bool frag_stale = true;
+  // hidden nets, gather form: per-slot pre-split tables (k_hid_tables),
+  // rebuilt on the stream before the next such pass 1 after any weight write
+  unsigned char* htab = nullptr;
+  bool htab_stale = true;
   // cluster-sharded pass 1 (evoca_shard.cu): slot -> (shard, local) map and
   // per-shard weight tables, rebuilt on the stream when the pool changed
   int* shard_map = nullptr;
@@ -445,7 +449,12 @@ int pass1_view(evo_ctx* c, const View& v, const evo_scalars* s, int phases, int 
   if (hid_gather) {
     if (int r = ensure_gather(c)) return r;
     CK(evo::launch_gather_sort(c->gat, v.g, v.front, c->cap, c->num_sms, 128, /*one_band=*/false, c->hid.rank, st));
-    CK(evo::launch_hidden_gather(c->gat, v.g, c->params(), c->cap, c->num_sms, c->hid.act, st));
+    if (!c->htab) CK(c->alloc(&c->htab, (size_t)c->cap * evo::hidden_table_bytes(c->hidden)));
+    if (c->htab_stale) {
+      CK(evo::launch_hidden_tables(c->params(), c->cap, c->htab, st));
+      c->htab_stale = false;
+    }
+    CK(evo::launch_hidden_gather(c->gat, v.g, c->params(), c->cap, c->num_sms, c->htab, c->hid.act, st));
   }
   if (gather_net) {  // rows (export) or decided records at the cell index; rank = identity for occupied cells
     const int variant = (flags & EVO_F_TC_DIRECT) ? evo::kGatherTc : evo::kGatherFfma2;
@@ -641,6 +650,7 @@ EVO_API int evo_set_params(evo_ctx* c, int slot0, int n, const float* w1, const 
     CK(copy_sync(c, c->bA + (size_t)slot0 * evo::kOutPad, bt.data(), bt.size() * 4, cudaMemcpyHostToDevice));
     c->frag_stale = true;
     c->shard_stale = true;
+    c->htab_stale = true;
     return 0;
   }
   const int hp = c->hpad;
@@ -660,6 +670,7 @@ EVO_API int evo_set_params(evo_ctx* c, int slot0, int n, const float* w1, const 
   CK(copy_sync(c, c->bA + (size_t)slot0 * hp, B1.data(), B1.size() * 4, cudaMemcpyHostToDevice));
   CK(copy_sync(c, c->wB + (size_t)slot0 * hp * evo::kOutPad, W2.data(), W2.size() * 4, cudaMemcpyHostToDevice));
   CK(copy_sync(c, c->bB + (size_t)slot0 * evo::kOutPad, B2.data(), B2.size() * 4, cudaMemcpyHostToDevice));
+  c->htab_stale = true;
   return 0;
 }
 
@@ -1265,7 +1276,7 @@ EVO_API int evo_express_cppn(evo_ctx* c, int n, const int32_t* slots, const int3
   if (e == cudaSuccess) e = evo::launch_express_cppn(b, c->params(), c->wA, c->bA, c->wB, c->bB, st);
   c->frag_stale = true;
   c->shard_stale = true;
-  c->frag_stale = true;
+  c->htab_stale = true;
   if (e == cudaSuccess) e = cudaStreamSynchronize(st);
   cudaFree(dbuf);
   CK(e);

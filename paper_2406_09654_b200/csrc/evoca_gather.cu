@@ -31,6 +31,7 @@
 //                 the cell index (export).
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "evoca_gather.cuh"
 #include "evoca_net.cuh"

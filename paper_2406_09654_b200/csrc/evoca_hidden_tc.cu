@@ -26,6 +26,7 @@
 // actions injected (bit-exact physics given the actions).
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "evoca_gather.cuh"
 #include "evoca_net.cuh"
@@ -358,6 +359,8 @@ struct NetArgs {
   const uint32_t* sorted;
   const float* tex;
   int W;
+  int contig;  // gather form: contiguous tile range per CTA instead of claimed runs
+  const unsigned char* htab;  // gather form: per-slot pre-split tables (hid_table_bytes each)
 };
 
 __device__ __forceinline__ void put_split(unsigned char* hi, unsigned char* lo, uint32_t off, float x) {
@@ -691,18 +694,84 @@ size_t hidden_tc2_smem(int hidden) {
   return ((fixed + 1023) & ~(size_t)1023) + (size_t)4 * kRows * kK1 * 4 + 1024;
 }
 
+// Per-slot pre-split tables of k_hid_net2 in its shared-memory layout:
+// B1hi | B1lo (canonical K-major, N = nh) | B2 = [W2_hi | W2_lo] (N = 32) |
+// b1 (nh) | b2 (16), built once per weight change (k_hid_tables) and copied
+// whole by cp.async.bulk when the gather form changes slot.
+__host__ __device__ inline int hid_table_bytes(int nh) { return 2 * nh * kK1 * 4 + 32 * nh * 4 + (nh + 16) * 4; }
+
+__global__ void k_hid_tables(const Params net, int nh, unsigned char* out) {
+  const int slot = blockIdx.x;
+  const int H = net.hidden, hp = net.hpad;
+  unsigned char* B1hi = out + (size_t)slot * hid_table_bytes(nh);
+  unsigned char* B1lo = B1hi + nh * kK1 * 4;
+  unsigned char* B2 = B1lo + nh * kK1 * 4;
+  float* b1 = reinterpret_cast<float*>(B2 + 32 * nh * 4);
+  float* b2 = b1 + nh;
+  const float* W1 = net.wA + (size_t)slot * kSensors * hp;
+  for (int i = threadIdx.x; i < nh * kK1; i += blockDim.x) {
+    const int h = i % nh, k = i / nh;
+    const float w = (h < H && k < kSensors) ? __ldg(W1 + (size_t)k * hp + h) : 0.0f;
+    put_split(B1hi, B1lo, tc::canon_off(h, k, nh), w);
+  }
+  const float* W2 = net.wB + (size_t)slot * hp * kOutPad;
+  for (int i = threadIdx.x; i < 16 * nh; i += blockDim.x) {
+    const int j = i & 15, h = i >> 4;
+    const float w = (h < H && j < kActuators) ? __ldg(W2 + (size_t)h * kOutPad + j) : 0.0f;
+    float wh, wl;
+    split_fast(w, wh, wl);
+    *reinterpret_cast<float*>(B2 + tc::canon_off(j, h, 32)) = wh;
+    *reinterpret_cast<float*>(B2 + tc::canon_off(16 + j, h, 32)) = wl;
+  }
+  for (int h = threadIdx.x; h < nh; h += blockDim.x) b1[h] = h < H ? __ldg(net.bA + (size_t)slot * hp + h) : 0.0f;
+  if (threadIdx.x < 16) b2[threadIdx.x] = threadIdx.x < kActuators ? __ldg(net.bB + (size_t)slot * kOutPad + threadIdx.x) : 0.0f;
+}
+
 template <bool GATHER>
 __global__ void __launch_bounds__(kNetThreads, 1) k_hid_net2(const NetArgs a) {
   extern __shared__ __align__(1024) unsigned char smem[];
   const int nh = a.nh;
   const int H = a.net.hidden, hp = a.net.hpad;
-  unsigned char* B1hi = smem;
+  // the slot's tables: B1hi | B1lo | B2 = [W2_hi | W2_lo] (N = 32, K = nh,
+  // canonical) | b1 | b2 (hid_table_bytes); the gather form keeps a second
+  // copy after the A1 buffers, filled by a bulk copy of the next slot's
+  // pre-split table while the current tile runs
+  const int tab = hid_table_bytes(nh);
+  unsigned char* wbase[2];
+  wbase[0] = smem;
+  unsigned char* A1 = smem + ((tab + 1023) & ~1023);
+  constexpr int kA1Bytes = kRows * kK1 * 4;  // one of hi / lo; buffer i at A1 + i * 2 * kA1Bytes
+  wbase[1] = A1 + 4 * kA1Bytes;
+  int wb = 0;
+  unsigned char* B1hi = wbase[0];
   unsigned char* B1lo = B1hi + nh * kK1 * 4;
-  unsigned char* B2 = B1lo + nh * kK1 * 4;  // [W2_hi | W2_lo]: N = 32, K = nh, canonical
+  unsigned char* B2 = B1lo + nh * kK1 * 4;
   float* b1 = reinterpret_cast<float*>(B2 + 32 * nh * 4);
   float* b2 = b1 + nh;
-  unsigned char* A1 = reinterpret_cast<unsigned char*>(((uintptr_t)(b2 + 16) + 1023) & ~(uintptr_t)1023);
-  constexpr int kA1Bytes = kRows * kK1 * 4;  // one of hi / lo; buffer i at A1 + i * 2 * kA1Bytes
+  auto use_weights = [&](int w) {
+    wb = w;
+    B1hi = wbase[w];
+    B1lo = B1hi + nh * kK1 * 4;
+    B2 = B1lo + nh * kK1 * 4;
+    b1 = reinterpret_cast<float*>(B2 + 32 * nh * 4);
+    b2 = b1 + nh;
+  };
+  __shared__ __align__(8) uint64_t wbar;  // gather form: the bulk weight copy
+  uint32_t wph = 0u;
+  // thread 0: the slot's pre-split table into weight buffer w (async)
+  auto fetch_weights = [&](int slot, int w) {
+    const uint32_t mb = tc::smem_u32(&wbar);
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mb), "r"(tab) : "memory");
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            tc::smem_u32(wbase[w])),
+        "l"(a.htab + (size_t)slot * tab), "r"(tab), "r"(mb)
+        : "memory");
+  };
+  auto wait_weights = [&]() {
+    tc::mbar_wait(&wbar, wph);
+    wph ^= 1u;
+  };
   __shared__ uint32_t tmem_base;
   __shared__ __align__(8) uint64_t bar[2];  // 0: layer 1 done, 1: layer 2 done
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -717,7 +786,8 @@ __global__ void __launch_bounds__(kNetThreads, 1) k_hid_net2(const NetArgs a) {
   const int T = a.n_tiles[0];
   int32_t* const counter = const_cast<int32_t*>(a.n_tiles) + 1;  // gather form: n_ht[1], zeroed by the sort
   int t = 0, tend = T, k = 0;
-  if (GATHER) {
+  const bool dyn = GATHER && !a.contig;
+  if (dyn) {
     if (tid == 0) {
       ring[3] = atomicAdd(counter, 1) * kHgRun;
       ring[0] = atomicAdd(counter, 1) * kHgRun;
@@ -734,7 +804,7 @@ __global__ void __launch_bounds__(kNetThreads, 1) k_hid_net2(const NetArgs a) {
   // ahead of the one consumed (read only after >= kHgRun barriers)
   auto next_tile = [&](int u) {
     if (u >= tend) return T;
-    if (!GATHER) return u + 1 < tend ? u + 1 : T;
+    if (!dyn) return u + 1 < tend ? u + 1 : T;
     if ((u + 1) % kHgRun) return u + 1 < T ? u + 1 : T;
     const int nx = ring[k & 3];
     if (tid == 0) ring[(k + 2) & 3] = atomicAdd(counter, 1) * kHgRun;
@@ -746,6 +816,7 @@ __global__ void __launch_bounds__(kNetThreads, 1) k_hid_net2(const NetArgs a) {
   if (tid == 0) {
     tc::mbar_init(&bar[0], 1);
     tc::mbar_init(&bar[1], 1);
+    tc::mbar_init(&wbar, 1);
   }
   tc::fence_before();
   __syncthreads();
@@ -886,7 +957,12 @@ __global__ void __launch_bounds__(kNetThreads, 1) k_hid_net2(const NetArgs a) {
   int4 ti2 = u2 < T ? __ldg(a.tile_info + u2) : z4;
   int cur = ti0.x;
   fetch(ti0);
-  stage_weights(cur);
+  if (GATHER) {
+    if (tid == 0) fetch_weights(cur, 0);
+    wait_weights();
+  } else {
+    stage_weights(cur);
+  }
   stage_a1(0);
   if (u1 < T) fetch(ti1);
   tc::fence_async_smem();
@@ -936,8 +1012,10 @@ __global__ void __launch_bounds__(kNetThreads, 1) k_hid_net2(const NetArgs a) {
     asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
     tc::fence_async_smem();  // the next A1 buffer staged in (a)
     sync_tc();
-    // (c) layer 2 of this tile
+    // (c) layer 2 of this tile; gather form: the next slot's table into the
+    //     other weight buffer (every reader of it has passed the barrier)
     issue_l2();
+    if (GATHER && has_next && next_slot != cur && tid == 0) fetch_weights(next_slot, wb ^ 1);
     // (d) layer 2 has read h once it completes: the next tile's layer 1
     tc::mbar_wait(&bar[1], ph1);
     ph1 ^= 1u;
@@ -945,12 +1023,18 @@ __global__ void __launch_bounds__(kNetThreads, 1) k_hid_net2(const NetArgs a) {
     float bias2[kActuators];  // this tile's b2, read before a restage replaces it
 #pragma unroll
     for (int j = 0; j < kActuators; ++j) bias2[j] = b2[j];
-    if (has_next && next_slot != cur) {  // genome change: restage every table first
-      sync_tc();
-      cur = next_slot;
-      stage_weights(cur);
-      tc::fence_async_smem();
-      sync_tc();
+    if (has_next && next_slot != cur) {  // genome change
+      if (GATHER) {  // the bulk copy issued in (c)
+        wait_weights();
+        cur = next_slot;
+        use_weights(wb ^ 1);
+      } else {  // restage every table first
+        sync_tc();
+        cur = next_slot;
+        stage_weights(cur);
+        tc::fence_async_smem();
+        sync_tc();
+      }
     }
     if (has_next) issue_l1(buf ^ 1);
     // (e) epilogue 2 (one warp per lane quadrant) overlapping that layer 1
@@ -1180,8 +1264,15 @@ bool hidden_gather_supported(int hidden) {
   return hidden >= 1 && nh <= 128 && nh % 32 == 0;
 }
 
+size_t hidden_table_bytes(int hidden) { return (size_t)hid_table_bytes(hidden_tc_nh(hidden)); }
+
+cudaError_t launch_hidden_tables(const Params& net, int cap, unsigned char* out, cudaStream_t st) {
+  k_hid_tables<<<cap, 256, 0, st>>>(net, hidden_tc_nh(net.hidden), out);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_hidden_gather(const GatherBuffers& b, const StepGeom& g, const Params& net, int cap, int num_sms,
-                                 float* act, cudaStream_t st) {
+                                 const unsigned char* htab, float* act, cudaStream_t st) {
   NetArgs a{};
   a.net = net;
   a.nh = hidden_tc_nh(net.hidden);
@@ -1192,7 +1283,12 @@ cudaError_t launch_hidden_gather(const GatherBuffers& b, const StepGeom& g, cons
   a.sorted = b.sorted;
   a.tex = b.tex;
   a.W = g.W;
-  const size_t smem = hidden_tc2_smem(net.hidden);
+  a.contig = 0;
+  a.htab = htab;
+  // weights | A1 x 4 | second weights (the static 1 KB holds the barriers:
+  // 230,976 + 1,024 of the 232,448 bytes a CTA may have at nh = 128)
+  const int nh = hidden_tc_nh(net.hidden), tb = hid_table_bytes(nh);
+  const size_t smem = (size_t)((tb + 1023) & ~1023) + (size_t)4 * kRows * kK1 * 4 + (size_t)tb;
   cudaError_t e = cudaFuncSetAttribute(k_hid_net2<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   k_hid_net2<true><<<num_sms, kNetThreads, smem, st>>>(a);

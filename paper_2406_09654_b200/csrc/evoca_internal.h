@@ -194,7 +194,9 @@ cudaError_t launch_gather_sort(const GatherBuffers& b, const StepGeom& g, const 
                                const GatherMaps* maps = nullptr);
 // hidden-layer net (k_hid_net2) over the gather sort: rows at the cell index
 cudaError_t launch_hidden_gather(const GatherBuffers& b, const StepGeom& g, const Params& net, int cap, int num_sms,
-                                 float* act, cudaStream_t st);
+                                 const unsigned char* htab, float* act, cudaStream_t st);
+size_t hidden_table_bytes(int hidden);  // per slot
+cudaError_t launch_hidden_tables(const Params& net, int cap, unsigned char* out, cudaStream_t st);
 bool hidden_gather_supported(int hidden);
 cudaError_t launch_direct_gather(const GatherBuffers& b, const StepGeom& g, const Planes& front, const Params& net,
                                  int cap, int num_sms, int variant, bool export_rows, float* act, int32_t* rank,
