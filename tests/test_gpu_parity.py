@@ -547,6 +547,31 @@ def test_genome_sorted_direct_path_matches_tile_path(genomes, shape):
     _step_vs_oracle(p0, net, phys, steps=2)
 
 
+@pytest.mark.parametrize("shape", [(96, 80), (70, 258), (1, 512)])
+def test_tma_texture_build_matches_lsu_build(shape, monkeypatch):
+    """The gather path's texture build through TMA (k_gs_count_tma, the
+    default for whole-strip steps) and the LSU kernel it replaced
+    (EVO_NO_TMA) give bit-identical steps, including widths that are not a
+    multiple of the 256-cell TMA box and a 1-row torus."""
+    h, w = shape
+    p0 = orc.synth_planes(h, w, 300, seed=w)
+    net = orc.synth_net(300, 0, seed=7)
+    params = oracle_phys_to_params(orc.Phys(cycle_period=20))
+    states = []
+    for no_tma in (False, True):  # the maps are made at a context's first gather step
+        if no_tma:
+            monkeypatch.setenv("EVO_NO_TMA", "1")
+        d = make_dev(p0, 300, net)
+        got = []
+        for t in range(3):
+            d.step_raw(physics.step_scalars(t, params), t)
+            got.append(download(d))
+        d.close()
+        states.append(got)
+    for t in range(3):
+        assert states[0][t].equal(states[1][t]), f"t={t}"
+
+
 @pytest.mark.parametrize("genomes,shape", [(8, (64, 64)), (64, (128, 96)), (1, (33, 40))])
 def test_gather_path_on_small_pools_matches_tile_path(genomes, shape):
     """EVO_F_GATHER_NET forces the large-pool gather path on a pool the tile
