@@ -55,14 +55,20 @@ def _gather(plan, strips, p_like):
 
 @pytest.mark.parametrize("world", [1, 2, 3, 4])
 @pytest.mark.parametrize("shape", [(64, 64), (70, 33)])
-def test_strips_match_single_context(world, shape):
+@pytest.mark.parametrize("genomes", [8, 300])
+def test_strips_match_single_context(world, shape, genomes):
+    """1-4 row strips (ghost rows filled by the halo exchange) reproduce the
+    single context bit for bit: 8 genomes run the per-tile kernel, 300 the
+    gather path (sense texture from the exchanged ghost rows, TMA build on
+    widths divisible by 4, the LSU build otherwise) - the path the weak-
+    scaling bench runs with config 3 on every GPU."""
     import torch
 
     H, W = shape
-    p0 = orc.synth_planes(H, W, 8, seed=H + world)
+    p0 = orc.synth_planes(H, W, genomes, seed=H + world)
     p0.I[np.random.default_rng(1).random((H, W)) < 0.3] = 0
-    net = orc.synth_net(8, 0, seed=2)
-    ref = make_dev(p0, 8, net)
+    net = orc.synth_net(genomes, 0, seed=2)
+    ref = make_dev(p0, genomes, net)
     plan, strips = _strips(p0, net, world)
     params = physics.PhysicsParams(cycle_period=20, explore_fraction=0.8)
     for t in range(6):
@@ -105,7 +111,7 @@ def test_strips_tensor_core_hidden_net(world):
     ref.close()
 
 
-def _rank_worker(rank, world, port, outdir, t_steps):
+def _rank_worker(rank, world, port, outdir, t_steps, genomes=9):
     """One rank of a world-2 run: its own process and CUDA context on cuda:0,
     DeviceStrip.step with the halo exchanges and census all_reduce going
     through gloo (StagedHaloComm) - the rank's kernels never wait on the
@@ -120,9 +126,9 @@ def _rank_worker(rank, world, port, outdir, t_steps):
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        p = orc.synth_planes(70, 48, 9, seed=21)
+        p = orc.synth_planes(70, 48, genomes, seed=21)
         p.I[np.random.default_rng(2).random((70, 48)) < 0.4] = 0  # contention across the strip seams
-        net = orc.synth_net(9, 0, seed=21)
+        net = orc.synth_net(genomes, 0, seed=21)
         plan = StripPlan(70, 48, world)
         s = DeviceStrip(plan, rank, net.capacity, hidden=0, device=0, comm=StagedHaloComm(rank, world))
         s.dev.set_params(_params(net))
@@ -146,10 +152,12 @@ def _rank_worker(rank, world, port, outdir, t_steps):
         dist.destroy_process_group()
 
 
-def test_device_strips_two_processes_match_single_context():
+@pytest.mark.parametrize("genomes", [9, 300])
+def test_device_strips_two_processes_match_single_context(genomes):
     """DeviceStrip.step itself with world size 2 (two processes, gloo-staged
     exchanges) equals the single-context device step bit for bit after
-    several steps, census included."""
+    several steps, census included (9 genomes: per-tile kernel; 300: the
+    gather path with its TMA texture build)."""
     import os
     import socket
     import tempfile
@@ -161,10 +169,10 @@ def test_device_strips_two_processes_match_single_context():
     port = sock.getsockname()[1]
     sock.close()
     steps = 5
-    p = orc.synth_planes(70, 48, 9, seed=21)
+    p = orc.synth_planes(70, 48, genomes, seed=21)
     p.I[np.random.default_rng(2).random((70, 48)) < 0.4] = 0
-    net = orc.synth_net(9, 0, seed=21)
-    dev = make_dev(p, 9, net)
+    net = orc.synth_net(genomes, 0, seed=21)
+    dev = make_dev(p, genomes, net)
     params = physics.PhysicsParams(cycle_period=20)
     for t in range(steps):
         dev.step_raw(physics.step_scalars(t, params), t)
@@ -172,7 +180,7 @@ def test_device_strips_two_processes_match_single_context():
     counts_want, state_want, _, _ = dev.read_census()
     dev.close()
     with tempfile.TemporaryDirectory() as d:
-        mp.spawn(_rank_worker, args=(2, port, d, steps), nprocs=2, join=True)
+        mp.spawn(_rank_worker, args=(2, port, d, steps, genomes), nprocs=2, join=True)
         got = orc.Planes(np.empty((70, 48), np.float32), np.empty((70, 48), np.float32),
                          np.empty((3, 70, 48), np.float32), np.empty((70, 48), np.int32), np.empty((70, 48), np.uint8))
         for r in range(2):
