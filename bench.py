@@ -125,7 +125,10 @@ def run_ours(args, rank, world, local):
 
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     cfg = BASELINE_CONFIGS[args.config]
-    state = engine.baseline_state(args.config, seed=args.seed + rank)
+    # strips: every rank holds the same seeded state (its strip of a
+    # (H * world) x W torus) so that the pool - and with it config 3's
+    # field radiation, which every rank applies identically - is shared
+    state = engine.baseline_state(args.config, seed=args.seed if (world > 1 or args.strips) else args.seed + rank)
     stream = torch.cuda.Stream()
     torch.cuda.set_stream(stream)
     sh = stream.cuda_stream
@@ -149,7 +152,7 @@ def run_ours(args, rank, world, local):
     dev.upload(state.substrate.front)
     dev.sync()
 
-    radiate = (not strips) and cfg.radiation_every > 0  # config 3: field radiation every 50 steps, amortised
+    radiate = cfg.radiation_every > 0  # config 3: field radiation every 50 steps, amortised
 
     def one_step(sc, t, e0=None, e1=None, e2=None):
         if e0 is not None:
@@ -158,6 +161,12 @@ def run_ours(args, rank, world, local):
             strip.step(sc, t)
             if e1 is not None:
                 e1.record(stream)
+            if radiate and (t + 1) % cfg.radiation_every == 0:
+                # over the strips: global draw order, summed parent counts,
+                # identical children on every rank (DeviceStrip.field_radiation)
+                stream.synchronize()
+                strip.field_radiation(state.pool, state.master_seed, t + 1, cfg.radiation_p)
+            if e2 is not None:
                 e2.record(stream)
             return
         dev.pass1(sc, t, stream=sh)

@@ -224,6 +224,13 @@ EVO_API int evo_express_cppn(evo_ctx* ctx, int n, const int32_t* slots, const in
  * evo_read_selected copies the selected cells (ascending) for inspection. */
 EVO_API int evo_select_cells(evo_ctx* ctx, uint64_t key_lo, uint64_t key_hi, double p, int32_t* parent_counts,
                              int64_t* n_selected);
+/* Row strips: the strip's r-th occupied cell takes draw first_draw + r (the
+ * occupied cells of the strips above it, e.g. an exclusive scan of
+ * evo_count_occupied over the ranks), so N strips select exactly the cells
+ * one context holding the whole torus would. */
+EVO_API int evo_count_occupied(evo_ctx* ctx, int64_t* n_occupied);
+EVO_API int evo_select_cells_at(evo_ctx* ctx, uint64_t key_lo, uint64_t key_hi, double p, int64_t first_draw,
+                                int32_t* parent_counts, int64_t* n_selected);
 EVO_API int evo_read_selected(evo_ctx* ctx, int64_t capacity, int64_t* cells, int64_t* n);
 EVO_API int evo_remap_selected(evo_ctx* ctx, const int32_t* slot_map);
 

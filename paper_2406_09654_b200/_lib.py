@@ -81,6 +81,8 @@ SIGNATURES = {
     "evo_read_events": [_P, _I64, _P, _P, _P, _P, _P, _P, C.POINTER(_I64)],
     "evo_patch_genomes": [_P, _P, _P, _I64],
     "evo_select_cells": [_P, C.c_uint64, C.c_uint64, C.c_double, _P, C.POINTER(_I64)],
+    "evo_select_cells_at": [_P, C.c_uint64, C.c_uint64, C.c_double, C.c_int64, _P, C.POINTER(_I64)],
+    "evo_count_occupied": [_P, C.POINTER(_I64)],
     "evo_read_selected": [_P, _I64, _P, C.POINTER(_I64)],
     "evo_remap_selected": [_P, _P],
     "evo_express_cppn": [_P, _I, _P, _P, _P, _P, _P, _P, _P, C.c_double, C.c_double, _P],

@@ -1283,23 +1283,43 @@ EVO_API int evo_express_cppn(evo_ctx* c, int n, const int32_t* slots, const int3
   return 0;
 }
 
-EVO_API int evo_select_cells(evo_ctx* c, uint64_t key_lo, uint64_t key_hi, double p, int32_t* parent_counts,
-                             int64_t* n_selected) {
+namespace {
+int ensure_select(evo_ctx* c) {
+  if (c->sel_list) return 0;
+  const long long n = c->ncell();
+  cudaError_t e;
+  if ((e = c->alloc(&c->sel_list, (size_t)n)) != cudaSuccess ||
+      (e = c->alloc(&c->sel_chunk_cnt, (size_t)evo::select_chunks(n) + 1)) != cudaSuccess ||
+      (e = c->alloc(&c->sel_chunk_off, (size_t)evo::select_chunks(n) + 1)) != cudaSuccess ||
+      (e = c->alloc(&c->sel_n, 1)) != cudaSuccess || (e = c->alloc(&c->sel_parent, (size_t)c->cap)) != cudaSuccess ||
+      (e = c->alloc(&c->sel_map, (size_t)c->cap)) != cudaSuccess)
+    return fail((int)e, std::string("selection buffers: ") + cudaGetErrorString(e));
+  return 0;
+}
+}  // namespace
+
+EVO_API int evo_count_occupied(evo_ctx* c, int64_t* n_occupied) {
+  if (int r = check_ctx(c)) return r;
+  if (!n_occupied) return fail(EVO_EINVAL, "n_occupied is null");
+  if (int r = ensure_select(c)) return r;
+  const long long n = c->ncell();
+  CK(evo::launch_count_occupied(c->buf[c->front].gi + c->W, n, c->sel_chunk_cnt, c->sel_chunk_off, c->stream));
+  long long tot = 0;
+  CK(cudaMemcpyAsync(&tot, c->sel_chunk_off + evo::select_chunks(n), sizeof(tot), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  *n_occupied = tot;
+  return 0;
+}
+
+EVO_API int evo_select_cells_at(evo_ctx* c, uint64_t key_lo, uint64_t key_hi, double p, int64_t first_draw,
+                                int32_t* parent_counts, int64_t* n_selected) {
   if (int r = check_ctx(c)) return r;
   if (!(p >= 0.0 && p <= 1.0)) return fail(EVO_EINVAL, "selection probability must be in [0, 1]");
-  if (c->strip) return fail(EVO_EINVAL, "field selection ranks cells over the whole torus: single-context only");
+  if (first_draw < 0) return fail(EVO_EINVAL, "first_draw must be >= 0");
+  if (int r = ensure_select(c)) return r;
   const long long n = c->ncell();
-  if (!c->sel_list) {
-    cudaError_t e;
-    if ((e = c->alloc(&c->sel_list, (size_t)n)) != cudaSuccess ||
-        (e = c->alloc(&c->sel_chunk_cnt, (size_t)evo::select_chunks(n) + 1)) != cudaSuccess ||
-        (e = c->alloc(&c->sel_chunk_off, (size_t)evo::select_chunks(n) + 1)) != cudaSuccess ||
-        (e = c->alloc(&c->sel_n, 1)) != cudaSuccess || (e = c->alloc(&c->sel_parent, (size_t)c->cap)) != cudaSuccess ||
-        (e = c->alloc(&c->sel_map, (size_t)c->cap)) != cudaSuccess)
-      return fail((int)e, std::string("selection buffers: ") + cudaGetErrorString(e));
-  }
   CK(evo::launch_select_cells(c->buf[c->front].gi + c->W, n, key_lo, key_hi, p, c->sel_chunk_cnt, c->sel_chunk_off,
-                              c->sel_list, c->sel_n, c->sel_parent, c->cap, c->stream));
+                              c->sel_list, c->sel_n, c->sel_parent, c->cap, (long long)first_draw, c->stream));
   c->have_select = true;
   unsigned long long ns = 0;
   CK(cudaMemcpyAsync(&ns, c->sel_n, sizeof(ns), cudaMemcpyDeviceToHost, c->stream));
@@ -1308,6 +1328,13 @@ EVO_API int evo_select_cells(evo_ctx* c, uint64_t key_lo, uint64_t key_hi, doubl
   CK(cudaStreamSynchronize(c->stream));
   if (n_selected) *n_selected = (int64_t)ns;
   return 0;
+}
+
+EVO_API int evo_select_cells(evo_ctx* c, uint64_t key_lo, uint64_t key_hi, double p, int32_t* parent_counts,
+                             int64_t* n_selected) {
+  if (int r = check_ctx(c)) return r;
+  if (c->strip) return fail(EVO_EINVAL, "a strip context draws after the strips above it: use evo_select_cells_at");
+  return evo_select_cells_at(c, key_lo, key_hi, p, 0, parent_counts, n_selected);
 }
 
 EVO_API int evo_read_selected(evo_ctx* c, int64_t capacity, int64_t* cells, int64_t* n) {

@@ -212,7 +212,10 @@ cudaError_t launch_hidden_tc(const HidBuffers& b, const StepGeom& g, const Plane
 int select_chunks(long long n);
 cudaError_t launch_select_cells(const int32_t* gi, long long n, unsigned long long k0, unsigned long long k1, double p,
                                 int32_t* chunk_cnt, long long* chunk_off, int32_t* list, unsigned long long* n_sel,
-                                int32_t* parent_cnt, int capacity, cudaStream_t st);
+                                int32_t* parent_cnt, int capacity, long long first_draw, cudaStream_t st);
+// occupied cells of the plane: chunk_off[select_chunks(n)] <- the total
+cudaError_t launch_count_occupied(const int32_t* gi, long long n, int32_t* chunk_cnt, long long* chunk_off,
+                                  cudaStream_t st);
 cudaError_t launch_remap_selected(int32_t* gi, const int32_t* list, const unsigned long long* n_sel,
                                   const int32_t* map, long long max_n, cudaStream_t st);
 int cppn_threads(int max_nodes);  // 0 -> program too large

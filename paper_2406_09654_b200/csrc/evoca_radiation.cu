@@ -67,10 +67,12 @@ __global__ void k_occ_count(const int32_t* gi, long long n, int32_t* chunk_cnt) 
 }
 
 // exclusive scan of the chunk counts (one CTA; chunk counts are few)
-__global__ void k_chunk_scan(const int32_t* cnt, long long* off, int nchunks) {
+// (offsets start at `first`: a row strip's cells draw after those of the
+// strips above it; off[nchunks] receives first + the strip's total)
+__global__ void k_chunk_scan(const int32_t* cnt, long long* off, int nchunks, long long first) {
   __shared__ long long carry;
   __shared__ long long warp_tot[32];
-  if (threadIdx.x == 0) carry = 0;
+  if (threadIdx.x == 0) carry = first;
   __syncthreads();
   for (int b0 = 0; b0 < nchunks; b0 += 1024) {
     const int i = b0 + threadIdx.x;
@@ -98,6 +100,7 @@ __global__ void k_chunk_scan(const int32_t* cnt, long long* off, int nchunks) {
     if (threadIdx.x == 1023) carry += warp_tot[w] + x;
     __syncthreads();
   }
+  if (threadIdx.x == 0) off[nchunks] = carry;
 }
 
 __global__ void k_select(const int32_t* gi, long long n, const long long* chunk_off, unsigned long long k0,
@@ -153,15 +156,24 @@ __global__ void k_remap(int32_t* gi, const int32_t* list, const unsigned long lo
 
 int select_chunks(long long n) { return (int)((n + kSelChunk - 1) / kSelChunk); }
 
+cudaError_t launch_count_occupied(const int32_t* gi, long long n, int32_t* chunk_cnt, long long* chunk_off,
+                                  cudaStream_t st) {
+  const int nch = select_chunks(n);
+  if (nch == 0) return cudaMemsetAsync(chunk_off, 0, sizeof(long long), st);
+  k_occ_count<<<nch, kSelThreads, 0, st>>>(gi, n, chunk_cnt);
+  k_chunk_scan<<<1, 1024, 0, st>>>(chunk_cnt, chunk_off, nch, 0);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_select_cells(const int32_t* gi, long long n, unsigned long long k0, unsigned long long k1, double p,
                                 int32_t* chunk_cnt, long long* chunk_off, int32_t* list, unsigned long long* n_sel,
-                                int32_t* parent_cnt, int capacity, cudaStream_t st) {
+                                int32_t* parent_cnt, int capacity, long long first_draw, cudaStream_t st) {
   const int nch = select_chunks(n);
   cudaError_t e = cudaMemsetAsync(n_sel, 0, sizeof(unsigned long long), st);
   if (e == cudaSuccess) e = cudaMemsetAsync(parent_cnt, 0, (size_t)capacity * sizeof(int32_t), st);
   if (e != cudaSuccess || nch == 0) return e;
   k_occ_count<<<nch, kSelThreads, 0, st>>>(gi, n, chunk_cnt);
-  k_chunk_scan<<<1, 1024, 0, st>>>(chunk_cnt, chunk_off, nch);
+  k_chunk_scan<<<1, 1024, 0, st>>>(chunk_cnt, chunk_off, nch, first_draw);
   k_select<<<nch, kSelThreads, 0, st>>>(gi, n, chunk_off, k0, k1, p, list, n_sel, parent_cnt);
   return cudaGetLastError();
 }

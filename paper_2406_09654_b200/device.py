@@ -303,6 +303,21 @@ class DeviceSubstrate:
         check(self.lib.evo_select_cells(self.ctx, lo, hi, float(p), ptr(counts), C.byref(n)))
         return counts, n.value
 
+    def count_occupied(self) -> int:
+        """Occupied cells of the front genome plane (evo_count_occupied)."""
+        n = C.c_int64()
+        check(self.lib.evo_count_occupied(self.ctx, C.byref(n)))
+        return n.value
+
+    def select_cells_at(self, key: int, p: float, first_draw: int):
+        """evo_select_cells_at: the selection of a row strip whose occupied
+        cells take draws first_draw, first_draw + 1, ... of the stream."""
+        counts = np.zeros(self.capacity, np.int32)
+        n = C.c_int64()
+        lo, hi = int(key) & 0xFFFFFFFFFFFFFFFF, (int(key) >> 64) & 0xFFFFFFFFFFFFFFFF
+        check(self.lib.evo_select_cells_at(self.ctx, lo, hi, float(p), int(first_draw), ptr(counts), C.byref(n)))
+        return counts, n.value
+
     def read_selected(self) -> np.ndarray:
         n = C.c_int64()
         check(self.lib.evo_read_selected(self.ctx, 0, None, C.byref(n)))

@@ -135,18 +135,14 @@ def apply_radiation(events, pool, rates, planes, master_seed: int, step: int) ->
             cells[tgt] = slot
 
 
-def field_radiation(state, t: int, p: float = 0.01, rates: neat.EvolutionRates | None = None,
-                    purpose: str = "field_radiation") -> dict:
-    """One config-3 radiation event on the state's device front (call between
-    steps).  Returns {"selected", "parents", "children"}."""
-    from .engine import _binding, _fold_census
-
-    b = _binding(state)
-    dev = b.dev
-    pool = state.pool
-    _fold_census(state)  # admission must see the device's deaths (slot states, peaks)
+def admit_children(pool, counts, master_seed: int, t: int, rates=None):
+    """The host half of a field-radiation event (config-3 extension): one
+    mutated child per parent slot with selected cells (``counts``, per slot),
+    admitted in ascending parent order until the pool refuses; returns
+    (slot_map: parent -> child or -1, parents, children).  Deterministic
+    given the pool and counts, so every rank of a strip run admits the same
+    children."""
     rates = rates or neat.EvolutionRates()
-    counts, n_sel = dev.select_cells(stream_key(state.master_seed, t, purpose), p)
     parents = np.flatnonzero(counts)
     slot_map = np.full(pool.capacity, -1, np.int32)
     # admissions only fill slots, so the first `room` parents (ascending slot)
@@ -155,7 +151,7 @@ def field_radiation(state, t: int, p: float = 0.01, rates: neat.EvolutionRates |
     room = int(np.count_nonzero(np.asarray(pool.slot_states()) != 1)) if hasattr(pool, "slot_states") else None
     take = [int(x) for x in (parents if room is None else parents[:room])]
     kids = neat.mutate_batch([pool.genome(par) for par in take], rates,
-                             [stream_key(state.master_seed, t, "mutate", par) for par in take], pool.innovations)
+                             [stream_key(master_seed, t, "mutate", par) for par in take], pool.innovations)
     if hasattr(pool, "admit_batch"):
         children = pool.admit_batch(kids, [(pool.lineage(par),) for par in take], birth_step=t)
         slot_map[np.asarray(take[:len(children)], np.int64)] = children
@@ -167,6 +163,36 @@ def field_radiation(state, t: int, p: float = 0.01, rates: neat.EvolutionRates |
                 break
             slot_map[par] = slot
             children.append(slot)
+    return slot_map, parents, list(children)
+
+
+def express_on(dev, pool, slots) -> None:
+    """Device tables of newly admitted slots whose parameters are
+    DeviceExpressed (one batched evo_express_cppn per (tau, w_max)), binding
+    them to ``dev``."""
+    by_expr = {}
+    for s in slots:
+        prm = pool.params(s)
+        if isinstance(prm, DeviceExpressed):
+            by_expr.setdefault((prm.tau, prm.w_max), []).append((s, prm))
+    for (tau, w_max), items in by_expr.items():
+        dev.express_cppn([s for s, _ in items], [prm.genome for _, prm in items], tau, w_max)
+        for s, prm in items:
+            prm.bind(dev, s)
+
+
+def field_radiation(state, t: int, p: float = 0.01, rates: neat.EvolutionRates | None = None,
+                    purpose: str = "field_radiation") -> dict:
+    """One config-3 radiation event on the state's device front (call between
+    steps).  Returns {"selected", "parents", "children"}."""
+    from .engine import _binding, _fold_census
+
+    b = _binding(state)
+    dev = b.dev
+    pool = state.pool
+    _fold_census(state)  # admission must see the device's deaths (slot states, peaks)
+    counts, n_sel = dev.select_cells(stream_key(state.master_seed, t, purpose), p)
+    slot_map, parents, children = admit_children(pool, counts, state.master_seed, t, rates)
     b.sync_params(pool)  # one batched evo_express_cppn for every new slot
     dev.remap_selected(slot_map)
     b.device_ahead = True

@@ -233,6 +233,37 @@ class DeviceStrip:
         self.dev.swap()
 
 
+    def field_radiation(self, pool, master_seed: int, t: int, p: float = 0.01, rates=None,
+                        purpose: str = "field_radiation") -> dict:
+        """Config-3 field radiation over row strips (every rank calls it with
+        an identical pool): the strip's occupied cells draw after those of
+        the strips above it (an exclusive scan of the per-rank occupancy), so
+        the union of the ranks' selections is the one-context selection; the
+        per-slot parent counts are summed over the ranks, every rank admits
+        the same children (deterministic host NEAT), expresses them on its
+        own device and moves its own selected cells.  The caller folds the
+        device census into ``pool`` first where deaths matter."""
+        import torch
+
+        from .neat import stream_key
+        from .radiation import admit_children, express_on
+
+        world = self.plan.world
+        occ = torch.zeros(world, dtype=torch.int64, device="cuda")
+        occ[self.rank] = self.dev.count_occupied()
+        self.comm.sum_(occ)
+        first = int(occ[: self.rank].sum().item())
+        counts, n_sel = self.dev.select_cells_at(stream_key(master_seed, t, purpose), p, first)
+        tot = torch.from_numpy(counts.astype(np.int64)).cuda()
+        self.comm.sum_(tot)
+        counts = tot.cpu().numpy().astype(np.int32)
+        slot_map, parents, children = admit_children(pool, counts, master_seed, t, rates)
+        express_on(self.dev, pool, children)
+        self.dev.set_slots(np.asarray(pool.slot_states(), np.int8))
+        self.dev.remap_selected(slot_map)
+        return {"selected": int(counts.sum()), "parents": len(parents), "children": len(children)}
+
+
 def step_local(strips, scalars, t: int, flags: int = 0) -> None:
     """Step several strips driven by ONE process (e.g. a single-GPU
     emulation of a multi-rank run, or peer devices in one process): the
@@ -275,3 +306,29 @@ def step_local(strips, scalars, t: int, flags: int = 0) -> None:
         c.copy_(total)
         s.dev.census_finish(t, stream=stream)
         s.dev.swap()
+
+
+def field_radiation_local(strips, pools, master_seed: int, t: int, p: float = 0.01, rates=None,
+                          purpose: str = "field_radiation") -> dict:
+    """``DeviceStrip.field_radiation`` for strips driven by ONE process (as
+    ``step_local``): the occupancy scan and the parent-count sum are done on
+    the host; ``pools`` holds one identical pool per strip."""
+    from .neat import stream_key
+    from .radiation import admit_children, express_on
+
+    occ = [s.dev.count_occupied() for s in strips]
+    counts = np.zeros(strips[0].dev.capacity, np.int64)
+    first = 0
+    for s, n in zip(strips, occ):
+        c, _ = s.dev.select_cells_at(stream_key(master_seed, t, purpose), p, first)
+        counts += c
+        first += n
+    counts = counts.astype(np.int32)
+    out = None
+    for s, pool in zip(strips, pools):
+        slot_map, parents, children = admit_children(pool, counts, master_seed, t, rates)
+        express_on(s.dev, pool, children)
+        s.dev.set_slots(np.asarray(pool.slot_states(), np.int8))
+        s.dev.remap_selected(slot_map)
+        out = {"selected": int(counts.sum()), "parents": len(parents), "children": len(children)}
+    return out

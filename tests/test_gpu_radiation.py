@@ -104,3 +104,57 @@ def test_run_equals_step_loop_with_radiation():
     assert engine.digest(a) == engine.digest(b)
     assert a.pool.live_count() == b.pool.live_count()
     assert a.pool.next_lineage_id == b.pool.next_lineage_id > 8
+
+
+@pytest.mark.parametrize("world", [1, 2, 3])
+def test_field_radiation_over_strips(world):
+    """Config-3 field radiation on 1-3 row strips (one identical pool per
+    strip, the strips' occupied cells drawing after those above them,
+    parent counts summed): the genome plane and the children equal the
+    host restatement of the one-context event."""
+    from paper_2406_09654_b200.strips import DeviceStrip, StripPlan, field_radiation_local
+
+    H, W = 80, 96
+    st = engine.baseline_state("c3", width=W, height=H, genomes=12)
+    t = 7
+    f = st.substrate.front
+    gi0 = f.genome_index.ravel().copy()
+    pools = [copy.deepcopy(st.pool) for _ in range(world)]
+    ref = copy.deepcopy(st.pool)
+    ref.net_factory = None
+    occ = np.flatnonzero(gi0 >= 0)
+    sel = occ[neat.stream(st.master_seed, t, "field_radiation").random(len(occ)) < 0.02]
+    exp_gi = gi0.copy()
+    children = {}
+    for par in np.unique(gi0[sel]):
+        child = neat.mutate(ref.genome(int(par)), neat.EvolutionRates(),
+                            neat.stream(st.master_seed, t, "mutate", int(par)), ref.innovations)
+        slot = ref.admit(child, parents=(ref.lineage(int(par)),), birth_step=t)
+        children[slot] = child
+        exp_gi[sel[gi0[sel] == par]] = slot
+    plan = StripPlan(H, W, world)
+    strips = []
+    for r, pool in zip(range(world), pools):
+        s = DeviceStrip(plan, r, pool.capacity, hidden=0)
+        s.dev.set_params([pool.params(k) for k in range(pool.capacity)])  # as bench.py's strip setup
+        s.dev.set_slots(np.asarray(pool.slot_states(), np.int8))
+        row0, h = plan.rows(r)
+        Cm = f.channels["communication"]
+        s.dev.upload_arrays(f.channels["energy"][0][row0:row0 + h], f.channels["infrastructure"][0][row0:row0 + h],
+                            Cm[:, row0:row0 + h], f.genome_index[row0:row0 + h], f.rotation[row0:row0 + h])
+        strips.append(s)
+    info = field_radiation_local(strips, pools, st.master_seed, t, 0.02)
+    assert info["selected"] == len(sel) and info["children"] == len(children) > 0
+    got = np.empty((H, W), np.int32)
+    for r, s in enumerate(strips):
+        row0, h = plan.rows(r)
+        E = np.empty((h, W), np.float32)
+        Cm = np.empty((3, h, W), np.float32)
+        gi = np.empty((h, W), np.int32)
+        s.dev.download_arrays(E, E.copy(), Cm, gi, np.empty((h, W), np.uint8))
+        got[row0:row0 + h] = gi
+        s.dev.close()
+    np.testing.assert_array_equal(got.ravel(), exp_gi)
+    for pool in pools:
+        for slot, child in children.items():
+            assert pool.genome(slot) == child
