@@ -192,7 +192,7 @@ size_t sense_smem_bytes(int cap) { return sizeof(SenseSmem) + (size_t)((cap + 3)
 
 __global__ void __launch_bounds__(kSortThreads, 2) k_hid_sense(const StepGeom g, const Planes f, const int32_t* offs,
                                                             const int32_t* cta_base, int cap, float* sens,
-                                                            int32_t* rank_of_cell) {
+                                                            int32_t* rank_of_cell, int identity_rank) {
   extern __shared__ __align__(16) unsigned char sraw[];
   SenseSmem& sm = *reinterpret_cast<SenseSmem*>(sraw);
   int* cursor = reinterpret_cast<int*>(sraw + sizeof(SenseSmem));
@@ -290,7 +290,8 @@ __global__ void __launch_bounds__(kSortThreads, 2) k_hid_sense(const StepGeom g,
           for (int part = 0; part < 12; ++part)
             row[part] = make_float4(v[4 * part], v[4 * part + 1], v[4 * part + 2], v[4 * part + 3]);
         }
-        if (rank_of_cell) rank_of_cell[c] = rank;
+        // (identity_rank: the net writes each actuator row at its cell index)
+        if (rank_of_cell) rank_of_cell[c] = identity_rank ? (rank >= 0 ? c : -1) : rank;
       }
       __syncwarp();
       for (int k = lane; k < 32 * 12; k += 32) {  // 12 lanes per 192-byte row
@@ -1059,7 +1060,11 @@ __global__ void __launch_bounds__(kNetThreads, 1) k_hid_net2(const NetArgs a) {
 #pragma unroll
         for (int j = 0; j < kActuators; ++j) o[j] = squash(__fadd_rn(zs[j], bias2[j]));
         o[13] = o[14] = o[15] = 0.0f;
-        const size_t row = GATHER ? (size_t)gs::gcell(__ldg(a.sorted + ti.y + r), a.W).cell : (size_t)(ti.y + r);
+        // the actuator row at the cell index (the physics then reads it
+        // coalesced): the gather form's list entry, or element 45 of the
+        // sensor row (its cell index, k_hid_sense)
+        const size_t row = GATHER ? (size_t)gs::gcell(__ldg(a.sorted + ti.y + r), a.W).cell
+                                  : (size_t)__float_as_int(__ldg(a.sens + (size_t)(ti.y + r) * kK1 + 45));
         float4* dst = reinterpret_cast<float4*>(a.act + row * 16);
 #pragma unroll
         for (int j = 0; j < 4; ++j) dst[j] = make_float4(o[4 * j], o[4 * j + 1], o[4 * j + 2], o[4 * j + 3]);
@@ -1319,7 +1324,8 @@ cudaError_t launch_hidden_tc(const HidBuffers& b, const StepGeom& g, const Plane
   }
   // decided records of direct nets land at the cell index: no cell -> row map
   int32_t* rank = decided && net.hidden == 0 ? nullptr : b.rank;
-  k_hid_sense<<<nctas, kSortThreads, ssmem, st>>>(g, front, b.offs, b.cta_hist, capacity, b.sens, rank);
+  const bool net2 = net.hidden > 0 && !l2_cuda_core && hidden_tc_nh(net.hidden) <= 128 && hidden_tc_nh(net.hidden) % 32 == 0;
+  k_hid_sense<<<nctas, kSortThreads, ssmem, st>>>(g, front, b.offs, b.cta_hist, capacity, b.sens, rank, net2 ? 1 : 0);
   NetArgs a;
   a.net = net;
   a.nh = net.hidden > 0 ? hidden_tc_nh(net.hidden) : 0;
@@ -1335,7 +1341,7 @@ cudaError_t launch_hidden_tc(const HidBuffers& b, const StepGeom& g, const Plane
     k_direct_rows<<<num_sms * 4, kDrThreads, 0, st>>>(a);  // 16 warps per SM, one wave
     return cudaGetLastError();
   }
-  if (!l2_cuda_core && hidden_tc_nh(net.hidden) <= 128 && hidden_tc_nh(net.hidden) % 32 == 0) {
+  if (net2) {
     const size_t smem = hidden_tc2_smem(net.hidden);
     e = cudaFuncSetAttribute(k_hid_net2<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
