@@ -76,6 +76,23 @@ class ClockSampler:
         self._t = threading.Thread(target=self._loop, daemon=True)
 
     def _loop(self):
+        # NVML every 2 ms (a config-3 window of 20 steps lasts ~40 ms); the
+        # nvidia-smi query below is the fallback (~50 ms per call)
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            mx = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+            bits = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown", 0x4: "sw_power_cap"}
+            while not self._stop.is_set():
+                sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+                r = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                self.samples.append([str(sm), str(mx), ""] + ["Active" if r & b else "Not Active" for b in bits])
+                self._stop.wait(0.002)
+            return
+        except Exception:
+            pass
         while not self._stop.is_set():
             try:
                 out = subprocess.run(
