@@ -76,7 +76,7 @@ class ClockSampler:
         self._t = threading.Thread(target=self._loop, daemon=True)
 
     def _loop(self):
-        # NVML every 2 ms (a config-3 window of 20 steps lasts ~40 ms); the
+        # NVML every 5 ms (a config-3 window of 20 steps lasts ~40 ms); the
         # nvidia-smi query below is the fallback (~50 ms per call)
         try:
             import pynvml
@@ -89,7 +89,7 @@ class ClockSampler:
                 sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
                 r = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
                 self.samples.append([str(sm), str(mx), ""] + ["Active" if r & b else "Not Active" for b in bits])
-                self._stop.wait(0.002)
+                self._stop.wait(0.005)
             return
         except Exception:
             pass

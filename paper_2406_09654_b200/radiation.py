@@ -192,8 +192,20 @@ def field_radiation(state, t: int, p: float = 0.01, rates: neat.EvolutionRates |
     pool = state.pool
     _fold_census(state)  # admission must see the device's deaths (slot states, peaks)
     counts, n_sel = dev.select_cells(stream_key(state.master_seed, t, purpose), p)
+    synced = getattr(pool, "version", None) is not None and b.pool_version == pool.version
     slot_map, parents, children = admit_children(pool, counts, state.master_seed, t, rates)
-    b.sync_params(pool)  # one batched evo_express_cppn for every new slot
+    if synced and all(isinstance(pool.params(s), DeviceExpressed) for s in children):
+        # only the children changed: express exactly those (one batched
+        # evo_express_cppn) instead of sync_params' scan of every slot
+        express_on(dev, pool, children)
+        for s in children:
+            b.param_ids[s] = pool.params(s)
+        from .engine import _peaks, _slot_states
+
+        dev.set_slots(_slot_states(pool), _peaks(pool))
+        b.pool_version = pool.version
+    else:
+        b.sync_params(pool)  # one batched evo_express_cppn for every new slot
     dev.remap_selected(slot_map)
     b.device_ahead = True
     return {"selected": int(n_sel), "parents": len(parents), "children": len(children)}
