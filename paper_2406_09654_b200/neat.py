@@ -413,14 +413,16 @@ class PackedGenome(CppnGenome):
     built on first access; the radiation feed itself (mutation of children
     in later events, program compilation) works on the arrays."""
 
-    def __init__(self, flat: Flat):  # noqa: D107 - bypasses the dataclass init on purpose
+    def __init__(self, flat: Flat | None, batch=None, index: int = 0):  # noqa: D107 - bypasses the dataclass init
         object.__setattr__(self, "_flat", flat)
+        object.__setattr__(self, "_batch", batch)  # (GenomeBatch, index) when flat is still unsliced
+        object.__setattr__(self, "_index", index)
         object.__setattr__(self, "_genes", None)
 
     def _materialise(self):
         genes = object.__getattribute__(self, "_genes")
         if genes is None:
-            f = object.__getattribute__(self, "_flat")
+            f = pack(self)
             nodes = tuple(NodeGene(int(i), ROLE_NAME[int(r)], ACTIVATIONS[int(a)])
                           for i, r, a in zip(f.nid.tolist(), f.nrole.tolist(), f.nact.tolist()))
             conns = tuple(ConnGene(n, s_, d, w, bool(e)) for n, s_, d, w, e in
@@ -446,14 +448,37 @@ class PackedGenome(CppnGenome):
         return hash((self.nodes, self.connections))
 
     def __repr__(self):
-        f = object.__getattribute__(self, "_flat")
+        f = pack(self)
         return f"PackedGenome({len(f.nid)} nodes, {len(f.inn)} connections)"
+
+
+class GenomeBatch:
+    """The concatenated arrays of one native mutation's children (node /
+    connection offsets per genome); its PackedGenome members slice it on
+    demand, and consecutive members are handed to the next native call as
+    one slice instead of being re-concatenated."""
+
+    __slots__ = ("node_off", "conn_off", "arrays")
+
+    def __init__(self, node_off, conn_off, arrays):
+        self.node_off, self.conn_off, self.arrays = node_off, conn_off, arrays  # arrays: Flat order
+
+    def flat(self, i: int) -> Flat:
+        a, b = int(self.node_off[i]), int(self.node_off[i + 1])
+        c, d = int(self.conn_off[i]), int(self.conn_off[i + 1])
+        nid, nrole, nact, inn, src, dst, w, en = self.arrays
+        return Flat(nid[a:b], nrole[a:b], nact[a:b], inn[c:d], src[c:d], dst[c:d], w[c:d], en[c:d])
 
 
 def pack(genome) -> Flat:
     """Flat arrays of a genome (cached on this package's genome objects)."""
     f = genome.__dict__.get("_flat") if hasattr(genome, "__dict__") else None
     if f is not None:
+        return f
+    b = genome.__dict__.get("_batch") if hasattr(genome, "__dict__") else None
+    if b is not None:
+        f = b.flat(genome.__dict__["_index"])
+        object.__setattr__(genome, "_flat", f)
         return f
     nodes, conns = genome.nodes, genome.connections
     f = Flat(np.fromiter((n.id for n in nodes), np.int64, len(nodes)),
@@ -469,18 +494,57 @@ def pack(genome) -> Flat:
     return f
 
 
-def _concat(flats):
-    def cat(name, dtype):
-        parts = [getattr(f, name) for f in flats]
-        return np.ascontiguousarray(np.concatenate(parts) if parts else np.empty(0, dtype), dtype)
+_FLAT_FIELDS = (("nid", np.int64), ("nrole", np.int8), ("nact", np.int8), ("inn", np.int64), ("src", np.int64),
+                ("dst", np.int64), ("w", np.float64), ("en", np.uint8))
 
-    node_off = np.zeros(len(flats) + 1, np.int32)
-    node_off[1:] = np.cumsum([len(f.nid) for f in flats])
-    conn_off = np.zeros(len(flats) + 1, np.int32)
-    conn_off[1:] = np.cumsum([len(f.inn) for f in flats])
-    return (node_off, cat("nid", np.int64), cat("nrole", np.int8), cat("nact", np.int8), conn_off,
-            cat("inn", np.int64), cat("src", np.int64), cat("dst", np.int64), cat("w", np.float64),
-            cat("en", np.uint8))
+
+def _concat(genomes):
+    """(node_off, nid, nrole, nact, conn_off, inn, src, dst, w, en) of a list
+    of genomes; runs of consecutive members of one GenomeBatch are taken as
+    single slices of its arrays.  A list with no such run becomes a batch
+    itself (the genomes are immutable), so the next call over the same
+    genomes - the seed population's first mutation after its expression -
+    skips the per-genome concatenation."""
+    n = len(genomes)
+    fresh = True
+    parts = [[] for _ in _FLAT_FIELDS]
+    node_off = np.zeros(n + 1, np.int32)
+    conn_off = np.zeros(n + 1, np.int32)
+    i = 0
+    while i < n:
+        g = genomes[i]
+        d = g.__dict__ if hasattr(g, "__dict__") else {}
+        b = d.get("_batch")
+        if b is not None:
+            fresh = False
+            i0 = d["_index"]
+            j = i + 1
+            while j < n and getattr(genomes[j], "__dict__", {}).get("_batch") is b and \
+                    genomes[j].__dict__["_index"] == i0 + (j - i):
+                j += 1
+            i1 = i0 + (j - i)
+            na, nb = int(b.node_off[i0]), int(b.node_off[i1])
+            ca, cb = int(b.conn_off[i0]), int(b.conn_off[i1])
+            for k, arr in enumerate(b.arrays):
+                parts[k].append(arr[na:nb] if k < 3 else arr[ca:cb])
+            node_off[i + 1:j + 1] = node_off[i] + (b.node_off[i0 + 1:i1 + 1] - na)
+            conn_off[i + 1:j + 1] = conn_off[i] + (b.conn_off[i0 + 1:i1 + 1] - ca)
+            i = j
+            continue
+        f = pack(g)
+        for k, (name, _) in enumerate(_FLAT_FIELDS):
+            parts[k].append(getattr(f, name))
+        node_off[i + 1] = node_off[i] + len(f.nid)
+        conn_off[i + 1] = conn_off[i] + len(f.inn)
+        i += 1
+    cat = [np.ascontiguousarray(np.concatenate(p) if len(p) > 1 else (p[0] if p else np.empty(0, dt)), dt)
+           for p, (_, dt) in zip(parts, _FLAT_FIELDS)]
+    if fresh and n > 1 and all(isinstance(g, CppnGenome) for g in genomes):
+        batch = GenomeBatch(node_off, conn_off, tuple(cat))
+        for i, g in enumerate(genomes):
+            object.__setattr__(g, "_batch", batch)
+            object.__setattr__(g, "_index", i)
+    return (node_off, cat[0], cat[1], cat[2], conn_off, cat[3], cat[4], cat[5], cat[6], cat[7])
 
 
 def _native():
@@ -505,12 +569,9 @@ def mutate_batch(genomes, rates, keys, counter: InnovationCounter) -> list:
     if n == 0:
         return []
     lib = _native()
-    flats = [pack(g) for g in genomes]
-    node_off, nid, nrole, nact, conn_off, inn, src, dst, w, en = _concat(flats)
-    kw = np.empty(2 * n, np.uint64)
+    node_off, nid, nrole, nact, conn_off, inn, src, dst, w, en = _concat(genomes)
     m = (1 << 64) - 1
-    for i, k in enumerate(keys):
-        kw[2 * i], kw[2 * i + 1] = int(k) & m, (int(k) >> 64) & m
+    kw = np.array([h for k in keys for h in (int(k) & m, (int(k) >> 64) & m)], np.uint64)
     r = np.array([rates.weight_reset_prob, rates.weight_perturb_prob, rates.weight_perturb_sigma,
                   rates.add_connection_prob, rates.add_node_prob, rates.toggle_enable_prob], np.float64)
     ctr = np.array([counter.next_innovation, counter.next_node_id], np.int64)
@@ -524,13 +585,8 @@ def mutate_batch(genomes, rates, keys, counter: InnovationCounter) -> list:
                                     ptr(o_nid), ptr(o_nrole), ptr(o_nact), ptr(o_conn_off), ptr(o_inn), ptr(o_src),
                                     ptr(o_dst), ptr(o_w), ptr(o_en)))
     counter.next_innovation, counter.next_node_id = int(ctr[0]), int(ctr[1])
-    out = []
-    for g in range(n):
-        a, b = o_node_off[g], o_node_off[g + 1]
-        c, d = o_conn_off[g], o_conn_off[g + 1]
-        out.append(PackedGenome(Flat(o_nid[a:b], o_nrole[a:b], o_nact[a:b], o_inn[c:d], o_src[c:d], o_dst[c:d],
-                                     o_w[c:d], o_en[c:d])))
-    return out
+    batch = GenomeBatch(o_node_off, o_conn_off, (o_nid, o_nrole, o_nact, o_inn, o_src, o_dst, o_w, o_en))
+    return [PackedGenome(None, batch, g) for g in range(n)]
 
 
 def compile_programs(genomes):
@@ -539,8 +595,7 @@ def compile_programs(genomes):
     from ._lib import ptr
 
     n = len(genomes)
-    flats = [pack(g) for g in genomes]
-    node_off, nid, nrole, nact, conn_off, inn, src, dst, w, en = _concat(flats)
+    node_off, nid, nrole, nact, conn_off, inn, src, dst, w, en = _concat(genomes)
     prog_off = np.empty(n + 1, np.int32)
     nodes = np.empty((max(len(nid), 1), 4), np.int32)
     esrc = np.empty(max(len(inn), 1), np.int32)

@@ -44,3 +44,16 @@ for k in range(4):
     tot = 1e3 * (time.perf_counter() - t0)
     print(f"radiation event {k}: {tot:.1f} ms {r} " + ", ".join(f"{n} {1e3 * v:.2f}" for n, v in timers.items()),
           flush=True)
+
+if "--profile" in sys.argv:
+    import cProfile
+    import pstats
+
+    st.substrate.step_counter = 300
+    pr = cProfile.Profile()
+    pr.enable()
+    for k in range(3):
+        radiation.field_radiation(st, 300 + 50 * k, 0.01)
+        dev.sync()
+    pr.disable()
+    pstats.Stats(pr).sort_stats("cumtime").print_stats(40)
