@@ -261,9 +261,10 @@ EVO_API int evo_neat_compile(int n, const int32_t* node_off, const int64_t* node
                              int32_t* nodes_out, int32_t* edge_src, double* edge_w, int32_t* outs) {
   int32_t np_ = 0, ne = 0;
   prog_off[0] = 0;
-  std::vector<int> indeg, order, pos_of, frontier;
+  // scratch reused across genomes (no per-genome allocations once grown);
+  // out-edges in CSR form, each node's list in connection order
+  std::vector<int> indeg, order, pos_of, frontier, csrc, cdst, adj_off, adj, inputs, outputs;
   std::vector<int64_t> ids;
-  std::vector<std::vector<int>> out_adj;
   for (int g = 0; g < n; ++g) {
     const int n0 = node_off[g], nn = node_off[g + 1] - n0;
     const int c0 = conn_off[g], nc = conn_off[g + 1] - c0;
@@ -274,8 +275,9 @@ EVO_API int evo_neat_compile(int n, const int32_t* node_off, const int64_t* node
       return -1;
     };
     indeg.assign(nn, 0);
-    out_adj.assign(nn, {});
-    std::vector<int> csrc(nc), cdst(nc);
+    adj_off.assign(nn + 1, 0);
+    csrc.resize(nc);
+    cdst.resize(nc);
     for (int k = 0; k < nc; ++k) {
       csrc[k] = local(c_src[c0 + k]);
       cdst[k] = local(c_dst[c0 + k]);
@@ -284,8 +286,16 @@ EVO_API int evo_neat_compile(int n, const int32_t* node_off, const int64_t* node
         return EVO_EINVAL;
       }
       indeg[cdst[k]]++;
-      out_adj[csrc[k]].push_back(cdst[k]);
+      adj_off[csrc[k] + 1]++;
     }
+    for (int i = 0; i < nn; ++i) adj_off[i + 1] += adj_off[i];
+    adj.resize(nc);
+    for (int k = 0, i; k < nc; ++k) {
+      i = csrc[k];
+      adj[adj_off[i]++] = cdst[k];
+    }
+    for (int i = nn; i > 0; --i) adj_off[i] = adj_off[i - 1];
+    adj_off[0] = 0;
     frontier.clear();
     for (int i = 0; i < nn; ++i)
       if (indeg[i] == 0) frontier.push_back(i);
@@ -297,8 +307,8 @@ EVO_API int evo_neat_compile(int n, const int32_t* node_off, const int64_t* node
       const int v = frontier.back();
       frontier.pop_back();
       order.push_back(v);
-      for (int m : out_adj[v])
-        if (--indeg[m] == 0) {
+      for (int e = adj_off[v]; e < adj_off[v + 1]; ++e)
+        if (const int m = adj[e]; --indeg[m] == 0) {
           frontier.push_back(m);
           std::push_heap(frontier.begin(), frontier.end(), by_id);
         }
@@ -310,11 +320,11 @@ EVO_API int evo_neat_compile(int n, const int32_t* node_off, const int64_t* node
     pos_of.assign(nn, 0);
     for (int p = 0; p < nn; ++p) pos_of[order[p]] = p;
     // input positions: inputs ranked by id
-    std::vector<int> inputs;
+    inputs.clear();
     for (int i = 0; i < nn; ++i)
       if (node_role[n0 + i] == 0) inputs.push_back(i);
     std::sort(inputs.begin(), inputs.end(), [&](int a, int b) { return ids[a] < ids[b]; });
-    std::vector<int> outputs;
+    outputs.clear();
     for (int i = 0; i < nn; ++i)
       if (node_role[n0 + i] == 2) outputs.push_back(i);
     std::sort(outputs.begin(), outputs.end(), [&](int a, int b) { return ids[a] < ids[b]; });
