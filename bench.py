@@ -181,8 +181,7 @@ def run_ours(args, rank, world, local):
             if radiate and (t + 1) % cfg.radiation_every == 0:
                 # over the strips: global draw order, summed parent counts,
                 # identical children on every rank (DeviceStrip.field_radiation)
-                stream.synchronize()
-                strip.field_radiation(state.pool, state.master_seed, t + 1, cfg.radiation_p)
+                strip.field_radiation(state.pool, state.master_seed, t + 1, cfg.radiation_p, wait=stream.synchronize)
             if e2 is not None:
                 e2.record(stream)
             return
@@ -195,8 +194,9 @@ def run_ours(args, rank, world, local):
             from paper_2406_09654_b200 import radiation
 
             state.substrate.step_counter = t + 1
-            stream.synchronize()  # the radiation calls run on the context's own stream
-            radiation.field_radiation(state, t + 1, cfg.radiation_p)  # host NEAT + device selection/expression
+            # host NEAT planned while the step runs; then the radiation's
+            # device calls (on the context's own stream) wait for the step
+            radiation.field_radiation(state, t + 1, cfg.radiation_p, wait=stream.synchronize)
         if e2 is not None:
             e2.record(stream)
 

@@ -255,6 +255,22 @@ EVO_API int evo_neat_mutate(int n, const uint64_t* keys, const double* rates, in
                             int32_t* o_node_off, int64_t* o_node_id, int8_t* o_node_role, int8_t* o_node_act,
                             int32_t* o_conn_off, int64_t* o_innov, int64_t* o_src, int64_t* o_dst, double* o_w,
                             uint8_t* o_en);
+/* evo_neat_mutate with the numbering deferred: the same draws, but the k-th
+ * new connection of a genome gets innovation -1 - k and its new node (at
+ * most one) the id EVO_NEAT_DEFERRED_NODE (above every real id, so program
+ * order is unaffected); no counter is read or consumed.  The caller numbers
+ * the genomes it admits, in order, from the shared counter afterwards
+ * (paper_2406_09654_b200.neat.number_deferred) - equal to evo_neat_mutate
+ * over the admitted genomes alone.  Lets the host draws of a radiation
+ * event run while the step before it is still on the device. */
+#define EVO_NEAT_DEFERRED_NODE INT64_MAX
+EVO_API int evo_neat_mutate_deferred(int n, const uint64_t* keys, const double* rates, const int32_t* node_off,
+                                     const int64_t* node_id, const int8_t* node_role, const int8_t* node_act,
+                                     const int32_t* conn_off, const int64_t* c_innov, const int64_t* c_src,
+                                     const int64_t* c_dst, const double* c_w, const uint8_t* c_en,
+                                     int32_t* o_node_off, int64_t* o_node_id, int8_t* o_node_role,
+                                     int8_t* o_node_act, int32_t* o_conn_off, int64_t* o_innov, int64_t* o_src,
+                                     int64_t* o_dst, double* o_w, uint8_t* o_en);
 /* The evo_express_cppn program arrays of n flat genomes (hypernet.py:100-155
  * order; paper_2406_09654_b200.neat.compile_programs layout): prog_off
  * [n+1], nodes_out [total nodes][4], edge_src / edge_w [total enabled

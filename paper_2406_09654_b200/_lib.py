@@ -96,6 +96,7 @@ SIGNATURES = {
     "evo_debug_phase_cycles": [_P, _I],
     "evo_debug_hidden_cycles": [_P, _I],
     "evo_neat_mutate": [_I, _P, _P, _P] + [_P] * 10 + [_P] * 10,
+    "evo_neat_mutate_deferred": [_I, _P, _P] + [_P] * 10 + [_P] * 10,
     "evo_neat_compile": [_I] + [_P] * 9 + [_P] * 5,
     "evo_neat_last_error": [],
 }

@@ -21,6 +21,7 @@
 #include <stdint.h>
 
 #include <algorithm>
+#include <cstdint>
 #include <cmath>
 #include <string>
 #include <utility>
@@ -145,26 +146,37 @@ bool creates_cycle(const std::vector<Conn>& cs, int64_t src, int64_t dst) {
 
 thread_local std::string g_neat_err;
 
+constexpr int64_t kDeferredNode = INT64_MAX;  // = EVO_NEAT_DEFERRED_NODE
+
 }  // namespace
 
 extern "C" {
 
 EVO_API const char* evo_neat_last_error(void) { return g_neat_err.c_str(); }
 
-EVO_API int evo_neat_mutate(int n, const uint64_t* keys, const double* rates, int64_t* counter,
-                            const int32_t* node_off, const int64_t* node_id, const int8_t* node_role,
-                            const int8_t* node_act, const int32_t* conn_off, const int64_t* c_innov,
-                            const int64_t* c_src, const int64_t* c_dst, const double* c_w, const uint8_t* c_en,
-                            int32_t* o_node_off, int64_t* o_node_id, int8_t* o_node_role, int8_t* o_node_act,
-                            int32_t* o_conn_off, int64_t* o_innov, int64_t* o_src, int64_t* o_dst, double* o_w,
-                            uint8_t* o_en) {
-  if (n < 0 || (n > 0 && (!keys || !rates || !counter || !node_off || !conn_off))) {
+}  // extern "C"
+
+namespace {
+
+// deferred: new genes keep placeholder numbers instead of drawing from the
+// shared counter - the k-th new connection of a genome gets innovation
+// -1 - k, its new node id kDeferredNode (larger than every existing id, as
+// the real one will be) - so the draws of a batch can run before it is known
+// which genomes will be admitted (the numbering is done afterwards, in the
+// admitted genomes' order: neat.number_deferred)
+int mutate_impl(bool deferred, int n, const uint64_t* keys, const double* rates, int64_t* counter,
+                const int32_t* node_off, const int64_t* node_id, const int8_t* node_role, const int8_t* node_act,
+                const int32_t* conn_off, const int64_t* c_innov, const int64_t* c_src, const int64_t* c_dst,
+                const double* c_w, const uint8_t* c_en, int32_t* o_node_off, int64_t* o_node_id, int8_t* o_node_role,
+                int8_t* o_node_act, int32_t* o_conn_off, int64_t* o_innov, int64_t* o_src, int64_t* o_dst,
+                double* o_w, uint8_t* o_en) {
+  if (n < 0 || (n > 0 && (!keys || !rates || (!deferred && !counter) || !node_off || !conn_off))) {
     g_neat_err = "evo_neat_mutate: bad arguments";
     return EVO_EINVAL;
   }
   const double p_reset = rates[0], p_perturb = rates[1], sigma = rates[2], p_conn = rates[3], p_node = rates[4],
                p_toggle = rates[5];
-  int64_t next_innov = counter[0], next_node = counter[1];
+  int64_t next_innov = deferred ? 0 : counter[0], next_node = deferred ? 0 : counter[1];
   std::vector<Conn> cs;
   std::vector<Node> ns;
   int32_t on = 0, oc = 0;
@@ -172,6 +184,8 @@ EVO_API int evo_neat_mutate(int n, const uint64_t* keys, const double* rates, in
   o_conn_off[0] = 0;
   for (int g = 0; g < n; ++g) {
     Philox rng(keys[2 * g], keys[2 * g + 1]);
+    int64_t k_new = 0;  // deferred: placeholders restart per genome
+    auto new_innov = [&]() { return deferred ? -1 - k_new++ : next_innov++; };
     cs.clear();
     ns.clear();
     for (int32_t i = conn_off[g]; i < conn_off[g + 1]; ++i)
@@ -206,7 +220,7 @@ EVO_API int evo_neat_mutate(int n, const uint64_t* keys, const double* rates, in
       if (!cands.empty()) {
         const auto pick = cands[(size_t)rng.integers((int64_t)cands.size())];
         const double w = rng.uniform(-1.0, 1.0);
-        cs.push_back({next_innov++, pick.first, pick.second, w, 1});
+        cs.push_back({new_innov(), pick.first, pick.second, w, 1});
       }
     }
     if (rng.random() < p_node) {
@@ -216,12 +230,13 @@ EVO_API int evo_neat_mutate(int n, const uint64_t* keys, const double* rates, in
       if (!enabled.empty()) {
         const int pick = enabled[(size_t)rng.integers((int64_t)enabled.size())];
         const Conn old = cs[pick];
-        const int64_t nid = next_node++;
+        const int64_t nid = deferred ? kDeferredNode : next_node++;
         const int8_t act = (int8_t)rng.integers(6);
         cs[pick].en = 0;
         ns.push_back({nid, 1, act});
-        cs.push_back({next_innov++, old.src, nid, 1.0, 1});
-        cs.push_back({next_innov++, nid, old.dst, old.w, 1});
+        const int64_t i0 = new_innov();
+        cs.push_back({i0, old.src, nid, 1.0, 1});
+        cs.push_back({new_innov(), nid, old.dst, old.w, 1});
       }
     }
     for (const Node& v : ns) {
@@ -241,9 +256,39 @@ EVO_API int evo_neat_mutate(int n, const uint64_t* keys, const double* rates, in
     o_node_off[g + 1] = on;
     o_conn_off[g + 1] = oc;
   }
-  counter[0] = next_innov;
-  counter[1] = next_node;
+  if (!deferred) {
+    counter[0] = next_innov;
+    counter[1] = next_node;
+  }
   return 0;
+}
+
+}  // namespace
+
+extern "C" {
+
+EVO_API int evo_neat_mutate(int n, const uint64_t* keys, const double* rates, int64_t* counter,
+                            const int32_t* node_off, const int64_t* node_id, const int8_t* node_role,
+                            const int8_t* node_act, const int32_t* conn_off, const int64_t* c_innov,
+                            const int64_t* c_src, const int64_t* c_dst, const double* c_w, const uint8_t* c_en,
+                            int32_t* o_node_off, int64_t* o_node_id, int8_t* o_node_role, int8_t* o_node_act,
+                            int32_t* o_conn_off, int64_t* o_innov, int64_t* o_src, int64_t* o_dst, double* o_w,
+                            uint8_t* o_en) {
+  return mutate_impl(false, n, keys, rates, counter, node_off, node_id, node_role, node_act, conn_off, c_innov, c_src,
+                     c_dst, c_w, c_en, o_node_off, o_node_id, o_node_role, o_node_act, o_conn_off, o_innov, o_src,
+                     o_dst, o_w, o_en);
+}
+
+EVO_API int evo_neat_mutate_deferred(int n, const uint64_t* keys, const double* rates, const int32_t* node_off,
+                                     const int64_t* node_id, const int8_t* node_role, const int8_t* node_act,
+                                     const int32_t* conn_off, const int64_t* c_innov, const int64_t* c_src,
+                                     const int64_t* c_dst, const double* c_w, const uint8_t* c_en,
+                                     int32_t* o_node_off, int64_t* o_node_id, int8_t* o_node_role,
+                                     int8_t* o_node_act, int32_t* o_conn_off, int64_t* o_innov, int64_t* o_src,
+                                     int64_t* o_dst, double* o_w, uint8_t* o_en) {
+  return mutate_impl(true, n, keys, rates, nullptr, node_off, node_id, node_role, node_act, conn_off, c_innov, c_src,
+                     c_dst, c_w, c_en, o_node_off, o_node_id, o_node_role, o_node_act, o_conn_off, o_innov, o_src,
+                     o_dst, o_w, o_en);
 }
 
 // Linearised pattern networks for evo_express_cppn (the layout of

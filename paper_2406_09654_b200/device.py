@@ -277,11 +277,13 @@ class DeviceSubstrate:
         check(self.lib.evo_get_params(self.ctx, slot0, n, ptr(w1), ptr(b1), ptr(w2), ptr(b2)))
         return w1, b1, w2, b2
 
-    def express_cppn(self, slots, genomes, tau: float = 0.2, w_max: float = 3.0, stream=None) -> None:
+    def express_cppn(self, slots, genomes, tau: float = 0.2, w_max: float = 3.0, stream=None,
+                     programs=None) -> None:
         """Generate the dense tables of ``slots`` from their pattern networks
         on the device (evo_express_cppn; reference generate_network,
         hypernet.py:183-220).  ``genomes`` are reference or neat.CppnGenome
-        objects; returns once the tables are written."""
+        objects (``programs``: their neat.compile_programs arrays, if already
+        compiled); returns once the tables are written."""
         from . import neat
 
         slots = np.ascontiguousarray(slots, np.int32)
@@ -289,7 +291,9 @@ class DeviceSubstrate:
             raise ValueError("one genome per slot")
         if len(slots) == 0:
             return
-        node_off, nodes, esrc, ew, outs = neat.compile_programs(genomes)
+        node_off, nodes, esrc, ew, outs = programs if programs is not None else neat.compile_programs(genomes)
+        if len(node_off) != len(slots) + 1:
+            raise ValueError("programs do not match the genomes")
         coords = neat.layout_coords(self.hidden)
         check(self.lib.evo_express_cppn(self.ctx, len(slots), ptr(slots), ptr(node_off), ptr(nodes), ptr(esrc),
                                         ptr(ew), ptr(outs), ptr(coords), float(tau), float(w_max), _stream(stream)))

@@ -45,6 +45,9 @@ __all__ = [
     "PackedGenome",
     "pack",
     "mutate_batch",
+    "mutate_batch_deferred",
+    "number_deferred",
+    "subset_programs",
     "layout_coords",
     "stream",
     "stream_key",
@@ -563,6 +566,54 @@ def mutate_batch(genomes, rates, keys, counter: InnovationCounter) -> list:
     ``stream_key(seed, t, "mutate", index)``), in list order, consuming the
     shared innovation counter as sequential ``mutate`` calls would; native
     (evo_neat_mutate).  Returns PackedGenome children."""
+    return _mutate_native(genomes, rates, keys, counter)
+
+
+DEFERRED_NODE = np.iinfo(np.int64).max  # EVO_NEAT_DEFERRED_NODE
+
+
+def mutate_batch_deferred(genomes, rates, keys) -> list:
+    """``mutate_batch`` with the numbering left open (evo_neat_mutate_deferred):
+    the k-th new connection of a child has innovation -1 - k, its new node
+    the id DEFERRED_NODE.  ``number_deferred`` over any ordered subset then
+    equals ``mutate_batch`` over the parents of that subset alone."""
+    return _mutate_native(genomes, rates, keys, None)
+
+
+def _excl_cumsum(x):
+    out = np.zeros(len(x), np.int64)
+    if len(x) > 1:
+        np.cumsum(x[:-1], out=out[1:])
+    return out
+
+
+def number_deferred(children, counter: InnovationCounter) -> list:
+    """Final innovation numbers / node ids for deferred children, taken from
+    ``counter`` in list order (per child: its new connections in creation
+    order, then its new node) - exactly what evo_neat_mutate draws."""
+    n = len(children)
+    if n == 0:
+        return []
+    node_off, nid, nrole, nact, conn_off, inn, src, dst, w, en = _concat(children)
+    gc = np.repeat(np.arange(n), np.diff(conn_off))
+    gn = np.repeat(np.arange(n), np.diff(node_off))
+    newc = inn < 0
+    cnt = np.bincount(gc[newc], minlength=n)
+    inn = inn.copy()
+    inn[newc] = (counter.next_innovation + _excl_cumsum(cnt))[gc[newc]] + (-1 - inn[newc])
+    newn = nid == DEFERRED_NODE
+    has = np.bincount(gn[newn], minlength=n)
+    nbase = counter.next_node_id + _excl_cumsum(has)
+    nid = np.where(newn, nbase[gn], nid)
+    src = np.where(src == DEFERRED_NODE, nbase[gc], src)
+    dst = np.where(dst == DEFERRED_NODE, nbase[gc], dst)
+    counter.next_innovation += int(cnt.sum())
+    counter.next_node_id += int(has.sum())
+    batch = GenomeBatch(node_off, conn_off, (nid, nrole, nact, inn, src, dst, w, en))
+    return [PackedGenome(None, batch, g) for g in range(n)]
+
+
+def _mutate_native(genomes, rates, keys, counter):
     from ._lib import ptr
 
     n = len(genomes)
@@ -574,19 +625,45 @@ def mutate_batch(genomes, rates, keys, counter: InnovationCounter) -> list:
     kw = np.array([h for k in keys for h in (int(k) & m, (int(k) >> 64) & m)], np.uint64)
     r = np.array([rates.weight_reset_prob, rates.weight_perturb_prob, rates.weight_perturb_sigma,
                   rates.add_connection_prob, rates.add_node_prob, rates.toggle_enable_prob], np.float64)
-    ctr = np.array([counter.next_innovation, counter.next_node_id], np.int64)
     NN, NC = len(nid) + n, len(inn) + 3 * n
     o_node_off, o_conn_off = np.empty(n + 1, np.int32), np.empty(n + 1, np.int32)
     o_nid, o_nrole, o_nact = np.empty(NN, np.int64), np.empty(NN, np.int8), np.empty(NN, np.int8)
     o_inn, o_src, o_dst = np.empty(NC, np.int64), np.empty(NC, np.int64), np.empty(NC, np.int64)
     o_w, o_en = np.empty(NC, np.float64), np.empty(NC, np.uint8)
-    _neat_check(lib.evo_neat_mutate(n, ptr(kw), ptr(r), ptr(ctr), ptr(node_off), ptr(nid), ptr(nrole), ptr(nact),
-                                    ptr(conn_off), ptr(inn), ptr(src), ptr(dst), ptr(w), ptr(en), ptr(o_node_off),
-                                    ptr(o_nid), ptr(o_nrole), ptr(o_nact), ptr(o_conn_off), ptr(o_inn), ptr(o_src),
-                                    ptr(o_dst), ptr(o_w), ptr(o_en)))
-    counter.next_innovation, counter.next_node_id = int(ctr[0]), int(ctr[1])
+    io = [ptr(node_off), ptr(nid), ptr(nrole), ptr(nact), ptr(conn_off), ptr(inn), ptr(src), ptr(dst), ptr(w),
+          ptr(en), ptr(o_node_off), ptr(o_nid), ptr(o_nrole), ptr(o_nact), ptr(o_conn_off), ptr(o_inn), ptr(o_src),
+          ptr(o_dst), ptr(o_w), ptr(o_en)]
+    if counter is None:
+        _neat_check(lib.evo_neat_mutate_deferred(n, ptr(kw), ptr(r), *io))
+    else:
+        ctr = np.array([counter.next_innovation, counter.next_node_id], np.int64)
+        _neat_check(lib.evo_neat_mutate(n, ptr(kw), ptr(r), ptr(ctr), *io))
+        counter.next_innovation, counter.next_node_id = int(ctr[0]), int(ctr[1])
     batch = GenomeBatch(o_node_off, o_conn_off, (o_nid, o_nrole, o_nact, o_inn, o_src, o_dst, o_w, o_en))
     return [PackedGenome(None, batch, g) for g in range(n)]
+
+
+def _ranges(starts, ends):
+    """Concatenated aranges [starts[i], ends[i])."""
+    lens = np.asarray(ends, np.int64) - np.asarray(starts, np.int64)
+    tot = int(lens.sum())
+    return np.repeat(np.asarray(starts, np.int64) - _excl_cumsum(lens), lens) + np.arange(tot)
+
+
+def subset_programs(programs, idx):
+    """The ``compile_programs`` arrays of the genomes ``idx`` (in that order)
+    cut out of the arrays of a larger batch (edge ranges rebased)."""
+    prog_off, nodes, esrc, ew, outs = programs
+    idx = np.asarray(idx, np.int64)
+    ns, nd = prog_off[idx].astype(np.int64), prog_off[idx + 1].astype(np.int64)
+    eb, ee = nodes[ns, 2].astype(np.int64), nodes[nd - 1, 3].astype(np.int64)
+    sub = nodes[_ranges(ns, nd)].copy()
+    shift = (_excl_cumsum(ee - eb) - eb).astype(np.int32)
+    sub[:, 2:4] += np.repeat(shift, nd - ns)[:, None]
+    eidx = _ranges(eb, ee)
+    off = np.zeros(len(idx) + 1, np.int32)
+    np.cumsum(nd - ns, out=off[1:])
+    return off, sub, np.ascontiguousarray(esrc[eidx]), np.ascontiguousarray(ew[eidx]), np.ascontiguousarray(outs[idx])
 
 
 def compile_programs(genomes):

@@ -25,7 +25,11 @@ Host NEAT (mutation, crossover, pool admission) stays on the host
   selected; one child per distinct parent slot is mutated on the host
   (native ``neat.mutate_batch``, each parent on ``stream(seed, t, "mutate",
   parent)``), admitted, its weights generated on the device, and the
-  selected cells move to it.
+  selected cells move to it.  The host draws do not depend on the
+  selection: ``plan_field_radiation`` mutates (numbering deferred) and
+  compiles a child for every live slot while the step before the event is
+  still running on the device, and the event numbers and admits the
+  children of the slots actually selected.
 """
 
 from __future__ import annotations
@@ -35,7 +39,7 @@ import numpy as np
 from . import neat
 
 __all__ = ["DeviceExpressed", "device_net_factory", "use_device_expression", "stream_key", "apply_radiation",
-           "field_radiation"]
+           "field_radiation", "plan_field_radiation", "FieldRadiationPlan"]
 
 
 stream_key = neat.stream_key
@@ -135,7 +139,48 @@ def apply_radiation(events, pool, rates, planes, master_seed: int, step: int) ->
             cells[tgt] = slot
 
 
-def admit_children(pool, counts, master_seed: int, t: int, rates=None):
+class FieldRadiationPlan:
+    """The selection-independent host half of a field-radiation event at
+    step ``t``: one deferred-numbering child (``neat.mutate_batch_deferred``,
+    parent slot s on ``stream(seed, t, "mutate", s)``) and its compiled
+    expression program for the first live slots (ascending) - as many as
+    the pool has room for, plus a margin: an event admits children for the
+    lowest parent slots only, until the pool is full."""
+
+    def __init__(self, pool, master_seed: int, t: int, rates=None):
+        self.master_seed, self.t = int(master_seed), int(t)
+        self.rates = rates or neat.EvolutionRates()
+        states = np.asarray(pool.slot_states())
+        room = int(np.count_nonzero(states != 1))  # grows if the census fold finds deaths: the margin
+        self.slots = np.flatnonzero(states == 1)[:room + max(32, room // 4)] if room else np.zeros(0, np.int64)
+        self.genomes = [pool.genome(int(s)) for s in self.slots]
+        self.children = neat.mutate_batch_deferred(
+            self.genomes, self.rates, [stream_key(master_seed, t, "mutate", int(s)) for s in self.slots])
+        self.programs = neat.compile_programs(self.children) if self.children else None
+        self.admitted = None  # plan positions of the children an event admitted
+
+    def positions(self, pool, master_seed: int, t: int, rates, take):
+        """Plan positions of the parent slots ``take``, or None when the plan
+        does not cover them unchanged (other step / seed / rates, a slot
+        not live at planning or holding another genome since)."""
+        if (int(master_seed), int(t)) != (self.master_seed, self.t) or (rates or neat.EvolutionRates()) != self.rates:
+            return None
+        take = np.asarray(take, np.int64)
+        pos = np.searchsorted(self.slots, take)
+        if len(take) and (pos.max() >= len(self.slots) or not np.array_equal(self.slots[pos], take)):
+            return None
+        if any(pool.genome(int(s)) is not self.genomes[int(i)] for s, i in zip(take, pos)):
+            return None
+        return pos
+
+
+def plan_field_radiation(pool, master_seed: int, t: int, rates=None) -> FieldRadiationPlan:
+    """Host NEAT of the field-radiation event at step ``t`` done ahead of the
+    device selection (call it while the preceding step runs)."""
+    return FieldRadiationPlan(pool, master_seed, t, rates)
+
+
+def admit_children(pool, counts, master_seed: int, t: int, rates=None, plan: FieldRadiationPlan | None = None):
     """The host half of a field-radiation event (config-3 extension): one
     mutated child per parent slot with selected cells (``counts``, per slot),
     admitted in ascending parent order until the pool refuses; returns
@@ -150,8 +195,12 @@ def admit_children(pool, counts, master_seed: int, t: int, rates=None):
     # refusal would mutate, consuming the innovation counter in that order
     room = int(np.count_nonzero(np.asarray(pool.slot_states()) != 1)) if hasattr(pool, "slot_states") else None
     take = [int(x) for x in (parents if room is None else parents[:room])]
-    kids = neat.mutate_batch([pool.genome(par) for par in take], rates,
-                             [stream_key(master_seed, t, "mutate", par) for par in take], pool.innovations)
+    pos = plan.positions(pool, master_seed, t, rates, take) if plan is not None else None
+    if pos is not None:  # the planned draws, numbered now in admission order
+        kids = neat.number_deferred([plan.children[int(i)] for i in pos], pool.innovations)
+    else:
+        kids = neat.mutate_batch([pool.genome(par) for par in take], rates,
+                                 [stream_key(master_seed, t, "mutate", par) for par in take], pool.innovations)
     if hasattr(pool, "admit_batch"):
         children = pool.admit_batch(kids, [(pool.lineage(par),) for par in take], birth_step=t)
         slot_map[np.asarray(take[:len(children)], np.int64)] = children
@@ -163,41 +212,59 @@ def admit_children(pool, counts, master_seed: int, t: int, rates=None):
                 break
             slot_map[par] = slot
             children.append(slot)
+    if plan is not None:
+        plan.admitted = pos[:len(children)] if pos is not None else None
     return slot_map, parents, list(children)
 
 
-def express_on(dev, pool, slots) -> None:
+def express_on(dev, pool, slots, programs=None) -> None:
     """Device tables of newly admitted slots whose parameters are
     DeviceExpressed (one batched evo_express_cppn per (tau, w_max)), binding
-    them to ``dev``."""
+    them to ``dev``.  ``programs``: the compiled programs of exactly
+    ``slots``' genomes, in order (used when they form one batch)."""
     by_expr = {}
     for s in slots:
         prm = pool.params(s)
         if isinstance(prm, DeviceExpressed):
             by_expr.setdefault((prm.tau, prm.w_max), []).append((s, prm))
+    whole = len(by_expr) == 1 and len(next(iter(by_expr.values()))) == len(slots)
     for (tau, w_max), items in by_expr.items():
-        dev.express_cppn([s for s, _ in items], [prm.genome for _, prm in items], tau, w_max)
+        dev.express_cppn([s for s, _ in items], [prm.genome for _, prm in items], tau, w_max,
+                         programs=programs if whole else None)
         for s, prm in items:
             prm.bind(dev, s)
 
 
+def _plan_programs(plan):
+    if plan is None or plan.admitted is None or plan.programs is None:
+        return None
+    return neat.subset_programs(plan.programs, plan.admitted)
+
+
 def field_radiation(state, t: int, p: float = 0.01, rates: neat.EvolutionRates | None = None,
-                    purpose: str = "field_radiation") -> dict:
+                    purpose: str = "field_radiation", wait=None) -> dict:
     """One config-3 radiation event on the state's device front (call between
-    steps).  Returns {"selected", "parents", "children"}."""
+    steps).  The host draws are planned first (``plan_field_radiation``), so
+    they overlap a step still running on the device; ``wait`` (optional) is
+    called after planning, before anything reads the device - e.g. the
+    synchronisation of a caller's own stream.  Returns {"selected",
+    "parents", "children"}."""
     from .engine import _binding, _fold_census
 
     b = _binding(state)
     dev = b.dev
     pool = state.pool
+    plan = plan_field_radiation(pool, state.master_seed, t, rates) if hasattr(pool, "slot_states") else None
+    if wait is not None:
+        wait()
     _fold_census(state)  # admission must see the device's deaths (slot states, peaks)
     counts, n_sel = dev.select_cells(stream_key(state.master_seed, t, purpose), p)
     synced = getattr(pool, "version", None) is not None and b.pool_version == pool.version
-    slot_map, parents, children = admit_children(pool, counts, state.master_seed, t, rates)
+    slot_map, parents, children = admit_children(pool, counts, state.master_seed, t, rates, plan)
     if synced and all(isinstance(pool.params(s), DeviceExpressed) for s in children):
         # only the children changed: express exactly those (one batched
         # evo_express_cppn) instead of sync_params' scan of every slot
-        express_on(dev, pool, children)
+        express_on(dev, pool, children, _plan_programs(plan))
         for s in children:
             b.param_ids[s] = pool.params(s)
         from .engine import _peaks, _slot_states

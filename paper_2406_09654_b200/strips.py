@@ -234,20 +234,24 @@ class DeviceStrip:
 
 
     def field_radiation(self, pool, master_seed: int, t: int, p: float = 0.01, rates=None,
-                        purpose: str = "field_radiation") -> dict:
+                        purpose: str = "field_radiation", wait=None) -> dict:
         """Config-3 field radiation over row strips (every rank calls it with
         an identical pool): the strip's occupied cells draw after those of
         the strips above it (an exclusive scan of the per-rank occupancy), so
         the union of the ranks' selections is the one-context selection; the
         per-slot parent counts are summed over the ranks, every rank admits
-        the same children (deterministic host NEAT), expresses them on its
+        the same children (deterministic host NEAT, planned before ``wait``
+        is called and anything reads the device), expresses them on its
         own device and moves its own selected cells.  The caller folds the
         device census into ``pool`` first where deaths matter."""
         import torch
 
         from .neat import stream_key
-        from .radiation import admit_children, express_on
+        from .radiation import _plan_programs, admit_children, express_on, plan_field_radiation
 
+        plan = plan_field_radiation(pool, master_seed, t, rates)  # host draws first: the step may still run
+        if wait is not None:
+            wait()
         world = self.plan.world
         occ = torch.zeros(world, dtype=torch.int64, device="cuda")
         occ[self.rank] = self.dev.count_occupied()
@@ -257,8 +261,8 @@ class DeviceStrip:
         tot = torch.from_numpy(counts.astype(np.int64)).cuda()
         self.comm.sum_(tot)
         counts = tot.cpu().numpy().astype(np.int32)
-        slot_map, parents, children = admit_children(pool, counts, master_seed, t, rates)
-        express_on(self.dev, pool, children)
+        slot_map, parents, children = admit_children(pool, counts, master_seed, t, rates, plan)
+        express_on(self.dev, pool, children, _plan_programs(plan))
         self.dev.set_slots(np.asarray(pool.slot_states(), np.int8))
         self.dev.remap_selected(slot_map)
         return {"selected": int(counts.sum()), "parents": len(parents), "children": len(children)}

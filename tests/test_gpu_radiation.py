@@ -59,17 +59,18 @@ def test_select_matches_host_stream(p, shape):
     dev.close()
 
 
-def test_field_radiation_vs_host_neat():
+@pytest.mark.parametrize("p", [0.02, 0.002])  # 0.002: some live slots get no child (the plan's subset path)
+def test_field_radiation_vs_host_neat(p):
     st = engine.baseline_state("c3", width=96, height=80, genomes=12)
     engine.run(st, 3)
     t = st.substrate.step_counter
     gi0 = st.substrate.front.genome_index.ravel().copy()
     pool_copy = copy.deepcopy(st.pool)
     pool_copy.net_factory = None
-    info = radiation.field_radiation(st, t, 0.02)
+    info = radiation.field_radiation(st, t, p)
     # host restatement of the same event
     occ = np.flatnonzero(gi0 >= 0)
-    sel = occ[neat.stream(st.master_seed, t, "field_radiation").random(len(occ)) < 0.02]
+    sel = occ[neat.stream(st.master_seed, t, "field_radiation").random(len(occ)) < p]
     parents = np.unique(gi0[sel])
     exp_gi = gi0.copy()
     children = {}

@@ -72,3 +72,27 @@ def test_native_normal_draws_match_numpy():
             rng.random()
             want.append(0.0 + rng.normal(0.0, 0.7))
         assert [c.weight for c in kids[i].connections] == want
+
+
+def test_deferred_numbering_equals_mutate_batch_on_subsets():
+    """A radiation event's host draws are made for every live slot before
+    the selection is known (evo_neat_mutate_deferred) and numbered for the
+    admitted ones afterwards: equal to mutate_batch over those parents
+    alone, children and compiled programs alike."""
+    wild = neat.EvolutionRates(add_connection_prob=0.5, add_node_prob=0.4, toggle_enable_prob=0.1)
+    parents, ctr = _lineage(20, 3, wild)
+    keys = [neat.stream_key(9, 150, "mutate", i) for i in range(len(parents))]
+    deferred = neat.mutate_batch_deferred(parents, wild, keys)
+    progs = neat.compile_programs(deferred)
+    rng = np.random.default_rng(5)
+    for take in (np.arange(len(parents)), np.sort(rng.choice(len(parents), 37, replace=False)), np.array([3]),
+                 np.array([], np.int64)):
+        c_ref = neat.InnovationCounter(ctr.next_innovation, ctr.next_node_id)
+        c_def = neat.InnovationCounter(ctr.next_innovation, ctr.next_node_id)
+        want = neat.mutate_batch([parents[i] for i in take], wild, [keys[i] for i in take], c_ref)
+        got = neat.number_deferred([deferred[i] for i in take], c_def)
+        assert (c_def.next_innovation, c_def.next_node_id) == (c_ref.next_innovation, c_ref.next_node_id)
+        assert len(got) == len(want) and all(a == b for a, b in zip(got, want))
+        if len(take):
+            for a, b in zip(neat.subset_programs(progs, take), neat.compile_programs(want)):
+                assert a.dtype == b.dtype and np.array_equal(a, b)

@@ -14,6 +14,7 @@ with p_radiation 0.02 / p_merge 0.2 (tests/golden/make_golden_radiation.py).
   equals those verified components driven by hand with the device's own
   actions, bit for bit; its actions on the reference's state within 1e-5."""
 
+import copy
 import json
 import os
 
@@ -302,3 +303,35 @@ def test_device_resident_run_with_radiation_equals_step(case):
     assert np.array_equal(a.pool.slot_states(), b.pool.slot_states())
     assert np.array_equal(_records(a.pool), _records(b.pool))
     assert a.pool.next_lineage_id > 64  # children were admitted
+
+
+def test_field_radiation_plan_covers_only_what_it_drew():
+    """FieldRadiationPlan is used only for the step, seed and rates it was
+    drawn for and for slots still holding the genome it mutated."""
+    pool = SlotPool(16)
+    gens, ctr = __import__("paper_2406_09654_b200.synth", fromlist=["x"]).synth_genomes(6, 2)
+    pool.innovations = ctr
+    for g in gens:
+        pool.admit(g, parents=(), birth_step=0)
+    plan = radiation.plan_field_radiation(pool, 11, 50)
+    live = [int(s) for s in pool.live_slots()]
+    assert list(plan.slots) == live and len(plan.children) == len(live)
+    assert np.array_equal(plan.positions(pool, 11, 50, None, live[1:4]), [1, 2, 3])
+    assert plan.positions(pool, 11, 100, None, live[:2]) is None          # another event
+    assert plan.positions(pool, 12, 50, None, live[:2]) is None           # another seed
+    assert plan.positions(pool, 11, 50, neat.EvolutionRates(add_node_prob=1.0), live[:2]) is None
+    assert plan.positions(pool, 11, 50, None, [15]) is None               # not live when planned
+    pool.set_genome(live[1], gens[0])
+    assert plan.positions(pool, 11, 50, None, live[:2]) is None           # slot holds another genome now
+    # admission through the plan == the unplanned path
+    counts = np.zeros(16, np.int32)
+    counts[[live[0], live[2], live[5]]] = 3
+    a, b = copy.deepcopy(pool), copy.deepcopy(pool)
+    plan_a = radiation.plan_field_radiation(a, 11, 50)
+    ra = radiation.admit_children(a, counts, 11, 50, None, plan_a)
+    rb = radiation.admit_children(b, counts, 11, 50, None)
+    assert plan_a.admitted is not None and len(plan_a.admitted) == 3
+    assert np.array_equal(ra[0], rb[0]) and ra[2] == rb[2]
+    assert all(a.genome(s) == b.genome(s) for s in ra[2])
+    assert (a.innovations.next_innovation, a.innovations.next_node_id) == \
+        (b.innovations.next_innovation, b.innovations.next_node_id)

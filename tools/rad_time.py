@@ -28,6 +28,8 @@ def timed(name, fn):
 
 
 neat.mutate_batch = timed("mutate_batch", neat.mutate_batch)
+neat.mutate_batch_deferred = timed("plan_mutate", neat.mutate_batch_deferred)
+neat.number_deferred = timed("number", neat.number_deferred)
 dev.select_cells = timed("select_cells", dev.select_cells)
 dev.remap_selected = timed("remap", dev.remap_selected)
 dev.express_cppn = timed("express_cppn", dev.express_cppn)
