@@ -185,7 +185,8 @@ def run_ours(args, rank, world, local):
             if e2 is not None:
                 e2.record(stream)
             return
-        dev.pass1(sc, t, stream=sh)
+        # evo_step's two launches groups, split by an event (F_FUSE_MID: what evo_step passes to its pass 1)
+        dev.pass1(sc, t, flags=_lib.F_FUSE_MID, stream=sh)
         if e1 is not None:
             e1.record(stream)
         dev.pass2(t, stream=sh)
@@ -295,10 +296,13 @@ def run_ours(args, rank, world, local):
                    "k_hid_net tcgen05 3xTF32 MLP, k_physics_rows)")
         launches_per_step = 8
     elif cap > 68:
-        p1_name = ("pass-1 pipeline, gather path (8 launches: k_gs_count sense texture + slot ranks, "
+        p1_name = ("pass-1 pipeline, gather path (7 launches: k_gs_count_tma sense texture + slot ranks, "
+                   "k_gs_colscan, k_gs_scan_band, k_gs_scan_bands, k_gs_scatter, k_gs_tilemap, "
+                   "k_direct_gather FFMA2 net + physics)" if not strips else
+                   "pass-1 pipeline, gather path (8 launches: k_gs_count sense texture + slot ranks, "
                    "k_gs_colscan, k_gs_scan_band, k_gs_scan_bands, k_gs_scatter, k_gs_tilemap, "
                    "k_direct_gather FFMA2 net, k_physics_rows)")
-        launches_per_step = 9
+        launches_per_step = 9 if strips else 8
     else:
         p1_name = "k_pass1_direct (pass 1: sense+net+physics)"
         launches_per_step = 2

@@ -26,6 +26,8 @@ F_ROWS_NET = 512  # large direct pools: genome-sorted sensor rows through HBM (t
 F_GATHER_NET = 1024  # the gather path for direct pools <= 68 slots and for tensor-core hidden nets (A/B)
 F_TC_DIRECT = 2048  # gather path: direct net on tcgen05 (3xTF32, A in TMEM) instead of FFMA2 warps
 F_L2_CUDA_CORE = 4096  # tensor-core hidden net: layer 2 on the CUDA cores (round-2 kernel; A/B)
+F_UNFUSED = 8192  # gather path in evo_step: physics as its own kernel over the mid planes (round-2d; A/B)
+F_FUSE_MID = 16384  # evo_pass1 when evo_pass2 follows at once: pass-1 outputs may stay records (evo_step sets it)
 
 
 class EvoScalars(C.Structure):

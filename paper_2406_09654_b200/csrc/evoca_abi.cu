@@ -87,6 +87,7 @@ struct evo_ctx {
   // built with the gather buffers, 0 = not available -> the LSU kernel)
   evo::GatherMaps* gmaps = nullptr;  // [2], 64-byte aligned host memory
   bool have_gmaps = false;
+  const float* mid_rec = nullptr;  // pass-1 records of a fused evo_step (consumed by its pass 2), else null
   int num_sms = 0;
   // rows / flags evo_get_actions reads (act_out, or hid.act after a tensor-core step)
   const float* exp_rows = nullptr;
@@ -404,6 +405,7 @@ int pass1_view(evo_ctx* c, const View& v, const evo_scalars* s, int phases, int 
   if (!s) return fail(EVO_EINVAL, "null scalars");
   const bool inject = flags & EVO_F_INJECT_ACTIONS;
   bool exp = (flags & EVO_F_EXPORT_ACTIONS) && !inject;
+  c->mid_rec = nullptr;
   if (inject && !c->act_in) return fail(EVO_EINVAL, "EVO_F_INJECT_ACTIONS without evo_set_actions");
   if ((inject || exp) && v.off != 0) return fail(EVO_EINVAL, "action injection/export needs a whole-strip pass");
   // wide hidden layers run on the tensor cores (sense -> genome buckets ->
@@ -462,6 +464,23 @@ int pass1_view(evo_ctx* c, const View& v, const evo_scalars* s, int phases, int 
     // TMA texture build for whole-strip steps (band views of evo_step_host
     // shift the planes: the LSU kernel)
     const evo::GatherMaps* maps = (c->have_gmaps && v.off == 0) ? &c->gmaps[c->front] : nullptr;
+    // evo_step / evo_run on a whole torus (or evo_pass1 with
+    // EVO_F_FUSE_MID): the physics runs in the net's epilogue and pass 2
+    // reads 32-byte pass-1 records (no k_physics_rows, no mid planes); a bare
+    // evo_pass1 keeps the mid planes it documents
+    if ((flags & EVO_F_FUSE_MID) && !(flags & EVO_F_UNFUSED) && maps && v.g.own_ghosts && !exp &&
+        variant == evo::kGatherFfma2) {
+      evo::FusedPhysics fp;
+      fp.s = to_scalars(*s);
+      fp.phases = phases;
+      fp.src_map = c->have_src_map ? c->src_map : nullptr;
+      fp.stats = stats;
+      CK(evo::launch_direct_gather(c->gat, v.g, v.front, c->params(), c->cap, c->num_sms, variant, false, c->hid.act,
+                                   c->hid.rank, st, maps, &fp));
+      c->mid_rec = c->hid.act;
+      c->have_export = false;
+      return 0;
+    }
     CK(evo::launch_direct_gather(c->gat, v.g, v.front, c->params(), c->cap, c->num_sms, variant, exp, c->hid.act,
                                  c->hid.rank, st, maps));
   }
@@ -534,6 +553,7 @@ int pass2_view(evo_ctx* c, const View& v, int64_t t, int flags, int run_census, 
   a.back = v.back;
   a.rot_front = v.front.rot;
   a.mid = v.mid;
+  a.mid_rec = v.off == 0 ? c->mid_rec : nullptr;
   a.census = c->census;
   a.ev.src = rec ? c->ev_src + v.off : nullptr;
   a.ev.q = rec ? c->ev_q + v.off : nullptr;
@@ -768,7 +788,9 @@ EVO_API int evo_swap(evo_ctx* c) {
 
 EVO_API int evo_step(evo_ctx* c, const evo_scalars* s, int64_t t, int phases, int flags, void* stream) {
   if (c && c->strip) return fail(EVO_EINVAL, "strip contexts step through evo_pass1/evo_pass2 with a halo exchange");
-  if (int r = evo_pass1(c, s, t, phases, flags, stream)) return r;
+  if (int r = check_ctx(c)) return r;
+  if (int r = pass1_view(c, full_view(c), s, phases, flags | EVO_F_FUSE_MID, c->census.stats, pick(c, stream)))
+    return r;
   if (int r = evo_pass2(c, t, flags, stream)) return r;
   return evo_swap(c);
 }

@@ -62,6 +62,14 @@ __device__ __forceinline__ void st_rec(float* p, float e, float i, float c0, flo
                "f"(c2), "f"(0.0f));
 }
 
+// Pass-1 record of the fused step (FusedPhysics, evoca_internal.h):
+// {E', C0', C1', C2' | I', q, genome, proposal byte}, one sector at the cell index.
+__device__ __forceinline__ void st_mid(float* p, const CellOut& o) {
+  asm volatile("st.global.v8.f32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "f"(o.e), "f"(o.c0), "f"(o.c1),
+               "f"(o.c2), "f"(o.inf), "f"(o.q), "f"(__int_as_float(o.slot)), "f"(__int_as_float((int)o.rp))
+               : "memory");
+}
+
 // Texture records of the CTA's rows (plus ghost row -1 / H on the first /
 // last CTA) and the band histogram by (slot, rotation).  Slots outside
 // [0, cap) are left out (no out-of-bounds shared-memory write); the step's
@@ -190,7 +198,8 @@ __device__ __forceinline__ void tma_store_3d(const CUtensorMap* m, const void* s
 
 __global__ void __launch_bounds__(kTmThreads) k_gs_count_tma(const StepGeom g, const __grid_constant__ GatherMaps maps,
                                                             const GsPlan p, int cap, int32_t* cta_hist,
-                                                            uint16_t* lrank, int32_t* rank) {
+                                                            uint16_t* lrank, int32_t* rank,
+                                                            const FusedPhysics fp, float* mid_rec) {
   extern __shared__ __align__(128) unsigned char dsm[];
   TmStage* stg = reinterpret_cast<TmStage*>(dsm);  // 2 stages
   int* hist = reinterpret_cast<int*>(dsm + 2 * sizeof(TmStage));
@@ -250,6 +259,10 @@ __global__ void __launch_bounds__(kTmThreads) k_gs_count_tma(const StepGeom g, c
       const bool occ = (unsigned)sl < (unsigned)cap;
       if (occ) lrank[i] = (uint16_t)atomicAdd(&hist[gs_bin(p, sl, 0)], 1);
       if (rank) rank[i] = occ ? (int)i : -1;
+      if (mid_rec && !occ) {  // fused step: the net never sees an unoccupied cell, its physics runs here
+        const CellState cs{s.pl[0][tid], s.pl[1][tid], s.pl[2][tid], s.pl[3][tid], s.pl[4][tid], -1, 0};
+        st_mid(mid_rec + i * 8, cell_physics(fp.s, fp.phases, fp.src_map, i, cs, CellAct{}));
+      }
     }
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     __syncthreads();
@@ -470,7 +483,9 @@ struct GatherArgs {
   int32_t* n_ht;  // [0] half-tiles, [1] work counter (chunks handed out)
   float* act;
   int export_rows;  // 0: 8-float decided records, 1: 16-float actuator rows (cell index)
+  FusedPhysics fp;  // kGwFused: the physics runs in the epilogue, act receives the pass-1 records
 };
+constexpr int kGwDecided = 0, kGwExport = 1, kGwFused = 2;  // k_direct_gather output forms
 
 // C cells per lane (a warp takes a tile of 32 C cells of one slot); D Moore
 // records per cell in flight.  C = 2, D = 3: 16 warps per SM (four resident
@@ -478,8 +493,13 @@ struct GatherArgs {
 // SM, 168 registers) took 1.54 ms against 1.05 ms on config 3 - fewer,
 // larger tiles in flight spread over more of the band and the DRAM reads of
 // the texture doubled.
-template <int C, int D, bool EXPORT>
+template <int C, int D, int MODE>
 __global__ void __launch_bounds__(kGwThreads, C == 2 ? 4 : 3) k_direct_gather(const GatherArgs a) {
+  constexpr bool EXPORT = MODE == kGwExport;
+  if (MODE == kGwFused && blockIdx.x == 0 && threadIdx.x == 0 && a.fp.stats) {
+    a.fp.stats[0] = 0;
+    a.fp.stats[1] = 0;
+  }
   __shared__ __align__(16) float wsm[kGwWarps][kGwW];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   float* W12 = wsm[warp];
@@ -544,8 +564,11 @@ __global__ void __launch_bounds__(kGwThreads, C == 2 ? 4 : 3) k_direct_gather(co
     }
     u64 acc[C][6];
     float acc12[C];
+    float ce[C], ci[C];  // fused: the cell's own E and I (Moore slot 0), kept for the physics
 #pragma unroll
     for (int c = 0; c < C; ++c) {
+      ce[c] = q[c][0].v[0];
+      ci[c] = q[c][0].v[1];
       acc12[c] = 0.0f;
 #pragma unroll
       for (int p = 0; p < 6; ++p) acc[c][p] = 0ull;
@@ -598,7 +621,28 @@ __global__ void __launch_bounds__(kGwThreads, C == 2 ? 4 : 3) k_direct_gather(co
       }
       z[12] = __fadd_rn(acc12[c], Bs[12]);
       const int cell = cc[c].cell;
-      if (!EXPORT) {  // 32 bytes at the cell index (explore_pick is exact)
+      if (MODE == kGwFused) {
+        CellAct ac{};
+        ac.acted = true;
+        ac.inv = squash(z[0]);
+        ac.liq = squash(z[1]);
+        ac.m0 = squash(z[2]);
+        ac.m1 = squash(z[3]);
+        ac.m2 = squash(z[4]);
+        explore_pick(z + 5, ac.kstar, ac.xmax);
+        // the communication channels only matter when the phase is off or
+        // the cell starves (rare): then the cell's record is read again
+        const CellState cs{ce[c], ci[c], 0.0f, 0.0f, 0.0f, slot, cc[c].rot};
+        CellOut o = cell_physics(a.fp.s, a.fp.phases, a.fp.src_map, cell, cs, ac);
+        if (!(a.fp.phases & EVO_PH_COMM) || o.slot < 0) {  // write_communication of cell_physics on the real channels
+          const f8r own = ld_rec(rec_ptr(a.tex, cc[c], W, cc[c].rot, 0));
+          const bool decay = (a.fp.phases & EVO_PH_COMM) != 0;  // here: the cell starved (physics.py:245-247)
+          o.c0 = decay ? __fmul_rn(own.v[2], 0.9f) : own.v[2];
+          o.c1 = decay ? __fmul_rn(own.v[3], 0.9f) : own.v[3];
+          o.c2 = decay ? __fmul_rn(own.v[4], 0.9f) : own.v[4];
+        }
+        st_mid(a.act + (size_t)cell * 8, o);
+      } else if (!EXPORT) {  // 32 bytes at the cell index (explore_pick is exact)
         int ks;
         float xm;
         explore_pick(z + 5, ks, xm);
@@ -951,13 +995,16 @@ GatherSizes gather_sizes(int W, int H, int cap, int num_sms) {
 }
 
 cudaError_t launch_gather_sort(const GatherBuffers& b, const StepGeom& g, const Planes& front, int cap, int num_sms,
-                               int tile, bool one_band, int32_t* rank, cudaStream_t st, const GatherMaps* maps) {
+                               int tile, bool one_band, int32_t* rank, cudaStream_t st, const GatherMaps* maps,
+                               const FusedPhysics* fused, float* mid_rec) {
+  if (fused && !maps) return cudaErrorInvalidValue;  // the fused step's unoccupied cells go through the TMA build
   const GsPlan p = make_plan(g.W, g.H, cap, num_sms, tile, one_band ? (long long)g.W * g.H : kGsBandCells);
   if (maps) {
     const size_t smem = 2 * sizeof(TmStage) + (size_t)p.bins * 4;
     cudaError_t e = cudaFuncSetAttribute(k_gs_count_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    k_gs_count_tma<<<p.nctas, kTmThreads, smem, st>>>(g, *maps, p, cap, b.cta_hist, b.lrank, rank);
+    k_gs_count_tma<<<p.nctas, kTmThreads, smem, st>>>(g, *maps, p, cap, b.cta_hist, b.lrank, rank,
+                                                     fused ? *fused : FusedPhysics{}, fused ? mid_rec : nullptr);
   } else {
     const size_t hsmem = (size_t)p.bins * 4;
     if (hsmem > 48 * 1024) {
@@ -977,10 +1024,11 @@ cudaError_t launch_gather_sort(const GatherBuffers& b, const StepGeom& g, const 
 
 cudaError_t launch_direct_gather(const GatherBuffers& b, const StepGeom& g, const Planes& front, const Params& net,
                                  int cap, int num_sms, int variant, bool export_rows, float* act, int32_t* rank,
-                                 cudaStream_t st, const GatherMaps* maps) {
+                                 cudaStream_t st, const GatherMaps* maps, const FusedPhysics* fused) {
   const bool tc = variant == kGatherTc;
-  cudaError_t e =
-      launch_gather_sort(b, g, front, cap, num_sms, tc ? 128 : 64, false, export_rows ? rank : nullptr, st, maps);
+  if (fused && (tc || export_rows)) return cudaErrorInvalidValue;
+  cudaError_t e = launch_gather_sort(b, g, front, cap, num_sms, tc ? 128 : 64, false, export_rows ? rank : nullptr,
+                                     st, maps, fused, act);
   if (e != cudaSuccess) return e;
   GatherArgs a;
   a.net = net;
@@ -991,12 +1039,15 @@ cudaError_t launch_direct_gather(const GatherBuffers& b, const StepGeom& g, cons
   a.n_ht = b.n_ht;
   a.act = act;
   a.export_rows = export_rows ? 1 : 0;
-  if (tc)
+  a.fp = fused ? *fused : FusedPhysics{};
+  if (fused)
+    k_direct_gather<2, 3, kGwFused><<<num_sms * 4, kGwThreads, 0, st>>>(a);
+  else if (tc)
     k_direct_tc<<<num_sms * 4, kTcThreads, 0, st>>>(a);  // 4 CTAs per SM, 128 TMEM columns each
   else if (export_rows)
-    k_direct_gather<2, 3, true><<<num_sms * 4, kGwThreads, 0, st>>>(a);
+    k_direct_gather<2, 3, kGwExport><<<num_sms * 4, kGwThreads, 0, st>>>(a);
   else
-    k_direct_gather<2, 3, false><<<num_sms * 4, kGwThreads, 0, st>>>(a);  // 16 warps per SM, one wave
+    k_direct_gather<2, 3, kGwDecided><<<num_sms * 4, kGwThreads, 0, st>>>(a);  // 16 warps per SM, one wave
   return cudaGetLastError();
 }
 

@@ -121,6 +121,8 @@ struct Pass2Args {
   Planes back;  // writes I, gi, rot
   const uint8_t* rot_front;  // pre-step rotation (pass 1 does not change it)
   Mid mid;
+  const float* mid_rec;  // non-null: pass-1 outputs as 32-byte records at the cell index instead of the mid
+                         // planes (FusedPhysics below); pass 2 then also writes the back E and C planes
   Census census;
   Events ev;     // ev.src == nullptr -> not recorded
   int capacity;
@@ -157,6 +159,17 @@ struct HidBuffers {
   int32_t* rank;     // [ncell] sorted row of each cell, -1 = empty
 };
 // Direct nets of large pools by gather (evoca_gather.cu): per-step buffers.
+// Physics fused into the gather net (whole-torus evo_step, TMA texture
+// build): the net's epilogue runs cell_physics on the cell's own texture
+// record and writes one 32-byte pass-1 record {E', C0', C1', C2' | I', q,
+// genome, proposal byte} at the cell index (unoccupied cells: the texture
+// build writes theirs), which pass 2 consumes instead of the mid planes.
+struct FusedPhysics {
+  Scalars s;
+  int phases;
+  const float* src_map;  // nullable, (H,W)
+  long long* stats;      // zeroed like pass 1 does
+};
 constexpr int kGatherMaxCap = 8192;  // per-CTA slot histogram in shared memory (32 KB)
 struct GatherBuffers {
   float* tex;          // [(H + 2) * W][8] sense records {E, I, C0, C1, C2, 0, 0, 0}
@@ -191,7 +204,8 @@ constexpr int kGatherFfma2 = 0, kGatherTc = 2;  // net variants of the gather pa
 // occupied cells, -1 otherwise
 cudaError_t launch_gather_sort(const GatherBuffers& b, const StepGeom& g, const Planes& front, int cap, int num_sms,
                                int tile, bool one_band, int32_t* rank, cudaStream_t st,
-                               const GatherMaps* maps = nullptr);
+                               const GatherMaps* maps = nullptr, const FusedPhysics* fused = nullptr,
+                               float* mid_rec = nullptr);
 // hidden-layer net (k_hid_net2) over the gather sort: rows at the cell index
 cudaError_t launch_hidden_gather(const GatherBuffers& b, const StepGeom& g, const Params& net, int cap, int num_sms,
                                  const unsigned char* htab, float* act, cudaStream_t st);
@@ -200,7 +214,8 @@ cudaError_t launch_hidden_tables(const Params& net, int cap, unsigned char* out,
 bool hidden_gather_supported(int hidden);
 cudaError_t launch_direct_gather(const GatherBuffers& b, const StepGeom& g, const Planes& front, const Params& net,
                                  int cap, int num_sms, int variant, bool export_rows, float* act, int32_t* rank,
-                                 cudaStream_t st, const GatherMaps* maps = nullptr);
+                                 cudaStream_t st, const GatherMaps* maps = nullptr,
+                                 const FusedPhysics* fused = nullptr);
 
 bool hidden_tc_supported(int hidden);
 int hidden_sort_ctas(int W, int H);

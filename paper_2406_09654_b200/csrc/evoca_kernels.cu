@@ -916,7 +916,12 @@ __device__ __forceinline__ int resolve_cell(const Pass2Args& a, const WarpTile& 
   return gnew;
 }
 
-template <bool kRecord>
+// kMidRec: pass 1 left 32-byte records {E', C0', C1', C2' | I', q, genome,
+// proposal byte} at the cell index (the fused gather step, FusedPhysics)
+// instead of the mid planes: the halo rows read the records' second halves
+// (rows wrap by index: single-strip steps only), the tile rows also copy the
+// first halves into the back E and C planes.
+template <bool kRecord, bool kMidRec>
 // 4 resident CTAs per SM (64 registers, no spills): the 4 x num_sms grid is
 // one wave; at 80 registers only 3 fitted and the last quarter of the grid ran
 // as a tail (k_resolve 22.5 -> 20.9 us on config 2, config 3 step 2.44 -> 2.40 ms)
@@ -942,7 +947,79 @@ __global__ void __launch_bounds__(kThreads2, EVO_K2_MIN_BLOCKS) k_resolve(const 
     const int x0 = (tile % tiles_x) * kWtW;
     const int y0 = (tile / tiles_x) * kWtH;
     const bool edge_tile = g.own_ghosts && (y0 == 0 || y0 + kWtH >= g.H);
-    {
+    if (kMidRec) {
+      constexpr int kRows = kWtH + 2;
+      int xa = x0 - 1 + lane;
+      xa = xa < 0 ? xa + g.W : (xa >= g.W ? xa - g.W : xa);
+      if (xa >= g.W) xa = g.W - 1;
+      // halo columns 32 and 33 of the six halo rows: one load on lanes 0..11
+      const bool extra = lane < 2 * kRows;
+      const int er = extra ? lane >> 1 : 0;
+      int xb = x0 + 31 + (lane & 1);
+      xb = xb >= g.W ? xb - g.W : xb;
+      if (xb >= g.W) xb = g.W - 1;
+      auto rec_row = [&](int r) {  // halo row r of the tile -> record row (torus wrap by index)
+        const int y = min(y0 + r - 1, g.H);
+        return y < 0 ? g.H - 1 : (y >= g.H ? 0 : y);
+      };
+      float4 hv[kRows], hx = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+#pragma unroll
+      for (int r = 0; r < kRows; ++r)
+        hv[r] = __ldg(reinterpret_cast<const float4*>(a.mid_rec + ((size_t)rec_row(r) * g.W + xa) * 8) + 1);
+      if (extra) hx = __ldg(reinterpret_cast<const float4*>(a.mid_rec + ((size_t)rec_row(er) * g.W + xb) * 8) + 1);
+      const int xi = min(x0 + lane, g.W - 1);
+      float4 fv[kWtH];
+      uint8_t vr[kWtH];
+#pragma unroll
+      for (int j = 0; j < kWtH; ++j) {
+        const int yj = min(y0 + j, g.H - 1);
+        fv[j] = __ldg(reinterpret_cast<const float4*>(a.mid_rec + ((size_t)yj * g.W + xi) * 8));
+        vr[j] = __ldg(a.rot_front + (unsigned)((yj + 1) * g.W + xi));
+      }
+      __syncwarp();
+#pragma unroll
+      for (int r = 0; r < kRows; ++r) {
+        wt.rp[r * kWtHW + lane] = (uint8_t)__float_as_int(hv[r].w);
+        wt.q[r * kWtHW + lane] = hv[r].y;
+        wt.gi[r * kWtHW + lane] = __float_as_int(hv[r].z);
+        if (r >= 1 && r <= kWtH && lane >= 1) wt.inf[(r - 1) * kWtW + lane - 1] = hv[r].x;
+      }
+      if (extra) {
+        wt.rp[er * kWtHW + 32 + (lane & 1)] = (uint8_t)__float_as_int(hx.w);
+        wt.q[er * kWtHW + 32 + (lane & 1)] = hx.y;
+        wt.gi[er * kWtHW + 32 + (lane & 1)] = __float_as_int(hx.z);
+        if (!(lane & 1) && er >= 1 && er <= kWtH) wt.inf[(er - 1) * kWtW + 31] = hx.x;
+      }
+      const unsigned pst = (unsigned)g.stride;
+#pragma unroll
+      for (int j = 0; j < kWtH; ++j) {
+        wt.rot[j * kWtW + lane] = vr[j];
+        const int y = y0 + j, x = x0 + lane;
+        if (y < g.H && x < g.W) {  // final E and C of the cell (pass 2 does not change them)
+          const unsigned o = (unsigned)((y + 1) * g.W + x);
+          a.back.E[o] = fv[j].x;
+          a.back.C[o] = fv[j].y;
+          a.back.C[pst + o] = fv[j].z;
+          a.back.C[2 * pst + o] = fv[j].w;
+          if (edge_tile && (y == 0 || y == g.H - 1)) {
+            if (y == 0) {
+              const unsigned og = (unsigned)((g.H + 1) * g.W + x);
+              a.back.E[og] = fv[j].x;
+              a.back.C[og] = fv[j].y;
+              a.back.C[pst + og] = fv[j].z;
+              a.back.C[2 * pst + og] = fv[j].w;
+            }
+            if (y == g.H - 1) {
+              a.back.E[x] = fv[j].x;
+              a.back.C[x] = fv[j].y;
+              a.back.C[pst + x] = fv[j].z;
+              a.back.C[2 * pst + x] = fv[j].w;
+            }
+          }
+        }
+      }
+      __syncwarp();
+    } else {
       // all staging loads of the warp tile issued before any shared store
       // halo column lane (x0-1+lane) of every halo row, plus halo columns 32
       // and 33 on lanes 0 and 1; ghost rows make the vertical wrap implicit
@@ -1394,17 +1471,20 @@ cudaError_t launch_pass2(const Pass2Args& a_in, cudaStream_t st) {
   const int need = (tiles + kWarps2 - 1) / kWarps2;
   if (grid > need) grid = need;
   const size_t smem = ((sizeof(WarpTile) * kWarps2 + 15) & ~(size_t)15) + (size_t)a.capacity * sizeof(int);
-  if (a.ev.src) {
-    static SmemOptIn cfg;
-    cudaError_t e = set_smem(k_resolve<true>, smem, cfg);
-    if (e != cudaSuccess) return e;
-    k_resolve<true><<<grid, kThreads2, smem, st>>>(a);
-  } else {
-    static SmemOptIn cfg;
-    cudaError_t e = set_smem(k_resolve<false>, smem, cfg);
-    if (e != cudaSuccess) return e;
-    k_resolve<false><<<grid, kThreads2, smem, st>>>(a);
+  if (a.mid_rec && !a.g.own_ghosts) return cudaErrorInvalidValue;  // records wrap by index: single-strip steps
+#define EVO_LAUNCH_K2(REC, MID)                                          \
+  {                                                                      \
+    static SmemOptIn cfg;                                                \
+    cudaError_t e = set_smem(k_resolve<REC, MID>, smem, cfg);            \
+    if (e != cudaSuccess) return e;                                      \
+    k_resolve<REC, MID><<<grid, kThreads2, smem, st>>>(a);               \
   }
+  if (a.ev.src) {
+    if (a.mid_rec) EVO_LAUNCH_K2(true, true) else EVO_LAUNCH_K2(true, false)
+  } else {
+    if (a.mid_rec) EVO_LAUNCH_K2(false, true) else EVO_LAUNCH_K2(false, false)
+  }
+#undef EVO_LAUNCH_K2
 #ifdef EVO_K2_SPLIT_CENSUS
   if (finish) {
     cudaError_t e = cudaGetLastError();

@@ -547,6 +547,59 @@ def test_genome_sorted_direct_path_matches_tile_path(genomes, shape):
     _step_vs_oracle(p0, net, phys, steps=2)
 
 
+@pytest.mark.parametrize("genomes,shape", [(300, (96, 80)), (1024, (64, 64)), (90, (1, 500)), (2048, (70, 260)),
+                                           (512, (2, 36)), (128, (131, 516))])
+@pytest.mark.parametrize("phases", [_lib.PH_ALL, _lib.PH_ENERGY | _lib.PH_INVEST | _lib.PH_EXPLORE,
+                                    _lib.PH_COMM | _lib.PH_EXPLORE])
+def test_fused_gather_step_matches_unfused(genomes, shape, phases):
+    """evo_step on the gather path runs the physics in the net's epilogue and
+    hands pass 2 one 32-byte record per cell (no k_physics_rows, no mid
+    planes; FusedPhysics in evoca_internal.h).  EVO_F_UNFUSED keeps the
+    round-2d kernels: planes, census counts, adoption events and stats are
+    bit-identical, with unoccupied cells (their records come from the texture
+    build), starving cells (communication decay re-reads the cell's record),
+    phase subsets, a 1- and a 2-row torus and widths off the 32-cell warp
+    tile and the 256-cell TMA box."""
+    h, w = shape
+    p0 = orc.synth_planes(h, w, genomes, seed=genomes + 1)
+    rng = np.random.default_rng(7)
+    p0.gi[rng.random((h, w)) < 0.3] = -1  # unoccupied cells
+    p0.I[rng.random((h, w)) < 0.2] *= np.float32(0.002)  # cells that starve below the death threshold
+    net = orc.synth_net(genomes, 0, seed=9)
+    phys = orc.Phys(cycle_period=4)
+    params = oracle_phys_to_params(phys)
+    a = make_dev(p0, genomes, net)
+    b = make_dev(p0, genomes, net)
+    for t in range(4):
+        sc = physics.step_scalars(t, params)
+        a.step_raw(sc, t, phases=phases, flags=_lib.F_RECORD_EVENTS)
+        b.step_raw(sc, t, phases=phases, flags=_lib.F_RECORD_EVENTS | _lib.F_UNFUSED)
+        assert download(a).equal(download(b)), f"t={t}"
+        for ca, cb in zip(a.read_census(), b.read_census()):
+            assert np.array_equal(ca, cb)
+        assert a.read_stats() == b.read_stats()
+        assert events_rows(a.read_events()) == events_rows(b.read_events())
+    # a step without event records, then a bare pass 1 / pass 2 pair (mid planes again)
+    sc = physics.step_scalars(4, params)
+    a.step_raw(sc, 4, phases=phases)
+    b.step_raw(sc, 4, phases=phases, flags=_lib.F_UNFUSED)
+    assert download(a).equal(download(b))
+    sc = physics.step_scalars(5, params)
+    a.pass1(sc, 5, phases=phases)
+    a.pass2(5)
+    a.swap()
+    b.step_raw(sc, 5, phases=phases)
+    assert download(a).equal(download(b))
+    sc = physics.step_scalars(6, params)  # the pair evo_step itself issues
+    a.pass1(sc, 6, phases=phases, flags=_lib.F_FUSE_MID)
+    a.pass2(6)
+    a.swap()
+    b.step_raw(sc, 6, phases=phases, flags=_lib.F_UNFUSED)
+    assert download(a).equal(download(b))
+    a.close()
+    b.close()
+
+
 @pytest.mark.parametrize("shape", [(96, 80), (70, 258), (1, 512)])
 def test_tma_texture_build_matches_lsu_build(shape, monkeypatch):
     """The gather path's texture build through TMA (k_gs_count_tma, the
