@@ -155,6 +155,15 @@ EVO_API int evo_msc(evo_ctx* ctx, int plane, int n_scales, double* squares, doub
 /* float64 totals of the front energy / infrastructure planes in numpy's
  * summation order (metrics.py:200-213 census: plane.sum(dtype=float64)). */
 EVO_API int evo_plane_sums(evo_ctx* ctx, double* energy, double* infrastructure);
+/* Per-step device timing of evo_step / evo_run (bench.py's roofline split):
+ * with profiling enabled every step records three events on its stream -
+ * start, between pass 1 and pass 2, end.  evo_profile_read waits for the
+ * recorded steps, returns the summed milliseconds of the two passes and the
+ * number of steps, and clears the record.  No reference counterpart
+ * (engine.py:233-248 times nothing); measurement only. */
+EVO_API int evo_profile(evo_ctx* ctx, int enable);
+EVO_API int evo_profile_read(evo_ctx* ctx, double* pass1_ms, double* pass2_ms, int* steps);
+
 /* k consecutive steps t0..t0+k-1 with per-step scalars s[0..k-1]. */
 EVO_API int evo_run(evo_ctx* ctx, const evo_scalars* s, int64_t t0, int k, void* stream);
 /* The two launches of a step, for halo exchange between them (multi-GPU) and

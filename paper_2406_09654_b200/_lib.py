@@ -65,6 +65,8 @@ SIGNATURES = {
     "evo_set_source_map": [_P, _P],
     "evo_step": [_P, C.POINTER(EvoScalars), _I64, _I, _I, _P],
     "evo_run": [_P, C.POINTER(EvoScalars), _I64, _I, _P],
+    "evo_profile": [_P, _I],
+    "evo_profile_read": [_P, _P, _P, _P],
     "evo_msc": [_P, _I, _I, _P, _P, _P, _P],
     "evo_plane_sums": [_P, _P, _P],
     "evo_render_rgb": [_P, C.c_double, C.c_double, _P, _P],

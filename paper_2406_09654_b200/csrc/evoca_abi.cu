@@ -88,6 +88,17 @@ struct evo_ctx {
   evo::GatherMaps* gmaps = nullptr;  // [2], 64-byte aligned host memory
   bool have_gmaps = false;
   const float* mid_rec = nullptr;  // pass-1 records of a fused evo_step (consumed by its pass 2), else null
+  // Lazy fused steps (evo_step / evo_run on the gather path): pass 2 writes
+  // E', C' and the final I into the sense texture instead of the planes, and
+  // the next such step builds no texture.  tex_state: the texture holds the
+  // FRONT buffer's E, I, C and that buffer's planes are stale (materialize()
+  // unpacks them before anything else touches them); tex_pending: pass 2 of
+  // the running evo_step wrote the texture for the buffer the swap makes front.
+  bool tex_state = false, tex_pending = false, lazy_step = false;
+  // evo_profile: per-step events (start, between the passes, end) of evo_step
+  bool profile = false;
+  std::vector<cudaEvent_t> prof_ev;
+  size_t prof_used = 0;
   int num_sms = 0;
   // rows / flags evo_get_actions reads (act_out, or hid.act after a tensor-core step)
   const float* exp_rows = nullptr;
@@ -400,6 +411,19 @@ View band_view(const evo_ctx* c, int r0, int rows) {
   return v;
 }
 
+constexpr int kLazyStep = 1 << 30;  // internal (evo_step): the swap follows at once, so pass 2 may leave E, I, C
+                                    // in the texture only
+
+// The front E, I, C planes from the texture after lazy fused steps: called by
+// every entry point that reads or writes those planes (not by evo_step itself).
+int materialize(evo_ctx* c, cudaStream_t st) {
+  if (!c->tex_state) return 0;
+  c->tex_state = false;
+  if (!c->num_sms) CK(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, c->device));
+  CK(evo::launch_tex_to_planes(c->gat.tex, c->geom(), c->buf[c->front], c->num_sms, st));
+  return 0;
+}
+
 int pass1_view(evo_ctx* c, const View& v, const evo_scalars* s, int phases, int flags, long long* stats,
                cudaStream_t st) {
   if (!s) return fail(EVO_EINVAL, "null scalars");
@@ -458,6 +482,10 @@ int pass1_view(evo_ctx* c, const View& v, const evo_scalars* s, int phases, int 
     }
     CK(evo::launch_hidden_gather(c->gat, v.g, c->params(), c->cap, c->num_sms, c->htab, c->hid.act, st));
   }
+  if (!gather_net || !(flags & kLazyStep)) {
+    if (int r = materialize(c, st)) return r;
+  }
+  c->lazy_step = false;
   if (gather_net) {  // rows (export) or decided records at the cell index; rank = identity for occupied cells
     const int variant = (flags & EVO_F_TC_DIRECT) ? evo::kGatherTc : evo::kGatherFfma2;
     if (int r = ensure_gather(c)) return r;
@@ -476,11 +504,13 @@ int pass1_view(evo_ctx* c, const View& v, const evo_scalars* s, int phases, int 
       fp.src_map = c->have_src_map ? c->src_map : nullptr;
       fp.stats = stats;
       CK(evo::launch_direct_gather(c->gat, v.g, v.front, c->params(), c->cap, c->num_sms, variant, false, c->hid.act,
-                                   c->hid.rank, st, maps, &fp));
+                                   c->hid.rank, st, maps, &fp, c->tex_state));
       c->mid_rec = c->hid.act;
+      c->lazy_step = (flags & kLazyStep) && !std::getenv("EVO_NO_LAZY");
       c->have_export = false;
       return 0;
     }
+    if (int r = materialize(c, st)) return r;  // a lazy evo_step that cannot fuse (export, tcgen05 variant, no TMA maps)
     CK(evo::launch_direct_gather(c->gat, v.g, v.front, c->params(), c->cap, c->num_sms, variant, exp, c->hid.act,
                                  c->hid.rank, st, maps));
   }
@@ -554,6 +584,14 @@ int pass2_view(evo_ctx* c, const View& v, int64_t t, int flags, int run_census, 
   a.rot_front = v.front.rot;
   a.mid = v.mid;
   a.mid_rec = v.off == 0 ? c->mid_rec : nullptr;
+  a.tex_out = (a.mid_rec && c->lazy_step) ? c->gat.tex : nullptr;
+  if (a.mid_rec && !a.tex_out && c->tex_state) {
+    // the fused pass 1 read the state from the texture, this pass 2 writes
+    // whole planes again: the front planes stay stale, the back ones are complete
+    c->tex_state = false;
+  }
+  c->tex_pending = a.tex_out != nullptr;
+  if (a.tex_out) c->tex_state = false;  // the texture now belongs to the buffer the swap makes front
   a.census = c->census;
   a.ev.src = rec ? c->ev_src + v.off : nullptr;
   a.ev.q = rec ? c->ev_q + v.off : nullptr;
@@ -586,6 +624,8 @@ EVO_API int evo_destroy(evo_ctx* c) {
   if (!c) return 0;
   cudaSetDevice(c->device);
   cudaStreamSynchronize(c->stream);
+  for (cudaEvent_t e : c->prof_ev) cudaEventDestroy(e);
+  c->prof_ev.clear();
   if (c->s_in) {
     cudaStreamSynchronize(c->s_in);
     cudaStreamSynchronize(c->s_out);
@@ -610,6 +650,7 @@ EVO_API int evo_upload_planes(evo_ctx* c, const float* E, const float* I, const 
                               const uint8_t* rot, void* stream) {
   if (int r = check_ctx(c)) return r;
   if (!E || !I || !C || !gi || !rot) return fail(EVO_EINVAL, "null plane pointer");
+  c->tex_state = false;  // every plane is overwritten
   cudaStream_t st = pick(c, stream);
   const evo::Planes& p = c->buf[c->front];
   const size_t n = (size_t)c->ncell();
@@ -628,6 +669,7 @@ EVO_API int evo_upload_planes(evo_ctx* c, const float* E, const float* I, const 
 EVO_API int evo_download_planes(evo_ctx* c, float* E, float* I, float* C, int32_t* gi, uint8_t* rot, void* stream) {
   if (int r = check_ctx(c)) return r;
   cudaStream_t st = pick(c, stream);
+  if (int r = materialize(c, st)) return r;
   const evo::Planes& p = c->buf[c->front];
   const size_t n = (size_t)c->ncell();
   const size_t W = (size_t)c->W;
@@ -766,7 +808,7 @@ EVO_API int evo_set_source_map(evo_ctx* c, const float* map) {
 EVO_API int evo_pass1(evo_ctx* c, const evo_scalars* s, int64_t t, int phases, int flags, void* stream) {
   if (int r = check_ctx(c)) return r;
   (void)t;
-  return pass1_view(c, full_view(c), s, phases, flags, c->census.stats, pick(c, stream));
+  return pass1_view(c, full_view(c), s, phases, flags & ~kLazyStep, c->census.stats, pick(c, stream));
 }
 
 EVO_API int evo_pass2(evo_ctx* c, int64_t t, int flags, void* stream) {
@@ -782,6 +824,13 @@ EVO_API int evo_census_finish(evo_ctx* c, int64_t t, void* stream) {
 
 EVO_API int evo_swap(evo_ctx* c) {
   if (!c) return fail(EVO_EINVAL, "null context");
+  if (c->tex_pending) {  // evo_step's own swap after a lazy pass 2
+    c->tex_pending = false;
+    c->front ^= 1;
+    c->tex_state = true;
+    return 0;
+  }
+  if (int r = materialize(c, c->stream)) return r;
   c->front ^= 1;
   return 0;
 }
@@ -789,9 +838,24 @@ EVO_API int evo_swap(evo_ctx* c) {
 EVO_API int evo_step(evo_ctx* c, const evo_scalars* s, int64_t t, int phases, int flags, void* stream) {
   if (c && c->strip) return fail(EVO_EINVAL, "strip contexts step through evo_pass1/evo_pass2 with a halo exchange");
   if (int r = check_ctx(c)) return r;
-  if (int r = pass1_view(c, full_view(c), s, phases, flags | EVO_F_FUSE_MID, c->census.stats, pick(c, stream)))
+  cudaStream_t st = pick(c, stream);
+  cudaEvent_t* pe = nullptr;
+  if (c->profile) {
+    if (c->prof_used + 3 > c->prof_ev.size()) {
+      const size_t old_n = c->prof_ev.size();
+      c->prof_ev.resize(old_n + 192);
+      for (size_t i = old_n; i < c->prof_ev.size(); ++i) CK(cudaEventCreate(&c->prof_ev[i]));
+    }
+    pe = &c->prof_ev[c->prof_used];
+    c->prof_used += 3;
+    CK(cudaEventRecord(pe[0], st));
+  }
+  if (int r = pass1_view(c, full_view(c), s, phases, (flags & ~kLazyStep) | EVO_F_FUSE_MID | kLazyStep,
+                         c->census.stats, st))
     return r;
-  if (int r = evo_pass2(c, t, flags, stream)) return r;
+  if (pe) CK(cudaEventRecord(pe[1], st));
+  if (int r = pass2_view(c, full_view(c), t, flags, (flags & EVO_F_NO_CENSUS) ? 0 : 1, st)) return r;
+  if (pe) CK(cudaEventRecord(pe[2], st));
   return evo_swap(c);
 }
 
@@ -804,6 +868,7 @@ EVO_API int evo_step_host(evo_ctx* c, const evo_scalars* s, int64_t t, int flags
   if (!s) return fail(EVO_EINVAL, "null scalars");
   if (!E || !I || !C || !gi || !rot || !E_out || !I_out || !C_out || !gi_out || !rot_out)
     return fail(EVO_EINVAL, "null plane pointer");
+  c->tex_state = false;  // the host planes replace the device state
   if (flags & (EVO_F_INJECT_ACTIONS | EVO_F_EXPORT_ACTIONS))
     return fail(EVO_EINVAL, "action injection/export is not available in the host-pipelined step");
   if (int r = ensure_pipe(c)) return r;
@@ -990,6 +1055,7 @@ EVO_API int evo_render_rgb(evo_ctx* c, double norm_energy, double norm_infrastru
   if (!(norm_energy != 0.0) || !(norm_infrastructure != 0.0)) return fail(EVO_EINVAL, "display norms must be non-zero");
   if (!c->rgba) CK(c->alloc(&c->rgba, (size_t)c->ncell()));
   cudaStream_t st = pick(c, stream);
+  if (int r = materialize(c, st)) return r;
   CK(evo::launch_render_rgb(c->buf[c->front], c->geom(), norm_energy, norm_infrastructure, c->rgba, st));
   CK(cudaMemcpyAsync(rgba, c->rgba, (size_t)c->ncell() * 4, cudaMemcpyDeviceToHost, st));
   if (!stream) CK(cudaStreamSynchronize(st));
@@ -1013,6 +1079,7 @@ EVO_API int evo_msc(evo_ctx* c, int plane, int n_scales, double* squares, double
   const int sd = evo::msc_side(c->W, c->H);
   if (sd < 2) return fail(EVO_EINVAL, "field side must be a power of two >= 2");
   if (int r = ensure_metrics(c)) return r;
+  if (int r = materialize(c, c->stream)) return r;
   const evo::Planes& f = c->buf[c->front];
   const float* p = plane == 0 ? f.E : (plane == 1 ? f.I : f.C + (plane - 2) * c->stride);
   double* out = c->msc_work + evo::msc_workspace_doubles(sd);
@@ -1032,6 +1099,7 @@ EVO_API int evo_plane_sums(evo_ctx* c, double* energy, double* infrastructure) {
   if (int r = check_ctx(c)) return r;
   if (c->strip) return fail(EVO_EINVAL, "evo_plane_sums needs a single-strip context");
   if (int r = ensure_metrics(c)) return r;
+  if (int r = materialize(c, c->stream)) return r;
   const int sd = evo::msc_side(c->W, c->H);
   double* res = c->msc_work + evo::msc_workspace_doubles(sd) + 64;
   double* chunks = res + 2;
@@ -1046,6 +1114,30 @@ EVO_API int evo_plane_sums(evo_ctx* c, double* energy, double* infrastructure) {
   return 0;
 }
 
+EVO_API int evo_profile(evo_ctx* c, int enable) {
+  if (int r = check_ctx(c)) return r;
+  c->profile = enable != 0;
+  c->prof_used = 0;
+  return 0;
+}
+
+EVO_API int evo_profile_read(evo_ctx* c, double* pass1_ms, double* pass2_ms, int* steps) {
+  if (int r = check_ctx(c)) return r;
+  if (!pass1_ms || !pass2_ms || !steps) return fail(EVO_EINVAL, "null argument");
+  *pass1_ms = *pass2_ms = 0.0;
+  *steps = (int)(c->prof_used / 3);
+  for (size_t i = 0; i + 2 < c->prof_used; i += 3) {
+    CK(cudaEventSynchronize(c->prof_ev[i + 2]));
+    float a = 0.0f, b = 0.0f;
+    CK(cudaEventElapsedTime(&a, c->prof_ev[i], c->prof_ev[i + 1]));
+    CK(cudaEventElapsedTime(&b, c->prof_ev[i + 1], c->prof_ev[i + 2]));
+    *pass1_ms += a;
+    *pass2_ms += b;
+  }
+  c->prof_used = 0;
+  return 0;
+}
+
 EVO_API int evo_run(evo_ctx* c, const evo_scalars* s, int64_t t0, int k, void* stream) {
   if (!s && k > 0) return fail(EVO_EINVAL, "null scalars");
   for (int i = 0; i < k; ++i)
@@ -1056,6 +1148,7 @@ EVO_API int evo_run(evo_ctx* c, const evo_scalars* s, int64_t t0, int k, void* s
 EVO_API int evo_refresh_ghosts(evo_ctx* c, void* stream) {
   if (int r = check_ctx(c)) return r;
   if (c->strip) return 0;
+  if (int r = materialize(c, pick(c, stream))) return r;
   CK(evo::launch_refresh_ghosts(c->buf[c->front], c->geom(), pick(c, stream)));
   return 0;
 }
@@ -1420,6 +1513,7 @@ EVO_API int evo_halo_row_words(evo_ctx* c, int which, int64_t* words) {
 EVO_API int evo_halo_pack(evo_ctx* c, int which, void* send, void* stream) {
   if (int r = check_ctx(c)) return r;
   if ((which != 0 && which != 1) || !send) return fail(EVO_EINVAL, "bad halo pack arguments");
+  if (int r = materialize(c, pick(c, stream))) return r;
   CK(evo::launch_halo(c->buf[c->front], c->mid, c->geom(), which, true, send, pick(c, stream)));
   return 0;
 }
@@ -1427,12 +1521,17 @@ EVO_API int evo_halo_pack(evo_ctx* c, int which, void* send, void* stream) {
 EVO_API int evo_halo_unpack(evo_ctx* c, int which, const void* recv, void* stream) {
   if (int r = check_ctx(c)) return r;
   if ((which != 0 && which != 1) || !recv) return fail(EVO_EINVAL, "bad halo unpack arguments");
+  if (int r = materialize(c, pick(c, stream))) return r;
   CK(evo::launch_halo(c->buf[c->front], c->mid, c->geom(), which, false, const_cast<void*>(recv), pick(c, stream)));
   return 0;
 }
 
 EVO_API int evo_plane_ptr(evo_ctx* c, int which, int buffer, void** ptr, int64_t* plane_stride) {
   if (!c || !ptr) return fail(EVO_EINVAL, "null argument");
+  if (which <= 2) {  // the caller may read or write E, I, C behind the library's back
+    if (int r = materialize(c, c->stream)) return r;
+    CK(cudaStreamSynchronize(c->stream));
+  }
   const evo::Planes& p = c->buf[(c->front ^ (buffer ? 1 : 0)) & 1];
   switch (which) {
     case 0: *ptr = p.E; break;

@@ -58,8 +58,8 @@ __device__ __forceinline__ int gs_bin(const GsPlan& p, int s, int r) { return s 
 __device__ __forceinline__ void st_rec(float* p, float e, float i, float c0, float c1, float c2) {
   // (no "memory" clobber: nothing in the writing kernel reads the texture,
   //  and the clobber would pin every later load behind the store)
-  asm volatile("st.global.v8.f32 [%0], {%1,%2,%3,%4,%5,%6,%6,%6};" ::"l"(p), "f"(e), "f"(i), "f"(c0), "f"(c1),
-               "f"(c2), "f"(0.0f));
+  asm volatile("st.global.v8.f32 [%0], {%1,%3,%4,%5,%2,%6,%6,%6};" ::"l"(p), "f"(e), "f"(i), "f"(c0), "f"(c1),
+               "f"(c2), "f"(0.0f));  // {E, C0, C1, C2 | I, 0, 0, 0}: tex_ch()
 }
 
 // Pass-1 record of the fused step (FusedPhysics, evoca_internal.h):
@@ -131,6 +131,53 @@ __global__ void __launch_bounds__(kGsThreads) k_gs_count(const StepGeom g, const
   __syncthreads();
   int32_t* out = cta_hist + (size_t)blockIdx.x * p.bins;
   for (int b = threadIdx.x; b < p.bins; b += blockDim.x) out[b] = hist[b];
+}
+
+// Slot ranks alone, for a fused step whose texture already holds the state
+// (written by the previous step's pass 2, FusedPhysics): the genome plane is
+// all that is read; an unoccupied cell's pass-1 record comes from its texture
+// record.  W % 4 == 0 (the fused step needs the TMA maps anyway).
+__global__ void __launch_bounds__(kGsThreads) k_gs_rank(const StepGeom g, const int32_t* gi, const GsPlan p, int cap,
+                                                         int32_t* cta_hist, uint16_t* lrank, const float* tex,
+                                                         const FusedPhysics fp, float* mid_rec) {
+  extern __shared__ int hist[];
+  for (int b = threadIdx.x; b < p.bins; b += blockDim.x) hist[b] = 0;
+  __syncthreads();
+  const int r0 = blockIdx.x * p.rows_per_cta, r1 = min(g.H, r0 + p.rows_per_cta);
+  const long long W = g.W, c0 = (long long)r0 * W, c1 = (long long)r1 * W;
+  for (long long i = c0 + 4 * threadIdx.x; i < c1; i += 4 * blockDim.x) {
+    const int4 G = __ldg(reinterpret_cast<const int4*>(gi + i + W));
+    const int sl[4] = {G.x, G.y, G.z, G.w};
+    uint16_t rk[4] = {0, 0, 0, 0};
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      if ((unsigned)sl[j] < (unsigned)cap) {
+        rk[j] = (uint16_t)atomicAdd(&hist[gs_bin(p, sl[j], 0)], 1);
+      } else {
+        const f8r r = ld_rec(tex + (size_t)(i + j + W) * 8);
+        const CellState cs{r.v[tex_ch(0)], r.v[tex_ch(1)], r.v[tex_ch(2)], r.v[tex_ch(3)], r.v[tex_ch(4)], -1, 0};
+        st_mid(mid_rec + (size_t)(i + j) * 8, cell_physics(fp.s, fp.phases, fp.src_map, i + j, cs, CellAct{}));
+      }
+    }
+    *reinterpret_cast<uint2*>(lrank + i) = make_uint2(rk[0] | ((unsigned)rk[1] << 16), rk[2] | ((unsigned)rk[3] << 16));
+  }
+  __syncthreads();
+  int32_t* out = cta_hist + (size_t)blockIdx.x * p.bins;
+  for (int b = threadIdx.x; b < p.bins; b += blockDim.x) out[b] = hist[b];
+}
+
+// Front E, I, C planes (ghost rows included) from the texture, when a lazy
+// fused step left the state there (evoca_abi.cu: materialize).
+__global__ void __launch_bounds__(256) k_tex_to_planes(const StepGeom g, const float* tex, const Planes f) {
+  const long long n = (long long)(g.H + 2) * g.W, st = g.stride;
+  for (long long o = blockIdx.x * (long long)blockDim.x + threadIdx.x; o < n; o += (long long)gridDim.x * blockDim.x) {
+    const f8r r = ld_rec(tex + (size_t)o * 8);
+    f.E[o] = r.v[tex_ch(0)];
+    f.I[o] = r.v[tex_ch(1)];
+    f.C[o] = r.v[tex_ch(2)];
+    f.C[st + o] = r.v[tex_ch(3)];
+    f.C[2 * st + o] = r.v[tex_ch(4)];
+  }
 }
 
 // per band and bin: exclusive scan of the per-CTA counts over the band's CTAs
@@ -250,8 +297,8 @@ __global__ void __launch_bounds__(kTmThreads) k_gs_count_tma(const StepGeom g, c
     const int ty = y_lo + c / per_row, x = (c % per_row) * kTmChunk + tid;
     // the record (two 16-byte halves; lanes 32 bytes apart)
     float4* rp = reinterpret_cast<float4*>(s.rec + tid * 8);
-    rp[0] = make_float4(s.pl[0][tid], s.pl[1][tid], s.pl[2][tid], s.pl[3][tid]);
-    rp[1] = make_float4(s.pl[4][tid], 0.0f, 0.0f, 0.0f);
+    rp[0] = make_float4(s.pl[0][tid], s.pl[2][tid], s.pl[3][tid], s.pl[4][tid]);  // {E, C0, C1, C2 | I, 0, 0, 0}
+    rp[1] = make_float4(s.pl[1][tid], 0.0f, 0.0f, 0.0f);
     const int y = ty - 1;  // strip row
     if (x < g.W && y >= r0 && y < r1) {
       const long long i = (long long)y * g.W + x;
@@ -567,8 +614,8 @@ __global__ void __launch_bounds__(kGwThreads, C == 2 ? 4 : 3) k_direct_gather(co
     float ce[C], ci[C];  // fused: the cell's own E and I (Moore slot 0), kept for the physics
 #pragma unroll
     for (int c = 0; c < C; ++c) {
-      ce[c] = q[c][0].v[0];
-      ci[c] = q[c][0].v[1];
+      ce[c] = q[c][0].v[tex_ch(0)];
+      ci[c] = q[c][0].v[tex_ch(1)];
       acc12[c] = 0.0f;
 #pragma unroll
       for (int p = 0; p < 6; ++p) acc[c][p] = 0ull;
@@ -593,7 +640,7 @@ __global__ void __launch_bounds__(kGwThreads, C == 2 ? 4 : 3) k_direct_gather(co
           const float w12 = W1[k];
 #pragma unroll
           for (int c = 0; c < C; ++c) {
-            const float x = q[c][j].v[ch];
+            const float x = q[c][j].v[tex_ch(ch)];
 #pragma unroll
             for (int p = 0; p < 6; ++p) ffma2(acc[c][p], x, wp[p]);
             acc12[c] = fmaf(x, w12, acc12[c]);
@@ -637,9 +684,9 @@ __global__ void __launch_bounds__(kGwThreads, C == 2 ? 4 : 3) k_direct_gather(co
         if (!(a.fp.phases & EVO_PH_COMM) || o.slot < 0) {  // write_communication of cell_physics on the real channels
           const f8r own = ld_rec(rec_ptr(a.tex, cc[c], W, cc[c].rot, 0));
           const bool decay = (a.fp.phases & EVO_PH_COMM) != 0;  // here: the cell starved (physics.py:245-247)
-          o.c0 = decay ? __fmul_rn(own.v[2], 0.9f) : own.v[2];
-          o.c1 = decay ? __fmul_rn(own.v[3], 0.9f) : own.v[3];
-          o.c2 = decay ? __fmul_rn(own.v[4], 0.9f) : own.v[4];
+          o.c0 = decay ? __fmul_rn(own.v[tex_ch(2)], 0.9f) : own.v[tex_ch(2)];
+          o.c1 = decay ? __fmul_rn(own.v[tex_ch(3)], 0.9f) : own.v[tex_ch(3)];
+          o.c2 = decay ? __fmul_rn(own.v[tex_ch(4)], 0.9f) : own.v[tex_ch(4)];
         }
         st_mid(a.act + (size_t)cell * 8, o);
       } else if (!EXPORT) {  // 32 bytes at the cell index (explore_pick is exact)
@@ -814,7 +861,7 @@ __global__ void __launch_bounds__(kTcThreads, 4) k_direct_tc(const GatherArgs a)
       for (int s = 0; s < 9; ++s)
 #pragma unroll
         for (int ch = 0; ch < 5; ++ch) {
-          const float x = q[s].v[ch];
+          const float x = q[s].v[tex_ch(ch)];
           const uint32_t hb = __float_as_uint(x) & 0xFFFFE000u;
           hv[s * 5 + ch] = hb;
           lv[s * 5 + ch] = __float_as_uint(__fsub_rn(x, __uint_as_float(hb)));
@@ -996,10 +1043,18 @@ GatherSizes gather_sizes(int W, int H, int cap, int num_sms) {
 
 cudaError_t launch_gather_sort(const GatherBuffers& b, const StepGeom& g, const Planes& front, int cap, int num_sms,
                                int tile, bool one_band, int32_t* rank, cudaStream_t st, const GatherMaps* maps,
-                               const FusedPhysics* fused, float* mid_rec) {
+                               const FusedPhysics* fused, float* mid_rec, bool tex_is_state) {
   if (fused && !maps) return cudaErrorInvalidValue;  // the fused step's unoccupied cells go through the TMA build
+  if (tex_is_state && (!fused || (g.W & 3))) return cudaErrorInvalidValue;
   const GsPlan p = make_plan(g.W, g.H, cap, num_sms, tile, one_band ? (long long)g.W * g.H : kGsBandCells);
-  if (maps) {
+  if (tex_is_state) {  // ranks only: the texture holds the state (lazy fused steps)
+    const size_t hsmem = (size_t)p.bins * 4;
+    if (hsmem > 48 * 1024) {
+      cudaError_t e = cudaFuncSetAttribute(k_gs_rank, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hsmem);
+      if (e != cudaSuccess) return e;
+    }
+    k_gs_rank<<<p.nctas, kGsThreads, hsmem, st>>>(g, front.gi, p, cap, b.cta_hist, b.lrank, b.tex, *fused, mid_rec);
+  } else if (maps) {
     const size_t smem = 2 * sizeof(TmStage) + (size_t)p.bins * 4;
     cudaError_t e = cudaFuncSetAttribute(k_gs_count_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
@@ -1024,11 +1079,12 @@ cudaError_t launch_gather_sort(const GatherBuffers& b, const StepGeom& g, const 
 
 cudaError_t launch_direct_gather(const GatherBuffers& b, const StepGeom& g, const Planes& front, const Params& net,
                                  int cap, int num_sms, int variant, bool export_rows, float* act, int32_t* rank,
-                                 cudaStream_t st, const GatherMaps* maps, const FusedPhysics* fused) {
+                                 cudaStream_t st, const GatherMaps* maps, const FusedPhysics* fused,
+                                 bool tex_is_state) {
   const bool tc = variant == kGatherTc;
   if (fused && (tc || export_rows)) return cudaErrorInvalidValue;
   cudaError_t e = launch_gather_sort(b, g, front, cap, num_sms, tc ? 128 : 64, false, export_rows ? rank : nullptr,
-                                     st, maps, fused, act);
+                                     st, maps, fused, act, tex_is_state);
   if (e != cudaSuccess) return e;
   GatherArgs a;
   a.net = net;
@@ -1048,6 +1104,12 @@ cudaError_t launch_direct_gather(const GatherBuffers& b, const StepGeom& g, cons
     k_direct_gather<2, 3, kGwExport><<<num_sms * 4, kGwThreads, 0, st>>>(a);
   else
     k_direct_gather<2, 3, kGwDecided><<<num_sms * 4, kGwThreads, 0, st>>>(a);  // 16 warps per SM, one wave
+  return cudaGetLastError();
+}
+
+cudaError_t launch_tex_to_planes(const float* tex, const StepGeom& g, const Planes& front, int num_sms,
+                                 cudaStream_t st) {
+  k_tex_to_planes<<<num_sms * 8, 256, 0, st>>>(g, tex, front);
   return cudaGetLastError();
 }
 

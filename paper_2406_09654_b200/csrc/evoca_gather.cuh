@@ -12,6 +12,11 @@ namespace gs {
 struct f8r {
   float v[8];
 };
+// Sense texture record {E, C0, C1, C2 | I, 0, 0, 0}: sensor channel ch (E, I,
+// C0, C1, C2: engine.py:164-190) sits at index tex_ch(ch).  The first half
+// equals the first half of a pass-1 record (FusedPhysics), so pass 2 of a
+// fused step can write the next step's texture from what it holds.
+__host__ __device__ constexpr int tex_ch(int ch) { return ch == 0 ? 0 : (ch == 1 ? 4 : ch - 1); }
 __device__ __forceinline__ f8r ld_rec(const float* p) {
   f8r r;
   asm volatile("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"

@@ -853,19 +853,19 @@ __global__ void __launch_bounds__(kNetThreads, 1) k_hid_net2(const NetArgs a) {
       float x0, x1, x2, x3;
       {  // aq = 0: k = kk
         const int k = kk, s = k / 5;
-        x0 = rec[s - 0].v[k % 5];
+        x0 = rec[s - 0].v[gs::tex_ch(k % 5)];
       }
       {  // aq = 1: k = 12 + kk
         const int k = 12 + kk, s = k / 5;
-        x1 = rec[s - 2].v[k % 5];
+        x1 = rec[s - 2].v[gs::tex_ch(k % 5)];
       }
       {  // aq = 2: k = 24 + kk
         const int k = 24 + kk, s = k / 5;
-        x2 = rec[s - 4].v[k % 5];
+        x2 = rec[s - 4].v[gs::tex_ch(k % 5)];
       }
       {  // aq = 3: k = 36 + kk (45 .. 47 pad)
         const int k = 36 + kk, s = k / 5;
-        x3 = k < kSensors ? rec[s - 7].v[k % 5] : 0.0f;
+        x3 = k < kSensors ? rec[s - 7].v[gs::tex_ch(k % 5)] : 0.0f;
       }
       v[kk] = aq == 0 ? x0 : aq == 1 ? x1 : aq == 2 ? x2 : x3;
     }

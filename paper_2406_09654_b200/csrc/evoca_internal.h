@@ -123,6 +123,8 @@ struct Pass2Args {
   Mid mid;
   const float* mid_rec;  // non-null: pass-1 outputs as 32-byte records at the cell index instead of the mid
                          // planes (FusedPhysics below); pass 2 then also writes the back E and C planes
+  float* tex_out;        // with mid_rec, non-null (lazy): E', C' and the final I go to the texture records
+                         // [(H + 2) * W][8] (the next step's sense texture) instead of the back E, I, C planes
   Census census;
   Events ev;     // ev.src == nullptr -> not recorded
   int capacity;
@@ -205,7 +207,7 @@ constexpr int kGatherFfma2 = 0, kGatherTc = 2;  // net variants of the gather pa
 cudaError_t launch_gather_sort(const GatherBuffers& b, const StepGeom& g, const Planes& front, int cap, int num_sms,
                                int tile, bool one_band, int32_t* rank, cudaStream_t st,
                                const GatherMaps* maps = nullptr, const FusedPhysics* fused = nullptr,
-                               float* mid_rec = nullptr);
+                               float* mid_rec = nullptr, bool tex_is_state = false);
 // hidden-layer net (k_hid_net2) over the gather sort: rows at the cell index
 cudaError_t launch_hidden_gather(const GatherBuffers& b, const StepGeom& g, const Params& net, int cap, int num_sms,
                                  const unsigned char* htab, float* act, cudaStream_t st);
@@ -215,7 +217,10 @@ bool hidden_gather_supported(int hidden);
 cudaError_t launch_direct_gather(const GatherBuffers& b, const StepGeom& g, const Planes& front, const Params& net,
                                  int cap, int num_sms, int variant, bool export_rows, float* act, int32_t* rank,
                                  cudaStream_t st, const GatherMaps* maps = nullptr,
-                                 const FusedPhysics* fused = nullptr);
+                                 const FusedPhysics* fused = nullptr, bool tex_is_state = false);
+// E, I, C planes of `front` (ghost rows included) from the texture records
+cudaError_t launch_tex_to_planes(const float* tex, const StepGeom& g, const Planes& front, int num_sms,
+                                 cudaStream_t st);
 
 bool hidden_tc_supported(int hidden);
 int hidden_sort_ctas(int W, int H);

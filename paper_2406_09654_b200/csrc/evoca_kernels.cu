@@ -792,9 +792,15 @@ __device__ __forceinline__ unsigned arrival_mask(const WarpTile& wt, int ty, int
 // Returns the cell's final genome slot.  KIND restricts the compiled paths
 // (1: at most one arrival, 2: exactly two, 3: three or more) so that a warp
 // never executes predicated-off code of the other cases.
-template <bool kRecord, int KIND>
+__device__ __forceinline__ void st_tex(float* p, const float4& f, float inf) {  // {E, C0, C1, C2 | I, 0, 0, 0}
+  asm volatile("st.global.v8.f32 [%0], {%1,%2,%3,%4,%5,%6,%6,%6};" ::"l"(p), "f"(f.x), "f"(f.y), "f"(f.z), "f"(f.w),
+               "f"(inf), "f"(0.0f)
+               : "memory");
+}
+
+template <bool kRecord, int KIND, bool kLazy = false>
 __device__ __forceinline__ int resolve_cell(const Pass2Args& a, const WarpTile& wt, int ty, int tx, int y, int x,
-                                            unsigned m, int& adopted, bool edge_tile) {
+                                            unsigned m, int& adopted, bool edge_tile, const float4* ec = nullptr) {
   const StepGeom& g = a.g;
   const int hc = (ty + 1) * kWtHW + tx + 1;
   const float before = wt.inf[ty * kWtW + tx];
@@ -897,18 +903,33 @@ __device__ __forceinline__ int resolve_cell(const Pass2Args& a, const WarpTile& 
   if (kRecord && !adopt) a.ev.src[(long long)y * g.W + x] = -1;
   adopted += adopt ? 1 : 0;
   const unsigned o = (unsigned)((y + 1) * g.W + x);
-  a.back.I[o] = acc;
+  // lazy fused steps: the final infrastructure is the second half of the
+  // next step's texture record {E, C0, C1, C2 | I, 0, 0, 0}
+  // (whole 32-byte records: half-sector stores made L2 fill the other half from DRAM)
+  float4 f4 = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+  if (kLazy) {
+    f4 = ec[ty * kWtW + tx];
+    st_tex(a.tex_out + (size_t)o * 8, f4, acc);
+  } else {
+    a.back.I[o] = acc;
+  }
   a.back.gi[o] = gnew;
   a.back.rot[o] = (uint8_t)rnew;
   if (edge_tile && (y == 0 || y == g.H - 1)) {  // warp-uniform pre-test per tile
     if (y == 0) {
       const unsigned og = (unsigned)((g.H + 1) * g.W + x);
-      a.back.I[og] = acc;
+      if (kLazy)
+        st_tex(a.tex_out + (size_t)og * 8, f4, acc);
+      else
+        a.back.I[og] = acc;
       a.back.gi[og] = gnew;
       a.back.rot[og] = (uint8_t)rnew;
     }
     if (y == g.H - 1) {
-      a.back.I[x] = acc;
+      if (kLazy)
+        st_tex(a.tex_out + (size_t)x * 8, f4, acc);
+      else
+        a.back.I[x] = acc;
       a.back.gi[x] = gnew;
       a.back.rot[x] = (uint8_t)rnew;
     }
@@ -921,7 +942,10 @@ __device__ __forceinline__ int resolve_cell(const Pass2Args& a, const WarpTile& 
 // instead of the mid planes: the halo rows read the records' second halves
 // (rows wrap by index: single-strip steps only), the tile rows also copy the
 // first halves into the back E and C planes.
-template <bool kRecord, bool kMidRec>
+// kMid 2 (lazy): the same, but E', C' and the final I go to the texture
+// records (the next step's sense texture) and the back E, I, C planes are
+// not written (evoca_abi.cu materialises them on demand).
+template <bool kRecord, int kMid>
 // 4 resident CTAs per SM (64 registers, no spills): the 4 x num_sms grid is
 // one wave; at 80 registers only 3 fitted and the last quarter of the grid ran
 // as a tail (k_resolve 22.5 -> 20.9 us on config 2, config 3 step 2.44 -> 2.40 ms)
@@ -929,9 +953,14 @@ template <bool kRecord, bool kMidRec>
 #define EVO_K2_MIN_BLOCKS 4
 #endif
 __global__ void __launch_bounds__(kThreads2, EVO_K2_MIN_BLOCKS) k_resolve(const Pass2Args a) {
+  constexpr bool kMidRec = kMid != 0, kLazy = kMid == 2;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   WarpTile* wts = reinterpret_cast<WarpTile*>(smem_raw);
   int* hist = reinterpret_cast<int*>(smem_raw + ((sizeof(WarpTile) * kWarps2 + 15) & ~(size_t)15));
+  // lazy: {E', C0', C1', C2'} of the warp's tile cells, behind the histogram
+  float4* ec = reinterpret_cast<float4*>(smem_raw + ((sizeof(WarpTile) * kWarps2 + 15) & ~(size_t)15) +
+                                         (((size_t)a.capacity * sizeof(int) + 15) & ~(size_t)15)) +
+               (threadIdx.x >> 5) * kWtCells;
   __shared__ int s_adopt;
   __shared__ bool s_last;
   const StepGeom& g = a.g;
@@ -995,7 +1024,9 @@ __global__ void __launch_bounds__(kThreads2, EVO_K2_MIN_BLOCKS) k_resolve(const 
       for (int j = 0; j < kWtH; ++j) {
         wt.rot[j * kWtW + lane] = vr[j];
         const int y = y0 + j, x = x0 + lane;
-        if (y < g.H && x < g.W) {  // final E and C of the cell (pass 2 does not change them)
+        if (kLazy) {  // first half of the next texture record, stored with the final I by resolve_cell
+          ec[j * kWtW + lane] = fv[j];
+        } else if (y < g.H && x < g.W) {  // final E and C of the cell (pass 2 does not change them)
           const unsigned o = (unsigned)((y + 1) * g.W + x);
           a.back.E[o] = fv[j].x;
           a.back.C[o] = fv[j].y;
@@ -1087,7 +1118,7 @@ __global__ void __launch_bounds__(kThreads2, EVO_K2_MIN_BLOCKS) k_resolve(const 
       if (y < g.H && x < g.W) {
         const unsigned m = arrival_mask(wt, ty, tx);
         if ((m & (m - 1)) == 0) {
-          const int gn = resolve_cell<kRecord, 1>(a, wt, ty, tx, y, x, m, my_adopt, edge_tile);
+          const int gn = resolve_cell<kRecord, 1, kLazy>(a, wt, ty, tx, y, x, m, my_adopt, edge_tile, ec);
           key = (gn >= 0 && gn < a.capacity) ? gn : -1;
         } else {
           kind = __popc(m) == 2 ? 2 : 3;
@@ -1107,16 +1138,16 @@ __global__ void __launch_bounds__(kThreads2, EVO_K2_MIN_BLOCKS) k_resolve(const 
     for (int e = lane; e < n2; e += 32) {
       const int i = wt.queue[e];
       const int ty = i / kWtW, tx = i - ty * kWtW;
-      const int gn = resolve_cell<kRecord, 2>(a, wt, ty, tx, y0 + ty, x0 + tx, arrival_mask(wt, ty, tx), my_adopt,
-                                              edge_tile);
+      const int gn = resolve_cell<kRecord, 2, kLazy>(a, wt, ty, tx, y0 + ty, x0 + tx, arrival_mask(wt, ty, tx), my_adopt,
+                                              edge_tile, ec);
       if (gn >= 0 && gn < a.capacity) atomicAdd(&hist[gn], 1);
     }
 #pragma unroll 1
     for (int e = lane; e < n3; e += 32) {
       const int i = wt.queue[kWtCells - 1 - e];
       const int ty = i / kWtW, tx = i - ty * kWtW;
-      const int gn = resolve_cell<kRecord, 3>(a, wt, ty, tx, y0 + ty, x0 + tx, arrival_mask(wt, ty, tx), my_adopt,
-                                              edge_tile);
+      const int gn = resolve_cell<kRecord, 3, kLazy>(a, wt, ty, tx, y0 + ty, x0 + tx, arrival_mask(wt, ty, tx), my_adopt,
+                                              edge_tile, ec);
       if (gn >= 0 && gn < a.capacity) atomicAdd(&hist[gn], 1);
     }
     __syncwarp();
@@ -1470,7 +1501,8 @@ cudaError_t launch_pass2(const Pass2Args& a_in, cudaStream_t st) {
   int grid = num_sms() * EVO_K2_GRID_FACTOR;
   const int need = (tiles + kWarps2 - 1) / kWarps2;
   if (grid > need) grid = need;
-  const size_t smem = ((sizeof(WarpTile) * kWarps2 + 15) & ~(size_t)15) + (size_t)a.capacity * sizeof(int);
+  size_t smem = ((sizeof(WarpTile) * kWarps2 + 15) & ~(size_t)15) + (size_t)a.capacity * sizeof(int);
+  if (a.tex_out) smem = ((smem + 15) & ~(size_t)15) + sizeof(float4) * kWtCells * kWarps2;
   if (a.mid_rec && !a.g.own_ghosts) return cudaErrorInvalidValue;  // records wrap by index: single-strip steps
 #define EVO_LAUNCH_K2(REC, MID)                                          \
   {                                                                      \
@@ -1479,10 +1511,11 @@ cudaError_t launch_pass2(const Pass2Args& a_in, cudaStream_t st) {
     if (e != cudaSuccess) return e;                                      \
     k_resolve<REC, MID><<<grid, kThreads2, smem, st>>>(a);               \
   }
+  if (a.tex_out && !a.mid_rec) return cudaErrorInvalidValue;
   if (a.ev.src) {
-    if (a.mid_rec) EVO_LAUNCH_K2(true, true) else EVO_LAUNCH_K2(true, false)
+    if (a.tex_out) EVO_LAUNCH_K2(true, 2) else if (a.mid_rec) EVO_LAUNCH_K2(true, 1) else EVO_LAUNCH_K2(true, 0)
   } else {
-    if (a.mid_rec) EVO_LAUNCH_K2(false, true) else EVO_LAUNCH_K2(false, false)
+    if (a.tex_out) EVO_LAUNCH_K2(false, 2) else if (a.mid_rec) EVO_LAUNCH_K2(false, 1) else EVO_LAUNCH_K2(false, 0)
   }
 #undef EVO_LAUNCH_K2
 #ifdef EVO_K2_SPLIT_CENSUS

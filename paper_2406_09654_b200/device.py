@@ -189,6 +189,16 @@ class DeviceSubstrate:
                 self.set_source_map(source_map)
         check(self.lib.evo_step(self.ctx, C.byref(scalars), int(t), phases, flags, _stream(stream)))
 
+    def profile(self, enable: bool = True) -> None:
+        """Per-step device timing of ``evo_step`` / ``evo_run`` (start, between the passes, end)."""
+        check(self.lib.evo_profile(self.ctx, 1 if enable else 0))
+
+    def profile_read(self):
+        """(pass-1 ms, pass-2 ms, steps) summed over the steps recorded since the last read."""
+        a, b, n = C.c_double(), C.c_double(), C.c_int()
+        check(self.lib.evo_profile_read(self.ctx, C.byref(a), C.byref(b), C.byref(n)))
+        return a.value, b.value, n.value
+
     def pass1(self, scalars, t: int, phases: int = _lib.PH_ALL, flags: int = 0, stream=None) -> None:
         check(self.lib.evo_pass1(self.ctx, C.byref(scalars), int(t), phases, flags, _stream(stream)))
 

@@ -596,6 +596,33 @@ def test_fused_gather_step_matches_unfused(genomes, shape, phases):
     a.swap()
     b.step_raw(sc, 6, phases=phases, flags=_lib.F_UNFUSED)
     assert download(a).equal(download(b))
+    # consecutive evo_steps are lazy: pass 2 leaves E', C' and the final I in
+    # the sense texture only (the next step ranks the genome plane and builds
+    # no texture) until something reads the planes; census, stats, events and
+    # genome patches do not
+    rng2 = np.random.default_rng(11)
+    for t in range(7, 12):
+        sc = physics.step_scalars(t, params)
+        a.step_raw(sc, t, phases=phases, flags=_lib.F_RECORD_EVENTS)
+        b.step_raw(sc, t, phases=phases, flags=_lib.F_RECORD_EVENTS | _lib.F_UNFUSED)
+        assert a.read_stats() == b.read_stats()
+        assert events_rows(a.read_events()) == events_rows(b.read_events())
+        if t == 9:  # a genome patch between lazy steps (field radiation's device half)
+            cells = rng2.choice(h * w, size=max(1, h * w // 50), replace=False).astype(np.int64)
+            slots = rng2.integers(0, genomes, size=len(cells)).astype(np.int32)
+            a.patch_genomes(cells, slots)
+            b.patch_genomes(cells, slots)
+        if t == 10:  # an observable straight from the lazy state
+            assert np.array_equal(a.render_rgb(), b.render_rgb())
+    for ca, cb in zip(a.read_census(), b.read_census()):
+        assert np.array_equal(ca, cb)
+    assert download(a).equal(download(b))
+    k = 4  # evo_run, then a plain download
+    scs = [physics.step_scalars(12 + i, params) for i in range(k)]
+    a.run(scs, 12)
+    for i in range(k):
+        b.step_raw(scs[i], 12 + i, flags=_lib.F_UNFUSED)
+    assert download(a).equal(download(b))
     a.close()
     b.close()
 

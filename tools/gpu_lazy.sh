@@ -1,0 +1,13 @@
+# lazy fused steps (state in the texture between evo_steps): parity, full suite, A/B timing, bench
+set -x
+timeout 900 python -m pytest tests/test_gpu_parity.py -x -q -k "fused or genome_sorted or tma_texture" > gpurun_out/l_pytest.log 2>&1; echo pytest=$?
+tail -5 gpurun_out/l_pytest.log
+timeout 1800 python -m pytest tests -m gpu -x -q > gpurun_out/l_pytest_all.log 2>&1; echo pytest_all=$?
+tail -5 gpurun_out/l_pytest_all.log
+for i in 1 2; do
+timeout 300 python tools/profile_step.py --config c3 --steps 12 --flush --time > gpurun_out/l_c3_lazy_$i.log 2>&1; tail -2 gpurun_out/l_c3_lazy_$i.log
+EVO_NO_LAZY=1 timeout 300 python tools/profile_step.py --config c3 --steps 12 --flush --time > gpurun_out/l_c3_fused_$i.log 2>&1; tail -2 gpurun_out/l_c3_fused_$i.log
+done
+timeout 900 python bench.py --steps 20 --warmup 5 --no-cpu-baseline > gpurun_out/l_bench_c3.log 2>&1; echo bench=$?
+tail -1 gpurun_out/l_bench_c3.log | cut -c1-300
+timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,smsp__inst_executed.sum --clock-control none --csv --log-file gpurun_out/l_launches_c3.csv python tools/profile_step.py --config c3 --steps 3 > gpurun_out/l_ncu.log 2>&1; echo launches=$?

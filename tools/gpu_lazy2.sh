@@ -1,0 +1,8 @@
+set -x
+timeout 900 python -m pytest tests/test_gpu_parity.py -x -q -k "fused or genome_sorted or tma_texture" > gpurun_out/l_pytest.log 2>&1; echo pytest=$?
+tail -5 gpurun_out/l_pytest.log
+for i in 1 2; do
+timeout 300 python tools/profile_step.py --config c3 --steps 12 --flush --time > gpurun_out/l_c3_lazy_$i.log 2>&1; tail -2 gpurun_out/l_c3_lazy_$i.log
+EVO_NO_LAZY=1 timeout 300 python tools/profile_step.py --config c3 --steps 12 --flush --time > gpurun_out/l_c3_fused_$i.log 2>&1; tail -2 gpurun_out/l_c3_fused_$i.log
+done
+timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,smsp__inst_executed.sum --clock-control none --csv --log-file gpurun_out/l_launches_c3.csv python tools/profile_step.py --config c3 --steps 3 > gpurun_out/l_ncu.log 2>&1; echo launches=$?
