@@ -304,9 +304,9 @@ def run_ours(args, rank, world, local):
                    "k_hid_net tcgen05 3xTF32 MLP, k_physics_rows)")
         launches_per_step = 8
     elif cap > 68:
-        p1_name = ("pass-1 pipeline, gather path (7 launches: k_gs_count_tma sense texture + slot ranks, "
-                   "k_gs_colscan, k_gs_scan_band, k_gs_scan_bands, k_gs_scatter, k_gs_tilemap, "
-                   "k_direct_gather FFMA2 net + physics)" if not strips else
+        p1_name = ("pass-1 pipeline, gather path, lazy fused evo_step (7 launches: k_gs_rank slot ranks - the "
+                   "previous pass 2 wrote the sense texture -, k_gs_colscan, k_gs_scan_band, k_gs_scan_bands, "
+                   "k_gs_scatter, k_gs_tilemap, k_direct_gather FFMA2 net + physics)" if not strips else
                    "pass-1 pipeline, gather path (8 launches: k_gs_count sense texture + slot ranks, "
                    "k_gs_colscan, k_gs_scan_band, k_gs_scan_bands, k_gs_scatter, k_gs_tilemap, "
                    "k_direct_gather FFMA2 net, k_physics_rows)")
@@ -380,7 +380,8 @@ def run_ours(args, rank, world, local):
                  "fp32_tflops": ncell * FLOP_PER_CELL_DIRECT / k1_s / 1e12 if cfg.hidden == 0 else None,
                  "fp32_peak_tflops_derived": fp32_peak},
             ] + ([] if strips else [
-                {"name": "k_resolve (pass 2: explore resolve+adoption+census)"
+                {"name": "k_resolve (pass 2: explore resolve+adoption+census"
+                 + ("; writes the next step's sense texture)" if cap > 68 and cfg.hidden == 0 else ")")
                  + (" + field radiation every %d steps" % cfg.radiation_every if radiate else ""),
                  "ms": k2_s * 1e3, "share": k2 / total_ms},
             ]),

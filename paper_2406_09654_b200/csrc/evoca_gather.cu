@@ -572,33 +572,39 @@ __global__ void __launch_bounds__(kGwThreads, C == 2 ? 4 : 3) k_direct_gather(co
     queued = claim();
     return q;
   };
-  auto cells_of = [&](const int4& t, GCell (&c)[C]) {
+  // the next tile's cells stay packed list entries until their records are
+  // asked for (decoded cells cost five registers each)
+  auto entries_of = [&](const int4& t, uint32_t (&e)[C]) {
 #pragma unroll
     for (int j = 0; j < C; ++j) {
       const int r = lane + 32 * j;
-      c[j] = gcell(__ldg(a.sorted + t.y + (r < t.z ? r : 0)), W);
+      e[j] = __ldg(a.sorted + t.y + (r < t.z ? r : 0));
     }
   };
   int cur = -1;
   int4 ti = __ldg(a.info + h);
   GCell cc[C];
-  cells_of(ti, cc);
+  uint32_t ne[C];
+  entries_of(ti, ne);
+#pragma unroll
+  for (int j = 0; j < C; ++j) cc[j] = gcell(ne[j], W);
   f8r q[C][3];  // ring of the D = 3 Moore records in flight per cell
 #pragma unroll
   for (int s = 0; s < D; ++s)
 #pragma unroll
     for (int j = 0; j < C; ++j) q[j][s] = ld_rec(rec_ptr(a.tex, cc[j], W, cc[j].rot, s));
+  // the tile info is read two tiles ahead and the cell list one tile ahead,
+  // so neither of the two dependent loads (info -> sorted entries -> record
+  // addresses) is waited for (13 % of the stall samples sat on that chain)
+  int hn = step(h);
+  int4 tn = make_int4(0, 0, 1, 0);
+  if (hn < n) tn = __ldg(a.info + hn);
   while (h < n) {
-    const int hn = step(h);
     const bool more = hn < n;
-    int4 tn = make_int4(0, 0, 1, 0);
-    GCell nc[C];
-#pragma unroll
-    for (int j = 0; j < C; ++j) nc[j] = cc[j];
-    if (more) {
-      tn = __ldg(a.info + hn);
-      cells_of(tn, nc);
-    }
+    if (more) entries_of(tn, ne);  // else: the last tile reloads its own cells
+    const int hnn = more ? step(hn) : hn;
+    int4 tnn = make_int4(0, 0, 1, 0);
+    if (hnn < n) tnn = __ldg(a.info + hnn);
     const int slot = ti.x;  // groups are (band, slot): each lane gathers in its own cell's Moore order
     if (slot != cur) {
       cur = slot;
@@ -649,9 +655,10 @@ __global__ void __launch_bounds__(kGwThreads, C == 2 ? 4 : 3) k_direct_gather(co
         // refill (unconditional for the next tile: the last tile reloads its
         // own cells, which keeps a single copy of the loop body)
 #pragma unroll
-        for (int c = 0; c < C; ++c)
-          q[c][j] = i < 2 ? ld_rec(rec_ptr(a.tex, cc[c], W, cc[c].rot, s + 3))
-                          : ld_rec(rec_ptr(a.tex, nc[c], W, nc[c].rot, j));
+        for (int c = 0; c < C; ++c) {
+          const GCell gc = i < 2 ? cc[c] : gcell(ne[c], W);
+          q[c][j] = ld_rec(rec_ptr(a.tex, gc, W, gc.rot, i < 2 ? s + 3 : j));
+        }
       }
     }
 #pragma unroll
@@ -709,8 +716,10 @@ __global__ void __launch_bounds__(kGwThreads, C == 2 ? 4 : 3) k_direct_gather(co
     }
     h = hn;
     ti = tn;
+    hn = hnn;
+    tn = tnn;
 #pragma unroll
-    for (int j = 0; j < C; ++j) cc[j] = nc[j];
+    for (int j = 0; j < C; ++j) cc[j] = gcell(ne[j], W);
   }
 }
 
