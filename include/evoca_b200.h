@@ -58,8 +58,12 @@ extern "C" {
 #define EVO_F_TC_DIRECT 2048    /* gather path: the direct net as tcgen05 3xTF32 MMAs (A in TMEM) instead of FFMA2 warps */
 #define EVO_F_L2_CUDA_CORE 4096 /* tensor-core hidden net: layer 2 as FP32 FMAs on the CUDA cores (round-2 kernel; A/B) */
 #define EVO_F_UNFUSED 8192      /* gather path in evo_step/evo_run: physics as its own kernel over the mid planes (round-2d; A/B) */
-#define EVO_F_FUSE_MID 16384    /* evo_pass1: the evo_pass2 of the same step follows with no halo exchange, so pass-1 outputs
-                                   may stay 32-byte records instead of the mid planes (evo_step sets it; gather path only) */
+#define EVO_F_FUSE_MID 16384    /* evo_pass1: the evo_pass2 of the same step follows (a strip's evo_halo_pack/unpack(1)
+                                   between them is fine), so pass-1 outputs may stay 32-byte records instead of the mid
+                                   planes (evo_step sets it; gather path only) */
+#define EVO_F_LAZY 32768        /* evo_pass1, with EVO_F_FUSE_MID: evo_pass2 and evo_swap follow, so pass 2 may leave E, I, C
+                                   in the sense texture and skip the planes until an entry point needs them (evo_step
+                                   sets it; strips: evo_halo_pack/unpack(0) then exchange texture rows) */
 
 /* Host-computed per-step scalars, exactly as the reference derives them:
  * rho = A*sin(2*pi*t/P) in float64 (physics.py:186); rho_mode 1 if rho > 0,

@@ -28,6 +28,7 @@ F_TC_DIRECT = 2048  # gather path: direct net on tcgen05 (3xTF32, A in TMEM) ins
 F_L2_CUDA_CORE = 4096  # tensor-core hidden net: layer 2 on the CUDA cores (round-2 kernel; A/B)
 F_UNFUSED = 8192  # gather path in evo_step: physics as its own kernel over the mid planes (round-2d; A/B)
 F_FUSE_MID = 16384  # evo_pass1 when evo_pass2 follows at once: pass-1 outputs may stay records (evo_step sets it)
+F_LAZY = 32768  # with F_FUSE_MID, when evo_pass2 and evo_swap follow: E, I, C may stay in the sense texture
 
 
 class EvoScalars(C.Structure):

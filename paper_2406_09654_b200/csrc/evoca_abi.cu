@@ -295,7 +295,7 @@ int ensure_actions_out(evo_ctx* c) {
 int ensure_sorted_out(evo_ctx* c) {
   if (c->hid.act) return 0;
   const size_t n = (size_t)c->ncell();
-  CK(c->alloc(&c->hid.act, n * 16));
+  CK(c->alloc(&c->hid.act, n * 16 + (size_t)c->W * 16));  // + two ghost rows of 8-float pass-1 records (strips)
   CK(c->alloc(&c->hid.rank, n));
   if (!c->num_sms) CK(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, c->device));
   return 0;
@@ -411,9 +411,6 @@ View band_view(const evo_ctx* c, int r0, int rows) {
   return v;
 }
 
-constexpr int kLazyStep = 1 << 30;  // internal (evo_step): the swap follows at once, so pass 2 may leave E, I, C
-                                    // in the texture only
-
 // The front E, I, C planes from the texture after lazy fused steps: called by
 // every entry point that reads or writes those planes (not by evo_step itself).
 int materialize(evo_ctx* c, cudaStream_t st) {
@@ -482,7 +479,7 @@ int pass1_view(evo_ctx* c, const View& v, const evo_scalars* s, int phases, int 
     }
     CK(evo::launch_hidden_gather(c->gat, v.g, c->params(), c->cap, c->num_sms, c->htab, c->hid.act, st));
   }
-  if (!gather_net || !(flags & kLazyStep)) {
+  if (!gather_net || !(flags & EVO_F_LAZY)) {
     if (int r = materialize(c, st)) return r;
   }
   c->lazy_step = false;
@@ -496,7 +493,7 @@ int pass1_view(evo_ctx* c, const View& v, const evo_scalars* s, int phases, int 
     // EVO_F_FUSE_MID): the physics runs in the net's epilogue and pass 2
     // reads 32-byte pass-1 records (no k_physics_rows, no mid planes); a bare
     // evo_pass1 keeps the mid planes it documents
-    if ((flags & EVO_F_FUSE_MID) && !(flags & EVO_F_UNFUSED) && maps && v.g.own_ghosts && !exp &&
+    if ((flags & EVO_F_FUSE_MID) && !(flags & EVO_F_UNFUSED) && maps && !exp &&
         variant == evo::kGatherFfma2) {
       evo::FusedPhysics fp;
       fp.s = to_scalars(*s);
@@ -506,7 +503,7 @@ int pass1_view(evo_ctx* c, const View& v, const evo_scalars* s, int phases, int 
       CK(evo::launch_direct_gather(c->gat, v.g, v.front, c->params(), c->cap, c->num_sms, variant, false, c->hid.act,
                                    c->hid.rank, st, maps, &fp, c->tex_state));
       c->mid_rec = c->hid.act;
-      c->lazy_step = (flags & kLazyStep) && !std::getenv("EVO_NO_LAZY");
+      c->lazy_step = (flags & EVO_F_LAZY) && !std::getenv("EVO_NO_LAZY");
       c->have_export = false;
       return 0;
     }
@@ -808,7 +805,7 @@ EVO_API int evo_set_source_map(evo_ctx* c, const float* map) {
 EVO_API int evo_pass1(evo_ctx* c, const evo_scalars* s, int64_t t, int phases, int flags, void* stream) {
   if (int r = check_ctx(c)) return r;
   (void)t;
-  return pass1_view(c, full_view(c), s, phases, flags & ~kLazyStep, c->census.stats, pick(c, stream));
+  return pass1_view(c, full_view(c), s, phases, flags, c->census.stats, pick(c, stream));
 }
 
 EVO_API int evo_pass2(evo_ctx* c, int64_t t, int flags, void* stream) {
@@ -850,7 +847,7 @@ EVO_API int evo_step(evo_ctx* c, const evo_scalars* s, int64_t t, int phases, in
     c->prof_used += 3;
     CK(cudaEventRecord(pe[0], st));
   }
-  if (int r = pass1_view(c, full_view(c), s, phases, (flags & ~kLazyStep) | EVO_F_FUSE_MID | kLazyStep,
+  if (int r = pass1_view(c, full_view(c), s, phases, flags | EVO_F_FUSE_MID | EVO_F_LAZY,
                          c->census.stats, st))
     return r;
   if (pe) CK(cudaEventRecord(pe[1], st));
@@ -1513,7 +1510,12 @@ EVO_API int evo_halo_row_words(evo_ctx* c, int which, int64_t* words) {
 EVO_API int evo_halo_pack(evo_ctx* c, int which, void* send, void* stream) {
   if (int r = check_ctx(c)) return r;
   if ((which != 0 && which != 1) || !send) return fail(EVO_EINVAL, "bad halo pack arguments");
-  if (int r = materialize(c, pick(c, stream))) return r;
+  // fused / lazy strip steps: the same rows from the pass-1 records, or from
+  // the sense texture while it holds the state
+  if ((which == 0 && c->tex_state) || (which == 1 && c->mid_rec)) {
+    CK(evo::launch_halo_rec(c->gat.tex, c->hid.act, c->geom(), which, true, send, pick(c, stream)));
+    return 0;
+  }
   CK(evo::launch_halo(c->buf[c->front], c->mid, c->geom(), which, true, send, pick(c, stream)));
   return 0;
 }
@@ -1521,7 +1523,11 @@ EVO_API int evo_halo_pack(evo_ctx* c, int which, void* send, void* stream) {
 EVO_API int evo_halo_unpack(evo_ctx* c, int which, const void* recv, void* stream) {
   if (int r = check_ctx(c)) return r;
   if ((which != 0 && which != 1) || !recv) return fail(EVO_EINVAL, "bad halo unpack arguments");
-  if (int r = materialize(c, pick(c, stream))) return r;
+  if ((which == 0 && c->tex_state) || (which == 1 && c->mid_rec)) {
+    CK(evo::launch_halo_rec(c->gat.tex, c->hid.act, c->geom(), which, false, const_cast<void*>(recv),
+                            pick(c, stream)));
+    return 0;
+  }
   CK(evo::launch_halo(c->buf[c->front], c->mid, c->geom(), which, false, const_cast<void*>(recv), pick(c, stream)));
   return 0;
 }

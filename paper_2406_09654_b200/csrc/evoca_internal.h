@@ -268,6 +268,9 @@ cudaError_t launch_wrap_mid(const Mid& m, const StepGeom& g, cudaStream_t st);
 cudaError_t launch_check_cells(int32_t* gi, uint8_t* rot, long long n, int capacity, int* bad, cudaStream_t st);
 cudaError_t launch_halo(const Planes& f, const Mid& m, const StepGeom& g, int which, bool pack, void* buf,
                         cudaStream_t st);
+// the same exchange on the fused step's buffers (texture records for which = 0, pass-1 records for which = 1)
+cudaError_t launch_halo_rec(float* tex, float* rec, const StepGeom& g, int which, bool pack, void* buf,
+                            cudaStream_t st);
 cudaError_t launch_scatter_actions(float* act, uint8_t* flag, const int64_t* cells, const float* rows, long long n,
                                    long long ncell, cudaStream_t st);
 cudaError_t launch_patch_genomes(int32_t* gi, int W, const int64_t* cells, const int32_t* slots, long long n,

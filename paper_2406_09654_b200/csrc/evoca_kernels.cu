@@ -33,6 +33,7 @@
 
 #include <algorithm>
 
+#include "evoca_gather.cuh"
 #include "evoca_tile.cuh"
 
 namespace evo {
@@ -987,9 +988,13 @@ __global__ void __launch_bounds__(kThreads2, EVO_K2_MIN_BLOCKS) k_resolve(const 
       int xb = x0 + 31 + (lane & 1);
       xb = xb >= g.W ? xb - g.W : xb;
       if (xb >= g.W) xb = g.W - 1;
-      auto rec_row = [&](int r) {  // halo row r of the tile -> record row (torus wrap by index)
+      // halo row r of the tile -> record row: a single strip wraps by index;
+      // strips keep their neighbours' rows (evo_halo_unpack) behind the last
+      // one: row H = ghost below, row H + 1 = ghost above
+      auto rec_row = [&](int r) {
         const int y = min(y0 + r - 1, g.H);
-        return y < 0 ? g.H - 1 : (y >= g.H ? 0 : y);
+        if (g.own_ghosts) return y < 0 ? g.H - 1 : (y >= g.H ? 0 : y);
+        return y < 0 ? g.H + 1 : y;
       };
       float4 hv[kRows], hx = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
 #pragma unroll
@@ -1348,6 +1353,43 @@ __global__ void k_halo_unpack(const Planes f, const Mid m, const StepGeom g, int
   }
 }
 
+// The same wire format from / to the fused step's buffers: which = 0 with the
+// state in the sense texture (lazy steps: E, I, C of rows 0 / H-1 out of, and
+// into the ghost rows of, the texture records), which = 1 with pass-1 records
+// (genome, quantity, proposal byte of rows 0 / H-1; the neighbours' rows go to
+// record rows H + 1 (above) and H (below), which k_resolve reads as its halo).
+__global__ void k_halo_pack_rec(const float* tex, const float* rec, const StepGeom g, int which, uint32_t* buf) {
+  const int np = which == 0 ? 5 : 3;
+  const int n = 2 * np * g.W;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int side = i / (np * g.W), r = i - side * np * g.W, pl = r / g.W, x = r - pl * g.W;
+    const int y = side ? g.H - 1 : 0;
+    uint32_t v;
+    if (which == 0) {
+      const int f = pl == 0 ? 0 : (pl == 1 ? 4 : pl - 1);  // gs::tex_ch
+      v = __float_as_uint(tex[((size_t)(y + 1) * g.W + x) * 8 + f]);
+    } else {
+      v = __float_as_uint(rec[((size_t)y * g.W + x) * 8 + (pl == 0 ? 6 : (pl == 1 ? 5 : 7))]);
+    }
+    buf[i] = v;
+  }
+}
+
+__global__ void k_halo_unpack_rec(float* tex, float* rec, const StepGeom g, int which, const uint32_t* buf) {
+  const int np = which == 0 ? 5 : 3;
+  const int n = 2 * np * g.W;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int side = i / (np * g.W), r = i - side * np * g.W, pl = r / g.W, x = r - pl * g.W;
+    const float v = __uint_as_float(buf[i]);
+    if (which == 0) {
+      const int f = pl == 0 ? 0 : (pl == 1 ? 4 : pl - 1);
+      tex[((size_t)(side ? g.H + 1 : 0) * g.W + x) * 8 + f] = v;
+    } else {
+      rec[((size_t)(side ? g.H : g.H + 1) * g.W + x) * 8 + (pl == 0 ? 6 : (pl == 1 ? 5 : 7))] = v;
+    }
+  }
+}
+
 __global__ void k_scatter_actions(float* act, uint8_t* flag, const int64_t* cells, const float* rows, long long n,
                                   long long ncell) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
@@ -1503,7 +1545,6 @@ cudaError_t launch_pass2(const Pass2Args& a_in, cudaStream_t st) {
   if (grid > need) grid = need;
   size_t smem = ((sizeof(WarpTile) * kWarps2 + 15) & ~(size_t)15) + (size_t)a.capacity * sizeof(int);
   if (a.tex_out) smem = ((smem + 15) & ~(size_t)15) + sizeof(float4) * kWtCells * kWarps2;
-  if (a.mid_rec && !a.g.own_ghosts) return cudaErrorInvalidValue;  // records wrap by index: single-strip steps
 #define EVO_LAUNCH_K2(REC, MID)                                          \
   {                                                                      \
     static SmemOptIn cfg;                                                \
@@ -1579,6 +1620,17 @@ cudaError_t launch_halo(const Planes& f, const Mid& m, const StepGeom& g, int wh
     k_halo_pack<<<blocks, 256, 0, st>>>(f, m, g, which, static_cast<uint32_t*>(buf));
   else
     k_halo_unpack<<<blocks, 256, 0, st>>>(f, m, g, which, static_cast<const uint32_t*>(buf));
+  return cudaGetLastError();
+}
+
+cudaError_t launch_halo_rec(float* tex, float* rec, const StepGeom& g, int which, bool pack, void* buf,
+                            cudaStream_t st) {
+  const int n = 2 * (which == 0 ? 5 : 3) * g.W;
+  const int blocks = (n + 255) / 256 > 1024 ? 1024 : (n + 255) / 256;
+  if (pack)
+    k_halo_pack_rec<<<blocks, 256, 0, st>>>(tex, rec, g, which, static_cast<uint32_t*>(buf));
+  else
+    k_halo_unpack_rec<<<blocks, 256, 0, st>>>(tex, rec, g, which, static_cast<const uint32_t*>(buf));
   return cudaGetLastError();
 }
 

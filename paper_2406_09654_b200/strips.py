@@ -221,6 +221,10 @@ class DeviceStrip:
         from . import _lib
 
         stream = torch.cuda.current_stream().cuda_stream
+        if not flags & (_lib.F_UNFUSED | _lib.F_EXPORT_ACTIONS | _lib.F_INJECT_ACTIONS):
+            # what evo_step passes to its pass 1: pass 2 and the swap follow (the
+            # halo calls exchange record / texture rows when the step is fused / lazy)
+            flags |= _lib.F_FUSE_MID | _lib.F_LAZY
         self.exchange_front()
         self.dev.pass1(scalars, t, flags=flags, stream=stream)
         self.exchange_mid()
@@ -298,6 +302,8 @@ def step_local(strips, scalars, t: int, flags: int = 0) -> None:
         for s, (_, recv) in zip(strips, bufs):
             check(s.dev.lib.evo_halo_unpack(s.dev.ctx, which, C.c_void_p(recv.data_ptr()), cstream))
 
+    if not flags & (_lib.F_UNFUSED | _lib.F_EXPORT_ACTIONS | _lib.F_INJECT_ACTIONS):
+        flags |= _lib.F_FUSE_MID | _lib.F_LAZY  # as DeviceStrip.step
     ring(0)
     for s in strips:
         s.dev.pass1(scalars, t, flags=flags, stream=stream)

@@ -88,6 +88,51 @@ def test_strips_match_single_context(world, shape, genomes):
 
 
 @pytest.mark.parametrize("world", [1, 2, 3])
+@pytest.mark.parametrize("shape", [(64, 64), (35, 132)])
+def test_lazy_strips_match_single_context(world, shape):
+    """Strips run the fused, lazy gather step too: between downloads the E, I,
+    C state of a strip lives in its sense texture, evo_halo_pack / unpack(0)
+    exchange texture rows (ghost rows of the texture) and (1) the pass-1
+    records' rows (kept behind the strip's last record row).  Five steps
+    without touching the planes, with unoccupied and starving cells, then a
+    download; twice; bit-identical to the single context and to EVO_F_UNFUSED
+    strips."""
+    import torch
+
+    from paper_2406_09654_b200 import _lib
+
+    H, W = shape
+    genomes = 300
+    p0 = orc.synth_planes(H, W, genomes, seed=3 * H + world)
+    rng = np.random.default_rng(5)
+    p0.gi[rng.random((H, W)) < 0.25] = -1
+    p0.I[rng.random((H, W)) < 0.2] *= np.float32(0.002)
+    net = orc.synth_net(genomes, 0, seed=4)
+    ref = make_dev(p0, genomes, net)
+    plan, strips = _strips(p0, net, world)
+    plan2, unfused = _strips(p0, net, world)
+    params = physics.PhysicsParams(cycle_period=6, explore_fraction=0.8)
+    t = 0
+    for _ in range(2):
+        for _ in range(5):
+            sc = physics.step_scalars(t, params)
+            ref.step_raw(sc, t)
+            step_local(strips, sc, t)
+            step_local(unfused, sc, t, flags=_lib.F_UNFUSED)
+            t += 1
+        torch.cuda.synchronize()
+        want = download(ref)
+        assert _gather(plan, strips, p0).equal(want), f"world={world} t={t}"
+        assert _gather(plan2, unfused, p0).equal(want), f"unfused world={world} t={t}"
+        c_ref = ref.read_census()[0]
+        for s in strips:
+            assert np.array_equal(s.dev.read_census()[0], c_ref)
+    for s in strips + unfused:
+        s.dev.close()
+    ref.close()
+
+
+@pytest.mark.parametrize("world", [1, 2, 3])
 def test_strips_tensor_core_hidden_net(world):
     """The config-5 net (45->128 tanh->13 on tcgen05) in strip mode: per-cell
     results do not depend on the strip / bucket / tile placement, so 1-3
