@@ -53,7 +53,8 @@ def main():
     ex, rec = _lib.F_EXPORT_ACTIONS, _lib.F_RECORD_EVENTS
     for n in (64, 256):
         world(n, 8, 0, [0, ex | rec, _lib.F_MMA_NET])                           # per-tile direct kernel
-        world(n, 300, 0, [0, ex, _lib.F_TC_DIRECT, _lib.F_TC_DIRECT | ex,      # gather (FFMA2 / tcgen05)
+        world(n, 300, 0, [0, rec, _lib.F_UNFUSED], steps=4)                      # gather: fused + lazy steps, unfused
+        world(n, 300, 0, [ex, _lib.F_TC_DIRECT, _lib.F_TC_DIRECT | ex,         # gather (export / tcgen05)
                           _lib.F_ROWS_NET, _lib.F_SHARD_NET, _lib.F_TILE_NET])   # rows / sharded / tile
         world(n, 20, 128, [0, ex, _lib.F_CUDA_CORE_NET])                        # tcgen05 hidden net
         world(n, 6, 16, [0, _lib.F_TC_NET])                                     # narrow hidden layer
@@ -73,6 +74,21 @@ def main():
         strips.append(s)
     for t in range(2):
         step_local(strips, physics.step_scalars(t, physics.PhysicsParams()), t)
+    # strips on the gather path: fused / lazy steps, record and texture rows through the halo calls
+    p = orc.synth_planes(64, 48, 300, seed=4)
+    net = orc.synth_net(300, 0, seed=4)
+    big = []
+    for r in range(2):
+        s = DeviceStrip(plan, r, 300)
+        s.dev.set_params(params(net))
+        s.dev.set_slots(np.ones(300, np.int8))
+        r0, h = plan.rows(r)
+        s.dev.upload_arrays(p.E[r0:r0 + h], p.I[r0:r0 + h], p.C[:, r0:r0 + h], p.gi[r0:r0 + h], p.rot[r0:r0 + h])
+        big.append(s)
+    for t in range(4):
+        step_local(big, physics.step_scalars(t, physics.PhysicsParams()), t)
+    for s in big:
+        s.dev.render_rgb()
     # engine with adoption radiation (device CPPN expression, host NEAT, patches),
     # field radiation (selection / remap), observables
     cfg = engine.ExperimentConfig(grid=engine.GridConfig(64, 64), seed=2, initial_population=30)
