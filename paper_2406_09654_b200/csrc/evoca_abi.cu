@@ -96,6 +96,9 @@ struct evo_ctx {
   // the running evo_step wrote the texture for the buffer the swap makes front.
   bool tex_state = false, tex_pending = false, lazy_step = false;
   // evo_profile: per-step events (start, between the passes, end) of evo_step
+  // evo_run's instantiated step graphs, destroyed once their stream has drained
+  std::vector<cudaGraphExec_t> run_execs;
+  cudaStream_t run_stream = nullptr;
   bool profile = false;
   std::vector<cudaEvent_t> prof_ev;
   size_t prof_used = 0;
@@ -602,6 +605,18 @@ int pass2_view(evo_ctx* c, const View& v, int64_t t, int flags, int run_census, 
 
 }  // namespace
 
+void drop_run_graphs(evo_ctx* c, bool force) {
+  if (c->run_execs.empty()) return;
+  if (!force && cudaStreamQuery(c->run_stream) != cudaSuccess) {
+    cudaGetLastError();
+    return;  // still running: keep them for the next call
+  }
+  if (force) cudaStreamSynchronize(c->run_stream);
+  for (cudaGraphExec_t e : c->run_execs) cudaGraphExecDestroy(e);
+  c->run_execs.clear();
+}
+
+
 extern "C" {
 
 EVO_API const char* evo_last_error(void) { return g_err.c_str(); }
@@ -621,6 +636,7 @@ EVO_API int evo_destroy(evo_ctx* c) {
   if (!c) return 0;
   cudaSetDevice(c->device);
   cudaStreamSynchronize(c->stream);
+  drop_run_graphs(c, true);
   for (cudaEvent_t e : c->prof_ev) cudaEventDestroy(e);
   c->prof_ev.clear();
   if (c->s_in) {
@@ -1135,10 +1151,55 @@ EVO_API int evo_profile_read(evo_ctx* c, double* pass1_ms, double* pass2_ms, int
   return 0;
 }
 
+// evo_run (engine.py:251-271's loop): the first step runs eagerly (it makes
+// the lazy allocations and shared-memory opt-ins), the others are captured
+// into CUDA graphs of up to kRunGraphSteps steps and launched as one unit -
+// small worlds are launch-bound (config 1: two ~5 us kernels per step).  The
+// host-side step state (front buffer, lazy-texture flags) advances while
+// capturing exactly as it does eagerly.  EVO_NO_GRAPH=1 keeps the eager loop.
+constexpr int kRunGraphSteps = 128;
+
 EVO_API int evo_run(evo_ctx* c, const evo_scalars* s, int64_t t0, int k, void* stream) {
   if (!s && k > 0) return fail(EVO_EINVAL, "null scalars");
-  for (int i = 0; i < k; ++i)
-    if (int r = evo_step(c, s + i, t0 + i, EVO_PH_ALL, 0, stream)) return r;
+  if (k <= 0) return 0;
+  if (int r = check_ctx(c)) return r;
+  static const bool no_graph = std::getenv("EVO_NO_GRAPH") != nullptr;
+  const bool graphs = k >= 4 && !c->strip && !c->profile && !no_graph;
+  if (!graphs) {
+    for (int i = 0; i < k; ++i)
+      if (int r = evo_step(c, s + i, t0 + i, EVO_PH_ALL, 0, stream)) return r;
+    return 0;
+  }
+  cudaStream_t st = pick(c, stream);
+  if (st != c->run_stream) drop_run_graphs(c, true);
+  c->run_stream = st;
+  drop_run_graphs(c, false);
+  if (int r = evo_step(c, s, t0, EVO_PH_ALL, 0, stream)) return r;
+  for (int i = 1; i < k;) {
+    const int n = std::min(k - i, kRunGraphSteps);
+    if (cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
+      cudaGetLastError();  // e.g. the legacy default stream: run the rest eagerly
+      for (; i < k; ++i)
+        if (int r = evo_step(c, s + i, t0 + i, EVO_PH_ALL, 0, stream)) return r;
+      return 0;
+    }
+    int rc = 0;
+    for (int j = 0; j < n && !rc; ++j) rc = evo_step(c, s + i + j, t0 + i + j, EVO_PH_ALL, 0, stream);
+    cudaGraph_t g = nullptr;
+    const cudaError_t e = cudaStreamEndCapture(st, &g);
+    if (rc || e != cudaSuccess) {
+      if (g) cudaGraphDestroy(g);
+      cudaGetLastError();
+      return rc ? rc : fail((int)e, std::string("evo_run: stream capture failed: ") + cudaGetErrorString(e));
+    }
+    cudaGraphExec_t ge = nullptr;
+    cudaError_t ei = cudaGraphInstantiate(&ge, g, 0);
+    cudaGraphDestroy(g);
+    CK(ei);
+    c->run_execs.push_back(ge);
+    CK(cudaGraphLaunch(ge, st));
+    i += n;
+  }
   return 0;
 }
 

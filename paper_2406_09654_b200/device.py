@@ -211,10 +211,13 @@ class DeviceSubstrate:
     def swap(self) -> None:
         check(self.lib.evo_swap(self.ctx))
 
-    def run(self, scalars_list, t0: int, stream=None) -> None:
+    def run(self, scalars_list, t0: int, stream=None, source_map=None) -> None:
         k = len(scalars_list)
         if k == 0:
             return
+        if source_map is not None or self._src_map_id is not None:
+            if source_map is None or id(source_map) != self._src_map_id:
+                self.set_source_map(source_map)
         arr = (_lib.EvoScalars * k)(*scalars_list)
         check(self.lib.evo_run(self.ctx, arr, int(t0), k, _stream(stream)))
 

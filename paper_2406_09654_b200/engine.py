@@ -592,17 +592,29 @@ def run(state, steps: int, hooks=(), should_stop: Optional[Callable[[], bool]] =
     if not b.device_ahead:
         b.dev.upload(sub.front)
     phys = state.config.physics
-    for _ in range(steps):
+    fr = getattr(state.config, "field_radiation", None)
+    periods = [h.every for h in hooks] + ([fr.every] if fr is not None and fr.every > 0 else [])
+    done = 0
+    while done < steps:
         if should_stop is not None and should_stop():
             break
         t = sub.step_counter
+        n = 1
         if rad:
             _device_radiation_step(state, b, t, phys)
         else:
-            b.dev.step_raw(step_scalars(t, phys), t, source_map=phys.energy_source_map)
-        sub.step_counter = t + 1
+            if should_stop is None:
+                # the steps up to the next hook / radiation event go down as one
+                # evo_run (one CUDA graph launch per 128 steps: small worlds
+                # are launch-bound)
+                n = min([steps - done] + [e - t % e for e in periods])
+            if n > 1:
+                b.dev.run([step_scalars(t + j, phys) for j in range(n)], t, source_map=phys.energy_source_map)
+            else:
+                b.dev.step_raw(step_scalars(t, phys), t, source_map=phys.energy_source_map)
+        sub.step_counter = t + n
+        done += n
         b.device_ahead = True
-        fr = getattr(state.config, "field_radiation", None)
         if fr is not None and fr.every > 0 and sub.step_counter % fr.every == 0:
             from .radiation import field_radiation
 

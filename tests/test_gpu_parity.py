@@ -627,6 +627,40 @@ def test_fused_gather_step_matches_unfused(genomes, shape, phases):
     b.close()
 
 
+@pytest.mark.parametrize("genomes,hidden,shape", [(8, 0, (64, 64)), (300, 0, (96, 80)), (20, 128, (64, 96)),
+                                                  (6, 16, (33, 70))])
+def test_evo_run_graphs_equal_step_loop(genomes, hidden, shape):
+    """evo_run captures its steps (all but the first) into CUDA graphs of up to
+    128 steps; the planes, census, stats and the device's step state afterwards
+    equal a loop of evo_step - per-tile kernel, gather path (lazy fused
+    steps inside the graph), tensor-core and CUDA-core hidden nets; two runs
+    back to back, a run of 3 (eager: below the graph threshold), then single
+    steps again."""
+    h, w = shape
+    p0 = orc.synth_planes(h, w, genomes, seed=genomes + 3)
+    net = orc.synth_net(genomes, hidden, seed=2)
+    params = oracle_phys_to_params(orc.Phys(cycle_period=7))
+    a = make_dev(p0, genomes, net)
+    b = make_dev(p0, genomes, net)
+    t = 0
+    for k in (9, 140, 3, 5):
+        scs = [physics.step_scalars(t + i, params) for i in range(k)]
+        a.run(scs, t)
+        for i in range(k):
+            b.step_raw(scs[i], t + i)
+        t += k
+        assert a.read_stats() == b.read_stats()
+        for ca, cb in zip(a.read_census(), b.read_census()):
+            assert np.array_equal(ca, cb)
+        assert download(a).equal(download(b)), f"k={k}"
+    sc = physics.step_scalars(t, params)
+    a.step_raw(sc, t)
+    b.step_raw(sc, t)
+    assert download(a).equal(download(b))
+    a.close()
+    b.close()
+
+
 @pytest.mark.parametrize("shape", [(96, 80), (70, 258), (1, 512)])
 def test_tma_texture_build_matches_lsu_build(shape, monkeypatch):
     """The gather path's texture build through TMA (k_gs_count_tma, the

@@ -21,6 +21,7 @@ def main():
     ap.add_argument("--height", type=int, default=None)
     ap.add_argument("--flags", type=int, default=0)
     ap.add_argument("--time", action="store_true", help="CUDA-event time per step")
+    ap.add_argument("--run", type=int, default=0, help="time dev.run (evo_run) of this many steps, wall clock")
     args = ap.parse_args()
     import torch
 
@@ -43,6 +44,17 @@ def main():
         e1.record(s)
         times.append((e0, e1))
     torch.cuda.synchronize()
+    if args.run:
+        import time
+
+        k = args.run
+        for rep in range(3):
+            scs = [physics.step_scalars(args.steps + rep * k + i, st.config.physics) for i in range(k)]
+            t0 = time.perf_counter()
+            dev.run(scs, args.steps + rep * k, stream=s.cuda_stream)
+            torch.cuda.synchronize()
+            dt = time.perf_counter() - t0
+            print(f"evo_run {k} steps: {dt / k * 1e6:.2f} us/step (EVO_NO_GRAPH={os.environ.get('EVO_NO_GRAPH')})")
     if args.time:
         ms = [a.elapsed_time(b) for a, b in times]
         n = st.substrate.width * st.substrate.height
