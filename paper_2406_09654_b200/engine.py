@@ -495,8 +495,9 @@ def _download_front(state) -> None:
     b.device_ahead = False
 
 
-def _fold_census(state) -> None:
-    """Bring the device's deferred census into the host pool."""
+def _fold_census(state):
+    """Bring the device's deferred census into the host pool; returns the
+    device's per-slot peaks (what the records of the live slots now hold)."""
     b = _binding(state)
     counts, st, death, peak = b.dev.read_census()
     pool = state.pool
@@ -504,7 +505,7 @@ def _fold_census(state) -> None:
         # the device already holds these slot states; pool.version is not
         # bumped, so changes the host made since the last sync stay pending
         pool.apply_device_census(st, death, peak)
-        return
+        return peak
     # foreign pool (e.g. the reference GenomePool): replay update_census in
     # death-step order, feeding each slot's peak so peaks update identically
     live = np.asarray(pool.live_mask(), bool)

@@ -47,6 +47,9 @@ class SlotPool:
         self.records: dict[int, SlotRecord] = {}
         self.next_lineage_id = 0
         self.version = 0  # bumped on every params/liveness change
+        # apply_device_census: the device peak and the occupant it was last folded for, per slot
+        self._seen_peak = np.full(capacity, -1, np.int64)
+        self._seen_lineage = np.full(capacity, -2, np.int64)
 
     def install(self, slot: int, params, birth_step: int = 0, genome=None) -> int:
         """Put a parameter set (and optionally its pattern network) in a slot
@@ -181,7 +184,15 @@ class SlotPool:
         step, peak) into the records; equivalent to having called
         update_census every step."""
         dead = []
-        for i in np.flatnonzero(self._state == 1):
+        live = np.flatnonzero(self._state == 1)
+        state, peak = np.asarray(state), np.asarray(peak)
+        # a live slot whose occupant and device peak are those of the last fold
+        # has nothing new (its record already holds that peak): the records
+        # are only visited for the others (a radiation event folds ~1000 slots)
+        lin = self._lineage[live]
+        pk = peak[live].astype(np.int64)
+        todo = (state[live] == 2) | (pk != self._seen_peak[live]) | (lin != self._seen_lineage[live])
+        for i in live[todo]:
             rec = self.records[int(self._lineage[i])]
             if peak[i] > rec.peak_population:
                 rec.peak_population = int(peak[i])
@@ -190,4 +201,6 @@ class SlotPool:
                 self._death[i] = int(death_step[i])
                 rec.death_step = int(death_step[i])
                 dead.append(int(i))
+        self._seen_peak[live] = pk
+        self._seen_lineage[live] = lin
         return dead

@@ -257,7 +257,7 @@ def field_radiation(state, t: int, p: float = 0.01, rates: neat.EvolutionRates |
     plan = plan_field_radiation(pool, state.master_seed, t, rates) if hasattr(pool, "slot_states") else None
     if wait is not None:
         wait()
-    _fold_census(state)  # admission must see the device's deaths (slot states, peaks)
+    dev_peak = _fold_census(state)  # admission must see the device's deaths (slot states, peaks)
     counts, n_sel = dev.select_cells(stream_key(state.master_seed, t, purpose), p)
     synced = getattr(pool, "version", None) is not None and b.pool_version == pool.version
     slot_map, parents, children = admit_children(pool, counts, state.master_seed, t, rates, plan)
@@ -269,7 +269,14 @@ def field_radiation(state, t: int, p: float = 0.01, rates: neat.EvolutionRates |
             b.param_ids[s] = pool.params(s)
         from .engine import _peaks, _slot_states
 
-        dev.set_slots(_slot_states(pool), _peaks(pool))
+        if dev_peak is None:
+            peaks = _peaks(pool)
+        else:
+            # the binding was in sync, so the device's peaks are the records'
+            # (the fold just took them); only the children's slots start over
+            peaks = np.array(dev_peak, np.int32)
+            peaks[np.asarray(list(children), np.int64)] = 0
+        dev.set_slots(_slot_states(pool), peaks)
         b.pool_version = pool.version
     else:
         b.sync_params(pool)  # one batched evo_express_cppn for every new slot

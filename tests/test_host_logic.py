@@ -159,3 +159,54 @@ def test_layout_coords_match_reference_layout():
     for hidden in (0, 16, 128):
         inp, hid, out = ocppn.make_layout(hidden)
         np.testing.assert_array_equal(neat.layout_coords(hidden), np.vstack([inp, hid, out]))
+
+
+def test_apply_device_census_incremental_fold():
+    """SlotPool.apply_device_census visits only the live slots whose occupant
+    or device peak changed since the last fold (a config-3 radiation event
+    folds ~1000 slots); records, states and deaths equal the plain per-slot
+    loop over random census sequences with deaths, re-installs into dead
+    slots and peaks written to the records behind its back."""
+    rng = np.random.default_rng(0)
+    cap = 64
+
+    def plain(pool, state, death, peak):
+        dead = []
+        for i in np.flatnonzero(pool._state == 1):
+            rec = pool.records[int(pool._lineage[i])]
+            if peak[i] > rec.peak_population:
+                rec.peak_population = int(peak[i])
+            if state[i] == 2:
+                pool._state[i] = 2
+                pool._death[i] = int(death[i])
+                rec.death_step = int(death[i])
+                dead.append(int(i))
+        return dead
+
+    a, b = SlotPool(cap), SlotPool(cap)
+    for pool in (a, b):
+        for s in range(40):
+            pool.install(s, object())
+    dev_peak = np.zeros(cap, np.int32)
+    for step in range(1, 60):
+        live = a._state == 1
+        dev_peak = np.where(live, np.maximum(dev_peak, rng.integers(0, 50, cap)), dev_peak).astype(np.int32)
+        if step % 3:
+            dev_peak = dev_peak.copy()  # many folds see unchanged peaks
+        st = a._state.copy()
+        dying = live & (rng.random(cap) < 0.05)
+        st[dying] = 2
+        death = np.where(dying, step, -1).astype(np.int64)
+        assert a.apply_device_census(st, death, dev_peak) == plain(b, st, death, dev_peak)
+        if step % 7 == 0:  # a dead slot gets a new occupant: the device peak starts over
+            for s in np.flatnonzero(a._state == 2)[:2]:
+                a.install(int(s), object(), birth_step=step)
+                b.install(int(s), object(), birth_step=step)
+                dev_peak[s] = 0
+        if step % 11 == 0:  # a snapshot load writes record peaks directly
+            s = int(np.flatnonzero(a._state == 1)[0])
+            for pool in (a, b):
+                pool.record_for_slot(s).peak_population = 1000
+        assert np.array_equal(a._state, b._state) and np.array_equal(a._death, b._death)
+        assert {k: (r.peak_population, r.death_step) for k, r in a.records.items()} == \
+               {k: (r.peak_population, r.death_step) for k, r in b.records.items()}
