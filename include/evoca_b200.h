@@ -328,6 +328,9 @@ EVO_API int evo_plane_ptr(evo_ctx* ctx, int which, int buffer, void** ptr, int64
  * CTAs (0 bucketing, 1 controller, 2 physics tail, 3 halo commit, 4 setup);
  * non-zero only in a library built with -DEVO_PHASE_TIMING. */
 EVO_API int evo_debug_phase_cycles(uint64_t* out8, int reset);
+/* Test hook: the sigmoid's inline reciprocal (hypernet.py:246-251's 1 / (1 + exp(-z)), correctly rounded)
+ * against __frcp_rn over every float in [1, 2^125); *mismatches must come back 0. */
+EVO_API int evo_debug_rcp_check(uint64_t* mismatches);
 /* Same for the tensor-core hidden-layer kernel (8 phases of its tile loop). */
 EVO_API int evo_debug_hidden_cycles(uint64_t* out8, int reset);
 

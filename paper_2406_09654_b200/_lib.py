@@ -99,6 +99,7 @@ SIGNATURES = {
     "evo_host_unregister": [_P],
     "evo_fnv1a64": [C.c_uint64, _P, _I64, C.POINTER(C.c_uint64)],
     "evo_debug_phase_cycles": [_P, _I],
+    "evo_debug_rcp_check": [_P],
     "evo_debug_hidden_cycles": [_P, _I],
     "evo_neat_mutate": [_I, _P, _P, _P] + [_P] * 10 + [_P] * 10,
     "evo_neat_mutate_deferred": [_I, _P, _P] + [_P] * 10 + [_P] * 10,

@@ -1618,6 +1618,14 @@ EVO_API int evo_plane_ptr(evo_ctx* c, int which, int buffer, void** ptr, int64_t
   return 0;
 }
 
+EVO_API int evo_debug_rcp_check(uint64_t* mismatches) {
+  if (!mismatches) return fail(EVO_EINVAL, "null argument");
+  unsigned long long n = 0;
+  CK(evo::debug_rcp_check(&n));
+  *mismatches = n;
+  return 0;
+}
+
 EVO_API int evo_debug_phase_cycles(uint64_t* out8, int reset) {
   if (!out8) return fail(EVO_EINVAL, "null argument");
   CK(cudaDeviceSynchronize());

@@ -250,6 +250,7 @@ cudaError_t launch_shard_plan(const int8_t* state, int cap, int Q, int* map, int
 cudaError_t launch_pass1_shard(const Pass1Args& a, const int* map, const float* tables, int Q, int num_sms,
                                cudaStream_t st);
 cudaError_t debug_phase_cycles(unsigned long long* out, bool reset);
+cudaError_t debug_rcp_check(unsigned long long* host_out);
 cudaError_t debug_hidden_cycles(unsigned long long* out, bool reset);
 cudaError_t launch_census_finish(const Census& c, int capacity, long long t, cudaStream_t st,
                                  const int* skip = nullptr);

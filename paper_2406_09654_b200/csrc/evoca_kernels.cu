@@ -1569,6 +1569,28 @@ cudaError_t launch_pass2(const Pass2Args& a_in, cudaStream_t st) {
   return cudaGetLastError();
 }
 
+// rcp_rn_ge1 against __frcp_rn over every float in [1, 2^125) (evo_debug_rcp_check)
+__global__ void k_rcp_check(unsigned long long* mismatches) {
+  unsigned long long bad = 0;
+  for (unsigned long long b = 0x3f800000ull + blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x;
+       b < 0x7e000000ull; b += (unsigned long long)gridDim.x * blockDim.x) {
+    const float d = __uint_as_float((unsigned)b);
+    bad += __float_as_uint(rcp_rn_ge1(d)) != __float_as_uint(__frcp_rn(d)) ? 1 : 0;
+  }
+  if (bad) atomicAdd(mismatches, bad);
+}
+
+cudaError_t debug_rcp_check(unsigned long long* host_out) {
+  unsigned long long* d = nullptr;
+  cudaError_t e = cudaMalloc(&d, sizeof(unsigned long long));
+  if (e != cudaSuccess) return e;
+  cudaMemset(d, 0, sizeof(unsigned long long));
+  k_rcp_check<<<num_sms() * 16, 256>>>(d);
+  e = cudaMemcpy(host_out, d, sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+  cudaFree(d);
+  return e;
+}
+
 cudaError_t debug_phase_cycles(unsigned long long* out, bool reset) {
   cudaError_t e = cudaMemcpyFromSymbol(out, g_phase_cycles, sizeof(unsigned long long) * 8);
   if (e == cudaSuccess && reset) {

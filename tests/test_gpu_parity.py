@@ -627,6 +627,18 @@ def test_fused_gather_step_matches_unfused(genomes, shape, phases):
     b.close()
 
 
+def test_sigmoid_reciprocal_is_correctly_rounded():
+    """squash (hypernet.py:246-251) divides through an inline MUFU.RCP +
+    residual step instead of __frcp_rn's branchy form: identical bits for
+    every float in [1, 2^125) - 1 + exp(-z) for z > -86.6 (below that the
+    output is clamped to 2^-126 either way)."""
+    import ctypes as C
+
+    n = C.c_uint64(1)
+    _lib.check(_lib.load().evo_debug_rcp_check(C.byref(n)))
+    assert n.value == 0
+
+
 @pytest.mark.parametrize("genomes,hidden,shape", [(8, 0, (64, 64)), (300, 0, (96, 80)), (20, 128, (64, 96)),
                                                   (6, 16, (33, 70))])
 def test_evo_run_graphs_equal_step_loop(genomes, hidden, shape):
