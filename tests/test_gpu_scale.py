@@ -59,6 +59,16 @@ def test_config3_full_size_tier_a():
         assert np.array_equal(oa.cells, cells)
         assert rel_err(acts, oa.a) <= TOL, f"t={t}"
         p = got
+    # the steady state of a run: six steps as one evo_run (CUDA graph; the E, I,
+    # C state stays in the sense texture between the steps) against six
+    # unfused steps, at full size
+    scs = [physics.step_scalars(2 + i, params) for i in range(6)]
+    fast.run(scs, 2)
+    for i in range(6):
+        rows.step_raw(scs[i], 2 + i, flags=_lib.F_UNFUSED)
+    assert fast.read_stats() == rows.read_stats()
+    assert np.array_equal(fast.read_census()[0], rows.read_census()[0])
+    assert download(fast).equal(download(rows))
     dev.close()
     fast.close()
     rows.close()
