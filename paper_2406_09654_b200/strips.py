@@ -154,6 +154,11 @@ class DeviceStrip:
         self.dev = DeviceSubstrate(plan.width, self.h, capacity, hidden, device, row0=self.row0,
                                    height_global=plan.height)
         self.comm = comm or HaloComm(rank, plan.world)
+        # field radiation's selection buffers are allocated now, as the single
+        # context's binding does (engine.py: select_cells(0, 0.0)), not inside
+        # the first radiation event of a run
+        self.dev.count_occupied()
+        self.dev.select_cells_at(0, 0.0, 0)
 
     # -- views ----------------------------------------------------------------
     def _plane(self, which: str, buffer: int, sub: int, dtype):
