@@ -49,6 +49,15 @@ constexpr int kGsThreads = 512;  // count / scatter CTA
 // which gathers each row in its own order); GsPlan.tile: cells per tile
 // (64 = one warp, 128 = one MMA M).
 constexpr int kGsBandCells = 1 << 20;
+// EVO_BAND_CELLS overrides the band size (tuning runs)
+static long long band_cells_default() {
+  static const long long v = [] {
+    const char* e = std::getenv("EVO_BAND_CELLS");
+    const long long x = e ? std::atoll(e) : 0;
+    return x >= 4096 ? x : (long long)kGsBandCells;
+  }();
+  return v;
+}
 
 struct GsPlan {
   int rows_per_cta, ctas_per_band, nctas, nbands, bins, rb, tile;
@@ -984,7 +993,7 @@ __global__ void __launch_bounds__(kTcThreads, 4) k_direct_tc(const GatherArgs a)
   if (warp == 0) tc::tmem_dealloc<kTcCols>(tmem);
 }
 
-GsPlan make_plan(int W, int H, int cap, int num_sms, int tile, long long band_cells = kGsBandCells) {
+GsPlan make_plan(int W, int H, int cap, int num_sms, int tile, long long band_cells = band_cells_default()) {
   GsPlan p;
   p.rb = 1;  // both nets gather each row in its own Moore order
   p.tile = tile;
@@ -1055,7 +1064,7 @@ cudaError_t launch_gather_sort(const GatherBuffers& b, const StepGeom& g, const 
                                const FusedPhysics* fused, float* mid_rec, bool tex_is_state) {
   if (fused && !maps) return cudaErrorInvalidValue;  // the fused step's unoccupied cells go through the TMA build
   if (tex_is_state && (!fused || (g.W & 3))) return cudaErrorInvalidValue;
-  const GsPlan p = make_plan(g.W, g.H, cap, num_sms, tile, one_band ? (long long)g.W * g.H : kGsBandCells);
+  const GsPlan p = make_plan(g.W, g.H, cap, num_sms, tile, one_band ? (long long)g.W * g.H : band_cells_default());
   if (tex_is_state) {  // ranks only: the texture holds the state (lazy fused steps)
     const size_t hsmem = (size_t)p.bins * 4;
     if (hsmem > 48 * 1024) {
