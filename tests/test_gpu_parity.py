@@ -548,7 +548,7 @@ def test_genome_sorted_direct_path_matches_tile_path(genomes, shape):
 
 
 @pytest.mark.parametrize("genomes,shape", [(300, (96, 80)), (1024, (64, 64)), (90, (1, 500)), (2048, (70, 260)),
-                                           (512, (2, 36)), (128, (131, 516))])
+                                           (512, (2, 36)), (128, (131, 516)), (8192, (64, 128))])
 @pytest.mark.parametrize("phases", [_lib.PH_ALL, _lib.PH_ENERGY | _lib.PH_INVEST | _lib.PH_EXPLORE,
                                     _lib.PH_COMM | _lib.PH_EXPLORE])
 def test_fused_gather_step_matches_unfused(genomes, shape, phases):
@@ -558,8 +558,9 @@ def test_fused_gather_step_matches_unfused(genomes, shape, phases):
     round-2d kernels: planes, census counts, adoption events and stats are
     bit-identical, with unoccupied cells (their records come from the texture
     build), starving cells (communication decay re-reads the cell's record),
-    phase subsets, a 1- and a 2-row torus and widths off the 32-cell warp
-    tile and the 256-cell TMA box."""
+    phase subsets, a 1- and a 2-row torus, widths off the 32-cell warp
+    tile and the 256-cell TMA box, and the largest pool (8192 slots: 70 KB of
+    shared memory per pass-2 CTA)."""
     h, w = shape
     p0 = orc.synth_planes(h, w, genomes, seed=genomes + 1)
     rng = np.random.default_rng(7)
