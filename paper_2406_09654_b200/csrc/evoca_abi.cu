@@ -515,7 +515,10 @@ int pass1_view(evo_ctx* c, const View& v, const evo_scalars* s, int phases, int 
                                  c->hid.rank, st, maps));
   }
   const bool via_rows = tc_net || rows_net || gather_net;
-  const bool decided = via_rows && c->hidden == 0 && !exp;  // 8-float records at the cell index
+  // 8-float decided records at the cell index: direct nets, and hidden nets through k_hid_net2
+  const bool decided = via_rows && !exp &&
+                       (c->hidden == 0 || (tc_net && !hid_gather &&
+                                           evo::hidden_net2_used(c->hidden, (flags & EVO_F_L2_CUDA_CORE) != 0)));
   c->have_export = exp || (via_rows && !decided);
   c->exp_rows = via_rows ? c->hid.act : c->act_out;
   c->exp_flag = via_rows ? nullptr : c->act_out_flag;

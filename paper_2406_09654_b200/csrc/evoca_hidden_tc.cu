@@ -1056,18 +1056,33 @@ __global__ void __launch_bounds__(kNetThreads, 1) k_hid_net2(const NetArgs a) {
         }
       }
       if (r < ti.z) {
-        float o[16];
-#pragma unroll
-        for (int j = 0; j < kActuators; ++j) o[j] = squash(__fadd_rn(zs[j], bias2[j]));
-        o[13] = o[14] = o[15] = 0.0f;
-        // the actuator row at the cell index (the physics then reads it
-        // coalesced): the gather form's list entry, or element 45 of the
-        // sensor row (its cell index, k_hid_sense)
+        // the row at the cell index (the physics then reads it coalesced):
+        // the gather form's list entry, or element 45 of the sensor row (its
+        // cell index, k_hid_sense)
         const size_t row = GATHER ? (size_t)gs::gcell(__ldg(a.sorted + ti.y + r), a.W).cell
                                   : (size_t)__float_as_int(__ldg(a.sens + (size_t)(ti.y + r) * kK1 + 45));
-        float4* dst = reinterpret_cast<float4*>(a.act + row * 16);
+        if (a.decided) {
+          // 32-byte decided record {inv, liq, m0..m2, xmax, kstar, 0}: five
+          // sigmoids and explore_pick (exact) instead of thirteen sigmoids
+          float z[kActuators];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) dst[j] = make_float4(o[4 * j], o[4 * j + 1], o[4 * j + 2], o[4 * j + 3]);
+          for (int j = 0; j < kActuators; ++j) z[j] = __fadd_rn(zs[j], bias2[j]);
+          int ks;
+          float xm;
+          explore_pick(z + 5, ks, xm);
+          asm volatile("st.global.v8.f32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(a.act + row * 8),
+                       "f"(squash(z[0])), "f"(squash(z[1])), "f"(squash(z[2])), "f"(squash(z[3])), "f"(squash(z[4])),
+                       "f"(xm), "f"(__int_as_float(ks)), "f"(0.0f)
+                       : "memory");
+        } else {
+          float o[16];
+#pragma unroll
+          for (int j = 0; j < kActuators; ++j) o[j] = squash(__fadd_rn(zs[j], bias2[j]));
+          o[13] = o[14] = o[15] = 0.0f;
+          float4* dst = reinterpret_cast<float4*>(a.act + row * 16);
+#pragma unroll
+          for (int j = 0; j < 4; ++j) dst[j] = make_float4(o[4 * j], o[4 * j + 1], o[4 * j + 2], o[4 * j + 3]);
+        }
       }
       tc::fence_before();  // the layer-2 columns are read before the next layer 2 (after the next epilogue 1's barrier)
     }
@@ -1300,6 +1315,12 @@ cudaError_t launch_hidden_gather(const GatherBuffers& b, const StepGeom& g, cons
   return cudaGetLastError();
 }
 
+// k_hid_net2 (both layers on the tensor core) serves this width; with
+// `decided` it leaves 32-byte decided records at the cell index
+bool hidden_net2_used(int hidden, bool l2_cuda_core) {
+  return hidden > 0 && !l2_cuda_core && hidden_tc_nh(hidden) <= 128 && hidden_tc_nh(hidden) % 32 == 0;
+}
+
 cudaError_t launch_hidden_tc(const HidBuffers& b, const StepGeom& g, const Planes& front, const Params& net,
                              int capacity, int num_sms, bool decided, bool l2_cuda_core, cudaStream_t st) {
   const int nctas = hidden_sort_ctas(g.W, g.H);
@@ -1324,7 +1345,7 @@ cudaError_t launch_hidden_tc(const HidBuffers& b, const StepGeom& g, const Plane
   }
   // decided records of direct nets land at the cell index: no cell -> row map
   int32_t* rank = decided && net.hidden == 0 ? nullptr : b.rank;
-  const bool net2 = net.hidden > 0 && !l2_cuda_core && hidden_tc_nh(net.hidden) <= 128 && hidden_tc_nh(net.hidden) % 32 == 0;
+  const bool net2 = hidden_net2_used(net.hidden, l2_cuda_core);
   k_hid_sense<<<nctas, kSortThreads, ssmem, st>>>(g, front, b.offs, b.cta_hist, capacity, b.sens, rank, net2 ? 1 : 0);
   NetArgs a;
   a.net = net;
@@ -1336,7 +1357,7 @@ cudaError_t launch_hidden_tc(const HidBuffers& b, const StepGeom& g, const Plane
   a.sens = b.sens;
   a.tile_info = b.tile_info;
   a.act = b.act;
-  a.decided = decided && net.hidden == 0 ? 1 : 0;
+  a.decided = decided && (net.hidden == 0 || net2) ? 1 : 0;
   if (net.hidden == 0) {
     k_direct_rows<<<num_sms * 4, kDrThreads, 0, st>>>(a);  // 16 warps per SM, one wave
     return cudaGetLastError();

@@ -223,6 +223,7 @@ cudaError_t launch_tex_to_planes(const float* tex, const StepGeom& g, const Plan
                                  cudaStream_t st);
 
 bool hidden_tc_supported(int hidden);
+bool hidden_net2_used(int hidden, bool l2_cuda_core);
 int hidden_sort_ctas(int W, int H);
 int hidden_tc_nh(int hidden);
 size_t hidden_tc_smem(int hidden);
